@@ -1,0 +1,154 @@
+/*
+ * b2sr_sm100.h -- C ABI of the B200-native Bit-GraphBLAS hot path.
+ *
+ * This is the drop-in boundary under the Python API of the reference package
+ * `b2sr` 0.1.0 (/root/reference/pkg/src/b2sr/__init__.py:3-96).  The Python
+ * mirror (paper_2201_08560_b200/) binds these symbols with ctypes -- the FFI
+ * a Python package uses -- and keeps the reference's names, argument meaning
+ * and exception classes.  Each entry point below cites the reference function
+ * it replaces.
+ *
+ * Conventions
+ *  - Every function returns an int status (B2SR_OK == 0).  On failure the
+ *    message is available from b2sr_last_error() (thread-local).  No C++
+ *    exception crosses this boundary.
+ *  - Status codes map onto the reference's exception classes
+ *    (SURVEY.md §8b): B2SR_EINVAL -> ValueError, B2SR_EFORMAT -> FormatError,
+ *    B2SR_ENOCONV -> RuntimeError, B2SR_ECUDA / B2SR_ENOMEM -> RuntimeError /
+ *    MemoryError.
+ *  - Matrices live on the device behind an opaque b2sr_matrix handle.  Their
+ *    arrays use the reference's layout exactly (formats.py:3-9, 228-240):
+ *    tile_row_ptr u32[ntr+1], tile_col_ind u32[T], bit_tiles word[T][dim],
+ *    word = u8/u8/u16/u32 for dim 4/8/16/32, LSB = lowest column.
+ *  - Vectors are caller-owned DEVICE pointers.  Bit vectors use the
+ *    reference BitVector word layout (formats.py:332-357); their buffers must
+ *    be padded to a multiple of 4 bytes (ceil(ntr*wordbytes/4)*4).
+ *  - `stream` is a cudaStream_t passed as void*; NULL = legacy default stream.
+ *    Calls are stream-ordered; functions that must return a host scalar
+ *    (tile counts, iteration counts, sums) synchronise that stream.
+ *  - Re-entrant: no hidden global mutable state besides the per-thread error
+ *    string and a lazily initialised, internally locked memory-pool setup.
+ */
+#ifndef B2SR_SM100_H
+#define B2SR_SM100_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    B2SR_OK = 0,
+    B2SR_EINVAL = 1,   /* ValueError   */
+    B2SR_EFORMAT = 2,  /* FormatError  */
+    B2SR_ECUDA = 3,    /* RuntimeError (CUDA failure) */
+    B2SR_ENOMEM = 4,   /* MemoryError  */
+    B2SR_ENOCONV = 5   /* RuntimeError (iteration cap, algorithms.py:91-92, 195-196) */
+};
+
+enum { B2SR_RING_BOOLEAN = 0, B2SR_RING_ARITHMETIC = 1, B2SR_RING_MINPLUS = 2, B2SR_RING_MAXTIMES = 3 };
+
+typedef struct b2sr_matrix b2sr_matrix;
+
+/* ---- library ----------------------------------------------------------- */
+const char *b2sr_last_error(void);
+int b2sr_version(void);
+/* Number of kernel launches issued by this process so far (evidence for
+ * bench.py's "gpu_launches"). */
+uint64_t b2sr_launch_count(void);
+
+/* ---- matrices (formats.py:228-329, 444-489) ---------------------------- */
+/* csr_to_b2sr (formats.py:444-464): device CSR (row_ptr u32[n+1], col_ind
+ * u32[nnz], strictly increasing columns per row) -> B2SR on the device.
+ * K1 (segmented tile-row count + scan) and K2 (merge/pack) kernels. */
+int b2sr_from_csr(uint32_t n, uint32_t dim, const uint32_t *d_row_ptr, const uint32_t *d_col_ind,
+                  uint64_t nnz, void *stream, b2sr_matrix **out);
+/* Adopt existing arrays (already validated on the host, e.g. a B2srMatrix
+ * built by the caller): copies from host pointers into a new device matrix. */
+int b2sr_from_host(uint32_t n, uint32_t dim, const uint32_t *h_trp, const uint32_t *h_tci,
+                   const void *h_tiles, uint64_t num_tiles, void *stream, b2sr_matrix **out);
+int b2sr_free(b2sr_matrix *m);
+int b2sr_info(const b2sr_matrix *m, uint32_t *n, uint32_t *dim, uint32_t *ntr, uint64_t *num_tiles);
+/* Device pointers of the three arrays (borrowed; valid until b2sr_free). */
+int b2sr_arrays(const b2sr_matrix *m, const uint32_t **trp, const uint32_t **tci, const void **tiles);
+/* Copy the three arrays to host buffers (sizes from b2sr_info). */
+int b2sr_to_host(const b2sr_matrix *m, uint32_t *h_trp, uint32_t *h_tci, void *h_tiles, void *stream);
+/* b2sr_transpose (formats.py:477-489): K3, radix sort by tile column +
+ * in-register bit transpose. */
+int b2sr_transpose(const b2sr_matrix *m, void *stream, b2sr_matrix **out);
+/* B2srMatrix.__eq__ (formats.py:320-329) on the device. */
+int b2sr_equal(const b2sr_matrix *a, const b2sr_matrix *b, void *stream, int *equal);
+/* b2sr_to_csr (formats.py:467-474), two phases: row_ptr (u32[n+1]) + nnz,
+ * then col_ind (u32[nnz]) given that row_ptr. */
+int b2sr_to_csr_rowptr(const b2sr_matrix *m, uint32_t *d_row_ptr, uint64_t *nnz, void *stream);
+int b2sr_to_csr_fill(const b2sr_matrix *m, const uint32_t *d_row_ptr, uint32_t *d_col_ind, void *stream);
+/* _drop_diagonal(b2sr_to_csr(m)) -> csr_to_b2sr (algorithms.py:96-101,111)
+ * done directly in tile form. */
+int b2sr_drop_diagonal(const b2sr_matrix *m, void *stream, b2sr_matrix **out);
+/* Rows [row_begin, row_end) of tile rows as a row-block matrix (multi-GPU
+ * 1-D partition).  Column space and n stay global. */
+int b2sr_row_block(const b2sr_matrix *m, uint32_t tr_begin, uint32_t tr_end, void *stream,
+                   b2sr_matrix **out);
+int b2sr_row_offset(const b2sr_matrix *m, uint32_t *tr_begin);
+/* used_columns (kernels.py:86-94): d_out u8[n] (0/1). */
+int b2sr_used_columns(const b2sr_matrix *m, uint8_t *d_out, void *stream);
+
+/* ---- bin-SpMV (kernels.py:97-249) -------------------------------------- */
+/* bmv_bin_bin_bin[_masked]: y words (tile width layout) = OR_j a_ij & x_j,
+ * cleared where keep is 0 (d_keep may be NULL).  For a row-block matrix, y
+ * holds only the block's words. */
+int b2sr_bmv_bbb(const b2sr_matrix *m, const void *d_x, const void *d_keep, void *d_y, void *stream);
+/* bmv_bin_bin_full[_masked]: y f64[n] (or the block's rows) = popcounts. */
+int b2sr_bmv_bbf(const b2sr_matrix *m, const void *d_x, const void *d_keep, double *d_y, void *stream);
+/* bmv_bin_full_full[_masked]: semiring gather over x f64[n]; ring is one of
+ * B2SR_RING_*, inc in {0,1} for minplus; d_scale (f64[n]) only with
+ * ARITHMETIC.  Terms reduce per output element in ascending column order
+ * (kernels.py:195-207), so ARITHMETIC is bit-identical to the reference.
+ * A zero scale at a used column fails with B2SR_EINVAL and *bad_col = j. */
+int b2sr_bmv_bff(const b2sr_matrix *m, const double *d_x, int ring, double inc, const double *d_scale,
+                 const void *d_keep, double *d_y, int64_t *bad_col, void *stream);
+
+/* ---- bin-SpGEMM (kernels.py:298-367) ----------------------------------- */
+/* bmm_bin_bin_sum: sum of all entries of A @ B (int64). */
+int b2sr_bmm_sum(const b2sr_matrix *a, const b2sr_matrix *b, int64_t *out, void *stream);
+/* bmm_bin_bin_sum_masked with B given TRANSPOSED (bt = transpose(b)):
+ * sum over mask bits (i,j) of popc(A_row_i & Bt_row_j) per common tile col. */
+int b2sr_bmm_sum_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_matrix *mask,
+                           int64_t *out, void *stream);
+
+/* ---- drivers (algorithms.py:75-215) ------------------------------------ */
+/* bfs on the TRANSPOSED matrix at (the caller does at = transpose(a),
+ * algorithms.py:78).  levels f64[n] (+inf unreachable); *iterations counts
+ * the final empty sweep like the reference. */
+int b2sr_bfs(const b2sr_matrix *at, uint32_t src, double *d_levels, int64_t *iterations, void *stream);
+/* sssp relaxation (algorithms.py:113-124) on at = transpose(drop_diag(a)). */
+int b2sr_sssp(const b2sr_matrix *at, uint32_t src, double *d_dist, int64_t *iterations, void *stream);
+/* pagerank (algorithms.py:127-163); a = transposed adjacency. */
+int b2sr_pagerank(const b2sr_matrix *a, const double *d_out_degree, double alpha, double epsilon,
+                  int64_t max_iter, double *d_rank, int64_t *iterations, int *converged,
+                  int64_t *bad_col, void *stream);
+/* connected_components (algorithms.py:166-196) on a symmetric matrix. */
+int b2sr_cc(const b2sr_matrix *a, double *d_labels, int64_t *iterations, void *stream);
+/* triangle_count core (algorithms.py:212-214): L = strict lower triangle in
+ * B2SR; count = bmm_masked(L, transpose(L), L). */
+int b2sr_tc(const b2sr_matrix *lower, int64_t *count, void *stream);
+
+/* ---- CSR utilities on the device (formats.py:96-225, algorithms.py:218) - */
+/* Strict lower triangle of a device CSR (two phases like b2sr_to_csr). */
+int b2sr_csr_lower_rowptr(uint32_t n, const uint32_t *d_row_ptr, const uint32_t *d_col_ind,
+                          uint32_t *d_lrow_ptr, uint64_t *lnnz, void *stream);
+int b2sr_csr_lower_fill(uint32_t n, const uint32_t *d_row_ptr, const uint32_t *d_col_ind,
+                        const uint32_t *d_lrow_ptr, uint32_t *d_lcol_ind, void *stream);
+/* Synthetic Graph500 R-MAT edges. */
+int b2sr_rmat_edges(int scale, uint64_t m, uint64_t seed, uint32_t *d_src, uint32_t *d_dst, void *stream);
+/* COO -> CSR with CsrMatrix.from_coo semantics (formats.py:156-190):
+ * symmetrize / drop self-loops / sort / de-duplicate.  d_row_ptr u32[n+1];
+ * d_col_ind must hold (symmetrize ? 2m : m) entries; *nnz returned. */
+int b2sr_coo_to_csr(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_t *d_dst, int symmetrize,
+                    int drop_loops, uint32_t *d_row_ptr, uint32_t *d_col_ind, uint64_t *nnz, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B2SR_SM100_H */

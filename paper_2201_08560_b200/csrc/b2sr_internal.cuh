@@ -1,0 +1,209 @@
+// Internal helpers shared by the sm_100a translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "b2sr_sm100.h"
+
+namespace b2sr {
+
+// ---------------------------------------------------------------- errors
+struct Error {
+    int code;
+    std::string msg;
+};
+
+void set_error(int code, const char *fmt, ...);
+void clear_error();
+
+// Thrown only inside the library; every extern "C" entry point catches it
+// (see API_BEGIN / API_END) and turns it into a status code.
+#define B2SR_THROW(code, ...)                                  \
+    do {                                                       \
+        ::b2sr::set_error((code), __VA_ARGS__);                \
+        throw ::b2sr::Error{(code), std::string()};            \
+    } while (0)
+
+#define CK(call)                                                                               \
+    do {                                                                                       \
+        cudaError_t e_ = (call);                                                               \
+        if (e_ != cudaSuccess) {                                                               \
+            int c_ = (e_ == cudaErrorMemoryAllocation) ? B2SR_ENOMEM : B2SR_ECUDA;             \
+            B2SR_THROW(c_, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__,   \
+                       __LINE__);                                                              \
+        }                                                                                      \
+    } while (0)
+
+#define API_BEGIN \
+    ::b2sr::clear_error(); \
+    try {
+#define API_END                                                                  \
+    }                                                                            \
+    catch (const ::b2sr::Error &e) {                                             \
+        return e.code;                                                           \
+    }                                                                            \
+    catch (...) {                                                                \
+        ::b2sr::set_error(B2SR_ECUDA, "unexpected C++ exception in b2sr");       \
+        return B2SR_ECUDA;                                                       \
+    }                                                                            \
+    return B2SR_OK;
+
+// ---------------------------------------------------------------- launches
+extern std::atomic<uint64_t> g_launches;
+#define LAUNCH(kernel, grid, block, smem, stream, ...)                     \
+    do {                                                                   \
+        if ((grid) > 0) {                                                  \
+            kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);    \
+            ::b2sr::g_launches.fetch_add(1, std::memory_order_relaxed);    \
+            CK(cudaGetLastError());                                        \
+        }                                                                  \
+    } while (0)
+
+// ---------------------------------------------------------------- memory
+void *dalloc(size_t bytes, cudaStream_t s);
+void dfree(void *p, cudaStream_t s);
+
+// Stream-ordered scratch buffer (freed on scope exit).
+template <typename T>
+struct Buf {
+    T *p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = nullptr;
+    Buf() = default;
+    Buf(size_t count, cudaStream_t st) : n(count), s(st) {
+        p = static_cast<T *>(dalloc(count * sizeof(T) + 16, st));
+    }
+    Buf(const Buf &) = delete;
+    Buf &operator=(const Buf &) = delete;
+    Buf(Buf &&o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; }
+    Buf &operator=(Buf &&o) noexcept {
+        reset();
+        p = o.p; n = o.n; s = o.s; o.p = nullptr;
+        return *this;
+    }
+    ~Buf() { reset(); }
+    void reset() {
+        if (p) dfree(p, s);
+        p = nullptr;
+    }
+    T *release() {
+        T *q = p;
+        p = nullptr;
+        return q;
+    }
+    T *get() const { return p; }
+};
+
+template <typename T>
+T read_scalar(const T *dptr, cudaStream_t s) {
+    T v;
+    CK(cudaMemcpyAsync(&v, dptr, sizeof(T), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return v;
+}
+
+// ---------------------------------------------------------------- matrix
+struct WorkItem {      // one bin-SpMV work unit: tiles [t0, t1) of local tile row `row`
+    uint32_t row;
+    uint32_t t0;
+    uint32_t t1;
+    uint32_t split;    // 1 when the row is shared with other items (atomic store)
+};
+
+}  // namespace b2sr
+
+struct b2sr_matrix {
+    uint32_t n = 0;          // logical dimension (global)
+    uint32_t dim = 0;        // tile width 4/8/16/32
+    uint32_t ntr = 0;        // tile rows stored here (== ceil(n/dim) unless a row block)
+    uint32_t row0 = 0;       // first global tile row (row blocks)
+    uint64_t num_tiles = 0;
+    uint32_t *trp = nullptr; // ntr + 1, local offsets starting at 0
+    uint32_t *tci = nullptr; // num_tiles
+    void *tiles = nullptr;   // num_tiles * dim words
+    int device = 0;
+    // cached bin-SpMV work partition (built lazily, immutable matrix)
+    b2sr::WorkItem *items = nullptr;
+    uint32_t n_items = 0;
+    bool any_split = false;
+};
+
+namespace b2sr {
+
+inline int word_bytes(int d) { return d == 32 ? 4 : (d == 16 ? 2 : 1); }
+inline uint32_t tile_rows(uint32_t n, uint32_t d) { return (n + d - 1) / d; }
+inline size_t padded_vec_bytes(uint32_t ntr, int d) { return ((size_t)ntr * word_bytes(d) + 3) / 4 * 4; }
+
+b2sr_matrix *new_matrix(uint32_t n, uint32_t dim, uint32_t ntr, uint64_t T, cudaStream_t s);
+void free_matrix(b2sr_matrix *m);
+void ensure_items(b2sr_matrix *m, cudaStream_t s);  // bin-SpMV work partition
+int num_sms();
+void launch_row_ids(const b2sr_matrix *m, uint32_t *rowid, cudaStream_t s);  // rowid[t] = tile row of t
+
+// scan.cu
+// out[i] = sum_{j<i} in[j] for i in [0, n]; out has n+1 entries (out[n] = total).
+void exclusive_scan_u32_to_u64(const uint32_t *in, uint64_t *out, size_t n, cudaStream_t s);
+void exclusive_scan_u64(const uint64_t *in, uint64_t *out, size_t n, cudaStream_t s);
+// sort.cu: stable LSD radix sort over the low `bits` bits of keys (values optional).
+size_t radix_sort_pairs_u32(uint32_t *keys, uint32_t *vals, size_t n, int bits, cudaStream_t s,
+                            uint32_t **keys_out, uint32_t **vals_out, Buf<uint32_t> *kalt,
+                            Buf<uint32_t> *valt);
+void radix_sort_keys_u64(uint64_t *keys, size_t n, int bits, cudaStream_t s, uint64_t **keys_out,
+                         Buf<uint64_t> *kalt);
+
+// ---------------------------------------------------------------- device helpers
+template <int D> struct WordT;
+template <> struct WordT<4> { using T = uint8_t; };
+template <> struct WordT<8> { using T = uint8_t; };
+template <> struct WordT<16> { using T = uint16_t; };
+template <> struct WordT<32> { using T = uint32_t; };
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+template <typename T>
+__device__ __forceinline__ T ldg_nc(const T *p) { return __ldg(p); }
+
+// Streaming 128-bit load that does not allocate in L1 (tiles are read once).
+__device__ __forceinline__ uint4 ld_stream128(const void *p) {
+    uint4 v;
+    asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_stream32(const void *p) {
+    uint32_t v;
+    asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+// Valid-bit mask of bit-vector word w (formats.py:433-441).
+__device__ __forceinline__ uint32_t valid_mask(uint32_t w, uint32_t n, int d) {
+    uint32_t full = d == 32 ? 0xFFFFFFFFu : ((1u << d) - 1u);
+    uint64_t lo = (uint64_t)w * d;
+    if (lo + d <= n) return full;
+    if (lo >= n) return 0u;
+    return (1u << (n - lo)) - 1u;
+}
+
+template <int D>
+__device__ __forceinline__ uint32_t load_word(const void *v, uint32_t i) {
+    return (uint32_t)(reinterpret_cast<const typename WordT<D>::T *>(v))[i];
+}
+
+// OR `val` into bit-vector word i of width D using a 32-bit atomic.
+template <int D>
+__device__ __forceinline__ void atomic_or_word(void *v, uint32_t i, uint32_t val) {
+    constexpr int WB = D == 32 ? 4 : (D == 16 ? 2 : 1);
+    size_t byte = (size_t)i * WB;
+    uint32_t *base = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(v) + (byte & ~(size_t)3));
+    atomicOr(base, val << (8 * (byte & 3)));
+}
+
+}  // namespace b2sr

@@ -1,0 +1,201 @@
+// K7/K8: bin-SpGEMM reductions (replaces kernels.py:271-367).
+//
+// bmm_bin_bin_sum: sum_ij (A B)_ij = sum_k colsum_A(k) * rowdeg_B(k), an
+// O(T) pass (the reference's per-pair colpop*rowpop sum regrouped by k;
+// integer arithmetic, so the regrouping is exact).
+//
+// bmm_bin_bin_sum_masked with B supplied transposed (Bt): for every stored
+// mask tile (I,J) the tile columns of A's row I and Bt's row J are
+// intersected, and each common K contributes, for every mask bit (r,c),
+// popc(A_IK[r] & Bt_JK[c]) == sum_k A[i,k] B[k,j] inside the tile pair.
+// One warp per mask tile: lanes take 32 entries of the shorter tile row and
+// binary-search them in the longer one; AND+POPC on the integer pipe (b1
+// MMA has no native sm_100a path -- SURVEY.md §0).  Triangle counting is
+// the instance A = Bt = M = L (transpose(transpose(L)) == L).
+#include "b2sr_internal.cuh"
+
+namespace b2sr {
+
+template <int D>
+__global__ void k_colsum_rowdeg(uint64_t T, const uint32_t *__restrict__ rowid, const uint32_t *__restrict__ tci,
+                                const typename WordT<D>::T *__restrict__ tiles, uint32_t *__restrict__ colsum,
+                                uint32_t *__restrict__ rowdeg) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < T; t += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t I = rowid[t], K = tci[t];
+#pragma unroll
+        for (int r = 0; r < D; r++) {
+            uint32_t w = tiles[t * D + r];
+            if (rowdeg && w) atomicAdd(rowdeg + (size_t)I * D + r, (uint32_t)__popc(w));
+            if (colsum) {
+                while (w) {
+                    int c = __ffs(w) - 1;
+                    w &= w - 1;
+                    atomicAdd(colsum + (size_t)K * D + c, 1u);
+                }
+            }
+        }
+    }
+}
+
+__global__ void k_dot_u32(size_t n, const uint32_t *a, const uint32_t *b, unsigned long long *out) {
+    unsigned long long acc = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        acc += (unsigned long long)a[i] * b[i];
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+static unsigned grid_for(uint64_t work) {
+    uint64_t b = (work + 255) / 256, cap = (uint64_t)num_sms() * 16;
+    return (unsigned)std::max<uint64_t>(1, std::min(b, cap));
+}
+
+static void row_ids(const b2sr_matrix *m, uint32_t *rowid, cudaStream_t s) { launch_row_ids(m, rowid, s); }
+
+static void colsum_rowdeg(const b2sr_matrix *m, uint32_t *colsum, uint32_t *rowdeg, cudaStream_t s) {
+    if (!m->num_tiles) return;
+    Buf<uint32_t> rowid(m->num_tiles, s);
+    row_ids(m, rowid.p, s);
+    unsigned g = grid_for(m->num_tiles);
+    switch (m->dim) {
+        case 4: LAUNCH(k_colsum_rowdeg<4>, g, 256, 0, s, m->num_tiles, rowid.p, m->tci, (const uint8_t *)m->tiles, colsum, rowdeg); break;
+        case 8: LAUNCH(k_colsum_rowdeg<8>, g, 256, 0, s, m->num_tiles, rowid.p, m->tci, (const uint8_t *)m->tiles, colsum, rowdeg); break;
+        case 16: LAUNCH(k_colsum_rowdeg<16>, g, 256, 0, s, m->num_tiles, rowid.p, m->tci, (const uint16_t *)m->tiles, colsum, rowdeg); break;
+        default: LAUNCH(k_colsum_rowdeg<32>, g, 256, 0, s, m->num_tiles, rowid.p, m->tci, (const uint32_t *)m->tiles, colsum, rowdeg); break;
+    }
+}
+
+// ------------------------------------------------------------ masked
+// lower_bound of `key` in v[lo, hi)
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t *__restrict__ v, uint32_t lo, uint32_t hi, uint32_t key) {
+    while (lo < hi) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(v + mid) < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_bmm_masked(uint64_t TM, const uint32_t *__restrict__ m_rowid,
+                                                    const uint32_t *__restrict__ m_tci,
+                                                    const typename WordT<D>::T *__restrict__ m_tiles,
+                                                    const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ a_tci,
+                                                    const typename WordT<D>::T *__restrict__ a_tiles,
+                                                    const uint32_t *__restrict__ b_trp, const uint32_t *__restrict__ b_tci,
+                                                    const typename WordT<D>::T *__restrict__ b_tiles,
+                                                    unsigned long long *__restrict__ out) {
+    const uint32_t lane = lane_id();
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long acc = 0;
+    for (uint64_t mt = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; mt < TM; mt += warps) {
+        uint32_t I = m_rowid[mt], J = m_tci[mt];
+        uint32_t mword = lane < (uint32_t)D ? (uint32_t)m_tiles[mt * D + lane] : 0u;
+        uint32_t rows_used = __ballot_sync(0xffffffffu, mword != 0);  // bit r: mask row r non-empty
+        uint32_t a0 = a_trp[I], a1 = a_trp[I + 1], b0 = b_trp[J], b1 = b_trp[J + 1];
+        if (a0 == a1 || b0 == b1 || rows_used == 0) continue;
+        // iterate the shorter tile row, search the longer one
+        bool a_short = (a1 - a0) <= (b1 - b0);
+        uint32_t s0 = a_short ? a0 : b0, s1 = a_short ? a1 : b1;
+        uint32_t l0 = a_short ? b0 : a0, l1 = a_short ? b1 : a1;
+        const uint32_t *stci = a_short ? a_tci : b_tci;
+        const uint32_t *ltci = a_short ? b_tci : a_tci;
+        for (uint32_t base = s0; base < s1; base += 32) {
+            uint32_t si = base + lane;
+            uint32_t ta = 0, tb = 0;
+            bool hit = false;
+            if (si < s1) {
+                uint32_t K = __ldg(stci + si);
+                uint32_t li = lower_bound_u32(ltci, l0, l1, K);
+                if (li < l1 && __ldg(ltci + li) == K) {
+                    hit = true;
+                    ta = a_short ? si : li;
+                    tb = a_short ? li : si;
+                }
+            }
+            uint32_t hits = __ballot_sync(0xffffffffu, hit);
+            if (!hits) continue;
+            uint32_t ru = rows_used;
+            while (ru) {  // warp-uniform loop over non-empty mask rows
+                int r = __ffs(ru) - 1;
+                ru &= ru - 1;
+                uint32_t mw = __shfl_sync(0xffffffffu, mword, r);
+                if (hit) {
+                    uint32_t aw = a_tiles[(size_t)ta * D + r];
+                    if (aw) {
+                        while (mw) {
+                            int c = __ffs(mw) - 1;
+                            mw &= mw - 1;
+                            acc += __popc(aw & (uint32_t)b_tiles[(size_t)tb * D + c]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0 && acc) atomicAdd(out, acc);
+}
+
+int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_matrix *mask, cudaStream_t s) {
+    if (!mask->num_tiles || !a->num_tiles || !bt->num_tiles) return 0;
+    Buf<uint32_t> rowid(mask->num_tiles, s);
+    row_ids(mask, rowid.p, s);
+    Buf<unsigned long long> out(1, s);
+    CK(cudaMemsetAsync(out.p, 0, 8, s));
+    uint64_t blocks = (mask->num_tiles + 7) / 8, cap = (uint64_t)num_sms() * 16;
+    unsigned g = (unsigned)std::min(blocks, cap);
+    switch (a->dim) {
+#define BMM_CASE(DD, W)                                                                                          \
+    case DD:                                                                                                     \
+        LAUNCH(k_bmm_masked<DD>, g, 256, 0, s, mask->num_tiles, rowid.p, mask->tci, (const W *)mask->tiles,     \
+               a->trp, a->tci, (const W *)a->tiles, bt->trp, bt->tci, (const W *)bt->tiles, out.p);              \
+        break;
+        BMM_CASE(4, uint8_t)
+        BMM_CASE(8, uint8_t)
+        BMM_CASE(16, uint16_t)
+        BMM_CASE(32, uint32_t)
+#undef BMM_CASE
+    }
+    return (int64_t)read_scalar(out.p, s);
+}
+
+}  // namespace b2sr
+
+using namespace b2sr;
+
+extern "C" {
+
+int b2sr_bmm_sum(const b2sr_matrix *a, const b2sr_matrix *b, int64_t *out, void *stream) {
+    API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    if (a->n != b->n || a->dim != b->dim) B2SR_THROW(B2SR_EINVAL, "operands must share n and tile width");
+    size_t rows = (size_t)tile_rows(a->n, a->dim) * a->dim;
+    Buf<uint32_t> colsum(rows, s), rowdeg(rows, s);
+    Buf<unsigned long long> acc(1, s);
+    CK(cudaMemsetAsync(colsum.p, 0, rows * 4, s));
+    CK(cudaMemsetAsync(rowdeg.p, 0, rows * 4, s));
+    CK(cudaMemsetAsync(acc.p, 0, 8, s));
+    colsum_rowdeg(a, colsum.p, nullptr, s);
+    colsum_rowdeg(b, nullptr, rowdeg.p, s);
+    LAUNCH(k_dot_u32, grid_for(rows), 256, 0, s, rows, colsum.p, rowdeg.p, acc.p);
+    *out = (int64_t)read_scalar(acc.p, s);
+    API_END
+}
+
+int b2sr_bmm_sum_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_matrix *mask, int64_t *out,
+                           void *stream) {
+    API_BEGIN
+    if (a->n != bt->n || a->dim != bt->dim || a->n != mask->n || a->dim != mask->dim)
+        B2SR_THROW(B2SR_EINVAL, "operands must share n and tile width");
+    *out = bmm_masked_bt(a, bt, mask, (cudaStream_t)stream);
+    API_END
+}
+
+int b2sr_tc(const b2sr_matrix *lower, int64_t *count, void *stream) {
+    API_BEGIN
+    // bmm_masked(L, transpose(L), L): B = transpose(L) enters transposed, i.e. L.
+    *count = bmm_masked_bt(lower, lower, lower, (cudaStream_t)stream);
+    API_END
+}
+
+}  // extern "C"

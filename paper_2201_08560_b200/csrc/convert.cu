@@ -1,0 +1,203 @@
+// K1/K2: CSR -> B2SR conversion on the device (replaces formats.py:444-464).
+//
+// The reference sorts all tile keys (r//d)*ntr + c//d with np.unique and ORs
+// the bits in with np.bitwise_or.at.  Here a tile row I owns the contiguous
+// col_ind segment of its d CSR rows, each already sorted, so its distinct
+// tile columns are the d-way merge of the d runs of c//d:
+//   * a group of d lanes takes one tile row (lane r = bit-row r), 32/d tile
+//     rows per warp;
+//   * each step the group min-reduces the current tile column (redux.sync
+//     at d=32, shfl_xor below), the lanes sitting on that column consume
+//     their run and build their row word, and one tile is emitted;
+//   * K1 runs the loop counting tiles -> exclusive scan -> tile_row_ptr;
+//     K2 re-runs it writing tile_col_ind and the bit rows.
+// Long tile rows (hubs) are split into column ranges of ~CONV_CHUNK entries
+// so no group walks a hub alone; the split points are found by binary
+// search and the ranges' counts are scanned in order, so the layout is
+// exactly the reference's (row-major tiles, ascending columns).
+#include "b2sr_internal.cuh"
+
+namespace b2sr {
+
+constexpr uint32_t CONV_CHUNK = 1024;  // CSR entries per work item (target)
+constexpr uint32_t INF32 = 0xFFFFFFFFu;
+
+struct ConvItem {
+    uint32_t row;   // tile row
+    uint32_t klo;   // first tile column of this range
+    uint32_t khi;   // one past the last tile column
+    uint32_t pad;
+};
+
+__global__ void k_conv_chunks(uint32_t n, uint32_t d, uint32_t ntr, const uint32_t *row_ptr, uint32_t *pcount) {
+    uint32_t I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= ntr) return;
+    uint64_t r0 = (uint64_t)I * d, r1 = min((uint64_t)n, r0 + d);
+    uint32_t e = row_ptr[r1] - row_ptr[r0];
+    uint32_t p = (e + CONV_CHUNK - 1) / CONV_CHUNK;
+    pcount[I] = p ? p : 1u;
+}
+
+__global__ void k_conv_items(uint32_t ntr, const uint64_t *pofs, ConvItem *items) {
+    uint32_t I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I >= ntr) return;
+    uint64_t b = pofs[I];
+    uint32_t P = (uint32_t)(pofs[I + 1] - b);
+    for (uint32_t j = 0; j < P; j++) {
+        ConvItem it;
+        it.row = I;
+        it.klo = (uint32_t)((uint64_t)j * ntr / P);
+        it.khi = (uint32_t)((uint64_t)(j + 1) * ntr / P);
+        it.pad = 0;
+        items[b + j] = it;
+    }
+}
+
+template <int D>
+__device__ __forceinline__ uint32_t group_min(uint32_t v) {
+    if constexpr (D == 32) {
+        return __reduce_min_sync(0xffffffffu, v);
+    } else {
+#pragma unroll
+        for (int o = D / 2; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o, D));
+        return v;
+    }
+}
+
+template <int D, bool PACK>
+__global__ void __launch_bounds__(256) k_conv(const ConvItem *__restrict__ items, uint32_t n_items, uint32_t n,
+                                              const uint32_t *__restrict__ row_ptr,
+                                              const uint32_t *__restrict__ col_ind, const uint64_t *__restrict__ iofs,
+                                              uint32_t *__restrict__ cnt, uint32_t *__restrict__ tci,
+                                              typename WordT<D>::T *__restrict__ tiles) {
+    constexpr uint32_t GPW = 32 / D;  // groups (items) per warp
+    const uint32_t lane = lane_id(), r = lane % D;
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t wb = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wb * GPW < n_items; wb += warps) {
+        uint32_t item = wb * GPW + lane / D;
+        bool valid = item < n_items;
+        ConvItem it = valid ? items[item] : ConvItem{0, 0, 0, 0};
+        uint64_t row = (uint64_t)it.row * D + r;
+        uint32_t p = 0, end = 0;
+        if (valid && row < n) {
+            p = row_ptr[row];
+            end = row_ptr[row + 1];
+            if (it.klo > 0) {  // split range: first entry with c >= klo*D
+                uint32_t key = it.klo * (uint32_t)D, a = p, b = end;
+                while (a < b) {
+                    uint32_t mid = (a + b) >> 1;
+                    if (col_ind[mid] < key) a = mid + 1; else b = mid;
+                }
+                p = a;
+            }
+        }
+        uint32_t c = 0, cur = INF32;
+        if (p < end) {
+            c = col_ind[p];
+            if (c / D < it.khi) cur = c / D;
+        }
+        uint64_t t = (PACK && valid) ? iofs[item] : 0;
+        uint32_t count = 0;
+        while (__any_sync(0xffffffffu, cur != INF32)) {
+            uint32_t K = group_min<D>(cur);
+            uint32_t word = 0;
+            while (cur == K && K != INF32) {  // consume this lane's run inside tile column K
+                word |= 1u << (c % D);
+                ++p;
+                cur = INF32;
+                if (p < end) {
+                    c = col_ind[p];
+                    uint32_t k = c / D;
+                    if (k < it.khi) cur = k;
+                }
+            }
+            if (K != INF32) {
+                if constexpr (PACK) {
+                    tiles[t * D + r] = (typename WordT<D>::T)word;
+                    if (r == 0) tci[t] = K;
+                }
+                ++t;
+                ++count;
+            }
+        }
+        if constexpr (!PACK) {
+            if (valid && r == 0) cnt[item] = count;
+        }
+    }
+}
+
+__global__ void k_conv_trp(uint32_t ntr, const uint64_t *pofs, const uint64_t *iofs, uint32_t *trp) {
+    uint32_t I = blockIdx.x * blockDim.x + threadIdx.x;
+    if (I <= ntr) trp[I] = (uint32_t)iofs[pofs[I]];
+}
+
+template <int D>
+static void conv_launch(bool pack, const ConvItem *items, uint32_t n_items, uint32_t n, const uint32_t *row_ptr,
+                        const uint32_t *col_ind, const uint64_t *iofs, uint32_t *cnt, uint32_t *tci, void *tiles,
+                        cudaStream_t s) {
+    constexpr uint32_t GPW = 32 / D;
+    uint64_t warps = (n_items + GPW - 1) / GPW;
+    uint64_t blocks = (warps + 7) / 8;
+    uint64_t cap = (uint64_t)num_sms() * 8;  // 8 CTAs x 8 warps per SM, grid-stride beyond
+    unsigned g = (unsigned)(blocks < cap ? blocks : cap);
+    if (pack)
+        LAUNCH((k_conv<D, true>), g, 256, 0, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
+               (typename WordT<D>::T *)tiles);
+    else
+        LAUNCH((k_conv<D, false>), g, 256, 0, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
+               (typename WordT<D>::T *)tiles);
+}
+
+static void conv_dispatch(uint32_t d, bool pack, const ConvItem *items, uint32_t n_items, uint32_t n,
+                          const uint32_t *row_ptr, const uint32_t *col_ind, const uint64_t *iofs, uint32_t *cnt,
+                          uint32_t *tci, void *tiles, cudaStream_t s) {
+    switch (d) {
+        case 4: conv_launch<4>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s); break;
+        case 8: conv_launch<8>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s); break;
+        case 16: conv_launch<16>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s); break;
+        default: conv_launch<32>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s); break;
+    }
+}
+
+b2sr_matrix *csr_to_b2sr_device(uint32_t n, uint32_t d, const uint32_t *row_ptr, const uint32_t *col_ind,
+                                cudaStream_t s) {
+    uint32_t ntr = tile_rows(n, d);
+    Buf<uint32_t> pcount(ntr, s);
+    Buf<uint64_t> pofs((size_t)ntr + 1, s);
+    LAUNCH(k_conv_chunks, (ntr + 255) / 256, 256, 0, s, n, d, ntr, row_ptr, pcount.p);
+    exclusive_scan_u32_to_u64(pcount.p, pofs.p, ntr, s);
+    uint64_t n_items64 = read_scalar(pofs.p + ntr, s);
+    if (n_items64 > 0xFFFFFFFFull) B2SR_THROW(B2SR_EINVAL, "too many conversion work items");
+    uint32_t n_items = (uint32_t)n_items64;
+    Buf<ConvItem> items(n_items, s);
+    LAUNCH(k_conv_items, (ntr + 255) / 256, 256, 0, s, ntr, pofs.p, items.p);
+    Buf<uint32_t> cnt(n_items, s);
+    Buf<uint64_t> iofs((size_t)n_items + 1, s);
+    conv_dispatch(d, false, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, nullptr, nullptr, s);
+    exclusive_scan_u32_to_u64(cnt.p, iofs.p, n_items, s);
+    uint64_t T = read_scalar(iofs.p + n_items, s);
+    if (T > 0xFFFFFFFFull) B2SR_THROW(B2SR_EFORMAT, "tile count exceeds 32-bit index range");
+    b2sr_matrix *m = new_matrix(n, d, ntr, T, s);
+    try {
+        LAUNCH(k_conv_trp, (ntr + 256) / 256, 256, 0, s, ntr, pofs.p, iofs.p, m->trp);
+        if (T) conv_dispatch(d, true, items.p, n_items, n, row_ptr, col_ind, iofs.p, nullptr, m->tci, m->tiles, s);
+    } catch (...) {
+        free_matrix(m);
+        throw;
+    }
+    return m;
+}
+
+}  // namespace b2sr
+
+using namespace b2sr;
+
+extern "C" int b2sr_from_csr(uint32_t n, uint32_t dim, const uint32_t *d_row_ptr, const uint32_t *d_col_ind,
+                             uint64_t nnz, void *stream, b2sr_matrix **out) {
+    API_BEGIN
+    (void)nnz;
+    if (dim != 4 && dim != 8 && dim != 16 && dim != 32) B2SR_THROW(B2SR_EINVAL, "tile dim must be 4/8/16/32");
+    if (n == 0) B2SR_THROW(B2SR_EFORMAT, "cannot tile an empty matrix");
+    *out = csr_to_b2sr_device(n, dim, d_row_ptr, d_col_ind, (cudaStream_t)stream);
+    API_END
+}

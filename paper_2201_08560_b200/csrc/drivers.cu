@@ -1,0 +1,530 @@
+// K9: device-resident algorithm drivers (replaces algorithms.py:75-196).
+//
+// Every sweep's state (frontier, visited, levels, distances, ranks, labels)
+// stays in HBM; the host sees one 4- or 8-byte flag per sweep (the
+// reference's loop condition) and the final vector.
+//
+// BFS (algorithms.py:75-93): level-synchronous masked bbb sweeps over the
+// transposed matrix.  The sweep kernel is the bbb stream with three
+// output-preserving shortcuts: tile rows whose keep word (~visited) is zero
+// are skipped, a tile's payload is only loaded when its frontier word is
+// non-zero, and a row stops as soon as every keep bit is hit.  Levels,
+// visited and the frontier-any flag are updated by one fused epilogue.
+//
+// PageRank delta (algorithms.py:157) is numpy's pairwise summation
+// reproduced exactly (same leaf blocks, 8 accumulators, same tree), so the
+// convergence test sees the reference's bits.
+#include <cmath>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "b2sr_internal.cuh"
+
+namespace b2sr {
+
+void launch_bff(const b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
+                cudaStream_t s);
+void used_column_words(const b2sr_matrix *m, uint32_t *colw, cudaStream_t s);
+
+static unsigned grid_for(uint64_t work) {
+    uint64_t b = (work + 255) / 256, cap = (uint64_t)num_sms() * 16;
+    return (unsigned)std::max<uint64_t>(1, std::min(b, cap));
+}
+
+// ================================================================ BFS
+template <int D> struct BGeo {
+    static constexpr int WB = D == 32 ? 4 : (D == 16 ? 2 : 1);
+    static constexpr int TB = D * WB;
+    static constexpr int TPL = TB >= 16 ? 1 : 16 / TB;
+    static constexpr int LPT = TB >= 16 ? TB / 16 : 1;
+    static constexpr int TPW = 32 * TPL / LPT;
+};
+
+__device__ __forceinline__ uint32_t nz_nibble_bytes_b(uint32_t v) {
+    v = (v | (v >> 1) | (v >> 2) | (v >> 3)) & 0x01010101u;
+    return (v * 0x10204080u) >> 28;
+}
+__device__ __forceinline__ uint32_t nz_bytes_b(uint32_t v) {
+    v = (v | (v >> 4)) & 0x0F0F0F0Fu;
+    v = (v | (v >> 2)) & 0x03030303u;
+    v = (v | (v >> 1)) & 0x01010101u;
+    return (v * 0x10204080u) >> 28;
+}
+
+// hit bits (row-word positions) of the tiles this lane covers; the payload
+// is only fetched for tiles whose frontier word is non-zero
+template <int D>
+__device__ __forceinline__ uint32_t bfs_lane(const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
+                                             const void *__restrict__ x, uint32_t base, uint32_t t0, uint32_t t1,
+                                             uint32_t lane) {
+    using G = BGeo<D>;
+    if constexpr (G::TPL > 1) {
+        uint32_t tl = base + lane * G::TPL;
+        if (!(tl < t1 && tl + G::TPL > t0)) return 0;
+        uint32_t cols[G::TPL], xw[G::TPL];
+        if constexpr (G::TPL == 4) {
+            uint4 c = ld_stream128(tci + tl);
+            cols[0] = c.x; cols[1] = c.y; cols[2] = c.z; cols[3] = c.w;
+        } else {
+            uint2 c = *reinterpret_cast<const uint2 *>(tci + tl);
+            cols[0] = c.x; cols[1] = c.y;
+        }
+        uint32_t anyx = 0;
+#pragma unroll
+        for (int j = 0; j < G::TPL; j++) {
+            bool ok = tl + j >= t0 && tl + j < t1;
+            xw[j] = ok ? load_word<D>(x, cols[j]) : 0u;
+            anyx |= xw[j];
+        }
+        if (!anyx) return 0;
+        uint4 v = ld_stream128(tiles + (size_t)tl * G::TB);
+        if constexpr (D == 4) {
+            uint32_t w[4] = {v.x, v.y, v.z, v.w}, a = 0;
+#pragma unroll
+            for (int j = 0; j < 4; j++) a |= nz_nibble_bytes_b(w[j] & (xw[j] * 0x01010101u));
+            return a;
+        } else {
+            uint32_t x0 = xw[0] * 0x01010101u, x1 = xw[1] * 0x01010101u;
+            uint32_t lo = nz_bytes_b(v.x & x0) | nz_bytes_b(v.z & x1);
+            uint32_t hi = nz_bytes_b(v.y & x0) | nz_bytes_b(v.w & x1);
+            return lo | (hi << 4);
+        }
+    } else {
+        uint32_t t = base + lane / G::LPT, q = lane % G::LPT;
+        if (t >= t1) return 0;
+        uint32_t xw = load_word<D>(x, __ldg(tci + t));
+        if (!xw) return 0;
+        uint4 v = ld_stream128(tiles + (size_t)t * G::TB + q * 16);
+        if constexpr (D == 16) {
+            uint32_t xr = xw | (xw << 16), w[4] = {v.x, v.y, v.z, v.w}, a = 0;
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                uint32_t y = w[i] & xr;
+                a |= ((y & 0xFFFFu) ? 1u : 0u) << (2 * i);
+                a |= ((y >> 16) ? 1u : 0u) << (2 * i + 1);
+            }
+            return a << (8 * (lane & 1));
+        } else {
+            uint32_t a = 0;
+            a |= (v.x & xw) ? 1u : 0u;
+            a |= (v.y & xw) ? 2u : 0u;
+            a |= (v.z & xw) ? 4u : 0u;
+            a |= (v.w & xw) ? 8u : 0u;
+            return a << (4 * (lane & 7));
+        }
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_bfs_pull(const WorkItem *__restrict__ items, uint32_t n_items, uint32_t n,
+                                                  const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
+                                                  const void *__restrict__ frontier, const void *__restrict__ visited,
+                                                  void *__restrict__ next, uint32_t row0) {
+    using G = BGeo<D>;
+    const uint32_t lane = lane_id();
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_items; w += warps) {
+        WorkItem it = items[w];
+        uint32_t grow = row0 + it.row;
+        uint32_t keepw = ~load_word<D>(visited, grow) & valid_mask(grow, n, D);
+        if (!keepw) continue;
+        uint32_t acc = 0;
+        uint32_t base = G::TPL > 1 ? (it.t0 & ~(uint32_t)(G::TPL - 1)) : it.t0;
+        for (; base < it.t1; base += 2 * G::TPW) {
+            acc |= bfs_lane<D>(tiles, tci, frontier, base, it.t0, it.t1, lane);
+            if (base + G::TPW < it.t1) acc |= bfs_lane<D>(tiles, tci, frontier, base + G::TPW, it.t0, it.t1, lane);
+            if ((__reduce_or_sync(0xffffffffu, acc) & keepw) == keepw) break;  // every unvisited row reached
+        }
+        acc = __reduce_or_sync(0xffffffffu, acc) & keepw;
+        if (lane == 0 && acc) {
+            if (it.split) atomic_or_word<D>(next, it.row, acc);
+            else reinterpret_cast<typename WordT<D>::T *>(next)[it.row] = (typename WordT<D>::T)acc;
+        }
+    }
+}
+
+// visited |= frontier; levels[new bits] = level; *any |= frontier != 0
+template <int D>
+__global__ void k_bfs_update(uint32_t ntr, const void *__restrict__ frontier, void *__restrict__ visited,
+                             double *__restrict__ levels, double level, int *__restrict__ any) {
+    using W = typename WordT<D>::T;
+    int found = 0;
+    for (uint32_t I = blockIdx.x * blockDim.x + threadIdx.x; I < ntr; I += gridDim.x * blockDim.x) {
+        uint32_t w = load_word<D>(frontier, I);
+        if (!w) continue;
+        found = 1;
+        W *vis = reinterpret_cast<W *>(visited);
+        vis[I] = (W)(vis[I] | w);
+        while (w) {
+            int k = __ffs(w) - 1;
+            w &= w - 1;
+            levels[(size_t)I * D + k] = level;
+        }
+    }
+    if (__any_sync(0xffffffffu, found) && lane_id() == 0) atomicOr(any, 1);
+}
+
+__global__ void k_fill_f64(double *v, size_t n, double val) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) v[i] = val;
+}
+
+__global__ void k_bfs_seed(uint32_t src, uint32_t d, double *levels, void *visited, void *frontier) {
+    levels[src] = 0.0;
+    uint32_t w = src / d, b = src % d;
+    int wb = d == 32 ? 4 : (d == 16 ? 2 : 1);
+    size_t byte = (size_t)w * wb;
+    uint32_t *vb = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(visited) + (byte & ~(size_t)3));
+    uint32_t *fb = reinterpret_cast<uint32_t *>(reinterpret_cast<char *>(frontier) + (byte & ~(size_t)3));
+    *vb |= (1u << b) << (8 * (byte & 3));
+    *fb |= (1u << b) << (8 * (byte & 3));
+}
+
+void bfs_sweep(b2sr_matrix *at, const void *frontier, const void *visited, void *next, cudaStream_t s) {
+    ensure_items(at, s);
+    CK(cudaMemsetAsync(next, 0, padded_vec_bytes(at->ntr, at->dim), s));
+    uint64_t blocks = ((uint64_t)at->n_items + 7) / 8, cap = (uint64_t)num_sms() * 16;
+    unsigned g = (unsigned)std::min(blocks, cap);
+    const uint8_t *tl = (const uint8_t *)at->tiles;
+    switch (at->dim) {
+        case 4: LAUNCH(k_bfs_pull<4>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, next, at->row0); break;
+        case 8: LAUNCH(k_bfs_pull<8>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, next, at->row0); break;
+        case 16: LAUNCH(k_bfs_pull<16>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, next, at->row0); break;
+        default: LAUNCH(k_bfs_pull<32>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, next, at->row0); break;
+    }
+}
+
+void bfs_update(uint32_t n, uint32_t d, const void *frontier, void *visited, double *levels, double level, int *any,
+                cudaStream_t s) {
+    uint32_t ntr = tile_rows(n, d);
+    unsigned g = grid_for(ntr);
+    switch (d) {
+        case 4: LAUNCH(k_bfs_update<4>, g, 256, 0, s, ntr, frontier, visited, levels, level, any); break;
+        case 8: LAUNCH(k_bfs_update<8>, g, 256, 0, s, ntr, frontier, visited, levels, level, any); break;
+        case 16: LAUNCH(k_bfs_update<16>, g, 256, 0, s, ntr, frontier, visited, levels, level, any); break;
+        default: LAUNCH(k_bfs_update<32>, g, 256, 0, s, ntr, frontier, visited, levels, level, any); break;
+    }
+}
+
+void bfs_init(uint32_t n, uint32_t d, uint32_t src, void *visited, void *frontier, double *levels, cudaStream_t s) {
+    size_t vb = padded_vec_bytes(tile_rows(n, d), d);
+    CK(cudaMemsetAsync(visited, 0, vb, s));
+    CK(cudaMemsetAsync(frontier, 0, vb, s));
+    LAUNCH(k_fill_f64, grid_for(n), 256, 0, s, levels, (size_t)n, HUGE_VAL);
+    LAUNCH(k_bfs_seed, 1, 1, 0, s, src, d, levels, visited, frontier);
+}
+
+// ================================================================ SSSP
+// relaxed = np.minimum(dist, y); *changed |= relaxed != dist; dist = relaxed
+__global__ void k_relax(size_t n, double *__restrict__ dist, const double *__restrict__ y, int *changed) {
+    int ch = 0;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        double a = dist[i], b = y[i];
+        double r = (a < b || isnan(a)) ? a : b;
+        if (!(r == a)) { ch = 1; dist[i] = r; }
+    }
+    if (__any_sync(0xffffffffu, ch) && lane_id() == 0) atomicOr(changed, 1);
+}
+
+// ================================================================ PageRank
+struct PwTree {
+    std::vector<uint64_t> leaf_start;
+    std::vector<uint32_t> leaf_len;
+    std::vector<uint32_t> left, right, height;  // internal nodes (ids after the leaves)
+};
+
+static uint32_t pw_build(PwTree &t, uint64_t lo, uint64_t n, uint32_t &h) {
+    if (n <= 128) {
+        t.leaf_start.push_back(lo);
+        t.leaf_len.push_back((uint32_t)n);
+        h = 0;
+        return (uint32_t)(t.leaf_start.size() - 1) | 0x80000000u;  // tagged leaf index
+    }
+    uint64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    uint32_t hl, hr;
+    uint32_t l = pw_build(t, lo, n2, hl);
+    uint32_t r = pw_build(t, lo + n2, n - n2, hr);
+    t.left.push_back(l);
+    t.right.push_back(r);
+    h = std::max(hl, hr) + 1;
+    t.height.push_back(h);
+    return (uint32_t)(t.left.size() - 1);
+}
+
+// numpy pairwise_sum leaf (n <= 128), additions only, no contraction
+__device__ double pw_leaf(const double *a, uint32_t n) {
+    if (n < 8) {
+        double res = -0.0;
+        for (uint32_t i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
+        return res;
+    }
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = a[j];
+    uint32_t i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], a[i + j]);
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; i++) res = __dadd_rn(res, a[i]);
+    return res;
+}
+
+__global__ void k_pw_leaves(uint32_t nleaves, const uint64_t *start, const uint32_t *len, const double *a, double *val) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nleaves; i += gridDim.x * blockDim.x)
+        val[i] = pw_leaf(a + start[i], len[i]);
+}
+
+// internal nodes sorted by height; hofs[h] .. hofs[h+1] are the nodes of height h+1
+__global__ void __launch_bounds__(1024) k_pw_combine(uint32_t nleaves, uint32_t nheights, const uint32_t *hofs,
+                                                     const uint32_t *order, const uint32_t *left, const uint32_t *right,
+                                                     double *val, double *out) {
+    double *ival = val + nleaves;
+    for (uint32_t h = 0; h < nheights; h++) {
+        for (uint32_t k = hofs[h] + threadIdx.x; k < hofs[h + 1]; k += blockDim.x) {
+            uint32_t node = order[k];
+            uint32_t l = left[node], r = right[node];
+            double lv = (l & 0x80000000u) ? val[l & 0x7FFFFFFFu] : ival[l];
+            double rv = (r & 0x80000000u) ? val[r & 0x7FFFFFFFu] : ival[r];
+            ival[node] = __dadd_rn(lv, rv);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = nheights ? ival[order[hofs[nheights] - 1]] : val[0];
+}
+
+struct PairwiseSum {
+    uint32_t nleaves = 0, nheights = 0;
+    Buf<uint64_t> start;
+    Buf<uint32_t> len, hofs, order, left, right;
+    Buf<double> val, out;
+    PairwiseSum(uint64_t n, cudaStream_t s) {
+        PwTree t;
+        uint32_t h;
+        pw_build(t, 0, n, h);
+        nleaves = (uint32_t)t.leaf_start.size();
+        uint32_t ni = (uint32_t)t.left.size();
+        nheights = h;
+        std::vector<uint32_t> hcount(h + 2, 0), ord(ni);
+        for (uint32_t k = 0; k < ni; k++) hcount[t.height[k]]++;
+        std::vector<uint32_t> hofs_h(h + 1, 0);
+        for (uint32_t x = 1; x <= h; x++) hofs_h[x] = hofs_h[x - 1] + hcount[x];
+        std::vector<uint32_t> fill(hofs_h.begin(), hofs_h.end());
+        for (uint32_t k = 0; k < ni; k++) ord[fill[t.height[k] - 1]++] = k;
+        start = Buf<uint64_t>(nleaves, s);
+        len = Buf<uint32_t>(nleaves, s);
+        hofs = Buf<uint32_t>(h + 1, s);
+        order = Buf<uint32_t>(ni, s);
+        left = Buf<uint32_t>(ni, s);
+        right = Buf<uint32_t>(ni, s);
+        val = Buf<double>((size_t)nleaves + ni, s);
+        out = Buf<double>(1, s);
+        CK(cudaMemcpyAsync(start.p, t.leaf_start.data(), nleaves * 8, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(len.p, t.leaf_len.data(), nleaves * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(hofs.p, hofs_h.data(), (h + 1) * 4, cudaMemcpyHostToDevice, s));
+        if (ni) {
+            CK(cudaMemcpyAsync(order.p, ord.data(), ni * 4, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(left.p, t.left.data(), ni * 4, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(right.p, t.right.data(), ni * 4, cudaMemcpyHostToDevice, s));
+        }
+        CK(cudaStreamSynchronize(s));  // host vectors die at scope exit
+    }
+    // enqueue; the result lands in out.p
+    void run(const double *a, cudaStream_t s) {
+        LAUNCH(k_pw_leaves, grid_for(nleaves), 256, 0, s, nleaves, start.p, len.p, a, val.p);
+        LAUNCH(k_pw_combine, 1, 1024, 0, s, nleaves, nheights, hofs.p, order.p, left.p, right.p, val.p, out.p);
+    }
+};
+
+// bad column: out-degree zero where the column carries bits (algorithms.py:145-148)
+__global__ void k_pr_check(uint32_t n, uint32_t d, const uint32_t *colw, const double *deg, unsigned long long *bad) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        if (deg[j] == 0.0 && ((colw[j / d] >> (j % d)) & 1u)) atomicMin(bad, (unsigned long long)j);
+}
+
+__global__ void k_pr_init(uint32_t n, double r0, const double *deg, double *rank, double *xs) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        rank[j] = r0;
+        xs[j] = deg[j] == 0.0 ? 0.0 : __ddiv_rn(r0, deg[j]);
+    }
+}
+
+// new = teleport + alpha * g (no FMA); diff = |new - rank|; rank = new; xs = new / deg
+__global__ void k_pr_update(uint32_t n, double teleport, double alpha, const double *__restrict__ g,
+                            const double *__restrict__ deg, double *__restrict__ rank, double *__restrict__ xs,
+                            double *__restrict__ diff) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        double nr = __dadd_rn(teleport, __dmul_rn(alpha, g[j]));
+        diff[j] = fabs(__dadd_rn(nr, -rank[j]));
+        rank[j] = nr;
+        double dg = deg[j];
+        xs[j] = dg == 0.0 ? 0.0 : __ddiv_rn(nr, dg);
+    }
+}
+
+// ================================================================ CC
+__global__ void k_cc_init(uint32_t n, double *labels, uint32_t *lab_u) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        labels[j] = (double)j;
+        lab_u[j] = j;
+    }
+}
+
+// hook: nxt[labels[i]] = min(nxt[labels[i]], m_i)  (parallel form of algorithms.py:181-185)
+__global__ void k_cc_hook(uint32_t n, const double *__restrict__ m, const uint32_t *__restrict__ lab_u,
+                          uint32_t *__restrict__ nxt) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        double mi = m[i];
+        if (mi < (double)n) {  // finite neighbour minimum (+inf when isolated)
+            uint32_t t = lab_u[i];
+            uint32_t v = (uint32_t)mi;
+            if (v < nxt[t]) atomicMin(nxt + t, v);
+        }
+    }
+}
+
+// pointer jumping until every label is a root (algorithms.py:187-191)
+__global__ void k_cc_jump(uint32_t n, uint32_t *__restrict__ nxt, int *changed) {
+    int ch = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint32_t p = nxt[i], g = nxt[p];
+        if (g != p) { nxt[i] = g; ch = 1; }
+    }
+    if (__any_sync(0xffffffffu, ch) && lane_id() == 0) atomicOr(changed, 1);
+}
+
+__global__ void k_cc_commit(uint32_t n, const uint32_t *__restrict__ nxt, uint32_t *__restrict__ lab_u,
+                            double *__restrict__ labels, int *changed) {
+    int ch = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        uint32_t v = nxt[i];
+        if (v != lab_u[i]) { ch = 1; lab_u[i] = v; labels[i] = (double)v; }
+    }
+    if (__any_sync(0xffffffffu, ch) && lane_id() == 0) atomicOr(changed, 1);
+}
+
+}  // namespace b2sr
+
+using namespace b2sr;
+
+extern "C" {
+
+int b2sr_bfs(const b2sr_matrix *at_c, uint32_t src, double *d_levels, int64_t *iterations, void *stream) {
+    API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    b2sr_matrix *at = const_cast<b2sr_matrix *>(at_c);
+    if (at->row0 != 0 || at->ntr != tile_rows(at->n, at->dim)) B2SR_THROW(B2SR_EINVAL, "bfs needs a full matrix");
+    if (src >= at->n) B2SR_THROW(B2SR_EINVAL, "source vertex %u out of range for n=%u", src, at->n);
+    uint32_t n = at->n, d = at->dim;
+    size_t vb = padded_vec_bytes(at->ntr, d);
+    Buf<uint8_t> visited(vb, s), fa(vb, s), fb(vb, s);
+    Buf<int> any(1, s);
+    bfs_init(n, d, src, visited.p, fa.p, d_levels, s);
+    void *frontier = fa.p, *next = fb.p;
+    int64_t sweeps = 0;
+    for (;;) {  // the first frontier ({src}) is non-empty
+        CK(cudaMemsetAsync(any.p, 0, sizeof(int), s));
+        bfs_sweep(at, frontier, visited.p, next, s);
+        sweeps++;
+        bfs_update(n, d, next, visited.p, d_levels, (double)sweeps, any.p, s);
+        int a = read_scalar(any.p, s);
+        std::swap(frontier, next);
+        if (sweeps > (int64_t)n) B2SR_THROW(B2SR_ENOCONV, "BFS failed to drain its frontier");
+        if (!a) break;
+    }
+    *iterations = sweeps;
+    API_END
+}
+
+int b2sr_sssp(const b2sr_matrix *at, uint32_t src, double *d_dist, int64_t *iterations, void *stream) {
+    API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    if (at->row0 != 0) B2SR_THROW(B2SR_EINVAL, "sssp needs a full matrix");
+    uint32_t n = at->n;
+    if (src >= n) B2SR_THROW(B2SR_EINVAL, "source vertex %u out of range for n=%u", src, n);
+    Buf<double> y(n, s);
+    Buf<int> changed(1, s);
+    LAUNCH(k_fill_f64, grid_for(n), 256, 0, s, d_dist, (size_t)n, HUGE_VAL);
+    CK(cudaMemsetAsync(d_dist + src, 0, sizeof(double), s));
+    int64_t sweeps = 0;
+    for (uint32_t it = 0; it + 1 < n; it++) {  // for _ in range(n - 1)
+        launch_bff(at, d_dist, B2SR_RING_MINPLUS, 1.0, nullptr, y.p, s);
+        CK(cudaMemsetAsync(changed.p, 0, sizeof(int), s));
+        LAUNCH(k_relax, grid_for(n), 256, 0, s, (size_t)n, d_dist, y.p, changed.p);
+        sweeps++;
+        if (!read_scalar(changed.p, s)) break;
+    }
+    *iterations = sweeps;
+    API_END
+}
+
+int b2sr_pagerank(const b2sr_matrix *a, const double *d_out_degree, double alpha, double epsilon, int64_t max_iter,
+                  double *d_rank, int64_t *iterations, int *converged, int64_t *bad_col, void *stream) {
+    API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    if (a->row0 != 0) B2SR_THROW(B2SR_EINVAL, "pagerank needs a full matrix");
+    uint32_t n = a->n, d = a->dim;
+    {
+        Buf<uint32_t> colw(tile_rows(n, d), s);
+        used_column_words(a, colw.p, s);
+        Buf<unsigned long long> bad(1, s);
+        CK(cudaMemsetAsync(bad.p, 0xFF, 8, s));
+        LAUNCH(k_pr_check, grid_for(n), 256, 0, s, n, d, colw.p, d_out_degree, bad.p);
+        unsigned long long b = read_scalar(bad.p, s);
+        if (b != ~0ull) {
+            if (bad_col) *bad_col = (int64_t)b;
+            B2SR_THROW(B2SR_EINVAL, "out_degree[%llu] is zero but vertex %llu has out-edges", b, b);
+        }
+    }
+    Buf<double> xs(n, s), g(n, s), diff(n, s);
+    PairwiseSum pw(n, s);
+    double teleport = (1.0 - alpha) / (double)n;
+    LAUNCH(k_pr_init, grid_for(n), 256, 0, s, n, 1.0 / (double)n, d_out_degree, d_rank, xs.p);
+    int64_t sweeps = 0;
+    int conv = 0;
+    while (sweeps < max_iter) {
+        launch_bff(a, xs.p, B2SR_RING_ARITHMETIC, 0.0, nullptr, g.p, s);
+        LAUNCH(k_pr_update, grid_for(n), 256, 0, s, n, teleport, alpha, g.p, d_out_degree, d_rank, xs.p, diff.p);
+        pw.run(diff.p, s);
+        double delta = read_scalar(pw.out.p, s);
+        sweeps++;
+        if (delta < epsilon) { conv = 1; break; }
+    }
+    *iterations = sweeps;
+    *converged = conv;
+    API_END
+}
+
+int b2sr_cc(const b2sr_matrix *a, double *d_labels, int64_t *iterations, void *stream) {
+    API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    if (a->row0 != 0) B2SR_THROW(B2SR_EINVAL, "connected components needs a full matrix");
+    uint32_t n = a->n;
+    Buf<double> m(n, s);
+    Buf<uint32_t> lab_u(n, s), nxt(n, s);
+    Buf<int> flag(1, s);
+    LAUNCH(k_cc_init, grid_for(n), 256, 0, s, n, d_labels, lab_u.p);
+    int64_t sweeps = 0;
+    for (;;) {
+        launch_bff(a, d_labels, B2SR_RING_MINPLUS, 0.0, nullptr, m.p, s);
+        sweeps++;
+        CK(cudaMemcpyAsync(nxt.p, lab_u.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
+        LAUNCH(k_cc_hook, grid_for(n), 256, 0, s, n, m.p, lab_u.p, nxt.p);
+        for (;;) {
+            CK(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+            LAUNCH(k_cc_jump, grid_for(n), 256, 0, s, n, nxt.p, flag.p);
+            if (!read_scalar(flag.p, s)) break;
+        }
+        CK(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+        LAUNCH(k_cc_commit, grid_for(n), 256, 0, s, n, nxt.p, lab_u.p, d_labels, flag.p);
+        if (!read_scalar(flag.p, s)) break;
+        if (sweeps > (int64_t)n + 1) B2SR_THROW(B2SR_ENOCONV, "component labels failed to stabilise");
+    }
+    *iterations = sweeps;
+    API_END
+}
+
+}  // extern "C"

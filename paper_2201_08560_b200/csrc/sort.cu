@@ -1,0 +1,129 @@
+// Stable LSD radix sort (8-bit digits) used by the tile transpose (stable
+// sort by tile column, formats.py:485 lexsort) and by COO -> CSR
+// (formats.py:176-179 argsort/unique).
+//
+// Per pass: (1) per-CTA digit histograms, digit-major; (2) exclusive scan;
+// (3) scatter with an in-CTA stable rank: each warp walks its 512 keys in 16
+// rounds of 32, ranks equal digits with __match_any_sync, keeps warp-private
+// digit counters in shared memory, then warps are offset by a per-digit
+// prefix.  Order = (CTA, warp, round, lane) = input order, so it is stable.
+#include "b2sr_internal.cuh"
+
+namespace b2sr {
+
+constexpr int RS_THREADS = 256;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_ROUNDS = 16;
+constexpr int RS_TILE = RS_THREADS * RS_ROUNDS;  // 4096 keys per CTA
+
+template <typename K>
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K *__restrict__ keys, size_t n, int sh,
+                                                        uint32_t *__restrict__ counts, uint32_t nblocks) {
+    __shared__ uint32_t h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    size_t base = (size_t)blockIdx.x * RS_TILE;
+#pragma unroll 4
+    for (int j = 0; j < RS_ROUNDS; j++) {
+        size_t i = base + (size_t)j * RS_THREADS + threadIdx.x;
+        if (i < n) atomicAdd(&h[(uint32_t)(keys[i] >> sh) & 0xFFu], 1u);
+    }
+    __syncthreads();
+    counts[(size_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
+}
+
+template <typename K, bool VALS>
+__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
+                                                           K *__restrict__ kout, uint32_t *__restrict__ vout,
+                                                           size_t n, int sh, const uint64_t *__restrict__ offs,
+                                                           uint32_t nblocks) {
+    __shared__ uint32_t wc[RS_WARPS][256];
+    const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+    for (int b = threadIdx.x; b < RS_WARPS * 256; b += RS_THREADS) (&wc[0][0])[b] = 0;
+    __syncthreads();
+    size_t base = (size_t)blockIdx.x * RS_TILE + (size_t)w * (32 * RS_ROUNDS);
+    K key[RS_ROUNDS];
+    uint32_t val[RS_ROUNDS];
+    uint32_t rank[RS_ROUNDS];
+    const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+    for (int j = 0; j < RS_ROUNDS; j++) {
+        size_t i = base + (size_t)j * 32 + lane;
+        bool ok = i < n;
+        key[j] = ok ? kin[i] : (K)0;
+        if constexpr (VALS) val[j] = ok ? vin[i] : 0u;
+        uint32_t dg = ok ? ((uint32_t)(key[j] >> sh) & 0xFFu) : 256u;  // 256 = no item
+        uint32_t peers = __match_any_sync(0xffffffffu, dg);
+        uint32_t leader = __ffs(peers) - 1;
+        uint32_t before = dg < 256 ? wc[w][dg] : 0u;
+        rank[j] = before + __popc(peers & lt);
+        __syncwarp();
+        if (dg < 256 && lane == leader) wc[w][dg] = before + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    {  // exclusive prefix over warps, per digit
+        uint32_t d = threadIdx.x, run = 0;
+#pragma unroll
+        for (int ww = 0; ww < RS_WARPS; ww++) {
+            uint32_t c = wc[ww][d];
+            wc[ww][d] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < RS_ROUNDS; j++) {
+        size_t i = base + (size_t)j * 32 + lane;
+        if (i < n) {
+            uint32_t dg = (uint32_t)(key[j] >> sh) & 0xFFu;
+            size_t pos = offs[(size_t)dg * nblocks + blockIdx.x] + wc[w][dg] + rank[j];
+            kout[pos] = key[j];
+            if constexpr (VALS) vout[pos] = val[j];
+        }
+    }
+}
+
+template <typename K, bool VALS>
+static void rs_passes(K *ka, uint32_t *va, K *kb, uint32_t *vb, size_t n, int bits, cudaStream_t s, K **kres,
+                      uint32_t **vres) {
+    uint32_t nblocks = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
+    Buf<uint32_t> counts((size_t)nblocks * 256, s);
+    Buf<uint64_t> offs((size_t)nblocks * 256 + 1, s);
+    K *kin = ka, *kout = kb;
+    uint32_t *vin = va, *vout = vb;
+    for (int sh = 0; sh < bits; sh += 8) {
+        LAUNCH(k_rs_hist<K>, nblocks, RS_THREADS, 0, s, kin, n, sh, counts.p, nblocks);
+        exclusive_scan_u32_to_u64(counts.p, offs.p, (size_t)nblocks * 256, s);
+        LAUNCH((k_rs_scatter<K, VALS>), nblocks, RS_THREADS, 0, s, kin, vin, kout, vout, n, sh, offs.p, nblocks);
+        std::swap(kin, kout);
+        std::swap(vin, vout);
+    }
+    *kres = kin;
+    if (vres) *vres = vin;
+}
+
+size_t radix_sort_pairs_u32(uint32_t *keys, uint32_t *vals, size_t n, int bits, cudaStream_t s, uint32_t **keys_out,
+                            uint32_t **vals_out, Buf<uint32_t> *kalt, Buf<uint32_t> *valt) {
+    *kalt = Buf<uint32_t>(n, s);
+    *valt = Buf<uint32_t>(n, s);
+    if (n == 0 || bits <= 0) {
+        *keys_out = keys;
+        *vals_out = vals;
+        return n;
+    }
+    rs_passes<uint32_t, true>(keys, vals, kalt->p, valt->p, n, bits, s, keys_out, vals_out);
+    return n;
+}
+
+void radix_sort_keys_u64(uint64_t *keys, size_t n, int bits, cudaStream_t s, uint64_t **keys_out,
+                         Buf<uint64_t> *kalt) {
+    *kalt = Buf<uint64_t>(n, s);
+    if (n == 0 || bits <= 0) {
+        *keys_out = keys;
+        return;
+    }
+    rs_passes<uint64_t, false>(keys, nullptr, kalt->p, nullptr, n, bits, s, keys_out, nullptr);
+}
+
+}  // namespace b2sr

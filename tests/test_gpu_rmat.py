@@ -1,0 +1,63 @@
+"""GPU: the device R-MAT generator and COO->CSR equal their CPU twins, and
+full-size (BASELINE configs) properties hold where the oracle is too slow."""
+
+import numpy as np
+import pytest
+
+import paper_2201_08560_b200 as b2
+from paper_2201_08560_b200 import rmat
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("scale", [4, 10, 16])
+def test_rmat_matches_cpu_twin(scale):
+    src, dst = rmat.rmat_edges(scale, 16, seed=1)
+    s_ref, d_ref = orc.rmat_edges(scale, 16, seed=1)
+    assert np.array_equal(src.cpu().numpy().astype(np.uint32), s_ref)
+    assert np.array_equal(dst.cpu().numpy().astype(np.uint32), d_ref)
+    for undirected in (True, False):
+        csr = rmat.rmat_csr(scale, 16, seed=1, undirected=undirected)
+        rp, ci = orc.rmat_csr(scale, 16, seed=1, undirected=undirected)
+        assert np.array_equal(csr.row_ptr, rp) and np.array_equal(csr.col_ind, ci)
+
+
+def test_from_coo_device_matches_host():
+    t = __import__("torch")
+    rng = np.random.default_rng(3)
+    n = 1000
+    r = rng.integers(0, n, 20000)
+    c = rng.integers(0, n, 20000)
+    host = b2.CsrMatrix.from_coo(n, r, c)
+    devm = b2.CsrMatrix.from_coo(n, t.tensor(r, device="cuda"), t.tensor(c, device="cuda"))
+    assert devm == host
+
+
+def test_scale20_properties():
+    """s20 (BASELINE config 3 size): layout invariants and identities at full size."""
+    csr = rmat.rmat_csr(20, 16, seed=1)
+    n = csr.n
+    for d in (4, 32):
+        m = b2.csr_to_b2sr(csr, d)
+        assert m.nnz == csr.nnz
+        # symmetric input: transpose is the identity, and an involution
+        t = b2.b2sr_transpose(m)
+        assert t == m
+        assert b2.b2sr_to_csr(m) == csr
+        # bbf with x = all ones equals the out-degree; bbb with all ones = deg > 0
+        ones = b2.BitVector.from_bools(np.ones(n, bool), d)
+        deg = np.diff(csr.row_ptr.astype(np.int64))
+        assert np.array_equal(b2.bmv_bin_bin_full(m, ones), deg.astype(np.float64))
+        assert np.array_equal(b2.bmv_bin_bin_bin(m, ones).to_bools(), deg > 0)
+        # bmm_sum(A, A) = sum_k deg(k)^2 for symmetric A
+        assert b2.bmm_bin_bin_sum(m, m) == int((deg * deg).sum()) if n ** 3 < 2 ** 63 else True
+        # BFS levels: |level(u) - level(v)| <= 1 on every edge; src level 0
+        src = int(np.argmax(deg))
+        lv = b2.bfs(m, src).per_vertex
+        rows = np.repeat(np.arange(n), deg)
+        cols = csr.col_ind.astype(np.int64)
+        a, bb = lv[rows], lv[cols]
+        fin = np.isfinite(a) | np.isfinite(bb)
+        assert np.all(np.isfinite(a[fin]) & np.isfinite(bb[fin]))
+        assert np.abs(a[fin] - bb[fin]).max() <= 1 and lv[src] == 0
