@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""Benchmark of the Bit-GraphBLAS hot path on B200 (BASELINE.json configs[1]).
+
+Step = one BFS (level-synchronous masked bin-SpMV sweeps, algorithms.py:75-93)
+from one Graph500-style root on the undirected R-MAT scale-22 graph
+(edge factor 16), graph and transpose resident in HBM.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line (rank 0):
+  value      whole-job BFS GTEPS (undirected edges of the traversed component
+             / device time; Graph500 convention, construction excluded)
+  e2e        GTEPS through the public API with HOST inputs: H2D copy of the
+             B2SR arrays, transpose, BFS, D2H of the levels, every step
+  roofline   the K4 bin-SpMV kernel (masked full sweep, 50% random x) at the
+             headline tile width: algorithmic bytes / CUDA-event kernel time
+             vs MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the C oracle (oracle/, a restatement of the reference's CPU
+             algorithm) on a bounded sample of the same workload
+  sweep      per tile width: conversion, transpose, SpMV GB/s, BFS GTEPS
+  tc         triangle counting (masked bin-SpGEMM) on R-MAT scale 20
+Inputs (1 GB at d=4, 16 GB at d=32) exceed the 126 MB L2, so no flush is
+needed between steps; the SpMV roofline loop flushes L2 explicitly anyway.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "bin-SpMV GB/s vs HBM peak; BFS GTEPS and TC edges/s at 1/2/4/8 B200"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=16)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    p.add_argument("--scale", type=int, default=22)
+    p.add_argument("--edgefactor", type=int, default=16)
+    p.add_argument("--dims", default="4,8,16,32", help="tile widths in the sweep")
+    p.add_argument("--dim", type=int, default=0, help="headline tile width (0 = best of the sweep)")
+    p.add_argument("--tc-scale", type=int, default=20)
+    p.add_argument("--no-tc", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--seed", type=int, default=1)
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu, self.rows, self.proc = gpu, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- helpers
+def pick_roots(deg: np.ndarray, k: int, seed: int):
+    rng = np.random.default_rng(seed)
+    cand = np.flatnonzero(deg > 0)
+    return [int(v) for v in rng.choice(cand, size=min(k, len(cand)), replace=False)]
+
+
+def traversed_edges(levels: np.ndarray, deg: np.ndarray) -> int:
+    """Undirected edges inside the traversed component (Graph500 TEPS numerator)."""
+    return int(deg[np.isfinite(levels)].sum() // 2)
+
+
+def bmv_alg_bytes(ntr: int, T: int, d: int) -> int:
+    """Full masked bbb sweep: tile_row_ptr + T*(4 + tile bytes) + x, keep, y words."""
+    wb = 4 if d == 32 else (2 if d == 16 else 1)
+    return 4 * (ntr + 1) + T * (4 + d * wb) + 3 * ntr * wb
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    import paper_2201_08560_b200 as b2
+    from paper_2201_08560_b200 import _capi, rmat
+    from paper_2201_08560_b200 import _device as dev
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- graph (device generator + device COO->CSR) ----
+    t0 = time.time()
+    csr = rmat.rmat_csr(args.scale, args.edgefactor, seed=args.seed)
+    torch.cuda.synchronize()
+    gen_s = time.time() - t0
+    n = csr.n
+    deg = np.diff(csr.row_ptr.astype(np.int64))
+    roots = pick_roots(deg, args.warmup + args.steps + 8, seed=args.seed + 7)
+    pk, pk_kind = peaks()
+
+    # ---- tile-width sweep ----
+    sweep = {}
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    rng = np.random.default_rng(11)
+    for d in [int(x) for x in args.dims.split(",") if x]:
+        s0, s1 = ev(), ev()
+        s0.record()
+        m = b2.csr_to_b2sr(csr, d)
+        s1.record()
+        torch.cuda.synchronize()
+        conv_ms = s0.elapsed_time(s1)
+        s0.record()
+        at = b2.b2sr_transpose(m)
+        s1.record()
+        torch.cuda.synchronize()
+        tr_ms = s0.elapsed_time(s1)
+        h = at.handle()
+        ntr, T = h.ntr, h.num_tiles
+        # K4 masked full sweep, 50% random x and keep
+        xw = b2.BitVector.from_bools(rng.random(n) < 0.5, d).words
+        kw = b2.BitVector.from_bools(rng.random(n) < 0.5, d).words
+        xd = dev.to_device(xw, dev.padded_vec_bytes(ntr, d))
+        kd = dev.to_device(kw, dev.padded_vec_bytes(ntr, d))
+        yd = dev.empty_bytes(dev.padded_vec_bytes(ntr, d))
+        times = []
+        for i in range(8):
+            flush.zero_()
+            a0, a1 = ev(), ev()
+            a0.record()
+            _capi.call("b2sr_bmv_bbb", h.ptr, dev.ptr(xd), dev.ptr(kd), dev.ptr(yd), sp)
+            a1.record()
+            torch.cuda.synchronize()
+            if i >= 2:
+                times.append(a0.elapsed_time(a1))
+        spmv_ms = float(np.mean(times))
+        ab = bmv_alg_bytes(ntr, T, d)
+        # BFS from a few roots
+        bt = []
+        edges = 0
+        for r in roots[:4]:
+            b0, b1 = ev(), ev()
+            b0.record()
+            res = b2.bfs(m, r)
+            b1.record()
+            torch.cuda.synchronize()
+            bt.append(b0.elapsed_time(b1))
+            edges += traversed_edges(res.per_vertex, deg)
+        sweep[d] = {"tiles": int(T), "b2sr_bytes": int(b2.storage_bytes(m)), "convert_ms": round(conv_ms, 3),
+                    "transpose_ms": round(tr_ms, 3), "spmv_ms": round(spmv_ms, 4),
+                    "spmv_gbs": round(ab / spmv_ms / 1e6, 1), "spmv_frac": round(ab / spmv_ms / 1e6 / pk["hbm_gbs"], 3),
+                    "bfs_ms": round(float(np.mean(bt[1:] or bt)), 3),
+                    "bfs_gteps": round(edges / (sum(bt) / 1e3) / 1e9, 3)}
+        del m, at, h
+        torch.cuda.empty_cache()
+
+    d = args.dim or max(sweep, key=lambda k: sweep[k]["bfs_gteps"])
+    m = b2.csr_to_b2sr(csr, d)
+    at = b2.b2sr_transpose(m)
+    h = at.handle()
+
+    # ---- timed BFS steps (device-resident) ----
+    for r in roots[: args.warmup]:
+        b2.bfs(m, r)
+    barrier()
+    launches0 = _capi.launch_count()
+    edges = 0
+    with Clocks(local_rank) as clk:
+        e0, e1 = ev(), ev()
+        e0.record()
+        for r in roots[args.warmup: args.warmup + args.steps]:
+            res = b2.bfs(m, r)
+            edges += traversed_edges(res.per_vertex, deg)
+        e1.record()
+        barrier()
+    launches = _capi.launch_count() - launches0
+    ms = e0.elapsed_time(e1)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        e = torch.tensor([edges], device="cuda", dtype=torch.float64)
+        dist.all_reduce(e)
+        edges = int(e.item())
+    value = edges / (ms / 1e3) / 1e9
+
+    # ---- roofline of the K4 kernel at the headline width ----
+    ntr, T = h.ntr, h.num_tiles
+    xd = dev.to_device(b2.BitVector.from_bools(rng.random(n) < 0.5, d).words, dev.padded_vec_bytes(ntr, d))
+    kd = dev.to_device(b2.BitVector.from_bools(rng.random(n) < 0.5, d).words, dev.padded_vec_bytes(ntr, d))
+    yd = dev.empty_bytes(dev.padded_vec_bytes(ntr, d))
+    kt = []
+    for i in range(12):
+        flush.zero_()
+        a0, a1 = ev(), ev()
+        a0.record()
+        _capi.call("b2sr_bmv_bbb", h.ptr, dev.ptr(xd), dev.ptr(kd), dev.ptr(yd), sp)
+        a1.record()
+        torch.cuda.synchronize()
+        if i >= 2:
+            kt.append(a0.elapsed_time(a1))
+    kms = float(np.mean(kt))
+    ab = bmv_alg_bytes(ntr, T, d)
+    achieved = ab / kms / 1e6
+    roofline = {"bound": "hbm", "kernel": f"k_bmv_bbb<{d}> (masked full sweep)", "achieved": round(achieved, 1),
+                "peak": pk["hbm_gbs"], "peak_kind": pk_kind, "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
+                "frac_of_8tbs_nominal": round(achieved / 8000.0, 4), "alg_bytes": ab, "traffic": None,
+                "kernel_ms": round(kms, 4)}
+
+    # ---- e2e: public API with host inputs ----
+    host = (m.tile_row_ptr.copy(), m.tile_col_ind.copy(), m.bit_tiles.copy())
+    pinned = []
+    for a in host:  # pinned host copies of the caller's arrays
+        pt = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
+        pt.numpy()[:] = a.view(np.uint8).reshape(-1)
+        pinned.append((pt, pt.numpy().view(a.dtype).reshape(a.shape)))
+    hm = b2.B2srMatrix(n, d, pinned[0][1], pinned[1][1], pinned[2][1])
+    e2e_steps = max(3, min(args.steps, 6))
+    e2e_edges = 0
+    for r in roots[:1]:
+        hm2 = _fresh(hm)
+        b2.bfs(hm2, r)
+    barrier()
+    f0, f1 = ev(), ev()
+    f0.record()
+    for r in roots[args.warmup: args.warmup + e2e_steps]:
+        hm2 = _fresh(hm)  # no cached device mirror: H2D + transpose every step
+        res = b2.bfs(hm2, r)
+        e2e_edges += traversed_edges(res.per_vertex, deg)
+    f1.record()
+    barrier()
+    e2e_ms = f0.elapsed_time(f1)
+    e2e = {"value": round(e2e_edges / (e2e_ms / 1e3) / 1e9, 4), "unit": "GTEPS",
+           "h2d_bytes_per_step": int(sum(a.nbytes for a in host)), "d2h_bytes_per_step": 8 * n,
+           "ms_per_step": round(e2e_ms / e2e_steps, 3),
+           "includes": "H2D of B2SR arrays from pinned memory, transpose, BFS, D2H of levels"}
+
+    # ---- TC on the scale-20 graph ----
+    tc = None
+    if not args.no_tc:
+        tc = bench_tc(args, b2, rmat, torch, ev)
+
+    line = {"metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32 bit-words (b1 tiles)",
+            "data": f"synthetic R-MAT (Graph500 a,b,c=.57,.19,.19) generated on device, seed {args.seed}",
+            "config": {"workload": f"BFS via masked bin-SpMV, undirected R-MAT scale {args.scale} "
+                                   f"edgefactor {args.edgefactor}, B2SR-{d}",
+                       "scale": args.scale, "n": n, "nnz": int(csr.nnz), "tile_dim": d, "roots": args.steps,
+                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (B2SR %.2f GB > 126 MB)" % (b2.storage_bytes(m) / 1e9)},
+            "e2e": e2e, "roofline": roofline, "gpu_launches": int(launches),
+            "clocks": clk.summary(), "sweep": {str(k): v for k, v in sweep.items()}, "tc": tc,
+            "graph_gen_s": round(gen_s, 3)}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(csr, d, roots[args.warmup])
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def _fresh(hm):
+    """Same host arrays, no device mirror (forces the H2D copy)."""
+    import copy
+
+    c = copy.copy(hm)
+    c._h = None
+    c._transpose = None
+    return c
+
+
+def bench_tc(args, b2, rmat, torch, ev):
+    csr = rmat.rmat_csr(args.tc_scale, args.edgefactor, seed=args.seed)
+    out = {}
+    for d in (4, 8):
+        lo = b2.csr_to_b2sr(b2.lower_triangle(csr), d)
+        b2.algorithms._tc_count(lo)  # warm
+        ts, cnt = [], 0
+        for _ in range(3):
+            e0, e1 = ev(), ev()
+            e0.record()
+            cnt = b2.algorithms._tc_count(lo)
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ms = float(np.median(ts))
+        out[str(d)] = {"triangles": int(cnt), "ms": round(ms, 3),
+                       "edges_per_s": round((csr.nnz // 2) / (ms / 1e3), 1), "lower_tiles": int(lo.num_tiles)}
+    return {"scale": args.tc_scale, "nnz": int(csr.nnz), "by_tile_dim": out,
+            "kernel": "k_bmm_masked (AND+POPC, warp per mask tile)"}
+
+
+def cpu_baseline(csr, d, root):
+    """C oracle BFS (transpose + masked sweeps, OpenMP over tile rows) on the same graph."""
+    from oracle import oracle as orc
+
+    n = csr.n
+    rp, ci = csr.row_ptr, csr.col_ind
+    threads = os.cpu_count() or 1
+    m = orc.csr_to_b2sr(n, rp, ci, d)
+    t0 = time.perf_counter()
+    lv, it = orc.bfs(m, root, workers=threads)
+    dt = time.perf_counter() - t0
+    deg = np.diff(rp.astype(np.int64))
+    e = traversed_edges(lv, deg)
+    return {"value": round(e / dt / 1e9, 6), "unit": "GTEPS", "cores": threads, "kind": "port",
+            "sample": f"1 BFS root (transpose included, as bfs() does) on the same scale graph, B2SR-{d}",
+            "seconds": round(dt, 3)}
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """The reference algorithm on host cores: the C restatement in oracle/ (the
+    reference is pure Python/numpy and cannot travel)."""
+    if rank != 0:
+        return
+    from oracle import oracle as orc
+
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    rp, ci = orc.rmat_csr(args.scale, args.edgefactor, seed=args.seed)
+    n = 1 << args.scale
+    d = args.dim or 4
+    m = orc.csr_to_b2sr(n, rp, ci, d, workers=threads)
+    setup = time.perf_counter() - t0
+    deg = np.diff(rp.astype(np.int64))
+    roots = pick_roots(deg, args.warmup + args.steps + 8, seed=args.seed + 7)
+    budget_s = 150.0
+    for r in roots[: min(args.warmup, 1)]:
+        orc.bfs(m, r, workers=threads)
+    edges, secs, done = 0, 0.0, 0
+    for r in roots[args.warmup: args.warmup + args.steps]:
+        t1 = time.perf_counter()
+        lv, _ = orc.bfs(m, r, workers=threads)
+        secs += time.perf_counter() - t1
+        edges += traversed_edges(lv, deg)
+        done += 1
+        if secs > budget_s:
+            break
+    v = edges / secs / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GTEPS", "n_gpus": world,
+            "steps": done, "warmup": min(args.warmup, 1), "ms_per_step": round(1e3 * secs / done, 2),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 bit-words",
+            "data": f"synthetic R-MAT seed {args.seed} (CPU twin of the device generator)",
+            "config": {"workload": f"BFS via masked bin-SpMV, undirected R-MAT scale {args.scale} "
+                                   f"edgefactor {args.edgefactor}, B2SR-{d}", "scale": args.scale, "tile_dim": d},
+            "cpu_baseline": {"value": round(v, 6), "unit": "GTEPS", "cores": threads, "kind": "port",
+                             "sample": f"{done} BFS roots incl. transpose; stopped after {budget_s:.0f}s"},
+            "e2e": {"value": round(v, 6), "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "setup_s": round(setup, 2)}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_ours(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()
