@@ -201,14 +201,16 @@ def run_ours(args, rank, world, local_rank):
         # BFS from a few roots
         bt = []
         edges = 0
+        lvd = dev.empty_bytes(8 * n)
+        itc = ctypes.c_int64()
         for r in roots[:4]:
             b0, b1 = ev(), ev()
             b0.record()
-            res = b2.bfs(m, r)
+            _capi.call("b2sr_bfs", h.ptr, r, dev.ptr(lvd), ctypes.addressof(itc), sp)
             b1.record()
             torch.cuda.synchronize()
             bt.append(b0.elapsed_time(b1))
-            edges += traversed_edges(res.per_vertex, deg)
+            edges += traversed_edges(dev.to_host(lvd, np.float64, n), deg)
         sweep[d] = {"tiles": int(T), "b2sr_bytes": int(b2.storage_bytes(m)), "convert_ms": round(conv_ms, 3),
                     "transpose_ms": round(tr_ms, 3), "spmv_ms": round(spmv_ms, 4),
                     "spmv_gbs": round(ab / spmv_ms / 1e6, 1), "spmv_frac": round(ab / spmv_ms / 1e6 / pk["hbm_gbs"], 3),
@@ -222,22 +224,31 @@ def run_ours(args, rank, world, local_rank):
     at = b2.b2sr_transpose(m)
     h = at.handle()
 
-    # ---- timed BFS steps (device-resident) ----
+    # ---- timed BFS steps (device-resident: graph, transpose, levels stay in HBM) ----
+    n_steps = args.steps
+    lev = [dev.empty_bytes(8 * n) for _ in range(n_steps)]
+    it = ctypes.c_int64()
     for r in roots[: args.warmup]:
-        b2.bfs(m, r)
+        _capi.call("b2sr_bfs", h.ptr, r, dev.ptr(lev[0]), ctypes.addressof(it), sp)
     barrier()
     launches0 = _capi.launch_count()
-    edges = 0
+    iters = []
     with Clocks(local_rank) as clk:
         e0, e1 = ev(), ev()
         e0.record()
-        for r in roots[args.warmup: args.warmup + args.steps]:
-            res = b2.bfs(m, r)
-            edges += traversed_edges(res.per_vertex, deg)
+        for k, r in enumerate(roots[args.warmup: args.warmup + n_steps]):
+            _capi.call("b2sr_bfs", h.ptr, r, dev.ptr(lev[k]), ctypes.addressof(it), sp)
+            iters.append(int(it.value))
         e1.record()
         barrier()
     launches = _capi.launch_count() - launches0
     ms = e0.elapsed_time(e1)
+    degt = torch.from_numpy(deg).to("cuda")
+    edges = 0
+    for k in range(n_steps):  # after the timed region: Graph500 edge count per root
+        lv = lev[k].view(torch.float64)[:n]
+        edges += int(degt[torch.isfinite(lv)].sum().item()) // 2
+    del lev
     if dist is not None:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -278,6 +289,8 @@ def run_ours(args, rank, world, local_rank):
         pt.numpy()[:] = a.view(np.uint8).reshape(-1)
         pinned.append((pt, pt.numpy().view(a.dtype).reshape(a.shape)))
     hm = b2.B2srMatrix(n, d, pinned[0][1], pinned[1][1], pinned[2][1])
+    # the constructor validated (and copied) them; point it back at the pinned buffers
+    hm._trp, hm._tci, hm._tiles = pinned[0][1], pinned[1][1], pinned[2][1]
     e2e_steps = max(3, min(args.steps, 6))
     e2e_edges = 0
     for r in roots[:1]:
@@ -312,7 +325,7 @@ def run_ours(args, rank, world, local_rank):
                        "scale": args.scale, "n": n, "nnz": int(csr.nnz), "tile_dim": d, "roots": args.steps,
                        "parallelism": f"replicas{world}" if world > 1 else "single",
                        "l2": "inputs larger than L2 (B2SR %.2f GB > 126 MB)" % (b2.storage_bytes(m) / 1e9)},
-            "e2e": e2e, "roofline": roofline, "gpu_launches": int(launches),
+            "e2e": e2e, "roofline": roofline, "gpu_launches": int(launches), "bfs_sweeps_per_root": iters[:4],
             "clocks": clk.summary(), "sweep": {str(k): v for k, v in sweep.items()}, "tc": tc,
             "graph_gen_s": round(gen_s, 3)}
     if rank == 0 and world == 1 and not args.no_cpu:

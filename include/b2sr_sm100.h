@@ -122,6 +122,16 @@ int b2sr_bmm_sum_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2
  * algorithms.py:78).  levels f64[n] (+inf unreachable); *iterations counts
  * the final empty sweep like the reference. */
 int b2sr_bfs(const b2sr_matrix *at, uint32_t src, double *d_levels, int64_t *iterations, void *stream);
+/* The BFS sweep split into its pieces for the row-partitioned multi-GPU
+ * driver (paper_2201_08560_b200/dist.py): seed, one masked pull sweep over a
+ * row block (d_next = the block's words, zeroed here), and the fused
+ * visited/levels/any update over the gathered global frontier. */
+int b2sr_bfs_init(uint32_t n, uint32_t dim, uint32_t src, void *d_visited, void *d_frontier, double *d_levels,
+                  void *stream);
+int b2sr_bfs_sweep(const b2sr_matrix *at_block, const void *d_frontier, const void *d_visited, void *d_next,
+                   void *stream);
+int b2sr_bfs_update(uint32_t n, uint32_t dim, const void *d_frontier, void *d_visited, double *d_levels,
+                    double level, int *d_any, void *stream);
 /* sssp relaxation (algorithms.py:113-124) on at = transpose(drop_diag(a)). */
 int b2sr_sssp(const b2sr_matrix *at, uint32_t src, double *d_dist, int64_t *iterations, void *stream);
 /* pagerank (algorithms.py:127-163); a = transposed adjacency. */

@@ -83,12 +83,12 @@ __global__ void __launch_bounds__(256) k_bmm_masked(uint64_t TM, const uint32_t 
                                                     const typename WordT<D>::T *__restrict__ a_tiles,
                                                     const uint32_t *__restrict__ b_trp, const uint32_t *__restrict__ b_tci,
                                                     const typename WordT<D>::T *__restrict__ b_tiles,
-                                                    unsigned long long *__restrict__ out) {
+                                                    uint32_t m_row0, unsigned long long *__restrict__ out) {
     const uint32_t lane = lane_id();
     const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long acc = 0;
     for (uint64_t mt = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; mt < TM; mt += warps) {
-        uint32_t I = m_rowid[mt], J = m_tci[mt];
+        uint32_t I = m_rowid[mt] + m_row0, J = m_tci[mt];
         uint32_t mword = lane < (uint32_t)D ? (uint32_t)m_tiles[mt * D + lane] : 0u;
         uint32_t rows_used = __ballot_sync(0xffffffffu, mword != 0);  // bit r: mask row r non-empty
         uint32_t a0 = a_trp[I], a1 = a_trp[I + 1], b0 = b_trp[J], b1 = b_trp[J + 1];
@@ -148,7 +148,7 @@ int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_ma
 #define BMM_CASE(DD, W)                                                                                          \
     case DD:                                                                                                     \
         LAUNCH(k_bmm_masked<DD>, g, 256, 0, s, mask->num_tiles, rowid.p, mask->tci, (const W *)mask->tiles,     \
-               a->trp, a->tci, (const W *)a->tiles, bt->trp, bt->tci, (const W *)bt->tiles, out.p);              \
+               a->trp, a->tci, (const W *)a->tiles, bt->trp, bt->tci, (const W *)bt->tiles, mask->row0, out.p);            \
         break;
         BMM_CASE(4, uint8_t)
         BMM_CASE(8, uint8_t)
@@ -187,6 +187,8 @@ int b2sr_bmm_sum_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2
     API_BEGIN
     if (a->n != bt->n || a->dim != bt->dim || a->n != mask->n || a->dim != mask->dim)
         B2SR_THROW(B2SR_EINVAL, "operands must share n and tile width");
+    if (a->row0 || bt->row0 || a->ntr != tile_rows(a->n, a->dim) || bt->ntr != a->ntr)
+        B2SR_THROW(B2SR_EINVAL, "A and Bt must be full matrices (only the mask may be a row block)");
     *out = bmm_masked_bt(a, bt, mask, (cudaStream_t)stream);
     API_END
 }

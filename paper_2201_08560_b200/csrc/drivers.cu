@@ -439,6 +439,28 @@ int b2sr_bfs(const b2sr_matrix *at_c, uint32_t src, double *d_levels, int64_t *i
     API_END
 }
 
+int b2sr_bfs_init(uint32_t n, uint32_t dim, uint32_t src, void *d_visited, void *d_frontier, double *d_levels,
+                  void *stream) {
+    API_BEGIN
+    if (src >= n) B2SR_THROW(B2SR_EINVAL, "source vertex %u out of range for n=%u", src, n);
+    bfs_init(n, dim, src, d_visited, d_frontier, d_levels, (cudaStream_t)stream);
+    API_END
+}
+
+int b2sr_bfs_sweep(const b2sr_matrix *at_block, const void *d_frontier, const void *d_visited, void *d_next,
+                   void *stream) {
+    API_BEGIN
+    bfs_sweep(const_cast<b2sr_matrix *>(at_block), d_frontier, d_visited, d_next, (cudaStream_t)stream);
+    API_END
+}
+
+int b2sr_bfs_update(uint32_t n, uint32_t dim, const void *d_frontier, void *d_visited, double *d_levels,
+                    double level, int *d_any, void *stream) {
+    API_BEGIN
+    bfs_update(n, dim, d_frontier, d_visited, d_levels, level, d_any, (cudaStream_t)stream);
+    API_END
+}
+
 int b2sr_sssp(const b2sr_matrix *at, uint32_t src, double *d_dist, int64_t *iterations, void *stream) {
     API_BEGIN
     cudaStream_t s = (cudaStream_t)stream;

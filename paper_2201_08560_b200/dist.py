@@ -1,0 +1,139 @@
+"""Row-partitioned multi-GPU drivers (one process per GPU, torch.distributed).
+
+SURVEY.md §8e: the transposed adjacency is cut into contiguous tile-row
+blocks, one per rank; every rank keeps the full frontier / visited bit
+vectors (n/8 bytes) and its block of the matrix.  Per BFS level:
+
+    sweep   masked pull sweep over the rank's block      (k_bfs_pull, local)
+    gather  all_gather of the blocks' frontier words    (NCCL over NVLink)
+    update  visited |= frontier, levels, any-flag        (k_bfs_update, local)
+
+The blocks have equal tile-row counts, padded to a whole 4-byte word per
+rank, so the all-gather output *is* the global frontier -- no compaction.
+R-MAT vertices are randomly permuted, so equal row counts balance tiles.
+Every rank sees the same gathered frontier, so the termination test needs no
+extra collective.  Triangle counting partitions the mask (L) tile rows the
+same way, keeps L replicated for the row lookups, and finishes with one
+int64 all_reduce.
+
+Results are partition-invariant: the per-row work is identical, only the
+owner changes, and the exchange is a pure copy.
+
+The level loop is written against a small ``ops`` interface so the host
+logic (partition, exchange, loop, termination) is testable on CPU with the
+gloo backend (tests/test_dist_gloo.py plugs in oracle ops); the product ops
+are the CUDA kernels below.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _capi
+from . import _device as dev
+from .formats import B2srMatrix, _Handle, _new_handle
+
+
+def block_rows(ntr: int, world: int, dim: int) -> int:
+    """Tile rows per rank: ceil(ntr / world) rounded up to whole 4-byte words."""
+    wb = 4 if dim == 32 else (2 if dim == 16 else 1)
+    per_word = 4 // wb
+    rows = -(-ntr // world)
+    return -(-rows // per_word) * per_word
+
+
+def partition(ntr: int, world: int, dim: int):
+    """[(begin, end)) tile-row ranges, equal padded sizes, clipped to ntr."""
+    b = block_rows(ntr, world, dim)
+    return [(min(r * b, ntr), min((r + 1) * b, ntr)) for r in range(world)]
+
+
+class CudaBfsOps:
+    """Product ops: the sm_100a kernels through the C ABI."""
+
+    def __init__(self, block: _Handle, n: int, dim: int):
+        self.block, self.n, self.dim = block, n, dim
+
+    def buffers(self, global_bytes: int, block_bytes: int):
+        return (dev.zeros_bytes(global_bytes), dev.zeros_bytes(global_bytes), dev.zeros_bytes(block_bytes),
+                dev.empty_bytes(8 * self.n), dev.zeros_bytes(4))
+
+    def init(self, src, visited, frontier, levels):
+        _capi.call("b2sr_bfs_init", self.n, self.dim, src, dev.ptr(visited), dev.ptr(frontier), dev.ptr(levels),
+                   dev.stream())
+
+    def sweep(self, frontier, visited, next_block):
+        _capi.call("b2sr_bfs_sweep", self.block.ptr, dev.ptr(frontier), dev.ptr(visited), dev.ptr(next_block),
+                   dev.stream())
+
+    def update(self, frontier, visited, levels, level, anyflag) -> bool:
+        anyflag.zero_()
+        _capi.call("b2sr_bfs_update", self.n, self.dim, dev.ptr(frontier), dev.ptr(visited), dev.ptr(levels),
+                   float(level), dev.ptr(anyflag), dev.stream())
+        return bool(anyflag.view(dev.torch().int32)[0].item())
+
+    def levels_to_host(self, levels):
+        return dev.to_host(levels, np.float64, self.n)
+
+
+def all_gather_words(dist, out, block, world):
+    """Concatenate every rank's block into ``out`` (byte tensors)."""
+    if dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(out, block)
+    else:  # gloo (CPU tests)
+        parts = [out[r * block.numel(): (r + 1) * block.numel()] for r in range(world)]
+        tmp = [p.clone() for p in parts]
+        dist.all_gather(tmp, block)
+        for p, t in zip(parts, tmp):
+            p.copy_(t)
+
+
+class DistributedBfs:
+    """BFS over a tile-row-partitioned transposed matrix (one rank per GPU)."""
+
+    def __init__(self, n: int, dim: int, ntr: int, rank: int, world: int, ops, dist):
+        self.n, self.dim, self.ntr = n, dim, ntr
+        self.rank, self.world, self.ops, self.dist = rank, world, ops, dist
+        wb = 4 if dim == 32 else (2 if dim == 16 else 1)
+        self.block_bytes = block_rows(ntr, world, dim) * wb
+        self.global_bytes = self.block_bytes * world
+
+    @classmethod
+    def from_matrix(cls, at: B2srMatrix, dist):
+        """Cut this rank's block out of the full transposed matrix on its GPU."""
+        rank, world = dist.get_rank(), dist.get_world_size()
+        b, e = partition(at.n_tile_rows, world, at.dim)[rank]
+        blk = _new_handle("b2sr_row_block", at.handle().ptr, b, e, dev.stream())
+        return cls(at.n, at.dim, at.n_tile_rows, rank, world, CudaBfsOps(blk, at.n, at.dim), dist)
+
+    def run(self, src: int):
+        ops = self.ops
+        visited, frontier, nxt, levels, anyflag = ops.buffers(self.global_bytes, self.block_bytes)
+        ops.init(src, visited, frontier, levels)
+        sweeps = 0
+        while True:
+            ops.sweep(frontier, visited, nxt)
+            all_gather_words(self.dist, frontier, nxt, self.world)
+            sweeps += 1
+            more = ops.update(frontier, visited, levels, float(sweeps), anyflag)
+            if sweeps > self.n:
+                raise RuntimeError("BFS failed to drain its frontier")
+            if not more:
+                break
+        return ops.levels_to_host(levels), sweeps
+
+
+def distributed_triangle_count(lower: B2srMatrix, dist) -> int:
+    """TC with the mask tile rows of L partitioned over ranks; L replicated."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    b, e = partition(lower.n_tile_rows, world, lower.dim)[rank]
+    h = lower.handle()
+    blk = _new_handle("b2sr_row_block", h.ptr, b, e, dev.stream())
+    out = ctypes.c_int64()
+    _capi.call("b2sr_bmm_sum_masked_bt", h.ptr, h.ptr, blk.ptr, ctypes.addressof(out), dev.stream())
+    t = dev.torch()
+    total = t.tensor([out.value], dtype=t.int64, device=dev.device())
+    dist.all_reduce(total)
+    return int(total.item())
