@@ -179,6 +179,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         tr_ms = s0.elapsed_time(s1)
         h = at.handle()
+        hA = m.handle()
         ntr, T = h.ntr, h.num_tiles
         # K4 masked full sweep, 50% random x and keep
         xw = b2.BitVector.from_bools(rng.random(n) < 0.5, d).words
@@ -206,7 +207,7 @@ def run_ours(args, rank, world, local_rank):
         for r in roots[:4]:
             b0, b1 = ev(), ev()
             b0.record()
-            _capi.call("b2sr_bfs", h.ptr, r, dev.ptr(lvd), ctypes.addressof(itc), sp)
+            _capi.call("b2sr_bfs", hA.ptr, h.ptr, r, dev.ptr(lvd), ctypes.addressof(itc), sp)
             b1.record()
             torch.cuda.synchronize()
             bt.append(b0.elapsed_time(b1))
@@ -216,20 +217,21 @@ def run_ours(args, rank, world, local_rank):
                     "spmv_gbs": round(ab / spmv_ms / 1e6, 1), "spmv_frac": round(ab / spmv_ms / 1e6 / pk["hbm_gbs"], 3),
                     "bfs_ms": round(float(np.mean(bt[1:] or bt)), 3),
                     "bfs_gteps": round(edges / (sum(bt) / 1e3) / 1e9, 3)}
-        del m, at, h
+        del m, at, h, hA
         torch.cuda.empty_cache()
 
     d = args.dim or max(sweep, key=lambda k: sweep[k]["bfs_gteps"])
     m = b2.csr_to_b2sr(csr, d)
     at = b2.b2sr_transpose(m)
     h = at.handle()
+    hA = m.handle()
 
     # ---- timed BFS steps (device-resident: graph, transpose, levels stay in HBM) ----
     n_steps = args.steps
     lev = [dev.empty_bytes(8 * n) for _ in range(n_steps)]
     it = ctypes.c_int64()
     for r in roots[: args.warmup]:
-        _capi.call("b2sr_bfs", h.ptr, r, dev.ptr(lev[0]), ctypes.addressof(it), sp)
+        _capi.call("b2sr_bfs", hA.ptr, h.ptr, r, dev.ptr(lev[0]), ctypes.addressof(it), sp)
     barrier()
     launches0 = _capi.launch_count()
     iters = []
@@ -237,7 +239,7 @@ def run_ours(args, rank, world, local_rank):
         e0, e1 = ev(), ev()
         e0.record()
         for k, r in enumerate(roots[args.warmup: args.warmup + n_steps]):
-            _capi.call("b2sr_bfs", h.ptr, r, dev.ptr(lev[k]), ctypes.addressof(it), sp)
+            _capi.call("b2sr_bfs", hA.ptr, h.ptr, r, dev.ptr(lev[k]), ctypes.addressof(it), sp)
             iters.append(int(it.value))
         e1.record()
         barrier()

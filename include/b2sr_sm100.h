@@ -118,10 +118,15 @@ int b2sr_bmm_sum_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2
                            int64_t *out, void *stream);
 
 /* ---- drivers (algorithms.py:75-215) ------------------------------------ */
-/* bfs on the TRANSPOSED matrix at (the caller does at = transpose(a),
- * algorithms.py:78).  levels f64[n] (+inf unreachable); *iterations counts
- * the final empty sweep like the reference. */
-int b2sr_bfs(const b2sr_matrix *at, uint32_t src, double *d_levels, int64_t *iterations, void *stream);
+/* bfs (algorithms.py:75-93).  at = transpose(a) (the caller transposes, as
+ * algorithms.py:78 does).  With a != NULL the driver is direction-optimizing:
+ * small frontiers push over a (top-down), large ones pull over at
+ * (bottom-up, masked bbb with early exit); both produce the identical
+ * next frontier.  a == NULL -> pull only.  levels f64[n] (+inf unreachable);
+ * *iterations counts the final empty sweep like the reference.  Env
+ * B2SR_BFS_ALPHA tunes the switch, B2SR_BFS_TRACE logs levels. */
+int b2sr_bfs(const b2sr_matrix *a, const b2sr_matrix *at, uint32_t src, double *d_levels, int64_t *iterations,
+             void *stream);
 /* The BFS sweep split into its pieces for the row-partitioned multi-GPU
  * driver (paper_2201_08560_b200/dist.py): seed, one masked pull sweep over a
  * row block (d_next = the block's words, zeroed here), and the fused

@@ -47,7 +47,7 @@ SIGNATURES = {
     "b2sr_bmv_bff": [P, P, i32, f64, P, P, P, P, P],
     "b2sr_bmm_sum": [P, P, P, P],
     "b2sr_bmm_sum_masked_bt": [P, P, P, P, P],
-    "b2sr_bfs": [P, u32, P, P, P],
+    "b2sr_bfs": [P, P, u32, P, P, P],
     "b2sr_bfs_init": [u32, u32, u32, P, P, P, P],
     "b2sr_bfs_sweep": [P, P, P, P, P],
     "b2sr_bfs_update": [u32, u32, P, P, P, f64, P, P],

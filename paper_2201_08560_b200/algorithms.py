@@ -83,7 +83,7 @@ def bfs(a: B2srMatrix, src: int, *, workers: int | None = None) -> AlgoResult:
     at = b2sr_transpose(a)
     levels = dev.empty_bytes(8 * a.n)
     it = ctypes.c_int64()
-    _capi.call("b2sr_bfs", at.handle().ptr, src, dev.ptr(levels), ctypes.addressof(it), dev.stream())
+    _capi.call("b2sr_bfs", a.handle().ptr, at.handle().ptr, src, dev.ptr(levels), ctypes.addressof(it), dev.stream())
     return AlgoResult(per_vertex=dev.to_host(levels, np.float64, a.n), iterations=int(it.value), converged=True)
 
 

@@ -180,6 +180,124 @@ __global__ void k_bfs_seed(uint32_t src, uint32_t d, double *levels, void *visit
     *fb |= (1u << b) << (8 * (byte & 3));
 }
 
+// ---------------------------------------------------------------- direction-optimizing pieces
+// Top-down (push) sweeps over the NON-transposed matrix a for small
+// frontiers: every frontier tile row scatters the OR of its frontier bit-rows
+// into next[K] & ~visited[K].  The set produced is exactly the pull sweep's
+// (A^T x) & ~visited, so levels are unchanged -- only the work differs.
+constexpr uint32_t PUSH_CH = 1024;  // tiles per push work entry (hub rows split)
+
+struct BfsCounters {
+    int any;
+    uint32_t list_n;                     // push work entries
+    unsigned long long frontier_tiles;   // tiles of a in frontier tile rows
+    unsigned long long unvisited_tiles;  // tiles of at in tile rows with keep != 0
+    unsigned long long frontier_vertices;
+};
+
+// visited |= next; levels[new] = level; counters; push work list for the next level
+template <int D>
+__global__ void k_bfs_update_dir(uint32_t ntr, uint32_t n, const void *__restrict__ next, void *__restrict__ visited,
+                                 double *__restrict__ levels, double level, const uint32_t *__restrict__ trp_a,
+                                 const uint32_t *__restrict__ trp_at, uint2 *__restrict__ list,
+                                 BfsCounters *__restrict__ cnt) {
+    using W = typename WordT<D>::T;
+    unsigned long long ft = 0, ut = 0, fv = 0;
+    int found = 0;
+    const uint32_t lane = lane_id();
+    uint32_t I0 = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t stride = gridDim.x * blockDim.x;
+    uint32_t iters = (ntr + stride - 1) / stride;  // warp-uniform trip count (ballots below)
+    for (uint32_t k = 0; k < iters; k++) {
+        uint32_t I = I0 + k * stride;
+        uint32_t w = 0, vis = 0, nch = 0, len = 0;
+        if (I < ntr) {
+            w = load_word<D>(next, I);
+            vis = load_word<D>(visited, I);
+            if (w) {
+                found = 1;
+                vis |= w;
+                reinterpret_cast<W *>(visited)[I] = (W)vis;
+                fv += __popc(w);
+                uint32_t b = w;
+                while (b) {
+                    int kk = __ffs(b) - 1;
+                    b &= b - 1;
+                    levels[(size_t)I * D + kk] = level;
+                }
+                if (trp_a) {
+                    len = trp_a[I + 1] - trp_a[I];
+                    ft += len;
+                    nch = (len + PUSH_CH - 1) / PUSH_CH;
+                }
+            }
+            uint32_t keep = ~vis & valid_mask(I, n, D);
+            if (keep) ut += trp_at[I + 1] - trp_at[I];
+        }
+        // warp-aggregated reservation of push entries
+        uint32_t incl = nch;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+        }
+        uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        uint32_t base = 0;
+        if (total) {
+            if (lane == 31) base = atomicAdd(&cnt->list_n, total);
+            base = __shfl_sync(0xffffffffu, base, 31);
+            uint32_t o = base + incl - nch;
+            for (uint32_t j = 0; j < nch; j++) list[o + j] = make_uint2(I, j);
+        }
+    }
+    ft = __reduce_add_sync(0xffffffffu, (uint32_t)ft) + 0ull;  // per-thread sums fit 32 bits per warp slice
+    ut = __reduce_add_sync(0xffffffffu, (uint32_t)ut) + 0ull;
+    fv = __reduce_add_sync(0xffffffffu, (uint32_t)fv) + 0ull;
+    if (lane == 0) {
+        if (ft) atomicAdd(&cnt->frontier_tiles, ft);
+        if (ut) atomicAdd(&cnt->unvisited_tiles, ut);
+        if (fv) atomicAdd(&cnt->frontier_vertices, fv);
+    }
+    if (__any_sync(0xffffffffu, found) && lane == 0) atomicOr(&cnt->any, 1);
+}
+
+// warp per push entry; lane-strided tiles
+template <int D>
+__global__ void __launch_bounds__(256) k_bfs_push(const uint2 *__restrict__ list, const BfsCounters *__restrict__ cnt,
+                                                  const uint32_t *__restrict__ trp, const uint32_t *__restrict__ tci,
+                                                  const typename WordT<D>::T *__restrict__ tiles,
+                                                  const void *__restrict__ frontier, const void *__restrict__ visited,
+                                                  void *__restrict__ next) {
+    const uint32_t lane = lane_id();
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t n_entries = cnt->list_n;
+    for (uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < n_entries; e += warps) {
+        uint2 ent = list[e];
+        uint32_t I = ent.x;
+        uint32_t t0 = trp[I] + ent.y * PUSH_CH;
+        uint32_t t1 = min(trp[I + 1], t0 + PUSH_CH);
+        uint32_t fw = load_word<D>(frontier, I);
+        for (uint32_t t = t0 + lane; t < t1; t += 32) {
+            uint32_t m = 0, f = fw;
+            while (f) {
+                int r = __ffs(f) - 1;
+                f &= f - 1;
+                m |= tiles[(size_t)t * D + r];
+            }
+            if (m) {
+                uint32_t K = __ldg(tci + t);
+                m &= ~load_word<D>(visited, K);
+                if (m) atomic_or_word<D>(next, K, m);
+            }
+        }
+    }
+}
+
+static double bfs_alpha() {
+    const char *e = getenv("B2SR_BFS_ALPHA");
+    return e ? atof(e) : 4.0;
+}
+
 void bfs_sweep(b2sr_matrix *at, const void *frontier, const void *visited, void *next, cudaStream_t s) {
     ensure_items(at, s);
     CK(cudaMemsetAsync(next, 0, padded_vec_bytes(at->ntr, at->dim), s));
@@ -412,28 +530,71 @@ using namespace b2sr;
 
 extern "C" {
 
-int b2sr_bfs(const b2sr_matrix *at_c, uint32_t src, double *d_levels, int64_t *iterations, void *stream) {
+int b2sr_bfs(const b2sr_matrix *a_c, const b2sr_matrix *at_c, uint32_t src, double *d_levels,
+             int64_t *iterations, void *stream) {
     API_BEGIN
     cudaStream_t s = (cudaStream_t)stream;
     b2sr_matrix *at = const_cast<b2sr_matrix *>(at_c);
+    const b2sr_matrix *a = a_c;
     if (at->row0 != 0 || at->ntr != tile_rows(at->n, at->dim)) B2SR_THROW(B2SR_EINVAL, "bfs needs a full matrix");
+    if (a && (a->n != at->n || a->dim != at->dim || a->row0 != 0 || a->ntr != at->ntr))
+        B2SR_THROW(B2SR_EINVAL, "a and at must be the same full matrix and its transpose");
     if (src >= at->n) B2SR_THROW(B2SR_EINVAL, "source vertex %u out of range for n=%u", src, at->n);
-    uint32_t n = at->n, d = at->dim;
-    size_t vb = padded_vec_bytes(at->ntr, d);
+    uint32_t n = at->n, d = at->dim, ntr = at->ntr;
+    size_t vb = padded_vec_bytes(ntr, d);
     Buf<uint8_t> visited(vb, s), fa(vb, s), fb(vb, s);
-    Buf<int> any(1, s);
-    bfs_init(n, d, src, visited.p, fa.p, d_levels, s);
-    void *frontier = fa.p, *next = fb.p;
+    Buf<BfsCounters> cnt(1, s);
+    size_t list_cap = a ? (size_t)ntr + a->num_tiles / PUSH_CH + 1 : 1;
+    Buf<uint2> list(list_cap, s);
+    const double alpha = bfs_alpha();
+    const bool trace = getenv("B2SR_BFS_TRACE") != nullptr;
+    // seed: next = {src}, visited = {}; the update makes it the level-0 frontier
+    LAUNCH(k_fill_f64, grid_for(n), 256, 0, s, d_levels, (size_t)n, HUGE_VAL);
+    CK(cudaMemsetAsync(visited.p, 0, vb, s));
+    CK(cudaMemsetAsync(fb.p, 0, vb, s));
+    CK(cudaMemsetAsync(fa.p, 0, vb, s));
+    LAUNCH(k_bfs_seed, 1, 1, 0, s, src, d, d_levels, fa.p, fb.p);  // sets the bit in both; fa re-zeroed below
+    CK(cudaMemsetAsync(fa.p, 0, vb, s));
+    void *frontier = fb.p, *next = fa.p;
+    BfsCounters h{};
+    auto update = [&](const void *fr, double level) {
+        CK(cudaMemsetAsync(cnt.p, 0, sizeof(BfsCounters), s));
+        unsigned g = grid_for(ntr);
+        const uint32_t *ta = a ? a->trp : nullptr;
+        switch (d) {
+            case 4: LAUNCH(k_bfs_update_dir<4>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, list.p, cnt.p); break;
+            case 8: LAUNCH(k_bfs_update_dir<8>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, list.p, cnt.p); break;
+            case 16: LAUNCH(k_bfs_update_dir<16>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, list.p, cnt.p); break;
+            default: LAUNCH(k_bfs_update_dir<32>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, list.p, cnt.p); break;
+        }
+        CK(cudaMemcpyAsync(&h, cnt.p, sizeof(BfsCounters), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    };
+    update(frontier, 0.0);  // level 0 = {src}
     int64_t sweeps = 0;
-    for (;;) {  // the first frontier ({src}) is non-empty
-        CK(cudaMemsetAsync(any.p, 0, sizeof(int), s));
-        bfs_sweep(at, frontier, visited.p, next, s);
+    for (;;) {
+        bool push = a && (double)h.frontier_tiles * alpha < (double)h.unvisited_tiles;
+        if (push) {
+            CK(cudaMemsetAsync(next, 0, vb, s));
+            uint64_t blocks = ((uint64_t)h.list_n + 7) / 8, cap = (uint64_t)num_sms() * 16;
+            unsigned g = (unsigned)std::max<uint64_t>(1, std::min(blocks, cap));
+            switch (d) {
+                case 4: LAUNCH(k_bfs_push<4>, g, 256, 0, s, list.p, cnt.p, a->trp, a->tci, (const uint8_t *)a->tiles, frontier, visited.p, next); break;
+                case 8: LAUNCH(k_bfs_push<8>, g, 256, 0, s, list.p, cnt.p, a->trp, a->tci, (const uint8_t *)a->tiles, frontier, visited.p, next); break;
+                case 16: LAUNCH(k_bfs_push<16>, g, 256, 0, s, list.p, cnt.p, a->trp, a->tci, (const uint16_t *)a->tiles, frontier, visited.p, next); break;
+                default: LAUNCH(k_bfs_push<32>, g, 256, 0, s, list.p, cnt.p, a->trp, a->tci, (const uint32_t *)a->tiles, frontier, visited.p, next); break;
+            }
+        } else {
+            bfs_sweep(at, frontier, visited.p, next, s);
+        }
         sweeps++;
-        bfs_update(n, d, next, visited.p, d_levels, (double)sweeps, any.p, s);
-        int a = read_scalar(any.p, s);
+        if (trace)
+            fprintf(stderr, "[b2sr bfs] level %lld %s frontier_v=%llu frontier_tiles=%llu unvisited_tiles=%llu\n",
+                    (long long)sweeps, push ? "push" : "pull", h.frontier_vertices, h.frontier_tiles, h.unvisited_tiles);
+        update(next, (double)sweeps);
         std::swap(frontier, next);
         if (sweeps > (int64_t)n) B2SR_THROW(B2SR_ENOCONV, "BFS failed to drain its frontier");
-        if (!a) break;
+        if (!h.any) break;
     }
     *iterations = sweeps;
     API_END
