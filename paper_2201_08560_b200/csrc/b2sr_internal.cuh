@@ -132,6 +132,10 @@ struct b2sr_matrix {
     b2sr::WorkItem *items = nullptr;
     uint32_t n_items = 0;
     bool any_split = false;
+    // cached row-liveness words (bit r of word I: bit-row I*dim+r holds any
+    // set bit), same layout as a BitVector; BFS never needs to wait for a
+    // vertex without in-edges
+    void *live = nullptr;
 };
 
 namespace b2sr {

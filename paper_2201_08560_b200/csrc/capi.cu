@@ -95,6 +95,7 @@ void free_matrix(b2sr_matrix *m) {
     dfree(m->tci, nullptr);
     dfree(m->tiles, nullptr);
     dfree(m->items, nullptr);
+    dfree(m->live, nullptr);
     if (cur != m->device) cudaSetDevice(cur);
     delete m;
 }

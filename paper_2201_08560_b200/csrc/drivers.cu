@@ -120,14 +120,14 @@ template <int D>
 __global__ void __launch_bounds__(256) k_bfs_pull(const WorkItem *__restrict__ items, uint32_t n_items, uint32_t n,
                                                   const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
                                                   const void *__restrict__ frontier, const void *__restrict__ visited,
-                                                  void *__restrict__ next, uint32_t row0) {
+                                                  const void *__restrict__ live, void *__restrict__ next, uint32_t row0) {
     using G = BGeo<D>;
     const uint32_t lane = lane_id();
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_items; w += warps) {
         WorkItem it = items[w];
         uint32_t grow = row0 + it.row;
-        uint32_t keepw = ~load_word<D>(visited, grow) & valid_mask(grow, n, D);
+        uint32_t keepw = ~load_word<D>(visited, grow) & load_word<D>(live, it.row);  // live is block-local
         if (!keepw) continue;
         uint32_t acc = 0;
         uint32_t base = G::TPL > 1 ? (it.t0 & ~(uint32_t)(G::TPL - 1)) : it.t0;
@@ -199,8 +199,8 @@ struct BfsCounters {
 template <int D>
 __global__ void k_bfs_update_dir(uint32_t ntr, uint32_t n, const void *__restrict__ next, void *__restrict__ visited,
                                  double *__restrict__ levels, double level, const uint32_t *__restrict__ trp_a,
-                                 const uint32_t *__restrict__ trp_at, uint2 *__restrict__ list,
-                                 BfsCounters *__restrict__ cnt) {
+                                 const uint32_t *__restrict__ trp_at, const void *__restrict__ live_at,
+                                 uint2 *__restrict__ list, BfsCounters *__restrict__ cnt) {
     using W = typename WordT<D>::T;
     unsigned long long ft = 0, ut = 0, fv = 0;
     int found = 0;
@@ -231,7 +231,7 @@ __global__ void k_bfs_update_dir(uint32_t ntr, uint32_t n, const void *__restric
                     nch = (len + PUSH_CH - 1) / PUSH_CH;
                 }
             }
-            uint32_t keep = ~vis & valid_mask(I, n, D);
+            uint32_t keep = ~vis & load_word<D>(live_at, I);
             if (keep) ut += trp_at[I + 1] - trp_at[I];
         }
         // warp-aggregated reservation of push entries
@@ -298,17 +298,48 @@ static double bfs_alpha() {
     return e ? atof(e) : 4.0;
 }
 
+// live[I] bit r: bit-row I*D+r of m has at least one set bit (warp per tile row)
+template <int D>
+__global__ void k_row_live(uint32_t ntr, const uint32_t *__restrict__ trp, const typename WordT<D>::T *__restrict__ tiles,
+                           typename WordT<D>::T *__restrict__ live) {
+    const uint32_t lane = lane_id();
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t I = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; I < ntr; I += warps) {
+        uint32_t o = 0;
+        for (uint32_t t = trp[I] + lane; t < trp[I + 1]; t += 32)
+#pragma unroll
+            for (int r = 0; r < D; r++) o |= (tiles[(size_t)t * D + r] ? 1u : 0u) << r;
+        o = __reduce_or_sync(0xffffffffu, o);
+        if (lane == 0) live[I] = (typename WordT<D>::T)o;
+    }
+}
+
+void ensure_live(b2sr_matrix *m, cudaStream_t s) {
+    if (m->live) return;
+    Buf<uint8_t> lv(padded_vec_bytes(m->ntr, m->dim), s);
+    CK(cudaMemsetAsync(lv.p, 0, padded_vec_bytes(m->ntr, m->dim), s));
+    unsigned g = grid_for((uint64_t)m->ntr * 32);
+    switch (m->dim) {
+        case 4: LAUNCH(k_row_live<4>, g, 256, 0, s, m->ntr, m->trp, (const uint8_t *)m->tiles, (uint8_t *)lv.p); break;
+        case 8: LAUNCH(k_row_live<8>, g, 256, 0, s, m->ntr, m->trp, (const uint8_t *)m->tiles, (uint8_t *)lv.p); break;
+        case 16: LAUNCH(k_row_live<16>, g, 256, 0, s, m->ntr, m->trp, (const uint16_t *)m->tiles, (uint16_t *)lv.p); break;
+        default: LAUNCH(k_row_live<32>, g, 256, 0, s, m->ntr, m->trp, (const uint32_t *)m->tiles, (uint32_t *)lv.p); break;
+    }
+    m->live = lv.release();
+}
+
 void bfs_sweep(b2sr_matrix *at, const void *frontier, const void *visited, void *next, cudaStream_t s) {
     ensure_items(at, s);
+    ensure_live(at, s);
     CK(cudaMemsetAsync(next, 0, padded_vec_bytes(at->ntr, at->dim), s));
     uint64_t blocks = ((uint64_t)at->n_items + 7) / 8, cap = (uint64_t)num_sms() * 16;
     unsigned g = (unsigned)std::min(blocks, cap);
     const uint8_t *tl = (const uint8_t *)at->tiles;
     switch (at->dim) {
-        case 4: LAUNCH(k_bfs_pull<4>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, next, at->row0); break;
-        case 8: LAUNCH(k_bfs_pull<8>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, next, at->row0); break;
-        case 16: LAUNCH(k_bfs_pull<16>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, next, at->row0); break;
-        default: LAUNCH(k_bfs_pull<32>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, next, at->row0); break;
+        case 4: LAUNCH(k_bfs_pull<4>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0); break;
+        case 8: LAUNCH(k_bfs_pull<8>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0); break;
+        case 16: LAUNCH(k_bfs_pull<16>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0); break;
+        default: LAUNCH(k_bfs_pull<32>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0); break;
     }
 }
 
@@ -546,6 +577,8 @@ int b2sr_bfs(const b2sr_matrix *a_c, const b2sr_matrix *at_c, uint32_t src, doub
     Buf<BfsCounters> cnt(1, s);
     size_t list_cap = a ? (size_t)ntr + a->num_tiles / PUSH_CH + 1 : 1;
     Buf<uint2> list(list_cap, s);
+    ensure_live(at, s);
+    ensure_items(at, s);
     const double alpha = bfs_alpha();
     const bool trace = getenv("B2SR_BFS_TRACE") != nullptr;
     // seed: next = {src}, visited = {}; the update makes it the level-0 frontier
@@ -562,10 +595,10 @@ int b2sr_bfs(const b2sr_matrix *a_c, const b2sr_matrix *at_c, uint32_t src, doub
         unsigned g = grid_for(ntr);
         const uint32_t *ta = a ? a->trp : nullptr;
         switch (d) {
-            case 4: LAUNCH(k_bfs_update_dir<4>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, list.p, cnt.p); break;
-            case 8: LAUNCH(k_bfs_update_dir<8>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, list.p, cnt.p); break;
-            case 16: LAUNCH(k_bfs_update_dir<16>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, list.p, cnt.p); break;
-            default: LAUNCH(k_bfs_update_dir<32>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, list.p, cnt.p); break;
+            case 4: LAUNCH(k_bfs_update_dir<4>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, at->live, list.p, cnt.p); break;
+            case 8: LAUNCH(k_bfs_update_dir<8>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, at->live, list.p, cnt.p); break;
+            case 16: LAUNCH(k_bfs_update_dir<16>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, at->live, list.p, cnt.p); break;
+            default: LAUNCH(k_bfs_update_dir<32>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, at->live, list.p, cnt.p); break;
         }
         CK(cudaMemcpyAsync(&h, cnt.p, sizeof(BfsCounters), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
