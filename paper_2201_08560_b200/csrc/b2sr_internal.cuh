@@ -136,6 +136,8 @@ struct b2sr_matrix {
     // set bit), same layout as a BitVector; BFS never needs to wait for a
     // vertex without in-edges
     void *live = nullptr;
+    // cached column-strip blocked layout for bin-SpMV (bmv_blocked.cu)
+    void *plan = nullptr;
 };
 
 namespace b2sr {
@@ -149,6 +151,11 @@ void free_matrix(b2sr_matrix *m);
 void ensure_items(b2sr_matrix *m, cudaStream_t s);  // bin-SpMV work partition
 int num_sms();
 void launch_row_ids(const b2sr_matrix *m, uint32_t *rowid, cudaStream_t s);  // rowid[t] = tile row of t
+void free_plan(void *plan);
+// blocked bin-SpMV: mode 0 = masked bbb, 1 = BFS pull; false if not applicable
+bool launch_blocked(b2sr_matrix *m, int mode, const void *x, const void *keep, void *y, cudaStream_t s);
+// B2SR_BLOCKED=0 selects the row-major stream kernels (A/B measurements)
+bool blocked_enabled();
 
 // scan.cu
 // out[i] = sum_{j<i} in[j] for i in [0, n]; out has n+1 entries (out[n] = total).

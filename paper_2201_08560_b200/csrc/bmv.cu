@@ -440,6 +440,7 @@ int64_t prescale(const b2sr_matrix *m, const double *x, const double *scale, dou
 
 // ------------------------------------------------------------ launchers
 void launch_bbb(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaStream_t s) {
+    if (blocked_enabled() && launch_blocked(m, 0, x, keep, y, s)) return;
     ensure_items(m, s);
     if (m->any_split) CK(cudaMemsetAsync(y, 0, padded_vec_bytes(m->ntr, m->dim), s));
     unsigned g = item_grid(m);

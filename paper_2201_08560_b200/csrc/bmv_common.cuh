@@ -1,0 +1,68 @@
+// Shared device helpers of the bin-SpMV family (bmv.cu, bmv_blocked.cu, drivers.cu).
+#pragma once
+
+#include "b2sr_internal.cuh"
+
+namespace b2sr {
+
+// Lane geometry of a 128-bit load over tiles of width D.
+template <int D> struct Geo {
+    static constexpr int WB = D == 32 ? 4 : (D == 16 ? 2 : 1);
+    static constexpr int TB = D * WB;                    // tile bytes
+    static constexpr int TPL = TB >= 16 ? 1 : 16 / TB;   // tiles per lane load
+    static constexpr int LPT = TB >= 16 ? TB / 16 : 1;   // lanes per tile
+    static constexpr int TPW = 32 * TPL / LPT;           // tiles per warp load
+    static constexpr uint32_t CHUNK = 64 * TPW;          // tiles per work item
+};
+
+// d=4: bit r set when byte r of v is non-zero (bytes carry a low nibble only)
+__device__ __forceinline__ uint32_t nz_nibble_bytes(uint32_t v) {
+    v = (v | (v >> 1) | (v >> 2) | (v >> 3)) & 0x01010101u;
+    return (v * 0x10204080u) >> 28;
+}
+// full-byte variant (d=8 rows)
+__device__ __forceinline__ uint32_t nz_bytes(uint32_t v) {
+    v = (v | (v >> 4)) & 0x0F0F0F0Fu;
+    v = (v | (v >> 2)) & 0x03030303u;
+    v = (v | (v >> 1)) & 0x01010101u;
+    return (v * 0x10204080u) >> 28;
+}
+// per-byte popcounts packed in the bytes of a u32
+__device__ __forceinline__ uint32_t popc_bytes(uint32_t v) {
+    v = v - ((v >> 1) & 0x55555555u);
+    v = (v & 0x33333333u) + ((v >> 2) & 0x33333333u);
+    return (v + (v >> 4)) & 0x0F0F0F0Fu;
+}
+
+// Hit bits (positions within the tile-row word) of the 16 bytes a lane holds.
+// xw[j] = x word of the j-th tile in the lane (0 for tiles outside the range).
+template <int D>
+__device__ __forceinline__ uint32_t hits16(uint4 v, const uint32_t *xw, uint32_t lane) {
+    if constexpr (D == 4) {
+        return nz_nibble_bytes(v.x & (xw[0] * 0x01010101u)) | nz_nibble_bytes(v.y & (xw[1] * 0x01010101u)) |
+               nz_nibble_bytes(v.z & (xw[2] * 0x01010101u)) | nz_nibble_bytes(v.w & (xw[3] * 0x01010101u));
+    } else if constexpr (D == 8) {
+        uint32_t x0 = xw[0] * 0x01010101u, x1 = xw[1] * 0x01010101u;
+        uint32_t lo = nz_bytes(v.x & x0) | nz_bytes(v.z & x1);
+        uint32_t hi = nz_bytes(v.y & x0) | nz_bytes(v.w & x1);
+        return lo | (hi << 4);
+    } else if constexpr (D == 16) {
+        uint32_t xr = xw[0] | (xw[0] << 16), w[4] = {v.x, v.y, v.z, v.w}, a = 0;
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            uint32_t y = w[i] & xr;
+            a |= ((y & 0xFFFFu) ? 1u : 0u) << (2 * i);
+            a |= ((y >> 16) ? 1u : 0u) << (2 * i + 1);
+        }
+        return a << (8 * (lane & 1));
+    } else {
+        uint32_t x = xw[0], a = 0;
+        a |= (v.x & x) ? 1u : 0u;
+        a |= (v.y & x) ? 2u : 0u;
+        a |= (v.z & x) ? 4u : 0u;
+        a |= (v.w & x) ? 8u : 0u;
+        return a << (4 * (lane & 7));
+    }
+}
+
+}  // namespace b2sr

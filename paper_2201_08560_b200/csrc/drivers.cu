@@ -329,8 +329,9 @@ void ensure_live(b2sr_matrix *m, cudaStream_t s) {
 }
 
 void bfs_sweep(b2sr_matrix *at, const void *frontier, const void *visited, void *next, cudaStream_t s) {
-    ensure_items(at, s);
     ensure_live(at, s);
+    if (blocked_enabled() && launch_blocked(at, 1, frontier, visited, next, s)) return;
+    ensure_items(at, s);
     CK(cudaMemsetAsync(next, 0, padded_vec_bytes(at->ntr, at->dim), s));
     uint64_t blocks = ((uint64_t)at->n_items + 7) / 8, cap = (uint64_t)num_sms() * 16;
     unsigned g = (unsigned)std::min(blocks, cap);

@@ -61,3 +61,25 @@ def test_scale20_properties():
         fin = np.isfinite(a) | np.isfinite(bb)
         assert np.all(np.isfinite(a[fin]) & np.isfinite(bb[fin]))
         assert np.abs(a[fin] - bb[fin]).max() <= 1 and lv[src] == 0
+
+
+@pytest.mark.parametrize("d", [4, 32])
+def test_scale21_blocked_path_against_oracle(d):
+    """n = 2^21 > one shared-memory strip: exercises the column-strip blocked
+    bbb and BFS-pull kernels (P = 2 strips) against the C oracle."""
+    scale = 21
+    n = 1 << scale
+    csr = rmat.rmat_csr(scale, 8, seed=2)
+    rp, ci = csr.row_ptr, csr.col_ind
+    m = b2.csr_to_b2sr(csr, d)
+    ref = (n, d, m.tile_row_ptr, m.tile_col_ind, m.bit_tiles)
+    rng = np.random.default_rng(21)
+    xb = rng.random(n) < 0.5
+    keep = rng.random(n) < 0.5
+    xw, kw = orc.pack_bits(xb, d), orc.pack_bits(keep, d)
+    got = b2.bmv_bin_bin_bin_masked(m, b2.BitVector.from_bools(xb, d), b2.BitVector.from_bools(keep, d))
+    assert np.array_equal(got.words, orc.bmv_bbb(ref, xw, kw))
+    src = int(np.argmax(np.diff(rp.astype(np.int64))))
+    lv, it = orc.bfs(ref, src)
+    r = b2.bfs(m, src)
+    assert r.per_vertex.tobytes() == lv.tobytes() and r.iterations == it
