@@ -164,6 +164,64 @@ BlockedPlan *ensure_plan(b2sr_matrix *m, cudaStream_t s) {
 // ------------------------------------------------------------ kernel
 template <int D> struct GroupSize { static constexpr int GS = D <= 8 ? 8 : (D == 16 ? 16 : 32); };
 
+constexpr uint32_t MAX_LONG = 256;
+
+// keep word of a row; false when the row needs no work
+template <int D, int MODE>
+__device__ __forceinline__ bool row_keep(const void *keep, const void *live, uint32_t grow, uint32_t I,
+                                         uint32_t &keepw) {
+    if constexpr (MODE == 1) {
+        keepw = ~load_word<D>(keep, grow) & load_word<D>(live, I);
+        return keepw != 0;
+    } else {
+        keepw = keep ? load_word<D>(keep, grow) : 0xffffffffu;
+        return true;
+    }
+}
+
+// hit bits of one group step (TILES_STEP tiles starting at base) for this lane
+template <int D, int MODE>
+__device__ __forceinline__ uint32_t seg_step(const uint32_t *__restrict__ tci, const uint8_t *__restrict__ tiles,
+                                             const uint32_t *xs, uint32_t c0, uint32_t base, uint32_t s0, uint32_t s1,
+                                             uint32_t gl, uint32_t lane, uint32_t xmask) {
+    using G = Geo<D>;
+    uint32_t xw[G::TPL];
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if constexpr (G::TPL > 1) {
+        uint32_t tl = base + gl * G::TPL;
+        uint32_t anyx = 0;
+#pragma unroll
+        for (int j = 0; j < G::TPL; j++) xw[j] = 0;
+        if (tl < s1 && tl + G::TPL > s0) {
+            uint32_t cols[G::TPL];
+            if constexpr (G::TPL == 4) {
+                uint4 c = ld_stream128(tci + tl);
+                cols[0] = c.x; cols[1] = c.y; cols[2] = c.z; cols[3] = c.w;
+            } else {
+                uint2 c = *reinterpret_cast<const uint2 *>(tci + tl);
+                cols[0] = c.x; cols[1] = c.y;
+            }
+#pragma unroll
+            for (int j = 0; j < G::TPL; j++) {
+                bool ok = tl + j >= s0 && tl + j < s1;
+                uint32_t bit = (cols[j] - c0) * D;
+                xw[j] = ok ? (xs[bit >> 5] >> (bit & 31)) & xmask : 0u;
+                anyx |= xw[j];
+            }
+            if (MODE == 0 || anyx) v = ld_stream128(tiles + (size_t)tl * G::TB);
+        }
+    } else {
+        uint32_t t = base + gl / G::LPT, q = gl % G::LPT;
+        xw[0] = 0;
+        if (t < s1) {
+            uint32_t bit = (__ldg(tci + t) - c0) * D;
+            xw[0] = (xs[bit >> 5] >> (bit & 31)) & xmask;
+            if (MODE == 0 || xw[0]) v = ld_stream128(tiles + (size_t)t * G::TB + q * 16);
+        }
+    }
+    return hits16<D>(v, xw, lane);
+}
+
 // MODE 0: y = (A x) & keep (keep may be null); MODE 1: BFS pull,
 // next = (A frontier) & ~visited & live with payload skipping and early exit.
 template <int D, int MODE>
@@ -175,8 +233,10 @@ k_blocked(uint32_t P, uint32_t R, uint32_t nB, uint32_t sc, uint32_t ntr, uint32
     using G = Geo<D>;
     constexpr int GS = GroupSize<D>::GS;
     constexpr uint32_t TILES_STEP = GS * G::TPL / G::LPT;  // tiles per group step
+    constexpr uint32_t MIN_LONG = 4 * TILES_STEP;          // pass-2 threshold floor (tiles)
     extern __shared__ uint32_t xs[];                        // strip bits
-    __shared__ uint32_t s_unit;
+    __shared__ uint32_t s_unit, s_nlong, s_overflow;
+    __shared__ uint32_t s_long[MAX_LONG];
     const uint32_t lane = lane_id();
     const uint32_t gl = threadIdx.x % GS;                   // lane within group
     const uint32_t group = threadIdx.x / GS, ngroups = blockDim.x / GS;
@@ -185,7 +245,11 @@ k_blocked(uint32_t P, uint32_t R, uint32_t nB, uint32_t sc, uint32_t ntr, uint32
     const uint32_t xmask = D == 32 ? 0xffffffffu : ((1u << D) - 1u);
     uint32_t cur_p = 0xffffffffu;
     for (;;) {
-        if (threadIdx.x == 0) s_unit = atomicAdd(counter, 1u);
+        if (threadIdx.x == 0) {
+            s_unit = atomicAdd(counter, 1u);
+            s_nlong = 0;
+            s_overflow = 0;
+        }
         __syncthreads();
         uint32_t unit = s_unit;
         __syncthreads();
@@ -218,56 +282,27 @@ k_blocked(uint32_t P, uint32_t R, uint32_t nB, uint32_t sc, uint32_t ntr, uint32
         const uint32_t c0 = p * sc;
         const uint32_t *sg = seg + (size_t)p * (ntr + 1);
         const uint32_t r_end = min(ntr, (B + 1) * R);
+        // a row longer than one group's fair share of the unit goes to pass 2
+        const uint32_t LONG = max(MIN_LONG, (sg[r_end] - sg[B * R]) / ngroups);
+        // pass 1: a group per row segment; segments longer than LONG tiles are
+        // deferred to pass 2 so a hub row never serialises the CTA
         for (uint32_t I = B * R + group; I < r_end; I += ngroups) {
             uint32_t s0 = sg[I], s1 = sg[I + 1];
             if (s0 == s1) continue;
-            uint32_t grow = row0 + I;
-            uint32_t keepw;
-            if constexpr (MODE == 1) {
-                keepw = ~load_word<D>(keep, grow) & load_word<D>(live, I);
-                if (!keepw) continue;
-            } else {
-                keepw = keep ? load_word<D>(keep, grow) : 0xffffffffu;
+            if (s1 - s0 > LONG) {
+                if (gl == 0) {
+                    uint32_t k = atomicAdd(&s_nlong, 1u);
+                    if (k < MAX_LONG) s_long[k] = I;
+                    else s_overflow = 1;  // processed below by a slow path
+                }
+                continue;
             }
+            uint32_t keepw;
+            if (!row_keep<D, MODE>(keep, live, row0 + I, I, keepw)) continue;
             uint32_t acc = 0;
             uint32_t base = G::TPL > 1 ? (s0 & ~(uint32_t)(G::TPL - 1)) : s0;
             for (; base < s1; base += TILES_STEP) {
-                uint32_t xw[G::TPL];
-                uint4 v = make_uint4(0, 0, 0, 0);
-                if constexpr (G::TPL > 1) {
-                    uint32_t tl = base + gl * G::TPL;
-                    uint32_t anyx = 0;
-                    if (tl < s1 && tl + G::TPL > s0) {
-                        uint32_t cols[G::TPL];
-                        if constexpr (G::TPL == 4) {
-                            uint4 c = ld_stream128(tci + tl);
-                            cols[0] = c.x; cols[1] = c.y; cols[2] = c.z; cols[3] = c.w;
-                        } else {
-                            uint2 c = *reinterpret_cast<const uint2 *>(tci + tl);
-                            cols[0] = c.x; cols[1] = c.y;
-                        }
-#pragma unroll
-                        for (int j = 0; j < G::TPL; j++) {
-                            bool ok = tl + j >= s0 && tl + j < s1;
-                            uint32_t bit = (cols[j] - c0) * D;
-                            xw[j] = ok ? (xs[bit >> 5] >> (bit & 31)) & xmask : 0u;
-                            anyx |= xw[j];
-                        }
-                        if (MODE == 0 || anyx) v = ld_stream128(tiles + (size_t)tl * G::TB);
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < G::TPL; j++) xw[j] = 0;
-                    }
-                } else {
-                    uint32_t t = base + gl / G::LPT, q = gl % G::LPT;
-                    xw[0] = 0;
-                    if (t < s1) {
-                        uint32_t bit = (__ldg(tci + t) - c0) * D;
-                        xw[0] = (xs[bit >> 5] >> (bit & 31)) & xmask;
-                        if (MODE == 0 || xw[0]) v = ld_stream128(tiles + (size_t)t * G::TB + q * 16);
-                    }
-                }
-                acc |= hits16<D>(v, xw, lane);
+                acc |= seg_step<D, MODE>(tci, tiles, xs, c0, base, s0, s1, gl, lane, xmask);
                 if constexpr (MODE == 1) {
                     uint32_t all = acc;
 #pragma unroll
@@ -275,6 +310,33 @@ k_blocked(uint32_t P, uint32_t R, uint32_t nB, uint32_t sc, uint32_t ntr, uint32
                     if ((all & keepw) == keepw) { acc = all; break; }
                 }
             }
+#pragma unroll
+            for (int o = GS / 2; o; o >>= 1) acc |= __shfl_xor_sync(gmask, acc, o);
+            acc &= keepw;
+            if (gl == 0 && acc) atomic_or_word<D>(y, I, acc);
+        }
+        __syncthreads();
+        // pass 2: every group of the CTA takes interleaved steps of each long segment
+        uint32_t nlong = min(s_nlong, MAX_LONG);
+        bool overflow = s_overflow != 0;
+        for (uint32_t k = 0; k < nlong + (overflow ? r_end - B * R : 0); k++) {
+            uint32_t I;
+            if (k < nlong) {
+                I = s_long[k];
+            } else {  // overflow slow path: rescan the unit for long rows not in the list
+                I = B * R + (k - nlong);
+                uint32_t a0 = sg[I], a1 = sg[I + 1];
+                bool listed = false;
+                for (uint32_t q = 0; q < nlong; q++) listed |= s_long[q] == I;
+                if (a1 - a0 <= LONG || listed) continue;
+            }
+            uint32_t s0 = sg[I], s1 = sg[I + 1];
+            uint32_t keepw;
+            if (!row_keep<D, MODE>(keep, live, row0 + I, I, keepw)) continue;
+            uint32_t acc = 0;
+            uint32_t start = G::TPL > 1 ? (s0 & ~(uint32_t)(G::TPL - 1)) : s0;
+            for (uint32_t base = start + group * TILES_STEP; base < s1; base += ngroups * TILES_STEP)
+                acc |= seg_step<D, MODE>(tci, tiles, xs, c0, base, s0, s1, gl, lane, xmask);
 #pragma unroll
             for (int o = GS / 2; o; o >>= 1) acc |= __shfl_xor_sync(gmask, acc, o);
             acc &= keepw;

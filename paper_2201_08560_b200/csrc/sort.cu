@@ -38,6 +38,9 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__
                                                            size_t n, int sh, const uint64_t *__restrict__ offs,
                                                            uint32_t nblocks) {
     __shared__ uint32_t wc[RS_WARPS][256];
+    __shared__ uint32_t dbase[256];            // CTA-local start of each digit run
+    __shared__ K skey[RS_TILE];                // keys re-ordered by digit inside the CTA
+    __shared__ uint32_t sval[VALS ? RS_TILE : 1];
     const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
     for (int b = threadIdx.x; b < RS_WARPS * 256; b += RS_THREADS) (&wc[0][0])[b] = 0;
     __syncthreads();
@@ -62,7 +65,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__
         __syncwarp();
     }
     __syncthreads();
-    {  // exclusive prefix over warps, per digit
+    {  // exclusive prefix over warps per digit, then over digits (CTA-local run starts)
         uint32_t d = threadIdx.x, run = 0;
 #pragma unroll
         for (int ww = 0; ww < RS_WARPS; ww++) {
@@ -70,20 +73,41 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__
             wc[ww][d] = run;
             run += c;
         }
+        // block-wide exclusive scan of the 256 digit totals (one per thread)
+        uint32_t inc = run;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= (uint32_t)o) inc += y;
+        }
+        __shared__ uint32_t wsum[RS_WARPS];
+        if (lane == 31) wsum[w] = inc;
+        __syncthreads();
+        uint32_t off = 0;
+        for (uint32_t ww = 0; ww < w; ww++) off += wsum[ww];
+        dbase[d] = off + inc - run;
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < RS_ROUNDS; j++) {
+    for (int j = 0; j < RS_ROUNDS; j++) {  // stage in digit order inside the CTA
         size_t i = base + (size_t)j * 32 + lane;
         if (i < n) {
             uint32_t dg = (uint32_t)(key[j] >> sh) & 0xFFu;
-            size_t pos = offs[(size_t)dg * nblocks + blockIdx.x] + wc[w][dg] + rank[j];
-            kout[pos] = key[j];
-            if constexpr (VALS) vout[pos] = val[j];
+            uint32_t lp = dbase[dg] + wc[w][dg] + rank[j];
+            skey[lp] = key[j];
+            if constexpr (VALS) sval[lp] = val[j];
         }
     }
+    __syncthreads();
+    // consecutive threads write consecutive slots of each digit run: coalesced
+    uint32_t count = (uint32_t)min((size_t)RS_TILE, n - (size_t)blockIdx.x * RS_TILE);
+    for (uint32_t lp = threadIdx.x; lp < count; lp += RS_THREADS) {
+        K k = skey[lp];
+        uint32_t dg = (uint32_t)(k >> sh) & 0xFFu;
+        size_t pos = offs[(size_t)dg * nblocks + blockIdx.x] + (lp - dbase[dg]);
+        kout[pos] = k;
+        if constexpr (VALS) vout[pos] = sval[lp];
+    }
 }
-
 template <typename K, bool VALS>
 static void rs_passes(K *ka, uint32_t *va, K *kb, uint32_t *vb, size_t n, int bits, cudaStream_t s, K **kres,
                       uint32_t **vres) {
