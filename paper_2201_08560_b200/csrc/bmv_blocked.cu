@@ -1,39 +1,51 @@
 // Column-strip blocked bin-SpMV (bbb and the BFS pull sweep).
 //
-// Why: in the row-major B2SR stream every tile gathers its x word from L2 at
-// a random column -- one 32-byte sector per tile.  At d=4/8 that sector
-// traffic is 4x / 2.7x the tile bytes themselves and caps the streaming
-// kernel far below HBM bandwidth (profiles/r01_ncu_full_k_bmv_bbb4_v1.csv:
-// 5.4 GB L1 sector traffic for 1.03 GB of matrix).
+// Why: in the row-major B2SR stream every tile gathers its x word at a random
+// column.  ncu on k_bmv_bbb<4> at R-MAT s22 (profiles/r01_ncu_*): L1tex
+// throughput 71 % of peak, 167 M L1 sectors for a 1.03 GB matrix -- each
+// 32-lane gather costs 32 L1 wavefronts, which caps d=4/8 at ~2 TB/s no
+// matter how the tiles are streamed.  Shared memory serves the same random
+// gather in a few wavefronts.
 //
-// Plan (built once per matrix, cached on the handle): the tile columns are cut
-// into P strips whose x bits fit in shared memory (STRIP_VERTS vertices =
-// 128 KB of bits); the tiles of every tile row are re-laid strip-major --
-// strip p holds, row after row, the (still column-sorted) tiles of that row
-// falling in strip p -- so each (row, strip) segment is contiguous.  Tile
-// bytes are identical to the reference layout, only their order changes.
-//
-// Kernel: persistent CTAs (1024 threads, one per SM) pull (strip, row block)
-// work units from an atomic counter in strip-major order; a CTA stages the x
-// strip into shared memory only when its strip changes, then groups of GS
-// lanes walk row segments with 128-bit streaming loads and gather x from
-// shared memory.  A row's strips are OR-combined into y with one atomicOr per
-// (row, strip) -- OR is order-free, so the result is bit-identical.
+// Plan (built once per matrix, cached on the handle):
+//   * tile columns are cut into P strips of STRIP_VERTS vertices whose x
+//     bits (128 KB) fit in shared memory;
+//   * tiles are re-laid strip-major (strip p = every row's column-sorted
+//     tiles that fall in strip p, row after row) -- same bytes, new order;
+//   * per strip, a work-item list of (row, tile range) chunks of at most
+//     ITEM_STEPS group steps (hub rows split);
+//   * CTAs are assigned to strips in proportion to the strip's tiles.
+// Kernel: one 1024-thread CTA per SM stages its strip's x bits with a TMA
+// bulk copy (cp.async.bulk + mbarrier), then groups of GS lanes walk the
+// strip's items with 128-bit streaming loads and gather x from shared memory.
+// No CTA barrier after the staging.  Each item ORs its hits into y with one
+// atomicOr (OR is order-free: bit-identical to the reference).
+#include <vector>
+
 #include "bmv_common.cuh"
 
 namespace b2sr {
 
-constexpr uint32_t STRIP_VERTS = 1u << 20;               // vertices per strip
-constexpr uint32_t STRIP_SMEM = STRIP_VERTS / 8;         // 128 KB of x bits
+constexpr uint32_t STRIP_VERTS = 1u << 20;        // vertices per strip
+constexpr uint32_t STRIP_SMEM = STRIP_VERTS / 8;  // 128 KB of x bits
 constexpr uint32_t MAX_STRIPS = 16;
 constexpr int BLK_THREADS = 1024;
+constexpr uint32_t ITEM_STEPS = 8;                // group steps per work item
+
+template <int D> struct GroupSize { static constexpr int GS = D <= 8 ? 8 : (D == 16 ? 16 : 32); };
+template <int D> constexpr uint32_t tiles_step() {
+    return GroupSize<D>::GS * Geo<D>::TPL / Geo<D>::LPT;
+}
 
 struct BlockedPlan {
-    uint32_t P = 1, R = 1, nB = 1, strip_cols = 1;
-    uint32_t *seg = nullptr;   // P x (ntr+1) tile offsets (strip-major)
-    uint32_t *tci = nullptr;   // strip-major tile columns
-    void *tiles = nullptr;     // strip-major tiles
-    bool owns = false;         // false when P == 1 (arrays alias the matrix)
+    uint32_t P = 1, strip_cols = 1, n_items = 0, n_ctas = 0;
+    uint32_t *seg = nullptr;          // P x (ntr+1) tile offsets (strip-major)
+    uint32_t *tci = nullptr;          // strip-major tile columns
+    void *tiles = nullptr;            // strip-major tiles
+    uint4 *items = nullptr;           // (row, t0, t1, 0) per strip, strip-major
+    uint32_t *strip_items = nullptr;  // P+1 item offsets per strip (device)
+    uint32_t *strip_ctas = nullptr;   // P+1 CTA offsets per strip (device)
+    bool owns = false;                // false when P == 1 (tile arrays alias the matrix)
 };
 
 void free_plan(void *p) {
@@ -44,6 +56,9 @@ void free_plan(void *p) {
         dfree(bp->tiles, nullptr);
     }
     dfree(bp->seg, nullptr);
+    dfree(bp->items, nullptr);
+    dfree(bp->strip_items, nullptr);
+    dfree(bp->strip_ctas, nullptr);
     delete bp;
 }
 
@@ -112,21 +127,40 @@ __global__ void k_plan_copy(uint32_t ntr, uint32_t P, uint32_t sc, const uint32_
     }
 }
 
+// items per (strip, row): ceil(len / chunk), strip-major
+__global__ void k_plan_item_counts(uint32_t ntr, uint32_t P, uint32_t chunk, const uint32_t *seg, uint32_t *cnt) {
+    size_t total = (size_t)P * ntr;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        size_t p = i / ntr, I = i % ntr;
+        uint32_t len = seg[p * (ntr + 1) + I + 1] - seg[p * (ntr + 1) + I];
+        cnt[i] = (len + chunk - 1) / chunk;
+    }
+}
+
+__global__ void k_plan_item_fill(uint32_t ntr, uint32_t P, uint32_t chunk, const uint32_t *seg, const uint64_t *ofs,
+                                 uint4 *items) {
+    size_t total = (size_t)P * ntr;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        size_t p = i / ntr, I = i % ntr;
+        uint32_t s0 = seg[p * (ntr + 1) + I], s1 = seg[p * (ntr + 1) + I + 1];
+        uint64_t o = ofs[i];
+        for (uint32_t t = s0; t < s1; t += chunk) items[o++] = make_uint4((uint32_t)I, t, min(s1, t + chunk), 0);
+    }
+}
+
 BlockedPlan *ensure_plan(b2sr_matrix *m, cudaStream_t s) {
     if (m->plan) return static_cast<BlockedPlan *>(m->plan);
     uint32_t d = m->dim, ntr = m->ntr;
-    uint32_t ncols = tile_rows(m->n, d);        // global tile columns
-    uint32_t sc = STRIP_VERTS / d;              // tile columns per strip
+    uint32_t ncols = tile_rows(m->n, d);  // global tile columns
+    uint32_t sc = STRIP_VERTS / d;        // tile columns per strip
     uint32_t P = (ncols + sc - 1) / sc;
-    if (P > MAX_STRIPS) return nullptr;         // too many strips: the row-major kernel is used
+    if (P > MAX_STRIPS) return nullptr;   // too many strips: the row-major kernel is used
+    uint32_t chunk = ITEM_STEPS * (d == 4 ? tiles_step<4>() : d == 8 ? tiles_step<8>()
+                                   : d == 16 ? tiles_step<16>() : tiles_step<32>());
     BlockedPlan *bp = new BlockedPlan();
     try {
         bp->P = P;
         bp->strip_cols = sc;
-        uint64_t units = (uint64_t)num_sms() * 16;  // ~16 work units per SM
-        uint64_t rows_per = ((uint64_t)ntr * P + units - 1) / units;
-        bp->R = (uint32_t)std::max<uint64_t>(64, rows_per);
-        bp->nB = (ntr + bp->R - 1) / bp->R;
         bp->seg = static_cast<uint32_t *>(dalloc((size_t)P * (ntr + 1) * 4, s));
         if (P == 1) {
             CK(cudaMemcpyAsync(bp->seg, m->trp, ((size_t)ntr + 1) * 4, cudaMemcpyDeviceToDevice, s));
@@ -153,6 +187,40 @@ BlockedPlan *ensure_plan(b2sr_matrix *m, cudaStream_t s) {
                 default: LAUNCH(k_plan_copy<128>, g, 256, 0, s, ntr, P, sc, m->trp, m->tci, src, bp->seg, bp->tci, dst); break;
             }
         }
+        // work items per strip
+        Buf<uint32_t> icnt((size_t)P * ntr, s);
+        Buf<uint64_t> iofs((size_t)P * ntr + 1, s);
+        LAUNCH(k_plan_item_counts, grid_for((uint64_t)P * ntr), 256, 0, s, ntr, P, chunk, bp->seg, icnt.p);
+        exclusive_scan_u32_to_u64(icnt.p, iofs.p, (size_t)P * ntr, s);
+        std::vector<uint64_t> h_iofs(P + 1);
+        std::vector<uint32_t> h_seg_end(P);
+        for (uint32_t p = 0; p <= P; p++)
+            CK(cudaMemcpyAsync(&h_iofs[p], iofs.p + (size_t)p * ntr, 8, cudaMemcpyDeviceToHost, s));
+        for (uint32_t p = 0; p < P; p++)
+            CK(cudaMemcpyAsync(&h_seg_end[p], bp->seg + (size_t)p * (ntr + 1) + ntr, 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        bp->n_items = (uint32_t)h_iofs[P];
+        bp->items = static_cast<uint4 *>(dalloc((size_t)bp->n_items * 16 + 16, s));
+        LAUNCH(k_plan_item_fill, grid_for((uint64_t)P * ntr), 256, 0, s, ntr, P, chunk, bp->seg, iofs.p, bp->items);
+        // CTAs per strip in proportion to the strip's tiles (at least one each)
+        uint32_t G = (uint32_t)num_sms();
+        std::vector<uint32_t> h_items(P + 1), h_ctas(P + 1, 0);
+        uint64_t prev_end = 0, T = m->num_tiles ? m->num_tiles : 1, assigned = 0;
+        for (uint32_t p = 0; p < P; p++) {
+            uint64_t tiles_p = h_seg_end[p] - prev_end;
+            prev_end = h_seg_end[p];
+            h_items[p] = (uint32_t)h_iofs[p];
+            h_ctas[p] = (uint32_t)assigned;
+            assigned += std::max<uint64_t>(1, (tiles_p * G + T / 2) / T);
+        }
+        h_items[P] = (uint32_t)h_iofs[P];
+        h_ctas[P] = (uint32_t)assigned;
+        bp->n_ctas = (uint32_t)assigned;
+        bp->strip_items = static_cast<uint32_t *>(dalloc((P + 1) * 4, s));
+        bp->strip_ctas = static_cast<uint32_t *>(dalloc((P + 1) * 4, s));
+        CK(cudaMemcpyAsync(bp->strip_items, h_items.data(), (P + 1) * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(bp->strip_ctas, h_ctas.data(), (P + 1) * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));  // host vectors die here
     } catch (...) {
         free_plan(bp);
         throw;
@@ -161,35 +229,63 @@ BlockedPlan *ensure_plan(b2sr_matrix *m, cudaStream_t s) {
     return bp;
 }
 
-// ------------------------------------------------------------ kernel
-template <int D> struct GroupSize { static constexpr int GS = D <= 8 ? 8 : (D == 16 ? 16 : 32); };
-
-constexpr uint32_t MAX_LONG = 256;
-
-// keep word of a row; false when the row needs no work
-template <int D, int MODE>
-__device__ __forceinline__ bool row_keep(const void *keep, const void *live, uint32_t grow, uint32_t I,
-                                         uint32_t &keepw) {
-    if constexpr (MODE == 1) {
-        keepw = ~load_word<D>(keep, grow) & load_word<D>(live, I);
-        return keepw != 0;
-    } else {
-        keepw = keep ? load_word<D>(keep, grow) : 0xffffffffu;
-        return true;
+// ------------------------------------------------------------ x bit packing
+// d=4 BitVector words are bytes with a low nibble; pack 8 of them per u32 so
+// every width hands the kernel a plain little-endian bitset
+__global__ void k_pack_nibbles(uint32_t nwords, const uint8_t *__restrict__ x, uint32_t *__restrict__ bits) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nwords; i += gridDim.x * blockDim.x) {
+        uint2 v = reinterpret_cast<const uint2 *>(x)[i];
+        uint32_t o = 0;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            o |= ((v.x >> (8 * j)) & 0xFu) << (4 * j);
+            o |= ((v.y >> (8 * j)) & 0xFu) << (16 + 4 * j);
+        }
+        bits[i] = o;
     }
 }
 
-// hit bits of one group step (TILES_STEP tiles starting at base) for this lane
+// ------------------------------------------------------------ TMA staging
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// Bulk-copy `bytes` (multiple of 16) from global to shared memory with the
+// TMA bulk path; completion is tracked by an mbarrier (transaction bytes).
+__device__ __forceinline__ void tma_stage(void *dst, const void *src, uint32_t bytes, uint64_t *mbar) {
+    uint32_t mb = smem_addr(mbar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+        const uint32_t CH = 32768;
+        for (uint32_t off = 0; off < bytes; off += CH) {
+            uint32_t len = min(CH, bytes - off);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr((char *)dst + off)),
+                "l"((const char *)src + off), "r"(len), "r"(mb)
+                : "memory");
+        }
+    }
+    __syncthreads();  // the barrier is initialised before anyone waits on it
+    asm volatile(
+        "{\n .reg .pred P1;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n @!P1 bra WAIT_%=;\n}" ::"r"(
+            mb)
+        : "memory");
+}
+
+// ------------------------------------------------------------ kernel
 template <int D, int MODE>
 __device__ __forceinline__ uint32_t seg_step(const uint32_t *__restrict__ tci, const uint8_t *__restrict__ tiles,
                                              const uint32_t *xs, uint32_t c0, uint32_t base, uint32_t s0, uint32_t s1,
-                                             uint32_t gl, uint32_t lane, uint32_t xmask) {
+                                             uint32_t gl, uint32_t lane) {
     using G = Geo<D>;
+    constexpr uint32_t xmask = D == 32 ? 0xffffffffu : ((1u << D) - 1u);
     uint32_t xw[G::TPL];
     uint4 v = make_uint4(0, 0, 0, 0);
     if constexpr (G::TPL > 1) {
         uint32_t tl = base + gl * G::TPL;
-        uint32_t anyx = 0;
 #pragma unroll
         for (int j = 0; j < G::TPL; j++) xw[j] = 0;
         if (tl < s1 && tl + G::TPL > s0) {
@@ -201,6 +297,8 @@ __device__ __forceinline__ uint32_t seg_step(const uint32_t *__restrict__ tci, c
                 uint2 c = *reinterpret_cast<const uint2 *>(tci + tl);
                 cols[0] = c.x; cols[1] = c.y;
             }
+            uint32_t anyx = 0;
+            if (MODE == 0) v = ld_stream128(tiles + (size_t)tl * G::TB);
 #pragma unroll
             for (int j = 0; j < G::TPL; j++) {
                 bool ok = tl + j >= s0 && tl + j < s1;
@@ -208,140 +306,76 @@ __device__ __forceinline__ uint32_t seg_step(const uint32_t *__restrict__ tci, c
                 xw[j] = ok ? (xs[bit >> 5] >> (bit & 31)) & xmask : 0u;
                 anyx |= xw[j];
             }
-            if (MODE == 0 || anyx) v = ld_stream128(tiles + (size_t)tl * G::TB);
+            if (MODE == 1 && anyx) v = ld_stream128(tiles + (size_t)tl * G::TB);
         }
     } else {
         uint32_t t = base + gl / G::LPT, q = gl % G::LPT;
         xw[0] = 0;
         if (t < s1) {
+            if (MODE == 0) v = ld_stream128(tiles + (size_t)t * G::TB + q * 16);
             uint32_t bit = (__ldg(tci + t) - c0) * D;
             xw[0] = (xs[bit >> 5] >> (bit & 31)) & xmask;
-            if (MODE == 0 || xw[0]) v = ld_stream128(tiles + (size_t)t * G::TB + q * 16);
+            if (MODE == 1 && xw[0]) v = ld_stream128(tiles + (size_t)t * G::TB + q * 16);
         }
     }
     return hits16<D>(v, xw, lane);
 }
 
-// MODE 0: y = (A x) & keep (keep may be null); MODE 1: BFS pull,
-// next = (A frontier) & ~visited & live with payload skipping and early exit.
+// MODE 0: y = (A x) & keep (keep may be null);  MODE 1: BFS pull,
+// next = (A frontier) & ~visited & live, payload skipping + early exit.
+// xbits is the little-endian bitset of x (vertex v = bit v).
 template <int D, int MODE>
 __global__ void __launch_bounds__(BLK_THREADS, 1)
-k_blocked(uint32_t P, uint32_t R, uint32_t nB, uint32_t sc, uint32_t ntr, uint32_t ncols, uint32_t row0,
-          const uint32_t *__restrict__ seg, const uint32_t *__restrict__ tci, const uint8_t *__restrict__ tiles,
-          const void *__restrict__ x, const void *__restrict__ keep, const void *__restrict__ live,
-          void *__restrict__ y, uint32_t *__restrict__ counter) {
-    using G = Geo<D>;
+k_blocked(uint32_t P, uint32_t sc, uint32_t nbits_bytes, uint32_t row0, const uint4 *__restrict__ items,
+          const uint32_t *__restrict__ strip_items, const uint32_t *__restrict__ strip_ctas,
+          const uint32_t *__restrict__ tci, const uint8_t *__restrict__ tiles, const uint8_t *__restrict__ xbits,
+          const void *__restrict__ keep, const void *__restrict__ live, void *__restrict__ y) {
     constexpr int GS = GroupSize<D>::GS;
-    constexpr uint32_t TILES_STEP = GS * G::TPL / G::LPT;  // tiles per group step
-    constexpr uint32_t MIN_LONG = 4 * TILES_STEP;          // pass-2 threshold floor (tiles)
-    extern __shared__ uint32_t xs[];                        // strip bits
-    __shared__ uint32_t s_unit, s_nlong, s_overflow;
-    __shared__ uint32_t s_long[MAX_LONG];
+    constexpr uint32_t TILES_STEP = tiles_step<D>();
+    extern __shared__ __align__(128) uint32_t xs[];
+    __shared__ __align__(8) uint64_t mbar;
     const uint32_t lane = lane_id();
-    const uint32_t gl = threadIdx.x % GS;                   // lane within group
-    const uint32_t group = threadIdx.x / GS, ngroups = blockDim.x / GS;
+    const uint32_t gl = threadIdx.x % GS;
     const uint32_t gmask = GS == 32 ? 0xffffffffu : (((1u << GS) - 1u) << (lane & ~(GS - 1u)));
-    const uint32_t nunits = P * nB;
-    const uint32_t xmask = D == 32 ? 0xffffffffu : ((1u << D) - 1u);
-    uint32_t cur_p = 0xffffffffu;
-    for (;;) {
-        if (threadIdx.x == 0) {
-            s_unit = atomicAdd(counter, 1u);
-            s_nlong = 0;
-            s_overflow = 0;
+    // this CTA's strip
+    uint32_t p = 0;
+    while (p + 1 < P && strip_ctas[p + 1] <= blockIdx.x) p++;
+    const uint32_t lcta = blockIdx.x - strip_ctas[p], ncta = strip_ctas[p + 1] - strip_ctas[p];
+    // stage x bits of vertices [p*STRIP_VERTS, (p+1)*STRIP_VERTS)
+    uint32_t b0 = p * STRIP_SMEM;
+    uint32_t bytes = min(STRIP_SMEM, nbits_bytes - b0);
+    bytes = (bytes + 15) & ~15u;
+    tma_stage(xs, xbits + b0, bytes, &mbar);
+    const uint32_t c0 = p * sc;
+    const uint32_t groups = ncta * (blockDim.x / GS);
+    const uint32_t gid = lcta * (blockDim.x / GS) + threadIdx.x / GS;
+    const uint32_t i1 = strip_items[p + 1];
+    for (uint32_t k = strip_items[p] + gid; k < i1; k += groups) {
+        uint4 it = items[k];
+        uint32_t I = it.x, s0 = it.y, s1 = it.z;
+        uint32_t grow = row0 + I;
+        uint32_t keepw;
+        if constexpr (MODE == 1) {
+            keepw = ~load_word<D>(keep, grow) & load_word<D>(live, I);
+            if (!keepw) continue;
+        } else {
+            keepw = keep ? load_word<D>(keep, grow) : 0xffffffffu;
         }
-        __syncthreads();
-        uint32_t unit = s_unit;
-        __syncthreads();
-        if (unit >= nunits) break;
-        uint32_t p = unit / nB, B = unit % nB;
-        if (p != cur_p) {  // stage x words of tile columns [p*sc, p*sc+sc) as packed bits
-            uint32_t c0 = p * sc, c1 = min(ncols, c0 + sc);
-            uint32_t nwords = ((c1 - c0) * D + 31) / 32;
-            for (uint32_t i = threadIdx.x; i < nwords; i += blockDim.x) {
-                uint32_t v = 0;
-                if constexpr (D == 4) {  // 8 nibble words -> one u32
+        uint32_t acc = 0;
+        uint32_t base = Geo<D>::TPL > 1 ? (s0 & ~(uint32_t)(Geo<D>::TPL - 1)) : s0;
+        for (; base < s1; base += TILES_STEP) {
+            acc |= seg_step<D, MODE>(tci, tiles, xs, c0, base, s0, s1, gl, lane);
+            if constexpr (MODE == 1) {
+                uint32_t all = acc;
 #pragma unroll
-                    for (int j = 0; j < 8; j++) {
-                        uint32_t c = c0 + i * 8 + j;
-                        if (c < c1) v |= (load_word<4>(x, c) & 0xFu) << (4 * j);
-                    }
-                } else {
-                    constexpr int PER = 32 / D;
-#pragma unroll
-                    for (int j = 0; j < PER; j++) {
-                        uint32_t c = c0 + i * PER + j;
-                        if (c < c1) v |= load_word<D>(x, c) << (D * j);
-                    }
-                }
-                xs[i] = v;
+                for (int o = GS / 2; o; o >>= 1) all |= __shfl_xor_sync(gmask, all, o);
+                if ((all & keepw) == keepw) { acc = all; break; }
             }
-            cur_p = p;
-            __syncthreads();
         }
-        const uint32_t c0 = p * sc;
-        const uint32_t *sg = seg + (size_t)p * (ntr + 1);
-        const uint32_t r_end = min(ntr, (B + 1) * R);
-        // a row longer than one group's fair share of the unit goes to pass 2
-        const uint32_t LONG = max(MIN_LONG, (sg[r_end] - sg[B * R]) / ngroups);
-        // pass 1: a group per row segment; segments longer than LONG tiles are
-        // deferred to pass 2 so a hub row never serialises the CTA
-        for (uint32_t I = B * R + group; I < r_end; I += ngroups) {
-            uint32_t s0 = sg[I], s1 = sg[I + 1];
-            if (s0 == s1) continue;
-            if (s1 - s0 > LONG) {
-                if (gl == 0) {
-                    uint32_t k = atomicAdd(&s_nlong, 1u);
-                    if (k < MAX_LONG) s_long[k] = I;
-                    else s_overflow = 1;  // processed below by a slow path
-                }
-                continue;
-            }
-            uint32_t keepw;
-            if (!row_keep<D, MODE>(keep, live, row0 + I, I, keepw)) continue;
-            uint32_t acc = 0;
-            uint32_t base = G::TPL > 1 ? (s0 & ~(uint32_t)(G::TPL - 1)) : s0;
-            for (; base < s1; base += TILES_STEP) {
-                acc |= seg_step<D, MODE>(tci, tiles, xs, c0, base, s0, s1, gl, lane, xmask);
-                if constexpr (MODE == 1) {
-                    uint32_t all = acc;
 #pragma unroll
-                    for (int o = GS / 2; o; o >>= 1) all |= __shfl_xor_sync(gmask, all, o);
-                    if ((all & keepw) == keepw) { acc = all; break; }
-                }
-            }
-#pragma unroll
-            for (int o = GS / 2; o; o >>= 1) acc |= __shfl_xor_sync(gmask, acc, o);
-            acc &= keepw;
-            if (gl == 0 && acc) atomic_or_word<D>(y, I, acc);
-        }
-        __syncthreads();
-        // pass 2: every group of the CTA takes interleaved steps of each long segment
-        uint32_t nlong = min(s_nlong, MAX_LONG);
-        bool overflow = s_overflow != 0;
-        for (uint32_t k = 0; k < nlong + (overflow ? r_end - B * R : 0); k++) {
-            uint32_t I;
-            if (k < nlong) {
-                I = s_long[k];
-            } else {  // overflow slow path: rescan the unit for long rows not in the list
-                I = B * R + (k - nlong);
-                uint32_t a0 = sg[I], a1 = sg[I + 1];
-                bool listed = false;
-                for (uint32_t q = 0; q < nlong; q++) listed |= s_long[q] == I;
-                if (a1 - a0 <= LONG || listed) continue;
-            }
-            uint32_t s0 = sg[I], s1 = sg[I + 1];
-            uint32_t keepw;
-            if (!row_keep<D, MODE>(keep, live, row0 + I, I, keepw)) continue;
-            uint32_t acc = 0;
-            uint32_t start = G::TPL > 1 ? (s0 & ~(uint32_t)(G::TPL - 1)) : s0;
-            for (uint32_t base = start + group * TILES_STEP; base < s1; base += ngroups * TILES_STEP)
-                acc |= seg_step<D, MODE>(tci, tiles, xs, c0, base, s0, s1, gl, lane, xmask);
-#pragma unroll
-            for (int o = GS / 2; o; o >>= 1) acc |= __shfl_xor_sync(gmask, acc, o);
-            acc &= keepw;
-            if (gl == 0 && acc) atomic_or_word<D>(y, I, acc);
-        }
+        for (int o = GS / 2; o; o >>= 1) acc |= __shfl_xor_sync(gmask, acc, o);
+        acc &= keepw;
+        if (gl == 0 && acc) atomic_or_word<D>(y, I, acc);
     }
 }
 
@@ -359,23 +393,32 @@ bool launch_blocked(b2sr_matrix *m, int mode, const void *x, const void *keep, v
     BlockedPlan *bp = ensure_plan(m, s);
     if (!bp) return false;
     CK(cudaMemsetAsync(y, 0, padded_vec_bytes(m->ntr, m->dim), s));
-    Buf<uint32_t> counter(1, s);
-    CK(cudaMemsetAsync(counter.p, 0, 4, s));
     uint32_t ncols = tile_rows(m->n, m->dim);
+    uint32_t nbits_bytes = (uint32_t)(((uint64_t)ncols * m->dim + 7) / 8);
+    const uint8_t *xbits = (const uint8_t *)x;
+    Buf<uint32_t> packed;
+    if (m->dim == 4) {  // nibble words -> bitset
+        uint32_t nwords = (ncols + 7) / 8;
+        packed = Buf<uint32_t>(nwords + 4, s);
+        LAUNCH(k_pack_nibbles, grid_for(nwords), 256, 0, s, nwords, (const uint8_t *)x, packed.p);
+        xbits = (const uint8_t *)packed.p;
+    }
+    unsigned g = bp->n_ctas;
     size_t smem = STRIP_SMEM;
-    unsigned g = (unsigned)num_sms();
     const uint8_t *tl = (const uint8_t *)bp->tiles;
-#define BLK_CASE(DD)                                                                                               \
-    case DD:                                                                                                       \
-        if (mode == 0) {                                                                                           \
-            CK(cudaFuncSetAttribute(k_blocked<DD, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));   \
-            LAUNCH((k_blocked<DD, 0>), g, BLK_THREADS, smem, s, bp->P, bp->R, bp->nB, bp->strip_cols, m->ntr,      \
-                   ncols, m->row0, bp->seg, bp->tci, tl, x, keep, (const void *)nullptr, y, counter.p);            \
-        } else {                                                                                                   \
-            CK(cudaFuncSetAttribute(k_blocked<DD, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));   \
-            LAUNCH((k_blocked<DD, 1>), g, BLK_THREADS, smem, s, bp->P, bp->R, bp->nB, bp->strip_cols, m->ntr,      \
-                   ncols, m->row0, bp->seg, bp->tci, tl, x, keep, (const void *)m->live, y, counter.p);            \
-        }                                                                                                          \
+#define BLK_CASE(DD)                                                                                             \
+    case DD:                                                                                                     \
+        if (mode == 0) {                                                                                         \
+            CK(cudaFuncSetAttribute(k_blocked<DD, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+            LAUNCH((k_blocked<DD, 0>), g, BLK_THREADS, smem, s, bp->P, bp->strip_cols, nbits_bytes, m->row0,     \
+                   bp->items, bp->strip_items, bp->strip_ctas, bp->tci, tl, xbits, keep, (const void *)nullptr,  \
+                   y);                                                                                           \
+        } else {                                                                                                 \
+            CK(cudaFuncSetAttribute(k_blocked<DD, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+            LAUNCH((k_blocked<DD, 1>), g, BLK_THREADS, smem, s, bp->P, bp->strip_cols, nbits_bytes, m->row0,     \
+                   bp->items, bp->strip_items, bp->strip_ctas, bp->tci, tl, xbits, keep,                         \
+                   (const void *)m->live, y);                                                                    \
+        }                                                                                                        \
         break;
     switch (m->dim) {
         BLK_CASE(4)
