@@ -154,7 +154,7 @@ void launch_row_ids(const b2sr_matrix *m, uint32_t *rowid, cudaStream_t s);  // 
 void free_plan(void *plan);
 // blocked bin-SpMV: mode 0 = masked bbb, 1 = BFS pull; false if not applicable
 bool launch_blocked(b2sr_matrix *m, int mode, const void *x, const void *keep, void *y, cudaStream_t s);
-// B2SR_BLOCKED=0 selects the row-major stream kernels (A/B measurements)
+// B2SR_BLOCKED=1 selects the column-strip blocked kernels (A/B measurements)
 bool blocked_enabled();
 
 // scan.cu

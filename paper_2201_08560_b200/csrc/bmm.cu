@@ -136,19 +136,118 @@ __global__ void __launch_bounds__(256) k_bmm_masked(uint64_t TM, const uint32_t 
     if (lane == 0 && acc) atomicAdd(out, acc);
 }
 
+// ------------------------------------------------------------ chunked items
+// A mask tile whose two tile rows are both long (hub x hub) would pin one
+// warp for milliseconds; split every mask tile into chunks of TC_CHUNK
+// entries of its shorter tile row so such pairs spread over many warps.
+constexpr uint32_t TC_CHUNK = 256;
+
+__global__ void k_tc_item_counts(uint64_t TM, const uint32_t *__restrict__ m_rowid, const uint32_t *__restrict__ m_tci,
+                                 uint32_t m_row0, const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ b_trp,
+                                 uint32_t *__restrict__ cnt) {
+    for (uint64_t mt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; mt < TM; mt += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t I = m_rowid[mt] + m_row0, J = m_tci[mt];
+        uint32_t la = a_trp[I + 1] - a_trp[I], lb = b_trp[J + 1] - b_trp[J];
+        uint32_t sh = min(la, lb);
+        cnt[mt] = la && lb ? (sh + TC_CHUNK - 1) / TC_CHUNK : 0;
+    }
+}
+
+__global__ void k_tc_item_fill(uint64_t TM, const uint32_t *__restrict__ cnt, const uint64_t *__restrict__ ofs,
+                               uint2 *__restrict__ items) {
+    for (uint64_t mt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; mt < TM; mt += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t o = ofs[mt];
+        for (uint32_t j = 0; j < cnt[mt]; j++) items[o + j] = make_uint2((uint32_t)mt, j);
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_bmm_masked_items(uint64_t n_items, const uint2 *__restrict__ items,
+                                                          const uint32_t *__restrict__ m_rowid,
+                                                          const uint32_t *__restrict__ m_tci,
+                                                          const typename WordT<D>::T *__restrict__ m_tiles,
+                                                          const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ a_tci,
+                                                          const typename WordT<D>::T *__restrict__ a_tiles,
+                                                          const uint32_t *__restrict__ b_trp, const uint32_t *__restrict__ b_tci,
+                                                          const typename WordT<D>::T *__restrict__ b_tiles,
+                                                          uint32_t m_row0, unsigned long long *__restrict__ out) {
+    const uint32_t lane = lane_id();
+    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long acc = 0;
+    for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_items; w += warps) {
+        uint2 it = items[w];
+        uint64_t mt = it.x;
+        uint32_t I = m_rowid[mt] + m_row0, J = m_tci[mt];
+        uint32_t mword = lane < (uint32_t)D ? (uint32_t)m_tiles[mt * D + lane] : 0u;
+        uint32_t rows_used = __ballot_sync(0xffffffffu, mword != 0);
+        uint32_t a0 = a_trp[I], a1 = a_trp[I + 1], b0 = b_trp[J], b1 = b_trp[J + 1];
+        bool a_short = (a1 - a0) <= (b1 - b0);
+        uint32_t s0 = a_short ? a0 : b0, s1 = a_short ? a1 : b1;
+        uint32_t l0 = a_short ? b0 : a0, l1 = a_short ? b1 : a1;
+        const uint32_t *stci = a_short ? a_tci : b_tci;
+        const uint32_t *ltci = a_short ? b_tci : a_tci;
+        uint32_t c0 = s0 + it.y * TC_CHUNK, c1 = min(s1, c0 + TC_CHUNK);
+        // narrow the long row to the chunk's value range once per warp
+        uint32_t first = __ldg(stci + c0), last = __ldg(stci + c1 - 1);
+        uint32_t lo = lower_bound_u32(ltci, l0, l1, first);
+        uint32_t hi = lower_bound_u32(ltci, lo, l1, last + 1);
+        if (lo == hi || rows_used == 0) continue;
+        for (uint32_t base = c0; base < c1; base += 32) {
+            uint32_t si = base + lane;
+            uint32_t ta = 0, tb = 0;
+            bool hit = false;
+            if (si < c1) {
+                uint32_t K = __ldg(stci + si);
+                uint32_t li = lower_bound_u32(ltci, lo, hi, K);
+                if (li < hi && __ldg(ltci + li) == K) {
+                    hit = true;
+                    ta = a_short ? si : li;
+                    tb = a_short ? li : si;
+                }
+            }
+            if (!__ballot_sync(0xffffffffu, hit)) continue;
+            uint32_t ru = rows_used;
+            while (ru) {  // warp-uniform loop over non-empty mask rows
+                int r = __ffs(ru) - 1;
+                ru &= ru - 1;
+                uint32_t mw = __shfl_sync(0xffffffffu, mword, r);
+                if (hit) {
+                    uint32_t aw = a_tiles[(size_t)ta * D + r];
+                    while (aw && mw) {
+                        int c = __ffs(mw) - 1;
+                        mw &= mw - 1;
+                        acc += __popc(aw & (uint32_t)b_tiles[(size_t)tb * D + c]);
+                    }
+                }
+            }
+        }
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0 && acc) atomicAdd(out, acc);
+}
+
 int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_matrix *mask, cudaStream_t s) {
     if (!mask->num_tiles || !a->num_tiles || !bt->num_tiles) return 0;
-    Buf<uint32_t> rowid(mask->num_tiles, s);
+    uint64_t TM = mask->num_tiles;
+    Buf<uint32_t> rowid(TM, s), cnt(TM, s);
+    Buf<uint64_t> ofs(TM + 1, s);
     row_ids(mask, rowid.p, s);
+    LAUNCH(k_tc_item_counts, grid_for(TM), 256, 0, s, TM, rowid.p, mask->tci, mask->row0, a->trp, bt->trp, cnt.p);
+    exclusive_scan_u32_to_u64(cnt.p, ofs.p, TM, s);
+    uint64_t n_items = read_scalar(ofs.p + TM, s);
     Buf<unsigned long long> out(1, s);
     CK(cudaMemsetAsync(out.p, 0, 8, s));
-    uint64_t blocks = (mask->num_tiles + 7) / 8, cap = (uint64_t)num_sms() * 16;
+    if (!n_items) return 0;
+    Buf<uint2> items(n_items, s);
+    LAUNCH(k_tc_item_fill, grid_for(TM), 256, 0, s, TM, cnt.p, ofs.p, items.p);
+    uint64_t blocks = (n_items + 7) / 8, cap = (uint64_t)num_sms() * 16;
     unsigned g = (unsigned)std::min(blocks, cap);
     switch (a->dim) {
-#define BMM_CASE(DD, W)                                                                                          \
-    case DD:                                                                                                     \
-        LAUNCH(k_bmm_masked<DD>, g, 256, 0, s, mask->num_tiles, rowid.p, mask->tci, (const W *)mask->tiles,     \
-               a->trp, a->tci, (const W *)a->tiles, bt->trp, bt->tci, (const W *)bt->tiles, mask->row0, out.p);            \
+#define BMM_CASE(DD, W)                                                                                        \
+    case DD:                                                                                                   \
+        LAUNCH(k_bmm_masked_items<DD>, g, 256, 0, s, n_items, items.p, rowid.p, mask->tci,                    \
+               (const W *)mask->tiles, a->trp, a->tci, (const W *)a->tiles, bt->trp, bt->tci,                 \
+               (const W *)bt->tiles, mask->row0, out.p);                                                      \
         break;
         BMM_CASE(4, uint8_t)
         BMM_CASE(8, uint8_t)

@@ -83,3 +83,10 @@ def test_scale21_blocked_path_against_oracle(d):
     lv, it = orc.bfs(ref, src)
     r = b2.bfs(m, src)
     assert r.per_vertex.tobytes() == lv.tobytes() and r.iterations == it
+
+
+def test_scale21_blocked_kernels_opt_in(monkeypatch):
+    """The opt-in column-strip blocked kernels (B2SR_BLOCKED=1) give the same bits."""
+    monkeypatch.setenv("B2SR_BLOCKED", "1")
+    test_scale21_blocked_path_against_oracle(4)
+    test_scale21_blocked_path_against_oracle(16)
