@@ -138,6 +138,8 @@ struct b2sr_matrix {
     void *live = nullptr;
     // cached column-strip blocked layout for bin-SpMV (bmv_blocked.cu)
     void *plan = nullptr;
+    uint64_t live_tiles = 0;          // tiles in rows with a live bit (set with `live`)
+    uint32_t *item_ofs = nullptr;     // ntr+1: first work item of each tile row (with `items`)
 };
 
 namespace b2sr {

@@ -17,18 +17,9 @@
 // bit-identical to the reference.
 #include <cmath>
 
-#include "b2sr_internal.cuh"
+#include "bmv_common.cuh"
 
 namespace b2sr {
-
-template <int D> struct Geo {
-    static constexpr int WB = D == 32 ? 4 : (D == 16 ? 2 : 1);
-    static constexpr int TB = D * WB;                    // tile bytes
-    static constexpr int TPL = TB >= 16 ? 1 : 16 / TB;   // tiles per lane load
-    static constexpr int LPT = TB >= 16 ? TB / 16 : 1;   // lanes per tile
-    static constexpr int TPW = 32 * TPL / LPT;           // tiles per warp load
-    static constexpr uint32_t CHUNK = 64 * TPW;          // tiles per work item
-};
 
 // ------------------------------------------------------------ work items
 __global__ void k_item_counts(uint32_t ntr, const uint32_t *trp, uint32_t chunk, uint32_t *cnt) {
@@ -54,6 +45,11 @@ __global__ void k_item_fill(uint32_t ntr, const uint32_t *trp, uint32_t chunk, c
     }
 }
 
+__global__ void k_ofs_u32(uint32_t n, const uint64_t *in, uint32_t *out) {
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (uint32_t)in[i];
+}
+
 void ensure_items(b2sr_matrix *m, cudaStream_t s) {
     if (m->items) return;
     uint32_t chunk = m->dim == 4 ? Geo<4>::CHUNK : m->dim == 8 ? Geo<8>::CHUNK
@@ -68,35 +64,17 @@ void ensure_items(b2sr_matrix *m, cudaStream_t s) {
     CK(cudaMemsetAsync(split.p, 0, sizeof(int), s));
     LAUNCH(k_item_fill, (m->ntr + 255) / 256, 256, 0, s, m->ntr, m->trp, chunk, ofs.p, items.p, split.p);
     m->any_split = read_scalar(split.p, s) != 0;
+    Buf<uint32_t> item_ofs((size_t)m->ntr + 1, s);  // per-row first item (BFS active lists)
+    LAUNCH(k_ofs_u32, (m->ntr + 256) / 256, 256, 0, s, m->ntr + 1, ofs.p, item_ofs.p);
     m->n_items = (uint32_t)n_items;
     m->items = items.release();
+    m->item_ofs = item_ofs.release();
 }
 
 static unsigned item_grid(const b2sr_matrix *m) {
     uint64_t blocks = ((uint64_t)m->n_items + 7) / 8;  // 8 warps per 256-thread CTA
     uint64_t cap = (uint64_t)num_sms() * 16;
     return (unsigned)(blocks < cap ? blocks : cap);
-}
-
-// ------------------------------------------------------------ bit tricks
-// d=4: four tiles' worth of 4 row-nibbles in a u32; bit r of the result is
-// set when byte r of v is non-zero (bytes only carry a low nibble).
-__device__ __forceinline__ uint32_t nz_nibble_bytes(uint32_t v) {
-    v = (v | (v >> 1) | (v >> 2) | (v >> 3)) & 0x01010101u;
-    return (v * 0x10204080u) >> 28;
-}
-// full-byte variant (d=8 rows)
-__device__ __forceinline__ uint32_t nz_bytes(uint32_t v) {
-    v = (v | (v >> 4)) & 0x0F0F0F0Fu;
-    v = (v | (v >> 2)) & 0x03030303u;
-    v = (v | (v >> 1)) & 0x01010101u;
-    return (v * 0x10204080u) >> 28;
-}
-// per-byte popcounts packed in the bytes of a u32
-__device__ __forceinline__ uint32_t popc_bytes(uint32_t v) {
-    v = v - ((v >> 1) & 0x55555555u);
-    v = (v & 0x33333333u) + ((v >> 2) & 0x33333333u);
-    return (v + (v >> 4)) & 0x0F0F0F0Fu;
 }
 
 // ------------------------------------------------------------ one warp load
@@ -142,33 +120,7 @@ __device__ __forceinline__ void load_lane(const uint8_t *__restrict__ tiles, con
 // bbb: hit bits of the rows this lane covers (positions within the row word)
 template <int D>
 __device__ __forceinline__ uint32_t lane_hits(const LaneTiles<D> &lt, uint32_t lane) {
-    if constexpr (D == 4) {
-        uint32_t a = 0, w[4] = {lt.v.x, lt.v.y, lt.v.z, lt.v.w};
-#pragma unroll
-        for (int j = 0; j < 4; j++) a |= nz_nibble_bytes(w[j] & (lt.xw[j] * 0x01010101u));
-        return a;
-    } else if constexpr (D == 8) {
-        uint32_t x0 = lt.xw[0] * 0x01010101u, x1 = lt.xw[1] * 0x01010101u;
-        uint32_t lo = nz_bytes(lt.v.x & x0) | nz_bytes(lt.v.z & x1);
-        uint32_t hi = nz_bytes(lt.v.y & x0) | nz_bytes(lt.v.w & x1);
-        return lo | (hi << 4);
-    } else if constexpr (D == 16) {
-        uint32_t xr = lt.xw[0] | (lt.xw[0] << 16), w[4] = {lt.v.x, lt.v.y, lt.v.z, lt.v.w}, a = 0;
-#pragma unroll
-        for (int i = 0; i < 4; i++) {
-            uint32_t v = w[i] & xr;
-            a |= ((v & 0xFFFFu) ? 1u : 0u) << (2 * i);
-            a |= ((v >> 16) ? 1u : 0u) << (2 * i + 1);
-        }
-        return a << (8 * (lane & 1));
-    } else {
-        uint32_t x = lt.xw[0], a = 0;
-        a |= (lt.v.x & x) ? 1u : 0u;
-        a |= (lt.v.y & x) ? 2u : 0u;
-        a |= (lt.v.z & x) ? 4u : 0u;
-        a |= (lt.v.w & x) ? 8u : 0u;
-        return a << (4 * (lane & 7));
-    }
+    return hits16<D>(lt.v, lt.xw, lane);
 }
 
 // ------------------------------------------------------------ K4 bbb

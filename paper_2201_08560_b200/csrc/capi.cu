@@ -96,6 +96,7 @@ void free_matrix(b2sr_matrix *m) {
     dfree(m->tiles, nullptr);
     dfree(m->items, nullptr);
     dfree(m->live, nullptr);
+    dfree(m->item_ofs, nullptr);
     free_plan(m->plan);
     if (cur != m->device) cudaSetDevice(cur);
     delete m;

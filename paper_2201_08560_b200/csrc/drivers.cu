@@ -19,7 +19,7 @@
 #include <mutex>
 #include <vector>
 
-#include "b2sr_internal.cuh"
+#include "bmv_common.cuh"
 
 namespace b2sr {
 
@@ -33,24 +33,7 @@ static unsigned grid_for(uint64_t work) {
 }
 
 // ================================================================ BFS
-template <int D> struct BGeo {
-    static constexpr int WB = D == 32 ? 4 : (D == 16 ? 2 : 1);
-    static constexpr int TB = D * WB;
-    static constexpr int TPL = TB >= 16 ? 1 : 16 / TB;
-    static constexpr int LPT = TB >= 16 ? TB / 16 : 1;
-    static constexpr int TPW = 32 * TPL / LPT;
-};
-
-__device__ __forceinline__ uint32_t nz_nibble_bytes_b(uint32_t v) {
-    v = (v | (v >> 1) | (v >> 2) | (v >> 3)) & 0x01010101u;
-    return (v * 0x10204080u) >> 28;
-}
-__device__ __forceinline__ uint32_t nz_bytes_b(uint32_t v) {
-    v = (v | (v >> 4)) & 0x0F0F0F0Fu;
-    v = (v | (v >> 2)) & 0x03030303u;
-    v = (v | (v >> 1)) & 0x01010101u;
-    return (v * 0x10204080u) >> 28;
-}
+template <int D> using BGeo = Geo<D>;
 
 // hit bits (row-word positions) of the tiles this lane covers; the payload
 // is only fetched for tiles whose frontier word is non-zero
@@ -82,12 +65,12 @@ __device__ __forceinline__ uint32_t bfs_lane(const uint8_t *__restrict__ tiles, 
         if constexpr (D == 4) {
             uint32_t w[4] = {v.x, v.y, v.z, v.w}, a = 0;
 #pragma unroll
-            for (int j = 0; j < 4; j++) a |= nz_nibble_bytes_b(w[j] & (xw[j] * 0x01010101u));
+            for (int j = 0; j < 4; j++) a |= nz_nibble_bytes(w[j] & (xw[j] * 0x01010101u));
             return a;
         } else {
             uint32_t x0 = xw[0] * 0x01010101u, x1 = xw[1] * 0x01010101u;
-            uint32_t lo = nz_bytes_b(v.x & x0) | nz_bytes_b(v.z & x1);
-            uint32_t hi = nz_bytes_b(v.y & x0) | nz_bytes_b(v.w & x1);
+            uint32_t lo = nz_bytes(v.x & x0) | nz_bytes(v.z & x1);
+            uint32_t hi = nz_bytes(v.y & x0) | nz_bytes(v.w & x1);
             return lo | (hi << 4);
         }
     } else {
@@ -120,12 +103,14 @@ template <int D>
 __global__ void __launch_bounds__(256) k_bfs_pull(const WorkItem *__restrict__ items, uint32_t n_items, uint32_t n,
                                                   const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
                                                   const void *__restrict__ frontier, const void *__restrict__ visited,
-                                                  const void *__restrict__ live, void *__restrict__ next, uint32_t row0) {
+                                                  const void *__restrict__ live, void *__restrict__ next, uint32_t row0,
+                                                  const uint32_t *__restrict__ idx, const uint32_t *__restrict__ idx_n) {
     using G = BGeo<D>;
     const uint32_t lane = lane_id();
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    if (idx) n_items = *idx_n;  // active-item list of a late pull level
     for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_items; w += warps) {
-        WorkItem it = items[w];
+        WorkItem it = items[idx ? idx[w] : w];
         uint32_t grow = row0 + it.row;
         uint32_t keepw = ~load_word<D>(visited, grow) & load_word<D>(live, it.row);  // live is block-local
         if (!keepw) continue;
@@ -191,33 +176,44 @@ struct BfsCounters {
     int any;
     uint32_t list_n;                     // push work entries
     unsigned long long frontier_tiles;   // tiles of a in frontier tile rows
-    unsigned long long unvisited_tiles;  // tiles of at in tile rows with keep != 0
+    unsigned long long removed_tiles;    // tiles of at rows whose keep word became zero
     unsigned long long frontier_vertices;
 };
 
-// visited |= next; levels[new] = level; counters; push work list for the next level
+// visited |= next; levels[new] = level; counters; push work list for the next
+// level.  Each thread owns 16 bytes of `next` (16/16/8/4 words); all-zero
+// chunks cost one vector load, so the kernel scales with the frontier, not n.
+// Unvisited tiles are tracked incrementally: removed_tiles counts the rows of
+// at whose keep word (~visited & live) just became zero.
 template <int D>
 __global__ void k_bfs_update_dir(uint32_t ntr, uint32_t n, const void *__restrict__ next, void *__restrict__ visited,
                                  double *__restrict__ levels, double level, const uint32_t *__restrict__ trp_a,
                                  const uint32_t *__restrict__ trp_at, const void *__restrict__ live_at,
                                  uint2 *__restrict__ list, BfsCounters *__restrict__ cnt) {
     using W = typename WordT<D>::T;
-    unsigned long long ft = 0, ut = 0, fv = 0;
+    constexpr int WB = sizeof(W), WPC = 16 / WB;
+    unsigned long long ft = 0, rt = 0, fv = 0;
     int found = 0;
     const uint32_t lane = lane_id();
-    uint32_t I0 = blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t stride = gridDim.x * blockDim.x;
-    uint32_t iters = (ntr + stride - 1) / stride;  // warp-uniform trip count (ballots below)
+    const uint32_t nchunks = (ntr + WPC - 1) / WPC;
+    const uint32_t c0 = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t iters = (nchunks + stride - 1) / stride;  // warp-uniform trip count (scan below)
     for (uint32_t k = 0; k < iters; k++) {
-        uint32_t I = I0 + k * stride;
-        uint32_t w = 0, vis = 0, nch = 0, len = 0;
-        if (I < ntr) {
-            w = load_word<D>(next, I);
-            vis = load_word<D>(visited, I);
-            if (w) {
-                found = 1;
-                vis |= w;
-                reinterpret_cast<W *>(visited)[I] = (W)vis;
+        uint32_t c = c0 + k * stride;
+        uint4 nv = c < nchunks ? reinterpret_cast<const uint4 *>(next)[c] : make_uint4(0, 0, 0, 0);
+        const W *nw = reinterpret_cast<const W *>(&nv);
+        uint32_t nch = 0;
+        if (nv.x | nv.y | nv.z | nv.w) {
+            found = 1;
+#pragma unroll
+            for (int j = 0; j < WPC; j++) {
+                uint32_t w = nw[j];
+                uint32_t I = c * WPC + j;
+                if (!w || I >= ntr) continue;
+                W *vp = reinterpret_cast<W *>(visited) + I;
+                uint32_t old = *vp, vis = old | w;
+                *vp = (W)vis;
                 fv += __popc(w);
                 uint32_t b = w;
                 while (b) {
@@ -225,40 +221,77 @@ __global__ void k_bfs_update_dir(uint32_t ntr, uint32_t n, const void *__restric
                     b &= b - 1;
                     levels[(size_t)I * D + kk] = level;
                 }
+                uint32_t lv = load_word<D>(live_at, I);
+                if ((~old & lv) && !(~vis & lv)) rt += trp_at[I + 1] - trp_at[I];
                 if (trp_a) {
-                    len = trp_a[I + 1] - trp_a[I];
+                    uint32_t len = trp_a[I + 1] - trp_a[I];
                     ft += len;
-                    nch = (len + PUSH_CH - 1) / PUSH_CH;
+                    nch += (len + PUSH_CH - 1) / PUSH_CH;
                 }
             }
-            uint32_t keep = ~vis & load_word<D>(live_at, I);
-            if (keep) ut += trp_at[I + 1] - trp_at[I];
         }
         // warp-aggregated reservation of push entries
-        uint32_t incl = nch;
+        if (__any_sync(0xffffffffu, nch != 0)) {
+            uint32_t incl = nch;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (uint32_t)o) incl += y;
+            }
+            uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            uint32_t base = 0;
+            if (lane == 31) base = atomicAdd(&cnt->list_n, total);
+            base = __shfl_sync(0xffffffffu, base, 31);
+            uint32_t o = base + incl - nch;
+            if (nch) {
+#pragma unroll
+                for (int j = 0; j < WPC; j++) {
+                    uint32_t I = c * WPC + j;
+                    if (!nw[j] || I >= ntr) continue;
+                    uint32_t len = trp_a[I + 1] - trp_a[I];
+                    for (uint32_t q = 0; q < (len + PUSH_CH - 1) / PUSH_CH; q++) list[o++] = make_uint2(I, q);
+                }
+            }
+        }
+    }
+    ft = __reduce_add_sync(0xffffffffu, (uint32_t)ft);  // per-warp sums < T < 2^32
+    rt = __reduce_add_sync(0xffffffffu, (uint32_t)rt);
+    fv = __reduce_add_sync(0xffffffffu, (uint32_t)fv);
+    if (lane == 0) {
+        if (ft) atomicAdd(&cnt->frontier_tiles, ft);
+        if (rt) atomicAdd(&cnt->removed_tiles, rt);
+        if (fv) atomicAdd(&cnt->frontier_vertices, fv);
+    }
+    if (__any_sync(0xffffffffu, found) && lane == 0) atomicOr(&cnt->any, 1);
+}
+
+// late pull levels: the items of tile rows that still have a keep bit
+template <int D>
+__global__ void k_active_items(uint32_t ntr, const void *__restrict__ visited, const void *__restrict__ live,
+                               const uint32_t *__restrict__ item_ofs, uint32_t *__restrict__ idx,
+                               uint32_t *__restrict__ count) {
+    const uint32_t lane = lane_id();
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t iters = (ntr + stride - 1) / stride;
+    for (uint32_t k = 0; k < iters; k++) {
+        uint32_t I = blockIdx.x * blockDim.x + threadIdx.x + k * stride;
+        uint32_t nit = 0, first = 0;
+        if (I < ntr && (~load_word<D>(visited, I) & load_word<D>(live, I))) {
+            first = item_ofs[I];
+            nit = item_ofs[I + 1] - first;
+        }
+        if (!__any_sync(0xffffffffu, nit != 0)) continue;
+        uint32_t incl = nit;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= (uint32_t)o) incl += y;
         }
-        uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        uint32_t base = 0;
-        if (total) {
-            if (lane == 31) base = atomicAdd(&cnt->list_n, total);
-            base = __shfl_sync(0xffffffffu, base, 31);
-            uint32_t o = base + incl - nch;
-            for (uint32_t j = 0; j < nch; j++) list[o + j] = make_uint2(I, j);
-        }
+        uint32_t total = __shfl_sync(0xffffffffu, incl, 31), base = 0;
+        if (lane == 31) base = atomicAdd(count, total);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        for (uint32_t j = 0; j < nit; j++) idx[base + incl - nit + j] = first + j;
     }
-    ft = __reduce_add_sync(0xffffffffu, (uint32_t)ft) + 0ull;  // per-thread sums fit 32 bits per warp slice
-    ut = __reduce_add_sync(0xffffffffu, (uint32_t)ut) + 0ull;
-    fv = __reduce_add_sync(0xffffffffu, (uint32_t)fv) + 0ull;
-    if (lane == 0) {
-        if (ft) atomicAdd(&cnt->frontier_tiles, ft);
-        if (ut) atomicAdd(&cnt->unvisited_tiles, ut);
-        if (fv) atomicAdd(&cnt->frontier_vertices, fv);
-    }
-    if (__any_sync(0xffffffffu, found) && lane == 0) atomicOr(&cnt->any, 1);
 }
 
 // warp per push entry; lane-strided tiles
@@ -314,6 +347,16 @@ __global__ void k_row_live(uint32_t ntr, const uint32_t *__restrict__ trp, const
     }
 }
 
+template <int D>
+__global__ void k_live_tiles(uint32_t ntr, const uint32_t *__restrict__ trp, const void *__restrict__ live,
+                             unsigned long long *__restrict__ out) {
+    unsigned long long acc = 0;
+    for (uint32_t I = blockIdx.x * blockDim.x + threadIdx.x; I < ntr; I += gridDim.x * blockDim.x)
+        if (load_word<D>(live, I)) acc += trp[I + 1] - trp[I];
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane_id() == 0 && acc) atomicAdd(out, acc);
+}
+
 void ensure_live(b2sr_matrix *m, cudaStream_t s) {
     if (m->live) return;
     Buf<uint8_t> lv(padded_vec_bytes(m->ntr, m->dim), s);
@@ -325,22 +368,33 @@ void ensure_live(b2sr_matrix *m, cudaStream_t s) {
         case 16: LAUNCH(k_row_live<16>, g, 256, 0, s, m->ntr, m->trp, (const uint16_t *)m->tiles, (uint16_t *)lv.p); break;
         default: LAUNCH(k_row_live<32>, g, 256, 0, s, m->ntr, m->trp, (const uint32_t *)m->tiles, (uint32_t *)lv.p); break;
     }
+    // tiles in rows with a live bit: the starting "unvisited tiles" of a BFS
+    Buf<unsigned long long> lt(1, s);
+    CK(cudaMemsetAsync(lt.p, 0, 8, s));
+    switch (m->dim) {
+        case 4: LAUNCH(k_live_tiles<4>, grid_for(m->ntr), 256, 0, s, m->ntr, m->trp, lv.p, lt.p); break;
+        case 8: LAUNCH(k_live_tiles<8>, grid_for(m->ntr), 256, 0, s, m->ntr, m->trp, lv.p, lt.p); break;
+        case 16: LAUNCH(k_live_tiles<16>, grid_for(m->ntr), 256, 0, s, m->ntr, m->trp, lv.p, lt.p); break;
+        default: LAUNCH(k_live_tiles<32>, grid_for(m->ntr), 256, 0, s, m->ntr, m->trp, lv.p, lt.p); break;
+    }
+    m->live_tiles = read_scalar(lt.p, s);
     m->live = lv.release();
 }
 
-void bfs_sweep(b2sr_matrix *at, const void *frontier, const void *visited, void *next, cudaStream_t s) {
+void bfs_sweep(b2sr_matrix *at, const void *frontier, const void *visited, void *next, cudaStream_t s,
+               const uint32_t *idx = nullptr, const uint32_t *idx_n = nullptr) {
     ensure_live(at, s);
-    if (blocked_enabled() && launch_blocked(at, 1, frontier, visited, next, s)) return;
+    if (!idx && blocked_enabled() && launch_blocked(at, 1, frontier, visited, next, s)) return;
     ensure_items(at, s);
     CK(cudaMemsetAsync(next, 0, padded_vec_bytes(at->ntr, at->dim), s));
     uint64_t blocks = ((uint64_t)at->n_items + 7) / 8, cap = (uint64_t)num_sms() * 16;
     unsigned g = (unsigned)std::min(blocks, cap);
     const uint8_t *tl = (const uint8_t *)at->tiles;
     switch (at->dim) {
-        case 4: LAUNCH(k_bfs_pull<4>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0); break;
-        case 8: LAUNCH(k_bfs_pull<8>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0); break;
-        case 16: LAUNCH(k_bfs_pull<16>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0); break;
-        default: LAUNCH(k_bfs_pull<32>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0); break;
+        case 4: LAUNCH(k_bfs_pull<4>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0, idx, idx_n); break;
+        case 8: LAUNCH(k_bfs_pull<8>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0, idx, idx_n); break;
+        case 16: LAUNCH(k_bfs_pull<16>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0, idx, idx_n); break;
+        default: LAUNCH(k_bfs_pull<32>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0, idx, idx_n); break;
     }
 }
 
@@ -604,10 +658,28 @@ int b2sr_bfs(const b2sr_matrix *a_c, const b2sr_matrix *at_c, uint32_t src, doub
         CK(cudaMemcpyAsync(&h, cnt.p, sizeof(BfsCounters), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
     };
-    update(frontier, 0.0);  // level 0 = {src}
+    uint64_t unvisited = at->live_tiles;  // tiles of at in rows that still have a keep bit
+    update(frontier, 0.0);                // level 0 = {src}
+    unvisited -= h.removed_tiles;
+    Buf<uint32_t> act_idx, act_n;         // active-item list for late pull levels
     int64_t sweeps = 0;
     for (;;) {
-        bool push = a && (double)h.frontier_tiles * alpha < (double)h.unvisited_tiles;
+        bool push = a && (double)h.frontier_tiles * alpha < (double)unvisited;
+        bool sparse_pull = !push && unvisited * 16 < at->num_tiles;
+        if (sparse_pull) {
+            if (!act_idx.p) {
+                act_idx = Buf<uint32_t>(at->n_items, s);
+                act_n = Buf<uint32_t>(1, s);
+            }
+            CK(cudaMemsetAsync(act_n.p, 0, 4, s));
+            unsigned g = grid_for(ntr);
+            switch (d) {
+                case 4: LAUNCH(k_active_items<4>, g, 256, 0, s, ntr, visited.p, at->live, at->item_ofs, act_idx.p, act_n.p); break;
+                case 8: LAUNCH(k_active_items<8>, g, 256, 0, s, ntr, visited.p, at->live, at->item_ofs, act_idx.p, act_n.p); break;
+                case 16: LAUNCH(k_active_items<16>, g, 256, 0, s, ntr, visited.p, at->live, at->item_ofs, act_idx.p, act_n.p); break;
+                default: LAUNCH(k_active_items<32>, g, 256, 0, s, ntr, visited.p, at->live, at->item_ofs, act_idx.p, act_n.p); break;
+            }
+        }
         if (push) {
             CK(cudaMemsetAsync(next, 0, vb, s));
             uint64_t blocks = ((uint64_t)h.list_n + 7) / 8, cap = (uint64_t)num_sms() * 16;
@@ -618,14 +690,18 @@ int b2sr_bfs(const b2sr_matrix *a_c, const b2sr_matrix *at_c, uint32_t src, doub
                 case 16: LAUNCH(k_bfs_push<16>, g, 256, 0, s, list.p, cnt.p, a->trp, a->tci, (const uint16_t *)a->tiles, frontier, visited.p, next); break;
                 default: LAUNCH(k_bfs_push<32>, g, 256, 0, s, list.p, cnt.p, a->trp, a->tci, (const uint32_t *)a->tiles, frontier, visited.p, next); break;
             }
+        } else if (sparse_pull) {
+            bfs_sweep(at, frontier, visited.p, next, s, act_idx.p, act_n.p);
         } else {
             bfs_sweep(at, frontier, visited.p, next, s);
         }
         sweeps++;
         if (trace)
             fprintf(stderr, "[b2sr bfs] level %lld %s frontier_v=%llu frontier_tiles=%llu unvisited_tiles=%llu\n",
-                    (long long)sweeps, push ? "push" : "pull", h.frontier_vertices, h.frontier_tiles, h.unvisited_tiles);
+                    (long long)sweeps, push ? "push" : (sparse_pull ? "pull(active)" : "pull"),
+                    h.frontier_vertices, h.frontier_tiles, (unsigned long long)unvisited);
         update(next, (double)sweeps);
+        unvisited -= h.removed_tiles;
         std::swap(frontier, next);
         if (sweeps > (int64_t)n) B2SR_THROW(B2SR_ENOCONV, "BFS failed to drain its frontier");
         if (!h.any) break;
