@@ -86,7 +86,7 @@ struct LaneTiles {
     uint32_t xw[Geo<D>::TPL]; // x word per tile (0 when invalid)
 };
 
-template <int D>
+template <int D, int XG = 0>
 __device__ __forceinline__ void load_lane(const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
                                           const void *__restrict__ x, uint32_t base, uint32_t t0, uint32_t t1,
                                           uint32_t lane, LaneTiles<D> &lt) {
@@ -106,14 +106,14 @@ __device__ __forceinline__ void load_lane(const uint8_t *__restrict__ tiles, con
 #pragma unroll
         for (int j = 0; j < G::TPL; j++) {
             bool ok = tl + j >= t0 && tl + j < t1;
-            lt.xw[j] = ok ? load_word<D>(x, cols[j]) : 0u;
+            lt.xw[j] = ok ? load_x<D, XG>(x, cols[j]) : 0u;
         }
     } else {
         uint32_t t = base + lane / G::LPT;
         uint32_t q = lane % G::LPT;
         bool ok = t < t1;
         lt.v = ok ? ld_stream128(tiles + (size_t)t * G::TB + q * 16) : make_uint4(0, 0, 0, 0);
-        lt.xw[0] = ok ? load_word<D>(x, __ldg(tci + t)) : 0u;
+        lt.xw[0] = ok ? load_x<D, XG>(x, __ldg(tci + t)) : 0u;
     }
 }
 
@@ -124,7 +124,7 @@ __device__ __forceinline__ uint32_t lane_hits(const LaneTiles<D> &lt, uint32_t l
 }
 
 // ------------------------------------------------------------ K4 bbb
-template <int D>
+template <int D, int XG>
 __global__ void __launch_bounds__(256) k_bmv_bbb(const WorkItem *__restrict__ items, uint32_t n_items,
                                                  const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
                                                  const void *__restrict__ x, const void *__restrict__ keep,
@@ -140,13 +140,13 @@ __global__ void __launch_bounds__(256) k_bmv_bbb(const WorkItem *__restrict__ it
         // two warp loads in flight per iteration
         for (; base + G::TPW < it.t1; base += 2 * G::TPW) {
             LaneTiles<D> a, b;
-            load_lane<D>(tiles, tci, x, base, it.t0, it.t1, lane, a);
-            load_lane<D>(tiles, tci, x, base + G::TPW, it.t0, it.t1, lane, b);
+            load_lane<D, XG>(tiles, tci, x, base, it.t0, it.t1, lane, a);
+            load_lane<D, XG>(tiles, tci, x, base + G::TPW, it.t0, it.t1, lane, b);
             acc |= lane_hits<D>(a, lane) | lane_hits<D>(b, lane);
         }
         if (base < it.t1) {
             LaneTiles<D> a;
-            load_lane<D>(tiles, tci, x, base, it.t0, it.t1, lane, a);
+            load_lane<D, XG>(tiles, tci, x, base, it.t0, it.t1, lane, a);
             acc |= lane_hits<D>(a, lane);
         }
         acc = __reduce_or_sync(0xffffffffu, acc);
@@ -397,12 +397,24 @@ void launch_bbb(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaSt
     if (m->any_split) CK(cudaMemsetAsync(y, 0, padded_vec_bytes(m->ntr, m->dim), s));
     unsigned g = item_grid(m);
     const uint8_t *tl = (const uint8_t *)m->tiles;
+    const char *xg_env = getenv("B2SR_XGATHER");  // cache policy of the x gathers (A/B)
+    int xg = xg_env ? atoi(xg_env) : 0;
+#define BBB_LAUNCH(DD, XX) \
+    LAUNCH((k_bmv_bbb<DD, XX>), g, 256, 0, s, m->items, m->n_items, tl, m->tci, x, keep, y, m->row0)
+#define BBB_CASE(DD)                                  \
+    case DD:                                          \
+        if (xg == 1) BBB_LAUNCH(DD, 1);               \
+        else if (xg == 2) BBB_LAUNCH(DD, 2);          \
+        else BBB_LAUNCH(DD, 0);                       \
+        break;
     switch (m->dim) {
-        case 4: LAUNCH(k_bmv_bbb<4>, g, 256, 0, s, m->items, m->n_items, tl, m->tci, x, keep, y, m->row0); break;
-        case 8: LAUNCH(k_bmv_bbb<8>, g, 256, 0, s, m->items, m->n_items, tl, m->tci, x, keep, y, m->row0); break;
-        case 16: LAUNCH(k_bmv_bbb<16>, g, 256, 0, s, m->items, m->n_items, tl, m->tci, x, keep, y, m->row0); break;
-        default: LAUNCH(k_bmv_bbb<32>, g, 256, 0, s, m->items, m->n_items, tl, m->tci, x, keep, y, m->row0); break;
+        BBB_CASE(4)
+        BBB_CASE(8)
+        BBB_CASE(16)
+        BBB_CASE(32)
     }
+#undef BBB_CASE
+#undef BBB_LAUNCH
 }
 
 static size_t local_rows(const b2sr_matrix *m) {
