@@ -140,6 +140,8 @@ struct b2sr_matrix {
     void *plan = nullptr;
     uint64_t live_tiles = 0;          // tiles in rows with a live bit (set with `live`)
     uint32_t *item_ofs = nullptr;     // ntr+1: first work item of each tile row (with `items`)
+    uint32_t *long_rows = nullptr;    // tile rows handled by the CTA-per-row float gather
+    uint32_t n_long = 0;
 };
 
 namespace b2sr {

@@ -289,7 +289,7 @@ __global__ void __launch_bounds__(256) k_bmv_bff(uint32_t ntr, uint32_t n, const
                                                  const uint32_t *__restrict__ tci,
                                                  const typename WordT<D>::T *__restrict__ tiles,
                                                  const double *__restrict__ x, double inc, const void *__restrict__ keep,
-                                                 double *__restrict__ y, uint32_t row0) {
+                                                 double *__restrict__ y, uint32_t row0, uint32_t long_thresh) {
     constexpr uint32_t GPW = 32 / D;
     const uint32_t lane = lane_id(), r = lane % D;
     const double ident = RING == B2SR_RING_MINPLUS ? __longlong_as_double(0x7FF0000000000000ll) : 0.0;
@@ -297,6 +297,7 @@ __global__ void __launch_bounds__(256) k_bmv_bff(uint32_t ntr, uint32_t n, const
     for (uint32_t I = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * GPW + lane / D; I < ntr; I += groups) {
         double acc = ident;
         uint32_t t = trp[I], t1 = trp[I + 1];
+        if (t1 - t > long_thresh) continue;  // k_bmv_bff_long owns this row
         // four tiles per step: indices and row words first, then the gathers
         for (; t + 4 <= t1; t += 4) {
             uint32_t k0 = __ldg(tci + t), k1 = __ldg(tci + t + 1), k2 = __ldg(tci + t + 2), k3 = __ldg(tci + t + 3);
@@ -328,6 +329,91 @@ __global__ void __launch_bounds__(256) k_bmv_bff(uint32_t ntr, uint32_t n, const
         if (vrow < n) {
             if (keep && !((load_word<D>(keep, grow) >> r) & 1u)) acc = ident;
             y[(size_t)I * D + r] = acc;
+        }
+    }
+}
+
+// ------------------------------------------------------------ K6 long rows
+// A hub tile row (R-MAT s24: ~1e5 tiles) walked by one group of d lanes is a
+// serial chain of dependent loads -- it alone took >150 ms per PageRank sweep.
+// Rows longer than LONG_ROW_TILES get a CTA: per chunk of LONG_CHUNK tiles
+// every thread stages one tile (its d row words, and the x values of the
+// columns any of its rows touch) in shared memory, then thread r folds bit-row
+// r over the staged tiles in ascending order -- the reference's summation
+// order, so ARITHMETIC stays bit-identical -- while the gathers ran in parallel.
+constexpr uint32_t LONG_ROW_TILES = 512;
+constexpr int LONG_THREADS = 256;
+
+__global__ void k_find_long(uint32_t ntr, const uint32_t *trp, uint32_t thresh, uint32_t *rows, uint32_t *count) {
+    for (uint32_t I = blockIdx.x * blockDim.x + threadIdx.x; I < ntr; I += gridDim.x * blockDim.x)
+        if (trp[I + 1] - trp[I] > thresh) rows[atomicAdd(count, 1u)] = I;
+}
+
+void ensure_long_rows(b2sr_matrix *m, cudaStream_t s) {
+    if (m->long_rows) return;
+    Buf<uint32_t> rows(m->ntr, s), cnt(1, s);
+    CK(cudaMemsetAsync(cnt.p, 0, 4, s));
+    unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((m->ntr + 255) / 256, (uint64_t)num_sms() * 16));
+    LAUNCH(k_find_long, g, 256, 0, s, m->ntr, m->trp, LONG_ROW_TILES, rows.p, cnt.p);
+    m->n_long = read_scalar(cnt.p, s);
+    m->long_rows = rows.release();
+}
+
+template <int D, int RING>
+__global__ void __launch_bounds__(LONG_THREADS) k_bmv_bff_long(uint32_t n_long, const uint32_t *__restrict__ long_rows,
+                                                               uint32_t n, const uint32_t *__restrict__ trp,
+                                                               const uint32_t *__restrict__ tci,
+                                                               const typename WordT<D>::T *__restrict__ tiles,
+                                                               const double *__restrict__ x, double inc,
+                                                               const void *__restrict__ keep, double *__restrict__ y,
+                                                               uint32_t row0) {
+    constexpr int C = D == 32 ? 128 : LONG_THREADS;  // tiles per chunk (smem: C*D*(8+4) bytes)
+    __shared__ double sx[C][D];
+    __shared__ uint32_t sw[C][D];
+    const double ident = RING == B2SR_RING_MINPLUS ? __longlong_as_double(0x7FF0000000000000ll) : 0.0;
+    const uint32_t tid = threadIdx.x;
+    for (uint32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
+        uint32_t I = long_rows[li];
+        uint32_t t0 = trp[I], t1 = trp[I + 1];
+        double acc = ident;  // meaningful in threads r < D
+        for (uint32_t base = t0; base < t1; base += C) {
+            uint32_t cnt = min((uint32_t)C, t1 - base);
+            if (tid < cnt) {
+                uint32_t t = base + tid;
+                const double *xs = x + (size_t)__ldg(tci + t) * D;
+                uint32_t any = 0;
+#pragma unroll
+                for (int r = 0; r < D; r++) {
+                    uint32_t w = tiles[(size_t)t * D + r];
+                    sw[tid][r] = w;
+                    any |= w;
+                }
+                while (any) {  // x values of every column this tile touches
+                    int k = __ffs(any) - 1;
+                    any &= any - 1;
+                    sx[tid][k] = __ldg(xs + k);
+                }
+            }
+            __syncthreads();
+            if (tid < (uint32_t)D) {
+                for (uint32_t j = 0; j < cnt; j++) {
+                    uint32_t w = sw[j][tid];
+                    while (w) {
+                        int k = __ffs(w) - 1;
+                        w &= w - 1;
+                        acc = ring_op<RING>(acc, sx[j][k], inc);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        if (tid < (uint32_t)D) {
+            uint32_t grow = row0 + I;
+            uint64_t vrow = (uint64_t)grow * D + tid;
+            if (vrow < n) {
+                if (keep && !((load_word<D>(keep, grow) >> tid) & 1u)) acc = ident;
+                y[(size_t)I * D + tid] = acc;
+            }
         }
     }
 }
@@ -440,17 +526,24 @@ template <int D>
 static void bff_ring(const b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
                      cudaStream_t s) {
     constexpr uint32_t GPW = 32 / D;
+    ensure_long_rows(const_cast<b2sr_matrix *>(m), s);
     uint64_t warps = ((uint64_t)m->ntr + GPW - 1) / GPW;
     uint64_t blocks = (warps + 7) / 8, cap = (uint64_t)num_sms() * 16;
     unsigned g = (unsigned)(blocks < cap ? blocks : cap);
+    unsigned gl = (unsigned)std::min<uint64_t>(m->n_long, (uint64_t)num_sms() * 8);
     using W = typename WordT<D>::T;
     const W *tl = (const W *)m->tiles;
-    if (ring == B2SR_RING_ARITHMETIC)
-        LAUNCH((k_bmv_bff<D, B2SR_RING_ARITHMETIC>), g, 256, 0, s, m->ntr, m->n, m->trp, m->tci, tl, x, inc, keep, y, m->row0);
-    else if (ring == B2SR_RING_MINPLUS)
-        LAUNCH((k_bmv_bff<D, B2SR_RING_MINPLUS>), g, 256, 0, s, m->ntr, m->n, m->trp, m->tci, tl, x, inc, keep, y, m->row0);
-    else
-        LAUNCH((k_bmv_bff<D, B2SR_RING_MAXTIMES>), g, 256, 0, s, m->ntr, m->n, m->trp, m->tci, tl, x, inc, keep, y, m->row0);
+#define BFF_RING(RR)                                                                                              \
+    do {                                                                                                          \
+        LAUNCH((k_bmv_bff<D, RR>), g, 256, 0, s, m->ntr, m->n, m->trp, m->tci, tl, x, inc, keep, y, m->row0,      \
+               LONG_ROW_TILES);                                                                                   \
+        LAUNCH((k_bmv_bff_long<D, RR>), gl, LONG_THREADS, 0, s, m->n_long, m->long_rows, m->n, m->trp, m->tci,   \
+               tl, x, inc, keep, y, m->row0);                                                                     \
+    } while (0)
+    if (ring == B2SR_RING_ARITHMETIC) BFF_RING(B2SR_RING_ARITHMETIC);
+    else if (ring == B2SR_RING_MINPLUS) BFF_RING(B2SR_RING_MINPLUS);
+    else BFF_RING(B2SR_RING_MAXTIMES);
+#undef BFF_RING
 }
 
 void launch_bff(const b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,

@@ -97,6 +97,7 @@ void free_matrix(b2sr_matrix *m) {
     dfree(m->items, nullptr);
     dfree(m->live, nullptr);
     dfree(m->item_ofs, nullptr);
+    dfree(m->long_rows, nullptr);
     free_plan(m->plan);
     if (cur != m->device) cudaSetDevice(cur);
     delete m;

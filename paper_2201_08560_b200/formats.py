@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes
 import struct
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -583,11 +584,14 @@ def b2sr_transpose(m: B2srMatrix) -> B2srMatrix:
     Matrices are immutable, so the result is cached on ``m`` (and ``m`` on
     the result): repeated ``bfs``/``sssp`` calls transpose once.
     """
-    if m._transpose is not None:
-        return m._transpose
+    cached = m._transpose
+    if cached is not None:
+        t = cached() if isinstance(cached, weakref.ref) else cached
+        if t is not None:
+            return t
     t = B2srMatrix._wrap(_new_handle("b2sr_transpose", m.handle().ptr, dev.stream()))
     m._transpose = t
-    t._transpose = m
+    t._transpose = weakref.ref(m)  # no reference cycle: device memory is freed by refcounting
     return t
 
 
