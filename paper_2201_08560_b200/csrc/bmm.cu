@@ -226,8 +226,161 @@ __global__ void __launch_bounds__(256) k_bmm_masked_items(uint64_t n_items, cons
     if (lane == 0 && acc) atomicAdd(out, acc);
 }
 
+// ------------------------------------------------------------ row-hash path
+// Work unit = (mask tile row I, up to ROW_UNIT of its mask tiles).  The CTA
+// hashes A's tile row I (column -> position) into shared memory once; each
+// warp then takes a mask tile (I, J), streams Bt's row J 32 columns at a
+// time (coalesced) and probes the table -- one memory round trip per 32
+// candidates instead of a dependent binary search per candidate.  Rows of A
+// longer than HASH_MAX fall back to the binary-search warp loop.
+constexpr uint32_t ROW_UNIT = 128;
+constexpr uint32_t HASH_MAX = 4096;              // A-row entries that fit the table
+constexpr uint32_t HASH_SLOTS = 2 * HASH_MAX;    // 64 KB of keys + positions
+constexpr uint32_t EMPTY_KEY = 0xFFFFFFFFu;
+
+__global__ void k_rowunit_counts(uint32_t mntr, uint32_t m_row0, const uint32_t *__restrict__ mtrp,
+                                 const uint32_t *__restrict__ a_trp, uint32_t *__restrict__ cnt) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < mntr; r += gridDim.x * blockDim.x) {
+        uint32_t I = r + m_row0, len = mtrp[r + 1] - mtrp[r];
+        cnt[r] = (a_trp[I + 1] > a_trp[I]) ? (len + ROW_UNIT - 1) / ROW_UNIT : 0;
+    }
+}
+
+__global__ void k_rowunit_fill(uint32_t mntr, const uint32_t *__restrict__ mtrp, const uint32_t *__restrict__ cnt,
+                               const uint64_t *__restrict__ ofs, uint4 *__restrict__ units) {
+    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < mntr; r += gridDim.x * blockDim.x) {
+        uint64_t o = ofs[r];
+        uint32_t m0 = mtrp[r], m1 = mtrp[r + 1];
+        for (uint32_t j = 0; j < cnt[r]; j++) units[o + j] = make_uint4(r, m0 + j * ROW_UNIT, min(m1, m0 + (j + 1) * ROW_UNIT), 0);
+    }
+}
+
+__device__ __forceinline__ uint32_t hash_slot(uint32_t k, uint32_t mask) { return (k * 0x9E3779B1u >> 7) & mask; }
+
+template <int D>
+__device__ __forceinline__ unsigned long long mask_tile_pops(uint32_t mword, uint32_t rows_used, bool hit, uint32_t ta,
+                                                             uint32_t tb, const typename WordT<D>::T *__restrict__ a_tiles,
+                                                             const typename WordT<D>::T *__restrict__ b_tiles) {
+    unsigned long long acc = 0;
+    uint32_t ru = rows_used;
+    while (ru) {  // warp-uniform loop over non-empty mask rows
+        int r = __ffs(ru) - 1;
+        ru &= ru - 1;
+        uint32_t mw = __shfl_sync(0xffffffffu, mword, r);
+        if (hit) {
+            uint32_t aw = a_tiles[(size_t)ta * D + r];
+            while (aw && mw) {
+                int c = __ffs(mw) - 1;
+                mw &= mw - 1;
+                acc += __popc(aw & (uint32_t)b_tiles[(size_t)tb * D + c]);
+            }
+        }
+    }
+    return acc;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_bmm_rowhash(uint32_t n_units, const uint4 *__restrict__ units, uint32_t m_row0,
+                                                     const uint32_t *__restrict__ m_tci,
+                                                     const typename WordT<D>::T *__restrict__ m_tiles,
+                                                     const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ a_tci,
+                                                     const typename WordT<D>::T *__restrict__ a_tiles,
+                                                     const uint32_t *__restrict__ b_trp, const uint32_t *__restrict__ b_tci,
+                                                     const typename WordT<D>::T *__restrict__ b_tiles,
+                                                     unsigned long long *__restrict__ out) {
+    extern __shared__ uint32_t hsm[];  // HASH_SLOTS keys then HASH_SLOTS positions
+    uint32_t *hkey = hsm, *hval = hsm + HASH_SLOTS;
+    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    unsigned long long acc = 0;
+    for (uint32_t u = blockIdx.x; u < n_units; u += gridDim.x) {
+        uint4 un = units[u];
+        uint32_t I = un.x + m_row0;
+        uint32_t a0 = a_trp[I], a1 = a_trp[I + 1], la = a1 - a0;
+        bool hashed = la <= HASH_MAX;
+        uint32_t hs = 64;
+        while (hs < 2 * la) hs <<= 1;
+        uint32_t hmask = hs - 1;
+        if (hashed) {
+            for (uint32_t i = threadIdx.x; i < hs; i += blockDim.x) hkey[i] = EMPTY_KEY;
+            __syncthreads();
+            for (uint32_t i = threadIdx.x; i < la; i += blockDim.x) {
+                uint32_t K = __ldg(a_tci + a0 + i), h = hash_slot(K, hmask);
+                while (atomicCAS(&hkey[h], EMPTY_KEY, K) != EMPTY_KEY) h = (h + 1) & hmask;
+                hval[h] = i;
+            }
+            __syncthreads();
+        }
+        for (uint32_t mt = un.y + warp; mt < un.z; mt += nwarps) {
+            uint32_t J = m_tci[mt];
+            uint32_t mword = lane < (uint32_t)D ? (uint32_t)m_tiles[(size_t)mt * D + lane] : 0u;
+            uint32_t rows_used = __ballot_sync(0xffffffffu, mword != 0);
+            uint32_t b0 = b_trp[J], b1 = b_trp[J + 1];
+            if (!rows_used || b0 == b1) continue;
+            if (hashed) {
+                for (uint32_t base = b0; base < b1; base += 32) {
+                    uint32_t bi = base + lane, ta = 0;
+                    bool hit = false;
+                    if (bi < b1) {
+                        uint32_t K = __ldg(b_tci + bi), h = hash_slot(K, hmask), key;
+                        while ((key = hkey[h]) != EMPTY_KEY && key != K) h = (h + 1) & hmask;
+                        if (key == K) { hit = true; ta = a0 + hval[h]; }
+                    }
+                    if (__ballot_sync(0xffffffffu, hit)) acc += mask_tile_pops<D>(mword, rows_used, hit, ta, bi, a_tiles, b_tiles);
+                }
+            } else {  // long A row: binary-search Bt's entries in it
+                for (uint32_t base = b0; base < b1; base += 32) {
+                    uint32_t bi = base + lane, ta = 0;
+                    bool hit = false;
+                    if (bi < b1) {
+                        uint32_t K = __ldg(b_tci + bi);
+                        uint32_t li = lower_bound_u32(a_tci, a0, a1, K);
+                        if (li < a1 && __ldg(a_tci + li) == K) { hit = true; ta = li; }
+                    }
+                    if (__ballot_sync(0xffffffffu, hit)) acc += mask_tile_pops<D>(mword, rows_used, hit, ta, bi, a_tiles, b_tiles);
+                }
+            }
+        }
+        __syncthreads();  // the table is rebuilt for the next unit
+    }
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0 && acc) atomicAdd(out, acc);
+}
+
+int64_t bmm_masked_rowhash(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_matrix *mask, cudaStream_t s) {
+    uint32_t mntr = mask->ntr;
+    Buf<uint32_t> cnt(mntr, s);
+    Buf<uint64_t> ofs((size_t)mntr + 1, s);
+    LAUNCH(k_rowunit_counts, grid_for(mntr), 256, 0, s, mntr, mask->row0, mask->trp, a->trp, cnt.p);
+    exclusive_scan_u32_to_u64(cnt.p, ofs.p, mntr, s);
+    uint64_t n_units = read_scalar(ofs.p + mntr, s);
+    Buf<unsigned long long> out(1, s);
+    CK(cudaMemsetAsync(out.p, 0, 8, s));
+    if (!n_units) return 0;
+    Buf<uint4> units(n_units, s);
+    LAUNCH(k_rowunit_fill, grid_for(mntr), 256, 0, s, mntr, mask->trp, cnt.p, ofs.p, units.p);
+    unsigned g = (unsigned)std::min<uint64_t>(n_units, (uint64_t)num_sms() * 3);
+    const int smem = 2 * HASH_SLOTS * 4;
+    switch (a->dim) {
+#define RH_CASE(DD, W)                                                                                          \
+    case DD:                                                                                                    \
+        CK(cudaFuncSetAttribute(k_bmm_rowhash<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));        \
+        LAUNCH(k_bmm_rowhash<DD>, g, 256, smem, s, (uint32_t)n_units, units.p, mask->row0, mask->tci,          \
+               (const W *)mask->tiles, a->trp, a->tci, (const W *)a->tiles, bt->trp, bt->tci,                  \
+               (const W *)bt->tiles, out.p);                                                                   \
+        break;
+        RH_CASE(4, uint8_t)
+        RH_CASE(8, uint8_t)
+        RH_CASE(16, uint16_t)
+        RH_CASE(32, uint32_t)
+#undef RH_CASE
+    }
+    return (int64_t)read_scalar(out.p, s);
+}
+
 int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_matrix *mask, cudaStream_t s) {
     if (!mask->num_tiles || !a->num_tiles || !bt->num_tiles) return 0;
+    const char *alg = getenv("B2SR_TC_ALG");  // "items" selects the chunked binary-search kernel (A/B)
+    if (!alg || alg[0] != 'i') return bmm_masked_rowhash(a, bt, mask, s);
     uint64_t TM = mask->num_tiles;
     Buf<uint32_t> rowid(TM, s), cnt(TM, s);
     Buf<uint64_t> ofs(TM + 1, s);
