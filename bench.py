@@ -56,6 +56,8 @@ def parse():
     p.add_argument("--tc-scale", type=int, default=20)
     p.add_argument("--no-tc", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--drivers-scale", type=int, default=24, help="PR/SSSP/CC scale (BASELINE configs[3])")
+    p.add_argument("--no-drivers", action="store_true")
     p.add_argument("--seed", type=int, default=1)
     return p.parse_args()
 
@@ -225,6 +227,7 @@ def run_ours(args, rank, world, local_rank):
     at = b2.b2sr_transpose(m)
     h = at.handle()
     hA = m.handle()
+    b2sr_gb = b2.storage_bytes(m) / 1e9
 
     # ---- timed BFS steps (device-resident: graph, transpose, levels stay in HBM) ----
     n_steps = args.steps
@@ -336,6 +339,11 @@ def run_ours(args, rank, world, local_rank):
     tc = None
     if not args.no_tc:
         tc = bench_tc(args, b2, rmat, torch, ev)
+    drivers = None
+    if not args.no_drivers:
+        del m, at, h, hA
+        torch.cuda.empty_cache()
+        drivers = bench_drivers(args, b2, rmat, torch, ev)
 
     line = {"metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
@@ -345,9 +353,9 @@ def run_ours(args, rank, world, local_rank):
                                    f"edgefactor {args.edgefactor}, B2SR-{d}",
                        "scale": args.scale, "n": n, "nnz": int(csr.nnz), "tile_dim": d, "roots": args.steps,
                        "parallelism": f"replicas{world}" if world > 1 else "single",
-                       "l2": "inputs larger than L2 (B2SR %.2f GB > 126 MB)" % (b2.storage_bytes(m) / 1e9)},
+                       "l2": "inputs larger than L2 (B2SR %.2f GB > 126 MB)" % b2sr_gb},
             "e2e": e2e, "roofline": roofline, "gpu_launches": int(launches), "bfs_sweeps_per_root": iters[:4],
-            "clocks": clk.summary(), "sweep": {str(k): v for k, v in sweep.items()}, "tc": tc,
+            "clocks": clk.summary(), "sweep": {str(k): v for k, v in sweep.items()}, "tc": tc, "drivers": drivers,
             "graph_gen_s": round(gen_s, 3)}
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(csr, d, roots[args.warmup])
@@ -365,6 +373,35 @@ def _fresh(hm):
     c._h = None
     c._transpose = None
     return c
+
+
+def bench_drivers(args, b2, rmat, torch, ev):
+    """BASELINE configs[3]: PageRank (10 iterations), SSSP and CC on R-MAT
+    scale 24 through the public API (parity vs the C oracle: tools/config4.py)."""
+    csr = rmat.rmat_csr(args.drivers_scale, args.edgefactor, seed=args.seed)
+    d = 4
+    m = b2.csr_to_b2sr(csr, d)
+    at = b2.b2sr_transpose(m)
+    deg = np.diff(csr.row_ptr.astype(np.int64)).astype(np.float64)
+    src = int(np.argmax(deg))
+    out = {"scale": args.drivers_scale, "tile_dim": d, "nnz": int(csr.nnz), "tiles": int(m.num_tiles)}
+
+    def timed(fn):
+        fn()  # warm (work partitions, long-row lists)
+        a0, a1 = ev(), ev()
+        a0.record()
+        r = fn()
+        a1.record()
+        torch.cuda.synchronize()
+        return r, a0.elapsed_time(a1)
+
+    r, ms = timed(lambda: b2.pagerank(at, deg))
+    out["pagerank"] = {"ms": round(ms, 3), "iterations": r.iterations, "ms_per_iter": round(ms / r.iterations, 3)}
+    r, ms = timed(lambda: b2.sssp(m, src))
+    out["sssp"] = {"ms": round(ms, 3), "iterations": r.iterations}
+    r, ms = timed(lambda: b2.connected_components(m))
+    out["cc"] = {"ms": round(ms, 3), "iterations": r.iterations}
+    return out
 
 
 def bench_tc(args, b2, rmat, torch, ev):

@@ -129,6 +129,46 @@ __global__ void __launch_bounds__(256) k_bfs_pull(const WorkItem *__restrict__ i
     }
 }
 
+// Sub-warp pull: a group of GS lanes per work item, GS*TPL/LPT tiles per step
+// (32 at d=4), and the all-keep-bits-hit exit is tested after every step, so a
+// tile row whose unvisited vertices find a parent early stops early.
+template <int D> struct PullGroup { static constexpr int GS = D <= 8 ? 8 : (D == 16 ? 16 : 32); };
+
+template <int D>
+__global__ void __launch_bounds__(256) k_bfs_pull_g(const WorkItem *__restrict__ items, uint32_t n_items, uint32_t n,
+                                                    const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
+                                                    const void *__restrict__ frontier, const void *__restrict__ visited,
+                                                    const void *__restrict__ live, void *__restrict__ next,
+                                                    uint32_t row0, const uint32_t *__restrict__ idx,
+                                                    const uint32_t *__restrict__ idx_n) {
+    using G = BGeo<D>;
+    constexpr int GS = PullGroup<D>::GS;
+    constexpr uint32_t STEP = GS * G::TPL / G::LPT;
+    const uint32_t lane = lane_id(), gl = lane % GS;
+    const uint32_t gmask = GS == 32 ? 0xffffffffu : (((1u << GS) - 1u) << (lane & ~(GS - 1u)));
+    const uint32_t groups = (gridDim.x * blockDim.x) / GS;
+    if (idx) n_items = *idx_n;
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / GS; w < n_items; w += groups) {
+        WorkItem it = items[idx ? idx[w] : w];
+        uint32_t grow = row0 + it.row;
+        uint32_t keepw = ~load_word<D>(visited, grow) & load_word<D>(live, it.row);  // live is block-local
+        if (!keepw) continue;
+        uint32_t acc = 0;
+        uint32_t base = G::TPL > 1 ? (it.t0 & ~(uint32_t)(G::TPL - 1)) : it.t0;
+        for (; base < it.t1; base += STEP) {
+            acc |= bfs_lane<D>(tiles, tci, frontier, base, it.t0, it.t1, gl);
+#pragma unroll
+            for (int o = GS / 2; o; o >>= 1) acc |= __shfl_xor_sync(gmask, acc, o);
+            if ((acc & keepw) == keepw) break;  // every unvisited row of the tile row reached
+        }
+        acc &= keepw;
+        if (gl == 0 && acc) {
+            if (it.split) atomic_or_word<D>(next, it.row, acc);
+            else reinterpret_cast<typename WordT<D>::T *>(next)[it.row] = (typename WordT<D>::T)acc;
+        }
+    }
+}
+
 // visited |= frontier; levels[new bits] = level; *any |= frontier != 0
 template <int D>
 __global__ void k_bfs_update(uint32_t ntr, const void *__restrict__ frontier, void *__restrict__ visited,
@@ -205,12 +245,12 @@ __global__ void k_bfs_update_dir(uint32_t ntr, uint32_t n, const void *__restric
         const W *nw = reinterpret_cast<const W *>(&nv);
         uint32_t nch = 0;
         if (nv.x | nv.y | nv.z | nv.w) {
-            found = 1;
 #pragma unroll
             for (int j = 0; j < WPC; j++) {
                 uint32_t w = nw[j];
                 uint32_t I = c * WPC + j;
-                if (!w || I >= ntr) continue;
+                if (!w || I >= ntr) continue;  // bytes past the last word are not part of the vector
+                found = 1;
                 W *vp = reinterpret_cast<W *>(visited) + I;
                 uint32_t old = *vp, vis = old | w;
                 *vp = (W)vis;
@@ -390,12 +430,24 @@ void bfs_sweep(b2sr_matrix *at, const void *frontier, const void *visited, void 
     uint64_t blocks = ((uint64_t)at->n_items + 7) / 8, cap = (uint64_t)num_sms() * 16;
     unsigned g = (unsigned)std::min(blocks, cap);
     const uint8_t *tl = (const uint8_t *)at->tiles;
+    const char *pv = getenv("B2SR_PULL");  // "warp" = one warp per item, two warp loads per exit test (A/B)
+    bool warp_pull = pv && pv[0] == 'w';
+#define PULL_CASE(DD)                                                                                              \
+    case DD:                                                                                                       \
+        if (warp_pull)                                                                                             \
+            LAUNCH(k_bfs_pull<DD>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited,    \
+                   at->live, next, at->row0, idx, idx_n);                                                          \
+        else                                                                                                       \
+            LAUNCH(k_bfs_pull_g<DD>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited,  \
+                   at->live, next, at->row0, idx, idx_n);                                                          \
+        break;
     switch (at->dim) {
-        case 4: LAUNCH(k_bfs_pull<4>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0, idx, idx_n); break;
-        case 8: LAUNCH(k_bfs_pull<8>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0, idx, idx_n); break;
-        case 16: LAUNCH(k_bfs_pull<16>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0, idx, idx_n); break;
-        default: LAUNCH(k_bfs_pull<32>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited, at->live, next, at->row0, idx, idx_n); break;
+        PULL_CASE(4)
+        PULL_CASE(8)
+        PULL_CASE(16)
+        PULL_CASE(32)
     }
+#undef PULL_CASE
 }
 
 void bfs_update(uint32_t n, uint32_t d, const void *frontier, void *visited, double *levels, double level, int *any,
