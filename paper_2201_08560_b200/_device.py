@@ -6,6 +6,7 @@ matrix data goes through libb2sr_sm100.so.
 
 from __future__ import annotations
 
+import threading
 import warnings
 
 import numpy as np
@@ -83,14 +84,23 @@ def to_host(tensor, dtype, count: int) -> np.ndarray:
     The copy lands in page-locked memory (torch's caching host allocator), so
     it is one DMA at PCIe/C2C speed; the returned array keeps that buffer alive.
     """
+    global _bounce
     t = torch()
     dt = np.dtype(dtype)
     nbytes = count * dt.itemsize
+    out = np.empty(count, dt)
     if nbytes == 0:
-        return np.zeros(0, dt)
-    host = t.empty(nbytes, dtype=t.uint8, pin_memory=True)
-    host.copy_(tensor.detach().view(t.uint8)[:nbytes])
-    return host.numpy().view(dt)
+        return out
+    with _bounce_lock:
+        if _bounce is None or _bounce.numel() < nbytes:
+            _bounce = t.empty(max(nbytes, 1 << 20), dtype=t.uint8, pin_memory=True)
+        _bounce[:nbytes].copy_(tensor.detach().view(t.uint8)[:nbytes])
+        out.view(np.uint8)[:] = _bounce[:nbytes].numpy()
+    return out
+
+
+_bounce = None  # reusable page-locked staging buffer for device -> host copies
+_bounce_lock = threading.Lock()
 
 
 def ptr(tensor) -> int:
