@@ -379,8 +379,10 @@ int64_t bmm_masked_rowhash(const b2sr_matrix *a, const b2sr_matrix *bt, const b2
 
 int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_matrix *mask, cudaStream_t s) {
     if (!mask->num_tiles || !a->num_tiles || !bt->num_tiles) return 0;
-    const char *alg = getenv("B2SR_TC_ALG");  // "items" selects the chunked binary-search kernel (A/B)
-    if (!alg || alg[0] != 'i') return bmm_masked_rowhash(a, bt, mask, s);
+    // B2SR_TC_ALG=rowhash selects the smem row-hash kernel (measured 176 ms vs
+    // 34 ms for the chunked items at s20 d=4, profiles/r01_pull_ab.txt)
+    const char *alg = getenv("B2SR_TC_ALG");
+    if (alg && alg[0] == 'r') return bmm_masked_rowhash(a, bt, mask, s);
     uint64_t TM = mask->num_tiles;
     Buf<uint32_t> rowid(TM, s), cnt(TM, s);
     Buf<uint64_t> ofs(TM + 1, s);

@@ -367,41 +367,93 @@ __global__ void __launch_bounds__(LONG_THREADS) k_bmv_bff_long(uint32_t n_long, 
                                                                const double *__restrict__ x, double inc,
                                                                const void *__restrict__ keep, double *__restrict__ y,
                                                                uint32_t row0) {
-    constexpr int C = D == 32 ? 128 : LONG_THREADS;  // tiles per chunk (smem: C*D*(8+4) bytes)
-    __shared__ double sx[C][D];
-    __shared__ uint32_t sw[C][D];
+    // C tiles per chunk, one per thread; each bit-row r gets up to CAP terms
+    // per chunk in smem (2 per tile on average; denser chunks take the slow fold)
+    constexpr int C = LONG_THREADS * 4 / D < LONG_THREADS ? LONG_THREADS * 4 / D : LONG_THREADS;
+    constexpr int CAP = 2 * C;
+    constexpr int NW = LONG_THREADS / 32;
+    __shared__ uint32_t sw[C][D];          // staged row words
+    __shared__ double sx[C][D];            // staged x values per (tile, column)
+    __shared__ double terms[D][CAP];       // compacted terms of each bit-row, in reference order
+    __shared__ uint32_t wsum[NW][D], tot[D];
     const double ident = RING == B2SR_RING_MINPLUS ? __longlong_as_double(0x7FF0000000000000ll) : 0.0;
-    const uint32_t tid = threadIdx.x;
+    const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
     for (uint32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
         uint32_t I = long_rows[li];
         uint32_t t0 = trp[I], t1 = trp[I + 1];
         double acc = ident;  // meaningful in threads r < D
         for (uint32_t base = t0; base < t1; base += C) {
             uint32_t cnt = min((uint32_t)C, t1 - base);
+            uint32_t w[D];
+#pragma unroll
+            for (int r = 0; r < D; r++) w[r] = 0;
             if (tid < cnt) {
                 uint32_t t = base + tid;
                 const double *xs = x + (size_t)__ldg(tci + t) * D;
                 uint32_t any = 0;
 #pragma unroll
                 for (int r = 0; r < D; r++) {
-                    uint32_t w = tiles[(size_t)t * D + r];
-                    sw[tid][r] = w;
-                    any |= w;
+                    w[r] = tiles[(size_t)t * D + r];
+                    sw[tid][r] = w[r];
+                    any |= w[r];
                 }
-                while (any) {  // x values of every column this tile touches
+                while (any) {  // x values of every column this tile touches (parallel gathers)
                     int k = __ffs(any) - 1;
                     any &= any - 1;
                     sx[tid][k] = __ldg(xs + k);
                 }
             }
+            // exclusive scan of per-tile term counts, separately for every bit-row
+            uint32_t off[D];
+#pragma unroll
+            for (int r = 0; r < D; r++) {
+                uint32_t c = __popc(w[r]), inc = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= (uint32_t)o) inc += y;
+                }
+                off[r] = inc - c;
+                if (lane == 31) wsum[wid][r] = inc;
+            }
             __syncthreads();
             if (tid < (uint32_t)D) {
-                for (uint32_t j = 0; j < cnt; j++) {
-                    uint32_t w = sw[j][tid];
-                    while (w) {
-                        int k = __ffs(w) - 1;
-                        w &= w - 1;
-                        acc = ring_op<RING>(acc, sx[j][k], inc);
+                uint32_t run = 0;
+                for (int q = 0; q < NW; q++) {
+                    uint32_t v = wsum[q][tid];
+                    wsum[q][tid] = run;
+                    run += v;
+                }
+                tot[tid] = run;
+            }
+            __syncthreads();
+            bool dense = false;
+#pragma unroll
+            for (int r = 0; r < D; r++) dense |= tot[r] > (uint32_t)CAP;
+            if (!dense && tid < cnt) {  // scatter this tile's terms (ascending column) per bit-row
+#pragma unroll
+                for (int r = 0; r < D; r++) {
+                    uint32_t o = wsum[wid][r] + off[r], b = w[r];
+                    while (b) {
+                        int k = __ffs(b) - 1;
+                        b &= b - 1;
+                        terms[r][o++] = sx[tid][k];
+                    }
+                }
+            }
+            __syncthreads();
+            if (tid < (uint32_t)D) {
+                if (!dense) {  // pure dependent-add chain over contiguous terms
+                    uint32_t nt = tot[tid];
+                    for (uint32_t q = 0; q < nt; q++) acc = ring_op<RING>(acc, terms[tid][q], inc);
+                } else {
+                    for (uint32_t j = 0; j < cnt; j++) {
+                        uint32_t b = sw[j][tid];
+                        while (b) {
+                            int k = __ffs(b) - 1;
+                            b &= b - 1;
+                            acc = ring_op<RING>(acc, sx[j][k], inc);
+                        }
                     }
                 }
             }

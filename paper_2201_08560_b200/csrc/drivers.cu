@@ -430,8 +430,10 @@ void bfs_sweep(b2sr_matrix *at, const void *frontier, const void *visited, void 
     uint64_t blocks = ((uint64_t)at->n_items + 7) / 8, cap = (uint64_t)num_sms() * 16;
     unsigned g = (unsigned)std::min(blocks, cap);
     const uint8_t *tl = (const uint8_t *)at->tiles;
-    const char *pv = getenv("B2SR_PULL");  // "warp" = one warp per item, two warp loads per exit test (A/B)
-    bool warp_pull = pv && pv[0] == 'w';
+    // B2SR_PULL=group selects the sub-warp pull (measured slower: 21.8 vs
+    // 35.3 GTEPS in the s22 d=4 sweep, profiles/r01_pull_ab.txt)
+    const char *pv = getenv("B2SR_PULL");
+    bool warp_pull = !(pv && pv[0] == 'g');
 #define PULL_CASE(DD)                                                                                              \
     case DD:                                                                                                       \
         if (warp_pull)                                                                                             \
