@@ -142,6 +142,8 @@ struct b2sr_matrix {
     uint32_t *item_ofs = nullptr;     // ntr+1: first work item of each tile row (with `items`)
     uint32_t *long_rows = nullptr;    // tile rows handled by the CTA-per-row float gather
     uint32_t n_long = 0;
+    uint32_t long_lo = 0;             // rows longer than this leave the group-per-row gather
+    void *vlong = nullptr;            // segmented plan for the very longest rows (bmv_vlong.cu)
 };
 
 namespace b2sr {
@@ -156,6 +158,10 @@ void ensure_items(b2sr_matrix *m, cudaStream_t s);  // bin-SpMV work partition
 int num_sms();
 void launch_row_ids(const b2sr_matrix *m, uint32_t *rowid, cudaStream_t s);  // rowid[t] = tile row of t
 void free_plan(void *plan);
+void free_vlong(void *plan);
+void *build_vlong(b2sr_matrix *m, uint32_t thresh, cudaStream_t s);
+void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
+                  cudaStream_t s);
 // blocked bin-SpMV: mode 0 = masked bbb, 1 = BFS pull; false if not applicable
 bool launch_blocked(b2sr_matrix *m, int mode, const void *x, const void *keep, void *y, cudaStream_t s);
 // B2SR_BLOCKED=1 selects the column-strip blocked kernels (A/B measurements)

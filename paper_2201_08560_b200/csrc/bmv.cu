@@ -344,9 +344,14 @@ __global__ void __launch_bounds__(256) k_bmv_bff(uint32_t ntr, uint32_t n, const
 constexpr uint32_t LONG_ROW_TILES = 512;
 constexpr int LONG_THREADS = 256;
 
-__global__ void k_find_long(uint32_t ntr, const uint32_t *trp, uint32_t thresh, uint32_t *rows, uint32_t *count) {
-    for (uint32_t I = blockIdx.x * blockDim.x + threadIdx.x; I < ntr; I += gridDim.x * blockDim.x)
-        if (trp[I + 1] - trp[I] > thresh) rows[atomicAdd(count, 1u)] = I;
+constexpr uint32_t VLONG_ROW_TILES = 16384;  // longer rows: bmv_vlong.cu (segmented scatter + fold)
+
+__global__ void k_find_long(uint32_t ntr, const uint32_t *trp, uint32_t lo, uint32_t hi, uint32_t *rows,
+                            uint32_t *count) {
+    for (uint32_t I = blockIdx.x * blockDim.x + threadIdx.x; I < ntr; I += gridDim.x * blockDim.x) {
+        uint32_t len = trp[I + 1] - trp[I];
+        if (len > lo && len <= hi) rows[atomicAdd(count, 1u)] = I;
+    }
 }
 
 void ensure_long_rows(b2sr_matrix *m, cudaStream_t s) {
@@ -354,8 +359,14 @@ void ensure_long_rows(b2sr_matrix *m, cudaStream_t s) {
     Buf<uint32_t> rows(m->ntr, s), cnt(1, s);
     CK(cudaMemsetAsync(cnt.p, 0, 4, s));
     unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((m->ntr + 255) / 256, (uint64_t)num_sms() * 16));
-    LAUNCH(k_find_long, g, 256, 0, s, m->ntr, m->trp, LONG_ROW_TILES, rows.p, cnt.p);
+    // thresholds are fixed per matrix when its plan is built; the env overrides
+    // exist so parity tests can push small matrices through all three paths
+    const char *el = getenv("B2SR_LONG_TILES"), *ev = getenv("B2SR_VLONG_TILES");
+    uint32_t lo = el ? (uint32_t)atoi(el) : LONG_ROW_TILES, hi = ev ? (uint32_t)atoi(ev) : VLONG_ROW_TILES;
+    m->long_lo = lo;
+    LAUNCH(k_find_long, g, 256, 0, s, m->ntr, m->trp, lo, hi, rows.p, cnt.p);
     m->n_long = read_scalar(cnt.p, s);
+    m->vlong = build_vlong(m, hi, s);
     m->long_rows = rows.release();
 }
 
@@ -588,7 +599,7 @@ static void bff_ring(const b2sr_matrix *m, const double *x, int ring, double inc
 #define BFF_RING(RR)                                                                                              \
     do {                                                                                                          \
         LAUNCH((k_bmv_bff<D, RR>), g, 256, 0, s, m->ntr, m->n, m->trp, m->tci, tl, x, inc, keep, y, m->row0,      \
-               LONG_ROW_TILES);                                                                                   \
+               m->long_lo);                                                                                       \
         LAUNCH((k_bmv_bff_long<D, RR>), gl, LONG_THREADS, 0, s, m->n_long, m->long_rows, m->n, m->trp, m->tci,   \
                tl, x, inc, keep, y, m->row0);                                                                     \
     } while (0)
@@ -596,6 +607,7 @@ static void bff_ring(const b2sr_matrix *m, const double *x, int ring, double inc
     else if (ring == B2SR_RING_MINPLUS) BFF_RING(B2SR_RING_MINPLUS);
     else BFF_RING(B2SR_RING_MAXTIMES);
 #undef BFF_RING
+    launch_vlong(const_cast<b2sr_matrix *>(m), x, ring, inc, keep, y, s);
 }
 
 void launch_bff(const b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,

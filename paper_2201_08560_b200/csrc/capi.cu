@@ -98,6 +98,7 @@ void free_matrix(b2sr_matrix *m) {
     dfree(m->live, nullptr);
     dfree(m->item_ofs, nullptr);
     dfree(m->long_rows, nullptr);
+    free_vlong(m->vlong);
     free_plan(m->plan);
     if (cur != m->device) cudaSetDevice(cur);
     delete m;
