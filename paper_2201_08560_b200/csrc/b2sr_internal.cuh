@@ -144,6 +144,8 @@ struct b2sr_matrix {
     uint32_t n_long = 0;
     uint32_t long_lo = 0;             // rows longer than this leave the group-per-row gather
     void *vlong = nullptr;            // segmented plan for the very longest rows (bmv_vlong.cu)
+    void *hot = nullptr;              // hot-column x cache plan (hot.cu)
+    void *stream = nullptr;           // flat tile-stream row hints (bmv_stream.cu)
 };
 
 namespace b2sr {
@@ -162,6 +164,22 @@ void free_vlong(void *plan);
 void *build_vlong(b2sr_matrix *m, uint32_t thresh, cudaStream_t s);
 void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
                   cudaStream_t s);
+// hot.cu: the S most referenced tile columns' x words live in shared memory
+constexpr uint32_t HOT_SMEM_BYTES = 196608;
+struct HotView {
+    uint32_t S;               // slots; tci2 values < S are slots, others S + column
+    const uint32_t *cols;     // slot -> tile column (null: identity)
+    const uint32_t *tci2;     // remapped tile-column indices
+};
+HotView hot_view(b2sr_matrix *m, cudaStream_t s);
+void free_hot(void *plan);
+size_t hot_fill_bytes(const HotView &hv, int dim);
+void hot_fill(const HotView &hv, int dim, const void *x, void *hx, cudaStream_t s);
+bool hot_enabled(int dim);
+// bmv_stream.cu: flat tile-stream K4 (d = 4, 8)
+bool stream_enabled(int dim);
+void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaStream_t s);
+void free_stream(void *plan);
 // blocked bin-SpMV: mode 0 = masked bbb, 1 = BFS pull; false if not applicable
 bool launch_blocked(b2sr_matrix *m, int mode, const void *x, const void *keep, void *y, cudaStream_t s);
 // B2SR_BLOCKED=1 selects the column-strip blocked kernels (A/B measurements)

@@ -86,9 +86,9 @@ struct LaneTiles {
     uint32_t xw[Geo<D>::TPL]; // x word per tile (0 when invalid)
 };
 
-template <int D, int XG = 0>
+template <int D, class GX>
 __device__ __forceinline__ void load_lane(const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
-                                          const void *__restrict__ x, uint32_t base, uint32_t t0, uint32_t t1,
+                                          const GX &gx, uint32_t base, uint32_t t0, uint32_t t1,
                                           uint32_t lane, LaneTiles<D> &lt) {
     using G = Geo<D>;
     if constexpr (G::TPL > 1) {
@@ -106,14 +106,14 @@ __device__ __forceinline__ void load_lane(const uint8_t *__restrict__ tiles, con
 #pragma unroll
         for (int j = 0; j < G::TPL; j++) {
             bool ok = tl + j >= t0 && tl + j < t1;
-            lt.xw[j] = ok ? load_x<D, XG>(x, cols[j]) : 0u;
+            lt.xw[j] = ok ? gx(cols[j]) : 0u;
         }
     } else {
         uint32_t t = base + lane / G::LPT;
         uint32_t q = lane % G::LPT;
         bool ok = t < t1;
         lt.v = ok ? ld_stream128(tiles + (size_t)t * G::TB + q * 16) : make_uint4(0, 0, 0, 0);
-        lt.xw[0] = ok ? load_x<D, XG>(x, __ldg(tci + t)) : 0u;
+        lt.xw[0] = ok ? gx(__ldg(tci + t)) : 0u;
     }
 }
 
@@ -124,11 +124,11 @@ __device__ __forceinline__ uint32_t lane_hits(const LaneTiles<D> &lt, uint32_t l
 }
 
 // ------------------------------------------------------------ K4 bbb
-template <int D, int XG>
-__global__ void __launch_bounds__(256) k_bmv_bbb(const WorkItem *__restrict__ items, uint32_t n_items,
-                                                 const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
-                                                 const void *__restrict__ x, const void *__restrict__ keep,
-                                                 void *__restrict__ y, uint32_t row0) {
+template <int D, class GX>
+__device__ __forceinline__ void bbb_items(const WorkItem *__restrict__ items, uint32_t n_items,
+                                          const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
+                                          const GX &gx, const void *__restrict__ keep, void *__restrict__ y,
+                                          uint32_t row0) {
     using G = Geo<D>;
     const uint32_t lane = lane_id();
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
@@ -140,13 +140,13 @@ __global__ void __launch_bounds__(256) k_bmv_bbb(const WorkItem *__restrict__ it
         // two warp loads in flight per iteration
         for (; base + G::TPW < it.t1; base += 2 * G::TPW) {
             LaneTiles<D> a, b;
-            load_lane<D, XG>(tiles, tci, x, base, it.t0, it.t1, lane, a);
-            load_lane<D, XG>(tiles, tci, x, base + G::TPW, it.t0, it.t1, lane, b);
+            load_lane<D>(tiles, tci, gx, base, it.t0, it.t1, lane, a);
+            load_lane<D>(tiles, tci, gx, base + G::TPW, it.t0, it.t1, lane, b);
             acc |= lane_hits<D>(a, lane) | lane_hits<D>(b, lane);
         }
         if (base < it.t1) {
             LaneTiles<D> a;
-            load_lane<D, XG>(tiles, tci, x, base, it.t0, it.t1, lane, a);
+            load_lane<D>(tiles, tci, gx, base, it.t0, it.t1, lane, a);
             acc |= lane_hits<D>(a, lane);
         }
         acc = __reduce_or_sync(0xffffffffu, acc);
@@ -160,6 +160,33 @@ __global__ void __launch_bounds__(256) k_bmv_bbb(const WorkItem *__restrict__ it
             }
         }
     }
+}
+
+template <int D, int XG>
+__global__ void __launch_bounds__(256) k_bmv_bbb(const WorkItem *__restrict__ items, uint32_t n_items,
+                                                 const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
+                                                 const void *__restrict__ x, const void *__restrict__ keep,
+                                                 void *__restrict__ y, uint32_t row0) {
+    bbb_items<D>(items, n_items, tiles, tci, XGlobal<D, XG>{x}, keep, y, row0);
+}
+
+// Hot-column variant: one 1024-thread CTA per SM, the hot x words in shared
+// memory (hot.cu), tci2 = remapped tile-column indices.
+constexpr int HOT_THREADS = 1024;
+
+template <int D>
+__global__ void __launch_bounds__(HOT_THREADS, 1) k_bmv_bbb_hot(const WorkItem *__restrict__ items, uint32_t n_items,
+                                                               const uint8_t *__restrict__ tiles,
+                                                               const uint32_t *__restrict__ tci2,
+                                                               const void *__restrict__ hx, uint32_t hx_bytes16,
+                                                               uint32_t S, const void *__restrict__ x,
+                                                               const void *__restrict__ keep, void *__restrict__ y,
+                                                               uint32_t row0) {
+    extern __shared__ uint4 hot_smem[];
+    stage_hot(hot_smem, hx, hx_bytes16);
+    __syncthreads();
+    XHot<D> gx{reinterpret_cast<const typename WordT<D>::T *>(hot_smem), x, S};
+    bbb_items<D>(items, n_items, tiles, tci2, gx, keep, y, row0);
 }
 
 // ------------------------------------------------------------ K5 bbf
@@ -216,14 +243,14 @@ __global__ void __launch_bounds__(256) k_bmv_bbf(const WorkItem *__restrict__ it
         uint32_t base = start;
         for (; base + G::TPW < it.t1; base += 2 * G::TPW) {
             LaneTiles<D> a, b;
-            load_lane<D>(tiles, tci, x, base, it.t0, it.t1, lane, a);
-            load_lane<D>(tiles, tci, x, base + G::TPW, it.t0, it.t1, lane, b);
+            load_lane<D>(tiles, tci, XGlobal<D>{x}, base, it.t0, it.t1, lane, a);
+            load_lane<D>(tiles, tci, XGlobal<D>{x}, base + G::TPW, it.t0, it.t1, lane, b);
             lane_counts<D>(a, c);
             lane_counts<D>(b, c);
         }
         if (base < it.t1) {
             LaneTiles<D> a;
-            load_lane<D>(tiles, tci, x, base, it.t0, it.t1, lane, a);
+            load_lane<D>(tiles, tci, XGlobal<D>{x}, base, it.t0, it.t1, lane, a);
             lane_counts<D>(a, c);
         }
         // reduce lanes that cover the same rows, then lane i takes row i
@@ -540,12 +567,41 @@ int64_t prescale(const b2sr_matrix *m, const double *x, const double *scale, dou
 }
 
 // ------------------------------------------------------------ launchers
+unsigned hot_grid(uint64_t n_items) {
+    uint64_t b = (n_items + HOT_THREADS / 32 - 1) / (HOT_THREADS / 32);
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(b, (uint64_t)num_sms()));
+}
+
 void launch_bbb(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaStream_t s) {
     if (blocked_enabled() && launch_blocked(m, 0, x, keep, y, s)) return;
+    if (stream_enabled(m->dim)) {
+        launch_bbb_stream(m, x, keep, y, s);
+        return;
+    }
     ensure_items(m, s);
     if (m->any_split) CK(cudaMemsetAsync(y, 0, padded_vec_bytes(m->ntr, m->dim), s));
-    unsigned g = item_grid(m);
     const uint8_t *tl = (const uint8_t *)m->tiles;
+    if (hot_enabled(m->dim)) {
+        HotView hv = hot_view(m, s);
+        size_t hb = hot_fill_bytes(hv, m->dim);
+        Buf<uint8_t> hx(hb, s);
+        hot_fill(hv, m->dim, x, hx.p, s);
+        unsigned g = hot_grid(m->n_items);
+#define HOT_CASE(DD)                                                                                              \
+    case DD:                                                                                                      \
+        hot_smem_attr(k_bmv_bbb_hot<DD>, hb);                                                                     \
+        LAUNCH(k_bmv_bbb_hot<DD>, g, HOT_THREADS, hb, s, m->items, m->n_items, tl, hv.tci2, hx.p, (uint32_t)hb,   \
+               hv.S, x, keep, y, m->row0);                                                                        \
+        break;
+        switch (m->dim) {
+            HOT_CASE(4)
+            HOT_CASE(8)
+            HOT_CASE(16)
+        }
+#undef HOT_CASE
+        return;
+    }
+    unsigned g = item_grid(m);
     const char *xg_env = getenv("B2SR_XGATHER");  // cache policy of the x gathers (A/B)
     int xg = xg_env ? atoi(xg_env) : 0;
 #define BBB_LAUNCH(DD, XX) \

@@ -1,6 +1,8 @@
 // Shared device helpers of the bin-SpMV family (bmv.cu, bmv_blocked.cu, drivers.cu).
 #pragma once
 
+#include <algorithm>
+
 #include "b2sr_internal.cuh"
 
 namespace b2sr {
@@ -63,6 +65,49 @@ __device__ __forceinline__ uint32_t hits16(uint4 v, const uint32_t *xw, uint32_t
         a |= (v.w & x) ? 8u : 0u;
         return a << (4 * (lane & 7));
     }
+}
+
+// Raise a kernel's dynamic shared-memory limit (idempotent, cheap).
+void hot_smem_attr_raw(const void *kernel, size_t bytes);  // hot.cu: per-kernel, cached
+template <typename K>
+inline void hot_smem_attr(K kernel, size_t bytes) {
+    hot_smem_attr_raw(reinterpret_cast<const void *>(kernel), bytes);
+}
+unsigned hot_grid(uint64_t n_items);  // one 1024-thread CTA per SM at most
+
+// x-word gathers used by the streaming kernels: plain global loads with a
+// selectable cache policy, or the hot-column cache (hot.cu) in shared memory
+template <int D, int XG = 0>
+struct XGlobal {
+    const void *x;
+    __device__ __forceinline__ uint32_t operator()(uint32_t c) const { return load_x<D, XG>(x, c); }
+};
+template <int D>
+struct XHot {
+    const typename WordT<D>::T *sx;  // S hot words in shared memory
+    const void *x;                   // the full vector (cold columns)
+    uint32_t S;
+    __device__ __forceinline__ uint32_t operator()(uint32_t c) const {
+        return c < S ? (uint32_t)sx[c] : load_word<D>(x, c - S);
+    }
+};
+
+// Copy the hot words (hot_fill output, 16-byte padded) into shared memory;
+// all threads of the CTA take part, the caller syncs.
+__device__ __forceinline__ void stage_hot(void *smem, const void *hx, uint32_t bytes16) {
+    const uint4 *src = static_cast<const uint4 *>(hx);
+    uint4 *dst = static_cast<uint4 *>(smem);
+    const uint32_t n = bytes16 / 16;
+    uint32_t i = threadIdx.x;
+    for (; i + 3 * blockDim.x < n; i += 4 * blockDim.x) {
+        uint4 a = __ldg(src + i), b = __ldg(src + i + blockDim.x), c = __ldg(src + i + 2 * blockDim.x),
+              d = __ldg(src + i + 3 * blockDim.x);
+        dst[i] = a;
+        dst[i + blockDim.x] = b;
+        dst[i + 2 * blockDim.x] = c;
+        dst[i + 3 * blockDim.x] = d;
+    }
+    for (; i < n; i += blockDim.x) dst[i] = __ldg(src + i);
 }
 
 }  // namespace b2sr

@@ -1,0 +1,309 @@
+// K4 bbb as a flat tile stream (d = 4, 8) -- replaces kernels.py:97-115, 219-225.
+//
+// The work-item kernel (bmv.cu) gives every warp one tile row at a time, so a
+// warp has a single row's loads in flight and the chain item -> tiles/tci ->
+// x gather -> store is paid once per row; with ~120 tiles per tile row at R-MAT
+// s22 d=4 that is one 128-bit warp load per chain.  Here the tile array is cut
+// into warp loads of TPW tiles (128 at d=4, 64 at d=8) and each warp streams a
+// contiguous range of them with the next loads already in flight, independent
+// of row boundaries:
+//   * the row of every tile is recovered from a per-load row hint (lrow[k] =
+//     tile row holding tile k*TPW, built once per matrix) plus a short search
+//     in tile_row_ptr (only when the load crosses a row boundary);
+//   * per-tile hit words are OR-combined per row with a segmented warp scan
+//     (rows are non-decreasing along the lanes) and stored with one atomicOr
+//     per (row, load) -- OR is order-independent, so the bits are exactly the
+//     reference's;
+//   * x words come from the hot-column cache in shared memory (hot.cu) or, for
+//     cold columns, from L1/L2.
+#include "bmv_common.cuh"
+
+namespace b2sr {
+
+constexpr int STREAM_THREADS = 1024;
+constexpr uint32_t SPAN = 7;  // row boundaries a load descriptor carries (more: searched)
+
+// One descriptor per warp load k (tiles [k*TPW, (k+1)*TPW)):
+//   x = ra, the tile row holding tile k*TPW;
+//   y, z = byte i: offset inside the load where row ra+1+i starts (i < span),
+//          0xFF when unused; the row of the tile at offset p is
+//          ra + #{i : off[i] <= p} (empty rows are counted, so rows line up);
+//   w = span (number of boundaries, 0 = the load lies in one row); span > SPAN
+//       loads search tile_row_ptr instead (x of descriptor k+1 bounds them).
+struct StreamPlan {
+    uint32_t n_loads = 0;
+    uint4 *desc = nullptr;  // n_loads + 1 (the last only carries the row of tile T-1)
+};
+
+void free_stream(void *p) {
+    StreamPlan *sp = static_cast<StreamPlan *>(p);
+    if (!sp) return;
+    dfree(sp->desc, nullptr);
+    delete sp;
+}
+
+__device__ __forceinline__ uint32_t row_of(const uint32_t *__restrict__ trp, uint32_t lo, uint32_t hi, uint64_t t) {
+    while (lo < hi) {  // largest r in [lo, hi] with trp[r] <= t
+        uint32_t mid = lo + (hi - lo + 1) / 2;
+        if (trp[mid] <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void k_stream_desc(uint32_t n_loads, uint32_t tpw, uint64_t T, uint32_t ntr, const uint32_t *__restrict__ trp,
+                              uint4 *__restrict__ desc) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= n_loads; k += gridDim.x * blockDim.x) {
+        uint64_t t = std::min<uint64_t>((uint64_t)k * tpw, T - 1);
+        uint32_t ra = row_of(trp, 0, ntr - 1, t);
+        uint4 o = make_uint4(ra, 0xFFFFFFFFu, 0xFFFFFFFFu, 0);
+        if (k < n_loads) {
+            uint64_t tn = std::min<uint64_t>((uint64_t)(k + 1) * tpw, T - 1);
+            uint32_t rb = row_of(trp, ra, ntr - 1, tn), span = rb - ra;
+            o.w = span;
+            if (span <= SPAN) {
+                for (uint32_t i = 0; i < span; i++) {
+                    uint32_t off = (uint32_t)(trp[ra + 1 + i] - (uint64_t)k * tpw);  // 1..tpw
+                    if (i < 4) o.y = (o.y & ~(0xFFu << (8 * i))) | (off << (8 * i));
+                    else o.z = (o.z & ~(0xFFu << (8 * (i - 4)))) | (off << (8 * (i - 4)));
+                }
+            }
+        }
+        desc[k] = o;
+    }
+}
+
+static StreamPlan *stream_plan(b2sr_matrix *m, uint32_t tpw, cudaStream_t s) {
+    if (!m->stream) {
+        StreamPlan *sp = new StreamPlan();
+        sp->n_loads = (uint32_t)((m->num_tiles + tpw - 1) / tpw);
+        try {
+            Buf<uint4> desc((size_t)sp->n_loads + 65, s);  // + 64: the warps read descriptors 64 ahead
+            CK(cudaMemsetAsync(desc.p, 0, ((size_t)sp->n_loads + 65) * 16, s));
+            unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((sp->n_loads + 256) / 256, (uint64_t)num_sms() * 16));
+            LAUNCH(k_stream_desc, g, 256, 0, s, sp->n_loads, tpw, m->num_tiles, m->ntr, m->trp, desc.p);
+            sp->desc = desc.release();
+        } catch (...) {
+            free_stream(sp);
+            throw;
+        }
+        m->stream = sp;
+    }
+    return static_cast<StreamPlan *>(m->stream);
+}
+
+// Raw masked words of a lane's tiles: byte r (row r) is non-zero iff the
+// row hits.  d=4: one u32 per tile; d=8: two (rows 0-3, rows 4-7).
+template <int D> struct Masked;
+template <> struct Masked<4> {
+    uint32_t m[4];
+    __device__ __forceinline__ void set(const uint4 &v, const uint32_t (&xw)[4]) {
+        m[0] = v.x & (xw[0] * 0x01010101u);
+        m[1] = v.y & (xw[1] * 0x01010101u);
+        m[2] = v.z & (xw[2] * 0x01010101u);
+        m[3] = v.w & (xw[3] * 0x01010101u);
+    }
+    __device__ __forceinline__ uint32_t all() const { return m[0] | m[1] | m[2] | m[3]; }   // raw OR
+    __device__ __forceinline__ static uint32_t hits(uint32_t raw) { return nz_nibble_bytes(raw); }
+    __device__ __forceinline__ uint32_t tile(int j) const { return nz_nibble_bytes(m[j]); }
+};
+template <> struct Masked<8> {
+    uint32_t lo[2], hi[2];
+    __device__ __forceinline__ void set(const uint4 &v, const uint32_t (&xw)[2]) {
+        uint32_t a = xw[0] * 0x01010101u, b = xw[1] * 0x01010101u;
+        lo[0] = v.x & a; hi[0] = v.y & a;
+        lo[1] = v.z & b; hi[1] = v.w & b;
+    }
+    __device__ __forceinline__ uint32_t tile(int j) const { return nz_bytes(lo[j]) | (nz_bytes(hi[j]) << 4); }
+};
+
+template <int D>
+__device__ __forceinline__ void or_row(void *__restrict__ y, uint32_t row, uint32_t acc) {
+    if (acc) atomic_or_word<D>(y, row, acc);
+}
+
+// rows of offsets p (0..TPW-1) relative to ra: #{i : off[i] <= p}
+__device__ __forceinline__ uint32_t rel_row(uint32_t p, uint32_t oa, uint32_t ob) {
+    uint32_t pp = p * 0x01010101u;
+    return (__popc(__vcmpgeu4(pp, oa)) + __popc(__vcmpgeu4(pp, ob))) >> 3;
+}
+
+template <int D, class GX>
+__device__ __forceinline__ void bbb_stream(uint32_t k0, uint32_t k1, uint64_t T, const uint4 *__restrict__ desc,
+                                           const uint32_t *__restrict__ trp, const uint8_t *__restrict__ tiles,
+                                           const uint32_t *__restrict__ tci, const GX &gx, void *__restrict__ y) {
+    using G = Geo<D>;
+    constexpr int TPL = G::TPL;          // tiles per lane: 4 (d=4) or 2 (d=8)
+    constexpr uint32_t TPW = G::TPW;     // tiles per warp load: 128 / 64
+    constexpr int SPW = 32 / D;          // packed D-bit row slots per u32: 8 / 4
+    constexpr int NW = (SPAN + 1 + SPW - 1) / SPW;  // accumulator words: 1 / 2
+    const uint32_t lane = lane_id();
+    struct Stage {
+        uint4 v;
+        uint32_t c[TPL], x[TPL];
+    };
+    auto issue = [&](uint32_t k, Stage &st) {
+        uint64_t t = (uint64_t)k * TPW + lane * TPL;
+        bool ok = k < k1 && t < T;
+        st.v = ok ? ld_stream128(tiles + t * G::TB) : make_uint4(0, 0, 0, 0);
+        if constexpr (TPL == 4) {
+            uint4 q = ok ? ld_stream128(tci + t) : make_uint4(0, 0, 0, 0);
+            st.c[0] = q.x; st.c[1] = q.y; st.c[2] = q.z; st.c[3] = q.w;
+        } else {
+            uint2 q = ok ? *reinterpret_cast<const uint2 *>(tci + t) : make_uint2(0, 0);
+            st.c[0] = q.x; st.c[1] = q.y;
+        }
+    };
+    auto gather = [&](uint32_t k, Stage &st) {
+        uint64_t t = (uint64_t)k * TPW + lane * TPL;
+        if (k < k1 && t + TPL <= T) {
+#pragma unroll
+            for (int j = 0; j < TPL; j++) st.x[j] = gx(st.c[j]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < TPL; j++) st.x[j] = (k < k1 && t + j < T) ? gx(st.c[j]) : 0u;
+        }
+    };
+    uint4 dcur = __ldg(desc + k0 + lane), dnxt = __ldg(desc + k0 + 32 + lane);  // desc has 64 entries of slack
+    auto compute = [&](uint32_t k, const Stage &st) {
+        const uint32_t i = (k - k0) & 31u;
+        if (i == 0 && k != k0) {
+            dcur = dnxt;
+            dnxt = __ldg(desc + k + 32 + lane);
+        }
+        const uint32_t ra = __shfl_sync(0xffffffffu, dcur.x, i);
+        const uint32_t span = __shfl_sync(0xffffffffu, dcur.w, i);
+        Masked<D> mk;
+        mk.set(st.v, st.x);
+        if (span == 0) {  // the whole load lies in one row
+            uint32_t acc;
+            if constexpr (D == 4) {
+                acc = __reduce_or_sync(0xffffffffu, mk.all());
+                if (lane == 0) or_row<D>(y, ra, Masked<4>::hits(acc));
+            } else {
+                acc = __reduce_or_sync(0xffffffffu, mk.tile(0) | mk.tile(1));
+                if (lane == 0) or_row<D>(y, ra, acc);
+            }
+        } else if (span <= SPAN) {
+            const uint32_t oa = __shfl_sync(0xffffffffu, dcur.y, i), ob = __shfl_sync(0xffffffffu, dcur.z, i);
+            const uint32_t qa = rel_row(lane * TPL, oa, ob), qb = rel_row(lane * TPL + TPL - 1, oa, ob);
+            uint32_t acc[NW];
+#pragma unroll
+            for (int u = 0; u < NW; u++) acc[u] = 0;
+            if (qa == qb) {  // the lane's tiles share one row
+                uint32_t h;
+                if constexpr (D == 4) h = Masked<4>::hits(mk.all());
+                else h = mk.tile(0) | mk.tile(1);
+#pragma unroll
+                for (int u = 0; u < NW; u++) acc[u] = (qa / SPW == (uint32_t)u) ? h << (D * (qa % SPW)) : 0u;
+            } else {
+#pragma unroll
+                for (int j = 0; j < TPL; j++) {
+                    uint32_t q = rel_row(lane * TPL + j, oa, ob), h = mk.tile(j);
+#pragma unroll
+                    for (int u = 0; u < NW; u++) acc[u] |= (q / SPW == (uint32_t)u) ? h << (D * (q % SPW)) : 0u;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < NW; u++) acc[u] = __reduce_or_sync(0xffffffffu, acc[u]);
+            if (lane <= span) {
+                uint32_t a = 0;
+#pragma unroll
+                for (int u = 0; u < NW; u++) a |= (lane / SPW == (uint32_t)u) ? acc[u] : 0u;
+                or_row<D>(y, ra + lane, (a >> (D * (lane % SPW))) & ((1u << D) - 1u));
+            }
+        } else {
+            // many short rows: search trp[ra..rb] per tile and write per tile
+            const uint32_t rb = i < 31 ? __shfl_sync(0xffffffffu, dcur.x, i + 1) : __shfl_sync(0xffffffffu, dnxt.x, 0);
+            const uint64_t t0 = (uint64_t)k * TPW + lane * TPL;
+#pragma unroll
+            for (int j = 0; j < TPL; j++) {
+                uint32_t h = mk.tile(j);
+                if (h) or_row<D>(y, row_of(trp, ra, rb, t0 + j), h);
+            }
+        }
+    };
+    if (k0 >= k1) return;
+    // two-stage pipeline, unrolled so the stages never move: while load k is
+    // reduced, the x gathers of k+1 are in flight; then the tiles of k+2 issue
+    Stage A, B;
+    issue(k0, A);
+    gather(k0, A);
+    issue(k0 + 1, B);
+    for (uint32_t k = k0; k < k1; k += 2) {
+        gather(k + 1, B);
+        compute(k, A);
+        issue(k + 2, A);
+        if (k + 1 >= k1) break;
+        gather(k + 2, A);
+        compute(k + 1, B);
+        issue(k + 3, B);
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(STREAM_THREADS, 1)
+    k_bmv_bbb_stream(uint32_t n_loads, uint64_t T, const uint4 *__restrict__ desc, const uint32_t *__restrict__ trp,
+                     const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci2, const void *__restrict__ hx,
+                     uint32_t hx_bytes16, uint32_t S, const void *__restrict__ x, void *__restrict__ y) {
+    extern __shared__ uint4 hot_smem[];
+    stage_hot(hot_smem, hx, hx_bytes16);
+    __syncthreads();
+    XHot<D> gx{reinterpret_cast<const typename WordT<D>::T *>(hot_smem), x, S};
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5, w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t per = (n_loads + warps - 1) / warps;
+    const uint32_t k0 = std::min(n_loads, w * per), k1 = std::min(n_loads, k0 + per);
+    bbb_stream<D>(k0, k1, T, desc, trp, tiles, tci2, gx, y);
+}
+
+// y &= keep (keep is indexed by global tile row: row0 offsets it for row blocks)
+__global__ void k_and_words(uint32_t nw, uint32_t *__restrict__ y, const uint32_t *__restrict__ keep) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x) y[i] &= keep[i];
+}
+__global__ void k_and_bytes(uint32_t nb, uint8_t *__restrict__ y, const uint8_t *__restrict__ keep) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) y[i] &= keep[i];
+}
+
+bool stream_enabled(int dim) {
+    const char *e = getenv("B2SR_STREAM");  // B2SR_STREAM=0: work-item kernel (A/B)
+    if (e && e[0] == '0') return false;
+    return (dim == 4 || dim == 8) && hot_enabled(dim);
+}
+
+void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaStream_t s) {
+    const size_t yb = padded_vec_bytes(m->ntr, m->dim);
+    CK(cudaMemsetAsync(y, 0, yb, s));
+    if (!m->num_tiles) return;
+    const uint32_t tpw = m->dim == 4 ? Geo<4>::TPW : Geo<8>::TPW;
+    StreamPlan *sp = stream_plan(m, tpw, s);
+    HotView hv = hot_view(m, s);
+    size_t hb = hot_fill_bytes(hv, m->dim);
+    Buf<uint8_t> hx(hb, s);
+    hot_fill(hv, m->dim, x, hx.p, s);
+    unsigned g = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t)num_sms(), ((uint64_t)sp->n_loads + 31) / 32));
+    const uint8_t *tl = (const uint8_t *)m->tiles;
+    if (m->dim == 4) {
+        hot_smem_attr(k_bmv_bbb_stream<4>, hb);
+        LAUNCH(k_bmv_bbb_stream<4>, g, STREAM_THREADS, hb, s, sp->n_loads, m->num_tiles, sp->desc, m->trp, tl, hv.tci2,
+               hx.p, (uint32_t)hb, hv.S, x, y);
+    } else {
+        hot_smem_attr(k_bmv_bbb_stream<8>, hb);
+        LAUNCH(k_bmv_bbb_stream<8>, g, STREAM_THREADS, hb, s, sp->n_loads, m->num_tiles, sp->desc, m->trp, tl, hv.tci2,
+               hx.p, (uint32_t)hb, hv.S, x, y);
+    }
+    if (keep) {  // masked variant: the keep words are applied once at the end (kernels.py:219-225)
+        const uint8_t *kp = static_cast<const uint8_t *>(keep) + (size_t)m->row0 * word_bytes(m->dim);
+        if (((uintptr_t)kp & 3) == 0) {
+            const uint32_t kw = (uint32_t)(yb / 4);
+            unsigned gk = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((kw + 255) / 256, (uint64_t)num_sms() * 8));
+            LAUNCH(k_and_words, gk, 256, 0, s, kw, (uint32_t *)y, (const uint32_t *)kp);
+        } else {
+            const uint32_t nb = (uint32_t)((size_t)m->ntr * word_bytes(m->dim));
+            unsigned gk = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nb + 255) / 256, (uint64_t)num_sms() * 8));
+            LAUNCH(k_and_bytes, gk, 256, 0, s, nb, (uint8_t *)y, kp);
+        }
+    }
+}
+
+}  // namespace b2sr

@@ -100,6 +100,8 @@ void free_matrix(b2sr_matrix *m) {
     dfree(m->long_rows, nullptr);
     free_vlong(m->vlong);
     free_plan(m->plan);
+    free_hot(m->hot);
+    free_stream(m->stream);
     if (cur != m->device) cudaSetDevice(cur);
     delete m;
 }

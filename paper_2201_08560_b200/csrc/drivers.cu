@@ -37,9 +37,9 @@ template <int D> using BGeo = Geo<D>;
 
 // hit bits (row-word positions) of the tiles this lane covers; the payload
 // is only fetched for tiles whose frontier word is non-zero
-template <int D>
+template <int D, class GX>
 __device__ __forceinline__ uint32_t bfs_lane(const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
-                                             const void *__restrict__ x, uint32_t base, uint32_t t0, uint32_t t1,
+                                             const GX &gx, uint32_t base, uint32_t t0, uint32_t t1,
                                              uint32_t lane) {
     using G = BGeo<D>;
     if constexpr (G::TPL > 1) {
@@ -57,7 +57,7 @@ __device__ __forceinline__ uint32_t bfs_lane(const uint8_t *__restrict__ tiles, 
 #pragma unroll
         for (int j = 0; j < G::TPL; j++) {
             bool ok = tl + j >= t0 && tl + j < t1;
-            xw[j] = ok ? load_word<D>(x, cols[j]) : 0u;
+            xw[j] = ok ? gx(cols[j]) : 0u;
             anyx |= xw[j];
         }
         if (!anyx) return 0;
@@ -76,7 +76,7 @@ __device__ __forceinline__ uint32_t bfs_lane(const uint8_t *__restrict__ tiles, 
     } else {
         uint32_t t = base + lane / G::LPT, q = lane % G::LPT;
         if (t >= t1) return 0;
-        uint32_t xw = load_word<D>(x, __ldg(tci + t));
+        uint32_t xw = gx(__ldg(tci + t));
         if (!xw) return 0;
         uint4 v = ld_stream128(tiles + (size_t)t * G::TB + q * 16);
         if constexpr (D == 16) {
@@ -99,12 +99,12 @@ __device__ __forceinline__ uint32_t bfs_lane(const uint8_t *__restrict__ tiles, 
     }
 }
 
-template <int D>
-__global__ void __launch_bounds__(256) k_bfs_pull(const WorkItem *__restrict__ items, uint32_t n_items, uint32_t n,
-                                                  const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
-                                                  const void *__restrict__ frontier, const void *__restrict__ visited,
-                                                  const void *__restrict__ live, void *__restrict__ next, uint32_t row0,
-                                                  const uint32_t *__restrict__ idx, const uint32_t *__restrict__ idx_n) {
+template <int D, class GX>
+__device__ __forceinline__ void pull_items(const WorkItem *__restrict__ items, uint32_t n_items,
+                                           const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
+                                           const GX &gx, const void *__restrict__ visited,
+                                           const void *__restrict__ live, void *__restrict__ next, uint32_t row0,
+                                           const uint32_t *__restrict__ idx, const uint32_t *__restrict__ idx_n) {
     using G = BGeo<D>;
     const uint32_t lane = lane_id();
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
@@ -117,8 +117,8 @@ __global__ void __launch_bounds__(256) k_bfs_pull(const WorkItem *__restrict__ i
         uint32_t acc = 0;
         uint32_t base = G::TPL > 1 ? (it.t0 & ~(uint32_t)(G::TPL - 1)) : it.t0;
         for (; base < it.t1; base += 2 * G::TPW) {
-            acc |= bfs_lane<D>(tiles, tci, frontier, base, it.t0, it.t1, lane);
-            if (base + G::TPW < it.t1) acc |= bfs_lane<D>(tiles, tci, frontier, base + G::TPW, it.t0, it.t1, lane);
+            acc |= bfs_lane<D>(tiles, tci, gx, base, it.t0, it.t1, lane);
+            if (base + G::TPW < it.t1) acc |= bfs_lane<D>(tiles, tci, gx, base + G::TPW, it.t0, it.t1, lane);
             if ((__reduce_or_sync(0xffffffffu, acc) & keepw) == keepw) break;  // every unvisited row reached
         }
         acc = __reduce_or_sync(0xffffffffu, acc) & keepw;
@@ -127,6 +127,32 @@ __global__ void __launch_bounds__(256) k_bfs_pull(const WorkItem *__restrict__ i
             else reinterpret_cast<typename WordT<D>::T *>(next)[it.row] = (typename WordT<D>::T)acc;
         }
     }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_bfs_pull(const WorkItem *__restrict__ items, uint32_t n_items, uint32_t n,
+                                                  const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
+                                                  const void *__restrict__ frontier, const void *__restrict__ visited,
+                                                  const void *__restrict__ live, void *__restrict__ next, uint32_t row0,
+                                                  const uint32_t *__restrict__ idx, const uint32_t *__restrict__ idx_n) {
+    pull_items<D>(items, n_items, tiles, tci, XGlobal<D>{frontier}, visited, live, next, row0, idx, idx_n);
+}
+
+// hot-column variant (hot.cu): frontier words of the hot tile columns in smem
+constexpr int PULL_HOT_THREADS = 1024;
+
+template <int D>
+__global__ void __launch_bounds__(PULL_HOT_THREADS, 1)
+    k_bfs_pull_hot(const WorkItem *__restrict__ items, uint32_t n_items, const uint8_t *__restrict__ tiles,
+                   const uint32_t *__restrict__ tci2, const void *__restrict__ hx, uint32_t hx_bytes16, uint32_t S,
+                   const void *__restrict__ frontier, const void *__restrict__ visited, const void *__restrict__ live,
+                   void *__restrict__ next, uint32_t row0, const uint32_t *__restrict__ idx,
+                   const uint32_t *__restrict__ idx_n) {
+    extern __shared__ uint4 hot_smem[];
+    stage_hot(hot_smem, hx, hx_bytes16);
+    __syncthreads();
+    XHot<D> gx{reinterpret_cast<const typename WordT<D>::T *>(hot_smem), frontier, S};
+    pull_items<D>(items, n_items, tiles, tci2, gx, visited, live, next, row0, idx, idx_n);
 }
 
 // Sub-warp pull: a group of GS lanes per work item, GS*TPL/LPT tiles per step
@@ -156,7 +182,7 @@ __global__ void __launch_bounds__(256) k_bfs_pull_g(const WorkItem *__restrict__
         uint32_t acc = 0;
         uint32_t base = G::TPL > 1 ? (it.t0 & ~(uint32_t)(G::TPL - 1)) : it.t0;
         for (; base < it.t1; base += STEP) {
-            acc |= bfs_lane<D>(tiles, tci, frontier, base, it.t0, it.t1, gl);
+            acc |= bfs_lane<D>(tiles, tci, XGlobal<D>{frontier}, base, it.t0, it.t1, gl);
 #pragma unroll
             for (int o = GS / 2; o; o >>= 1) acc |= __shfl_xor_sync(gmask, acc, o);
             if ((acc & keepw) == keepw) break;  // every unvisited row of the tile row reached
@@ -434,6 +460,29 @@ void bfs_sweep(b2sr_matrix *at, const void *frontier, const void *visited, void 
     // 35.3 GTEPS in the s22 d=4 sweep, profiles/r01_pull_ab.txt)
     const char *pv = getenv("B2SR_PULL");
     bool warp_pull = !(pv && pv[0] == 'g');
+    const char *hs = getenv("B2SR_HOT_SPARSE");  // hot cache for active-list pulls too (A/B)
+    const char *hp = getenv("B2SR_HOT_PULL");    // hot-cache pull: 1024-thread CTAs (A/B, default off)
+    if (warp_pull && hp && hp[0] == '1' && hot_enabled(at->dim) && (!idx || (hs && hs[0] == '1'))) {
+        HotView hv = hot_view(at, s);
+        size_t hb = hot_fill_bytes(hv, at->dim);
+        Buf<uint8_t> hx(hb, s);
+        hot_fill(hv, at->dim, frontier, hx.p, s);
+        // active lists are short: size the grid by the full item count anyway
+        unsigned gh = hot_grid(at->n_items);
+#define PULL_HOT(DD)                                                                                               \
+    case DD:                                                                                                       \
+        hot_smem_attr(k_bfs_pull_hot<DD>, hb);                                                                     \
+        LAUNCH(k_bfs_pull_hot<DD>, gh, PULL_HOT_THREADS, hb, s, at->items, at->n_items, tl, hv.tci2, hx.p,         \
+               (uint32_t)hb, hv.S, frontier, visited, at->live, next, at->row0, idx, idx_n);                      \
+        break;
+        switch (at->dim) {
+            PULL_HOT(4)
+            PULL_HOT(8)
+            PULL_HOT(16)
+        }
+#undef PULL_HOT
+        return;
+    }
 #define PULL_CASE(DD)                                                                                              \
     case DD:                                                                                                       \
         if (warp_pull)                                                                                             \
