@@ -182,10 +182,9 @@ __global__ void __launch_bounds__(HOT_THREADS, 1) k_bmv_bbb_hot(const WorkItem *
                                                                uint32_t S, const void *__restrict__ x,
                                                                const void *__restrict__ keep, void *__restrict__ y,
                                                                uint32_t row0) {
-    extern __shared__ uint4 hot_smem[];
-    stage_hot(hot_smem, hx, hx_bytes16);
+    stage_hot(const_cast<uint8_t *>(hot_bytes()), hx, hx_bytes16);
     __syncthreads();
-    XHot<D> gx{reinterpret_cast<const typename WordT<D>::T *>(hot_smem), x, S};
+    XHot<D> gx(x, S);
     bbb_items<D>(items, n_items, tiles, tci2, gx, keep, y, row0);
 }
 

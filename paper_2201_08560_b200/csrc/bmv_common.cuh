@@ -82,13 +82,43 @@ struct XGlobal {
     const void *x;
     __device__ __forceinline__ uint32_t operator()(uint32_t c) const { return load_x<D, XG>(x, c); }
 };
+// The hot words live in the kernel's dynamic shared memory; indexing the
+// extern array directly lets ptxas address it with LDS immediates instead of
+// re-deriving a generic->shared pointer for every gather.
+__device__ __forceinline__ const uint8_t *hot_bytes() {
+    extern __shared__ uint4 hot_dyn_smem[];
+    return reinterpret_cast<const uint8_t *>(hot_dyn_smem);
+}
+
 template <int D>
 struct XHot {
-    const typename WordT<D>::T *sx;  // S hot words in shared memory
-    const void *x;                   // the full vector (cold columns)
+    uint32_t sbase;                        // shared-window address of the hot words
+    const typename WordT<D>::T *xm;        // x - S: cold column c (>= S) reads xm[c]
     uint32_t S;
+    __device__ __forceinline__ XHot(const void *x, uint32_t s)
+        : xm(reinterpret_cast<const typename WordT<D>::T *>(x) - s), S(s) {
+        // opaque to ptxas, so the base stays in a register instead of being
+        // re-derived (S2R CgaCtaId + LEA) before every LDS
+        asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(sbase) : "l"(hot_bytes()));
+    }
     __device__ __forceinline__ uint32_t operator()(uint32_t c) const {
-        return c < S ? (uint32_t)sx[c] : load_word<D>(x, c - S);
+        uint32_t v;
+        if (c < S) {
+            if constexpr (D == 4) {  // two 4-bit words per byte (hot.cu packs them)
+                asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(sbase + (c >> 1)));
+                return (v >> ((c & 1u) * 4u)) & 0xFu;
+            } else if constexpr (sizeof(typename WordT<D>::T) == 1) {
+                asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(sbase + c));
+            } else if constexpr (sizeof(typename WordT<D>::T) == 2) {
+                unsigned short h;
+                asm("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(sbase + 2 * c));
+                v = h;
+            } else {
+                asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(sbase + 4 * c));
+            }
+            return v;
+        }
+        return (uint32_t)__ldg(xm + c);
     }
 };
 

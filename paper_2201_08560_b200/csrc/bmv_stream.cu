@@ -20,7 +20,6 @@
 
 namespace b2sr {
 
-constexpr int STREAM_THREADS = 1024;
 constexpr uint32_t SPAN = 7;  // row boundaries a load descriptor carries (more: searched)
 
 // One descriptor per warp load k (tiles [k*TPW, (k+1)*TPW)):
@@ -92,37 +91,53 @@ static StreamPlan *stream_plan(b2sr_matrix *m, uint32_t tpw, cudaStream_t s) {
     return static_cast<StreamPlan *>(m->stream);
 }
 
-// Raw masked words of a lane's tiles: byte r (row r) is non-zero iff the
-// row hits.  d=4: one u32 per tile; d=8: two (rows 0-3, rows 4-7).
-template <int D> struct Masked;
-template <> struct Masked<4> {
-    uint32_t m[4];
-    __device__ __forceinline__ void set(const uint4 &v, const uint32_t (&xw)[4]) {
+// Lane geometry of one warp load of LT = 128 tiles.  A lane holds NG groups of
+// GT consecutive tiles: d=4: one 16-byte group of 4 tiles at 4*lane; d=8: two
+// 16-byte groups of 2 tiles, at 2*lane and 64 + 2*lane (each load instruction
+// stays fully coalesced).
+template <int D> struct SGeo;
+template <> struct SGeo<4> {
+    static constexpr int NG = 1, GT = 4;
+    __device__ static uint32_t pos(uint32_t lane, int g) { return 4 * lane; }
+};
+template <> struct SGeo<8> {
+    static constexpr int NG = 2, GT = 2;
+    __device__ static uint32_t pos(uint32_t lane, int g) { return 64 * g + 2 * lane; }
+};
+constexpr uint32_t LT = 128;  // tiles per warp load
+
+// masked tile words of one group: byte r (row r) non-zero iff the row hits
+template <int D>
+__device__ __forceinline__ void mask_group(const uint4 &v, const uint32_t *xw, uint32_t (&m)[4]) {
+    if constexpr (D == 4) {
         m[0] = v.x & (xw[0] * 0x01010101u);
         m[1] = v.y & (xw[1] * 0x01010101u);
         m[2] = v.z & (xw[2] * 0x01010101u);
         m[3] = v.w & (xw[3] * 0x01010101u);
-    }
-    __device__ __forceinline__ uint32_t all() const { return m[0] | m[1] | m[2] | m[3]; }   // raw OR
-    __device__ __forceinline__ static uint32_t hits(uint32_t raw) { return nz_nibble_bytes(raw); }
-    __device__ __forceinline__ uint32_t tile(int j) const { return nz_nibble_bytes(m[j]); }
-};
-template <> struct Masked<8> {
-    uint32_t lo[2], hi[2];
-    __device__ __forceinline__ void set(const uint4 &v, const uint32_t (&xw)[2]) {
+    } else {
         uint32_t a = xw[0] * 0x01010101u, b = xw[1] * 0x01010101u;
-        lo[0] = v.x & a; hi[0] = v.y & a;
-        lo[1] = v.z & b; hi[1] = v.w & b;
+        m[0] = v.x & a; m[1] = v.y & a;  // tile 0: rows 0-3, rows 4-7
+        m[2] = v.z & b; m[3] = v.w & b;  // tile 1
     }
-    __device__ __forceinline__ uint32_t tile(int j) const { return nz_bytes(lo[j]) | (nz_bytes(hi[j]) << 4); }
-};
+}
+// hit word of tile j of a group / of all tiles of a group
+template <int D>
+__device__ __forceinline__ uint32_t tile_hits(const uint32_t (&m)[4], int j) {
+    if constexpr (D == 4) return nz_nibble_bytes(m[j]);
+    else return nz_bytes(m[2 * j]) | (nz_bytes(m[2 * j + 1]) << 4);
+}
+template <int D>
+__device__ __forceinline__ uint32_t group_hits(const uint32_t (&m)[4]) {
+    if constexpr (D == 4) return nz_nibble_bytes(m[0] | m[1] | m[2] | m[3]);
+    else return nz_bytes(m[0] | m[2]) | (nz_bytes(m[1] | m[3]) << 4);
+}
 
 template <int D>
 __device__ __forceinline__ void or_row(void *__restrict__ y, uint32_t row, uint32_t acc) {
     if (acc) atomic_or_word<D>(y, row, acc);
 }
 
-// rows of offsets p (0..TPW-1) relative to ra: #{i : off[i] <= p}
+// row of offset p (0..LT-1) relative to ra: #{i : off[i] <= p}
 __device__ __forceinline__ uint32_t rel_row(uint32_t p, uint32_t oa, uint32_t ob) {
     uint32_t pp = p * 0x01010101u;
     return (__popc(__vcmpgeu4(pp, oa)) + __popc(__vcmpgeu4(pp, ob))) >> 3;
@@ -132,36 +147,43 @@ template <int D, class GX>
 __device__ __forceinline__ void bbb_stream(uint32_t k0, uint32_t k1, uint64_t T, const uint4 *__restrict__ desc,
                                            const uint32_t *__restrict__ trp, const uint8_t *__restrict__ tiles,
                                            const uint32_t *__restrict__ tci, const GX &gx, void *__restrict__ y) {
-    using G = Geo<D>;
-    constexpr int TPL = G::TPL;          // tiles per lane: 4 (d=4) or 2 (d=8)
-    constexpr uint32_t TPW = G::TPW;     // tiles per warp load: 128 / 64
-    constexpr int SPW = 32 / D;          // packed D-bit row slots per u32: 8 / 4
+    using SG = SGeo<D>;
+    constexpr int NG = SG::NG, GT = SG::GT, TB = Geo<D>::TB;
+    constexpr int SPW = 32 / D;                     // packed D-bit row slots per u32: 8 / 4
     constexpr int NW = (SPAN + 1 + SPW - 1) / SPW;  // accumulator words: 1 / 2
     const uint32_t lane = lane_id();
     struct Stage {
-        uint4 v;
-        uint32_t c[TPL], x[TPL];
+        uint4 v[NG];
+        uint32_t cx[NG * GT];  // tile columns after issue(), x words after gather()
     };
     auto issue = [&](uint32_t k, Stage &st) {
-        uint64_t t = (uint64_t)k * TPW + lane * TPL;
-        bool ok = k < k1 && t < T;
-        st.v = ok ? ld_stream128(tiles + t * G::TB) : make_uint4(0, 0, 0, 0);
-        if constexpr (TPL == 4) {
-            uint4 q = ok ? ld_stream128(tci + t) : make_uint4(0, 0, 0, 0);
-            st.c[0] = q.x; st.c[1] = q.y; st.c[2] = q.z; st.c[3] = q.w;
-        } else {
-            uint2 q = ok ? *reinterpret_cast<const uint2 *>(tci + t) : make_uint2(0, 0);
-            st.c[0] = q.x; st.c[1] = q.y;
+#pragma unroll
+        for (int g = 0; g < NG; g++) {
+            uint64_t t = (uint64_t)k * LT + SG::pos(lane, g);
+            bool ok = k < k1 && t < T;
+            st.v[g] = ok ? ld_stream128(tiles + t * TB) : make_uint4(0, 0, 0, 0);
+            if constexpr (GT == 4) {
+                uint4 q = ok ? ld_stream128(tci + t) : make_uint4(0, 0, 0, 0);
+                st.cx[0] = q.x; st.cx[1] = q.y; st.cx[2] = q.z; st.cx[3] = q.w;
+            } else {
+                uint2 q = ok ? *reinterpret_cast<const uint2 *>(tci + t) : make_uint2(0, 0);
+                st.cx[2 * g] = q.x; st.cx[2 * g + 1] = q.y;
+            }
         }
     };
     auto gather = [&](uint32_t k, Stage &st) {
-        uint64_t t = (uint64_t)k * TPW + lane * TPL;
-        if (k < k1 && t + TPL <= T) {
+        const bool full = k + 1 < k1 || (uint64_t)(k + 1) * LT <= T;  // every tile of load k exists
+        if (full) {
 #pragma unroll
-            for (int j = 0; j < TPL; j++) st.x[j] = gx(st.c[j]);
+            for (int j = 0; j < NG * GT; j++) st.cx[j] = gx(st.cx[j]);
         } else {
 #pragma unroll
-            for (int j = 0; j < TPL; j++) st.x[j] = (k < k1 && t + j < T) ? gx(st.c[j]) : 0u;
+            for (int g = 0; g < NG; g++)
+#pragma unroll
+                for (int j = 0; j < GT; j++) {
+                    uint64_t t = (uint64_t)k * LT + SG::pos(lane, g) + j;
+                    st.cx[g * GT + j] = (k < k1 && t < T) ? gx(st.cx[g * GT + j]) : 0u;
+                }
         }
     };
     uint4 dcur = __ldg(desc + k0 + lane), dnxt = __ldg(desc + k0 + 32 + lane);  // desc has 64 entries of slack
@@ -173,35 +195,41 @@ __device__ __forceinline__ void bbb_stream(uint32_t k0, uint32_t k1, uint64_t T,
         }
         const uint32_t ra = __shfl_sync(0xffffffffu, dcur.x, i);
         const uint32_t span = __shfl_sync(0xffffffffu, dcur.w, i);
-        Masked<D> mk;
-        mk.set(st.v, st.x);
+        uint32_t m[NG][4];
+#pragma unroll
+        for (int g = 0; g < NG; g++) mask_group<D>(st.v[g], st.cx + g * GT, m[g]);
         if (span == 0) {  // the whole load lies in one row
-            uint32_t acc;
+            uint32_t raw = 0;
             if constexpr (D == 4) {
-                acc = __reduce_or_sync(0xffffffffu, mk.all());
-                if (lane == 0) or_row<D>(y, ra, Masked<4>::hits(acc));
+                raw = m[0][0] | m[0][1] | m[0][2] | m[0][3];  // OR raw words, test once
+                raw = __reduce_or_sync(0xffffffffu, raw);
+                if (lane == 0) or_row<D>(y, ra, nz_nibble_bytes(raw));
             } else {
-                acc = __reduce_or_sync(0xffffffffu, mk.tile(0) | mk.tile(1));
-                if (lane == 0) or_row<D>(y, ra, acc);
+                uint32_t lo = m[0][0] | m[0][2] | m[1][0] | m[1][2], hi = m[0][1] | m[0][3] | m[1][1] | m[1][3];
+                lo = __reduce_or_sync(0xffffffffu, lo);
+                hi = __reduce_or_sync(0xffffffffu, hi);
+                if (lane == 0) or_row<D>(y, ra, nz_bytes(lo) | (nz_bytes(hi) << 4));
             }
         } else if (span <= SPAN) {
             const uint32_t oa = __shfl_sync(0xffffffffu, dcur.y, i), ob = __shfl_sync(0xffffffffu, dcur.z, i);
-            const uint32_t qa = rel_row(lane * TPL, oa, ob), qb = rel_row(lane * TPL + TPL - 1, oa, ob);
             uint32_t acc[NW];
 #pragma unroll
             for (int u = 0; u < NW; u++) acc[u] = 0;
-            if (qa == qb) {  // the lane's tiles share one row
-                uint32_t h;
-                if constexpr (D == 4) h = Masked<4>::hits(mk.all());
-                else h = mk.tile(0) | mk.tile(1);
 #pragma unroll
-                for (int u = 0; u < NW; u++) acc[u] = (qa / SPW == (uint32_t)u) ? h << (D * (qa % SPW)) : 0u;
-            } else {
+            for (int g = 0; g < NG; g++) {
+                const uint32_t p0 = SG::pos(lane, g);
+                const uint32_t qa = rel_row(p0, oa, ob), qb = rel_row(p0 + GT - 1, oa, ob);
+                if (qa == qb) {  // the group's tiles share one row
+                    uint32_t h = group_hits<D>(m[g]);
 #pragma unroll
-                for (int j = 0; j < TPL; j++) {
-                    uint32_t q = rel_row(lane * TPL + j, oa, ob), h = mk.tile(j);
+                    for (int u = 0; u < NW; u++) acc[u] |= (qa / SPW == (uint32_t)u) ? h << (D * (qa % SPW)) : 0u;
+                } else {
 #pragma unroll
-                    for (int u = 0; u < NW; u++) acc[u] |= (q / SPW == (uint32_t)u) ? h << (D * (q % SPW)) : 0u;
+                    for (int j = 0; j < GT; j++) {
+                        uint32_t q = rel_row(p0 + j, oa, ob), h = tile_hits<D>(m[g], j);
+#pragma unroll
+                        for (int u = 0; u < NW; u++) acc[u] |= (q / SPW == (uint32_t)u) ? h << (D * (q % SPW)) : 0u;
+                    }
                 }
             }
 #pragma unroll
@@ -215,41 +243,45 @@ __device__ __forceinline__ void bbb_stream(uint32_t k0, uint32_t k1, uint64_t T,
         } else {
             // many short rows: search trp[ra..rb] per tile and write per tile
             const uint32_t rb = i < 31 ? __shfl_sync(0xffffffffu, dcur.x, i + 1) : __shfl_sync(0xffffffffu, dnxt.x, 0);
-            const uint64_t t0 = (uint64_t)k * TPW + lane * TPL;
 #pragma unroll
-            for (int j = 0; j < TPL; j++) {
-                uint32_t h = mk.tile(j);
-                if (h) or_row<D>(y, row_of(trp, ra, rb, t0 + j), h);
-            }
+            for (int g = 0; g < NG; g++)
+#pragma unroll
+                for (int j = 0; j < GT; j++) {
+                    uint32_t h = tile_hits<D>(m[g], j);
+                    if (h) or_row<D>(y, row_of(trp, ra, rb, (uint64_t)k * LT + SG::pos(lane, g) + j), h);
+                }
         }
     };
     if (k0 >= k1) return;
-    // two-stage pipeline, unrolled so the stages never move: while load k is
-    // reduced, the x gathers of k+1 are in flight; then the tiles of k+2 issue
-    Stage A, B;
+    // three-stage pipeline, unrolled so the stages never move: while load k is
+    // reduced, the x gathers of k+1 and the tile/column loads of k+2 are in flight
+    Stage A, B, C;
     issue(k0, A);
-    gather(k0, A);
     issue(k0 + 1, B);
-    for (uint32_t k = k0; k < k1; k += 2) {
+    gather(k0, A);
+    for (uint32_t k = k0; k < k1; k += 3) {
+        issue(k + 2, C);
         gather(k + 1, B);
         compute(k, A);
-        issue(k + 2, A);
         if (k + 1 >= k1) break;
-        gather(k + 2, A);
+        issue(k + 3, A);
+        gather(k + 2, C);
         compute(k + 1, B);
-        issue(k + 3, B);
+        if (k + 2 >= k1) break;
+        issue(k + 4, B);
+        gather(k + 3, A);
+        compute(k + 2, C);
     }
 }
 
-template <int D>
-__global__ void __launch_bounds__(STREAM_THREADS, 1)
+template <int D, int NT>
+__global__ void __launch_bounds__(NT, 1)
     k_bmv_bbb_stream(uint32_t n_loads, uint64_t T, const uint4 *__restrict__ desc, const uint32_t *__restrict__ trp,
                      const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci2, const void *__restrict__ hx,
                      uint32_t hx_bytes16, uint32_t S, const void *__restrict__ x, void *__restrict__ y) {
-    extern __shared__ uint4 hot_smem[];
-    stage_hot(hot_smem, hx, hx_bytes16);
+    stage_hot(const_cast<uint8_t *>(hot_bytes()), hx, hx_bytes16);
     __syncthreads();
-    XHot<D> gx{reinterpret_cast<const typename WordT<D>::T *>(hot_smem), x, S};
+    XHot<D> gx(x, S);
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5, w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t per = (n_loads + warps - 1) / warps;
     const uint32_t k0 = std::min(n_loads, w * per), k1 = std::min(n_loads, k0 + per);
@@ -274,7 +306,7 @@ void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y,
     const size_t yb = padded_vec_bytes(m->ntr, m->dim);
     CK(cudaMemsetAsync(y, 0, yb, s));
     if (!m->num_tiles) return;
-    const uint32_t tpw = m->dim == 4 ? Geo<4>::TPW : Geo<8>::TPW;
+    const uint32_t tpw = LT;
     StreamPlan *sp = stream_plan(m, tpw, s);
     HotView hv = hot_view(m, s);
     size_t hb = hot_fill_bytes(hv, m->dim);
@@ -283,15 +315,24 @@ void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y,
     unsigned g = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((uint64_t)num_sms(), ((uint64_t)sp->n_loads + 31) / 32));
     const uint8_t *tl = (const uint8_t *)m->tiles;
+    const char *te = getenv("B2SR_STREAM_THREADS");  // A/B: 512 / 768 / 1024 threads per CTA
+    int nt = te ? atoi(te) : (m->dim == 4 ? 1024 : 768);
+#define STREAM_LAUNCH(DD, NT)                                                                                       \
+    do {                                                                                                            \
+        hot_smem_attr(k_bmv_bbb_stream<DD, NT>, hb);                                                                \
+        LAUNCH((k_bmv_bbb_stream<DD, NT>), g, NT, hb, s, sp->n_loads, m->num_tiles, sp->desc, m->trp, tl, hv.tci2,  \
+               hx.p, (uint32_t)hb, hv.S, x, y);                                                                     \
+    } while (0)
     if (m->dim == 4) {
-        hot_smem_attr(k_bmv_bbb_stream<4>, hb);
-        LAUNCH(k_bmv_bbb_stream<4>, g, STREAM_THREADS, hb, s, sp->n_loads, m->num_tiles, sp->desc, m->trp, tl, hv.tci2,
-               hx.p, (uint32_t)hb, hv.S, x, y);
+        if (nt == 512) STREAM_LAUNCH(4, 512);
+        else if (nt == 768) STREAM_LAUNCH(4, 768);
+        else STREAM_LAUNCH(4, 1024);
     } else {
-        hot_smem_attr(k_bmv_bbb_stream<8>, hb);
-        LAUNCH(k_bmv_bbb_stream<8>, g, STREAM_THREADS, hb, s, sp->n_loads, m->num_tiles, sp->desc, m->trp, tl, hv.tci2,
-               hx.p, (uint32_t)hb, hv.S, x, y);
+        if (nt == 512) STREAM_LAUNCH(8, 512);
+        else if (nt == 1024) STREAM_LAUNCH(8, 1024);
+        else STREAM_LAUNCH(8, 768);
     }
+#undef STREAM_LAUNCH
     if (keep) {  // masked variant: the keep words are applied once at the end (kernels.py:219-225)
         const uint8_t *kp = static_cast<const uint8_t *>(keep) + (size_t)m->row0 * word_bytes(m->dim);
         if (((uintptr_t)kp & 3) == 0) {

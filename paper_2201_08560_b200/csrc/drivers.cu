@@ -148,10 +148,9 @@ __global__ void __launch_bounds__(PULL_HOT_THREADS, 1)
                    const void *__restrict__ frontier, const void *__restrict__ visited, const void *__restrict__ live,
                    void *__restrict__ next, uint32_t row0, const uint32_t *__restrict__ idx,
                    const uint32_t *__restrict__ idx_n) {
-    extern __shared__ uint4 hot_smem[];
-    stage_hot(hot_smem, hx, hx_bytes16);
+    stage_hot(const_cast<uint8_t *>(hot_bytes()), hx, hx_bytes16);
     __syncthreads();
-    XHot<D> gx{reinterpret_cast<const typename WordT<D>::T *>(hot_smem), frontier, S};
+    XHot<D> gx(frontier, S);
     pull_items<D>(items, n_items, tiles, tci2, gx, visited, live, next, row0, idx, idx_n);
 }
 

@@ -80,7 +80,7 @@ HotView hot_view(b2sr_matrix *m, cudaStream_t s) {
         const uint32_t wb = (uint32_t)word_bytes((int)m->dim);
         const char *e = getenv("B2SR_HOT_BYTES");     // parity tests force the remapped path on small graphs
         uint32_t budget = e ? (uint32_t)atoi(e) : HOT_SMEM_BYTES;
-        uint32_t cap = budget / wb;
+        uint32_t cap = m->dim == 4 ? budget * 2 : budget / wb;  // d=4: two 4-bit words per byte
         HotPlan *h = new HotPlan();
         try {
             if (nc <= cap) {
@@ -122,13 +122,33 @@ __global__ void k_hot_fill(uint32_t S, const uint32_t *__restrict__ cols, const 
         hx[i] = x[cols ? cols[i] : i];
 }
 
-size_t hot_fill_bytes(const HotView &hv, int dim) { return ((size_t)hv.S * word_bytes(dim) + 15) / 16 * 16; }
+// d=4: slot pair (2i, 2i+1) shares byte i (low nibble = even slot)
+__global__ void k_hot_fill4(uint32_t S, const uint32_t *__restrict__ cols, const uint8_t *__restrict__ x,
+                            uint8_t *__restrict__ hx) {
+    const uint32_t nb = (S + 1) / 2;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x) {
+        uint32_t a = 2 * i, b = 2 * i + 1;
+        uint32_t lo = x[cols ? cols[a] : a] & 0xFu;
+        uint32_t hi = b < S ? (x[cols ? cols[b] : b] & 0xFu) : 0u;
+        hx[i] = (uint8_t)(lo | (hi << 4));
+    }
+}
+
+static size_t hot_used_bytes(const HotView &hv, int dim) {
+    return dim == 4 ? ((size_t)hv.S + 1) / 2 : (size_t)hv.S * word_bytes(dim);
+}
+
+size_t hot_fill_bytes(const HotView &hv, int dim) { return (hot_used_bytes(hv, dim) + 15) / 16 * 16; }
 
 void hot_fill(const HotView &hv, int dim, const void *x, void *hx, cudaStream_t s) {
     size_t b = hot_fill_bytes(hv, dim);
-    size_t used = (size_t)hv.S * word_bytes(dim);
+    size_t used = hot_used_bytes(hv, dim);
     if (b > used) CK(cudaMemsetAsync(static_cast<char *>(hx) + used, 0, b - used, s));
     unsigned g = hgrid(hv.S);
+    if (dim == 4) {
+        LAUNCH(k_hot_fill4, g, 256, 0, s, hv.S, hv.cols, (const uint8_t *)x, (uint8_t *)hx);
+        return;
+    }
     switch (word_bytes(dim)) {
         case 1: LAUNCH(k_hot_fill<uint8_t>, g, 256, 0, s, hv.S, hv.cols, (const uint8_t *)x, (uint8_t *)hx); break;
         case 2: LAUNCH(k_hot_fill<uint16_t>, g, 256, 0, s, hv.S, hv.cols, (const uint16_t *)x, (uint16_t *)hx); break;
