@@ -178,7 +178,10 @@ void hot_fill(const HotView &hv, int dim, const void *x, void *hx, cudaStream_t 
 bool hot_enabled(int dim);
 // bmv_stream.cu: flat tile-stream K4 (d = 4, 8)
 bool stream_enabled(int dim);
-void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaStream_t s);
+// visited != null: BFS pull (y &= ~visited & live instead of keep)
+// active_only (with visited): only the loads that hold a row with an unvisited live vertex
+void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaStream_t s,
+                       const void *visited = nullptr, bool active_only = false);
 void free_stream(void *plan);
 // blocked bin-SpMV: mode 0 = masked bbb, 1 = BFS pull; false if not applicable
 bool launch_blocked(b2sr_matrix *m, int mode, const void *x, const void *keep, void *y, cudaStream_t s);

@@ -143,8 +143,11 @@ __device__ __forceinline__ uint32_t rel_row(uint32_t p, uint32_t oa, uint32_t ob
     return (__popc(__vcmpgeu4(pp, oa)) + __popc(__vcmpgeu4(pp, ob))) >> 3;
 }
 
-template <int D, class GX>
-__device__ __forceinline__ void bbb_stream(uint32_t k0, uint32_t k1, uint64_t T, const uint4 *__restrict__ desc,
+// Streams the loads at positions [p0, p1): load k = list[p] with a list (BFS
+// pull over the loads that still hold an unvisited vertex), else k = p.
+template <int D, bool LIST, class GX>
+__device__ __forceinline__ void bbb_stream(uint32_t p0, uint32_t p1, uint32_t n_loads, uint64_t T,
+                                           const uint32_t *__restrict__ list, const uint4 *__restrict__ desc,
                                            const uint32_t *__restrict__ trp, const uint8_t *__restrict__ tiles,
                                            const uint32_t *__restrict__ tci, const GX &gx, void *__restrict__ y) {
     using SG = SGeo<D>;
@@ -156,11 +159,33 @@ __device__ __forceinline__ void bbb_stream(uint32_t k0, uint32_t k1, uint64_t T,
         uint4 v[NG];
         uint32_t cx[NG * GT];  // tile columns after issue(), x words after gather()
     };
-    auto issue = [&](uint32_t k, Stage &st) {
+    // per 32 positions: load index (list mode) and descriptor, one block ahead
+    uint32_t bb = p0;  // first position of the current block
+    uint32_t kc = 0, kn = 0;
+    if constexpr (LIST) {
+        kc = p0 + lane < p1 ? __ldg(list + p0 + lane) : 0u;
+        kn = p0 + 32 + lane < p1 ? __ldg(list + p0 + 32 + lane) : 0u;
+    } else {
+        kc = p0 + lane;
+        kn = p0 + 32 + lane;
+    }
+    uint4 dcur = __ldg(desc + std::min(kc, n_loads)), dnxt = __ldg(desc + std::min(kn, n_loads));
+    auto kat = [&](uint32_t p) -> uint32_t {  // load index of position p (p - bb < 64)
+        if constexpr (LIST) {
+            uint32_t o = p - bb;
+            uint32_t a = __shfl_sync(0xffffffffu, kc, o & 31), b = __shfl_sync(0xffffffffu, kn, o & 31);
+            return o < 32 ? a : b;
+        } else {
+            return p;
+        }
+    };
+    auto issue = [&](uint32_t p, Stage &st) {
+        const bool live = p < p1;
+        const uint32_t k = kat(p);
 #pragma unroll
         for (int g = 0; g < NG; g++) {
             uint64_t t = (uint64_t)k * LT + SG::pos(lane, g);
-            bool ok = k < k1 && t < T;
+            bool ok = live && t < T;
             st.v[g] = ok ? ld_stream128(tiles + t * TB) : make_uint4(0, 0, 0, 0);
             if constexpr (GT == 4) {
                 uint4 q = ok ? ld_stream128(tci + t) : make_uint4(0, 0, 0, 0);
@@ -171,8 +196,9 @@ __device__ __forceinline__ void bbb_stream(uint32_t k0, uint32_t k1, uint64_t T,
             }
         }
     };
-    auto gather = [&](uint32_t k, Stage &st) {
-        const bool full = k + 1 < k1 || (uint64_t)(k + 1) * LT <= T;  // every tile of load k exists
+    auto gather = [&](uint32_t p, Stage &st) {
+        const uint32_t k = kat(p);
+        const bool full = p < p1 && (k + 1 < n_loads || (uint64_t)(k + 1) * LT <= T);  // every tile of load k exists
         if (full) {
 #pragma unroll
             for (int j = 0; j < NG * GT; j++) st.cx[j] = gx(st.cx[j]);
@@ -182,26 +208,30 @@ __device__ __forceinline__ void bbb_stream(uint32_t k0, uint32_t k1, uint64_t T,
 #pragma unroll
                 for (int j = 0; j < GT; j++) {
                     uint64_t t = (uint64_t)k * LT + SG::pos(lane, g) + j;
-                    st.cx[g * GT + j] = (k < k1 && t < T) ? gx(st.cx[g * GT + j]) : 0u;
+                    st.cx[g * GT + j] = (p < p1 && t < T) ? gx(st.cx[g * GT + j]) : 0u;
                 }
         }
     };
-    uint4 dcur = __ldg(desc + k0 + lane), dnxt = __ldg(desc + k0 + 32 + lane);  // desc has 64 entries of slack
-    auto compute = [&](uint32_t k, const Stage &st) {
-        const uint32_t i = (k - k0) & 31u;
-        if (i == 0 && k != k0) {
+    auto compute = [&](uint32_t p, const Stage &st) {
+        if (p - bb == 32) {  // next block of 32 positions
+            bb = p;
+            kc = kn;
             dcur = dnxt;
-            dnxt = __ldg(desc + k + 32 + lane);
+            uint32_t q = p + 32 + lane;
+            if constexpr (LIST) kn = q < p1 ? __ldg(list + q) : 0u;
+            else kn = q;
+            dnxt = __ldg(desc + std::min(kn, n_loads));
         }
+        const uint32_t i = p - bb;
+        const uint32_t k = LIST ? __shfl_sync(0xffffffffu, kc, i) : p;
         const uint32_t ra = __shfl_sync(0xffffffffu, dcur.x, i);
         const uint32_t span = __shfl_sync(0xffffffffu, dcur.w, i);
         uint32_t m[NG][4];
 #pragma unroll
         for (int g = 0; g < NG; g++) mask_group<D>(st.v[g], st.cx + g * GT, m[g]);
         if (span == 0) {  // the whole load lies in one row
-            uint32_t raw = 0;
             if constexpr (D == 4) {
-                raw = m[0][0] | m[0][1] | m[0][2] | m[0][3];  // OR raw words, test once
+                uint32_t raw = m[0][0] | m[0][1] | m[0][2] | m[0][3];  // OR raw words, test once
                 raw = __reduce_or_sync(0xffffffffu, raw);
                 if (lane == 0) or_row<D>(y, ra, nz_nibble_bytes(raw));
             } else {
@@ -217,8 +247,8 @@ __device__ __forceinline__ void bbb_stream(uint32_t k0, uint32_t k1, uint64_t T,
             for (int u = 0; u < NW; u++) acc[u] = 0;
 #pragma unroll
             for (int g = 0; g < NG; g++) {
-                const uint32_t p0 = SG::pos(lane, g);
-                const uint32_t qa = rel_row(p0, oa, ob), qb = rel_row(p0 + GT - 1, oa, ob);
+                const uint32_t q0 = SG::pos(lane, g);
+                const uint32_t qa = rel_row(q0, oa, ob), qb = rel_row(q0 + GT - 1, oa, ob);
                 if (qa == qb) {  // the group's tiles share one row
                     uint32_t h = group_hits<D>(m[g]);
 #pragma unroll
@@ -226,7 +256,7 @@ __device__ __forceinline__ void bbb_stream(uint32_t k0, uint32_t k1, uint64_t T,
                 } else {
 #pragma unroll
                     for (int j = 0; j < GT; j++) {
-                        uint32_t q = rel_row(p0 + j, oa, ob), h = tile_hits<D>(m[g], j);
+                        uint32_t q = rel_row(q0 + j, oa, ob), h = tile_hits<D>(m[g], j);
 #pragma unroll
                         for (int u = 0; u < NW; u++) acc[u] |= (q / SPW == (uint32_t)u) ? h << (D * (q % SPW)) : 0u;
                     }
@@ -242,7 +272,7 @@ __device__ __forceinline__ void bbb_stream(uint32_t k0, uint32_t k1, uint64_t T,
             }
         } else {
             // many short rows: search trp[ra..rb] per tile and write per tile
-            const uint32_t rb = i < 31 ? __shfl_sync(0xffffffffu, dcur.x, i + 1) : __shfl_sync(0xffffffffu, dnxt.x, 0);
+            const uint32_t rb = __ldg(&desc[k + 1].x);
 #pragma unroll
             for (int g = 0; g < NG; g++)
 #pragma unroll
@@ -252,40 +282,69 @@ __device__ __forceinline__ void bbb_stream(uint32_t k0, uint32_t k1, uint64_t T,
                 }
         }
     };
-    if (k0 >= k1) return;
-    // three-stage pipeline, unrolled so the stages never move: while load k is
-    // reduced, the x gathers of k+1 and the tile/column loads of k+2 are in flight
+    if (p0 >= p1) return;
+    // three-stage pipeline, unrolled so the stages never move: while load p is
+    // reduced, the x gathers of p+1 and the tile/column loads of p+2 are in flight
     Stage A, B, C;
-    issue(k0, A);
-    issue(k0 + 1, B);
-    gather(k0, A);
-    for (uint32_t k = k0; k < k1; k += 3) {
-        issue(k + 2, C);
-        gather(k + 1, B);
-        compute(k, A);
-        if (k + 1 >= k1) break;
-        issue(k + 3, A);
-        gather(k + 2, C);
-        compute(k + 1, B);
-        if (k + 2 >= k1) break;
-        issue(k + 4, B);
-        gather(k + 3, A);
-        compute(k + 2, C);
+    issue(p0, A);
+    issue(p0 + 1, B);
+    gather(p0, A);
+    for (uint32_t p = p0; p < p1; p += 3) {
+        issue(p + 2, C);
+        gather(p + 1, B);
+        compute(p, A);
+        if (p + 1 >= p1) break;
+        issue(p + 3, A);
+        gather(p + 2, C);
+        compute(p + 1, B);
+        if (p + 2 >= p1) break;
+        issue(p + 4, B);
+        gather(p + 3, A);
+        compute(p + 2, C);
     }
 }
 
-template <int D, int NT>
+template <int D, int NT, bool LIST>
 __global__ void __launch_bounds__(NT, 1)
-    k_bmv_bbb_stream(uint32_t n_loads, uint64_t T, const uint4 *__restrict__ desc, const uint32_t *__restrict__ trp,
+    k_bmv_bbb_stream(uint32_t n_loads, const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_n,
+                     uint64_t T, const uint4 *__restrict__ desc, const uint32_t *__restrict__ trp,
                      const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci2, const void *__restrict__ hx,
                      uint32_t hx_bytes16, uint32_t S, const void *__restrict__ x, void *__restrict__ y) {
+    const uint32_t n_pos = LIST ? *list_n : n_loads;
+    if (n_pos == 0) return;
     stage_hot(const_cast<uint8_t *>(hot_bytes()), hx, hx_bytes16);
     __syncthreads();
     XHot<D> gx(x, S);
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5, w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t per = (n_loads + warps - 1) / warps;
-    const uint32_t k0 = std::min(n_loads, w * per), k1 = std::min(n_loads, k0 + per);
-    bbb_stream<D>(k0, k1, T, desc, trp, tiles, tci2, gx, y);
+    const uint32_t per = (n_pos + warps - 1) / warps;
+    const uint32_t p0 = std::min(n_pos, w * per), p1 = std::min(n_pos, p0 + per);
+    bbb_stream<D, LIST>(p0, p1, n_loads, T, list, desc, trp, tiles, tci2, gx, y);
+}
+
+// BFS pull over part of the matrix: the loads holding a tile of a row with an
+// unvisited live vertex (rows [ra, next ra] of every load are checked).
+template <int D>
+__global__ void k_active_loads(uint32_t n_loads, const uint4 *__restrict__ desc, const void *__restrict__ visited,
+                               const void *__restrict__ live, uint32_t row0, uint32_t *__restrict__ list,
+                               uint32_t *__restrict__ count) {
+    const uint32_t lane = lane_id();
+    const uint32_t stride = gridDim.x * blockDim.x;
+    const uint32_t iters = (n_loads + stride - 1) / stride;
+    for (uint32_t it = 0; it < iters; it++) {
+        uint32_t k = blockIdx.x * blockDim.x + threadIdx.x + it * stride;
+        bool act = false;
+        if (k < n_loads) {
+            uint32_t ra = desc[k].x, rb = desc[k + 1].x;
+            for (uint32_t r = ra; r <= rb && !act; r++)
+                act = (~load_word<D>(visited, row0 + r) & load_word<D>(live, r)) != 0;
+        }
+        uint32_t bal = __ballot_sync(0xffffffffu, act);
+        if (!bal) continue;
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(count, (uint32_t)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (act) list[base + __popc(bal & ((1u << lane) - 1u))] = k;
+    }
 }
 
 // y &= keep (keep is indexed by global tile row: row0 offsets it for row blocks)
@@ -302,38 +361,74 @@ bool stream_enabled(int dim) {
     return (dim == 4 || dim == 8) && hot_enabled(dim);
 }
 
-void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaStream_t s) {
+// y &= ~visited & live (BFS pull: only unvisited vertices with in-edges take a level)
+__global__ void k_pull_mask(uint32_t nb, uint8_t *__restrict__ y, const uint8_t *__restrict__ visited,
+                            const uint8_t *__restrict__ live, bool aligned) {
+    if (aligned) {
+        uint32_t nw = nb / 4;
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nw; i += gridDim.x * blockDim.x)
+            reinterpret_cast<uint32_t *>(y)[i] &= ~reinterpret_cast<const uint32_t *>(visited)[i] &
+                                                  reinterpret_cast<const uint32_t *>(live)[i];
+    } else {
+        for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nb; i += gridDim.x * blockDim.x)
+            y[i] &= (uint8_t)(~visited[i] & live[i]);
+    }
+}
+
+void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaStream_t s,
+                       const void *visited, bool active_only) {
     const size_t yb = padded_vec_bytes(m->ntr, m->dim);
     CK(cudaMemsetAsync(y, 0, yb, s));
     if (!m->num_tiles) return;
-    const uint32_t tpw = LT;
-    StreamPlan *sp = stream_plan(m, tpw, s);
+    StreamPlan *sp = stream_plan(m, LT, s);
     HotView hv = hot_view(m, s);
     size_t hb = hot_fill_bytes(hv, m->dim);
     Buf<uint8_t> hx(hb, s);
+    Buf<uint32_t> list, list_n;
+    if (active_only && visited) {  // compact the loads that still matter
+        list = Buf<uint32_t>(sp->n_loads, s);
+        list_n = Buf<uint32_t>(1, s);
+        CK(cudaMemsetAsync(list_n.p, 0, 4, s));
+        unsigned ga = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((sp->n_loads + 255) / 256, (uint64_t)num_sms() * 8));
+        if (m->dim == 4)
+            LAUNCH(k_active_loads<4>, ga, 256, 0, s, sp->n_loads, sp->desc, visited, m->live, m->row0, list.p, list_n.p);
+        else
+            LAUNCH(k_active_loads<8>, ga, 256, 0, s, sp->n_loads, sp->desc, visited, m->live, m->row0, list.p, list_n.p);
+    }
     hot_fill(hv, m->dim, x, hx.p, s);
     unsigned g = (unsigned)std::max<uint64_t>(
         1, std::min<uint64_t>((uint64_t)num_sms(), ((uint64_t)sp->n_loads + 31) / 32));
     const uint8_t *tl = (const uint8_t *)m->tiles;
     const char *te = getenv("B2SR_STREAM_THREADS");  // A/B: 512 / 768 / 1024 threads per CTA
     int nt = te ? atoi(te) : (m->dim == 4 ? 1024 : 768);
-#define STREAM_LAUNCH(DD, NT)                                                                                       \
-    do {                                                                                                            \
-        hot_smem_attr(k_bmv_bbb_stream<DD, NT>, hb);                                                                \
-        LAUNCH((k_bmv_bbb_stream<DD, NT>), g, NT, hb, s, sp->n_loads, m->num_tiles, sp->desc, m->trp, tl, hv.tci2,  \
-               hx.p, (uint32_t)hb, hv.S, x, y);                                                                     \
+#define STREAM_LAUNCH(DD, NT)                                                                                        \
+    do {                                                                                                             \
+        if (list.p) {                                                                                                \
+            hot_smem_attr(k_bmv_bbb_stream<DD, NT, true>, hb);                                                       \
+            LAUNCH((k_bmv_bbb_stream<DD, NT, true>), g, NT, hb, s, sp->n_loads, list.p, list_n.p, m->num_tiles,      \
+                   sp->desc, m->trp, tl, hv.tci2, hx.p, (uint32_t)hb, hv.S, x, y);                                   \
+        } else {                                                                                                     \
+            hot_smem_attr(k_bmv_bbb_stream<DD, NT, false>, hb);                                                      \
+            LAUNCH((k_bmv_bbb_stream<DD, NT, false>), g, NT, hb, s, sp->n_loads, nullptr, nullptr, m->num_tiles,     \
+                   sp->desc, m->trp, tl, hv.tci2, hx.p, (uint32_t)hb, hv.S, x, y);                                   \
+        }                                                                                                            \
     } while (0)
     if (m->dim == 4) {
-        if (nt == 512) STREAM_LAUNCH(4, 512);
-        else if (nt == 768) STREAM_LAUNCH(4, 768);
+        if (nt == 768) STREAM_LAUNCH(4, 768);
         else STREAM_LAUNCH(4, 1024);
     } else {
-        if (nt == 512) STREAM_LAUNCH(8, 512);
-        else if (nt == 1024) STREAM_LAUNCH(8, 1024);
+        if (nt == 1024) STREAM_LAUNCH(8, 1024);
         else STREAM_LAUNCH(8, 768);
     }
 #undef STREAM_LAUNCH
-    if (keep) {  // masked variant: the keep words are applied once at the end (kernels.py:219-225)
+    if (visited) {  // BFS pull: keep = ~visited & live, applied once at the end
+        const uint8_t *vp = static_cast<const uint8_t *>(visited) + (size_t)m->row0 * word_bytes(m->dim);
+        const uint32_t nb = (uint32_t)yb;
+        bool aligned = ((uintptr_t)vp & 3) == 0;
+        unsigned gk = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((nb / (aligned ? 4 : 1) + 255) / 256,
+                                                                         (uint64_t)num_sms() * 8));
+        LAUNCH(k_pull_mask, gk, 256, 0, s, nb, (uint8_t *)y, vp, (const uint8_t *)m->live, aligned);
+    } else if (keep) {  // masked variant: the keep words are applied once at the end (kernels.py:219-225)
         const uint8_t *kp = static_cast<const uint8_t *>(keep) + (size_t)m->row0 * word_bytes(m->dim);
         if (((uintptr_t)kp & 3) == 0) {
             const uint32_t kw = (uint32_t)(yb / 4);

@@ -446,10 +446,21 @@ void ensure_live(b2sr_matrix *m, cudaStream_t s) {
     m->live = lv.release();
 }
 
+// pull levels run on the flat tile stream (bmv_stream.cu) where it applies
+static bool pull_stream(const b2sr_matrix *at) {
+    const char *ps = getenv("B2SR_PULL_STREAM");  // B2SR_PULL_STREAM=0: work-item pull kernels (A/B)
+    return stream_enabled(at->dim) && !(ps && ps[0] == '0') && !blocked_enabled();
+}
+
 void bfs_sweep(b2sr_matrix *at, const void *frontier, const void *visited, void *next, cudaStream_t s,
-               const uint32_t *idx = nullptr, const uint32_t *idx_n = nullptr) {
+               const uint32_t *idx = nullptr, const uint32_t *idx_n = nullptr, int active_only = -1) {
     ensure_live(at, s);
     if (!idx && blocked_enabled() && launch_blocked(at, 1, frontier, visited, next, s)) return;
+    if (!idx && pull_stream(at)) {
+        // only the loads that still hold an unvisited vertex, once few are left
+        launch_bbb_stream(at, frontier, nullptr, next, s, visited, active_only > 0);
+        return;
+    }
     ensure_items(at, s);
     CK(cudaMemsetAsync(next, 0, padded_vec_bytes(at->ntr, at->dim), s));
     uint64_t blocks = ((uint64_t)at->n_items + 7) / 8, cap = (uint64_t)num_sms() * 16;
@@ -768,6 +779,11 @@ int b2sr_bfs(const b2sr_matrix *a_c, const b2sr_matrix *at_c, uint32_t src, doub
     for (;;) {
         bool push = a && (double)h.frontier_tiles * alpha < (double)unvisited;
         bool sparse_pull = !push && unvisited * 16 < at->num_tiles;
+        if (!push && pull_stream(at)) {
+            // flat-stream pull; restricted to the loads of unvisited rows once they are few
+            bfs_sweep(at, frontier, visited.p, next, s, nullptr, nullptr, unvisited * 2 < at->num_tiles ? 1 : 0);
+            sparse_pull = false;
+        }
         if (sparse_pull) {
             if (!act_idx.p) {
                 act_idx = Buf<uint32_t>(at->n_items, s);
@@ -782,7 +798,9 @@ int b2sr_bfs(const b2sr_matrix *a_c, const b2sr_matrix *at_c, uint32_t src, doub
                 default: LAUNCH(k_active_items<32>, g, 256, 0, s, ntr, visited.p, at->live, at->item_ofs, act_idx.p, act_n.p); break;
             }
         }
-        if (push) {
+        if (!push && pull_stream(at)) {
+            // swept above
+        } else if (push) {
             CK(cudaMemsetAsync(next, 0, vb, s));
             uint64_t blocks = ((uint64_t)h.list_n + 7) / 8, cap = (uint64_t)num_sms() * 16;
             unsigned g = (unsigned)std::max<uint64_t>(1, std::min(blocks, cap));
