@@ -183,6 +183,9 @@ bool stream_enabled(int dim);
 void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaStream_t s,
                        const void *visited = nullptr, bool active_only = false);
 void free_stream(void *plan);
+const uint4 *stream_desc(b2sr_matrix *m, cudaStream_t s, uint32_t *n_loads);  // per-load row descriptors
+void launch_stream_sweep(b2sr_matrix *m, const uint32_t *list, const uint32_t *list_n, const void *hx, size_t hb,
+                         const void *x, void *y, const int *gate, int want, cudaStream_t s);
 // blocked bin-SpMV: mode 0 = masked bbb, 1 = BFS pull; false if not applicable
 bool launch_blocked(b2sr_matrix *m, int mode, const void *x, const void *keep, void *y, cudaStream_t s);
 // B2SR_BLOCKED=1 selects the column-strip blocked kernels (A/B measurements)

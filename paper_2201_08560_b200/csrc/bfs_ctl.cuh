@@ -1,0 +1,40 @@
+// Device-side state of the BFS driver (drivers.cu) shared with the fused
+// level-sweep kernel (bmv_stream.cu).
+#pragma once
+
+#include "b2sr_internal.cuh"
+
+namespace b2sr {
+
+constexpr uint32_t PUSH_CH = 1024;  // tiles per push work entry (hub rows split)
+
+struct BfsCounters {
+    int any;
+    uint32_t list_n;                     // push work entries
+    unsigned long long frontier_tiles;   // tiles of a in frontier tile rows
+    unsigned long long removed_tiles;    // tiles of at rows whose keep word became zero
+    unsigned long long frontier_vertices;
+};
+
+// Direction of one level, chosen on the device from the previous level's counters.
+enum BfsMode : int { BFS_NONE = 0, BFS_PUSH = 1, BFS_PULL = 2, BFS_PULL_ACTIVE = 3 };
+
+struct BfsCtl {
+    int mode;
+    int done;
+    uint32_t list_n;       // push entries of this level (copied from cnt)
+    uint32_t active_n;     // active loads of this level
+    unsigned long long unvisited;
+    long long sweeps;
+    uint32_t blocks_done;  // last-block detection in the update kernel
+    BfsCounters cnt;       // written by the level's update, consumed by the next plan
+};
+
+// Top-down sweep over the non-transposed matrix a (bmv_stream.cu): OR of the
+// frontier bit-rows of every listed tile-row chunk scattered into next.
+// Raw: already-visited vertices are masked by the update kernel.
+void launch_bfs_level(b2sr_matrix *at, const b2sr_matrix *a, BfsCtl *ctl, const uint2 *push_list,
+                      const uint32_t *active_list, const void *hx, size_t hb, const void *frontier, void *next,
+                      cudaStream_t s);
+
+}  // namespace b2sr

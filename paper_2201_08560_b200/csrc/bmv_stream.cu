@@ -16,6 +16,7 @@
 //     reference's;
 //   * x words come from the hot-column cache in shared memory (hot.cu) or, for
 //     cold columns, from L1/L2.
+#include "bfs_ctl.cuh"
 #include "bmv_common.cuh"
 
 namespace b2sr {
@@ -309,7 +310,9 @@ __global__ void __launch_bounds__(NT, 1)
     k_bmv_bbb_stream(uint32_t n_loads, const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_n,
                      uint64_t T, const uint4 *__restrict__ desc, const uint32_t *__restrict__ trp,
                      const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci2, const void *__restrict__ hx,
-                     uint32_t hx_bytes16, uint32_t S, const void *__restrict__ x, void *__restrict__ y) {
+                     uint32_t hx_bytes16, uint32_t S, const void *__restrict__ x, void *__restrict__ y,
+                     const int *__restrict__ gate, int want) {
+    if (gate && *gate != want) return;  // device-side BFS direction choice (drivers.cu)
     const uint32_t n_pos = LIST ? *list_n : n_loads;
     if (n_pos == 0) return;
     stage_hot(const_cast<uint8_t *>(hot_bytes()), hx, hx_bytes16);
@@ -319,6 +322,117 @@ __global__ void __launch_bounds__(NT, 1)
     const uint32_t per = (n_pos + warps - 1) / warps;
     const uint32_t p0 = std::min(n_pos, w * per), p1 = std::min(n_pos, p0 + per);
     bbb_stream<D, LIST>(p0, p1, n_loads, T, list, desc, trp, tiles, tci2, gx, y);
+}
+
+// ------------------------------------------------------------ fused BFS level
+// Push body: warp per (frontier tile row, 1024-tile chunk) entry of a; each
+// lane holds TPL consecutive tiles of one 128-bit load; the bit-rows of the
+// frontier word select the tile bytes, folded to the column word and OR'd into
+// next[col] (fire-and-forget RED; visited vertices are masked by the update).
+template <int D>
+__device__ __forceinline__ void push_entries(uint32_t n_entries, const uint2 *__restrict__ plist,
+                                             const uint32_t *__restrict__ trp, const uint32_t *__restrict__ tci,
+                                             const uint8_t *__restrict__ tiles, const void *__restrict__ frontier,
+                                             void *__restrict__ next) {
+    using G = Geo<D>;
+    constexpr int TPL = G::TPL;
+    const uint32_t lane = lane_id();
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < n_entries; e += warps) {
+        const uint2 ent = plist[e];
+        const uint32_t I = ent.x;
+        const uint32_t t0 = __ldg(trp + I) + ent.y * PUSH_CH;
+        const uint32_t t1 = min(__ldg(trp + I + 1), t0 + PUSH_CH);
+        const uint32_t fw = load_word<D>(frontier, I);
+        // 0xFF in the bytes of the frontier bit-rows
+        const uint32_t sl = ((fw & 0xFu) * 0x00204081u & 0x01010101u) * 0xFFu;
+        const uint32_t sh = (((fw >> 4) & 0xFu) * 0x00204081u & 0x01010101u) * 0xFFu;
+        for (uint32_t base = t0 & ~(uint32_t)(TPL - 1); base < t1; base += 2 * G::TPW) {
+            uint4 v[2];
+            uint32_t c[2][TPL];
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                uint32_t tl = base + u * G::TPW + lane * TPL;
+                bool any = tl < t1 && tl + TPL > t0;
+                v[u] = any ? ld_stream128(tiles + (size_t)tl * G::TB) : make_uint4(0, 0, 0, 0);
+                if constexpr (TPL == 4) {
+                    uint4 q = any ? ld_stream128(tci + tl) : make_uint4(0, 0, 0, 0);
+                    c[u][0] = q.x; c[u][1] = q.y; c[u][2] = q.z; c[u][3] = q.w;
+                } else {
+                    uint2 q = any ? *reinterpret_cast<const uint2 *>(tci + tl) : make_uint2(0, 0);
+                    c[u][0] = q.x; c[u][1] = q.y;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                const uint32_t tl = base + u * G::TPW + lane * TPL;
+#pragma unroll
+                for (int j = 0; j < TPL; j++) {
+                    uint32_t m;
+                    if constexpr (D == 4) {
+                        uint32_t w = (j == 0 ? v[u].x : j == 1 ? v[u].y : j == 2 ? v[u].z : v[u].w) & sl;
+                        w |= w >> 16;
+                        m = (w | (w >> 8)) & 0xFFu;
+                    } else {
+                        uint32_t w = ((j == 0 ? v[u].x : v[u].z) & sl) | ((j == 0 ? v[u].y : v[u].w) & sh);
+                        w |= w >> 16;
+                        m = (w | (w >> 8)) & 0xFFu;
+                    }
+                    if (m && tl + j >= t0 && tl + j < t1) atomic_or_word<D>(next, c[u][j], m);
+                }
+            }
+        }
+    }
+}
+
+// One BFS level in one launch: the direction chosen by the device-side plan
+// (BfsCtl::mode) selects the push body, the full flat-stream pull, or the
+// stream over the listed active loads.
+template <int D, int NT>
+__global__ void __launch_bounds__(NT, 1)
+    k_bfs_level(const BfsCtl *__restrict__ ctl, const uint2 *__restrict__ plist, const uint32_t *__restrict__ a_trp,
+                const uint32_t *__restrict__ a_tci, const uint8_t *__restrict__ a_tiles, uint32_t n_loads,
+                const uint32_t *__restrict__ alist, uint64_t T, const uint4 *__restrict__ desc,
+                const uint32_t *__restrict__ trp, const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci2,
+                const void *__restrict__ hx, uint32_t hx_bytes16, uint32_t S, const void *__restrict__ frontier,
+                void *__restrict__ next) {
+    const int mode = ctl->mode;
+    if (mode == BFS_NONE) return;
+    if (mode == BFS_PUSH) {
+        push_entries<D>(ctl->list_n, plist, a_trp, a_tci, a_tiles, frontier, next);
+        return;
+    }
+    const uint32_t n_pos = mode == BFS_PULL_ACTIVE ? ctl->active_n : n_loads;
+    if (n_pos == 0) return;
+    stage_hot(const_cast<uint8_t *>(hot_bytes()), hx, hx_bytes16);
+    __syncthreads();
+    XHot<D> gx(frontier, S);
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5, w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t per = (n_pos + warps - 1) / warps;
+    const uint32_t p0 = std::min(n_pos, w * per), p1 = std::min(n_pos, p0 + per);
+    if (mode == BFS_PULL_ACTIVE) bbb_stream<D, true>(p0, p1, n_loads, T, alist, desc, trp, tiles, tci2, gx, next);
+    else bbb_stream<D, false>(p0, p1, n_loads, T, nullptr, desc, trp, tiles, tci2, gx, next);
+}
+
+void launch_bfs_level(b2sr_matrix *at, const b2sr_matrix *a, BfsCtl *ctl, const uint2 *push_list,
+                      const uint32_t *active_list, const void *hx, size_t hb, const void *frontier, void *next,
+                      cudaStream_t s) {
+    StreamPlan *sp = stream_plan(at, LT, s);
+    HotView hv = hot_view(at, s);
+    const unsigned g = (unsigned)num_sms();
+    const uint32_t *atrp = a ? a->trp : nullptr, *atci = a ? a->tci : nullptr;
+    const uint8_t *atl = a ? (const uint8_t *)a->tiles : nullptr;
+    if (at->dim == 4) {
+        hot_smem_attr(k_bfs_level<4, 1024>, hb);
+        LAUNCH((k_bfs_level<4, 1024>), g, 1024, hb, s, ctl, push_list, atrp, atci, atl, sp->n_loads, active_list,
+               at->num_tiles, sp->desc, at->trp, (const uint8_t *)at->tiles, hv.tci2, hx, (uint32_t)hb, hv.S,
+               frontier, next);
+    } else {
+        hot_smem_attr(k_bfs_level<8, 768>, hb);
+        LAUNCH((k_bfs_level<8, 768>), g, 768, hb, s, ctl, push_list, atrp, atci, atl, sp->n_loads, active_list,
+               at->num_tiles, sp->desc, at->trp, (const uint8_t *)at->tiles, hv.tci2, hx, (uint32_t)hb, hv.S,
+               frontier, next);
+    }
 }
 
 // BFS pull over part of the matrix: the loads holding a tile of a row with an
@@ -375,6 +489,44 @@ __global__ void k_pull_mask(uint32_t nb, uint8_t *__restrict__ y, const uint8_t 
     }
 }
 
+const uint4 *stream_desc(b2sr_matrix *m, cudaStream_t s, uint32_t *n_loads) {
+    StreamPlan *sp = stream_plan(m, LT, s);
+    *n_loads = sp->n_loads;
+    return sp->desc;
+}
+
+// The stream kernel alone: y must be zeroed and hx filled (hot_fill) by the caller.
+void launch_stream_sweep(b2sr_matrix *m, const uint32_t *list, const uint32_t *list_n, const void *hx, size_t hb,
+                         const void *x, void *y, const int *gate, int want, cudaStream_t s) {
+    if (!m->num_tiles) return;
+    StreamPlan *sp = stream_plan(m, LT, s);
+    HotView hv = hot_view(m, s);
+    unsigned g = (unsigned)std::max<uint64_t>(
+        1, std::min<uint64_t>((uint64_t)num_sms(), ((uint64_t)sp->n_loads + 31) / 32));
+    const uint8_t *tl = (const uint8_t *)m->tiles;
+    const char *te = getenv("B2SR_STREAM_THREADS");  // A/B: 768 / 1024 threads per CTA
+    int nt = te ? atoi(te) : (m->dim == 4 ? 1024 : 768);
+#define STREAM_LAUNCH(DD, NT)                                                                                        \
+    do {                                                                                                             \
+        if (list) {                                                                                                  \
+            hot_smem_attr(k_bmv_bbb_stream<DD, NT, true>, hb);                                                       \
+            LAUNCH((k_bmv_bbb_stream<DD, NT, true>), g, NT, hb, s, sp->n_loads, list, list_n, m->num_tiles,          \
+                   sp->desc, m->trp, tl, hv.tci2, hx, (uint32_t)hb, hv.S, x, y, gate, want);                         \
+        } else {                                                                                                     \
+            hot_smem_attr(k_bmv_bbb_stream<DD, NT, false>, hb);                                                      \
+            LAUNCH((k_bmv_bbb_stream<DD, NT, false>), g, NT, hb, s, sp->n_loads, nullptr, nullptr, m->num_tiles,     \
+                   sp->desc, m->trp, tl, hv.tci2, hx, (uint32_t)hb, hv.S, x, y, gate, want);                         \
+        }                                                                                                            \
+    } while (0)
+    if (m->dim == 4) {
+        if (nt == 768) STREAM_LAUNCH(4, 768);
+        else STREAM_LAUNCH(4, 1024);
+    } else {
+        STREAM_LAUNCH(8, 768);
+    }
+#undef STREAM_LAUNCH
+}
+
 void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaStream_t s,
                        const void *visited, bool active_only) {
     const size_t yb = padded_vec_bytes(m->ntr, m->dim);
@@ -396,31 +548,7 @@ void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y,
             LAUNCH(k_active_loads<8>, ga, 256, 0, s, sp->n_loads, sp->desc, visited, m->live, m->row0, list.p, list_n.p);
     }
     hot_fill(hv, m->dim, x, hx.p, s);
-    unsigned g = (unsigned)std::max<uint64_t>(
-        1, std::min<uint64_t>((uint64_t)num_sms(), ((uint64_t)sp->n_loads + 31) / 32));
-    const uint8_t *tl = (const uint8_t *)m->tiles;
-    const char *te = getenv("B2SR_STREAM_THREADS");  // A/B: 512 / 768 / 1024 threads per CTA
-    int nt = te ? atoi(te) : (m->dim == 4 ? 1024 : 768);
-#define STREAM_LAUNCH(DD, NT)                                                                                        \
-    do {                                                                                                             \
-        if (list.p) {                                                                                                \
-            hot_smem_attr(k_bmv_bbb_stream<DD, NT, true>, hb);                                                       \
-            LAUNCH((k_bmv_bbb_stream<DD, NT, true>), g, NT, hb, s, sp->n_loads, list.p, list_n.p, m->num_tiles,      \
-                   sp->desc, m->trp, tl, hv.tci2, hx.p, (uint32_t)hb, hv.S, x, y);                                   \
-        } else {                                                                                                     \
-            hot_smem_attr(k_bmv_bbb_stream<DD, NT, false>, hb);                                                      \
-            LAUNCH((k_bmv_bbb_stream<DD, NT, false>), g, NT, hb, s, sp->n_loads, nullptr, nullptr, m->num_tiles,     \
-                   sp->desc, m->trp, tl, hv.tci2, hx.p, (uint32_t)hb, hv.S, x, y);                                   \
-        }                                                                                                            \
-    } while (0)
-    if (m->dim == 4) {
-        if (nt == 768) STREAM_LAUNCH(4, 768);
-        else STREAM_LAUNCH(4, 1024);
-    } else {
-        if (nt == 1024) STREAM_LAUNCH(8, 1024);
-        else STREAM_LAUNCH(8, 768);
-    }
-#undef STREAM_LAUNCH
+    launch_stream_sweep(m, list.p, list_n.p, hx.p, hb, x, y, nullptr, 0, s);
     if (visited) {  // BFS pull: keep = ~visited & live, applied once at the end
         const uint8_t *vp = static_cast<const uint8_t *>(visited) + (size_t)m->row0 * word_bytes(m->dim);
         const uint32_t nb = (uint32_t)yb;

@@ -19,6 +19,7 @@
 #include <mutex>
 #include <vector>
 
+#include "bfs_ctl.cuh"
 #include "bmv_common.cuh"
 
 namespace b2sr {
@@ -235,15 +236,6 @@ __global__ void k_bfs_seed(uint32_t src, uint32_t d, double *levels, void *visit
 // frontiers: every frontier tile row scatters the OR of its frontier bit-rows
 // into next[K] & ~visited[K].  The set produced is exactly the pull sweep's
 // (A^T x) & ~visited, so levels are unchanged -- only the work differs.
-constexpr uint32_t PUSH_CH = 1024;  // tiles per push work entry (hub rows split)
-
-struct BfsCounters {
-    int any;
-    uint32_t list_n;                     // push work entries
-    unsigned long long frontier_tiles;   // tiles of a in frontier tile rows
-    unsigned long long removed_tiles;    // tiles of at rows whose keep word became zero
-    unsigned long long frontier_vertices;
-};
 
 // visited |= next; levels[new] = level; counters; push work list for the next
 // level.  Each thread owns 16 bytes of `next` (16/16/8/4 words); all-zero
@@ -251,11 +243,14 @@ struct BfsCounters {
 // Unvisited tiles are tracked incrementally: removed_tiles counts the rows of
 // at whose keep word (~visited & live) just became zero.
 template <int D>
-__global__ void k_bfs_update_dir(uint32_t ntr, uint32_t n, const void *__restrict__ next, void *__restrict__ visited,
+__global__ void k_bfs_update_dir(uint32_t ntr, uint32_t n, void *__restrict__ next, void *__restrict__ visited,
                                  double *__restrict__ levels, double level, const uint32_t *__restrict__ trp_a,
                                  const uint32_t *__restrict__ trp_at, const void *__restrict__ live_at,
-                                 uint2 *__restrict__ list, BfsCounters *__restrict__ cnt) {
+                                 uint2 *__restrict__ list, BfsCounters *__restrict__ cnt,
+                                 const int *__restrict__ gate, int mask, BfsCtl *__restrict__ ctl,
+                                 uint4 *__restrict__ zero_buf, double alpha, unsigned long long tiles_at, int has_a) {
     using W = typename WordT<D>::T;
+    if (gate && *gate == 0) return;  // device-controlled BFS: no sweep this level
     constexpr int WB = sizeof(W), WPC = 16 / WB;
     unsigned long long ft = 0, rt = 0, fv = 0;
     int found = 0;
@@ -267,6 +262,17 @@ __global__ void k_bfs_update_dir(uint32_t ntr, uint32_t n, const void *__restric
     for (uint32_t k = 0; k < iters; k++) {
         uint32_t c = c0 + k * stride;
         uint4 nv = c < nchunks ? reinterpret_cast<const uint4 *>(next)[c] : make_uint4(0, 0, 0, 0);
+        if (zero_buf && c < nchunks) zero_buf[c] = make_uint4(0, 0, 0, 0);  // recycled as the next output
+        if (mask && (nv.x | nv.y | nv.z | nv.w)) {
+            // a raw pull sweep: keep only unvisited vertices with in-edges, and
+            // store the masked words back -- they are the next frontier
+            uint4 vv = reinterpret_cast<const uint4 *>(visited)[c], lv = reinterpret_cast<const uint4 *>(live_at)[c];
+            uint4 mv = make_uint4(nv.x & ~vv.x & lv.x, nv.y & ~vv.y & lv.y, nv.z & ~vv.z & lv.z, nv.w & ~vv.w & lv.w);
+            if (mv.x != nv.x || mv.y != nv.y || mv.z != nv.z || mv.w != nv.w) {
+                reinterpret_cast<uint4 *>(next)[c] = mv;
+                nv = mv;
+            }
+        }
         const W *nw = reinterpret_cast<const W *>(&nv);
         uint32_t nch = 0;
         if (nv.x | nv.y | nv.z | nv.w) {
@@ -328,6 +334,34 @@ __global__ void k_bfs_update_dir(uint32_t ntr, uint32_t n, const void *__restric
         if (fv) atomicAdd(&cnt->frontier_vertices, fv);
     }
     if (__any_sync(0xffffffffu, found) && lane == 0) atomicOr(&cnt->any, 1);
+    if (ctl) {  // the last block to finish plans the next level on the device
+        __shared__ bool last;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) last = atomicAdd(&ctl->blocks_done, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (last && threadIdx.x == 0) {
+            __threadfence();
+            volatile BfsCtl *c = ctl;
+            c->blocks_done = 0;
+            if (c->done || !c->cnt.any) {  // this sweep found nothing: BFS is over
+                c->done = 1;
+                c->mode = BFS_NONE;
+            } else {
+                c->unvisited -= c->cnt.removed_tiles;
+                bool push = has_a && (double)c->cnt.frontier_tiles * alpha < (double)c->unvisited;
+                c->mode = push ? BFS_PUSH : (c->unvisited * 2 < tiles_at ? BFS_PULL_ACTIVE : BFS_PULL);
+                c->list_n = c->cnt.list_n;
+                c->active_n = 0;
+                c->sweeps = c->sweeps + 1;
+                c->cnt.any = 0;
+                c->cnt.list_n = 0;
+                c->cnt.frontier_tiles = 0;
+                c->cnt.removed_tiles = 0;
+                c->cnt.frontier_vertices = 0;
+            }
+        }
+    }
 }
 
 // late pull levels: the items of tile rows that still have a keep bit
@@ -361,14 +395,15 @@ __global__ void k_active_items(uint32_t ntr, const void *__restrict__ visited, c
 
 // warp per push entry; lane-strided tiles
 template <int D>
-__global__ void __launch_bounds__(256) k_bfs_push(const uint2 *__restrict__ list, const BfsCounters *__restrict__ cnt,
+__global__ void __launch_bounds__(256) k_bfs_push(const uint2 *__restrict__ list, const uint32_t *__restrict__ list_n,
                                                   const uint32_t *__restrict__ trp, const uint32_t *__restrict__ tci,
                                                   const typename WordT<D>::T *__restrict__ tiles,
                                                   const void *__restrict__ frontier, const void *__restrict__ visited,
-                                                  void *__restrict__ next) {
+                                                  void *__restrict__ next, const int *__restrict__ gate) {
+    if (gate && *gate != 1) return;  // device-controlled BFS: not a push level
     const uint32_t lane = lane_id();
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-    const uint32_t n_entries = cnt->list_n;
+    const uint32_t n_entries = *list_n;
     for (uint32_t e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < n_entries; e += warps) {
         uint2 ent = list[e];
         uint32_t I = ent.x;
@@ -723,6 +758,125 @@ __global__ void k_cc_commit(uint32_t n, const uint32_t *__restrict__ nxt, uint32
     if (__any_sync(0xffffffffu, ch) && lane_id() == 0) atomicOr(changed, 1);
 }
 
+// ================================================================ device-controlled BFS
+// The direction choice of every level (push / full pull / pull over the
+// loads of unvisited rows) is made on the device from the previous level's
+// counters, and every kernel of a level is gated on it, so the host enqueues
+// levels back to back and only polls for termination every few levels --
+// instead of one D2H round trip plus a launch ramp per level.
+__global__ void k_bfs_ctl_init(BfsCtl *c, unsigned long long unvisited) {
+    c->mode = BFS_NONE;
+    c->done = 0;
+    c->list_n = 0;
+    c->active_n = 0;
+    c->unvisited = unvisited;
+    c->sweeps = 0;
+    c->blocks_done = 0;
+    c->cnt = BfsCounters{};
+}
+
+// pull levels: fill the hot x words from the frontier, and for
+// late pull levels list the loads that still hold an unvisited live vertex
+template <int D>
+__global__ void k_bfs_prep(BfsCtl *__restrict__ c, uint32_t S,
+                           const uint32_t *__restrict__ cols, const void *__restrict__ frontier,
+                           uint8_t *__restrict__ hx, uint32_t n_loads, const uint4 *__restrict__ desc,
+                           const void *__restrict__ visited, const void *__restrict__ live,
+                           uint32_t *__restrict__ alist) {
+    const int mode = c->mode;
+    if (mode == BFS_NONE) return;
+    if (mode == BFS_PUSH) return;
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    const uint8_t *fr = static_cast<const uint8_t *>(frontier);
+    if constexpr (D == 4) {
+        for (uint32_t i = tid; i < (S + 1) / 2; i += stride) {
+            uint32_t a = 2 * i, b = 2 * i + 1;
+            uint32_t lo = fr[cols ? cols[a] : a] & 0xFu, hi = b < S ? (fr[cols ? cols[b] : b] & 0xFu) : 0u;
+            hx[i] = (uint8_t)(lo | (hi << 4));
+        }
+    } else {
+        for (uint32_t i = tid; i < S; i += stride) hx[i] = fr[cols ? cols[i] : i];
+    }
+    if (mode != BFS_PULL_ACTIVE) return;
+    const uint32_t lane = lane_id(), iters = (n_loads + stride - 1) / stride;
+    for (uint32_t it = 0; it < iters; it++) {
+        uint32_t k = tid + it * stride;
+        bool act = false;
+        if (k < n_loads) {
+            uint32_t ra = desc[k].x, rb = desc[k + 1].x;
+            for (uint32_t r = ra; r <= rb && !act; r++)
+                act = (~load_word<D>(visited, r) & load_word<D>(live, r)) != 0;
+        }
+        uint32_t bal = __ballot_sync(0xffffffffu, act);
+        if (!bal) continue;
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&c->active_n, (uint32_t)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (act) alist[base + __popc(bal & ((1u << lane) - 1u))] = k;
+    }
+}
+
+template <int D>
+static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, double *d_levels, int64_t *iterations,
+                       cudaStream_t s) {
+    const uint32_t n = at->n, ntr = at->ntr;
+    const size_t vb = padded_vec_bytes(ntr, D);
+    const uint32_t n16 = (uint32_t)((vb + 15) / 16);
+    Buf<uint8_t> visited(n16 * 16, s), fa(n16 * 16, s), fb(n16 * 16, s);
+    Buf<BfsCtl> ctl(1, s);
+    size_t list_cap = a ? (size_t)ntr + a->num_tiles / PUSH_CH + 1 : 1;
+    Buf<uint2> list(list_cap, s);
+    ensure_live(at, s);
+    HotView hv = hot_view(at, s);
+    const size_t hb = hot_fill_bytes(hv, D);
+    Buf<uint8_t> hx(hb, s);
+    CK(cudaMemsetAsync(hx.p, 0, hb, s));
+    uint32_t n_loads = 0;
+    const uint4 *desc = stream_desc(at, s, &n_loads);
+    Buf<uint32_t> alist(std::max<uint32_t>(n_loads, 1), s);
+    const double alpha = bfs_alpha();
+    const bool trace = getenv("B2SR_BFS_TRACE") != nullptr;
+    LAUNCH(k_fill_f64, grid_for(n), 256, 0, s, d_levels, (size_t)n, HUGE_VAL);
+    CK(cudaMemsetAsync(visited.p, 0, n16 * 16, s));
+    CK(cudaMemsetAsync(fb.p, 0, n16 * 16, s));
+    CK(cudaMemsetAsync(fa.p, 0, n16 * 16, s));
+    LAUNCH(k_bfs_seed, 1, 1, 0, s, src, (uint32_t)D, d_levels, fa.p, fb.p);
+    CK(cudaMemsetAsync(fa.p, 0, n16 * 16, s));
+    LAUNCH(k_bfs_ctl_init, 1, 1, 0, s, ctl.p, (unsigned long long)at->live_tiles);
+    const unsigned gu = grid_for(ntr);
+    const uint32_t *ta = a ? a->trp : nullptr;
+    // level 0 = {src}: visited, levels, counters, the push list of level 1 and its plan
+    LAUNCH(k_bfs_update_dir<D>, gu, 256, 0, s, ntr, n, fb.p, visited.p, d_levels, 0.0, ta, at->trp, at->live, list.p,
+           &ctl.p->cnt, nullptr, 0, ctl.p, nullptr, alpha, (unsigned long long)at->num_tiles, a ? 1 : 0);
+    void *frontier = fb.p, *next = fa.p;
+    const unsigned gp = (unsigned)num_sms() * 8;
+    BfsCtl h{};
+    for (uint32_t L = 1;; L++) {
+        LAUNCH(k_bfs_prep<D>, gp, 256, 0, s, ctl.p, hv.S, hv.cols, frontier, hx.p, n_loads, desc, visited.p, at->live,
+               alist.p);
+        launch_bfs_level(at, a, ctl.p, list.p, alist.p, hx.p, hb, frontier, next, s);
+        LAUNCH(k_bfs_update_dir<D>, gu, 256, 0, s, ntr, n, next, visited.p, d_levels, (double)L, ta, at->trp,
+               at->live, list.p, &ctl.p->cnt, &ctl.p->mode, 1, ctl.p, (uint4 *)frontier, alpha,
+               (unsigned long long)at->num_tiles, a ? 1 : 0);
+        std::swap(frontier, next);
+        if (trace || (L >= 4 && L % 2 == 0)) {  // poll for the end every other level
+            CK(cudaMemcpyAsync(&h, ctl.p, sizeof(BfsCtl), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (trace)
+                fprintf(stderr, "[b2sr bfs] after level %u: next mode %d unvisited_tiles=%llu done=%d\n", L, h.mode,
+                        h.unvisited, h.done);
+            if (h.done) break;
+        }
+        if (L > n + 2) B2SR_THROW(B2SR_ENOCONV, "BFS failed to drain its frontier");
+    }
+    *iterations = h.sweeps;
+}
+
+static bool bfs_devctl_enabled(const b2sr_matrix *at) {
+    const char *e = getenv("B2SR_BFS_DEVCTL");  // B2SR_BFS_DEVCTL=0: host-controlled levels (A/B)
+    return pull_stream(at) && !(e && e[0] == '0');
+}
+
 }  // namespace b2sr
 
 using namespace b2sr;
@@ -739,6 +893,11 @@ int b2sr_bfs(const b2sr_matrix *a_c, const b2sr_matrix *at_c, uint32_t src, doub
     if (a && (a->n != at->n || a->dim != at->dim || a->row0 != 0 || a->ntr != at->ntr))
         B2SR_THROW(B2SR_EINVAL, "a and at must be the same full matrix and its transpose");
     if (src >= at->n) B2SR_THROW(B2SR_EINVAL, "source vertex %u out of range for n=%u", src, at->n);
+    if (bfs_devctl_enabled(at)) {
+        if (at->dim == 4) bfs_devctl<4>(a, at, src, d_levels, iterations, s);
+        else bfs_devctl<8>(a, at, src, d_levels, iterations, s);
+        return B2SR_OK;
+    }
     uint32_t n = at->n, d = at->dim, ntr = at->ntr;
     size_t vb = padded_vec_bytes(ntr, d);
     Buf<uint8_t> visited(vb, s), fa(vb, s), fb(vb, s);
@@ -763,10 +922,10 @@ int b2sr_bfs(const b2sr_matrix *a_c, const b2sr_matrix *at_c, uint32_t src, doub
         unsigned g = grid_for(ntr);
         const uint32_t *ta = a ? a->trp : nullptr;
         switch (d) {
-            case 4: LAUNCH(k_bfs_update_dir<4>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, at->live, list.p, cnt.p); break;
-            case 8: LAUNCH(k_bfs_update_dir<8>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, at->live, list.p, cnt.p); break;
-            case 16: LAUNCH(k_bfs_update_dir<16>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, at->live, list.p, cnt.p); break;
-            default: LAUNCH(k_bfs_update_dir<32>, g, 256, 0, s, ntr, n, fr, visited.p, d_levels, level, ta, at->trp, at->live, list.p, cnt.p); break;
+            case 4: LAUNCH(k_bfs_update_dir<4>, g, 256, 0, s, ntr, n, const_cast<void *>(fr), visited.p, d_levels, level, ta, at->trp, at->live, list.p, cnt.p, nullptr, 0, nullptr, nullptr, 0.0, 0ull, 0); break;
+            case 8: LAUNCH(k_bfs_update_dir<8>, g, 256, 0, s, ntr, n, const_cast<void *>(fr), visited.p, d_levels, level, ta, at->trp, at->live, list.p, cnt.p, nullptr, 0, nullptr, nullptr, 0.0, 0ull, 0); break;
+            case 16: LAUNCH(k_bfs_update_dir<16>, g, 256, 0, s, ntr, n, const_cast<void *>(fr), visited.p, d_levels, level, ta, at->trp, at->live, list.p, cnt.p, nullptr, 0, nullptr, nullptr, 0.0, 0ull, 0); break;
+            default: LAUNCH(k_bfs_update_dir<32>, g, 256, 0, s, ntr, n, const_cast<void *>(fr), visited.p, d_levels, level, ta, at->trp, at->live, list.p, cnt.p, nullptr, 0, nullptr, nullptr, 0.0, 0ull, 0); break;
         }
         CK(cudaMemcpyAsync(&h, cnt.p, sizeof(BfsCounters), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -805,10 +964,10 @@ int b2sr_bfs(const b2sr_matrix *a_c, const b2sr_matrix *at_c, uint32_t src, doub
             uint64_t blocks = ((uint64_t)h.list_n + 7) / 8, cap = (uint64_t)num_sms() * 16;
             unsigned g = (unsigned)std::max<uint64_t>(1, std::min(blocks, cap));
             switch (d) {
-                case 4: LAUNCH(k_bfs_push<4>, g, 256, 0, s, list.p, cnt.p, a->trp, a->tci, (const uint8_t *)a->tiles, frontier, visited.p, next); break;
-                case 8: LAUNCH(k_bfs_push<8>, g, 256, 0, s, list.p, cnt.p, a->trp, a->tci, (const uint8_t *)a->tiles, frontier, visited.p, next); break;
-                case 16: LAUNCH(k_bfs_push<16>, g, 256, 0, s, list.p, cnt.p, a->trp, a->tci, (const uint16_t *)a->tiles, frontier, visited.p, next); break;
-                default: LAUNCH(k_bfs_push<32>, g, 256, 0, s, list.p, cnt.p, a->trp, a->tci, (const uint32_t *)a->tiles, frontier, visited.p, next); break;
+                case 4: LAUNCH(k_bfs_push<4>, g, 256, 0, s, list.p, &cnt.p->list_n, a->trp, a->tci, (const uint8_t *)a->tiles, frontier, visited.p, next, nullptr); break;
+                case 8: LAUNCH(k_bfs_push<8>, g, 256, 0, s, list.p, &cnt.p->list_n, a->trp, a->tci, (const uint8_t *)a->tiles, frontier, visited.p, next, nullptr); break;
+                case 16: LAUNCH(k_bfs_push<16>, g, 256, 0, s, list.p, &cnt.p->list_n, a->trp, a->tci, (const uint16_t *)a->tiles, frontier, visited.p, next, nullptr); break;
+                default: LAUNCH(k_bfs_push<32>, g, 256, 0, s, list.p, &cnt.p->list_n, a->trp, a->tci, (const uint32_t *)a->tiles, frontier, visited.p, next, nullptr); break;
             }
         } else if (sparse_pull) {
             bfs_sweep(at, frontier, visited.p, next, s, act_idx.p, act_n.p);
