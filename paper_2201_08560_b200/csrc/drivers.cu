@@ -775,18 +775,128 @@ __global__ void k_bfs_ctl_init(BfsCtl *c, unsigned long long unvisited) {
     c->cnt = BfsCounters{};
 }
 
+// Level update of the device-controlled BFS.  Per 16-byte chunk of the raw
+// sweep output: keep unvisited live vertices (stored back: the next frontier),
+// visited |= it (one vector RMW), levels of the new vertices, counters for the
+// plan; the recycled output buffer of the next level is zeroed on the way.
+// The last block to finish plans the next level (push / pull / active pull).
+template <int D>
+__global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *__restrict__ visited,
+                                double *__restrict__ levels, double level, const uint32_t *__restrict__ trp_a,
+                                const uint32_t *__restrict__ trp_at, const uint4 *__restrict__ live_at,
+                                BfsCtl *__restrict__ ctl, uint4 *__restrict__ zero_buf, int mask, double alpha,
+                                unsigned long long tiles_at, int has_a) {
+    using W = typename WordT<D>::T;
+    if (ctl->mode == BFS_NONE && mask) return;  // BFS already over
+    constexpr int WPC = 16 / sizeof(W);
+    unsigned long long ft = 0, rt = 0, fv = 0;
+    int found = 0;
+    const uint32_t lane = lane_id();
+    const uint32_t nchunks = (ntr + WPC - 1) / WPC;
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += gridDim.x * blockDim.x) {
+        uint4 nv = next[c];
+        if (zero_buf) zero_buf[c] = make_uint4(0, 0, 0, 0);  // recycled as the next level's output
+        if (!(nv.x | nv.y | nv.z | nv.w)) continue;
+        const uint4 vv = visited[c], lv = live_at[c];
+        if (mask) {
+            uint4 mv = make_uint4(nv.x & ~vv.x & lv.x, nv.y & ~vv.y & lv.y, nv.z & ~vv.z & lv.z, nv.w & ~vv.w & lv.w);
+            if (mv.x != nv.x || mv.y != nv.y || mv.z != nv.z || mv.w != nv.w) next[c] = mv;
+            nv = mv;
+            if (!(nv.x | nv.y | nv.z | nv.w)) continue;
+        }
+        visited[c] = make_uint4(vv.x | nv.x, vv.y | nv.y, vv.z | nv.z, vv.w | nv.w);
+        found = 1;
+        const W *nw = reinterpret_cast<const W *>(&nv);
+        const W *vw = reinterpret_cast<const W *>(&vv);
+        const W *lw = reinterpret_cast<const W *>(&lv);
+#pragma unroll
+        for (int j = 0; j < WPC; j++) {
+            const uint32_t w = nw[j], I = c * WPC + j;
+            if (!w) continue;  // words past ntr are zero (padding)
+            fv += __popc(w);
+            uint32_t b = w;
+            while (b) {
+                int kk = __ffs(b) - 1;
+                b &= b - 1;
+                levels[(size_t)I * D + kk] = level;
+            }
+            const uint32_t old = vw[j], l = lw[j];
+            if ((~old & l) && !(~(old | w) & l)) rt += __ldg(trp_at + I + 1) - __ldg(trp_at + I);
+            if (trp_a) ft += __ldg(trp_a + I + 1) - __ldg(trp_a + I);
+        }
+    }
+    ft = __reduce_add_sync(0xffffffffu, (uint32_t)ft);  // per-warp sums < T < 2^32
+    rt = __reduce_add_sync(0xffffffffu, (uint32_t)rt);
+    fv = __reduce_add_sync(0xffffffffu, (uint32_t)fv);
+    BfsCounters *cnt = &ctl->cnt;
+    if (lane == 0) {
+        if (ft) atomicAdd(&cnt->frontier_tiles, ft);
+        if (rt) atomicAdd(&cnt->removed_tiles, rt);
+        if (fv) atomicAdd(&cnt->frontier_vertices, fv);
+    }
+    if (__any_sync(0xffffffffu, found) && lane == 0) atomicOr(&cnt->any, 1);
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&ctl->blocks_done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last && threadIdx.x == 0) {  // the last block plans the next level
+        __threadfence();
+        volatile BfsCtl *cv = ctl;
+        cv->blocks_done = 0;
+        if (cv->done || !cv->cnt.any) {  // this sweep found nothing: BFS is over
+            cv->done = 1;
+            cv->mode = BFS_NONE;
+        } else {
+            cv->unvisited -= cv->cnt.removed_tiles;
+            bool push = has_a && (double)cv->cnt.frontier_tiles * alpha < (double)cv->unvisited;
+            cv->mode = push ? BFS_PUSH : (cv->unvisited * 2 < tiles_at ? BFS_PULL_ACTIVE : BFS_PULL);
+            cv->list_n = 0;
+            cv->active_n = 0;
+            cv->sweeps = cv->sweeps + 1;
+            cv->cnt.any = 0;
+            cv->cnt.frontier_tiles = 0;
+            cv->cnt.removed_tiles = 0;
+            cv->cnt.frontier_vertices = 0;
+        }
+    }
+}
+
 // pull levels: fill the hot x words from the frontier, and for
 // late pull levels list the loads that still hold an unvisited live vertex
 template <int D>
-__global__ void k_bfs_prep(BfsCtl *__restrict__ c, uint32_t S,
+__global__ void k_bfs_prep(BfsCtl *__restrict__ c, uint32_t ntr, const uint32_t *__restrict__ a_trp,
+                           uint2 *__restrict__ plist, uint32_t S,
                            const uint32_t *__restrict__ cols, const void *__restrict__ frontier,
                            uint8_t *__restrict__ hx, uint32_t n_loads, const uint4 *__restrict__ desc,
                            const void *__restrict__ visited, const void *__restrict__ live,
                            uint32_t *__restrict__ alist) {
     const int mode = c->mode;
     if (mode == BFS_NONE) return;
-    if (mode == BFS_PUSH) return;
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    const uint32_t lane = lane_id();
+    if (mode == BFS_PUSH) {  // work list: (frontier tile row of a, 1024-tile chunk)
+        const uint32_t iters = (ntr + stride - 1) / stride;
+        for (uint32_t it = 0; it < iters; it++) {
+            uint32_t I = tid + it * stride, nch = 0, len = 0;
+            if (I < ntr && load_word<D>(frontier, I)) {
+                len = a_trp[I + 1] - a_trp[I];
+                nch = (len + PUSH_CH - 1) / PUSH_CH;
+            }
+            if (!__any_sync(0xffffffffu, nch != 0)) continue;
+            uint32_t incl = nch;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (uint32_t)o) incl += y;
+            }
+            uint32_t total = __shfl_sync(0xffffffffu, incl, 31), base = 0;
+            if (lane == 31) base = atomicAdd(&c->list_n, total);
+            base = __shfl_sync(0xffffffffu, base, 31);
+            for (uint32_t q = 0; q < nch; q++) plist[base + incl - nch + q] = make_uint2(I, q);
+        }
+        return;
+    }
     const uint8_t *fr = static_cast<const uint8_t *>(frontier);
     if constexpr (D == 4) {
         for (uint32_t i = tid; i < (S + 1) / 2; i += stride) {
@@ -798,7 +908,7 @@ __global__ void k_bfs_prep(BfsCtl *__restrict__ c, uint32_t S,
         for (uint32_t i = tid; i < S; i += stride) hx[i] = fr[cols ? cols[i] : i];
     }
     if (mode != BFS_PULL_ACTIVE) return;
-    const uint32_t lane = lane_id(), iters = (n_loads + stride - 1) / stride;
+    const uint32_t iters = (n_loads + stride - 1) / stride;
     for (uint32_t it = 0; it < iters; it++) {
         uint32_t k = tid + it * stride;
         bool act = false;
@@ -846,17 +956,17 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     const unsigned gu = grid_for(ntr);
     const uint32_t *ta = a ? a->trp : nullptr;
     // level 0 = {src}: visited, levels, counters, the push list of level 1 and its plan
-    LAUNCH(k_bfs_update_dir<D>, gu, 256, 0, s, ntr, n, fb.p, visited.p, d_levels, 0.0, ta, at->trp, at->live, list.p,
-           &ctl.p->cnt, nullptr, 0, ctl.p, nullptr, alpha, (unsigned long long)at->num_tiles, a ? 1 : 0);
+    LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)fb.p, (uint4 *)visited.p, d_levels, 0.0, ta, at->trp,
+           (const uint4 *)at->live, ctl.p, nullptr, 0, alpha, (unsigned long long)at->num_tiles, a ? 1 : 0);
     void *frontier = fb.p, *next = fa.p;
     const unsigned gp = (unsigned)num_sms() * 8;
     BfsCtl h{};
     for (uint32_t L = 1;; L++) {
-        LAUNCH(k_bfs_prep<D>, gp, 256, 0, s, ctl.p, hv.S, hv.cols, frontier, hx.p, n_loads, desc, visited.p, at->live,
-               alist.p);
+        LAUNCH(k_bfs_prep<D>, gp, 256, 0, s, ctl.p, ntr, ta, list.p, hv.S, hv.cols, frontier, hx.p, n_loads, desc,
+               visited.p, at->live, alist.p);
         launch_bfs_level(at, a, ctl.p, list.p, alist.p, hx.p, hb, frontier, next, s);
-        LAUNCH(k_bfs_update_dir<D>, gu, 256, 0, s, ntr, n, next, visited.p, d_levels, (double)L, ta, at->trp,
-               at->live, list.p, &ctl.p->cnt, &ctl.p->mode, 1, ctl.p, (uint4 *)frontier, alpha,
+        LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L, ta,
+               at->trp, (const uint4 *)at->live, ctl.p, (uint4 *)frontier, 1, alpha,
                (unsigned long long)at->num_tiles, a ? 1 : 0);
         std::swap(frontier, next);
         if (trace || (L >= 4 && L % 2 == 0)) {  // poll for the end every other level
