@@ -46,7 +46,7 @@ METRIC = "bin-SpMV GB/s vs HBM peak; BFS GTEPS and TC edges/s at 1/2/4/8 B200"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=16)
+    p.add_argument("--steps", type=int, default=64)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
     p.add_argument("--scale", type=int, default=22)
@@ -71,44 +71,66 @@ def peaks():
 
 # ---------------------------------------------------------------- clocks
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """NVML sampler (every 2 ms) of SM clock and clock-event reasons, running
+    during the timed region; falls back to nvidia-smi -lms when NVML is absent."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, gpu: int):
-        self.gpu, self.rows, self.proc = gpu, [], None
+    def __init__(self, cuda_index: int):
+        self.cuda_index, self.sm, self.reasons, self.max = cuda_index, [], set(), None
+        self._stop = threading.Event()
+        self.t = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            idx = torch.cuda._get_nvml_device_index(self.cuda_index)
+            self.nv, self.h = pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.t = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+    def _sample(self):
+        nv = self.nv
+        self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        for name, attr in self.REASONS:
+            if r & getattr(nv, attr, 0):
+                self.reasons.add(name)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self._sample()
+            except Exception:
+                return
+            time.sleep(0.002)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            self.proc.wait(timeout=5)
+        self._stop.set()
+        if self.t:
+            self.t.join(timeout=2)
+            if not self.sm:
+                try:
+                    self._sample()
+                except Exception:
+                    pass
 
     def summary(self):
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": "nvml, 2 ms"}
 
 
 # ---------------------------------------------------------------- helpers
@@ -121,6 +143,19 @@ def pick_roots(deg: np.ndarray, k: int, seed: int):
 def traversed_edges(levels: np.ndarray, deg: np.ndarray) -> int:
     """Undirected edges inside the traversed component (Graph500 TEPS numerator)."""
     return int(deg[np.isfinite(levels)].sum() // 2)
+
+
+def measured_traffic(kernel: str, scale: int, d: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from the
+    committed ncu --set full capture (profiles/*_traffic.json), or None."""
+    for f in sorted((ROOT / "profiles").glob("*_traffic.json"), reverse=True):
+        try:
+            for row in json.loads(f.read_text()):
+                if row["kernel"] == kernel and row["scale"] == scale and row["tile_dim"] == d:
+                    return row["dram_bytes"]
+        except Exception:
+            continue
+    return None
 
 
 def bmv_alg_bytes(ntr: int, T: int, d: int) -> int:
@@ -206,6 +241,7 @@ def run_ours(args, rank, world, local_rank):
         edges = 0
         lvd = dev.empty_bytes(8 * n)
         itc = ctypes.c_int64()
+        _capi.call("b2sr_bfs", hA.ptr, h.ptr, roots[-1], dev.ptr(lvd), ctypes.addressof(itc), sp)  # warm plans
         for r in roots[:4]:
             b0, b1 = ev(), ev()
             b0.record()
@@ -283,8 +319,9 @@ def run_ours(args, rank, world, local_rank):
     achieved = ab / kms / 1e6
     roofline = {"bound": "hbm", "kernel": f"k_bmv_bbb<{d}> (masked full sweep)", "achieved": round(achieved, 1),
                 "peak": pk["hbm_gbs"], "peak_kind": pk_kind, "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
-                "frac_of_8tbs_nominal": round(achieved / 8000.0, 4), "alg_bytes": ab, "traffic": None,
-                "kernel_ms": round(kms, 4)}
+                "frac_of_8tbs_nominal": round(achieved / 8000.0, 4), "alg_bytes": ab,
+                "traffic": measured_traffic(f"k_bmv_bbb_stream<{d}>", args.scale, d), "kernel_ms": round(kms, 4),
+                "timed": "b2sr_bmv_bbb call (memset, hot fill, stream kernel, keep AND)"}
 
     # ---- e2e: public API with host inputs ----
     host = (m.tile_row_ptr.copy(), m.tile_col_ind.copy(), m.bit_tiles.copy())
@@ -443,6 +480,142 @@ def cpu_baseline(csr, d, root):
             "seconds": round(dt, 3)}
 
 
+# ---------------------------------------------------------------- multi-GPU arm
+def run_dist(args, rank, world, local_rank):
+    """N > 1: row-partitioned BFS (dist.py), Graph500-style weak scaling: the
+    graph has scale + log2(N) (per-GPU vertices fixed), each rank owns an equal
+    block of tile rows of the transposed adjacency, and one all-gather of
+    frontier words per level joins the blocks.  value = traversed edges of the
+    whole job / max-over-ranks device time."""
+    import torch
+    import torch.distributed as tdist
+
+    import paper_2201_08560_b200 as b2
+    from paper_2201_08560_b200 import _capi, rmat
+    from paper_2201_08560_b200 import _device as dev
+    from paper_2201_08560_b200 import dist as bdist
+
+    local_rank %= max(1, torch.cuda.device_count())  # several ranks may share a GPU in gloo tests
+    torch.cuda.set_device(local_rank)
+    backend = os.environ.get("B2SR_DIST_BACKEND", "nccl")  # gloo: several ranks on one GPU (tests)
+    if backend == "nccl":
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    else:
+        tdist.init_process_group(backend)
+    sp = torch.cuda.current_stream().cuda_stream
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def barrier():
+        tdist.barrier()
+        torch.cuda.synchronize()
+
+    scale = args.scale + max(0, int(round(np.log2(world))))
+    d = args.dim or 4
+    t0 = time.time()
+    csr = rmat.rmat_csr(scale, args.edgefactor, seed=args.seed)
+    n = csr.n
+    deg = np.diff(csr.row_ptr.astype(np.int64))
+    m = b2.csr_to_b2sr(csr, d)
+    at = b2.b2sr_transpose(m)
+    del csr
+    b, e = bdist.partition(at.n_tile_rows, world, d)[rank]
+    blk = b2.formats._new_handle("b2sr_row_block", at.handle().ptr, b, e, dev.stream())
+    host_blk = bdist.block_to_host(blk)  # the caller's copy of this rank's block (e2e leg)
+    b2sr_bytes = b2.storage_bytes(m)
+    del m, at
+    torch.cuda.empty_cache()
+    gen_s = time.time() - t0
+    db = bdist.DistributedBfs.from_block(blk, n, d, tdist)
+    roots = pick_roots(deg, args.warmup + args.steps + 8, seed=args.seed + 7)
+    degt = torch.from_numpy(deg).to("cuda")
+    for r in roots[: args.warmup]:
+        db.run(r, to_host=False)
+    barrier()
+    launches0 = _capi.launch_count()
+    outs, iters = [], []
+    with Clocks(local_rank) as clk:
+        e0, e1 = ev(), ev()
+        e0.record()
+        for r in roots[args.warmup: args.warmup + args.steps]:
+            lv, it = db.run(r, to_host=False)
+            outs.append(lv.clone())
+            iters.append(it)
+        e1.record()
+        barrier()
+    launches = _capi.launch_count() - launches0
+    ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+    tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
+    ms = float(ms.item())
+    edges = sum(int(degt[torch.isfinite(lv)].sum().item()) // 2 for lv in outs)
+    del outs
+    value = edges / (ms / 1e3) / 1e9
+
+    # e2e: every step each rank uploads its own block from pinned host memory,
+    # runs the distributed BFS and rank 0 reads the levels back
+    e2e_steps = max(3, min(args.steps, 6))
+    barrier()
+    f0, f1 = ev(), ev()
+    f0.record()
+    e2e_edges = 0
+    for r in roots[args.warmup: args.warmup + e2e_steps]:
+        hb = bdist.block_from_host(n, d, b, e, host_blk)
+        lv, _ = bdist.DistributedBfs.from_block(hb, n, d, tdist).run(r, to_host=(rank == 0))
+        if rank == 0:
+            e2e_edges += traversed_edges(lv, deg)
+        del hb
+    f1.record()
+    barrier()
+    e2e_ms = torch.tensor([f0.elapsed_time(f1)], device="cuda")
+    tdist.all_reduce(e2e_ms, op=tdist.ReduceOp.MAX)
+    e2e_ms = float(e2e_ms.item())
+    h2d = int(sum(h[1].nbytes for h in host_blk)) * world
+    roofline = None
+    if rank == 0:  # K4 masked sweep over this rank's block (x, keep: global 50 % random)
+        pk, pk_kind = peaks()
+        rng = np.random.default_rng(11)
+        gb = dev.padded_vec_bytes(-(-n // d), d)
+        xd = dev.to_device(b2.BitVector.from_bools(rng.random(n) < 0.5, d).words, gb)
+        kd = dev.to_device(b2.BitVector.from_bools(rng.random(n) < 0.5, d).words, gb)
+        yd = dev.empty_bytes(dev.padded_vec_bytes(blk.ntr, d) + 16)
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+        kt = []
+        for i in range(10):
+            flush.zero_()
+            a0, a1 = ev(), ev()
+            a0.record()
+            _capi.call("b2sr_bmv_bbb", blk.ptr, dev.ptr(xd), dev.ptr(kd), dev.ptr(yd), sp)
+            a1.record()
+            torch.cuda.synchronize()
+            if i >= 2:
+                kt.append(a0.elapsed_time(a1))
+        kms = float(np.mean(kt))
+        ab = bmv_alg_bytes(blk.ntr, blk.num_tiles, d)
+        roofline = {"bound": "hbm", "kernel": f"k_bmv_bbb_stream<{d}> (masked sweep of rank 0's block)",
+                    "achieved": round(ab / kms / 1e6, 1), "peak": pk["hbm_gbs"], "peak_kind": pk_kind, "unit": "GB/s",
+                    "frac": round(ab / kms / 1e6 / pk["hbm_gbs"], 4), "alg_bytes": ab,
+                    "traffic": measured_traffic(f"k_bmv_bbb_stream<{d}>", scale, d), "kernel_ms": round(kms, 4),
+                    "timed": "b2sr_bmv_bbb call (memset, hot fill, stream kernel, keep AND)"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u32 bit-words (b1 tiles)",
+                "data": f"synthetic R-MAT (Graph500 a,b,c=.57,.19,.19) generated on device, seed {args.seed}",
+                "config": {"workload": f"row-partitioned BFS, undirected R-MAT scale {scale} (= {args.scale} + "
+                                       f"log2 N) edgefactor {args.edgefactor}, B2SR-{d}",
+                           "scale": scale, "n": n, "tile_dim": d, "roots": args.steps,
+                           "parallelism": f"row-partitioned x{world}, frontier all-gather ({backend})",
+                           "l2": "inputs larger than L2 (B2SR %.2f GB)" % (b2sr_bytes / 1e9)},
+                "e2e": {"value": round(e2e_edges / (e2e_ms / 1e3) / 1e9, 4), "unit": "GTEPS",
+                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * n,
+                        "ms_per_step": round(e2e_ms / e2e_steps, 3),
+                        "includes": "H2D of every rank's B2SR row block from pinned memory, distributed BFS, "
+                                    "D2H of the levels on rank 0"},
+                "roofline": roofline, "gpu_launches": int(launches), "bfs_sweeps_per_root": iters[:4],
+                "clocks": clk.summary(), "graph_gen_s": round(gen_s, 3)}
+        print(json.dumps(line), flush=True)
+    tdist.destroy_process_group()
+
+
 # ---------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
     """The reference algorithm on host cores: the C restatement in oracle/ (the
@@ -493,6 +666,9 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if world > 1:
+        run_dist(args, rank, world, local_rank)
         return
     run_ours(args, rank, world, local_rank)
 

@@ -91,6 +91,12 @@ int b2sr_drop_diagonal(const b2sr_matrix *m, void *stream, b2sr_matrix **out);
 int b2sr_row_block(const b2sr_matrix *m, uint32_t tr_begin, uint32_t tr_end, void *stream,
                    b2sr_matrix **out);
 int b2sr_row_offset(const b2sr_matrix *m, uint32_t *tr_begin);
+/* A row block [tr_begin, tr_end) uploaded from host arrays (tile_row_ptr
+ * local to the block, starting at 0): the multi-GPU end-to-end path, where
+ * every rank copies only its own block of the caller's matrix. */
+int b2sr_block_from_host(uint32_t n, uint32_t dim, uint32_t tr_begin, uint32_t tr_end, const uint32_t *h_trp,
+                         const uint32_t *h_tci, const void *h_tiles, uint64_t num_tiles, void *stream,
+                         b2sr_matrix **out);
 /* used_columns (kernels.py:86-94): d_out u8[n] (0/1). */
 int b2sr_used_columns(const b2sr_matrix *m, uint8_t *d_out, void *stream);
 

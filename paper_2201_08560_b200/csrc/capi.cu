@@ -247,4 +247,29 @@ int b2sr_row_block(const b2sr_matrix *m, uint32_t tr_begin, uint32_t tr_end, voi
     API_END
 }
 
+int b2sr_block_from_host(uint32_t n, uint32_t dim, uint32_t tr_begin, uint32_t tr_end, const uint32_t *h_trp,
+                         const uint32_t *h_tci, const void *h_tiles, uint64_t num_tiles, void *stream,
+                         b2sr_matrix **out) {
+    API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dim != 4 && dim != 8 && dim != 16 && dim != 32) B2SR_THROW(B2SR_EINVAL, "tile dim must be 4/8/16/32");
+    if (n == 0) B2SR_THROW(B2SR_EFORMAT, "matrix dimension must be positive");
+    if (tr_begin > tr_end || tr_end > tile_rows(n, dim)) B2SR_THROW(B2SR_EINVAL, "row block out of range");
+    uint32_t rows = tr_end - tr_begin;
+    b2sr_matrix *m = new_matrix(n, dim, rows, num_tiles, s);
+    m->row0 = tr_begin;
+    try {
+        CK(cudaMemcpyAsync(m->trp, h_trp, ((size_t)rows + 1) * 4, cudaMemcpyHostToDevice, s));
+        if (num_tiles) {
+            CK(cudaMemcpyAsync(m->tci, h_tci, num_tiles * 4, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(m->tiles, h_tiles, num_tiles * dim * word_bytes(dim), cudaMemcpyHostToDevice, s));
+        }
+    } catch (...) {
+        free_matrix(m);
+        throw;
+    }
+    *out = m;
+    API_END
+}
+
 }  // extern "C"

@@ -77,6 +77,9 @@ class CudaBfsOps:
     def levels_to_host(self, levels):
         return dev.to_host(levels, np.float64, self.n)
 
+    def levels_on_device(self, levels):
+        return levels.view(dev.torch().float64)[: self.n]
+
 
 def all_gather_words(dist, out, block, world):
     """Concatenate every rank's block into ``out`` (byte tensors)."""
@@ -108,7 +111,16 @@ class DistributedBfs:
         blk = _new_handle("b2sr_row_block", at.handle().ptr, b, e, dev.stream())
         return cls(at.n, at.dim, at.n_tile_rows, rank, world, CudaBfsOps(blk, at.n, at.dim), dist)
 
-    def run(self, src: int):
+    @classmethod
+    def from_block(cls, block: _Handle, n: int, dim: int, dist):
+        """A rank's own row block (e.g. uploaded with b2sr_block_from_host)."""
+        rank, world = dist.get_rank(), dist.get_world_size()
+        ntr = -(-n // dim)
+        return cls(n, dim, ntr, rank, world, CudaBfsOps(block, n, dim), dist)
+
+    def run(self, src: int, to_host: bool = True):
+        """Levels (float64, inf = unreached) and the sweep count; with
+        ``to_host=False`` the levels stay on the device (product ops only)."""
         ops = self.ops
         visited, frontier, nxt, levels, anyflag = ops.buffers(self.global_bytes, self.block_bytes)
         ops.init(src, visited, frontier, levels)
@@ -122,7 +134,31 @@ class DistributedBfs:
                 raise RuntimeError("BFS failed to drain its frontier")
             if not more:
                 break
+        if not to_host:
+            return ops.levels_on_device(levels), sweeps
         return ops.levels_to_host(levels), sweeps
+
+
+def block_to_host(block: _Handle, pinned: bool = True):
+    """(trp, tci, tiles) host copies of a device row block, in pinned memory."""
+    t = dev.torch()
+
+    def buf(count, dtype):
+        a = t.empty(max(count, 1) * np.dtype(dtype).itemsize, dtype=t.uint8, pin_memory=pinned)
+        return a, a.numpy().view(dtype)[:count]
+
+    wdt = {4: np.uint8, 8: np.uint8, 16: np.uint16, 32: np.uint32}[block.dim]
+    trp, tci, tiles = buf(block.ntr + 1, np.uint32), buf(block.num_tiles, np.uint32), buf(block.num_tiles * block.dim, wdt)
+    _capi.call("b2sr_to_host", block.ptr, trp[1].ctypes.data, tci[1].ctypes.data, tiles[1].ctypes.data, dev.stream())
+    t.cuda.synchronize()
+    return trp, tci, tiles
+
+
+def block_from_host(n: int, dim: int, begin: int, end: int, host) -> _Handle:
+    """Upload a rank's row block from host arrays (b2sr_block_from_host)."""
+    trp, tci, tiles = (h[1] for h in host)
+    return _new_handle("b2sr_block_from_host", n, dim, begin, end, trp.ctypes.data, tci.ctypes.data,
+                       tiles.ctypes.data, len(tci), dev.stream())
 
 
 def distributed_triangle_count(lower: B2srMatrix, dist) -> int:

@@ -90,3 +90,56 @@ def test_scale21_blocked_kernels_opt_in(monkeypatch):
     monkeypatch.setenv("B2SR_BLOCKED", "1")
     test_scale21_blocked_path_against_oracle(4)
     test_scale21_blocked_path_against_oracle(16)
+
+
+def _dist_bfs_worker(rank, world, port, scale, d, src, q):
+    import os
+
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2201_08560_b200 import dist as bdist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    csr = rmat.rmat_csr(scale, 16, seed=5)
+    at = b2.b2sr_transpose(b2.csr_to_b2sr(csr, d))
+    lv, it = bdist.DistributedBfs.from_matrix(at, tdist).run(src)
+    # the e2e leg: a rank's block re-uploaded from host arrays gives the same levels
+    b, e = bdist.partition(at.n_tile_rows, world, d)[rank]
+    blk = b2.formats._new_handle("b2sr_row_block", at.handle().ptr, b, e, 0)
+    hb = bdist.block_from_host(csr.n, d, b, e, bdist.block_to_host(blk))
+    lv2, it2 = bdist.DistributedBfs.from_block(hb, csr.n, d, tdist).run(src)
+    if rank == 0:
+        q.put((lv.tobytes(), it, lv2.tobytes(), it2))
+    tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("d", [4, 8, 32])
+def test_row_partitioned_bfs_two_ranks_one_gpu(d):
+    """dist.py with the real kernels: 2 ranks (gloo, sharing cuda:0) give the
+    oracle's levels and sweep count, also from blocks uploaded from host."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    scale = 14
+    rp, ci = orc.rmat_csr(scale, 16, seed=5)
+    n = 1 << scale
+    src = int(np.argmax(np.diff(rp.astype(np.int64))))
+    lv_ref, it_ref = orc.bfs(orc.csr_to_b2sr(n, rp, ci, d), src)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_dist_bfs_worker, args=(r, 2, port, scale, d, src, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = q.get(timeout=300)
+    for p in ps:
+        p.join(timeout=60)
+    assert got[0] == lv_ref.tobytes() and got[1] == it_ref
+    assert got[2] == lv_ref.tobytes() and got[3] == it_ref
