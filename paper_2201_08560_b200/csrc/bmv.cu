@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(256) k_bmv_bff(uint32_t ntr, uint32_t n, const
 constexpr uint32_t LONG_ROW_TILES = 512;
 constexpr int LONG_THREADS = 256;
 
-constexpr uint32_t VLONG_ROW_TILES = 16384;  // longer rows: bmv_vlong.cu (segmented scatter + fold)
+constexpr uint32_t VLONG_ROW_TILES = 512;  // longer rows: bmv_vlong.cu (segmented scatter + fold)
 
 __global__ void k_find_long(uint32_t ntr, const uint32_t *trp, uint32_t lo, uint32_t hi, uint32_t *rows,
                             uint32_t *count) {

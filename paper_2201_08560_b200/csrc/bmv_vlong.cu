@@ -41,9 +41,43 @@ void free_vlong(void *p) {
     delete v;
 }
 
-__global__ void k_find_vlong(uint32_t ntr, const uint32_t *trp, uint32_t thresh, uint32_t *rows, uint32_t *count) {
+__global__ void k_vlong_flags(uint32_t ntr, const uint32_t *__restrict__ trp, uint32_t thresh, uint32_t *__restrict__ f) {
     for (uint32_t I = blockIdx.x * blockDim.x + threadIdx.x; I < ntr; I += gridDim.x * blockDim.x)
-        if (trp[I + 1] - trp[I] > thresh) rows[atomicAdd(count, 1u)] = I;
+        f[I] = trp[I + 1] - trp[I] > thresh ? 1u : 0u;
+}
+
+// rows (ascending) and their unit counts
+__global__ void k_vlong_rows(uint32_t ntr, const uint32_t *__restrict__ trp, const uint32_t *__restrict__ f,
+                             const uint64_t *__restrict__ pos, uint32_t *__restrict__ rows, uint32_t *__restrict__ nu) {
+    for (uint32_t I = blockIdx.x * blockDim.x + threadIdx.x; I < ntr; I += gridDim.x * blockDim.x)
+        if (f[I]) {
+            uint32_t i = (uint32_t)pos[I];
+            rows[i] = I;
+            nu[i] = (trp[I + 1] - trp[I] + VSEG - 1) / VSEG;
+        }
+}
+
+__global__ void k_vlong_units(uint32_t nr, const uint32_t *__restrict__ rows, const uint32_t *__restrict__ trp,
+                              const uint64_t *__restrict__ uofs, uint4 *__restrict__ units) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x) {
+        uint32_t t0 = trp[rows[i]], t1 = trp[rows[i] + 1];
+        uint64_t u = uofs[i];
+        for (uint32_t t = t0; t < t1; t += VSEG, u++) units[u] = make_uint4(i, t, min(t1, t + VSEG), 0);
+    }
+}
+
+// per (row, bit-row): offsets of its units inside the region, and the region length
+template <int D>
+__global__ void k_vlong_offsets(uint32_t nr, const uint64_t *__restrict__ uofs, const uint32_t *__restrict__ cnt,
+                                uint32_t *__restrict__ unit_off, uint32_t *__restrict__ total) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nr * D; k += gridDim.x * blockDim.x) {
+        uint32_t i = k / D, r = k % D, off = 0;
+        for (uint64_t u = uofs[i]; u < uofs[i + 1]; u++) {
+            unit_off[u * D + r] = off;
+            off += cnt[u * D + r];
+        }
+        total[k] = off;
+    }
 }
 
 // per (unit, bit-row) term counts
@@ -79,63 +113,54 @@ __global__ void __launch_bounds__(VTHREADS) k_vlong_counts(uint32_t n_units, con
 void *build_vlong(b2sr_matrix *m, uint32_t thresh, cudaStream_t s) {
     const uint32_t D = m->dim, ntr = m->ntr;
     VLongPlan *v = new VLongPlan();
+    auto grid = [](uint64_t work) {
+        return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, (uint64_t)num_sms() * 16));
+    };
     try {
-        Buf<uint32_t> rows(ntr, s), cnt1(1, s);
-        CK(cudaMemsetAsync(cnt1.p, 0, 4, s));
-        unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((ntr + 255) / 256, (uint64_t)num_sms() * 16));
-        LAUNCH(k_find_vlong, g, 256, 0, s, ntr, m->trp, thresh, rows.p, cnt1.p);
-        uint32_t nr = read_scalar(cnt1.p, s);
+        Buf<uint32_t> f(ntr, s);
+        Buf<uint64_t> pos((size_t)ntr + 1, s);
+        LAUNCH(k_vlong_flags, grid(ntr), 256, 0, s, ntr, m->trp, thresh, f.p);
+        exclusive_scan_u32_to_u64(f.p, pos.p, ntr, s);
+        const uint32_t nr = (uint32_t)read_scalar(pos.p + ntr, s);
         v->n_rows = nr;
         if (nr) {
-            std::vector<uint32_t> h_rows(nr), h_t0(nr), h_t1(nr);
-            CK(cudaMemcpyAsync(h_rows.data(), rows.p, nr * 4, cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            for (uint32_t i = 0; i < nr; i++) {
-                CK(cudaMemcpyAsync(&h_t0[i], m->trp + h_rows[i], 4, cudaMemcpyDeviceToHost, s));
-                CK(cudaMemcpyAsync(&h_t1[i], m->trp + h_rows[i] + 1, 4, cudaMemcpyDeviceToHost, s));
-            }
-            CK(cudaStreamSynchronize(s));
-            std::vector<uint4> h_units;
-            for (uint32_t i = 0; i < nr; i++)
-                for (uint32_t t = h_t0[i]; t < h_t1[i]; t += VSEG)
-                    h_units.push_back(make_uint4(i, t, std::min(h_t1[i], t + VSEG), 0));
-            v->n_units = (uint32_t)h_units.size();
-            v->rows = static_cast<uint32_t *>(dalloc(nr * 4, s));
-            v->units = static_cast<uint4 *>(dalloc(h_units.size() * 16, s));
-            CK(cudaMemcpyAsync(v->rows, h_rows.data(), nr * 4, cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(v->units, h_units.data(), h_units.size() * 16, cudaMemcpyHostToDevice, s));
-            Buf<uint32_t> cnt((size_t)v->n_units * D, s);
+            Buf<uint32_t> rows(nr, s), nu(nr, s);
+            Buf<uint64_t> uofs((size_t)nr + 1, s);
+            LAUNCH(k_vlong_rows, grid(ntr), 256, 0, s, ntr, m->trp, f.p, pos.p, rows.p, nu.p);
+            exclusive_scan_u32_to_u64(nu.p, uofs.p, nr, s);
+            v->n_units = (uint32_t)read_scalar(uofs.p + nr, s);
+            Buf<uint4> units(v->n_units, s);
+            LAUNCH(k_vlong_units, grid(nr), 256, 0, s, nr, rows.p, m->trp, uofs.p, units.p);
+            Buf<uint32_t> cnt((size_t)v->n_units * D, s), unit_off((size_t)v->n_units * D, s), total((size_t)nr * D, s);
             unsigned gu = std::min<unsigned>(v->n_units, (unsigned)num_sms() * 8);
             switch (D) {
-                case 4: LAUNCH(k_vlong_counts<4>, gu, VTHREADS, 0, s, v->n_units, v->units, (const uint8_t *)m->tiles, cnt.p); break;
-                case 8: LAUNCH(k_vlong_counts<8>, gu, VTHREADS, 0, s, v->n_units, v->units, (const uint8_t *)m->tiles, cnt.p); break;
-                case 16: LAUNCH(k_vlong_counts<16>, gu, VTHREADS, 0, s, v->n_units, v->units, (const uint16_t *)m->tiles, cnt.p); break;
-                default: LAUNCH(k_vlong_counts<32>, gu, VTHREADS, 0, s, v->n_units, v->units, (const uint32_t *)m->tiles, cnt.p); break;
+                case 4:
+                    LAUNCH(k_vlong_counts<4>, gu, VTHREADS, 0, s, v->n_units, units.p, (const uint8_t *)m->tiles, cnt.p);
+                    LAUNCH(k_vlong_offsets<4>, grid(nr * 4), 256, 0, s, nr, uofs.p, cnt.p, unit_off.p, total.p);
+                    break;
+                case 8:
+                    LAUNCH(k_vlong_counts<8>, gu, VTHREADS, 0, s, v->n_units, units.p, (const uint8_t *)m->tiles, cnt.p);
+                    LAUNCH(k_vlong_offsets<8>, grid(nr * 8), 256, 0, s, nr, uofs.p, cnt.p, unit_off.p, total.p);
+                    break;
+                case 16:
+                    LAUNCH(k_vlong_counts<16>, gu, VTHREADS, 0, s, v->n_units, units.p, (const uint16_t *)m->tiles, cnt.p);
+                    LAUNCH(k_vlong_offsets<16>, grid(nr * 16), 256, 0, s, nr, uofs.p, cnt.p, unit_off.p, total.p);
+                    break;
+                default:
+                    LAUNCH(k_vlong_counts<32>, gu, VTHREADS, 0, s, v->n_units, units.p, (const uint32_t *)m->tiles, cnt.p);
+                    LAUNCH(k_vlong_offsets<32>, grid(nr * 32), 256, 0, s, nr, uofs.p, cnt.p, unit_off.p, total.p);
+                    break;
             }
-            std::vector<uint32_t> h_cnt((size_t)v->n_units * D), h_off((size_t)v->n_units * D), h_tot((size_t)nr * D, 0);
-            CK(cudaMemcpyAsync(h_cnt.data(), cnt.p, h_cnt.size() * 4, cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            for (uint32_t u = 0; u < v->n_units; u++)  // units of a row are consecutive, in tile order
-                for (uint32_t r = 0; r < D; r++) {
-                    uint32_t row = h_units[u].x;
-                    h_off[(size_t)u * D + r] = h_tot[(size_t)row * D + r];
-                    h_tot[(size_t)row * D + r] += h_cnt[(size_t)u * D + r];
-                }
-            std::vector<uint64_t> h_base((size_t)nr * D);
-            uint64_t run = 0;
-            for (size_t k = 0; k < h_base.size(); k++) {
-                h_base[k] = run;
-                run += h_tot[k];
-            }
-            v->n_terms = run;
-            v->unit_off = static_cast<uint32_t *>(dalloc(h_off.size() * 4, s));
-            v->base = static_cast<uint64_t *>(dalloc(h_base.size() * 8, s));
-            v->total = static_cast<uint32_t *>(dalloc(h_tot.size() * 4, s));
-            v->terms = static_cast<double *>(dalloc(std::max<uint64_t>(run, 1) * 8, s));
-            CK(cudaMemcpyAsync(v->unit_off, h_off.data(), h_off.size() * 4, cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(v->base, h_base.data(), h_base.size() * 8, cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(v->total, h_tot.data(), h_tot.size() * 4, cudaMemcpyHostToDevice, s));
-            CK(cudaStreamSynchronize(s));  // host vectors die here
+            Buf<uint64_t> base((size_t)nr * D + 1, s);
+            exclusive_scan_u32_to_u64(total.p, base.p, (size_t)nr * D, s);
+            v->n_terms = read_scalar(base.p + (size_t)nr * D, s);
+            v->terms = static_cast<double *>(dalloc(std::max<uint64_t>(v->n_terms, 1) * 8, s));
+            v->rows = rows.release();
+            v->units = units.release();
+            v->unit_off = unit_off.release();
+            v->base = base.release();
+            v->total = total.release();
+            CK(cudaStreamSynchronize(s));  // scratch buffers die here
         }
     } catch (...) {
         free_vlong(v);
@@ -209,6 +234,10 @@ __global__ void __launch_bounds__(VTHREADS) k_vlong_scatter(uint32_t n_units, co
     }
 }
 
+// RING_MIN_COMBINE: the min-plus step without the increment (combining
+// partial minima that already include it)
+constexpr int RING_MIN_COMBINE = B2SR_RING_MAXTIMES + 1;
+
 template <int RING>
 __device__ __forceinline__ double vring_op(double cur, double term, double inc) {
     if constexpr (RING == B2SR_RING_ARITHMETIC) {
@@ -216,37 +245,78 @@ __device__ __forceinline__ double vring_op(double cur, double term, double inc) 
     } else if constexpr (RING == B2SR_RING_MINPLUS) {
         double t = __dadd_rn(term, inc);
         return (cur < t || isnan(cur)) ? cur : t;
+    } else if constexpr (RING == RING_MIN_COMBINE) {
+        return (cur < term || isnan(cur)) ? cur : term;
     } else {
         return (cur > term || isnan(cur)) ? cur : term;
     }
 }
 
-// one thread per (row, bit-row): the reference-order fold
+// One warp per (row, bit-row) over its contiguous term region.
+//  * ARITHMETIC: the reference-order fold (kernels.py:195-207) is a dependent
+//    chain of float64 adds (8 cycles each on B200); lanes keep four chunks of
+//    32 terms in flight (coalesced) and every lane applies them in order from
+//    shuffles, so the chain itself is the only serial part.
+//  * MINPLUS / MAXTIMES: the reference's np.minimum / np.maximum step
+//    f(cur, t) = (cur < t || isnan(cur)) ? cur : t (ties to the later term, the
+//    first NaN sticks) is associative, so each lane folds one contiguous
+//    segment and the segments are combined in order by a shuffle tree --
+//    bit-identical to the sequential fold.
 template <int D, int RING>
-__global__ void k_vlong_fold(uint32_t n_rows, const uint32_t *__restrict__ rows, const uint64_t *__restrict__ base,
-                             const uint32_t *__restrict__ total, const double *__restrict__ terms, double inc, uint32_t n,
-                             const void *__restrict__ keep, double *__restrict__ y, uint32_t row0) {
+__global__ void __launch_bounds__(256) k_vlong_fold(uint32_t n_rows, const uint32_t *__restrict__ rows,
+                                                    const uint64_t *__restrict__ base,
+                                                    const uint32_t *__restrict__ total,
+                                                    const double *__restrict__ terms, double inc, uint32_t n,
+                                                    const void *__restrict__ keep, double *__restrict__ y,
+                                                    uint32_t row0) {
     const double ident = RING == B2SR_RING_MINPLUS ? __longlong_as_double(0x7FF0000000000000ll) : 0.0;
-    uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n_rows * D) return;
-    uint32_t i = k / D, r = k % D, I = rows[i];
-    const double *p = terms + base[k];
-    uint32_t nt = total[k];
-    double acc = ident;
-    uint32_t q = 0;
-    for (; q + 4 <= nt; q += 4) {  // loads batched ahead of the dependent adds
-        double a = p[q], b = p[q + 1], c = p[q + 2], d = p[q + 3];
-        acc = vring_op<RING>(acc, a, inc);
-        acc = vring_op<RING>(acc, b, inc);
-        acc = vring_op<RING>(acc, c, inc);
-        acc = vring_op<RING>(acc, d, inc);
-    }
-    for (; q < nt; q++) acc = vring_op<RING>(acc, p[q], inc);
-    uint32_t grow = row0 + I;
-    uint64_t vrow = (uint64_t)grow * D + r;
-    if (vrow < n) {
-        if (keep && !((load_word<D>(keep, grow) >> r) & 1u)) acc = ident;
-        y[(size_t)I * D + r] = acc;
+    const uint32_t lane = lane_id();
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_rows * D; k += warps) {
+        const uint32_t i = k / D, r = k % D, I = rows[i];
+        const double *p = terms + base[k];
+        const uint32_t nt = total[k];
+        double acc = ident;
+        if constexpr (RING == B2SR_RING_ARITHMETIC) {
+            double c0 = lane < nt ? p[lane] : 0.0, c1 = 32 + lane < nt ? p[32 + lane] : 0.0;
+            double c2 = 64 + lane < nt ? p[64 + lane] : 0.0, c3 = 96 + lane < nt ? p[96 + lane] : 0.0;
+            for (uint32_t q = 0; q < nt; q += 32) {
+                double c4 = q + 128 + lane < nt ? p[q + 128 + lane] : 0.0;  // four chunks ahead
+                const uint32_t m = min(32u, nt - q);
+                if (m == 32) {
+#pragma unroll
+                    for (int j0 = 0; j0 < 32; j0 += 8) {
+                        double t[8];
+#pragma unroll
+                        for (int j = 0; j < 8; j++) t[j] = __shfl_sync(0xffffffffu, c0, j0 + j);
+#pragma unroll
+                        for (int j = 0; j < 8; j++) acc = __dadd_rn(acc, t[j]);
+                    }
+                } else {
+                    for (uint32_t j = 0; j < m; j++) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, c0, j));
+                }
+                c0 = c1;
+                c1 = c2;
+                c2 = c3;
+                c3 = c4;
+            }
+        } else {
+            const uint32_t seg = (nt + 31) / 32, a = min(nt, lane * seg), b = min(nt, a + seg);
+            for (uint32_t q = a; q < b; q++) acc = vring_op<RING>(acc, p[q], inc);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {  // ordered combine: lane l's segments precede lane l+o's
+                double other = __shfl_down_sync(0xffffffffu, acc, o);
+                if (lane + o < 32) acc = vring_op<RING == B2SR_RING_MINPLUS ? RING_MIN_COMBINE : RING>(acc, other, 0.0);
+            }
+        }
+        if (lane == 0) {
+            uint32_t grow = row0 + I;
+            uint64_t vrow = (uint64_t)grow * D + r;
+            if (vrow < n) {
+                if (keep && !((load_word<D>(keep, grow) >> r) & 1u)) acc = ident;
+                y[(size_t)I * D + r] = acc;
+            }
+        }
     }
 }
 
@@ -255,19 +325,19 @@ void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const v
     VLongPlan *v = static_cast<VLongPlan *>(m->vlong);
     if (!v || !v->n_rows) return;
     unsigned gu = std::min<unsigned>(v->n_units, (unsigned)num_sms() * 8);
-    unsigned gf = (v->n_rows * m->dim + 127) / 128;
+    unsigned gf = (unsigned)std::min<uint64_t>(((uint64_t)v->n_rows * m->dim + 7) / 8, (uint64_t)num_sms() * 8);
 #define VL_CASE(DD, W)                                                                                            \
     case DD:                                                                                                      \
         LAUNCH(k_vlong_scatter<DD>, gu, VTHREADS, 0, s, v->n_units, v->units, v->unit_off, v->base, m->tci,      \
                (const W *)m->tiles, x, v->terms);                                                                 \
         if (ring == B2SR_RING_ARITHMETIC)                                                                         \
-            LAUNCH((k_vlong_fold<DD, B2SR_RING_ARITHMETIC>), gf, 128, 0, s, v->n_rows, v->rows, v->base, v->total, \
+            LAUNCH((k_vlong_fold<DD, B2SR_RING_ARITHMETIC>), gf, 256, 0, s, v->n_rows, v->rows, v->base, v->total, \
                    v->terms, inc, m->n, keep, y, m->row0);                                                        \
         else if (ring == B2SR_RING_MINPLUS)                                                                       \
-            LAUNCH((k_vlong_fold<DD, B2SR_RING_MINPLUS>), gf, 128, 0, s, v->n_rows, v->rows, v->base, v->total,   \
+            LAUNCH((k_vlong_fold<DD, B2SR_RING_MINPLUS>), gf, 256, 0, s, v->n_rows, v->rows, v->base, v->total,   \
                    v->terms, inc, m->n, keep, y, m->row0);                                                        \
         else                                                                                                      \
-            LAUNCH((k_vlong_fold<DD, B2SR_RING_MAXTIMES>), gf, 128, 0, s, v->n_rows, v->rows, v->base, v->total,  \
+            LAUNCH((k_vlong_fold<DD, B2SR_RING_MAXTIMES>), gf, 256, 0, s, v->n_rows, v->rows, v->base, v->total,  \
                    v->terms, inc, m->n, keep, y, m->row0);                                                        \
         break;
     switch (m->dim) {
