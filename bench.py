@@ -81,7 +81,7 @@ class Clocks:
                ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
     def __init__(self, cuda_index: int):
-        self.cuda_index, self.sm, self.reasons, self.max = cuda_index, [], set(), None
+        self.cuda_index, self.sm, self.reasons, self.max, self.errors = cuda_index, [], set(), None, set()
         self._stop = threading.Event()
         self.t = None
 
@@ -103,7 +103,14 @@ class Clocks:
     def _sample(self):
         nv = self.nv
         self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
-        r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        try:
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            try:
+                r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+            except Exception as e:
+                self.errors.add(type(e).__name__)
+                return
         for name, attr in self.REASONS:
             if r & getattr(nv, attr, 0):
                 self.reasons.add(name)
@@ -112,8 +119,8 @@ class Clocks:
         while not self._stop.is_set():
             try:
                 self._sample()
-            except Exception:
-                return
+            except Exception as e:
+                self.errors.add(type(e).__name__)
             time.sleep(0.002)
 
     def __exit__(self, *a):
@@ -129,8 +136,11 @@ class Clocks:
     def summary(self):
         if not self.sm:
             return {"sm_mhz": None, "sm_max_mhz": self.max, "reasons": ["unsampled"]}
-        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
-                "samples": len(self.sm), "source": "nvml, 2 ms"}
+        out = {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.max, "reasons": sorted(self.reasons),
+               "samples": len(self.sm), "source": "nvml, 2 ms"}
+        if self.errors:
+            out["nvml_errors"] = sorted(self.errors)
+        return out
 
 
 # ---------------------------------------------------------------- helpers
@@ -156,6 +166,28 @@ def measured_traffic(kernel: str, scale: int, d: int):
         except Exception:
             continue
     return None
+
+
+def k4_time(_capi, dev, torch, h, xd, kd, yd, flush, sp, reps=10):
+    """Masked K4 sweeps with an L2 flush before each: (mean streaming-kernel ms
+    from the library's CUDA-event bracket on the launch stream, mean ms of the
+    whole b2sr_bmv_bbb call incl. its small memset / hot-fill / keep kernels)."""
+    _capi.call("b2sr_set_kernel_timing", 1)
+    kt, ct = [], []
+    ms = ctypes.c_float()
+    for i in range(reps + 2):
+        flush.zero_()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        _capi.call("b2sr_bmv_bbb", h.ptr, dev.ptr(xd), dev.ptr(kd), dev.ptr(yd), sp)
+        a1.record()
+        torch.cuda.synchronize()
+        _capi.call("b2sr_last_kernel_ms", ctypes.addressof(ms))
+        if i >= 2:
+            kt.append(ms.value)
+            ct.append(a0.elapsed_time(a1))
+    _capi.call("b2sr_set_kernel_timing", 0)
+    return float(np.mean(kt)), float(np.mean(ct))
 
 
 def bmv_alg_bytes(ntr: int, T: int, d: int) -> int:
@@ -224,17 +256,7 @@ def run_ours(args, rank, world, local_rank):
         xd = dev.to_device(xw, dev.padded_vec_bytes(ntr, d))
         kd = dev.to_device(kw, dev.padded_vec_bytes(ntr, d))
         yd = dev.empty_bytes(dev.padded_vec_bytes(ntr, d))
-        times = []
-        for i in range(8):
-            flush.zero_()
-            a0, a1 = ev(), ev()
-            a0.record()
-            _capi.call("b2sr_bmv_bbb", h.ptr, dev.ptr(xd), dev.ptr(kd), dev.ptr(yd), sp)
-            a1.record()
-            torch.cuda.synchronize()
-            if i >= 2:
-                times.append(a0.elapsed_time(a1))
-        spmv_ms = float(np.mean(times))
+        spmv_ms, spmv_call_ms = k4_time(_capi, dev, torch, h, xd, kd, yd, flush, sp, reps=6)
         ab = bmv_alg_bytes(ntr, T, d)
         # BFS from a few roots
         bt = []
@@ -251,7 +273,7 @@ def run_ours(args, rank, world, local_rank):
             bt.append(b0.elapsed_time(b1))
             edges += traversed_edges(dev.to_host(lvd, np.float64, n), deg)
         sweep[d] = {"tiles": int(T), "b2sr_bytes": int(b2.storage_bytes(m)), "convert_ms": round(conv_ms, 3),
-                    "transpose_ms": round(tr_ms, 3), "spmv_ms": round(spmv_ms, 4),
+                    "transpose_ms": round(tr_ms, 3), "spmv_ms": round(spmv_ms, 4), "spmv_call_ms": round(spmv_call_ms, 4),
                     "spmv_gbs": round(ab / spmv_ms / 1e6, 1), "spmv_frac": round(ab / spmv_ms / 1e6 / pk["hbm_gbs"], 3),
                     "bfs_ms": round(float(np.mean(bt[1:] or bt)), 3),
                     "bfs_gteps": round(edges / (sum(bt) / 1e3) / 1e9, 3)}
@@ -304,24 +326,16 @@ def run_ours(args, rank, world, local_rank):
     xd = dev.to_device(b2.BitVector.from_bools(rng.random(n) < 0.5, d).words, dev.padded_vec_bytes(ntr, d))
     kd = dev.to_device(b2.BitVector.from_bools(rng.random(n) < 0.5, d).words, dev.padded_vec_bytes(ntr, d))
     yd = dev.empty_bytes(dev.padded_vec_bytes(ntr, d))
-    kt = []
-    for i in range(12):
-        flush.zero_()
-        a0, a1 = ev(), ev()
-        a0.record()
-        _capi.call("b2sr_bmv_bbb", h.ptr, dev.ptr(xd), dev.ptr(kd), dev.ptr(yd), sp)
-        a1.record()
-        torch.cuda.synchronize()
-        if i >= 2:
-            kt.append(a0.elapsed_time(a1))
-    kms = float(np.mean(kt))
+    kms, call_ms = k4_time(_capi, dev, torch, h, xd, kd, yd, flush, sp, reps=10)
     ab = bmv_alg_bytes(ntr, T, d)
     achieved = ab / kms / 1e6
-    roofline = {"bound": "hbm", "kernel": f"k_bmv_bbb<{d}> (masked full sweep)", "achieved": round(achieved, 1),
+    roofline = {"bound": "hbm", "kernel": f"k_bmv_bbb_stream<{d}> (masked full sweep, R-MAT s{args.scale})", "achieved": round(achieved, 1),
                 "peak": pk["hbm_gbs"], "peak_kind": pk_kind, "unit": "GB/s", "frac": round(achieved / pk["hbm_gbs"], 4),
                 "frac_of_8tbs_nominal": round(achieved / 8000.0, 4), "alg_bytes": ab,
                 "traffic": measured_traffic(f"k_bmv_bbb_stream<{d}>", args.scale, d), "kernel_ms": round(kms, 4),
-                "timed": "b2sr_bmv_bbb call (memset, hot fill, stream kernel, keep AND)"}
+                "call_ms": round(call_ms, 4), "call_frac": round(ab / call_ms / 1e6 / pk["hbm_gbs"], 4),
+                "timed": "CUDA events around the streaming kernel on its launch stream (b2sr_set_kernel_timing); "
+                         "call_ms: the whole b2sr_bmv_bbb call incl. memset, hot fill and keep AND kernels"}
 
     # ---- e2e: public API with host inputs ----
     host = (m.tile_row_ptr.copy(), m.tile_col_ind.copy(), m.bit_tiles.copy())
@@ -578,23 +592,14 @@ def run_dist(args, rank, world, local_rank):
         kd = dev.to_device(b2.BitVector.from_bools(rng.random(n) < 0.5, d).words, gb)
         yd = dev.empty_bytes(dev.padded_vec_bytes(blk.ntr, d) + 16)
         flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-        kt = []
-        for i in range(10):
-            flush.zero_()
-            a0, a1 = ev(), ev()
-            a0.record()
-            _capi.call("b2sr_bmv_bbb", blk.ptr, dev.ptr(xd), dev.ptr(kd), dev.ptr(yd), sp)
-            a1.record()
-            torch.cuda.synchronize()
-            if i >= 2:
-                kt.append(a0.elapsed_time(a1))
-        kms = float(np.mean(kt))
+        kms, call_ms = k4_time(_capi, dev, torch, blk, xd, kd, yd, flush, sp, reps=8)
         ab = bmv_alg_bytes(blk.ntr, blk.num_tiles, d)
         roofline = {"bound": "hbm", "kernel": f"k_bmv_bbb_stream<{d}> (masked sweep of rank 0's block)",
                     "achieved": round(ab / kms / 1e6, 1), "peak": pk["hbm_gbs"], "peak_kind": pk_kind, "unit": "GB/s",
                     "frac": round(ab / kms / 1e6 / pk["hbm_gbs"], 4), "alg_bytes": ab,
                     "traffic": measured_traffic(f"k_bmv_bbb_stream<{d}>", scale, d), "kernel_ms": round(kms, 4),
-                    "timed": "b2sr_bmv_bbb call (memset, hot fill, stream kernel, keep AND)"}
+                    "call_ms": round(call_ms, 4),
+                    "timed": "CUDA events around the streaming kernel on its launch stream (b2sr_set_kernel_timing)"}
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,

@@ -57,6 +57,11 @@ int b2sr_version(void);
 /* Number of kernel launches issued by this process so far (evidence for
  * bench.py's "gpu_launches"). */
 uint64_t b2sr_launch_count(void);
+/* Measurement hook: when on, the calling thread's bin-SpMV calls bracket
+ * their main streaming kernel with CUDA events on the launch stream, and
+ * b2sr_last_kernel_ms returns that kernel's duration (waits for it). */
+int b2sr_set_kernel_timing(int on);
+int b2sr_last_kernel_ms(float *ms);
 
 /* ---- matrices (formats.py:228-329, 444-489) ---------------------------- */
 /* csr_to_b2sr (formats.py:444-464): device CSR (row_ptr u32[n+1], col_ind

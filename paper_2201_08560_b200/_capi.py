@@ -40,6 +40,8 @@ SIGNATURES = {
     "b2sr_to_csr_fill": [P, P, P, P],
     "b2sr_drop_diagonal": [P, P, PP],
     "b2sr_row_block": [P, u32, u32, P, PP],
+    "b2sr_set_kernel_timing": [ctypes.c_int],
+    "b2sr_last_kernel_ms": [P],
     "b2sr_block_from_host": [u32, u32, u32, u32, P, P, P, u64, P, PP],
     "b2sr_row_offset": [P, P],
     "b2sr_used_columns": [P, P, P],

@@ -65,6 +65,15 @@ extern std::atomic<uint64_t> g_launches;
         }                                                                  \
     } while (0)
 
+// Per-thread CUDA-event bracket around one streaming kernel (b2sr_set_kernel_timing).
+struct KernelTimer {
+    bool on = false, recorded = false;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    void begin(cudaStream_t s);
+    void end(cudaStream_t s);
+};
+KernelTimer &kernel_timer();
+
 // ---------------------------------------------------------------- memory
 void *dalloc(size_t bytes, cudaStream_t s);
 void dfree(void *p, cudaStream_t s);

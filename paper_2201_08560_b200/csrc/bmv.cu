@@ -603,6 +603,7 @@ void launch_bbb(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaSt
     unsigned g = item_grid(m);
     const char *xg_env = getenv("B2SR_XGATHER");  // cache policy of the x gathers (A/B)
     int xg = xg_env ? atoi(xg_env) : 0;
+    kernel_timer().begin(s);
 #define BBB_LAUNCH(DD, XX) \
     LAUNCH((k_bmv_bbb<DD, XX>), g, 256, 0, s, m->items, m->n_items, tl, m->tci, x, keep, y, m->row0)
 #define BBB_CASE(DD)                                  \
@@ -617,6 +618,7 @@ void launch_bbb(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaSt
         BBB_CASE(16)
         BBB_CASE(32)
     }
+    kernel_timer().end(s);
 #undef BBB_CASE
 #undef BBB_LAUNCH
 }

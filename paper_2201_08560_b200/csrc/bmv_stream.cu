@@ -548,7 +548,9 @@ void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y,
             LAUNCH(k_active_loads<8>, ga, 256, 0, s, sp->n_loads, sp->desc, visited, m->live, m->row0, list.p, list_n.p);
     }
     hot_fill(hv, m->dim, x, hx.p, s);
+    kernel_timer().begin(s);
     launch_stream_sweep(m, list.p, list_n.p, hx.p, hb, x, y, nullptr, 0, s);
+    kernel_timer().end(s);
     if (visited) {  // BFS pull: keep = ~visited & live, applied once at the end
         const uint8_t *vp = static_cast<const uint8_t *>(visited) + (size_t)m->row0 * word_bytes(m->dim);
         const uint32_t nb = (uint32_t)yb;

@@ -11,6 +11,26 @@ namespace b2sr {
 static thread_local std::string t_err;
 std::atomic<uint64_t> g_launches{0};
 
+KernelTimer &kernel_timer() {
+    static thread_local KernelTimer t;
+    return t;
+}
+
+void KernelTimer::begin(cudaStream_t s) {
+    if (!on) return;
+    if (!e0) {
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+    }
+    CK(cudaEventRecord(e0, s));
+}
+
+void KernelTimer::end(cudaStream_t s) {
+    if (!on) return;
+    CK(cudaEventRecord(e1, s));
+    recorded = true;
+}
+
 void set_error(int code, const char *fmt, ...) {
     (void)code;
     char buf[1024];
@@ -138,6 +158,21 @@ extern "C" {
 const char *b2sr_last_error(void) { return t_err.c_str(); }
 int b2sr_version(void) { return 100; }
 uint64_t b2sr_launch_count(void) { return g_launches.load(); }
+
+int b2sr_set_kernel_timing(int on) {
+    API_BEGIN
+    kernel_timer().on = on != 0;
+    API_END
+}
+
+int b2sr_last_kernel_ms(float *ms) {
+    API_BEGIN
+    KernelTimer &t = kernel_timer();
+    if (!t.recorded) B2SR_THROW(B2SR_EINVAL, "no timed kernel recorded (b2sr_set_kernel_timing(1) first)");
+    CK(cudaEventSynchronize(t.e1));
+    CK(cudaEventElapsedTime(ms, t.e0, t.e1));
+    API_END
+}
 
 int b2sr_free(b2sr_matrix *m) {
     API_BEGIN
