@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <functional>
 #include <string>
 
 #include "b2sr_sm100.h"
@@ -155,6 +156,7 @@ struct b2sr_matrix {
     void *vlong = nullptr;            // segmented plan for the very longest rows (bmv_vlong.cu)
     void *hot = nullptr;              // hot-column x cache plan (hot.cu)
     void *stream = nullptr;           // flat tile-stream row hints (bmv_stream.cu)
+    void *bff = nullptr;              // float-gather row order (bmv_bff.cu)
 };
 
 namespace b2sr {
@@ -172,7 +174,7 @@ void free_plan(void *plan);
 void free_vlong(void *plan);
 void *build_vlong(b2sr_matrix *m, uint32_t thresh, cudaStream_t s);
 void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
-                  cudaStream_t s);
+                  cudaStream_t s, const std::function<void()> &overlap = {});
 // hot.cu: the S most referenced tile columns' x words live in shared memory
 constexpr uint32_t HOT_SMEM_BYTES = 196608;
 struct HotView {
@@ -192,6 +194,10 @@ bool stream_enabled(int dim);
 void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaStream_t s,
                        const void *visited = nullptr, bool active_only = false);
 void free_stream(void *plan);
+// bmv_bff.cu: float gather over the rows with <= thresh tiles
+void launch_bff_rows(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
+                     uint32_t thresh, cudaStream_t s);
+void free_bff(void *plan);
 const uint4 *stream_desc(b2sr_matrix *m, cudaStream_t s, uint32_t *n_loads);  // per-load row descriptors
 void launch_stream_sweep(b2sr_matrix *m, const uint32_t *list, const uint32_t *list_n, const void *hx, size_t hb,
                          const void *x, void *y, const int *gate, int want, cudaStream_t s);

@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(256) k_bmv_bff(uint32_t ntr, uint32_t n, const
 constexpr uint32_t LONG_ROW_TILES = 512;
 constexpr int LONG_THREADS = 256;
 
-constexpr uint32_t VLONG_ROW_TILES = 512;  // longer rows: bmv_vlong.cu (segmented scatter + fold)
+constexpr uint32_t VLONG_ROW_TILES = 256;  // longer rows: bmv_vlong.cu (segmented scatter + fold)
 
 __global__ void k_find_long(uint32_t ntr, const uint32_t *trp, uint32_t lo, uint32_t hi, uint32_t *rows,
                             uint32_t *count) {
@@ -647,6 +647,17 @@ static void bff_ring(const b2sr_matrix *m, const double *x, int ring, double inc
                      cudaStream_t s) {
     constexpr uint32_t GPW = 32 / D;
     ensure_long_rows(const_cast<b2sr_matrix *>(m), s);
+    const char *old = getenv("B2SR_BFF_OLD");  // A/B: the group-per-row + CTA-per-row kernels
+    if (!(old && old[0] == '1')) {
+        // rows up to the segmented-plan threshold: pipelined group-per-row walk
+        // (bmv_bff.cu); longer rows: segmented scatter + warp folds (bmv_vlong.cu)
+        const char *ev = getenv("B2SR_VLONG_TILES");
+        uint32_t hi = ev ? (uint32_t)atoi(ev) : VLONG_ROW_TILES;
+        launch_vlong(const_cast<b2sr_matrix *>(m), x, ring, inc, keep, y, s, [&] {
+            launch_bff_rows(const_cast<b2sr_matrix *>(m), x, ring, inc, keep, y, hi, s);
+        });
+        return;
+    }
     uint64_t warps = ((uint64_t)m->ntr + GPW - 1) / GPW;
     uint64_t blocks = (warps + 7) / 8, cap = (uint64_t)num_sms() * 16;
     unsigned g = (unsigned)(blocks < cap ? blocks : cap);

@@ -9,13 +9,14 @@
 // (row, bit-row) then folds its region -- a pure dependent-add chain over
 // contiguous memory, bit-identical to the reference.  The region layout only
 // depends on the matrix's bits, so it is planned once and cached.
+#include <functional>
 #include <vector>
 
 #include "bmv_common.cuh"
 
 namespace b2sr {
 
-constexpr uint32_t VSEG = 2048;          // tiles per scatter unit
+constexpr uint32_t VSEG = 128;           // tiles per scatter unit (one warp, four rounds of 32)
 constexpr int VTHREADS = 256;
 
 struct VLongPlan {
@@ -27,7 +28,11 @@ struct VLongPlan {
     uint64_t *base = nullptr;      // n_rows * D: region starts
     uint32_t *total = nullptr;     // n_rows * D: region lengths
     double *terms = nullptr;       // n_terms
+    uint32_t *order = nullptr;     // n_rows * D vertices (row*D + r), fewest terms first
+    uint32_t n_small = 0;          // the first n_small fold lane-per-vertex, the rest warp-per-vertex
 };
+
+constexpr uint32_t LANE_FOLD_MAX = 2048;  // terms: above, one warp folds the vertex
 
 void free_vlong(void *p) {
     VLongPlan *v = static_cast<VLongPlan *>(p);
@@ -38,6 +43,7 @@ void free_vlong(void *p) {
     dfree(v->base, nullptr);
     dfree(v->total, nullptr);
     dfree(v->terms, nullptr);
+    dfree(v->order, nullptr);
     delete v;
 }
 
@@ -63,6 +69,15 @@ __global__ void k_vlong_units(uint32_t nr, const uint32_t *__restrict__ rows, co
         uint32_t t0 = trp[rows[i]], t1 = trp[rows[i] + 1];
         uint64_t u = uofs[i];
         for (uint32_t t = t0; t < t1; t += VSEG, u++) units[u] = make_uint4(i, t, min(t1, t + VSEG), 0);
+    }
+}
+
+__global__ void k_vlong_order_keys(uint32_t nv, const uint32_t *__restrict__ total, uint32_t *__restrict__ key,
+                                   uint32_t *__restrict__ val, uint32_t *__restrict__ n_small) {
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < nv; k += gridDim.x * blockDim.x) {
+        key[k] = total[k];
+        val[k] = k;
+        if (total[k] <= LANE_FOLD_MAX) atomicAdd(n_small, 1u);
     }
 }
 
@@ -159,6 +174,19 @@ void *build_vlong(b2sr_matrix *m, uint32_t thresh, cudaStream_t s) {
             v->units = units.release();
             v->unit_off = unit_off.release();
             v->base = base.release();
+            {  // fold order: vertices sorted by term count
+                const uint32_t nv = nr * D;
+                Buf<uint32_t> key(nv, s), val(nv, s), nsm(1, s);
+                CK(cudaMemsetAsync(nsm.p, 0, 4, s));
+                LAUNCH(k_vlong_order_keys, grid(nv), 256, 0, s, nv, total.p, key.p, val.p, nsm.p);
+                uint32_t *ko, *vo;
+                Buf<uint32_t> kalt, valt;
+                radix_sort_pairs_u32(key.p, val.p, nv, 32, s, &ko, &vo, &kalt, &valt);
+                Buf<uint32_t> order(nv, s);
+                CK(cudaMemcpyAsync(order.p, vo, (size_t)nv * 4, cudaMemcpyDeviceToDevice, s));
+                v->n_small = read_scalar(nsm.p, s);
+                v->order = order.release();
+            }
             v->total = total.release();
             CK(cudaStreamSynchronize(s));  // scratch buffers die here
         }
@@ -238,6 +266,81 @@ __global__ void __launch_bounds__(VTHREADS) k_vlong_scatter(uint32_t n_units, co
 // partial minima that already include it)
 constexpr int RING_MIN_COMBINE = B2SR_RING_MAXTIMES + 1;
 
+// d = 4, 8: one warp per 128-tile unit, four rounds of one tile per lane.
+// The per-bit-row term counts of a tile are packed into byte (d=4) or 16-bit
+// (d=8) fields of one or two words, so a single shuffle scan gives every lane
+// its output positions for all bit-rows at once; the running offsets of the
+// unit's bit-rows live in registers.  Terms are the x values in reference
+// order (tile, then column), written into each (row, bit-row) region.
+template <int D>
+__global__ void __launch_bounds__(256) k_vlong_scatter_w(uint32_t n_units, const uint4 *__restrict__ units,
+                                                         const uint32_t *__restrict__ unit_off,
+                                                         const uint64_t *__restrict__ base,
+                                                         const uint32_t *__restrict__ tci,
+                                                         const uint8_t *__restrict__ tiles,
+                                                         const double *__restrict__ x, double *__restrict__ terms) {
+    constexpr int NPW = D == 4 ? 1 : 4;       // packed count words
+    constexpr int FPW = D == 4 ? 4 : 2;       // fields per word
+    constexpr int FB = 32 / FPW;              // field bits
+    const uint32_t lane = lane_id();
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n_units; u += warps) {
+        const uint4 un = units[u];
+        uint64_t off[D];
+#pragma unroll
+        for (int r = 0; r < D; r++) off[r] = base[(size_t)un.x * D + r] + unit_off[(size_t)u * D + r];
+        for (uint32_t t = un.y + lane; t - lane < un.z; t += 32) {
+            const bool ok = t < un.z;
+            uint32_t rw[D];  // row words of this lane's tile
+            uint32_t c = 0;
+            if (ok) {
+                c = __ldg(tci + t);
+                if constexpr (D == 4) {
+                    uint32_t w = __ldg(reinterpret_cast<const uint32_t *>(tiles) + t);
+#pragma unroll
+                    for (int r = 0; r < 4; r++) rw[r] = (w >> (8 * r)) & 0xFFu;
+                } else {
+                    uint2 w = __ldg(reinterpret_cast<const uint2 *>(tiles) + t);
+#pragma unroll
+                    for (int r = 0; r < 8; r++) rw[r] = ((r < 4 ? w.x : w.y) >> (8 * (r & 3))) & 0xFFu;
+                }
+            } else {
+#pragma unroll
+                for (int r = 0; r < D; r++) rw[r] = 0;
+            }
+            uint32_t pk[NPW], inc[NPW];
+#pragma unroll
+            for (int q = 0; q < NPW; q++) pk[q] = 0;
+#pragma unroll
+            for (int r = 0; r < D; r++) pk[r / FPW] |= (uint32_t)__popc(rw[r]) << (FB * (r % FPW));
+#pragma unroll
+            for (int q = 0; q < NPW; q++) {
+                inc[q] = pk[q];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    uint32_t v = __shfl_up_sync(0xffffffffu, inc[q], o);
+                    if (lane >= (uint32_t)o) inc[q] += v;
+                }
+            }
+            const double *xs = x + (size_t)c * D;
+#pragma unroll
+            for (int r = 0; r < D; r++) {
+                const uint32_t mask = FB == 32 ? 0xFFFFFFFFu : ((1u << FB) - 1u);
+                const uint32_t incl = (inc[r / FPW] >> (FB * (r % FPW))) & mask;
+                const uint32_t mine = (pk[r / FPW] >> (FB * (r % FPW))) & mask;
+                uint32_t b = rw[r];
+                double *dst = terms + off[r] + (incl - mine);
+                while (b) {
+                    int k = __ffs(b) - 1;
+                    b &= b - 1;
+                    *dst++ = __ldg(xs + k);
+                }
+                off[r] += __shfl_sync(0xffffffffu, incl, 31);  // the round's total for this bit-row
+            }
+        }
+    }
+}
+
 template <int RING>
 __device__ __forceinline__ double vring_op(double cur, double term, double inc) {
     if constexpr (RING == B2SR_RING_ARITHMETIC) {
@@ -252,48 +355,103 @@ __device__ __forceinline__ double vring_op(double cur, double term, double inc) 
     }
 }
 
-// One warp per (row, bit-row) over its contiguous term region.
-//  * ARITHMETIC: the reference-order fold (kernels.py:195-207) is a dependent
-//    chain of float64 adds (8 cycles each on B200); lanes keep four chunks of
-//    32 terms in flight (coalesced) and every lane applies them in order from
-//    shuffles, so the chain itself is the only serial part.
+template <int D, int RING>
+__device__ __forceinline__ void vlong_store(uint32_t k, double acc, const uint32_t *__restrict__ rows, uint32_t n,
+                                            const void *__restrict__ keep, double *__restrict__ y, uint32_t row0) {
+    const double ident = RING == B2SR_RING_MINPLUS ? __longlong_as_double(0x7FF0000000000000ll) : 0.0;
+    const uint32_t I = rows[k / D], r = k % D, grow = row0 + I;
+    if ((uint64_t)grow * D + r < n) {
+        if (keep && !((load_word<D>(keep, grow) >> r) & 1u)) acc = ident;
+        y[(size_t)I * D + r] = acc;
+    }
+}
+
+// Vertices with few terms: one lane per vertex folds its region in order
+// (kernels.py:195-207); 32 independent chains per warp, 16-byte loads two
+// terms at a time, the next four already in flight.
+template <int D, int RING>
+__global__ void __launch_bounds__(256) k_vlong_fold_lanes(uint32_t n_small, const uint32_t *__restrict__ order,
+                                                          const uint32_t *__restrict__ rows,
+                                                          const uint64_t *__restrict__ base,
+                                                          const uint32_t *__restrict__ total,
+                                                          const double *__restrict__ terms, double inc, uint32_t n,
+                                                          const void *__restrict__ keep, double *__restrict__ y,
+                                                          uint32_t row0) {
+    const double ident = RING == B2SR_RING_MINPLUS ? __longlong_as_double(0x7FF0000000000000ll) : 0.0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_small; i += gridDim.x * blockDim.x) {
+        const uint32_t k = order[i];
+        const uint64_t b0 = base[k];
+        const uint32_t nt = total[k];
+        const double *p = terms + b0;
+        double acc = ident;
+        uint32_t q = 0;
+        if ((b0 & 1) && nt) acc = vring_op<RING>(acc, p[q++], inc);  // to a 16-byte boundary
+        for (; q + 8 <= nt; q += 8) {
+            const double2 *v = reinterpret_cast<const double2 *>(p + q);
+            double2 a = __ldg(v), b = __ldg(v + 1), c = __ldg(v + 2), e = __ldg(v + 3);
+            acc = vring_op<RING>(acc, a.x, inc); acc = vring_op<RING>(acc, a.y, inc);
+            acc = vring_op<RING>(acc, b.x, inc); acc = vring_op<RING>(acc, b.y, inc);
+            acc = vring_op<RING>(acc, c.x, inc); acc = vring_op<RING>(acc, c.y, inc);
+            acc = vring_op<RING>(acc, e.x, inc); acc = vring_op<RING>(acc, e.y, inc);
+        }
+        for (; q < nt; q++) acc = vring_op<RING>(acc, p[q], inc);
+        vlong_store<D, RING>(k, acc, rows, n, keep, y, row0);
+    }
+}
+
+// Vertices with many terms (the hubs): one warp per vertex.
+//  * ARITHMETIC: the reference-order fold is a dependent chain of float64
+//    adds (8 cycles each on B200, tools/micro_dadd.cu); lanes load 32
+//    consecutive terms per step (coalesced, four steps ahead) into a per-warp
+//    shared buffer and every lane applies them in order from broadcast 16-byte
+//    reads, so the chain itself is the only serial part.
 //  * MINPLUS / MAXTIMES: the reference's np.minimum / np.maximum step
 //    f(cur, t) = (cur < t || isnan(cur)) ? cur : t (ties to the later term, the
 //    first NaN sticks) is associative, so each lane folds one contiguous
 //    segment and the segments are combined in order by a shuffle tree --
 //    bit-identical to the sequential fold.
 template <int D, int RING>
-__global__ void __launch_bounds__(256) k_vlong_fold(uint32_t n_rows, const uint32_t *__restrict__ rows,
+__global__ void __launch_bounds__(256) k_vlong_fold(uint32_t n_big, const uint32_t *__restrict__ order,
+                                                    const uint32_t *__restrict__ rows,
                                                     const uint64_t *__restrict__ base,
                                                     const uint32_t *__restrict__ total,
                                                     const double *__restrict__ terms, double inc, uint32_t n,
                                                     const void *__restrict__ keep, double *__restrict__ y,
                                                     uint32_t row0) {
+    __shared__ double2 sbuf[256 / 32][16];
     const double ident = RING == B2SR_RING_MINPLUS ? __longlong_as_double(0x7FF0000000000000ll) : 0.0;
-    const uint32_t lane = lane_id();
+    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < n_rows * D; k += warps) {
-        const uint32_t i = k / D, r = k % D, I = rows[i];
+    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_big; i += warps) {
+        const uint32_t k = order[n_big - 1 - i];  // largest first: the longest chain starts at once
         const double *p = terms + base[k];
         const uint32_t nt = total[k];
         double acc = ident;
         if constexpr (RING == B2SR_RING_ARITHMETIC) {
             double c0 = lane < nt ? p[lane] : 0.0, c1 = 32 + lane < nt ? p[32 + lane] : 0.0;
             double c2 = 64 + lane < nt ? p[64 + lane] : 0.0, c3 = 96 + lane < nt ? p[96 + lane] : 0.0;
+            double *sb = reinterpret_cast<double *>(sbuf[wid]);
             for (uint32_t q = 0; q < nt; q += 32) {
-                double c4 = q + 128 + lane < nt ? p[q + 128 + lane] : 0.0;  // four chunks ahead
+                if (q + 2048 + lane < nt)  // 16 KB ahead into L2: the region streams from HBM
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p + q + 2048 + lane));
+                double c4 = q + 128 + lane < nt ? p[q + 128 + lane] : 0.0;  // four steps ahead
+                __syncwarp();
+                sb[lane] = c0;
+                __syncwarp();
                 const uint32_t m = min(32u, nt - q);
                 if (m == 32) {
+                    // all 16 broadcast reads first, then the 32-add chain: the
+                    // shared-memory latency is paid once per 32 terms, not per pair
+                    double2 t[16];
 #pragma unroll
-                    for (int j0 = 0; j0 < 32; j0 += 8) {
-                        double t[8];
+                    for (int j = 0; j < 16; j++) t[j] = sbuf[wid][j];
 #pragma unroll
-                        for (int j = 0; j < 8; j++) t[j] = __shfl_sync(0xffffffffu, c0, j0 + j);
-#pragma unroll
-                        for (int j = 0; j < 8; j++) acc = __dadd_rn(acc, t[j]);
+                    for (int j = 0; j < 16; j++) {
+                        acc = __dadd_rn(acc, t[j].x);
+                        acc = __dadd_rn(acc, t[j].y);
                     }
                 } else {
-                    for (uint32_t j = 0; j < m; j++) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, c0, j));
+                    for (uint32_t j = 0; j < m; j++) acc = __dadd_rn(acc, sb[j]);
                 }
                 c0 = c1;
                 c1 = c2;
@@ -302,51 +460,113 @@ __global__ void __launch_bounds__(256) k_vlong_fold(uint32_t n_rows, const uint3
             }
         } else {
             const uint32_t seg = (nt + 31) / 32, a = min(nt, lane * seg), b = min(nt, a + seg);
-            for (uint32_t q = a; q < b; q++) acc = vring_op<RING>(acc, p[q], inc);
+            uint32_t q = a;
+            for (; q + 8 <= b; q += 8) {  // eight independent loads, then the ordered steps
+                double t[8];
+#pragma unroll
+                for (int j = 0; j < 8; j++) t[j] = __ldg(p + q + j);
+#pragma unroll
+                for (int j = 0; j < 8; j++) acc = vring_op<RING>(acc, t[j], inc);
+            }
+            for (; q < b; q++) acc = vring_op<RING>(acc, p[q], inc);
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {  // ordered combine: lane l's segments precede lane l+o's
                 double other = __shfl_down_sync(0xffffffffu, acc, o);
                 if (lane + o < 32) acc = vring_op<RING == B2SR_RING_MINPLUS ? RING_MIN_COMBINE : RING>(acc, other, 0.0);
             }
         }
-        if (lane == 0) {
-            uint32_t grow = row0 + I;
-            uint64_t vrow = (uint64_t)grow * D + r;
-            if (vrow < n) {
-                if (keep && !((load_word<D>(keep, grow) >> r) & 1u)) acc = ident;
-                y[(size_t)I * D + r] = acc;
-            }
-        }
+        if (lane == 0) vlong_store<D, RING>(k, acc, rows, n, keep, y, row0);
     }
 }
 
+// Side stream for the hub folds (one per device and host thread), so their
+// long dependent chains overlap the rest of the sweep.
+static cudaStream_t side_stream() {
+    static thread_local cudaStream_t ss[16] = {};
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev >= 16) return nullptr;
+    if (!ss[dev]) CK(cudaStreamCreateWithFlags(&ss[dev], cudaStreamNonBlocking));
+    return ss[dev];
+}
+
+// Scatter, then the folds; `overlap` runs while the hub folds proceed on the
+// side stream (the main stream waits for them before returning).
 void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
-                  cudaStream_t s) {
+                  cudaStream_t s, const std::function<void()> &overlap) {
     VLongPlan *v = static_cast<VLongPlan *>(m->vlong);
-    if (!v || !v->n_rows) return;
-    unsigned gu = std::min<unsigned>(v->n_units, (unsigned)num_sms() * 8);
-    unsigned gf = (unsigned)std::min<uint64_t>(((uint64_t)v->n_rows * m->dim + 7) / 8, (uint64_t)num_sms() * 8);
-#define VL_CASE(DD, W)                                                                                            \
-    case DD:                                                                                                      \
-        LAUNCH(k_vlong_scatter<DD>, gu, VTHREADS, 0, s, v->n_units, v->units, v->unit_off, v->base, m->tci,      \
-               (const W *)m->tiles, x, v->terms);                                                                 \
-        if (ring == B2SR_RING_ARITHMETIC)                                                                         \
-            LAUNCH((k_vlong_fold<DD, B2SR_RING_ARITHMETIC>), gf, 256, 0, s, v->n_rows, v->rows, v->base, v->total, \
-                   v->terms, inc, m->n, keep, y, m->row0);                                                        \
-        else if (ring == B2SR_RING_MINPLUS)                                                                       \
-            LAUNCH((k_vlong_fold<DD, B2SR_RING_MINPLUS>), gf, 256, 0, s, v->n_rows, v->rows, v->base, v->total,   \
-                   v->terms, inc, m->n, keep, y, m->row0);                                                        \
-        else                                                                                                      \
-            LAUNCH((k_vlong_fold<DD, B2SR_RING_MAXTIMES>), gf, 256, 0, s, v->n_rows, v->rows, v->base, v->total,  \
-                   v->terms, inc, m->n, keep, y, m->row0);                                                        \
-        break;
-    switch (m->dim) {
-        VL_CASE(4, uint8_t)
-        VL_CASE(8, uint8_t)
-        VL_CASE(16, uint16_t)
-        VL_CASE(32, uint32_t)
+    if (!v || !v->n_rows) {
+        if (overlap) overlap();
+        return;
     }
-#undef VL_CASE
+    unsigned gu = std::min<unsigned>(v->n_units, (unsigned)num_sms() * 8);
+    const uint32_t nv = v->n_rows * m->dim, n_big = nv - v->n_small;
+    unsigned gw = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)v->n_units + 7) / 8, (uint64_t)num_sms() * 16));
+    unsigned gl = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((v->n_small + 255) / 256, (uint64_t)num_sms() * 8));
+    switch (m->dim) {  // scatter every unit's terms into the regions
+        case 4: LAUNCH(k_vlong_scatter_w<4>, gw, 256, 0, s, v->n_units, v->units, v->unit_off, v->base, m->tci, (const uint8_t *)m->tiles, x, v->terms); break;
+        case 8: LAUNCH(k_vlong_scatter_w<8>, gw, 256, 0, s, v->n_units, v->units, v->unit_off, v->base, m->tci, (const uint8_t *)m->tiles, x, v->terms); break;
+        case 16: LAUNCH(k_vlong_scatter<16>, gu, VTHREADS, 0, s, v->n_units, v->units, v->unit_off, v->base, m->tci, (const uint16_t *)m->tiles, x, v->terms); break;
+        default: LAUNCH(k_vlong_scatter<32>, gu, VTHREADS, 0, s, v->n_units, v->units, v->unit_off, v->base, m->tci, (const uint32_t *)m->tiles, x, v->terms); break;
+    }
+    cudaStream_t s2 = n_big ? side_stream() : nullptr;
+    cudaEvent_t e1 = nullptr, e2 = nullptr;
+    cudaStream_t sb = s;
+    if (s2) {
+        CK(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
+        CK(cudaEventRecord(e1, s));
+        CK(cudaStreamWaitEvent(s2, e1, 0));
+        sb = s2;
+    }
+    // the largest vertices first, one warp per SM (a large dynamic shared
+    // allocation keeps other fold warps off that SM: their chains would slow
+    // the longest one down); then the rest, eight warps per block
+    const uint32_t n_top = std::min<uint32_t>(n_big, (uint32_t)num_sms());
+    const uint32_t n_rest = n_big - n_top;
+    const size_t top_smem = 160 * 1024;
+    unsigned gr = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)n_rest + 7) / 8, (uint64_t)num_sms() * 8));
+#define VL_BIG(DD, RR)                                                                                             \
+    do {                                                                                                           \
+        hot_smem_attr(k_vlong_fold<DD, RR>, top_smem);                                                             \
+        LAUNCH((k_vlong_fold<DD, RR>), n_top, 32, top_smem, sb, n_top, v->order + v->n_small + n_rest, v->rows,     \
+               v->base, v->total, v->terms, inc, m->n, keep, y, m->row0);                                          \
+        if (n_rest)                                                                                                \
+            LAUNCH((k_vlong_fold<DD, RR>), gr, 256, 0, sb, n_rest, v->order + v->n_small, v->rows, v->base,        \
+                   v->total, v->terms, inc, m->n, keep, y, m->row0);                                               \
+    } while (0)
+#define VL_SMALL(DD, RR)                                                                                           \
+    LAUNCH((k_vlong_fold_lanes<DD, RR>), gl, 256, 0, s, v->n_small, v->order, v->rows, v->base, v->total, v->terms, \
+           inc, m->n, keep, y, m->row0)
+#define VL_RING(DD)                                                                                                \
+    do {                                                                                                           \
+        if (ring == B2SR_RING_ARITHMETIC) {                                                                        \
+            if (n_big) VL_BIG(DD, B2SR_RING_ARITHMETIC);                                                           \
+            if (v->n_small) VL_SMALL(DD, B2SR_RING_ARITHMETIC);                                                    \
+        } else if (ring == B2SR_RING_MINPLUS) {                                                                    \
+            if (n_big) VL_BIG(DD, B2SR_RING_MINPLUS);                                                              \
+            if (v->n_small) VL_SMALL(DD, B2SR_RING_MINPLUS);                                                       \
+        } else {                                                                                                   \
+            if (n_big) VL_BIG(DD, B2SR_RING_MAXTIMES);                                                             \
+            if (v->n_small) VL_SMALL(DD, B2SR_RING_MAXTIMES);                                                      \
+        }                                                                                                          \
+    } while (0)
+    switch (m->dim) {
+        case 4: VL_RING(4); break;
+        case 8: VL_RING(8); break;
+        case 16: VL_RING(16); break;
+        default: VL_RING(32); break;
+    }
+#undef VL_RING
+#undef VL_SMALL
+#undef VL_BIG
+    if (overlap) overlap();
+    if (s2) {
+        CK(cudaEventRecord(e2, s2));
+        CK(cudaStreamWaitEvent(s, e2, 0));
+        cudaEventDestroy(e1);  // released once the recorded work completes
+        cudaEventDestroy(e2);
+    }
 }
 
 }  // namespace b2sr

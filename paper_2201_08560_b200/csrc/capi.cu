@@ -122,6 +122,7 @@ void free_matrix(b2sr_matrix *m) {
     free_plan(m->plan);
     free_hot(m->hot);
     free_stream(m->stream);
+    free_bff(m->bff);
     if (cur != m->device) cudaSetDevice(cur);
     delete m;
 }

@@ -1,0 +1,34 @@
+"""Float-gather probe: one ARITHMETIC and one MINPLUS bmv_bin_full_full on R-MAT
+at the given scale (for ncu), checked against the oracle when --check."""
+import argparse, sys, time
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import numpy as np, torch
+import paper_2201_08560_b200 as b2
+from paper_2201_08560_b200 import rmat
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--scale", type=int, default=20)
+ap.add_argument("--dim", type=int, default=4)
+ap.add_argument("--reps", type=int, default=2)
+ap.add_argument("--check", action="store_true")
+a = ap.parse_args()
+csr = rmat.rmat_csr(a.scale, 16, seed=1)
+m = b2.csr_to_b2sr(csr, a.dim)
+rng = np.random.default_rng(3)
+x = rng.random(csr.n)
+for _ in range(a.reps):
+    t0 = time.time(); ya = b2.bmv_bin_full_full(m, x, b2.ARITHMETIC); t1 = time.time()
+    yb = b2.bmv_bin_full_full(m, x, b2.min_plus(1)); t2 = time.time()
+    print(f"arith {1e3*(t1-t0):.2f} ms  minplus {1e3*(t2-t1):.2f} ms", flush=True)
+if a.check:
+    from oracle import oracle as orc
+    ref = (csr.n, a.dim, m.tile_row_ptr, m.tile_col_ind, m.bit_tiles)
+    ra = orc.bmv_bff(ref, x, "arithmetic", workers=16)
+    rb = orc.bmv_bff(ref, x, "minplus", 1.0, workers=16)
+    print("arith equal", ya.tobytes() == ra.tobytes(), "minplus equal", yb.tobytes() == rb.tobytes())
+    bad = np.flatnonzero(yb != rb)
+    print("minplus mismatches", len(bad), bad[:5], yb[bad[:5]], rb[bad[:5]])
+if a.scale >= 23:  # vertex term-count profile of the segmented plan rows
+    deg = np.diff(csr.row_ptr.astype(np.int64))
+    print("deg>2048:", int((deg > 2048).sum()), "terms", int(deg[deg > 2048].sum()), "max", int(deg.max()))
