@@ -423,6 +423,7 @@ def _fresh(hm):
     c = copy.copy(hm)
     c._h = None
     c._transpose = None
+    c._nodiag = None
     return c
 
 

@@ -297,7 +297,8 @@ class B2srMatrix:
     ``bit_tiles[t, i]`` is row word ``i`` of stored tile ``t``.
     """
 
-    __slots__ = ("n", "tile_dim", "_trp", "_tci", "_tiles", "_h", "_num_tiles", "_transpose", "__weakref__")
+    __slots__ = ("n", "tile_dim", "_trp", "_tci", "_tiles", "_h", "_num_tiles", "_transpose", "_nodiag",
+                 "__weakref__")
 
     def __init__(self, n, tile_dim, tile_row_ptr, tile_col_ind, bit_tiles):
         n = int(n)
@@ -338,6 +339,7 @@ class B2srMatrix:
         self._h = None
         self._num_tiles = T
         self._transpose = None
+        self._nodiag = None
 
     @classmethod
     def _wrap(cls, h: _Handle) -> "B2srMatrix":
@@ -348,6 +350,7 @@ class B2srMatrix:
         self._h = h
         self._num_tiles = h.num_tiles
         self._transpose = None
+        self._nodiag = None
         return self
 
     # device mirror ---------------------------------------------------
@@ -596,8 +599,11 @@ def b2sr_transpose(m: B2srMatrix) -> B2srMatrix:
 
 
 def drop_diagonal(m: B2srMatrix) -> B2srMatrix:
-    """csr_to_b2sr(_drop_diagonal(b2sr_to_csr(m))) done in tile form (algorithms.py:96-101, 111)."""
-    return B2srMatrix._wrap(_new_handle("b2sr_drop_diagonal", m.handle().ptr, dev.stream()))
+    """csr_to_b2sr(_drop_diagonal(b2sr_to_csr(m))) done in tile form (algorithms.py:96-101, 111).
+    Matrices are immutable, so the result is cached on ``m`` (as transposes are)."""
+    if m._nodiag is None:
+        m._nodiag = B2srMatrix._wrap(_new_handle("b2sr_drop_diagonal", m.handle().ptr, dev.stream()))
+    return m._nodiag
 
 
 # ---------------------------------------------------------------- byte accounting

@@ -17,10 +17,26 @@ csr = rmat.rmat_csr(a.scale, 16, seed=1)
 m = b2.csr_to_b2sr(csr, a.dim)
 rng = np.random.default_rng(3)
 x = rng.random(csr.n)
+import ctypes
+from paper_2201_08560_b200 import _capi
+from paper_2201_08560_b200 import _device as dev
+h = m.handle()
+xd = dev.to_device(x)
+yd = dev.empty_bytes(8 * csr.n)
+bad = ctypes.c_int64(-1)
+sp = torch.cuda.current_stream().cuda_stream
 for _ in range(a.reps):
-    t0 = time.time(); ya = b2.bmv_bin_full_full(m, x, b2.ARITHMETIC); t1 = time.time()
-    yb = b2.bmv_bin_full_full(m, x, b2.min_plus(1)); t2 = time.time()
-    print(f"arith {1e3*(t1-t0):.2f} ms  minplus {1e3*(t2-t1):.2f} ms", flush=True)
+    ts = []
+    for ring, inc in ((1, 0.0), (2, 1.0)):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        _capi.call("b2sr_bmv_bff", h.ptr, dev.ptr(xd), ring, inc, None, None, dev.ptr(yd), ctypes.addressof(bad), sp)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    print(f"device: arith {ts[0]:.3f} ms  minplus {ts[1]:.3f} ms", flush=True)
+ya = b2.bmv_bin_full_full(m, x, b2.ARITHMETIC)
+yb = b2.bmv_bin_full_full(m, x, b2.min_plus(1))
 if a.check:
     from oracle import oracle as orc
     ref = (csr.n, a.dim, m.tile_row_ptr, m.tile_col_ind, m.bit_tiles)
