@@ -1167,11 +1167,24 @@ int b2sr_pagerank(const b2sr_matrix *a, const double *d_out_degree, double alpha
     LAUNCH(k_pr_init, grid_for(n), 256, 0, s, n, 1.0 / (double)n, d_out_degree, d_rank, xs.p);
     int64_t sweeps = 0;
     int conv = 0;
+    const bool trace = getenv("B2SR_PR_TRACE") != nullptr;
+    cudaEvent_t ev[4] = {};
+    if (trace)
+        for (auto &e : ev) CK(cudaEventCreate(&e));
     while (sweeps < max_iter) {
+        if (trace) CK(cudaEventRecord(ev[0], s));
         launch_bff(a, xs.p, B2SR_RING_ARITHMETIC, 0.0, nullptr, g.p, s);
+        if (trace) CK(cudaEventRecord(ev[1], s));
         LAUNCH(k_pr_update, grid_for(n), 256, 0, s, n, teleport, alpha, g.p, d_out_degree, d_rank, xs.p, diff.p);
         pw.run(diff.p, s);
+        if (trace) CK(cudaEventRecord(ev[2], s));
         double delta = read_scalar(pw.out.p, s);
+        if (trace) {
+            float t1, t2;
+            CK(cudaEventElapsedTime(&t1, ev[0], ev[1]));
+            CK(cudaEventElapsedTime(&t2, ev[1], ev[2]));
+            fprintf(stderr, "[b2sr pr] sweep %lld gather %.3f ms update+delta %.3f ms\n", (long long)sweeps, t1, t2);
+        }
         sweeps++;
         if (delta < epsilon) { conv = 1; break; }
     }
