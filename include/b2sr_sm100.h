@@ -166,6 +166,14 @@ int b2sr_csr_lower_rowptr(uint32_t n, const uint32_t *d_row_ptr, const uint32_t 
                           uint32_t *d_lrow_ptr, uint64_t *lnnz, void *stream);
 int b2sr_csr_lower_fill(uint32_t n, const uint32_t *d_row_ptr, const uint32_t *d_col_ind,
                         const uint32_t *d_lrow_ptr, uint32_t *d_lcol_ind, void *stream);
+/* Degree-oriented triangle DAG of a symmetric device CSR: keep (u, v) iff
+ * (deg u, u) < (deg v, v) (edges point at higher degree).  triangle_count (algorithms.py:199-215) runs its
+ * masked bin-SpGEMM on this instead of the ID-ordered lower triangle: the
+ * count is the same for any total vertex order, and hub rows stay short. */
+int b2sr_csr_orient_rowptr(uint32_t n, const uint32_t *d_row_ptr, const uint32_t *d_col_ind, uint32_t *d_orow_ptr,
+                           uint64_t *onnz, void *stream);
+int b2sr_csr_orient_fill(uint32_t n, const uint32_t *d_row_ptr, const uint32_t *d_col_ind, const uint32_t *d_orow_ptr,
+                         uint32_t *d_ocol_ind, void *stream);
 /* Synthetic Graph500 R-MAT edges. */
 int b2sr_rmat_edges(int scale, uint64_t m, uint64_t seed, uint32_t *d_src, uint32_t *d_dst, void *stream);
 /* COO -> CSR with CsrMatrix.from_coo semantics (formats.py:156-190):

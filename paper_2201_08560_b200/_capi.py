@@ -60,6 +60,8 @@ SIGNATURES = {
     "b2sr_tc": [P, P, P],
     "b2sr_csr_lower_rowptr": [u32, P, P, P, P, P],
     "b2sr_csr_lower_fill": [u32, P, P, P, P, P],
+    "b2sr_csr_orient_rowptr": [u32, P, P, P, P, P],
+    "b2sr_csr_orient_fill": [u32, P, P, P, P, P],
     "b2sr_rmat_edges": [i32, u64, u64, P, P, P],
     "b2sr_coo_to_csr": [u32, u64, P, P, i32, i32, P, P, P, P],
 }
