@@ -17,7 +17,10 @@ struct BfsCounters {
 };
 
 // Direction of one level, chosen on the device from the previous level's counters.
-enum BfsMode : int { BFS_NONE = 0, BFS_PUSH = 1, BFS_PULL = 2, BFS_PULL_ACTIVE = 3 };
+// BFS_PULL_DENSE: a pull over a dense frontier -- the first tiles of every
+// unvisited row are checked first (most rows find a parent there), then the
+// listed loads of the rows still missing one are streamed like BFS_PULL_ACTIVE.
+enum BfsMode : int { BFS_NONE = 0, BFS_PUSH = 1, BFS_PULL = 2, BFS_PULL_ACTIVE = 3, BFS_PULL_DENSE = 4 };
 
 struct BfsCtl {
     int mode;
@@ -27,6 +30,7 @@ struct BfsCtl {
     unsigned long long unvisited;
     long long sweeps;
     uint32_t blocks_done;  // last-block detection in the update kernel
+    int sparse;            // pull over a sparse frontier: fetch tile bytes lazily
     BfsCounters cnt;       // written by the level's update, consumed by the next plan
 };
 

@@ -146,7 +146,7 @@ __device__ __forceinline__ uint32_t rel_row(uint32_t p, uint32_t oa, uint32_t ob
 
 // Streams the loads at positions [p0, p1): load k = list[p] with a list (BFS
 // pull over the loads that still hold an unvisited vertex), else k = p.
-template <int D, bool LIST, class GX>
+template <int D, bool LIST, class GX, bool LAZY = false>
 __device__ __forceinline__ void bbb_stream(uint32_t p0, uint32_t p1, uint32_t n_loads, uint64_t T,
                                            const uint32_t *__restrict__ list, const uint4 *__restrict__ desc,
                                            const uint32_t *__restrict__ trp, const uint8_t *__restrict__ tiles,
@@ -187,7 +187,9 @@ __device__ __forceinline__ void bbb_stream(uint32_t p0, uint32_t p1, uint32_t n_
         for (int g = 0; g < NG; g++) {
             uint64_t t = (uint64_t)k * LT + SG::pos(lane, g);
             bool ok = live && t < T;
-            st.v[g] = ok ? ld_stream128(tiles + t * TB) : make_uint4(0, 0, 0, 0);
+            // LAZY (sparse BFS frontiers): the tile bytes are fetched after the
+            // x words, only by lanes whose x words are not all zero
+            if constexpr (!LAZY) st.v[g] = ok ? ld_stream128(tiles + t * TB) : make_uint4(0, 0, 0, 0);
             if constexpr (GT == 4) {
                 uint4 q = ok ? ld_stream128(tci + t) : make_uint4(0, 0, 0, 0);
                 st.cx[0] = q.x; st.cx[1] = q.y; st.cx[2] = q.z; st.cx[3] = q.w;
@@ -211,6 +213,16 @@ __device__ __forceinline__ void bbb_stream(uint32_t p0, uint32_t p1, uint32_t n_
                     uint64_t t = (uint64_t)k * LT + SG::pos(lane, g) + j;
                     st.cx[g * GT + j] = (p < p1 && t < T) ? gx(st.cx[g * GT + j]) : 0u;
                 }
+        }
+        if constexpr (LAZY) {
+#pragma unroll
+            for (int g = 0; g < NG; g++) {
+                uint32_t any = 0;
+#pragma unroll
+                for (int j = 0; j < GT; j++) any |= st.cx[g * GT + j];
+                const uint64_t t = (uint64_t)k * LT + SG::pos(lane, g);
+                st.v[g] = any ? ld_stream128(tiles + t * TB) : make_uint4(0, 0, 0, 0);
+            }
         }
     };
     auto compute = [&](uint32_t p, const Stage &st) {
@@ -402,7 +414,8 @@ __global__ void __launch_bounds__(NT, 1)
         push_entries<D>(ctl->list_n, plist, a_trp, a_tci, a_tiles, frontier, next);
         return;
     }
-    const uint32_t n_pos = mode == BFS_PULL_ACTIVE ? ctl->active_n : n_loads;
+    const bool listed = mode == BFS_PULL_ACTIVE || mode == BFS_PULL_DENSE;
+    const uint32_t n_pos = listed ? ctl->active_n : n_loads;
     if (n_pos == 0) return;
     stage_hot(const_cast<uint8_t *>(hot_bytes()), hx, hx_bytes16);
     __syncthreads();
@@ -410,7 +423,8 @@ __global__ void __launch_bounds__(NT, 1)
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5, w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t per = (n_pos + warps - 1) / warps;
     const uint32_t p0 = std::min(n_pos, w * per), p1 = std::min(n_pos, p0 + per);
-    if (mode == BFS_PULL_ACTIVE) bbb_stream<D, true>(p0, p1, n_loads, T, alist, desc, trp, tiles, tci2, gx, next);
+    if (listed) bbb_stream<D, true>(p0, p1, n_loads, T, alist, desc, trp, tiles, tci2, gx, next);
+    else if (ctl->sparse) bbb_stream<D, false, XHot<D>, true>(p0, p1, n_loads, T, nullptr, desc, trp, tiles, tci2, gx, next);
     else bbb_stream<D, false>(p0, p1, n_loads, T, nullptr, desc, trp, tiles, tci2, gx, next);
 }
 

@@ -772,6 +772,7 @@ __global__ void k_bfs_ctl_init(BfsCtl *c, unsigned long long unvisited) {
     c->unvisited = unvisited;
     c->sweeps = 0;
     c->blocks_done = 0;
+    c->sparse = 0;
     c->cnt = BfsCounters{};
 }
 
@@ -785,7 +786,7 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
                                 double *__restrict__ levels, double level, const uint32_t *__restrict__ trp_a,
                                 const uint32_t *__restrict__ trp_at, const uint4 *__restrict__ live_at,
                                 BfsCtl *__restrict__ ctl, uint4 *__restrict__ zero_buf, int mask, double alpha,
-                                unsigned long long tiles_at, int has_a) {
+                                unsigned long long tiles_at, int has_a, int head_ok) {
     using W = typename WordT<D>::T;
     if (ctl->mode == BFS_NONE && mask) return;  // BFS already over
     constexpr int WPC = 16 / sizeof(W);
@@ -850,7 +851,11 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
         } else {
             cv->unvisited -= cv->cnt.removed_tiles;
             bool push = has_a && (double)cv->cnt.frontier_tiles * alpha < (double)cv->unvisited;
-            cv->mode = push ? BFS_PUSH : (cv->unvisited * 2 < tiles_at ? BFS_PULL_ACTIVE : BFS_PULL);
+            const bool dense = cv->cnt.frontier_vertices * 8 > (unsigned long long)ntr * D && head_ok;
+            cv->mode = push ? BFS_PUSH
+                            : (cv->unvisited * 2 < tiles_at ? BFS_PULL_ACTIVE : (dense ? BFS_PULL_DENSE : BFS_PULL));
+            // a frontier of < 1/16 of the vertices: most 4-tile groups see all-zero x words
+            cv->sparse = cv->cnt.frontier_vertices * 16 < (unsigned long long)ntr * D;
             cv->list_n = 0;
             cv->active_n = 0;
             cv->sweeps = cv->sweeps + 1;
@@ -907,7 +912,7 @@ __global__ void k_bfs_prep(BfsCtl *__restrict__ c, uint32_t ntr, const uint32_t 
     } else {
         for (uint32_t i = tid; i < S; i += stride) hx[i] = fr[cols ? cols[i] : i];
     }
-    if (mode != BFS_PULL_ACTIVE) return;
+    if (mode != BFS_PULL_ACTIVE) return;  // BFS_PULL_DENSE lists its loads after the head pass
     const uint32_t iters = (n_loads + stride - 1) / stride;
     for (uint32_t it = 0; it < iters; it++) {
         uint32_t k = tid + it * stride;
@@ -916,6 +921,59 @@ __global__ void k_bfs_prep(BfsCtl *__restrict__ c, uint32_t ntr, const uint32_t 
             uint32_t ra = desc[k].x, rb = desc[k + 1].x;
             for (uint32_t r = ra; r <= rb && !act; r++)
                 act = (~load_word<D>(visited, r) & load_word<D>(live, r)) != 0;
+        }
+        uint32_t bal = __ballot_sync(0xffffffffu, act);
+        if (!bal) continue;
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&c->active_n, (uint32_t)__popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (act) alist[base + __popc(bal & ((1u << lane) - 1u))] = k;
+    }
+}
+
+// BFS_PULL_DENSE, step 1: one thread per tile row with unvisited live
+// vertices checks the row's first HEAD_TILES tiles against the frontier and
+// stores the hits (next is zero here).  Step 2 lists the loads of the rows
+// that still miss a parent for the stream.
+constexpr uint32_t HEAD_TILES = 16;
+
+template <int D>
+__global__ void k_bfs_head(const BfsCtl *__restrict__ c, uint32_t ntr, const uint32_t *__restrict__ trp,
+                           const uint32_t *__restrict__ tci, const typename WordT<D>::T *__restrict__ tiles,
+                           const void *__restrict__ frontier, const void *__restrict__ visited,
+                           const void *__restrict__ live, void *__restrict__ next) {
+    if (c->mode != BFS_PULL_DENSE) return;
+    using W = typename WordT<D>::T;
+    for (uint32_t I = blockIdx.x * blockDim.x + threadIdx.x; I < ntr; I += gridDim.x * blockDim.x) {
+        const uint32_t keep = ~load_word<D>(visited, I) & load_word<D>(live, I);
+        if (!keep) continue;
+        const uint32_t t0 = trp[I], t1 = min(trp[I + 1], t0 + HEAD_TILES);
+        uint32_t acc = 0;
+        for (uint32_t t = t0; t < t1 && (acc & keep) != keep; t++) {
+            const uint32_t xw = load_word<D>(frontier, __ldg(tci + t));
+            if (!xw) continue;
+#pragma unroll
+            for (int r = 0; r < D; r++)
+                if (tiles[(size_t)t * D + r] & xw) acc |= 1u << r;
+        }
+        if (acc & keep) reinterpret_cast<W *>(next)[I] = (W)(acc & keep);
+    }
+}
+
+template <int D>
+__global__ void k_bfs_dense_list(BfsCtl *__restrict__ c, uint32_t n_loads, const uint4 *__restrict__ desc,
+                                 const void *__restrict__ visited, const void *__restrict__ live,
+                                 const void *__restrict__ next, uint32_t *__restrict__ alist) {
+    if (c->mode != BFS_PULL_DENSE) return;
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    const uint32_t lane = lane_id(), iters = (n_loads + stride - 1) / stride;
+    for (uint32_t it = 0; it < iters; it++) {
+        uint32_t k = tid + it * stride;
+        bool act = false;
+        if (k < n_loads) {
+            uint32_t ra = desc[k].x, rb = desc[k + 1].x;
+            for (uint32_t r = ra; r <= rb && !act; r++)
+                act = (~load_word<D>(visited, r) & load_word<D>(live, r) & ~load_word<D>(next, r)) != 0;
         }
         uint32_t bal = __ballot_sync(0xffffffffu, act);
         if (!bal) continue;
@@ -946,6 +1004,11 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     Buf<uint32_t> alist(std::max<uint32_t>(n_loads, 1), s);
     const double alpha = bfs_alpha();
     const bool trace = getenv("B2SR_BFS_TRACE") != nullptr;
+    // B2SR_BFS_HEAD=1: head pass + listed stream for dense-frontier pulls
+    // (measured slower at R-MAT s22 d=4: 296 vs 249 us for that level -- a
+    // load stays listed while any of its rows misses a parent)
+    const char *he = getenv("B2SR_BFS_HEAD");
+    const int head = he && he[0] == '1';
     LAUNCH(k_fill_f64, grid_for(n), 256, 0, s, d_levels, (size_t)n, HUGE_VAL);
     CK(cudaMemsetAsync(visited.p, 0, n16 * 16, s));
     CK(cudaMemsetAsync(fb.p, 0, n16 * 16, s));
@@ -957,17 +1020,22 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     const uint32_t *ta = a ? a->trp : nullptr;
     // level 0 = {src}: visited, levels, counters, the push list of level 1 and its plan
     LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)fb.p, (uint4 *)visited.p, d_levels, 0.0, ta, at->trp,
-           (const uint4 *)at->live, ctl.p, nullptr, 0, alpha, (unsigned long long)at->num_tiles, a ? 1 : 0);
+           (const uint4 *)at->live, ctl.p, nullptr, 0, alpha, (unsigned long long)at->num_tiles, a ? 1 : 0, head);
     void *frontier = fb.p, *next = fa.p;
     const unsigned gp = (unsigned)num_sms() * 8;
     BfsCtl h{};
     for (uint32_t L = 1;; L++) {
         LAUNCH(k_bfs_prep<D>, gp, 256, 0, s, ctl.p, ntr, ta, list.p, hv.S, hv.cols, frontier, hx.p, n_loads, desc,
                visited.p, at->live, alist.p);
+        if (head) {
+            LAUNCH(k_bfs_head<D>, grid_for(ntr), 256, 0, s, ctl.p, ntr, at->trp, at->tci,
+                   (const typename WordT<D>::T *)at->tiles, frontier, visited.p, at->live, next);
+            LAUNCH(k_bfs_dense_list<D>, gp, 256, 0, s, ctl.p, n_loads, desc, visited.p, at->live, next, alist.p);
+        }
         launch_bfs_level(at, a, ctl.p, list.p, alist.p, hx.p, hb, frontier, next, s);
         LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L, ta,
                at->trp, (const uint4 *)at->live, ctl.p, (uint4 *)frontier, 1, alpha,
-               (unsigned long long)at->num_tiles, a ? 1 : 0);
+               (unsigned long long)at->num_tiles, a ? 1 : 0, head);
         std::swap(frontier, next);
         if (trace || (L >= 4 && L % 2 == 0)) {  // poll for the end every other level
             CK(cudaMemcpyAsync(&h, ctl.p, sizeof(BfsCtl), cudaMemcpyDeviceToHost, s));
