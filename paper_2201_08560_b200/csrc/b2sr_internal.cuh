@@ -174,7 +174,7 @@ void free_plan(void *plan);
 void free_vlong(void *plan);
 void *build_vlong(b2sr_matrix *m, uint32_t thresh, cudaStream_t s);
 void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
-                  cudaStream_t s, const std::function<void()> &overlap = {});
+                  cudaStream_t s, const std::function<void(cudaStream_t)> &overlap = {});
 // hot.cu: the S most referenced tile columns' x words live in shared memory
 constexpr uint32_t HOT_SMEM_BYTES = 196608;
 struct HotView {
@@ -196,7 +196,7 @@ void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y,
 void free_stream(void *plan);
 // bmv_bff.cu: float gather over the rows with <= thresh tiles
 void launch_bff_rows(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
-                     uint32_t thresh, cudaStream_t s);
+                     uint32_t thresh, cudaStream_t s, bool plan_only = false);
 void free_bff(void *plan);
 const uint4 *stream_desc(b2sr_matrix *m, cudaStream_t s, uint32_t *n_loads);  // per-load row descriptors
 void launch_stream_sweep(b2sr_matrix *m, const uint32_t *list, const uint32_t *list_n, const void *hx, size_t hb,

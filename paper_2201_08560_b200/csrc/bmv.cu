@@ -653,8 +653,9 @@ static void bff_ring(const b2sr_matrix *m, const double *x, int ring, double inc
         // (bmv_bff.cu); longer rows: segmented scatter + warp folds (bmv_vlong.cu)
         const char *ev = getenv("B2SR_VLONG_TILES");
         uint32_t hi = ev ? (uint32_t)atoi(ev) : VLONG_ROW_TILES;
-        launch_vlong(const_cast<b2sr_matrix *>(m), x, ring, inc, keep, y, s, [&] {
-            launch_bff_rows(const_cast<b2sr_matrix *>(m), x, ring, inc, keep, y, hi, s);
+        launch_bff_rows(const_cast<b2sr_matrix *>(m), x, ring, inc, keep, y, hi, s, /*plan_only=*/true);
+        launch_vlong(const_cast<b2sr_matrix *>(m), x, ring, inc, keep, y, s, [&](cudaStream_t so) {
+            launch_bff_rows(const_cast<b2sr_matrix *>(m), x, ring, inc, keep, y, hi, so);
         });
         return;
     }

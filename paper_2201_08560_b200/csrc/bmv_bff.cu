@@ -189,8 +189,8 @@ __global__ void __launch_bounds__(BFF_THREADS) k_bff_rows(uint32_t n_rows, const
 template <int D>
 static void bff_rows_ring(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
                           uint32_t thresh, cudaStream_t s) {
-    BffPlan *p = bff_plan(m, thresh, s);
-    if (!p->n_rows) return;
+    BffPlan *p = static_cast<BffPlan *>(m->bff);  // built by a plan_only call on the caller's stream
+    if (!p || !p->n_rows) return;
     constexpr uint32_t GPW = 32 / D;
     uint64_t warps = ((uint64_t)p->n_rows + GPW - 1) / GPW;
     unsigned g = (unsigned)std::min<uint64_t>((warps + BFF_THREADS / 32 - 1) / (BFF_THREADS / 32),
@@ -208,7 +208,9 @@ static void bff_rows_ring(b2sr_matrix *m, const double *x, int ring, double inc,
 }
 
 void launch_bff_rows(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
-                     uint32_t thresh, cudaStream_t s) {
+                     uint32_t thresh, cudaStream_t s, bool plan_only) {
+    bff_plan(m, thresh, s);
+    if (plan_only) return;
     switch (m->dim) {
         case 4: bff_rows_ring<4>(m, x, ring, inc, keep, y, thresh, s); break;
         case 8: bff_rows_ring<8>(m, x, ring, inc, keep, y, thresh, s); break;

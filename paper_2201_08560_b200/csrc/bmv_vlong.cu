@@ -30,7 +30,15 @@ struct VLongPlan {
     double *terms = nullptr;       // n_terms
     uint32_t *order = nullptr;     // n_rows * D vertices (row*D + r), fewest terms first
     uint32_t n_small = 0;          // the first n_small fold lane-per-vertex, the rest warp-per-vertex
+    // rows are ordered longest first; the first top_rows rows' units
+    // [0, top_units) are scattered first so their big vertices (big_top) can
+    // start their long fold chains while everything else is still running
+    uint32_t top_rows = 0, top_units = 0, n_big_top = 0, n_big_rest = 0;
+    uint32_t *big_top = nullptr;   // big vertices of the top rows, fewest terms first
+    uint32_t *big_rest = nullptr;  // the other big vertices, fewest terms first
 };
+
+constexpr uint32_t TOP_ROWS = 64;  // rows whose big vertices fold on the side stream first
 
 constexpr uint32_t LANE_FOLD_MAX = 2048;  // terms: above, one warp folds the vertex
 
@@ -44,6 +52,8 @@ void free_vlong(void *p) {
     dfree(v->total, nullptr);
     dfree(v->terms, nullptr);
     dfree(v->order, nullptr);
+    dfree(v->big_top, nullptr);
+    dfree(v->big_rest, nullptr);
     delete v;
 }
 
@@ -79,6 +89,18 @@ __global__ void k_vlong_order_keys(uint32_t nv, const uint32_t *__restrict__ tot
         val[k] = k;
         if (total[k] <= LANE_FOLD_MAX) atomicAdd(n_small, 1u);
     }
+}
+
+__global__ void k_vlong_len_keys(uint32_t nr, const uint32_t *__restrict__ rows, const uint32_t *__restrict__ trp,
+                                 uint32_t *__restrict__ key) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x)
+        key[i] = 0xFFFFFFFFu - (trp[rows[i] + 1] - trp[rows[i]]);
+}
+
+__global__ void k_vlong_nu(uint32_t nr, const uint32_t *__restrict__ rows, const uint32_t *__restrict__ trp,
+                           uint32_t *__restrict__ nu) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nr; i += gridDim.x * blockDim.x)
+        nu[i] = (trp[rows[i] + 1] - trp[rows[i]] + VSEG - 1) / VSEG;
 }
 
 // per (row, bit-row): offsets of its units inside the region, and the region length
@@ -142,7 +164,19 @@ void *build_vlong(b2sr_matrix *m, uint32_t thresh, cudaStream_t s) {
             Buf<uint32_t> rows(nr, s), nu(nr, s);
             Buf<uint64_t> uofs((size_t)nr + 1, s);
             LAUNCH(k_vlong_rows, grid(ntr), 256, 0, s, ntr, m->trp, f.p, pos.p, rows.p, nu.p);
+            {  // longest rows first (their hub vertices start folding first)
+                Buf<uint32_t> key(nr, s);
+                LAUNCH(k_vlong_len_keys, grid(nr), 256, 0, s, nr, rows.p, m->trp, key.p);
+                uint32_t *ko, *vo;
+                Buf<uint32_t> kalt, valt;
+                radix_sort_pairs_u32(key.p, rows.p, nr, 32, s, &ko, &vo, &kalt, &valt);
+                if (vo != rows.p) CK(cudaMemcpyAsync(rows.p, vo, (size_t)nr * 4, cudaMemcpyDeviceToDevice, s));
+                LAUNCH(k_vlong_nu, grid(nr), 256, 0, s, nr, rows.p, m->trp, nu.p);
+                CK(cudaStreamSynchronize(s));
+            }
             exclusive_scan_u32_to_u64(nu.p, uofs.p, nr, s);
+            v->top_rows = std::min<uint32_t>(nr, TOP_ROWS);
+            v->top_units = (uint32_t)read_scalar(uofs.p + v->top_rows, s);
             v->n_units = (uint32_t)read_scalar(uofs.p + nr, s);
             Buf<uint4> units(v->n_units, s);
             LAUNCH(k_vlong_units, grid(nr), 256, 0, s, nr, rows.p, m->trp, uofs.p, units.p);
@@ -185,6 +219,19 @@ void *build_vlong(b2sr_matrix *m, uint32_t thresh, cudaStream_t s) {
                 Buf<uint32_t> order(nv, s);
                 CK(cudaMemcpyAsync(order.p, vo, (size_t)nv * 4, cudaMemcpyDeviceToDevice, s));
                 v->n_small = read_scalar(nsm.p, s);
+                // split the big vertices by row (host side: a few thousand entries)
+                const uint32_t nb = nv - v->n_small;
+                std::vector<uint32_t> big(nb), top, rest;
+                if (nb) CK(cudaMemcpyAsync(big.data(), order.p + v->n_small, (size_t)nb * 4, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                for (uint32_t k : big) (k / D < v->top_rows ? top : rest).push_back(k);
+                v->n_big_top = (uint32_t)top.size();
+                v->n_big_rest = (uint32_t)rest.size();
+                v->big_top = static_cast<uint32_t *>(dalloc(std::max<size_t>(top.size(), 1) * 4, s));
+                v->big_rest = static_cast<uint32_t *>(dalloc(std::max<size_t>(rest.size(), 1) * 4, s));
+                if (!top.empty()) CK(cudaMemcpyAsync(v->big_top, top.data(), top.size() * 4, cudaMemcpyHostToDevice, s));
+                if (!rest.empty()) CK(cudaMemcpyAsync(v->big_rest, rest.data(), rest.size() * 4, cudaMemcpyHostToDevice, s));
+                CK(cudaStreamSynchronize(s));
                 v->order = order.release();
             }
             v->total = total.release();
@@ -481,86 +528,84 @@ __global__ void __launch_bounds__(256) k_vlong_fold(uint32_t n_big, const uint32
 
 // Side stream for the hub folds (one per device and host thread), so their
 // long dependent chains overlap the rest of the sweep.
-static cudaStream_t side_stream() {
-    static thread_local cudaStream_t ss[16] = {};
+static cudaStream_t side_stream(int which = 0) {
+    static thread_local cudaStream_t ss[1][16] = {};
     int dev = 0;
     CK(cudaGetDevice(&dev));
     if (dev >= 16) return nullptr;
-    if (!ss[dev]) CK(cudaStreamCreateWithFlags(&ss[dev], cudaStreamNonBlocking));
-    return ss[dev];
+    if (!ss[which][dev]) CK(cudaStreamCreateWithFlags(&ss[which][dev], cudaStreamNonBlocking));
+    return ss[which][dev];
 }
 
 // Scatter, then the folds; `overlap` runs while the hub folds proceed on the
 // side stream (the main stream waits for them before returning).
 void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
-                  cudaStream_t s, const std::function<void()> &overlap) {
+                  cudaStream_t s, const std::function<void(cudaStream_t)> &overlap) {
     VLongPlan *v = static_cast<VLongPlan *>(m->vlong);
     if (!v || !v->n_rows) {
-        if (overlap) overlap();
+        if (overlap) overlap(s);
         return;
     }
-    unsigned gu = std::min<unsigned>(v->n_units, (unsigned)num_sms() * 8);
-    const uint32_t nv = v->n_rows * m->dim, n_big = nv - v->n_small;
-    unsigned gw = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)v->n_units + 7) / 8, (uint64_t)num_sms() * 16));
-    unsigned gl = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((v->n_small + 255) / 256, (uint64_t)num_sms() * 8));
-    switch (m->dim) {  // scatter every unit's terms into the regions
-        case 4: LAUNCH(k_vlong_scatter_w<4>, gw, 256, 0, s, v->n_units, v->units, v->unit_off, v->base, m->tci, (const uint8_t *)m->tiles, x, v->terms); break;
-        case 8: LAUNCH(k_vlong_scatter_w<8>, gw, 256, 0, s, v->n_units, v->units, v->unit_off, v->base, m->tci, (const uint8_t *)m->tiles, x, v->terms); break;
-        case 16: LAUNCH(k_vlong_scatter<16>, gu, VTHREADS, 0, s, v->n_units, v->units, v->unit_off, v->base, m->tci, (const uint16_t *)m->tiles, x, v->terms); break;
-        default: LAUNCH(k_vlong_scatter<32>, gu, VTHREADS, 0, s, v->n_units, v->units, v->unit_off, v->base, m->tci, (const uint32_t *)m->tiles, x, v->terms); break;
-    }
-    cudaStream_t s2 = n_big ? side_stream() : nullptr;
+    auto scatter = [&](uint32_t u0, uint32_t u1) {  // units [u0, u1)
+        if (u1 <= u0) return;
+        const uint32_t nu = u1 - u0;
+        unsigned gu = std::min<unsigned>(nu, (unsigned)num_sms() * 8);
+        unsigned gw = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)nu + 7) / 8, (uint64_t)num_sms() * 16));
+        const uint4 *un = v->units + u0;
+        const uint32_t *uo = v->unit_off + (size_t)u0 * m->dim;
+        switch (m->dim) {
+            case 4: LAUNCH(k_vlong_scatter_w<4>, gw, 256, 0, s, nu, un, uo, v->base, m->tci, (const uint8_t *)m->tiles, x, v->terms); break;
+            case 8: LAUNCH(k_vlong_scatter_w<8>, gw, 256, 0, s, nu, un, uo, v->base, m->tci, (const uint8_t *)m->tiles, x, v->terms); break;
+            case 16: LAUNCH(k_vlong_scatter<16>, gu, VTHREADS, 0, s, nu, un, uo, v->base, m->tci, (const uint16_t *)m->tiles, x, v->terms); break;
+            default: LAUNCH(k_vlong_scatter<32>, gu, VTHREADS, 0, s, nu, un, uo, v->base, m->tci, (const uint32_t *)m->tiles, x, v->terms); break;
+        }
+    };
+    // 1. the top rows' terms, then their big vertices' chains on the side stream
+    scatter(0, v->top_units);
+    cudaStream_t s2 = v->n_big_top ? side_stream() : nullptr;
     cudaEvent_t e1 = nullptr, e2 = nullptr;
-    cudaStream_t sb = s;
+    const size_t top_smem = 160 * 1024;  // one fold warp per SM: its chain is the critical path
     if (s2) {
         CK(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&e2, cudaEventDisableTiming));
         CK(cudaEventRecord(e1, s));
         CK(cudaStreamWaitEvent(s2, e1, 0));
-        sb = s2;
     }
-    // the largest vertices first, one warp per SM (a large dynamic shared
-    // allocation keeps other fold warps off that SM: their chains would slow
-    // the longest one down); then the rest, eight warps per block
-    const uint32_t n_top = std::min<uint32_t>(n_big, (uint32_t)num_sms());
-    const uint32_t n_rest = n_big - n_top;
-    const size_t top_smem = 160 * 1024;
-    unsigned gr = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)n_rest + 7) / 8, (uint64_t)num_sms() * 8));
-#define VL_BIG(DD, RR)                                                                                             \
-    do {                                                                                                           \
-        hot_smem_attr(k_vlong_fold<DD, RR>, top_smem);                                                             \
-        LAUNCH((k_vlong_fold<DD, RR>), n_top, 32, top_smem, sb, n_top, v->order + v->n_small + n_rest, v->rows,     \
-               v->base, v->total, v->terms, inc, m->n, keep, y, m->row0);                                          \
-        if (n_rest)                                                                                                \
-            LAUNCH((k_vlong_fold<DD, RR>), gr, 256, 0, sb, n_rest, v->order + v->n_small, v->rows, v->base,        \
-                   v->total, v->terms, inc, m->n, keep, y, m->row0);                                               \
+    // 2. the rest of the terms, the other big vertices, the small ones, then `overlap`
+    const unsigned gr = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)v->n_big_rest + 7) / 8, (uint64_t)num_sms() * 8));
+    const unsigned gl = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((v->n_small + 255) / 256, (uint64_t)num_sms() * 8));
+#define VL_RING(DD, RR)                                                                                             \
+    do {                                                                                                            \
+        if (s2) {                                                                                                   \
+            hot_smem_attr(k_vlong_fold<DD, RR>, top_smem);                                                          \
+            LAUNCH((k_vlong_fold<DD, RR>), std::min<uint32_t>(v->n_big_top, (uint32_t)num_sms()), 32, top_smem, s2, \
+                   v->n_big_top, v->big_top, v->rows, v->base, v->total, v->terms, inc, m->n, keep, y, m->row0);    \
+        }                                                                                                           \
+        scatter(v->top_units, v->n_units);                                                                          \
+        if (v->n_big_rest)                                                                                          \
+            LAUNCH((k_vlong_fold<DD, RR>), gr, 256, 0, s, v->n_big_rest, v->big_rest, v->rows, v->base, v->total,   \
+                   v->terms, inc, m->n, keep, y, m->row0);                                                          \
+        if (v->n_small)                                                                                             \
+            LAUNCH((k_vlong_fold_lanes<DD, RR>), gl, 256, 0, s, v->n_small, v->order, v->rows, v->base, v->total,   \
+                   v->terms, inc, m->n, keep, y, m->row0);                                                          \
     } while (0)
-#define VL_SMALL(DD, RR)                                                                                           \
-    LAUNCH((k_vlong_fold_lanes<DD, RR>), gl, 256, 0, s, v->n_small, v->order, v->rows, v->base, v->total, v->terms, \
-           inc, m->n, keep, y, m->row0)
-#define VL_RING(DD)                                                                                                \
-    do {                                                                                                           \
-        if (ring == B2SR_RING_ARITHMETIC) {                                                                        \
-            if (n_big) VL_BIG(DD, B2SR_RING_ARITHMETIC);                                                           \
-            if (v->n_small) VL_SMALL(DD, B2SR_RING_ARITHMETIC);                                                    \
-        } else if (ring == B2SR_RING_MINPLUS) {                                                                    \
-            if (n_big) VL_BIG(DD, B2SR_RING_MINPLUS);                                                              \
-            if (v->n_small) VL_SMALL(DD, B2SR_RING_MINPLUS);                                                       \
-        } else {                                                                                                   \
-            if (n_big) VL_BIG(DD, B2SR_RING_MAXTIMES);                                                             \
-            if (v->n_small) VL_SMALL(DD, B2SR_RING_MAXTIMES);                                                      \
-        }                                                                                                          \
+#define VL_DIM(DD)                                                                                                  \
+    do {                                                                                                            \
+        if (ring == B2SR_RING_ARITHMETIC) VL_RING(DD, B2SR_RING_ARITHMETIC);                                        \
+        else if (ring == B2SR_RING_MINPLUS) VL_RING(DD, B2SR_RING_MINPLUS);                                         \
+        else VL_RING(DD, B2SR_RING_MAXTIMES);                                                                       \
     } while (0)
     switch (m->dim) {
-        case 4: VL_RING(4); break;
-        case 8: VL_RING(8); break;
-        case 16: VL_RING(16); break;
-        default: VL_RING(32); break;
+        case 4: VL_DIM(4); break;
+        case 8: VL_DIM(8); break;
+        case 16: VL_DIM(16); break;
+        default: VL_DIM(32); break;
     }
+#undef VL_DIM
 #undef VL_RING
-#undef VL_SMALL
-#undef VL_BIG
-    if (overlap) overlap();
+    // `overlap` (the short-row kernel) follows on the main stream: running it on
+    // a third stream as well was measured slower (memory contention)
+    if (overlap) overlap(s);
     if (s2) {
         CK(cudaEventRecord(e2, s2));
         CK(cudaStreamWaitEvent(s, e2, 0));
