@@ -634,8 +634,9 @@ def run_reference(args, rank, world):
 
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
-    rp, ci = orc.rmat_csr(args.scale, args.edgefactor, seed=args.seed)
-    n = 1 << args.scale
+    scale = args.scale + (max(0, int(round(np.log2(world)))) if world > 1 else 0)  # our arm's graph
+    rp, ci = orc.rmat_csr(scale, args.edgefactor, seed=args.seed)
+    n = 1 << scale
     d = args.dim or 4
     m = orc.csr_to_b2sr(n, rp, ci, d, workers=threads)
     setup = time.perf_counter() - t0
@@ -658,8 +659,8 @@ def run_reference(args, rank, world):
             "steps": done, "warmup": min(args.warmup, 1), "ms_per_step": round(1e3 * secs / done, 2),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 bit-words",
             "data": f"synthetic R-MAT seed {args.seed} (CPU twin of the device generator)",
-            "config": {"workload": f"BFS via masked bin-SpMV, undirected R-MAT scale {args.scale} "
-                                   f"edgefactor {args.edgefactor}, B2SR-{d}", "scale": args.scale, "tile_dim": d},
+            "config": {"workload": f"BFS via masked bin-SpMV, undirected R-MAT scale {scale} "
+                                   f"edgefactor {args.edgefactor}, B2SR-{d}", "scale": scale, "tile_dim": d},
             "cpu_baseline": {"value": round(v, 6), "unit": "GTEPS", "cores": threads, "kind": "port",
                              "sample": f"{done} BFS roots incl. transpose; stopped after {budget_s:.0f}s"},
             "e2e": {"value": round(v, 6), "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
