@@ -81,26 +81,18 @@ def zeros_bytes(nbytes: int):
 def to_host(tensor, dtype, count: int) -> np.ndarray:
     """Copy the first ``count`` elements of ``dtype`` out of a device buffer.
 
-    The copy lands in page-locked memory (torch's caching host allocator), so
-    it is one DMA at PCIe/C2C speed; the returned array keeps that buffer alive.
+    The copy lands directly in page-locked memory (torch's caching host
+    allocator: one DMA at PCIe/C2C speed, no second host copy); the returned
+    array keeps that buffer alive.
     """
-    global _bounce
     t = torch()
     dt = np.dtype(dtype)
     nbytes = count * dt.itemsize
-    out = np.empty(count, dt)
     if nbytes == 0:
-        return out
-    with _bounce_lock:
-        if _bounce is None or _bounce.numel() < nbytes:
-            _bounce = t.empty(max(nbytes, 1 << 20), dtype=t.uint8, pin_memory=True)
-        _bounce[:nbytes].copy_(tensor.detach().view(t.uint8)[:nbytes])
-        out.view(np.uint8)[:] = _bounce[:nbytes].numpy()
-    return out
-
-
-_bounce = None  # reusable page-locked staging buffer for device -> host copies
-_bounce_lock = threading.Lock()
+        return np.empty(count, dt)
+    host = t.empty(nbytes, dtype=t.uint8, pin_memory=True)
+    host.copy_(tensor.detach().view(t.uint8)[:nbytes])
+    return host.numpy().view(dt)
 
 
 def ptr(tensor) -> int:

@@ -17,7 +17,7 @@ constexpr int RS_ROUNDS = 16;
 constexpr int RS_TILE = RS_THREADS * RS_ROUNDS;  // 4096 keys per CTA
 
 template <typename K>
-__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K *__restrict__ keys, size_t n, int sh,
+__global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K *__restrict__ keys, size_t n, int sh, uint32_t dm,
                                                         uint32_t *__restrict__ counts, uint32_t nblocks) {
     __shared__ uint32_t h[256];
     h[threadIdx.x] = 0;
@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K *__restrict__ ke
 #pragma unroll 4
     for (int j = 0; j < RS_ROUNDS; j++) {
         size_t i = base + (size_t)j * RS_THREADS + threadIdx.x;
-        if (i < n) atomicAdd(&h[(uint32_t)(keys[i] >> sh) & 0xFFu], 1u);
+        if (i < n) atomicAdd(&h[(uint32_t)(keys[i] >> sh) & dm], 1u);
     }
     __syncthreads();
     counts[(size_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
@@ -35,8 +35,8 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K *__restrict__ ke
 template <typename K, bool VALS>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
                                                            K *__restrict__ kout, uint32_t *__restrict__ vout,
-                                                           size_t n, int sh, const uint64_t *__restrict__ offs,
-                                                           uint32_t nblocks) {
+                                                           size_t n, int sh, uint32_t dm,
+                                                           const uint64_t *__restrict__ offs, uint32_t nblocks) {
     __shared__ uint32_t wc[RS_WARPS][256];
     __shared__ uint32_t dbase[256];            // CTA-local start of each digit run
     __shared__ K skey[RS_TILE];                // keys re-ordered by digit inside the CTA
@@ -55,7 +55,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__
         bool ok = i < n;
         key[j] = ok ? kin[i] : (K)0;
         if constexpr (VALS) val[j] = ok ? vin[i] : 0u;
-        uint32_t dg = ok ? ((uint32_t)(key[j] >> sh) & 0xFFu) : 256u;  // 256 = no item
+        uint32_t dg = ok ? ((uint32_t)(key[j] >> sh) & dm) : 256u;  // 256 = no item
         uint32_t peers = __match_any_sync(0xffffffffu, dg);
         uint32_t leader = __ffs(peers) - 1;
         uint32_t before = dg < 256 ? wc[w][dg] : 0u;
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__
     for (int j = 0; j < RS_ROUNDS; j++) {  // stage in digit order inside the CTA
         size_t i = base + (size_t)j * 32 + lane;
         if (i < n) {
-            uint32_t dg = (uint32_t)(key[j] >> sh) & 0xFFu;
+            uint32_t dg = (uint32_t)(key[j] >> sh) & dm;
             uint32_t lp = dbase[dg] + wc[w][dg] + rank[j];
             skey[lp] = key[j];
             if constexpr (VALS) sval[lp] = val[j];
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__
     uint32_t count = (uint32_t)min((size_t)RS_TILE, n - (size_t)blockIdx.x * RS_TILE);
     for (uint32_t lp = threadIdx.x; lp < count; lp += RS_THREADS) {
         K k = skey[lp];
-        uint32_t dg = (uint32_t)(k >> sh) & 0xFFu;
+        uint32_t dg = (uint32_t)(k >> sh) & dm;
         size_t pos = offs[(size_t)dg * nblocks + blockIdx.x] + (lp - dbase[dg]);
         kout[pos] = k;
         if constexpr (VALS) vout[pos] = sval[lp];
@@ -117,9 +117,12 @@ static void rs_passes(K *ka, uint32_t *va, K *kb, uint32_t *vb, size_t n, int bi
     K *kin = ka, *kout = kb;
     uint32_t *vin = va, *vout = vb;
     for (int sh = 0; sh < bits; sh += 8) {
-        LAUNCH(k_rs_hist<K>, nblocks, RS_THREADS, 0, s, kin, n, sh, counts.p, nblocks);
+        // the last digit covers only the remaining key bits: bits above `bits`
+        // may carry payload (the d=4 transpose packs row and tile there)
+        const uint32_t dm = bits - sh >= 8 ? 0xFFu : (1u << (bits - sh)) - 1u;
+        LAUNCH(k_rs_hist<K>, nblocks, RS_THREADS, 0, s, kin, n, sh, dm, counts.p, nblocks);
         exclusive_scan_u32_to_u64(counts.p, offs.p, (size_t)nblocks * 256, s);
-        LAUNCH((k_rs_scatter<K, VALS>), nblocks, RS_THREADS, 0, s, kin, vin, kout, vout, n, sh, offs.p, nblocks);
+        LAUNCH((k_rs_scatter<K, VALS>), nblocks, RS_THREADS, 0, s, kin, vin, kout, vout, n, sh, dm, offs.p, nblocks);
         std::swap(kin, kout);
         std::swap(vin, vout);
     }

@@ -114,6 +114,31 @@ __global__ void __launch_bounds__(256) k_transpose_gather(uint64_t T, const uint
     }
 }
 
+// d=4 fast path: a 4x4 tile is 16 bits of payload, so (column | row | tile)
+// fits one 64-bit key and a stable radix sort over the column bits carries
+// every tile to its transposed position -- no random gathers afterwards.
+__global__ void k_pack4(uint64_t T, const uint32_t *__restrict__ rowid, const uint32_t *__restrict__ tci,
+                        const uint32_t *__restrict__ tiles, int cb, uint64_t *__restrict__ keys) {
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < T; t += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t w = tiles[t];  // four row bytes, low nibbles
+        uint32_t nib = (w & 0xFu) | ((w >> 4) & 0xF0u) | ((w >> 8) & 0xF00u) | ((w >> 12) & 0xF000u);
+        keys[t] = (uint64_t)tci[t] | ((uint64_t)rowid[t] << cb) | ((uint64_t)nib << (2 * cb));
+    }
+}
+
+__global__ void k_unpack4(uint64_t T, const uint64_t *__restrict__ keys, int cb, uint32_t *__restrict__ tci_out,
+                          uint32_t *__restrict__ tiles_out) {
+    const uint64_t mask = (1ull << cb) - 1;
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < T; p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[p];
+        tci_out[p] = (uint32_t)((k >> cb) & mask);  // the source row is the transposed column
+        uint32_t nib = (uint32_t)(k >> (2 * cb));
+        uint32_t a[4] = {nib & 0xFu, (nib >> 4) & 0xFu, (nib >> 8) & 0xFu, (nib >> 12) & 0xFu};
+        bit_transpose<4>(a);
+        tiles_out[p] = a[0] | (a[1] << 8) | (a[2] << 16) | (a[3] << 24);
+    }
+}
+
 void launch_row_ids(const b2sr_matrix *m, uint32_t *rowid, cudaStream_t s) {
     uint64_t b = ((uint64_t)m->ntr * 32 + 255) / 256, cap = (uint64_t)num_sms() * 16;
     LAUNCH(k_row_ids, (unsigned)std::max<uint64_t>(1, std::min(b, cap)), 256, 0, s, m->ntr, m->trp, rowid);
@@ -143,7 +168,18 @@ b2sr_matrix *transpose_device(const b2sr_matrix *m, cudaStream_t s) {
         if (T) LAUNCH(k_col_hist, grid_for(T), 256, 0, s, T, m->tci, cnt.p);
         exclusive_scan_u32_to_u64(cnt.p, ofs.p, ntr, s);
         LAUNCH(k_u64_to_u32, grid_for(ntr + 1), 256, 0, s, ofs.p, o->trp, (size_t)ntr + 1);
-        if (T) {
+        const int cb = bits_for(ntr - 1);
+        if (T && m->dim == 4 && 2 * cb + 16 <= 64) {
+            Buf<uint64_t> keys(T, s), kalt;
+            {
+                Buf<uint32_t> rowid(T, s);
+                LAUNCH(k_row_ids, grid_for((uint64_t)ntr * 32), 256, 0, s, ntr, m->trp, rowid.p);
+                LAUNCH(k_pack4, grid_for(T), 256, 0, s, T, rowid.p, m->tci, (const uint32_t *)m->tiles, cb, keys.p);
+            }
+            uint64_t *ks = nullptr;
+            radix_sort_keys_u64(keys.p, T, cb, s, &ks, &kalt);
+            LAUNCH(k_unpack4, grid_for(T), 256, 0, s, T, ks, cb, o->tci, (uint32_t *)o->tiles);
+        } else if (T) {
             Buf<uint32_t> keys(T, s), vals(T, s), rowid(T, s), kalt, valt;
             CK(cudaMemcpyAsync(keys.p, m->tci, T * 4, cudaMemcpyDeviceToDevice, s));
             LAUNCH(k_iota, grid_for(T), 256, 0, s, vals.p, T);
