@@ -148,6 +148,18 @@ int b2sr_bfs_sweep(const b2sr_matrix *at_block, const void *d_frontier, const vo
                    void *stream);
 int b2sr_bfs_update(uint32_t n, uint32_t dim, const void *d_frontier, void *d_visited, double *d_levels,
                     double level, int *d_any, void *stream);
+/* Row-partitioned levels with the single-GPU sweep shortcuts: flags
+ * B2SR_SWEEP_ACTIVE streams only the loads whose rows still hold an
+ * unvisited vertex, B2SR_SWEEP_LAZY fetches tile bytes only where the
+ * frontier words are non-zero (sparse frontiers).  Same output as
+ * b2sr_bfs_sweep.  b2sr_bfs_update_ex also adds the frontier's vertex count
+ * to *d_frontier_vertices (u64, caller-zeroed). */
+#define B2SR_SWEEP_ACTIVE 1
+#define B2SR_SWEEP_LAZY 2
+int b2sr_bfs_sweep_ex(const b2sr_matrix *at_block, const void *d_frontier, const void *d_visited, void *d_next,
+                      int flags, void *stream);
+int b2sr_bfs_update_ex(uint32_t n, uint32_t dim, const void *d_frontier, void *d_visited, double *d_levels,
+                       double level, int *d_any, uint64_t *d_frontier_vertices, void *stream);
 /* sssp relaxation (algorithms.py:113-124) on at = transpose(drop_diag(a)). */
 int b2sr_sssp(const b2sr_matrix *at, uint32_t src, double *d_dist, int64_t *iterations, void *stream);
 /* pagerank (algorithms.py:127-163); a = transposed adjacency. */

@@ -54,6 +54,8 @@ SIGNATURES = {
     "b2sr_bfs_init": [u32, u32, u32, P, P, P, P],
     "b2sr_bfs_sweep": [P, P, P, P, P],
     "b2sr_bfs_update": [u32, u32, P, P, P, f64, P, P],
+    "b2sr_bfs_sweep_ex": [P, P, P, P, i32, P],
+    "b2sr_bfs_update_ex": [u32, u32, P, P, P, f64, P, P, P],
     "b2sr_sssp": [P, u32, P, P, P],
     "b2sr_pagerank": [P, P, f64, f64, i64, P, P, P, P, P],
     "b2sr_cc": [P, P, P, P],

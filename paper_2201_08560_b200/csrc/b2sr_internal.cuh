@@ -192,7 +192,7 @@ bool stream_enabled(int dim);
 // visited != null: BFS pull (y &= ~visited & live instead of keep)
 // active_only (with visited): only the loads that hold a row with an unvisited live vertex
 void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaStream_t s,
-                       const void *visited = nullptr, bool active_only = false);
+                       const void *visited = nullptr, bool active_only = false, bool lazy = false);
 void free_stream(void *plan);
 // bmv_bff.cu: float gather over the rows with <= thresh tiles
 void launch_bff_rows(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
@@ -200,7 +200,7 @@ void launch_bff_rows(b2sr_matrix *m, const double *x, int ring, double inc, cons
 void free_bff(void *plan);
 const uint4 *stream_desc(b2sr_matrix *m, cudaStream_t s, uint32_t *n_loads);  // per-load row descriptors
 void launch_stream_sweep(b2sr_matrix *m, const uint32_t *list, const uint32_t *list_n, const void *hx, size_t hb,
-                         const void *x, void *y, const int *gate, int want, cudaStream_t s);
+                         const void *x, void *y, const int *gate, int want, cudaStream_t s, bool lazy = false);
 // blocked bin-SpMV: mode 0 = masked bbb, 1 = BFS pull; false if not applicable
 bool launch_blocked(b2sr_matrix *m, int mode, const void *x, const void *keep, void *y, cudaStream_t s);
 // B2SR_BLOCKED=1 selects the column-strip blocked kernels (A/B measurements)

@@ -317,7 +317,7 @@ __device__ __forceinline__ void bbb_stream(uint32_t p0, uint32_t p1, uint32_t n_
     }
 }
 
-template <int D, int NT, bool LIST>
+template <int D, int NT, bool LIST, bool LAZY = false>
 __global__ void __launch_bounds__(NT, 1)
     k_bmv_bbb_stream(uint32_t n_loads, const uint32_t *__restrict__ list, const uint32_t *__restrict__ list_n,
                      uint64_t T, const uint4 *__restrict__ desc, const uint32_t *__restrict__ trp,
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(NT, 1)
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5, w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t per = (n_pos + warps - 1) / warps;
     const uint32_t p0 = std::min(n_pos, w * per), p1 = std::min(n_pos, p0 + per);
-    bbb_stream<D, LIST>(p0, p1, n_loads, T, list, desc, trp, tiles, tci2, gx, y);
+    bbb_stream<D, LIST, XHot<D>, LAZY>(p0, p1, n_loads, T, list, desc, trp, tiles, tci2, gx, y);
 }
 
 // ------------------------------------------------------------ fused BFS level
@@ -511,7 +511,7 @@ const uint4 *stream_desc(b2sr_matrix *m, cudaStream_t s, uint32_t *n_loads) {
 
 // The stream kernel alone: y must be zeroed and hx filled (hot_fill) by the caller.
 void launch_stream_sweep(b2sr_matrix *m, const uint32_t *list, const uint32_t *list_n, const void *hx, size_t hb,
-                         const void *x, void *y, const int *gate, int want, cudaStream_t s) {
+                         const void *x, void *y, const int *gate, int want, cudaStream_t s, bool lazy) {
     if (!m->num_tiles) return;
     StreamPlan *sp = stream_plan(m, LT, s);
     HotView hv = hot_view(m, s);
@@ -520,16 +520,21 @@ void launch_stream_sweep(b2sr_matrix *m, const uint32_t *list, const uint32_t *l
     const uint8_t *tl = (const uint8_t *)m->tiles;
     const char *te = getenv("B2SR_STREAM_THREADS");  // A/B: 768 / 1024 threads per CTA
     int nt = te ? atoi(te) : (m->dim == 4 ? 1024 : 768);
+#define STREAM_LAUNCH3(DD, NT, LI, LZ)                                                                               \
+    do {                                                                                                             \
+        hot_smem_attr(k_bmv_bbb_stream<DD, NT, LI, LZ>, hb);                                                         \
+        LAUNCH((k_bmv_bbb_stream<DD, NT, LI, LZ>), g, NT, hb, s, sp->n_loads, LI ? list : nullptr,                   \
+               LI ? list_n : nullptr, m->num_tiles, sp->desc, m->trp, tl, hv.tci2, hx, (uint32_t)hb, hv.S, x, y,    \
+               gate, want);                                                                                          \
+    } while (0)
 #define STREAM_LAUNCH(DD, NT)                                                                                        \
     do {                                                                                                             \
         if (list) {                                                                                                  \
-            hot_smem_attr(k_bmv_bbb_stream<DD, NT, true>, hb);                                                       \
-            LAUNCH((k_bmv_bbb_stream<DD, NT, true>), g, NT, hb, s, sp->n_loads, list, list_n, m->num_tiles,          \
-                   sp->desc, m->trp, tl, hv.tci2, hx, (uint32_t)hb, hv.S, x, y, gate, want);                         \
+            if (lazy) STREAM_LAUNCH3(DD, NT, true, true);                                                            \
+            else STREAM_LAUNCH3(DD, NT, true, false);                                                                \
         } else {                                                                                                     \
-            hot_smem_attr(k_bmv_bbb_stream<DD, NT, false>, hb);                                                      \
-            LAUNCH((k_bmv_bbb_stream<DD, NT, false>), g, NT, hb, s, sp->n_loads, nullptr, nullptr, m->num_tiles,     \
-                   sp->desc, m->trp, tl, hv.tci2, hx, (uint32_t)hb, hv.S, x, y, gate, want);                         \
+            if (lazy) STREAM_LAUNCH3(DD, NT, false, true);                                                           \
+            else STREAM_LAUNCH3(DD, NT, false, false);                                                               \
         }                                                                                                            \
     } while (0)
     if (m->dim == 4) {
@@ -539,10 +544,11 @@ void launch_stream_sweep(b2sr_matrix *m, const uint32_t *list, const uint32_t *l
         STREAM_LAUNCH(8, 768);
     }
 #undef STREAM_LAUNCH
+#undef STREAM_LAUNCH3
 }
 
 void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaStream_t s,
-                       const void *visited, bool active_only) {
+                       const void *visited, bool active_only, bool lazy) {
     const size_t yb = padded_vec_bytes(m->ntr, m->dim);
     CK(cudaMemsetAsync(y, 0, yb, s));
     if (!m->num_tiles) return;
@@ -563,7 +569,7 @@ void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y,
     }
     hot_fill(hv, m->dim, x, hx.p, s);
     kernel_timer().begin(s);
-    launch_stream_sweep(m, list.p, list_n.p, hx.p, hb, x, y, nullptr, 0, s);
+    launch_stream_sweep(m, list.p, list_n.p, hx.p, hb, x, y, nullptr, 0, s, lazy);
     kernel_timer().end(s);
     if (visited) {  // BFS pull: keep = ~visited & live, applied once at the end
         const uint8_t *vp = static_cast<const uint8_t *>(visited) + (size_t)m->row0 * word_bytes(m->dim);

@@ -198,13 +198,16 @@ __global__ void __launch_bounds__(256) k_bfs_pull_g(const WorkItem *__restrict__
 // visited |= frontier; levels[new bits] = level; *any |= frontier != 0
 template <int D>
 __global__ void k_bfs_update(uint32_t ntr, const void *__restrict__ frontier, void *__restrict__ visited,
-                             double *__restrict__ levels, double level, int *__restrict__ any) {
+                             double *__restrict__ levels, double level, int *__restrict__ any,
+                             unsigned long long *__restrict__ fv) {
     using W = typename WordT<D>::T;
     int found = 0;
+    uint32_t cnt = 0;
     for (uint32_t I = blockIdx.x * blockDim.x + threadIdx.x; I < ntr; I += gridDim.x * blockDim.x) {
         uint32_t w = load_word<D>(frontier, I);
         if (!w) continue;
         found = 1;
+        cnt += __popc(w);
         W *vis = reinterpret_cast<W *>(visited);
         vis[I] = (W)(vis[I] | w);
         while (w) {
@@ -214,6 +217,10 @@ __global__ void k_bfs_update(uint32_t ntr, const void *__restrict__ frontier, vo
         }
     }
     if (__any_sync(0xffffffffu, found) && lane_id() == 0) atomicOr(any, 1);
+    if (fv) {
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane_id() == 0 && cnt) atomicAdd(fv, (unsigned long long)cnt);
+    }
 }
 
 __global__ void k_fill_f64(double *v, size_t n, double val) {
@@ -488,12 +495,13 @@ static bool pull_stream(const b2sr_matrix *at) {
 }
 
 void bfs_sweep(b2sr_matrix *at, const void *frontier, const void *visited, void *next, cudaStream_t s,
-               const uint32_t *idx = nullptr, const uint32_t *idx_n = nullptr, int active_only = -1) {
+               const uint32_t *idx = nullptr, const uint32_t *idx_n = nullptr, int active_only = -1,
+               bool lazy = false) {
     ensure_live(at, s);
     if (!idx && blocked_enabled() && launch_blocked(at, 1, frontier, visited, next, s)) return;
     if (!idx && pull_stream(at)) {
         // only the loads that still hold an unvisited vertex, once few are left
-        launch_bbb_stream(at, frontier, nullptr, next, s, visited, active_only > 0);
+        launch_bbb_stream(at, frontier, nullptr, next, s, visited, active_only > 0, lazy);
         return;
     }
     ensure_items(at, s);
@@ -547,14 +555,14 @@ void bfs_sweep(b2sr_matrix *at, const void *frontier, const void *visited, void 
 }
 
 void bfs_update(uint32_t n, uint32_t d, const void *frontier, void *visited, double *levels, double level, int *any,
-                cudaStream_t s) {
+                cudaStream_t s, unsigned long long *fv = nullptr) {
     uint32_t ntr = tile_rows(n, d);
     unsigned g = grid_for(ntr);
     switch (d) {
-        case 4: LAUNCH(k_bfs_update<4>, g, 256, 0, s, ntr, frontier, visited, levels, level, any); break;
-        case 8: LAUNCH(k_bfs_update<8>, g, 256, 0, s, ntr, frontier, visited, levels, level, any); break;
-        case 16: LAUNCH(k_bfs_update<16>, g, 256, 0, s, ntr, frontier, visited, levels, level, any); break;
-        default: LAUNCH(k_bfs_update<32>, g, 256, 0, s, ntr, frontier, visited, levels, level, any); break;
+        case 4: LAUNCH(k_bfs_update<4>, g, 256, 0, s, ntr, frontier, visited, levels, level, any, fv); break;
+        case 8: LAUNCH(k_bfs_update<8>, g, 256, 0, s, ntr, frontier, visited, levels, level, any, fv); break;
+        case 16: LAUNCH(k_bfs_update<16>, g, 256, 0, s, ntr, frontier, visited, levels, level, any, fv); break;
+        default: LAUNCH(k_bfs_update<32>, g, 256, 0, s, ntr, frontier, visited, levels, level, any, fv); break;
     }
 }
 
@@ -1186,6 +1194,22 @@ int b2sr_bfs_update(uint32_t n, uint32_t dim, const void *d_frontier, void *d_vi
                     double level, int *d_any, void *stream) {
     API_BEGIN
     bfs_update(n, dim, d_frontier, d_visited, d_levels, level, d_any, (cudaStream_t)stream);
+    API_END
+}
+
+int b2sr_bfs_sweep_ex(const b2sr_matrix *at_block, const void *d_frontier, const void *d_visited, void *d_next,
+                      int flags, void *stream) {
+    API_BEGIN
+    bfs_sweep(const_cast<b2sr_matrix *>(at_block), d_frontier, d_visited, d_next, (cudaStream_t)stream, nullptr,
+              nullptr, (flags & B2SR_SWEEP_ACTIVE) ? 1 : 0, (flags & B2SR_SWEEP_LAZY) != 0);
+    API_END
+}
+
+int b2sr_bfs_update_ex(uint32_t n, uint32_t dim, const void *d_frontier, void *d_visited, double *d_levels,
+                       double level, int *d_any, uint64_t *d_frontier_vertices, void *stream) {
+    API_BEGIN
+    bfs_update(n, dim, d_frontier, d_visited, d_levels, level, d_any, (cudaStream_t)stream,
+               reinterpret_cast<unsigned long long *>(d_frontier_vertices));
     API_END
 }
 

@@ -4,7 +4,8 @@ SURVEY.md §8e: the transposed adjacency is cut into contiguous tile-row
 blocks, one per rank; every rank keeps the full frontier / visited bit
 vectors (n/8 bytes) and its block of the matrix.  Per BFS level:
 
-    sweep   masked pull sweep over the rank's block      (k_bfs_pull, local)
+    sweep   masked pull sweep over the rank's block      (K4 stream: loads of rows
+            with unvisited vertices, lazy tile bytes behind sparse frontiers)
     gather  all_gather of the blocks' frontier words    (NCCL over NVLink)
     update  visited |= frontier, levels, any-flag        (k_bfs_update, local)
 
@@ -58,21 +59,26 @@ class CudaBfsOps:
 
     def buffers(self, global_bytes: int, block_bytes: int):
         return (dev.zeros_bytes(global_bytes), dev.zeros_bytes(global_bytes), dev.zeros_bytes(block_bytes),
-                dev.empty_bytes(8 * self.n), dev.zeros_bytes(4))
+                dev.empty_bytes(8 * self.n), dev.zeros_bytes(16))
 
     def init(self, src, visited, frontier, levels):
         _capi.call("b2sr_bfs_init", self.n, self.dim, src, dev.ptr(visited), dev.ptr(frontier), dev.ptr(levels),
                    dev.stream())
 
-    def sweep(self, frontier, visited, next_block):
-        _capi.call("b2sr_bfs_sweep", self.block.ptr, dev.ptr(frontier), dev.ptr(visited), dev.ptr(next_block),
-                   dev.stream())
+    def sweep(self, frontier, visited, next_block, sparse=False):
+        # the block's loads of rows with unvisited vertices only; tile bytes
+        # fetched lazily behind a sparse frontier (same output either way)
+        flags = 1 | (2 if sparse else 0)  # B2SR_SWEEP_ACTIVE | B2SR_SWEEP_LAZY
+        _capi.call("b2sr_bfs_sweep_ex", self.block.ptr, dev.ptr(frontier), dev.ptr(visited), dev.ptr(next_block),
+                   flags, dev.stream())
 
-    def update(self, frontier, visited, levels, level, anyflag) -> bool:
+    def update(self, frontier, visited, levels, level, anyflag):
+        """visited |= frontier, levels; (any new vertex, frontier vertex count)."""
         anyflag.zero_()
-        _capi.call("b2sr_bfs_update", self.n, self.dim, dev.ptr(frontier), dev.ptr(visited), dev.ptr(levels),
-                   float(level), dev.ptr(anyflag), dev.stream())
-        return bool(anyflag.view(dev.torch().int32)[0].item())
+        _capi.call("b2sr_bfs_update_ex", self.n, self.dim, dev.ptr(frontier), dev.ptr(visited), dev.ptr(levels),
+                   float(level), dev.ptr(anyflag), dev.ptr(anyflag) + 8, dev.stream())
+        h = anyflag.cpu()
+        return bool(h[:4].view(dev.torch().int32)[0].item()), int(h[8:16].view(dev.torch().int64)[0].item())
 
     def levels_to_host(self, levels):
         return dev.to_host(levels, np.float64, self.n)
@@ -125,11 +131,13 @@ class DistributedBfs:
         visited, frontier, nxt, levels, anyflag = ops.buffers(self.global_bytes, self.block_bytes)
         ops.init(src, visited, frontier, levels)
         sweeps = 0
+        sparse = True  # level 1: the frontier is {src}
         while True:
-            ops.sweep(frontier, visited, nxt)
+            ops.sweep(frontier, visited, nxt, sparse)
             all_gather_words(self.dist, frontier, nxt, self.world)
             sweeps += 1
-            more = ops.update(frontier, visited, levels, float(sweeps), anyflag)
+            more, fv = ops.update(frontier, visited, levels, float(sweeps), anyflag)
+            sparse = fv * 16 < self.n  # every rank sees the same gathered frontier: same choice
             if sweeps > self.n:
                 raise RuntimeError("BFS failed to drain its frontier")
             if not more:

@@ -52,7 +52,7 @@ class OracleBfsOps:
         self._words(visited)[src // self.d] |= 1 << (src % self.d)
         self._words(frontier)[src // self.d] |= 1 << (src % self.d)
 
-    def sweep(self, frontier, visited, nxt):
+    def sweep(self, frontier, visited, nxt, sparse=False):
         fw, vw, out = self._words(frontier), self._words(visited), self._words(nxt)
         out[:] = 0
         ntr_global = orc.tile_rows(self.n, self.d)
@@ -82,7 +82,7 @@ class OracleBfsOps:
                 for k in range(self.d):
                     if (w >> k) & 1:
                         lv[i * self.d + k] = level
-        return found
+        return found, int(sum(bin(int(w)).count("1") for w in fw[: orc.tile_rows(self.n, self.d)]))
 
     def levels_to_host(self, levels):
         return levels.numpy().copy()
