@@ -166,6 +166,16 @@ int b2sr_sssp(const b2sr_matrix *at, uint32_t src, double *d_dist, int64_t *iter
 int b2sr_pagerank(const b2sr_matrix *a, const double *d_out_degree, double alpha, double epsilon,
                   int64_t max_iter, double *d_rank, int64_t *iterations, int *converged,
                   int64_t *bad_col, void *stream);
+/* Pieces of the drivers for the row-partitioned loops (dist.py), each the
+ * exact arithmetic of the single-GPU driver:
+ *   b2sr_pr_step      rank' = teleport + alpha*g (no FMA), diff = |rank'-rank|,
+ *                     xs = rank'/deg (0 where deg == 0) -- algorithms.py:150-157
+ *   b2sr_pairwise_sum numpy's pairwise float64 sum (the PR delta, algorithms.py:157)
+ *   b2sr_min_relax    dist = np.minimum(dist, y), *changed |= any change (algorithms.py:119-122) */
+int b2sr_pr_step(uint32_t count, double teleport, double alpha, const double *d_g, const double *d_deg, double *d_rank,
+                 double *d_xs, double *d_diff, void *stream);
+int b2sr_pairwise_sum(const double *d_a, uint64_t n, double *d_out, void *stream);
+int b2sr_min_relax(uint64_t count, double *d_dist, const double *d_y, int *d_changed, void *stream);
 /* connected_components (algorithms.py:166-196) on a symmetric matrix. */
 int b2sr_cc(const b2sr_matrix *a, double *d_labels, int64_t *iterations, void *stream);
 /* triangle_count core (algorithms.py:212-214): L = strict lower triangle in

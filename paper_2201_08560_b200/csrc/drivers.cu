@@ -1235,6 +1235,34 @@ int b2sr_sssp(const b2sr_matrix *at, uint32_t src, double *d_dist, int64_t *iter
     API_END
 }
 
+int b2sr_pr_step(uint32_t count, double teleport, double alpha, const double *d_g, const double *d_deg, double *d_rank,
+                 double *d_xs, double *d_diff, void *stream) {
+    API_BEGIN
+    if (count) LAUNCH(k_pr_update, grid_for(count), 256, 0, (cudaStream_t)stream, count, teleport, alpha, d_g, d_deg,
+                      d_rank, d_xs, d_diff);
+    API_END
+}
+
+int b2sr_pairwise_sum(const double *d_a, uint64_t n, double *d_out, void *stream) {
+    API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!n) {
+        CK(cudaMemsetAsync(d_out, 0, 8, s));
+    } else {
+        PairwiseSum pw(n, s);
+        pw.run(d_a, s);
+        CK(cudaMemcpyAsync(d_out, pw.out.p, 8, cudaMemcpyDeviceToDevice, s));
+        CK(cudaStreamSynchronize(s));  // pw's buffers die at scope exit
+    }
+    API_END
+}
+
+int b2sr_min_relax(uint64_t count, double *d_dist, const double *d_y, int *d_changed, void *stream) {
+    API_BEGIN
+    if (count) LAUNCH(k_relax, grid_for(count), 256, 0, (cudaStream_t)stream, (size_t)count, d_dist, d_y, d_changed);
+    API_END
+}
+
 int b2sr_pagerank(const b2sr_matrix *a, const double *d_out_degree, double alpha, double epsilon, int64_t max_iter,
                   double *d_rank, int64_t *iterations, int *converged, int64_t *bad_col, void *stream) {
     API_BEGIN

@@ -169,6 +169,94 @@ def block_from_host(n: int, dim: int, begin: int, end: int, host) -> _Handle:
                        tiles.ctypes.data, len(tci), dev.stream())
 
 
+# ---------------------------------------------------------------- float-gather drivers
+def _slices(n: int, dim: int, world: int, rank: int):
+    """(vertex begin, valid count, padded slice length) of this rank's rows."""
+    ntr = -(-n // dim)
+    b, e = partition(ntr, world, dim)[rank]
+    per = block_rows(ntr, world, dim) * dim
+    v0 = b * dim
+    return b, e, v0, max(0, min(e * dim, n) - v0), per
+
+
+def _bff_block(blk: _Handle, x, ring: int, inc: float, y):
+    bad = ctypes.c_int64(-1)
+    _capi.call("b2sr_bmv_bff", blk.ptr, dev.ptr(x), ring, float(inc), None, None, dev.ptr(y),
+               ctypes.addressof(bad), dev.stream())
+
+
+def distributed_pagerank(at: B2srMatrix, out_degree, dist, alpha: float = 0.85, epsilon: float = 1e-9,
+                         max_iter: int = 10):
+    """PageRank (algorithms.py:127-163) with the tile rows of ``at`` (the
+    transposed adjacency) partitioned over ranks.  Per sweep: the rank's rows
+    of g = bff(at, rank/deg) and of the update, then one all-gather of the new
+    rank/deg slices and one of the |delta| slices; every rank evaluates numpy's
+    pairwise delta over the full vector, so the bits and the iteration count
+    are those of the single-GPU driver.  Returns (rank, iterations, converged)."""
+    t = dev.torch()
+    rank, world = dist.get_rank(), dist.get_world_size()
+    n, d = at.n, at.dim
+    b, e, v0, cnt, per = _slices(n, d, world, rank)
+    blk = _new_handle("b2sr_row_block", at.handle().ptr, b, e, dev.stream())
+    full = per * world
+    deg = t.zeros(full, dtype=t.float64, device=dev.device())
+    deg[:n] = t.as_tensor(np.asarray(out_degree, dtype=np.float64).reshape(-1), device=dev.device())
+    r = t.full((full,), 1.0 / n, dtype=t.float64, device=dev.device())
+    r[n:] = 0.0
+    xs = t.where(deg == 0, t.zeros_like(r), r / t.where(deg == 0, t.ones_like(deg), deg))
+    diff = t.zeros(full, dtype=t.float64, device=dev.device())
+    g = t.zeros(per + 16, dtype=t.float64, device=dev.device())
+    r_loc, xs_loc, diff_loc = (t.zeros(per, dtype=t.float64, device=dev.device()) for _ in range(3))
+    out = t.zeros(2, dtype=t.float64, device=dev.device())
+    teleport = (1.0 - alpha) / n
+    it, conv = 0, False
+    while it < max_iter:
+        _bff_block(blk, xs, 1, 0.0, g)  # B2SR_RING_ARITHMETIC
+        r_loc[:cnt].copy_(r[v0:v0 + cnt])
+        _capi.call("b2sr_pr_step", cnt, teleport, float(alpha), dev.ptr(g), dev.ptr(deg[v0:]), dev.ptr(r_loc),
+                   dev.ptr(xs_loc), dev.ptr(diff_loc), dev.stream())
+        all_gather_words(dist, xs.view(t.uint8), xs_loc.view(t.uint8), world)
+        all_gather_words(dist, diff.view(t.uint8), diff_loc.view(t.uint8), world)
+        all_gather_words(dist, r.view(t.uint8), r_loc.view(t.uint8), world)
+        _capi.call("b2sr_pairwise_sum", dev.ptr(diff), n, dev.ptr(out), dev.stream())
+        it += 1
+        if float(out[0].item()) < epsilon:
+            conv = True
+            break
+    return dev.to_host(r, np.float64, n), it, conv
+
+
+def distributed_sssp(at: B2srMatrix, src: int, dist):
+    """Unit-weight SSSP relaxation (algorithms.py:113-124) on ``at`` =
+    transpose(drop_diagonal(a)), tile rows partitioned over ranks: per round
+    the rank's rows of bff(at, dist, min-plus(1)) are relaxed into its slice,
+    the slices are all-gathered and an all-reduce of the changed flags ends
+    the loop exactly where the single-GPU driver stops.  Returns (dist, rounds)."""
+    t = dev.torch()
+    rank, world = dist.get_rank(), dist.get_world_size()
+    n, d = at.n, at.dim
+    b, e, v0, cnt, per = _slices(n, d, world, rank)
+    blk = _new_handle("b2sr_row_block", at.handle().ptr, b, e, dev.stream())
+    full = per * world
+    dd = t.full((full,), float("inf"), dtype=t.float64, device=dev.device())
+    dd[src] = 0.0
+    y = t.zeros(per + 16, dtype=t.float64, device=dev.device())
+    loc = t.zeros(per, dtype=t.float64, device=dev.device())
+    flag = t.zeros(4, dtype=t.int32, device=dev.device())
+    rounds = 0
+    for _ in range(n - 1):
+        _bff_block(blk, dd, 2, 1.0, y)  # B2SR_RING_MINPLUS, edge increment 1
+        loc.copy_(dd[v0:v0 + per])
+        flag.zero_()
+        _capi.call("b2sr_min_relax", cnt, dev.ptr(loc), dev.ptr(y), dev.ptr(flag), dev.stream())
+        all_gather_words(dist, dd.view(t.uint8), loc.view(t.uint8), world)
+        dist.all_reduce(flag)
+        rounds += 1
+        if not int(flag[0].item()):
+            break
+    return dev.to_host(dd, np.float64, n), rounds
+
+
 def distributed_triangle_count(lower: B2srMatrix, dist) -> int:
     """TC with the mask tile rows of L partitioned over ranks; L replicated."""
     rank, world = dist.get_rank(), dist.get_world_size()

@@ -143,3 +143,57 @@ def test_row_partitioned_bfs_two_ranks_one_gpu(d):
         p.join(timeout=60)
     assert got[0] == lv_ref.tobytes() and got[1] == it_ref
     assert got[2] == lv_ref.tobytes() and got[3] == it_ref
+
+
+def _dist_float_worker(rank, world, port, scale, d, src, q):
+    import os
+
+    import torch
+    import torch.distributed as tdist
+
+    from paper_2201_08560_b200 import dist as bdist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    csr = rmat.rmat_csr(scale, 16, seed=7)
+    m = b2.csr_to_b2sr(csr, d)
+    deg = np.diff(csr.row_ptr.astype(np.int64)).astype(np.float64)
+    pr, pit, pconv = bdist.distributed_pagerank(b2.b2sr_transpose(m), deg, tdist)
+    ss, sit = bdist.distributed_sssp(b2.b2sr_transpose(b2.formats.drop_diagonal(m)), src, tdist)
+    if rank == 0:
+        q.put((pr.tobytes(), pit, pconv, ss.tobytes(), sit))
+    tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("d", [4, 8])
+def test_row_partitioned_pagerank_sssp_two_ranks_one_gpu(d, monkeypatch):
+    """dist.py float-gather drivers with the real kernels (2 ranks sharing
+    cuda:0 over gloo, small segmented-plan threshold so both gather paths run):
+    PageRank and SSSP give the single-GPU drivers' bits and iteration counts."""
+    import socket
+
+    import torch.multiprocessing as mp
+
+    monkeypatch.setenv("B2SR_VLONG_TILES", "24")
+    scale = 13
+    csr = rmat.rmat_csr(scale, 16, seed=7)
+    m = b2.csr_to_b2sr(csr, d)
+    deg = np.diff(csr.row_ptr.astype(np.int64)).astype(np.float64)
+    src = int(np.argmax(deg))
+    want_pr = b2.pagerank(b2.b2sr_transpose(m), deg)
+    want_ss = b2.sssp(m, src)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_dist_float_worker, args=(r, 2, port, scale, d, src, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    got = q.get(timeout=120)
+    for p in ps:
+        p.join(timeout=60)
+    assert got[0] == want_pr.per_vertex.tobytes() and got[1] == want_pr.iterations and got[2] == want_pr.converged
+    assert got[3] == want_ss.per_vertex.tobytes() and got[4] == want_ss.iterations
