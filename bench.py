@@ -457,26 +457,48 @@ def bench_drivers(args, b2, rmat, torch, ev):
 
 
 def bench_tc(args, b2, rmat, torch, ev):
+    """BASELINE configs[2]: triangle counting on R-MAT scale 20 through the
+    masked bin-SpGEMM.  Besides the end-to-end count time, the SpGEMM kernel
+    is timed alone (CUDA events on its stream) and its AND+POPC work W is
+    counted, for W/t against the measured AND+POPC peak."""
+    from paper_2201_08560_b200 import _capi
+
     csr = rmat.rmat_csr(args.tc_scale, args.edgefactor, seed=args.seed)
     out = {}
+    try:
+        popc_peak = json.loads((ROOT / "profiles" / "r01_popc_peak.json").read_text())["and_popc_units_per_s"]
+    except Exception:
+        popc_peak = 148 * 16 * 1.965e9
     dag = b2.algorithms._degree_oriented(csr)  # what triangle_count() feeds the masked SpGEMM
     for d in (4, 8):
         lo = b2.csr_to_b2sr(dag, d)
+        h = lo.handle()
+        cnt, work, kms_ = ctypes.c_int64(), ctypes.c_uint64(), ctypes.c_float()
+        _capi.call("b2sr_tc_work", h.ptr, ctypes.addressof(cnt), ctypes.addressof(work), 0)
         b2.algorithms._tc_count(lo)  # warm
-        ts, cnt = [], 0
+        ts, ks = [], []
+        _capi.call("b2sr_set_kernel_timing", 1)
         for _ in range(3):
             e0, e1 = ev(), ev()
             e0.record()
-            cnt = b2.algorithms._tc_count(lo)
+            c = b2.algorithms._tc_count(lo)
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1))
-        ms = float(np.median(ts))
-        out[str(d)] = {"triangles": int(cnt), "ms": round(ms, 3),
-                       "edges_per_s": round((csr.nnz // 2) / (ms / 1e3), 1), "lower_tiles": int(lo.num_tiles)}
+            _capi.call("b2sr_last_kernel_ms", ctypes.addressof(kms_))
+            ks.append(kms_.value)
+        _capi.call("b2sr_set_kernel_timing", 0)
+        ms, kms = float(np.median(ts)), float(np.median(ks))
+        assert c == cnt.value
+        out[str(d)] = {"triangles": int(c), "ms": round(ms, 3), "edges_per_s": round((csr.nnz // 2) / (ms / 1e3), 1),
+                       "lower_tiles": int(lo.num_tiles), "spgemm_kernel_ms": round(kms, 3),
+                       "work_units": int(work.value), "units_per_s": round(work.value / (kms / 1e3), 1),
+                       "popc_peak_units_per_s": popc_peak,
+                       "popc_frac": round(work.value / (kms / 1e3) / popc_peak, 4)}
     return {"scale": args.tc_scale, "nnz": int(csr.nnz), "by_tile_dim": out,
             "kernel": "k_bmm_masked_items (AND+POPC): sum over the degree-oriented DAG L of (L L^T) "
-                      "(= triangles; the reference uses the ID-ordered lower triangle)"}
+                      "(= triangles; the reference uses the ID-ordered lower triangle)",
+            "note": "work_units = AND+POPC units W; the kernel is bound by intersection search, not POPC"}
 
 
 def cpu_baseline(csr, d, root):

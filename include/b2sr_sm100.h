@@ -181,6 +181,9 @@ int b2sr_cc(const b2sr_matrix *a, double *d_labels, int64_t *iterations, void *s
 /* triangle_count core (algorithms.py:212-214): L = strict lower triangle in
  * B2SR; count = bmm_masked(L, transpose(L), L). */
 int b2sr_tc(const b2sr_matrix *lower, int64_t *count, void *stream);
+/* The same count plus W, the AND+POPC units the masked SpGEMM executed
+ * (SURVEY.md §8d TC roofline; counting costs a little time). */
+int b2sr_tc_work(const b2sr_matrix *lower, int64_t *count, uint64_t *work, void *stream);
 
 /* ---- CSR utilities on the device (formats.py:96-225, algorithms.py:218) - */
 /* Strict lower triangle of a device CSR (two phases like b2sr_to_csr). */

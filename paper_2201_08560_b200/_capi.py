@@ -54,6 +54,7 @@ SIGNATURES = {
     "b2sr_bfs_init": [u32, u32, u32, P, P, P, P],
     "b2sr_bfs_sweep": [P, P, P, P, P],
     "b2sr_bfs_update": [u32, u32, P, P, P, f64, P, P],
+    "b2sr_tc_work": [P, P, P, P],
     "b2sr_pr_step": [u32, f64, f64, P, P, P, P, P, P],
     "b2sr_pairwise_sum": [P, u64, P, P],
     "b2sr_min_relax": [u64, P, P, P, P],
