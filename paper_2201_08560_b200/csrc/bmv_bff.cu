@@ -146,7 +146,7 @@ __device__ __forceinline__ double bff_fold(const double *__restrict__ x, const B
 }
 
 template <int D, int RING>
-__global__ void __launch_bounds__(BFF_THREADS) k_bff_rows(uint32_t n_rows, const uint32_t *__restrict__ rows, uint32_t n,
+__global__ void __launch_bounds__(BFF_THREADS, 4) k_bff_rows(uint32_t n_rows, const uint32_t *__restrict__ rows, uint32_t n,
                                                          const uint32_t *__restrict__ trp, const uint32_t *__restrict__ tci,
                                                          const uint8_t *__restrict__ tiles, const double *__restrict__ x,
                                                          double inc, const void *__restrict__ keep,
@@ -160,22 +160,18 @@ __global__ void __launch_bounds__(BFF_THREADS) k_bff_rows(uint32_t n_rows, const
         const uint32_t t0 = trp[I], t1 = trp[I + 1];
         double acc = ident;
         uint32_t b = t0 & ~3u;
-        BffStep s0, s1, s2;
+        BffStep s0, s1;
         bff_load<D>(tiles, tci, b, t0, t1, r, s0);
-        bff_load<D>(tiles, tci, b + 4, t0, t1, r, s1);
         bff_gather<D>(x, s0);
-        for (; b < t1; b += 12) {
-            bff_load<D>(tiles, tci, b + 8, t0, t1, r, s2);
-            bff_gather<D>(x, s1);
+        for (; b < t1; b += 8) {
+            bff_load<D>(tiles, tci, b + 4, t0, t1, r, s1);
             acc = bff_fold<D, RING>(x, s0, acc, inc);
             if (b + 4 >= t1) break;
-            bff_load<D>(tiles, tci, b + 12, t0, t1, r, s0);
-            bff_gather<D>(x, s2);
+            bff_gather<D>(x, s1);
+            bff_load<D>(tiles, tci, b + 8, t0, t1, r, s0);
             acc = bff_fold<D, RING>(x, s1, acc, inc);
             if (b + 8 >= t1) break;
-            bff_load<D>(tiles, tci, b + 16, t0, t1, r, s1);
             bff_gather<D>(x, s0);
-            acc = bff_fold<D, RING>(x, s2, acc, inc);
         }
         const uint32_t grow = row0 + I;
         const uint64_t vrow = (uint64_t)grow * D + r;
