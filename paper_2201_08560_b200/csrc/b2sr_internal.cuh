@@ -177,6 +177,7 @@ void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const v
                   cudaStream_t s, const std::function<void(cudaStream_t)> &overlap = {});
 // hot.cu: the S most referenced tile columns' x words live in shared memory
 constexpr uint32_t HOT_SMEM_BYTES = 196608;
+constexpr bool HOT_NIBBLES = true;   // d=4: pack two 4-bit x words per byte (2x the slots, more ALU per gather)
 struct HotView {
     uint32_t S;               // slots; tci2 values < S are slots, others S + column
     const uint32_t *cols;     // slot -> tile column (null: identity)

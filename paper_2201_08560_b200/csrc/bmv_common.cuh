@@ -104,7 +104,7 @@ struct XHot {
     __device__ __forceinline__ uint32_t operator()(uint32_t c) const {
         uint32_t v;
         if (c < S) {
-            if constexpr (D == 4) {  // two 4-bit words per byte (hot.cu packs them)
+            if constexpr (D == 4 && HOT_NIBBLES) {  // two 4-bit words per byte (hot.cu packs them)
                 asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(sbase + (c >> 1)));
                 return (v >> ((c & 1u) * 4u)) & 0xFu;
             } else if constexpr (sizeof(typename WordT<D>::T) == 1) {

@@ -911,7 +911,7 @@ __global__ void k_bfs_prep(BfsCtl *__restrict__ c, uint32_t ntr, const uint32_t 
         return;
     }
     const uint8_t *fr = static_cast<const uint8_t *>(frontier);
-    if constexpr (D == 4) {
+    if constexpr (D == 4 && HOT_NIBBLES) {
         for (uint32_t i = tid; i < (S + 1) / 2; i += stride) {
             uint32_t a = 2 * i, b = 2 * i + 1;
             uint32_t lo = fr[cols ? cols[a] : a] & 0xFu, hi = b < S ? (fr[cols ? cols[b] : b] & 0xFu) : 0u;

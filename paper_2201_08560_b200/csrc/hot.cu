@@ -80,7 +80,7 @@ HotView hot_view(b2sr_matrix *m, cudaStream_t s) {
         const uint32_t wb = (uint32_t)word_bytes((int)m->dim);
         const char *e = getenv("B2SR_HOT_BYTES");     // parity tests force the remapped path on small graphs
         uint32_t budget = e ? (uint32_t)atoi(e) : HOT_SMEM_BYTES;
-        uint32_t cap = m->dim == 4 ? budget * 2 : budget / wb;  // d=4: two 4-bit words per byte
+        uint32_t cap = (m->dim == 4 && HOT_NIBBLES) ? budget * 2 : budget / wb;  // d=4: two 4-bit words per byte
         HotPlan *h = new HotPlan();
         try {
             if (nc <= cap) {
@@ -135,7 +135,7 @@ __global__ void k_hot_fill4(uint32_t S, const uint32_t *__restrict__ cols, const
 }
 
 static size_t hot_used_bytes(const HotView &hv, int dim) {
-    return dim == 4 ? ((size_t)hv.S + 1) / 2 : (size_t)hv.S * word_bytes(dim);
+    return (dim == 4 && HOT_NIBBLES) ? ((size_t)hv.S + 1) / 2 : (size_t)hv.S * word_bytes(dim);
 }
 
 size_t hot_fill_bytes(const HotView &hv, int dim) { return (hot_used_bytes(hv, dim) + 15) / 16 * 16; }
@@ -145,7 +145,7 @@ void hot_fill(const HotView &hv, int dim, const void *x, void *hx, cudaStream_t 
     size_t used = hot_used_bytes(hv, dim);
     if (b > used) CK(cudaMemsetAsync(static_cast<char *>(hx) + used, 0, b - used, s));
     unsigned g = hgrid(hv.S);
-    if (dim == 4) {
+    if (dim == 4 && HOT_NIBBLES) {
         LAUNCH(k_hot_fill4, g, 256, 0, s, hv.S, hv.cols, (const uint8_t *)x, (uint8_t *)hx);
         return;
     }
