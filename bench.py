@@ -608,6 +608,27 @@ def run_dist(args, rank, world, local_rank):
     tdist.all_reduce(e2e_ms, op=tdist.ReduceOp.MAX)
     e2e_ms = float(e2e_ms.item())
     h2d = int(sum(h[1].nbytes for h in host_blk)) * world
+    # TC with the mask rows of the degree-oriented DAG partitioned, one int64 all-reduce
+    tc = None
+    if not args.no_tc:
+        tscale = args.tc_scale + max(0, int(round(np.log2(world))))
+        tcsr = rmat.rmat_csr(tscale, args.edgefactor, seed=args.seed)
+        lo = b2.csr_to_b2sr(b2.algorithms._degree_oriented(tcsr), d)
+        bdist.distributed_triangle_count(lo, tdist)  # warm
+        barrier()
+        t0_, t1_ = ev(), ev()
+        t0_.record()
+        tri = bdist.distributed_triangle_count(lo, tdist)
+        t1_.record()
+        barrier()
+        tms = torch.tensor([t0_.elapsed_time(t1_)], device="cuda")
+        tdist.all_reduce(tms, op=tdist.ReduceOp.MAX)
+        tms = float(tms.item())
+        tc = {"scale": tscale, "nnz": int(tcsr.nnz), "triangles": int(tri), "ms": round(tms, 3),
+              "edges_per_s": round((tcsr.nnz // 2) / (tms / 1e3), 1),
+              "parallelism": f"mask tile rows x{world}, L replicated, int64 all-reduce"}
+        del lo, tcsr
+        torch.cuda.empty_cache()
     roofline = None
     if rank == 0:  # K4 masked sweep over this rank's block (x, keep: global 50 % random)
         pk, pk_kind = peaks()
@@ -641,7 +662,7 @@ def run_dist(args, rank, world, local_rank):
                         "includes": "H2D of every rank's B2SR row block from pinned memory, distributed BFS, "
                                     "D2H of the levels on rank 0"},
                 "roofline": roofline, "gpu_launches": int(launches), "bfs_sweeps_per_root": iters[:4],
-                "clocks": clk.summary(), "graph_gen_s": round(gen_s, 3)}
+                "clocks": clk.summary(), "tc": tc, "graph_gen_s": round(gen_s, 3)}
         print(json.dumps(line), flush=True)
     tdist.destroy_process_group()
 
