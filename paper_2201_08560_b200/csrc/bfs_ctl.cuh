@@ -34,6 +34,13 @@ struct BfsCtl {
     BfsCounters cnt;       // written by the level's update, consumed by the next plan
 };
 
+// One level's outcome as the host sees it (mapped host memory ring).
+struct BfsSnap {
+    uint32_t level;  // written last: the slot is valid for this level
+    int done;
+    long long sweeps;
+};
+
 // Top-down sweep over the non-transposed matrix a (bmv_stream.cu): OR of the
 // frontier bit-rows of every listed tile-row chunk scattered into next.
 // Raw: already-visited vertices are masked by the update kernel.

@@ -17,6 +17,7 @@
 #include <cmath>
 #include <map>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "bfs_ctl.cuh"
@@ -794,7 +795,8 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
                                 double *__restrict__ levels, double level, const uint32_t *__restrict__ trp_a,
                                 const uint32_t *__restrict__ trp_at, const uint4 *__restrict__ live_at,
                                 BfsCtl *__restrict__ ctl, uint4 *__restrict__ zero_buf, int mask, double alpha,
-                                unsigned long long tiles_at, int has_a, int head_ok) {
+                                unsigned long long tiles_at, int has_a, int head_ok, BfsSnap *__restrict__ snap,
+                                uint32_t level_no) {
     using W = typename WordT<D>::T;
     if (ctl->mode == BFS_NONE && mask) return;  // BFS already over
     constexpr int WPC = 16 / sizeof(W);
@@ -871,6 +873,14 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
             cv->cnt.frontier_tiles = 0;
             cv->cnt.removed_tiles = 0;
             cv->cnt.frontier_vertices = 0;
+        }
+        if (snap) {  // the level's outcome, straight into mapped host memory
+            volatile BfsSnap *hs = snap + level_no % 8;
+            hs->done = cv->done;
+            hs->sweeps = cv->sweeps;
+            __threadfence_system();
+            hs->level = level_no;
+            __threadfence_system();
         }
     }
 }
@@ -992,6 +1002,34 @@ __global__ void k_bfs_dense_list(BfsCtl *__restrict__ c, uint32_t n_loads, const
     }
 }
 
+// Mapped (zero-copy) host ring the update kernel's last block writes each
+// level's outcome into: the host learns that the BFS is over without a copy
+// or a sync in the stream (one per host thread and device).
+struct BfsSnapshots {
+    static constexpr uint32_t N = 8;
+    BfsSnap *host = nullptr, *dev = nullptr;
+    BfsSnapshots() {
+        CK(cudaHostAlloc(&host, N * sizeof(BfsSnap), cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dev), host, 0));
+        reset();
+    }
+    void reset() {
+        for (uint32_t i = 0; i < N; i++) host[i].level = 0xFFFFFFFFu;
+    }
+    const volatile BfsSnap *slot(uint32_t level) const { return host + level % N; }
+};
+constexpr uint32_t LOOKAHEAD = 1;  // levels enqueued beyond the one whose end is being checked
+
+static BfsSnapshots &bfs_snapshots() {
+    // per host thread (re-entrant C ABI) and per device (the events belong to one)
+    static thread_local BfsSnapshots *snaps[16] = {};
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    dev &= 15;
+    if (!snaps[dev]) snaps[dev] = new BfsSnapshots();
+    return *snaps[dev];
+}
+
 template <int D>
 static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, double *d_levels, int64_t *iterations,
                        cudaStream_t s) {
@@ -1026,12 +1064,16 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     LAUNCH(k_bfs_ctl_init, 1, 1, 0, s, ctl.p, (unsigned long long)at->live_tiles);
     const unsigned gu = grid_for(ntr);
     const uint32_t *ta = a ? a->trp : nullptr;
+    BfsSnapshots &snaps = bfs_snapshots();
+    snaps.reset();
     // level 0 = {src}: visited, levels, counters, the push list of level 1 and its plan
     LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)fb.p, (uint4 *)visited.p, d_levels, 0.0, ta, at->trp,
-           (const uint4 *)at->live, ctl.p, nullptr, 0, alpha, (unsigned long long)at->num_tiles, a ? 1 : 0, head);
+           (const uint4 *)at->live, ctl.p, nullptr, 0, alpha, (unsigned long long)at->num_tiles, a ? 1 : 0, head,
+           snaps.dev, 0u);
     void *frontier = fb.p, *next = fa.p;
     const unsigned gp = (unsigned)num_sms() * 8;
-    BfsCtl h{};
+    int done = 0;
+    long long sweeps = 0;
     for (uint32_t L = 1;; L++) {
         LAUNCH(k_bfs_prep<D>, gp, 256, 0, s, ctl.p, ntr, ta, list.p, hv.S, hv.cols, frontier, hx.p, n_loads, desc,
                visited.p, at->live, alist.p);
@@ -1043,19 +1085,31 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
         launch_bfs_level(at, a, ctl.p, list.p, alist.p, hx.p, hb, frontier, next, s);
         LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L, ta,
                at->trp, (const uint4 *)at->live, ctl.p, (uint4 *)frontier, 1, alpha,
-               (unsigned long long)at->num_tiles, a ? 1 : 0, head);
+               (unsigned long long)at->num_tiles, a ? 1 : 0, head, snaps.dev, L);
         std::swap(frontier, next);
-        if (trace || (L >= 4 && L % 2 == 0)) {  // poll for the end every other level
-            CK(cudaMemcpyAsync(&h, ctl.p, sizeof(BfsCtl), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            if (trace)
-                fprintf(stderr, "[b2sr bfs] after level %u: next mode %d unvisited_tiles=%llu done=%d\n", L, h.mode,
-                        h.unvisited, h.done);
-            if (h.done) break;
+        // the host checks level L-LOOKAHEAD's outcome while levels up to L are
+        // already enqueued (levels past the end are gated no-ops): no poll
+        // ever drains the queue
+        if (trace || L > LOOKAHEAD) {
+            const uint32_t Lc = trace ? L : L - LOOKAHEAD;
+            const volatile BfsSnap *sn = snaps.slot(Lc);
+            while (sn->level != Lc) {
+                const cudaError_t q = cudaStreamQuery(s);
+                if (q != cudaErrorNotReady && sn->level != Lc) {
+                    CK(q);  // a failed kernel surfaces here
+                    B2SR_THROW(B2SR_ECUDA, "BFS level %u finished without its outcome", Lc);
+                }
+                std::this_thread::yield();
+            }
+            done = sn->done;
+            sweeps = sn->sweeps;
+            if (trace) fprintf(stderr, "[b2sr bfs] after level %u: done=%d sweeps=%lld\n", Lc, done, sweeps);
+            if (done) break;
         }
-        if (L > n + 2) B2SR_THROW(B2SR_ENOCONV, "BFS failed to drain its frontier");
+        if (L > n + 2 + LOOKAHEAD) B2SR_THROW(B2SR_ENOCONV, "BFS failed to drain its frontier");
     }
-    *iterations = h.sweeps;
+    CK(cudaStreamSynchronize(s));  // the enqueued no-op levels are done
+    *iterations = sweeps;
 }
 
 static bool bfs_devctl_enabled(const b2sr_matrix *at) {
