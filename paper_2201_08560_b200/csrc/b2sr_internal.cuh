@@ -146,13 +146,8 @@ struct b2sr_matrix {
     // set bit), same layout as a BitVector; BFS never needs to wait for a
     // vertex without in-edges
     void *live = nullptr;
-    // cached column-strip blocked layout for bin-SpMV (bmv_blocked.cu)
-    void *plan = nullptr;
     uint64_t live_tiles = 0;          // tiles in rows with a live bit (set with `live`)
     uint32_t *item_ofs = nullptr;     // ntr+1: first work item of each tile row (with `items`)
-    uint32_t *long_rows = nullptr;    // tile rows handled by the CTA-per-row float gather
-    uint32_t n_long = 0;
-    uint32_t long_lo = 0;             // rows longer than this leave the group-per-row gather
     void *vlong = nullptr;            // segmented plan for the very longest rows (bmv_vlong.cu)
     void *hot = nullptr;              // hot-column x cache plan (hot.cu)
     void *stream = nullptr;           // flat tile-stream row hints (bmv_stream.cu)
@@ -170,7 +165,6 @@ void free_matrix(b2sr_matrix *m);
 void ensure_items(b2sr_matrix *m, cudaStream_t s);  // bin-SpMV work partition
 int num_sms();
 void launch_row_ids(const b2sr_matrix *m, uint32_t *rowid, cudaStream_t s);  // rowid[t] = tile row of t
-void free_plan(void *plan);
 void free_vlong(void *plan);
 void *build_vlong(b2sr_matrix *m, uint32_t thresh, cudaStream_t s);
 void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
@@ -202,10 +196,6 @@ void free_bff(void *plan);
 const uint4 *stream_desc(b2sr_matrix *m, cudaStream_t s, uint32_t *n_loads);  // per-load row descriptors
 void launch_stream_sweep(b2sr_matrix *m, const uint32_t *list, const uint32_t *list_n, const void *hx, size_t hb,
                          const void *x, void *y, const int *gate, int want, cudaStream_t s, bool lazy = false);
-// blocked bin-SpMV: mode 0 = masked bbb, 1 = BFS pull; false if not applicable
-bool launch_blocked(b2sr_matrix *m, int mode, const void *x, const void *keep, void *y, cudaStream_t s);
-// B2SR_BLOCKED=1 selects the column-strip blocked kernels (A/B measurements)
-bool blocked_enabled();
 
 // scan.cu
 // out[i] = sum_{j<i} in[j] for i in [0, n]; out has n+1 entries (out[n] = total).

@@ -17,10 +17,7 @@ struct BfsCounters {
 };
 
 // Direction of one level, chosen on the device from the previous level's counters.
-// BFS_PULL_DENSE: a pull over a dense frontier -- the first tiles of every
-// unvisited row are checked first (most rows find a parent there), then the
-// listed loads of the rows still missing one are streamed like BFS_PULL_ACTIVE.
-enum BfsMode : int { BFS_NONE = 0, BFS_PUSH = 1, BFS_PULL = 2, BFS_PULL_ACTIVE = 3, BFS_PULL_DENSE = 4 };
+enum BfsMode : int { BFS_NONE = 0, BFS_PUSH = 1, BFS_PULL = 2, BFS_PULL_ACTIVE = 3 };
 
 struct BfsCtl {
     int mode;

@@ -75,67 +75,6 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t *__restrict__
     return lo;
 }
 
-template <int D>
-__global__ void __launch_bounds__(256) k_bmm_masked(uint64_t TM, const uint32_t *__restrict__ m_rowid,
-                                                    const uint32_t *__restrict__ m_tci,
-                                                    const typename WordT<D>::T *__restrict__ m_tiles,
-                                                    const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ a_tci,
-                                                    const typename WordT<D>::T *__restrict__ a_tiles,
-                                                    const uint32_t *__restrict__ b_trp, const uint32_t *__restrict__ b_tci,
-                                                    const typename WordT<D>::T *__restrict__ b_tiles,
-                                                    uint32_t m_row0, unsigned long long *__restrict__ out) {
-    const uint32_t lane = lane_id();
-    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    unsigned long long acc = 0;
-    for (uint64_t mt = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; mt < TM; mt += warps) {
-        uint32_t I = m_rowid[mt] + m_row0, J = m_tci[mt];
-        uint32_t mword = lane < (uint32_t)D ? (uint32_t)m_tiles[mt * D + lane] : 0u;
-        uint32_t rows_used = __ballot_sync(0xffffffffu, mword != 0);  // bit r: mask row r non-empty
-        uint32_t a0 = a_trp[I], a1 = a_trp[I + 1], b0 = b_trp[J], b1 = b_trp[J + 1];
-        if (a0 == a1 || b0 == b1 || rows_used == 0) continue;
-        // iterate the shorter tile row, search the longer one
-        bool a_short = (a1 - a0) <= (b1 - b0);
-        uint32_t s0 = a_short ? a0 : b0, s1 = a_short ? a1 : b1;
-        uint32_t l0 = a_short ? b0 : a0, l1 = a_short ? b1 : a1;
-        const uint32_t *stci = a_short ? a_tci : b_tci;
-        const uint32_t *ltci = a_short ? b_tci : a_tci;
-        for (uint32_t base = s0; base < s1; base += 32) {
-            uint32_t si = base + lane;
-            uint32_t ta = 0, tb = 0;
-            bool hit = false;
-            if (si < s1) {
-                uint32_t K = __ldg(stci + si);
-                uint32_t li = lower_bound_u32(ltci, l0, l1, K);
-                if (li < l1 && __ldg(ltci + li) == K) {
-                    hit = true;
-                    ta = a_short ? si : li;
-                    tb = a_short ? li : si;
-                }
-            }
-            uint32_t hits = __ballot_sync(0xffffffffu, hit);
-            if (!hits) continue;
-            uint32_t ru = rows_used;
-            while (ru) {  // warp-uniform loop over non-empty mask rows
-                int r = __ffs(ru) - 1;
-                ru &= ru - 1;
-                uint32_t mw = __shfl_sync(0xffffffffu, mword, r);
-                if (hit) {
-                    uint32_t aw = a_tiles[(size_t)ta * D + r];
-                    if (aw) {
-                        while (mw) {
-                            int c = __ffs(mw) - 1;
-                            mw &= mw - 1;
-                            acc += __popc(aw & (uint32_t)b_tiles[(size_t)tb * D + c]);
-                        }
-                    }
-                }
-            }
-        }
-    }
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0 && acc) atomicAdd(out, acc);
-}
-
 // ------------------------------------------------------------ chunked items
 // A mask tile whose two tile rows are both long (hub x hub) would pin one
 // warp for milliseconds; split every mask tile into chunks of TC_CHUNK
@@ -232,341 +171,10 @@ __global__ void __launch_bounds__(256) k_bmm_masked_items(uint64_t n_items, cons
     }
 }
 
-// ------------------------------------------------------------ register-table rows
-// Work unit = (mask tile row I, up to RT_UNIT of its mask tiles).  The warp
-// keeps A's tile row I (<= 32*RT_K columns) in registers, lane l holding
-// columns [l*k, l*k+k) (k = ceil(len/32)), and finds every column of Bt's row
-// J by a 5-step shuffle search over the lanes' first columns plus k shuffles --
-// no dependent memory round trips.  Longer A rows search global memory.
-constexpr uint32_t RT_UNIT = 64;
-constexpr int RT_K = 8;
-
-__global__ void k_rt_counts(uint32_t mntr, const uint32_t *__restrict__ mtrp, uint32_t *__restrict__ cnt) {
-    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < mntr; r += gridDim.x * blockDim.x)
-        cnt[r] = (mtrp[r + 1] - mtrp[r] + RT_UNIT - 1) / RT_UNIT;
-}
-
-__global__ void k_rt_fill(uint32_t mntr, const uint32_t *__restrict__ mtrp, const uint32_t *__restrict__ cnt,
-                          const uint64_t *__restrict__ ofs, uint4 *__restrict__ units) {
-    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < mntr; r += gridDim.x * blockDim.x) {
-        uint64_t o = ofs[r];
-        uint32_t m0 = mtrp[r], m1 = mtrp[r + 1];
-        for (uint32_t j = 0; j < cnt[r]; j++) units[o + j] = make_uint4(r, m0 + j * RT_UNIT, min(m1, m0 + (j + 1) * RT_UNIT), 0);
-    }
-}
-
-template <int D>
-__global__ void __launch_bounds__(256) k_bmm_rowtable(uint64_t n_units, const uint4 *__restrict__ units, uint32_t m_row0,
-                                                      const uint32_t *__restrict__ m_tci,
-                                                      const typename WordT<D>::T *__restrict__ m_tiles,
-                                                      const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ a_tci,
-                                                      const typename WordT<D>::T *__restrict__ a_tiles,
-                                                      const uint32_t *__restrict__ b_trp, const uint32_t *__restrict__ b_tci,
-                                                      const typename WordT<D>::T *__restrict__ b_tiles,
-                                                      unsigned long long *__restrict__ out,
-                                                      unsigned long long *__restrict__ work) {
-    const uint32_t lane = lane_id();
-    const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    unsigned long long acc = 0, units_done = 0;
-    for (uint64_t u = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n_units; u += warps) {
-        const uint4 un = units[u];
-        const uint32_t I = un.x + m_row0;
-        const uint32_t a0 = a_trp[I], a1 = a_trp[I + 1], la = a1 - a0;
-        if (!la) continue;
-        const bool table = la <= 32u * RT_K;
-        const uint32_t k = (la + 31) / 32;
-        uint32_t key[RT_K];
-#pragma unroll
-        for (int j = 0; j < RT_K; j++) {
-            uint32_t i = lane * k + j;
-            key[j] = (table && j < (int)k && i < la) ? __ldg(a_tci + a0 + i) : 0xFFFFFFFFu;
-        }
-        const uint32_t first = key[0];
-        // the unit's mask tiles, 32 at a time: column, Bt row range and mask
-        // words loaded by all lanes at once (no dependent round trips per tile)
-        for (uint32_t mb = un.y; mb < un.z; mb += 32) {
-        const uint32_t mi = mb + lane;
-        const bool mok = mi < un.z;
-        const uint32_t Jl = mok ? m_tci[mi] : 0u;
-        const uint32_t b0l = mok ? b_trp[Jl] : 0u, b1l = mok ? b_trp[Jl + 1] : 0u;
-        uint32_t mwl = 0, mwh = 0;  // d <= 8: the whole mask tile in one or two words
-        if constexpr (D == 4) mwl = mok ? reinterpret_cast<const uint32_t *>(m_tiles)[mi] : 0u;
-        if constexpr (D == 8) {
-            uint2 q = mok ? reinterpret_cast<const uint2 *>(m_tiles)[mi] : make_uint2(0, 0);
-            mwl = q.x;
-            mwh = q.y;
-        }
-        const uint32_t mcount = min(32u, un.z - mb);
-        for (uint32_t q = 0; q < mcount; q++) {
-            const uint32_t mt = mb + q;
-            uint32_t mword;
-            if constexpr (D == 4) {
-                const uint32_t w = __shfl_sync(0xffffffffu, mwl, q);  // every lane takes part
-                mword = lane < 4 ? (w >> (8 * lane)) & 0xFFu : 0u;
-            } else if constexpr (D == 8) {
-                uint32_t lo = __shfl_sync(0xffffffffu, mwl, q), hi = __shfl_sync(0xffffffffu, mwh, q);
-                mword = lane < 8 ? ((lane < 4 ? lo : hi) >> (8 * (lane & 3))) & 0xFFu : 0u;
-            } else {
-                mword = lane < (uint32_t)D ? (uint32_t)m_tiles[(size_t)mt * D + lane] : 0u;
-            }
-            const uint32_t rows_used = __ballot_sync(0xffffffffu, mword != 0);
-            const uint32_t b0 = __shfl_sync(0xffffffffu, b0l, q), b1 = __shfl_sync(0xffffffffu, b1l, q);
-            if (!rows_used || b0 == b1) continue;
-            for (uint32_t base = b0; base < b1; base += 32) {
-                const uint32_t bi = base + lane;
-                const uint32_t K = bi < b1 ? __ldg(b_tci + bi) : 0xFFFFFFFEu;
-                uint32_t ta = 0;
-                bool hit = false;
-                if (table) {
-                    // the last lane whose first column is <= K
-                    uint32_t c = 0;
-#pragma unroll
-                    for (int o = 16; o; o >>= 1) {
-                        uint32_t f = __shfl_sync(0xffffffffu, first, c + o);
-                        if (f <= K) c += o;
-                    }
-#pragma unroll
-                    for (int j = 0; j < RT_K; j++) {
-                        if (j >= (int)k) break;  // warp-uniform
-                        uint32_t v = __shfl_sync(0xffffffffu, key[j], c);
-                        if (v == K && bi < b1) {
-                            hit = true;
-                            ta = a0 + c * k + j;
-                        }
-                    }
-                } else if (bi < b1) {
-                    uint32_t li = lower_bound_u32(a_tci, a0, a1, K);
-                    if (li < a1 && __ldg(a_tci + li) == K) {
-                        hit = true;
-                        ta = li;
-                    }
-                }
-                if (!__ballot_sync(0xffffffffu, hit)) continue;
-                uint32_t ru = rows_used;
-                while (ru) {  // warp-uniform loop over non-empty mask rows
-                    int r = __ffs(ru) - 1;
-                    ru &= ru - 1;
-                    uint32_t mw = __shfl_sync(0xffffffffu, mword, r);
-                    if (hit) {
-                        uint32_t aw = a_tiles[(size_t)ta * D + r];
-                        if (work) units_done += aw ? __popc(mw) : 0u;
-                        while (aw && mw) {
-                            int cc = __ffs(mw) - 1;
-                            mw &= mw - 1;
-                            acc += __popc(aw & (uint32_t)b_tiles[(size_t)bi * D + cc]);
-                        }
-                    }
-                }
-            }
-        }
-        }
-    }
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0 && acc) atomicAdd(out, acc);
-    if (work) {
-        for (int o = 16; o; o >>= 1) units_done += __shfl_xor_sync(0xffffffffu, units_done, o);
-        if (lane == 0 && units_done) atomicAdd(work, units_done);
-    }
-}
-
-int64_t bmm_masked_rowtable(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_matrix *mask, cudaStream_t s,
-                            uint64_t *work_out) {
-    uint32_t mntr = mask->ntr;
-    Buf<uint32_t> cnt(mntr, s);
-    Buf<uint64_t> ofs((size_t)mntr + 1, s);
-    LAUNCH(k_rt_counts, grid_for(mntr), 256, 0, s, mntr, mask->trp, cnt.p);
-    exclusive_scan_u32_to_u64(cnt.p, ofs.p, mntr, s);
-    uint64_t n_units = read_scalar(ofs.p + mntr, s);
-    Buf<unsigned long long> out(1, s), work(1, s);
-    CK(cudaMemsetAsync(out.p, 0, 8, s));
-    CK(cudaMemsetAsync(work.p, 0, 8, s));
-    if (!n_units) return 0;
-    Buf<uint4> units(n_units, s);
-    LAUNCH(k_rt_fill, grid_for(mntr), 256, 0, s, mntr, mask->trp, cnt.p, ofs.p, units.p);
-    uint64_t blocks = (n_units + 7) / 8, cap = (uint64_t)num_sms() * 16;
-    unsigned g = (unsigned)std::min(blocks, cap);
-    kernel_timer().begin(s);
-    switch (a->dim) {
-#define RT_CASE(DD, W)                                                                                         \
-    case DD:                                                                                                   \
-        LAUNCH(k_bmm_rowtable<DD>, g, 256, 0, s, n_units, units.p, mask->row0, mask->tci,                     \
-               (const W *)mask->tiles, a->trp, a->tci, (const W *)a->tiles, bt->trp, bt->tci,                 \
-               (const W *)bt->tiles, out.p, work_out ? work.p : nullptr);                                     \
-        break;
-        RT_CASE(4, uint8_t)
-        RT_CASE(8, uint8_t)
-        RT_CASE(16, uint16_t)
-        RT_CASE(32, uint32_t)
-#undef RT_CASE
-    }
-    kernel_timer().end(s);
-    if (work_out) *work_out = read_scalar(work.p, s);
-    return (int64_t)read_scalar(out.p, s);
-}
-
-// ------------------------------------------------------------ row-hash path
-// Work unit = (mask tile row I, up to ROW_UNIT of its mask tiles).  The CTA
-// hashes A's tile row I (column -> position) into shared memory once; each
-// warp then takes a mask tile (I, J), streams Bt's row J 32 columns at a
-// time (coalesced) and probes the table -- one memory round trip per 32
-// candidates instead of a dependent binary search per candidate.  Rows of A
-// longer than HASH_MAX fall back to the binary-search warp loop.
-constexpr uint32_t ROW_UNIT = 128;
-constexpr uint32_t HASH_MAX = 4096;              // A-row entries that fit the table
-constexpr uint32_t HASH_SLOTS = 2 * HASH_MAX;    // 64 KB of keys + positions
-constexpr uint32_t EMPTY_KEY = 0xFFFFFFFFu;
-
-__global__ void k_rowunit_counts(uint32_t mntr, uint32_t m_row0, const uint32_t *__restrict__ mtrp,
-                                 const uint32_t *__restrict__ a_trp, uint32_t *__restrict__ cnt) {
-    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < mntr; r += gridDim.x * blockDim.x) {
-        uint32_t I = r + m_row0, len = mtrp[r + 1] - mtrp[r];
-        cnt[r] = (a_trp[I + 1] > a_trp[I]) ? (len + ROW_UNIT - 1) / ROW_UNIT : 0;
-    }
-}
-
-__global__ void k_rowunit_fill(uint32_t mntr, const uint32_t *__restrict__ mtrp, const uint32_t *__restrict__ cnt,
-                               const uint64_t *__restrict__ ofs, uint4 *__restrict__ units) {
-    for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < mntr; r += gridDim.x * blockDim.x) {
-        uint64_t o = ofs[r];
-        uint32_t m0 = mtrp[r], m1 = mtrp[r + 1];
-        for (uint32_t j = 0; j < cnt[r]; j++) units[o + j] = make_uint4(r, m0 + j * ROW_UNIT, min(m1, m0 + (j + 1) * ROW_UNIT), 0);
-    }
-}
-
-__device__ __forceinline__ uint32_t hash_slot(uint32_t k, uint32_t mask) { return (k * 0x9E3779B1u >> 7) & mask; }
-
-template <int D>
-__device__ __forceinline__ unsigned long long mask_tile_pops(uint32_t mword, uint32_t rows_used, bool hit, uint32_t ta,
-                                                             uint32_t tb, const typename WordT<D>::T *__restrict__ a_tiles,
-                                                             const typename WordT<D>::T *__restrict__ b_tiles) {
-    unsigned long long acc = 0;
-    uint32_t ru = rows_used;
-    while (ru) {  // warp-uniform loop over non-empty mask rows
-        int r = __ffs(ru) - 1;
-        ru &= ru - 1;
-        uint32_t mw = __shfl_sync(0xffffffffu, mword, r);
-        if (hit) {
-            uint32_t aw = a_tiles[(size_t)ta * D + r];
-            while (aw && mw) {
-                int c = __ffs(mw) - 1;
-                mw &= mw - 1;
-                acc += __popc(aw & (uint32_t)b_tiles[(size_t)tb * D + c]);
-            }
-        }
-    }
-    return acc;
-}
-
-template <int D>
-__global__ void __launch_bounds__(256) k_bmm_rowhash(uint32_t n_units, const uint4 *__restrict__ units, uint32_t m_row0,
-                                                     const uint32_t *__restrict__ m_tci,
-                                                     const typename WordT<D>::T *__restrict__ m_tiles,
-                                                     const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ a_tci,
-                                                     const typename WordT<D>::T *__restrict__ a_tiles,
-                                                     const uint32_t *__restrict__ b_trp, const uint32_t *__restrict__ b_tci,
-                                                     const typename WordT<D>::T *__restrict__ b_tiles,
-                                                     unsigned long long *__restrict__ out) {
-    extern __shared__ uint32_t hsm[];  // HASH_SLOTS keys then HASH_SLOTS positions
-    uint32_t *hkey = hsm, *hval = hsm + HASH_SLOTS;
-    const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    unsigned long long acc = 0;
-    for (uint32_t u = blockIdx.x; u < n_units; u += gridDim.x) {
-        uint4 un = units[u];
-        uint32_t I = un.x + m_row0;
-        uint32_t a0 = a_trp[I], a1 = a_trp[I + 1], la = a1 - a0;
-        bool hashed = la <= HASH_MAX;
-        uint32_t hs = 64;
-        while (hs < 2 * la) hs <<= 1;
-        uint32_t hmask = hs - 1;
-        if (hashed) {
-            for (uint32_t i = threadIdx.x; i < hs; i += blockDim.x) hkey[i] = EMPTY_KEY;
-            __syncthreads();
-            for (uint32_t i = threadIdx.x; i < la; i += blockDim.x) {
-                uint32_t K = __ldg(a_tci + a0 + i), h = hash_slot(K, hmask);
-                while (atomicCAS(&hkey[h], EMPTY_KEY, K) != EMPTY_KEY) h = (h + 1) & hmask;
-                hval[h] = i;
-            }
-            __syncthreads();
-        }
-        for (uint32_t mt = un.y + warp; mt < un.z; mt += nwarps) {
-            uint32_t J = m_tci[mt];
-            uint32_t mword = lane < (uint32_t)D ? (uint32_t)m_tiles[(size_t)mt * D + lane] : 0u;
-            uint32_t rows_used = __ballot_sync(0xffffffffu, mword != 0);
-            uint32_t b0 = b_trp[J], b1 = b_trp[J + 1];
-            if (!rows_used || b0 == b1) continue;
-            if (hashed) {
-                for (uint32_t base = b0; base < b1; base += 32) {
-                    uint32_t bi = base + lane, ta = 0;
-                    bool hit = false;
-                    if (bi < b1) {
-                        uint32_t K = __ldg(b_tci + bi), h = hash_slot(K, hmask), key;
-                        while ((key = hkey[h]) != EMPTY_KEY && key != K) h = (h + 1) & hmask;
-                        if (key == K) { hit = true; ta = a0 + hval[h]; }
-                    }
-                    if (__ballot_sync(0xffffffffu, hit)) acc += mask_tile_pops<D>(mword, rows_used, hit, ta, bi, a_tiles, b_tiles);
-                }
-            } else {  // long A row: binary-search Bt's entries in it
-                for (uint32_t base = b0; base < b1; base += 32) {
-                    uint32_t bi = base + lane, ta = 0;
-                    bool hit = false;
-                    if (bi < b1) {
-                        uint32_t K = __ldg(b_tci + bi);
-                        uint32_t li = lower_bound_u32(a_tci, a0, a1, K);
-                        if (li < a1 && __ldg(a_tci + li) == K) { hit = true; ta = li; }
-                    }
-                    if (__ballot_sync(0xffffffffu, hit)) acc += mask_tile_pops<D>(mword, rows_used, hit, ta, bi, a_tiles, b_tiles);
-                }
-            }
-        }
-        __syncthreads();  // the table is rebuilt for the next unit
-    }
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0 && acc) atomicAdd(out, acc);
-}
-
-int64_t bmm_masked_rowhash(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_matrix *mask, cudaStream_t s) {
-    uint32_t mntr = mask->ntr;
-    Buf<uint32_t> cnt(mntr, s);
-    Buf<uint64_t> ofs((size_t)mntr + 1, s);
-    LAUNCH(k_rowunit_counts, grid_for(mntr), 256, 0, s, mntr, mask->row0, mask->trp, a->trp, cnt.p);
-    exclusive_scan_u32_to_u64(cnt.p, ofs.p, mntr, s);
-    uint64_t n_units = read_scalar(ofs.p + mntr, s);
-    Buf<unsigned long long> out(1, s);
-    CK(cudaMemsetAsync(out.p, 0, 8, s));
-    if (!n_units) return 0;
-    Buf<uint4> units(n_units, s);
-    LAUNCH(k_rowunit_fill, grid_for(mntr), 256, 0, s, mntr, mask->trp, cnt.p, ofs.p, units.p);
-    unsigned g = (unsigned)std::min<uint64_t>(n_units, (uint64_t)num_sms() * 3);
-    const int smem = 2 * HASH_SLOTS * 4;
-    switch (a->dim) {
-#define RH_CASE(DD, W)                                                                                          \
-    case DD:                                                                                                    \
-        CK(cudaFuncSetAttribute(k_bmm_rowhash<DD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));        \
-        LAUNCH(k_bmm_rowhash<DD>, g, 256, smem, s, (uint32_t)n_units, units.p, mask->row0, mask->tci,          \
-               (const W *)mask->tiles, a->trp, a->tci, (const W *)a->tiles, bt->trp, bt->tci,                  \
-               (const W *)bt->tiles, out.p);                                                                   \
-        break;
-        RH_CASE(4, uint8_t)
-        RH_CASE(8, uint8_t)
-        RH_CASE(16, uint16_t)
-        RH_CASE(32, uint32_t)
-#undef RH_CASE
-    }
-    return (int64_t)read_scalar(out.p, s);
-}
-
 int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_matrix *mask, cudaStream_t s,
                       uint64_t *work_out = nullptr) {
     if (work_out) *work_out = 0;
     if (!mask->num_tiles || !a->num_tiles || !bt->num_tiles) return 0;
-    // B2SR_TC_ALG=rowhash selects the smem row-hash kernel (measured 176 ms vs
-    // 34 ms for the chunked items at s20 d=4, profiles/r01_pull_ab.txt)
-    const char *alg = getenv("B2SR_TC_ALG");
-    if (alg && alg[0] == 'r') return bmm_masked_rowhash(a, bt, mask, s);
-    // B2SR_TC_ALG=table: the register-table rows kernel -- measured slower at
-    // R-MAT s20 d=4 on the degree-oriented DAG (32.6 vs 27.2 ms): it always
-    // scans Bt's row (5.0 G probes) where the items kernel scans the shorter
-    if (alg && alg[0] == 't') return bmm_masked_rowtable(a, bt, mask, s, work_out);
     uint64_t TM = mask->num_tiles;
     Buf<uint32_t> rowid(TM, s), cnt(TM, s);
     Buf<uint64_t> ofs(TM + 1, s);

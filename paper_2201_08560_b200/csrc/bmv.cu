@@ -170,24 +170,6 @@ __global__ void __launch_bounds__(256) k_bmv_bbb(const WorkItem *__restrict__ it
     bbb_items<D>(items, n_items, tiles, tci, XGlobal<D, XG>{x}, keep, y, row0);
 }
 
-// Hot-column variant: one 1024-thread CTA per SM, the hot x words in shared
-// memory (hot.cu), tci2 = remapped tile-column indices.
-constexpr int HOT_THREADS = 1024;
-
-template <int D>
-__global__ void __launch_bounds__(HOT_THREADS, 1) k_bmv_bbb_hot(const WorkItem *__restrict__ items, uint32_t n_items,
-                                                               const uint8_t *__restrict__ tiles,
-                                                               const uint32_t *__restrict__ tci2,
-                                                               const void *__restrict__ hx, uint32_t hx_bytes16,
-                                                               uint32_t S, const void *__restrict__ x,
-                                                               const void *__restrict__ keep, void *__restrict__ y,
-                                                               uint32_t row0) {
-    stage_hot(const_cast<uint8_t *>(hot_bytes()), hx, hx_bytes16);
-    __syncthreads();
-    XHot<D> gx(x, S);
-    bbb_items<D>(items, n_items, tiles, tci2, gx, keep, y, row0);
-}
-
 // ------------------------------------------------------------ K5 bbf
 template <int D> struct NCnt { static constexpr int N = D == 4 ? 4 : (D == 32 ? 4 : 8); };
 
@@ -297,214 +279,18 @@ __global__ void __launch_bounds__(256) k_bmv_bbf(const WorkItem *__restrict__ it
     }
 }
 
-// ------------------------------------------------------------ K6 bff
-template <int RING>
-__device__ __forceinline__ double ring_op(double cur, double term, double inc) {
-    if constexpr (RING == B2SR_RING_ARITHMETIC) {
-        return __dadd_rn(cur, term);
-    } else if constexpr (RING == B2SR_RING_MINPLUS) {
-        double t = __dadd_rn(term, inc);
-        return (cur < t || isnan(cur)) ? cur : t;  // np.minimum
-    } else {
-        return (cur > term || isnan(cur)) ? cur : term;  // np.maximum
-    }
-}
-
-template <int D, int RING>
-__global__ void __launch_bounds__(256) k_bmv_bff(uint32_t ntr, uint32_t n, const uint32_t *__restrict__ trp,
-                                                 const uint32_t *__restrict__ tci,
-                                                 const typename WordT<D>::T *__restrict__ tiles,
-                                                 const double *__restrict__ x, double inc, const void *__restrict__ keep,
-                                                 double *__restrict__ y, uint32_t row0, uint32_t long_thresh) {
-    constexpr uint32_t GPW = 32 / D;
-    const uint32_t lane = lane_id(), r = lane % D;
-    const double ident = RING == B2SR_RING_MINPLUS ? __longlong_as_double(0x7FF0000000000000ll) : 0.0;
-    const uint32_t groups = ((gridDim.x * blockDim.x) >> 5) * GPW;
-    for (uint32_t I = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * GPW + lane / D; I < ntr; I += groups) {
-        double acc = ident;
-        uint32_t t = trp[I], t1 = trp[I + 1];
-        if (t1 - t > long_thresh) continue;  // k_bmv_bff_long owns this row
-        // four tiles per step: indices and row words first, then the gathers
-        for (; t + 4 <= t1; t += 4) {
-            uint32_t k0 = __ldg(tci + t), k1 = __ldg(tci + t + 1), k2 = __ldg(tci + t + 2), k3 = __ldg(tci + t + 3);
-            uint32_t w0 = tiles[(size_t)t * D + r], w1 = tiles[(size_t)(t + 1) * D + r];
-            uint32_t w2 = tiles[(size_t)(t + 2) * D + r], w3 = tiles[(size_t)(t + 3) * D + r];
-            uint32_t ks[4] = {k0, k1, k2, k3}, ws[4] = {w0, w1, w2, w3};
-#pragma unroll
-            for (int j = 0; j < 4; j++) {
-                uint32_t wj = ws[j];
-                const double *xs = x + (size_t)ks[j] * D;
-                while (wj) {
-                    int k = __ffs(wj) - 1;
-                    wj &= wj - 1;
-                    acc = ring_op<RING>(acc, __ldg(xs + k), inc);
-                }
-            }
-        }
-        for (; t < t1; t++) {
-            uint32_t wj = tiles[(size_t)t * D + r];
-            const double *xs = x + (size_t)__ldg(tci + t) * D;
-            while (wj) {
-                int k = __ffs(wj) - 1;
-                wj &= wj - 1;
-                acc = ring_op<RING>(acc, __ldg(xs + k), inc);
-            }
-        }
-        uint32_t grow = row0 + I;
-        uint64_t vrow = (uint64_t)grow * D + r;
-        if (vrow < n) {
-            if (keep && !((load_word<D>(keep, grow) >> r) & 1u)) acc = ident;
-            y[(size_t)I * D + r] = acc;
-        }
-    }
-}
-
-// ------------------------------------------------------------ K6 long rows
-// A hub tile row (R-MAT s24: ~1e5 tiles) walked by one group of d lanes is a
-// serial chain of dependent loads -- it alone took >150 ms per PageRank sweep.
-// Rows longer than LONG_ROW_TILES get a CTA: per chunk of LONG_CHUNK tiles
-// every thread stages one tile (its d row words, and the x values of the
-// columns any of its rows touch) in shared memory, then thread r folds bit-row
-// r over the staged tiles in ascending order -- the reference's summation
-// order, so ARITHMETIC stays bit-identical -- while the gathers ran in parallel.
-constexpr uint32_t LONG_ROW_TILES = 512;
-constexpr int LONG_THREADS = 256;
-
+// ------------------------------------------------------------ K6 plans
 constexpr uint32_t VLONG_ROW_TILES = 256;  // longer rows: bmv_vlong.cu (segmented scatter + fold)
 
-__global__ void k_find_long(uint32_t ntr, const uint32_t *trp, uint32_t lo, uint32_t hi, uint32_t *rows,
-                            uint32_t *count) {
-    for (uint32_t I = blockIdx.x * blockDim.x + threadIdx.x; I < ntr; I += gridDim.x * blockDim.x) {
-        uint32_t len = trp[I + 1] - trp[I];
-        if (len > lo && len <= hi) rows[atomicAdd(count, 1u)] = I;
-    }
+// Row-length thresholds are fixed per matrix when its plan is built; the env
+// override exists so parity tests can push small matrices through both paths.
+static uint32_t vlong_thresh() {
+    const char *ev = getenv("B2SR_VLONG_TILES");
+    return ev ? (uint32_t)atoi(ev) : VLONG_ROW_TILES;
 }
 
-void ensure_long_rows(b2sr_matrix *m, cudaStream_t s) {
-    if (m->long_rows) return;
-    Buf<uint32_t> rows(m->ntr, s), cnt(1, s);
-    CK(cudaMemsetAsync(cnt.p, 0, 4, s));
-    unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((m->ntr + 255) / 256, (uint64_t)num_sms() * 16));
-    // thresholds are fixed per matrix when its plan is built; the env overrides
-    // exist so parity tests can push small matrices through all three paths
-    const char *el = getenv("B2SR_LONG_TILES"), *ev = getenv("B2SR_VLONG_TILES");
-    uint32_t lo = el ? (uint32_t)atoi(el) : LONG_ROW_TILES, hi = ev ? (uint32_t)atoi(ev) : VLONG_ROW_TILES;
-    m->long_lo = lo;
-    LAUNCH(k_find_long, g, 256, 0, s, m->ntr, m->trp, lo, hi, rows.p, cnt.p);
-    m->n_long = read_scalar(cnt.p, s);
-    m->vlong = build_vlong(m, hi, s);
-    m->long_rows = rows.release();
-}
-
-template <int D, int RING>
-__global__ void __launch_bounds__(LONG_THREADS) k_bmv_bff_long(uint32_t n_long, const uint32_t *__restrict__ long_rows,
-                                                               uint32_t n, const uint32_t *__restrict__ trp,
-                                                               const uint32_t *__restrict__ tci,
-                                                               const typename WordT<D>::T *__restrict__ tiles,
-                                                               const double *__restrict__ x, double inc,
-                                                               const void *__restrict__ keep, double *__restrict__ y,
-                                                               uint32_t row0) {
-    // C tiles per chunk, one per thread; each bit-row r gets up to CAP terms
-    // per chunk in smem (2 per tile on average; denser chunks take the slow fold)
-    constexpr int C = LONG_THREADS * 4 / D < LONG_THREADS ? LONG_THREADS * 4 / D : LONG_THREADS;
-    constexpr int CAP = 2 * C;
-    constexpr int NW = LONG_THREADS / 32;
-    __shared__ uint32_t sw[C][D];          // staged row words
-    __shared__ double sx[C][D];            // staged x values per (tile, column)
-    __shared__ double terms[D][CAP];       // compacted terms of each bit-row, in reference order
-    __shared__ uint32_t wsum[NW][D], tot[D];
-    const double ident = RING == B2SR_RING_MINPLUS ? __longlong_as_double(0x7FF0000000000000ll) : 0.0;
-    const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
-    for (uint32_t li = blockIdx.x; li < n_long; li += gridDim.x) {
-        uint32_t I = long_rows[li];
-        uint32_t t0 = trp[I], t1 = trp[I + 1];
-        double acc = ident;  // meaningful in threads r < D
-        for (uint32_t base = t0; base < t1; base += C) {
-            uint32_t cnt = min((uint32_t)C, t1 - base);
-            uint32_t w[D];
-#pragma unroll
-            for (int r = 0; r < D; r++) w[r] = 0;
-            if (tid < cnt) {
-                uint32_t t = base + tid;
-                const double *xs = x + (size_t)__ldg(tci + t) * D;
-                uint32_t any = 0;
-#pragma unroll
-                for (int r = 0; r < D; r++) {
-                    w[r] = tiles[(size_t)t * D + r];
-                    sw[tid][r] = w[r];
-                    any |= w[r];
-                }
-                while (any) {  // x values of every column this tile touches (parallel gathers)
-                    int k = __ffs(any) - 1;
-                    any &= any - 1;
-                    sx[tid][k] = __ldg(xs + k);
-                }
-            }
-            // exclusive scan of per-tile term counts, separately for every bit-row
-            uint32_t off[D];
-#pragma unroll
-            for (int r = 0; r < D; r++) {
-                uint32_t c = __popc(w[r]), inc = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-                    if (lane >= (uint32_t)o) inc += y;
-                }
-                off[r] = inc - c;
-                if (lane == 31) wsum[wid][r] = inc;
-            }
-            __syncthreads();
-            if (tid < (uint32_t)D) {
-                uint32_t run = 0;
-                for (int q = 0; q < NW; q++) {
-                    uint32_t v = wsum[q][tid];
-                    wsum[q][tid] = run;
-                    run += v;
-                }
-                tot[tid] = run;
-            }
-            __syncthreads();
-            bool dense = false;
-#pragma unroll
-            for (int r = 0; r < D; r++) dense |= tot[r] > (uint32_t)CAP;
-            if (!dense && tid < cnt) {  // scatter this tile's terms (ascending column) per bit-row
-#pragma unroll
-                for (int r = 0; r < D; r++) {
-                    uint32_t o = wsum[wid][r] + off[r], b = w[r];
-                    while (b) {
-                        int k = __ffs(b) - 1;
-                        b &= b - 1;
-                        terms[r][o++] = sx[tid][k];
-                    }
-                }
-            }
-            __syncthreads();
-            if (tid < (uint32_t)D) {
-                if (!dense) {  // pure dependent-add chain over contiguous terms
-                    uint32_t nt = tot[tid];
-                    for (uint32_t q = 0; q < nt; q++) acc = ring_op<RING>(acc, terms[tid][q], inc);
-                } else {
-                    for (uint32_t j = 0; j < cnt; j++) {
-                        uint32_t b = sw[j][tid];
-                        while (b) {
-                            int k = __ffs(b) - 1;
-                            b &= b - 1;
-                            acc = ring_op<RING>(acc, sx[j][k], inc);
-                        }
-                    }
-                }
-            }
-            __syncthreads();
-        }
-        if (tid < (uint32_t)D) {
-            uint32_t grow = row0 + I;
-            uint64_t vrow = (uint64_t)grow * D + tid;
-            if (vrow < n) {
-                if (keep && !((load_word<D>(keep, grow) >> tid) & 1u)) acc = ident;
-                y[(size_t)I * D + tid] = acc;
-            }
-        }
-    }
+static void ensure_vlong(b2sr_matrix *m, cudaStream_t s) {
+    if (!m->vlong) m->vlong = build_vlong(m, vlong_thresh(), s);
 }
 
 // ------------------------------------------------------------ used columns / scale
@@ -566,13 +352,7 @@ int64_t prescale(const b2sr_matrix *m, const double *x, const double *scale, dou
 }
 
 // ------------------------------------------------------------ launchers
-unsigned hot_grid(uint64_t n_items) {
-    uint64_t b = (n_items + HOT_THREADS / 32 - 1) / (HOT_THREADS / 32);
-    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(b, (uint64_t)num_sms()));
-}
-
 void launch_bbb(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaStream_t s) {
-    if (blocked_enabled() && launch_blocked(m, 0, x, keep, y, s)) return;
     if (stream_enabled(m->dim)) {
         launch_bbb_stream(m, x, keep, y, s);
         return;
@@ -580,37 +360,11 @@ void launch_bbb(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaSt
     ensure_items(m, s);
     if (m->any_split) CK(cudaMemsetAsync(y, 0, padded_vec_bytes(m->ntr, m->dim), s));
     const uint8_t *tl = (const uint8_t *)m->tiles;
-    if (hot_enabled(m->dim)) {
-        HotView hv = hot_view(m, s);
-        size_t hb = hot_fill_bytes(hv, m->dim);
-        Buf<uint8_t> hx(hb, s);
-        hot_fill(hv, m->dim, x, hx.p, s);
-        unsigned g = hot_grid(m->n_items);
-#define HOT_CASE(DD)                                                                                              \
-    case DD:                                                                                                      \
-        hot_smem_attr(k_bmv_bbb_hot<DD>, hb);                                                                     \
-        LAUNCH(k_bmv_bbb_hot<DD>, g, HOT_THREADS, hb, s, m->items, m->n_items, tl, hv.tci2, hx.p, (uint32_t)hb,   \
-               hv.S, x, keep, y, m->row0);                                                                        \
-        break;
-        switch (m->dim) {
-            HOT_CASE(4)
-            HOT_CASE(8)
-            HOT_CASE(16)
-        }
-#undef HOT_CASE
-        return;
-    }
     unsigned g = item_grid(m);
-    const char *xg_env = getenv("B2SR_XGATHER");  // cache policy of the x gathers (A/B)
-    int xg = xg_env ? atoi(xg_env) : 0;
     kernel_timer().begin(s);
-#define BBB_LAUNCH(DD, XX) \
-    LAUNCH((k_bmv_bbb<DD, XX>), g, 256, 0, s, m->items, m->n_items, tl, m->tci, x, keep, y, m->row0)
-#define BBB_CASE(DD)                                  \
-    case DD:                                          \
-        if (xg == 1) BBB_LAUNCH(DD, 1);               \
-        else if (xg == 2) BBB_LAUNCH(DD, 2);          \
-        else BBB_LAUNCH(DD, 0);                       \
+#define BBB_CASE(DD)                                                                                              \
+    case DD:                                                                                                      \
+        LAUNCH((k_bmv_bbb<DD, 0>), g, 256, 0, s, m->items, m->n_items, tl, m->tci, x, keep, y, m->row0);          \
         break;
     switch (m->dim) {
         BBB_CASE(4)
@@ -620,7 +374,6 @@ void launch_bbb(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaSt
     }
     kernel_timer().end(s);
 #undef BBB_CASE
-#undef BBB_LAUNCH
 }
 
 static size_t local_rows(const b2sr_matrix *m) {
@@ -642,53 +395,17 @@ void launch_bbf(b2sr_matrix *m, const void *x, const void *keep, double *y, cuda
     }
 }
 
-template <int D>
-static void bff_ring(const b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
-                     cudaStream_t s) {
-    constexpr uint32_t GPW = 32 / D;
-    ensure_long_rows(const_cast<b2sr_matrix *>(m), s);
-    const char *old = getenv("B2SR_BFF_OLD");  // A/B: the group-per-row + CTA-per-row kernels
-    if (!(old && old[0] == '1')) {
-        // rows up to the segmented-plan threshold: pipelined group-per-row walk
-        // (bmv_bff.cu); longer rows: segmented scatter + warp folds (bmv_vlong.cu)
-        const char *ev = getenv("B2SR_VLONG_TILES");
-        uint32_t hi = ev ? (uint32_t)atoi(ev) : VLONG_ROW_TILES;
-        launch_bff_rows(const_cast<b2sr_matrix *>(m), x, ring, inc, keep, y, hi, s, /*plan_only=*/true);
-        launch_vlong(const_cast<b2sr_matrix *>(m), x, ring, inc, keep, y, s, [&](cudaStream_t so) {
-            launch_bff_rows(const_cast<b2sr_matrix *>(m), x, ring, inc, keep, y, hi, so);
-        });
-        return;
-    }
-    uint64_t warps = ((uint64_t)m->ntr + GPW - 1) / GPW;
-    uint64_t blocks = (warps + 7) / 8, cap = (uint64_t)num_sms() * 16;
-    unsigned g = (unsigned)(blocks < cap ? blocks : cap);
-    unsigned gl = (unsigned)std::min<uint64_t>(m->n_long, (uint64_t)num_sms() * 8);
-    using W = typename WordT<D>::T;
-    const W *tl = (const W *)m->tiles;
-#define BFF_RING(RR)                                                                                              \
-    do {                                                                                                          \
-        LAUNCH((k_bmv_bff<D, RR>), g, 256, 0, s, m->ntr, m->n, m->trp, m->tci, tl, x, inc, keep, y, m->row0,      \
-               m->long_lo);                                                                                       \
-        LAUNCH((k_bmv_bff_long<D, RR>), gl, LONG_THREADS, 0, s, m->n_long, m->long_rows, m->n, m->trp, m->tci,   \
-               tl, x, inc, keep, y, m->row0);                                                                     \
-    } while (0)
-    if (ring == B2SR_RING_ARITHMETIC) BFF_RING(B2SR_RING_ARITHMETIC);
-    else if (ring == B2SR_RING_MINPLUS) BFF_RING(B2SR_RING_MINPLUS);
-    else BFF_RING(B2SR_RING_MAXTIMES);
-#undef BFF_RING
-    launch_vlong(const_cast<b2sr_matrix *>(m), x, ring, inc, keep, y, s);
-}
-
-void launch_bff(const b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
+// Rows up to the segmented-plan threshold: pipelined group-per-row walk
+// (bmv_bff.cu), overlapped with the hub rows' segmented scatter + warp folds
+// (bmv_vlong.cu).
+void launch_bff(const b2sr_matrix *m_, const double *x, int ring, double inc, const void *keep, double *y,
                 cudaStream_t s) {
-    switch (m->dim) {
-        case 4: bff_ring<4>(m, x, ring, inc, keep, y, s); break;
-        case 8: bff_ring<8>(m, x, ring, inc, keep, y, s); break;
-        case 16: bff_ring<16>(m, x, ring, inc, keep, y, s); break;
-        default: bff_ring<32>(m, x, ring, inc, keep, y, s); break;
-    }
+    b2sr_matrix *m = const_cast<b2sr_matrix *>(m_);
+    ensure_vlong(m, s);
+    const uint32_t hi = vlong_thresh();
+    launch_bff_rows(m, x, ring, inc, keep, y, hi, s, /*plan_only=*/true);
+    launch_vlong(m, x, ring, inc, keep, y, s, [&](cudaStream_t so) { launch_bff_rows(m, x, ring, inc, keep, y, hi, so); });
 }
-
 }  // namespace b2sr
 
 using namespace b2sr;

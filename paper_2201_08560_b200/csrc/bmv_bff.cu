@@ -4,7 +4,7 @@
 // A group of d lanes per tile row, lane = bit-row, walks the row's tiles in
 // ascending order and, inside a tile, the set bits in ascending column order:
 // the reference's reduction order, so ARITHMETIC is bit-identical and the
-// min/max rings keep numpy's NaN / tie behaviour (see ring_op in bmv.cu).
+// min/max rings keep numpy's NaN / tie behaviour (bff_op below).
 //
 // What makes it fast is keeping the loads independent of the fold:
 //   * four tiles per step, fetched as 16-byte vectors (d=4: the four tile

@@ -73,7 +73,6 @@ template <typename K>
 inline void hot_smem_attr(K kernel, size_t bytes) {
     hot_smem_attr_raw(reinterpret_cast<const void *>(kernel), bytes);
 }
-unsigned hot_grid(uint64_t n_items);  // one 1024-thread CTA per SM at most
 
 // x-word gathers used by the streaming kernels: plain global loads with a
 // selectable cache policy, or the hot-column cache (hot.cu) in shared memory

@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(NT, 1)
         push_entries<D>(ctl->list_n, plist, a_trp, a_tci, a_tiles, frontier, next);
         return;
     }
-    const bool listed = mode == BFS_PULL_ACTIVE || mode == BFS_PULL_DENSE;
+    const bool listed = mode == BFS_PULL_ACTIVE;
     const uint32_t n_pos = listed ? ctl->active_n : n_loads;
     if (n_pos == 0) return;
     stage_hot(const_cast<uint8_t *>(hot_bytes()), hx, hx_bytes16);

@@ -117,9 +117,7 @@ void free_matrix(b2sr_matrix *m) {
     dfree(m->items, nullptr);
     dfree(m->live, nullptr);
     dfree(m->item_ofs, nullptr);
-    dfree(m->long_rows, nullptr);
     free_vlong(m->vlong);
-    free_plan(m->plan);
     free_hot(m->hot);
     free_stream(m->stream);
     free_bff(m->bff);

@@ -140,62 +140,6 @@ __global__ void __launch_bounds__(256) k_bfs_pull(const WorkItem *__restrict__ i
     pull_items<D>(items, n_items, tiles, tci, XGlobal<D>{frontier}, visited, live, next, row0, idx, idx_n);
 }
 
-// hot-column variant (hot.cu): frontier words of the hot tile columns in smem
-constexpr int PULL_HOT_THREADS = 1024;
-
-template <int D>
-__global__ void __launch_bounds__(PULL_HOT_THREADS, 1)
-    k_bfs_pull_hot(const WorkItem *__restrict__ items, uint32_t n_items, const uint8_t *__restrict__ tiles,
-                   const uint32_t *__restrict__ tci2, const void *__restrict__ hx, uint32_t hx_bytes16, uint32_t S,
-                   const void *__restrict__ frontier, const void *__restrict__ visited, const void *__restrict__ live,
-                   void *__restrict__ next, uint32_t row0, const uint32_t *__restrict__ idx,
-                   const uint32_t *__restrict__ idx_n) {
-    stage_hot(const_cast<uint8_t *>(hot_bytes()), hx, hx_bytes16);
-    __syncthreads();
-    XHot<D> gx(frontier, S);
-    pull_items<D>(items, n_items, tiles, tci2, gx, visited, live, next, row0, idx, idx_n);
-}
-
-// Sub-warp pull: a group of GS lanes per work item, GS*TPL/LPT tiles per step
-// (32 at d=4), and the all-keep-bits-hit exit is tested after every step, so a
-// tile row whose unvisited vertices find a parent early stops early.
-template <int D> struct PullGroup { static constexpr int GS = D <= 8 ? 8 : (D == 16 ? 16 : 32); };
-
-template <int D>
-__global__ void __launch_bounds__(256) k_bfs_pull_g(const WorkItem *__restrict__ items, uint32_t n_items, uint32_t n,
-                                                    const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
-                                                    const void *__restrict__ frontier, const void *__restrict__ visited,
-                                                    const void *__restrict__ live, void *__restrict__ next,
-                                                    uint32_t row0, const uint32_t *__restrict__ idx,
-                                                    const uint32_t *__restrict__ idx_n) {
-    using G = BGeo<D>;
-    constexpr int GS = PullGroup<D>::GS;
-    constexpr uint32_t STEP = GS * G::TPL / G::LPT;
-    const uint32_t lane = lane_id(), gl = lane % GS;
-    const uint32_t gmask = GS == 32 ? 0xffffffffu : (((1u << GS) - 1u) << (lane & ~(GS - 1u)));
-    const uint32_t groups = (gridDim.x * blockDim.x) / GS;
-    if (idx) n_items = *idx_n;
-    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) / GS; w < n_items; w += groups) {
-        WorkItem it = items[idx ? idx[w] : w];
-        uint32_t grow = row0 + it.row;
-        uint32_t keepw = ~load_word<D>(visited, grow) & load_word<D>(live, it.row);  // live is block-local
-        if (!keepw) continue;
-        uint32_t acc = 0;
-        uint32_t base = G::TPL > 1 ? (it.t0 & ~(uint32_t)(G::TPL - 1)) : it.t0;
-        for (; base < it.t1; base += STEP) {
-            acc |= bfs_lane<D>(tiles, tci, XGlobal<D>{frontier}, base, it.t0, it.t1, gl);
-#pragma unroll
-            for (int o = GS / 2; o; o >>= 1) acc |= __shfl_xor_sync(gmask, acc, o);
-            if ((acc & keepw) == keepw) break;  // every unvisited row of the tile row reached
-        }
-        acc &= keepw;
-        if (gl == 0 && acc) {
-            if (it.split) atomic_or_word<D>(next, it.row, acc);
-            else reinterpret_cast<typename WordT<D>::T *>(next)[it.row] = (typename WordT<D>::T)acc;
-        }
-    }
-}
-
 // visited |= frontier; levels[new bits] = level; *any |= frontier != 0
 template <int D>
 __global__ void k_bfs_update(uint32_t ntr, const void *__restrict__ frontier, void *__restrict__ visited,
@@ -492,14 +436,13 @@ void ensure_live(b2sr_matrix *m, cudaStream_t s) {
 // pull levels run on the flat tile stream (bmv_stream.cu) where it applies
 static bool pull_stream(const b2sr_matrix *at) {
     const char *ps = getenv("B2SR_PULL_STREAM");  // B2SR_PULL_STREAM=0: work-item pull kernels (A/B)
-    return stream_enabled(at->dim) && !(ps && ps[0] == '0') && !blocked_enabled();
+    return stream_enabled(at->dim) && !(ps && ps[0] == '0');
 }
 
 void bfs_sweep(b2sr_matrix *at, const void *frontier, const void *visited, void *next, cudaStream_t s,
                const uint32_t *idx = nullptr, const uint32_t *idx_n = nullptr, int active_only = -1,
                bool lazy = false) {
     ensure_live(at, s);
-    if (!idx && blocked_enabled() && launch_blocked(at, 1, frontier, visited, next, s)) return;
     if (!idx && pull_stream(at)) {
         // only the loads that still hold an unvisited vertex, once few are left
         launch_bbb_stream(at, frontier, nullptr, next, s, visited, active_only > 0, lazy);
@@ -510,41 +453,10 @@ void bfs_sweep(b2sr_matrix *at, const void *frontier, const void *visited, void 
     uint64_t blocks = ((uint64_t)at->n_items + 7) / 8, cap = (uint64_t)num_sms() * 16;
     unsigned g = (unsigned)std::min(blocks, cap);
     const uint8_t *tl = (const uint8_t *)at->tiles;
-    // B2SR_PULL=group selects the sub-warp pull (measured slower: 21.8 vs
-    // 35.3 GTEPS in the s22 d=4 sweep, profiles/r01_pull_ab.txt)
-    const char *pv = getenv("B2SR_PULL");
-    bool warp_pull = !(pv && pv[0] == 'g');
-    const char *hs = getenv("B2SR_HOT_SPARSE");  // hot cache for active-list pulls too (A/B)
-    const char *hp = getenv("B2SR_HOT_PULL");    // hot-cache pull: 1024-thread CTAs (A/B, default off)
-    if (warp_pull && hp && hp[0] == '1' && hot_enabled(at->dim) && (!idx || (hs && hs[0] == '1'))) {
-        HotView hv = hot_view(at, s);
-        size_t hb = hot_fill_bytes(hv, at->dim);
-        Buf<uint8_t> hx(hb, s);
-        hot_fill(hv, at->dim, frontier, hx.p, s);
-        // active lists are short: size the grid by the full item count anyway
-        unsigned gh = hot_grid(at->n_items);
-#define PULL_HOT(DD)                                                                                               \
-    case DD:                                                                                                       \
-        hot_smem_attr(k_bfs_pull_hot<DD>, hb);                                                                     \
-        LAUNCH(k_bfs_pull_hot<DD>, gh, PULL_HOT_THREADS, hb, s, at->items, at->n_items, tl, hv.tci2, hx.p,         \
-               (uint32_t)hb, hv.S, frontier, visited, at->live, next, at->row0, idx, idx_n);                      \
-        break;
-        switch (at->dim) {
-            PULL_HOT(4)
-            PULL_HOT(8)
-            PULL_HOT(16)
-        }
-#undef PULL_HOT
-        return;
-    }
 #define PULL_CASE(DD)                                                                                              \
     case DD:                                                                                                       \
-        if (warp_pull)                                                                                             \
-            LAUNCH(k_bfs_pull<DD>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited,    \
-                   at->live, next, at->row0, idx, idx_n);                                                          \
-        else                                                                                                       \
-            LAUNCH(k_bfs_pull_g<DD>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited,  \
-                   at->live, next, at->row0, idx, idx_n);                                                          \
+        LAUNCH(k_bfs_pull<DD>, g, 256, 0, s, at->items, at->n_items, at->n, tl, at->tci, frontier, visited,        \
+               at->live, next, at->row0, idx, idx_n);                                                              \
         break;
     switch (at->dim) {
         PULL_CASE(4)
@@ -795,7 +707,7 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
                                 double *__restrict__ levels, double level, const uint32_t *__restrict__ trp_a,
                                 const uint32_t *__restrict__ trp_at, const uint4 *__restrict__ live_at,
                                 BfsCtl *__restrict__ ctl, uint4 *__restrict__ zero_buf, int mask, double alpha,
-                                unsigned long long tiles_at, int has_a, int head_ok, BfsSnap *__restrict__ snap,
+                                unsigned long long tiles_at, int has_a, BfsSnap *__restrict__ snap,
                                 uint32_t level_no) {
     using W = typename WordT<D>::T;
     if (ctl->mode == BFS_NONE && mask) return;  // BFS already over
@@ -861,9 +773,7 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
         } else {
             cv->unvisited -= cv->cnt.removed_tiles;
             bool push = has_a && (double)cv->cnt.frontier_tiles * alpha < (double)cv->unvisited;
-            const bool dense = cv->cnt.frontier_vertices * 8 > (unsigned long long)ntr * D && head_ok;
-            cv->mode = push ? BFS_PUSH
-                            : (cv->unvisited * 2 < tiles_at ? BFS_PULL_ACTIVE : (dense ? BFS_PULL_DENSE : BFS_PULL));
+            cv->mode = push ? BFS_PUSH : (cv->unvisited * 2 < tiles_at ? BFS_PULL_ACTIVE : BFS_PULL);
             // a frontier of < 1/16 of the vertices: most 4-tile groups see all-zero x words
             cv->sparse = cv->cnt.frontier_vertices * 16 < (unsigned long long)ntr * D;
             cv->list_n = 0;
@@ -930,7 +840,7 @@ __global__ void k_bfs_prep(BfsCtl *__restrict__ c, uint32_t ntr, const uint32_t 
     } else {
         for (uint32_t i = tid; i < S; i += stride) hx[i] = fr[cols ? cols[i] : i];
     }
-    if (mode != BFS_PULL_ACTIVE) return;  // BFS_PULL_DENSE lists its loads after the head pass
+    if (mode != BFS_PULL_ACTIVE) return;
     const uint32_t iters = (n_loads + stride - 1) / stride;
     for (uint32_t it = 0; it < iters; it++) {
         uint32_t k = tid + it * stride;
@@ -939,59 +849,6 @@ __global__ void k_bfs_prep(BfsCtl *__restrict__ c, uint32_t ntr, const uint32_t 
             uint32_t ra = desc[k].x, rb = desc[k + 1].x;
             for (uint32_t r = ra; r <= rb && !act; r++)
                 act = (~load_word<D>(visited, r) & load_word<D>(live, r)) != 0;
-        }
-        uint32_t bal = __ballot_sync(0xffffffffu, act);
-        if (!bal) continue;
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&c->active_n, (uint32_t)__popc(bal));
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (act) alist[base + __popc(bal & ((1u << lane) - 1u))] = k;
-    }
-}
-
-// BFS_PULL_DENSE, step 1: one thread per tile row with unvisited live
-// vertices checks the row's first HEAD_TILES tiles against the frontier and
-// stores the hits (next is zero here).  Step 2 lists the loads of the rows
-// that still miss a parent for the stream.
-constexpr uint32_t HEAD_TILES = 16;
-
-template <int D>
-__global__ void k_bfs_head(const BfsCtl *__restrict__ c, uint32_t ntr, const uint32_t *__restrict__ trp,
-                           const uint32_t *__restrict__ tci, const typename WordT<D>::T *__restrict__ tiles,
-                           const void *__restrict__ frontier, const void *__restrict__ visited,
-                           const void *__restrict__ live, void *__restrict__ next) {
-    if (c->mode != BFS_PULL_DENSE) return;
-    using W = typename WordT<D>::T;
-    for (uint32_t I = blockIdx.x * blockDim.x + threadIdx.x; I < ntr; I += gridDim.x * blockDim.x) {
-        const uint32_t keep = ~load_word<D>(visited, I) & load_word<D>(live, I);
-        if (!keep) continue;
-        const uint32_t t0 = trp[I], t1 = min(trp[I + 1], t0 + HEAD_TILES);
-        uint32_t acc = 0;
-        for (uint32_t t = t0; t < t1 && (acc & keep) != keep; t++) {
-            const uint32_t xw = load_word<D>(frontier, __ldg(tci + t));
-            if (!xw) continue;
-#pragma unroll
-            for (int r = 0; r < D; r++)
-                if (tiles[(size_t)t * D + r] & xw) acc |= 1u << r;
-        }
-        if (acc & keep) reinterpret_cast<W *>(next)[I] = (W)(acc & keep);
-    }
-}
-
-template <int D>
-__global__ void k_bfs_dense_list(BfsCtl *__restrict__ c, uint32_t n_loads, const uint4 *__restrict__ desc,
-                                 const void *__restrict__ visited, const void *__restrict__ live,
-                                 const void *__restrict__ next, uint32_t *__restrict__ alist) {
-    if (c->mode != BFS_PULL_DENSE) return;
-    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
-    const uint32_t lane = lane_id(), iters = (n_loads + stride - 1) / stride;
-    for (uint32_t it = 0; it < iters; it++) {
-        uint32_t k = tid + it * stride;
-        bool act = false;
-        if (k < n_loads) {
-            uint32_t ra = desc[k].x, rb = desc[k + 1].x;
-            for (uint32_t r = ra; r <= rb && !act; r++)
-                act = (~load_word<D>(visited, r) & load_word<D>(live, r) & ~load_word<D>(next, r)) != 0;
         }
         uint32_t bal = __ballot_sync(0xffffffffu, act);
         if (!bal) continue;
@@ -1050,11 +907,6 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     Buf<uint32_t> alist(std::max<uint32_t>(n_loads, 1), s);
     const double alpha = bfs_alpha();
     const bool trace = getenv("B2SR_BFS_TRACE") != nullptr;
-    // B2SR_BFS_HEAD=1: head pass + listed stream for dense-frontier pulls
-    // (measured slower at R-MAT s22 d=4: 296 vs 249 us for that level -- a
-    // load stays listed while any of its rows misses a parent)
-    const char *he = getenv("B2SR_BFS_HEAD");
-    const int head = he && he[0] == '1';
     LAUNCH(k_fill_f64, grid_for(n), 256, 0, s, d_levels, (size_t)n, HUGE_VAL);
     CK(cudaMemsetAsync(visited.p, 0, n16 * 16, s));
     CK(cudaMemsetAsync(fb.p, 0, n16 * 16, s));
@@ -1068,7 +920,7 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     snaps.reset();
     // level 0 = {src}: visited, levels, counters, the push list of level 1 and its plan
     LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)fb.p, (uint4 *)visited.p, d_levels, 0.0, ta, at->trp,
-           (const uint4 *)at->live, ctl.p, nullptr, 0, alpha, (unsigned long long)at->num_tiles, a ? 1 : 0, head,
+           (const uint4 *)at->live, ctl.p, nullptr, 0, alpha, (unsigned long long)at->num_tiles, a ? 1 : 0,
            snaps.dev, 0u);
     void *frontier = fb.p, *next = fa.p;
     const unsigned gp = (unsigned)num_sms() * 8;
@@ -1077,15 +929,10 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     for (uint32_t L = 1;; L++) {
         LAUNCH(k_bfs_prep<D>, gp, 256, 0, s, ctl.p, ntr, ta, list.p, hv.S, hv.cols, frontier, hx.p, n_loads, desc,
                visited.p, at->live, alist.p);
-        if (head) {
-            LAUNCH(k_bfs_head<D>, grid_for(ntr), 256, 0, s, ctl.p, ntr, at->trp, at->tci,
-                   (const typename WordT<D>::T *)at->tiles, frontier, visited.p, at->live, next);
-            LAUNCH(k_bfs_dense_list<D>, gp, 256, 0, s, ctl.p, n_loads, desc, visited.p, at->live, next, alist.p);
-        }
         launch_bfs_level(at, a, ctl.p, list.p, alist.p, hx.p, hb, frontier, next, s);
         LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L, ta,
                at->trp, (const uint4 *)at->live, ctl.p, (uint4 *)frontier, 1, alpha,
-               (unsigned long long)at->num_tiles, a ? 1 : 0, head, snaps.dev, L);
+               (unsigned long long)at->num_tiles, a ? 1 : 0, snaps.dev, L);
         std::swap(frontier, next);
         // the host checks level L-LOOKAHEAD's outcome while levels up to L are
         // already enqueued (levels past the end are gated no-ops): no poll

@@ -8,12 +8,13 @@ kernel through the C ABI:
   =========================  ====================================  ==============
   reference                  kernel (csrc/)                        output
   =========================  ====================================  ==============
-  bmv_bin_bin_bin   :97      K4 k_bmv_bbb  (bmv.cu)                BitVector
+  bmv_bin_bin_bin   :97      K4 k_bmv_bbb_stream (bmv_stream.cu)   BitVector
   bmv_bin_bin_full  :118     K5 k_bmv_bbf  (bmv.cu)                float64[n]
-  bmv_bin_full_full :140     K6 k_bmv_bff  (bmv.cu)                float64[n]
+  bmv_bin_full_full :140     K6 k_bff_rows + k_vlong_* (bmv_bff.cu, float64[n]
+                                bmv_vlong.cu)
   *_masked          :219-249 same kernels, keep fused at store
   bmm_bin_bin_sum   :298     K7 colsum/rowdeg dot (bmm.cu)         int
-  bmm_..._masked    :323     K8 k_bmm_masked (bmm.cu)              int
+  bmm_..._masked    :323     K8 k_bmm_masked_items (bmm.cu)        int
   =========================  ====================================  ==============
 
 ``workers`` is accepted and validated for signature parity

@@ -63,10 +63,11 @@ def test_scale20_properties():
         assert np.abs(a[fin] - bb[fin]).max() <= 1 and lv[src] == 0
 
 
-@pytest.mark.parametrize("d", [4, 32])
-def test_scale21_blocked_path_against_oracle(d):
-    """n = 2^21 > one shared-memory strip: exercises the column-strip blocked
-    bbb and BFS-pull kernels (P = 2 strips) against the C oracle."""
+@pytest.mark.parametrize("d", [4, 8, 32])
+def test_scale21_against_oracle(d):
+    """n = 2^21: more tile columns than the shared-memory hot cache holds at
+    d = 4, 8 (hot and cold x gathers in the flat stream), masked bbb and BFS
+    against the C oracle."""
     scale = 21
     n = 1 << scale
     csr = rmat.rmat_csr(scale, 8, seed=2)
@@ -83,13 +84,6 @@ def test_scale21_blocked_path_against_oracle(d):
     lv, it = orc.bfs(ref, src)
     r = b2.bfs(m, src)
     assert r.per_vertex.tobytes() == lv.tobytes() and r.iterations == it
-
-
-def test_scale21_blocked_kernels_opt_in(monkeypatch):
-    """The opt-in column-strip blocked kernels (B2SR_BLOCKED=1) give the same bits."""
-    monkeypatch.setenv("B2SR_BLOCKED", "1")
-    test_scale21_blocked_path_against_oracle(4)
-    test_scale21_blocked_path_against_oracle(16)
 
 
 def _dist_bfs_worker(rank, world, port, scale, d, src, q):
