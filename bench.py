@@ -349,41 +349,41 @@ def run_ours(args, rank, world, local_rank):
     hm._trp, hm._tci, hm._tiles = pinned[0][1], pinned[1][1], pinned[2][1]
     e2e_steps = max(3, min(args.steps, 6))
     e2e_edges = 0
-    for r in roots[:1]:
-        hm2 = _fresh(hm)
-        b2.bfs(hm2, r)
+    # untimed warm-up of the same loop (the result arrays are kept alive, as in
+    # the timed loop, so the pinned result pool reaches its steady state)
+    warm = [b2.bfs(_fresh(hm), r).per_vertex for r in roots[: max(args.warmup, e2e_steps)]]
+    del warm
     barrier()
     f0, f1 = ev(), ev()
     outs = []
     f0.record()
     for r in roots[args.warmup: args.warmup + e2e_steps]:
-        hm2 = _fresh(hm)  # no cached device mirror: H2D + transpose every step
+        hm2 = _fresh(hm)  # no cached device mirror or transpose: H2D every step
         outs.append(b2.bfs(hm2, r).per_vertex)
     f1.record()
     barrier()
     e2e_ms = f0.elapsed_time(f1)
     e2e_edges = sum(traversed_edges(lv, deg) for lv in outs)
+    del outs
     # phase breakdown of one extra call (not part of the value)
-    ph = [ev() for _ in range(5)]
+    ph = [ev() for _ in range(4)]
     hm2 = _fresh(hm)
     ph[0].record()
     hh = hm2.handle()
     ph[1].record()
-    hat = b2.b2sr_transpose(hm2).handle()
-    ph[2].record()
     lvd = dev.empty_bytes(8 * n)
-    _capi.call("b2sr_bfs", hh.ptr, hat.ptr, roots[args.warmup], dev.ptr(lvd), ctypes.addressof(it), sp)
+    _capi.call("b2sr_bfs", hh.ptr, None, roots[args.warmup], dev.ptr(lvd), ctypes.addressof(it), sp)
+    ph[2].record()
+    lv_host = dev.to_host(lvd, np.float64, n)
     ph[3].record()
-    dev.to_host(lvd, np.float64, n)
-    ph[4].record()
     torch.cuda.synchronize()
-    breakdown = {k: round(ph[i].elapsed_time(ph[i + 1]), 3)
-                 for i, k in enumerate(("h2d", "transpose", "bfs", "d2h"))}
-    del hh, hat, hm2
+    breakdown = {k: round(ph[i].elapsed_time(ph[i + 1]), 3) for i, k in enumerate(("h2d", "bfs", "d2h"))}
+    del hh, hm2, lv_host
     e2e = {"value": round(e2e_edges / (e2e_ms / 1e3) / 1e9, 4), "unit": "GTEPS",
            "h2d_bytes_per_step": int(sum(a.nbytes for a in host)), "d2h_bytes_per_step": 8 * n,
            "ms_per_step": round(e2e_ms / e2e_steps, 3),
-           "includes": "H2D of B2SR arrays from pinned memory, transpose, BFS, D2H of levels",
+           "includes": "H2D of B2SR arrays from pinned memory, BFS (a fresh matrix has no transpose: "
+                       "push-only levels), D2H of levels into the pinned result pool",
            "breakdown_ms": breakdown}
 
     # ---- TC on the scale-20 graph ----
@@ -424,6 +424,7 @@ def _fresh(hm):
     c._h = None
     c._transpose = None
     c._nodiag = None
+    c._bfs_push = 0
     return c
 
 

@@ -133,7 +133,9 @@ int b2sr_bmm_sum_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2
  * algorithms.py:78 does).  With a != NULL the driver is direction-optimizing:
  * small frontiers push over a (top-down), large ones pull over at
  * (bottom-up, masked bbb with early exit); both produce the identical
- * next frontier.  a == NULL -> pull only.  levels f64[n] (+inf unreachable);
+ * next frontier.  a == NULL -> pull only.  at == NULL -> push only over a
+ * (d = 4, 8; no transpose needed: for a matrix that has none yet).
+ * levels f64[n] (+inf unreachable);
  * *iterations counts the final empty sweep like the reference.  Env
  * B2SR_BFS_ALPHA tunes the switch, B2SR_BFS_TRACE logs levels. */
 int b2sr_bfs(const b2sr_matrix *a, const b2sr_matrix *at, uint32_t src, double *d_levels, int64_t *iterations,

@@ -6,6 +6,8 @@ matrix data goes through libb2sr_sm100.so.
 
 from __future__ import annotations
 
+import os
+import sys
 import threading
 import warnings
 
@@ -78,30 +80,96 @@ def zeros_bytes(nbytes: int):
     return t.zeros((int(nbytes) + 15) // 16 * 16 or 16, dtype=t.uint8, device=device())
 
 
+class _PinnedBlock:
+    __slots__ = ("tensor", "root", "size")
+
+    def __init__(self, size: int):
+        t = torch()
+        self.tensor = t.empty(size, dtype=t.uint8, pin_memory=True)
+        self.root = self.tensor.numpy()  # every array handed out is a view of root
+        self.size = size
+
+    def free(self) -> bool:
+        # references: this attribute + getrefcount's argument; any live result
+        # array (or a view of one) holds one more -- numpy collapses view bases
+        return sys.getrefcount(self.root) <= 2
+
+
+class _PinnedPool:
+    """Page-locked result buffers, recycled once the caller drops the array.
+
+    A device->host result copied straight into page-locked memory runs at the
+    PCIe rate; copying it into a fresh numpy array afterwards costs several
+    times more (first-touch page faults + a host memcpy).  So result arrays
+    ARE views of pinned blocks: a block is reused when no array or view of it
+    is alive any more.  Bounded (B2SR_PINNED_POOL_MB, default 2048); past the
+    bound, results go through one reused staging buffer instead.
+    """
+
+    GRAIN = 2 << 20
+
+    def __init__(self):
+        self.blocks: list[_PinnedBlock] = []
+        self.bytes = 0
+        self.cap = int(os.environ.get("B2SR_PINNED_POOL_MB", "2048")) << 20
+        self.lock = threading.Lock()
+
+    def lease(self, nbytes: int):
+        """A free block of at least nbytes (None: over the bound)."""
+        with self.lock:
+            best = None
+            for b in self.blocks:
+                if nbytes <= b.size <= 2 * nbytes + self.GRAIN and b.free() and (best is None or b.size < best.size):
+                    best = b
+            if best is not None:
+                return best
+            size = (nbytes + self.GRAIN - 1) // self.GRAIN * self.GRAIN
+            if self.bytes + size > self.cap:
+                for b in list(self.blocks):  # make room from free blocks of other sizes
+                    if self.bytes + size <= self.cap:
+                        break
+                    if b.free():
+                        self.blocks.remove(b)
+                        self.bytes -= b.size
+                if self.bytes + size > self.cap:
+                    return None
+            b = _PinnedBlock(size)
+            self.blocks.append(b)
+            self.bytes += size
+            return b
+
+
+_pool = _PinnedPool()
+
+
 def to_host(tensor, dtype, count: int) -> np.ndarray:
     """Copy the first ``count`` elements of ``dtype`` out of a device buffer.
 
-    One DMA into a reused page-locked bounce buffer, then a host copy into the
-    fresh result array (measured: a fresh pinned allocation per call costs
-    twice as much; the host copy is dominated by first-touch page faults of
-    the result, which any new array pays).
+    One DMA into a page-locked block of the result pool; the returned array
+    is a view of that block (see _PinnedPool).  Without a block (pool bound
+    reached): DMA into a reused staging buffer, then a host copy.
     """
     global _bounce
     t = torch()
     dt = np.dtype(dtype)
     nbytes = count * dt.itemsize
-    out = np.empty(count, dt)
     if nbytes == 0:
-        return out
+        return np.empty(count, dt)
+    src = tensor.detach().view(t.uint8)[:nbytes]
+    blk = _pool.lease(nbytes)
+    if blk is not None:
+        blk.tensor[:nbytes].copy_(src)
+        return blk.root[:nbytes].view(dt)
+    out = np.empty(count, dt)
     with _bounce_lock:
         if _bounce is None or _bounce.numel() < nbytes:
             _bounce = t.empty(max(nbytes, 1 << 20), dtype=t.uint8, pin_memory=True)
-        _bounce[:nbytes].copy_(tensor.detach().view(t.uint8)[:nbytes])
+        _bounce[:nbytes].copy_(src)
         out.view(np.uint8)[:] = _bounce[:nbytes].numpy()
     return out
 
 
-_bounce = None  # reusable page-locked staging buffer for device -> host copies
+_bounce = None  # staging buffer for results past the pool bound
 _bounce_lock = threading.Lock()
 
 

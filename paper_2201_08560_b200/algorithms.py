@@ -7,8 +7,8 @@ buffers and turns the final vector into the reference's ``AlgoResult``.
 =====================  ===========================================  =================
 reference              B200 path                                    parity
 =====================  ===========================================  =================
-bfs :75-93             transpose (K3) + masked pull sweeps          bit-exact levels,
-                                                                    same iterations
+bfs :75-93             push-only levels over a until transposed;    bit-exact levels,
+                       then K3 + direction-optimizing push/pull     same iterations
 sssp :104-124          tile-form diagonal drop + K3 + min-plus(1)   bit-exact, same
                                                                     iterations
 pagerank :127-163      K6 arithmetic (ascending-j order) + fused    bit-exact ranks and
@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -77,13 +78,35 @@ def _source(n: int, src) -> int:
     return src
 
 
+# BFS calls on a matrix without a transpose that run push-only before the
+# transpose is built: the transpose (K3 + pull plans) costs about as much as a
+# dozen push-only traversals and saves ~half of each later one (ski rental).
+BFS_PUSH_CALLS = int(os.environ.get("B2SR_BFS_PUSH_CALLS", "8"))
+
+
+def _cached_transpose(a: B2srMatrix):
+    t = a._transpose
+    return t() if isinstance(t, weakref.ref) else t
+
+
 def bfs(a: B2srMatrix, src: int, *, workers: int | None = None) -> AlgoResult:
-    """Level-synchronous BFS; hop counts, +inf where unreachable."""
+    """Level-synchronous BFS; hop counts, +inf where unreachable.
+
+    The reference transposes on every call (algorithms.py:78).  Here the
+    transpose is cached on the matrix; until one exists (and for the first
+    BFS_PUSH_CALLS calls) d = 4/8 matrices run push-only levels over ``a``,
+    which need no transpose at all.  Levels and iterations are identical.
+    """
     src = _source(a.n, src)
     resolve_workers(workers)
-    at = b2sr_transpose(a)
     levels = dev.empty_bytes(8 * a.n)
     it = ctypes.c_int64()
+    at = _cached_transpose(a)
+    if at is None and a.dim <= 8 and a._bfs_push < BFS_PUSH_CALLS:
+        a._bfs_push += 1
+        _capi.call("b2sr_bfs", a.handle().ptr, None, src, dev.ptr(levels), ctypes.addressof(it), dev.stream())
+        return AlgoResult(per_vertex=dev.to_host(levels, np.float64, a.n), iterations=int(it.value), converged=True)
+    at = at if at is not None else b2sr_transpose(a)
     _capi.call("b2sr_bfs", a.handle().ptr, at.handle().ptr, src, dev.ptr(levels), ctypes.addressof(it), dev.stream())
     return AlgoResult(per_vertex=dev.to_host(levels, np.float64, a.n), iterations=int(it.value), converged=True)
 

@@ -44,5 +44,9 @@ struct BfsSnap {
 void launch_bfs_level(b2sr_matrix *at, const b2sr_matrix *a, BfsCtl *ctl, const uint2 *push_list,
                       const uint32_t *active_list, const void *hx, size_t hb, const void *frontier, void *next,
                       cudaStream_t s);
+// Top-down level of the push-only BFS (no transpose; d = 4, 8): the listed
+// chunks of a, bits of visited vertices dropped before the scatter.
+void launch_bfs_push_level(const b2sr_matrix *a, const BfsCtl *ctl, const uint2 *push_list, const void *frontier,
+                           const void *visited, void *next, cudaStream_t s);
 
 }  // namespace b2sr

@@ -341,11 +341,13 @@ __global__ void __launch_bounds__(NT, 1)
 // lane holds TPL consecutive tiles of one 128-bit load; the bit-rows of the
 // frontier word select the tile bytes, folded to the column word and OR'd into
 // next[col] (fire-and-forget RED; visited vertices are masked by the update).
+// With `visited`, bits of already visited vertices are dropped before the RED:
+// on dense levels that skips most atomics, hub columns (reached early) included.
 template <int D>
 __device__ __forceinline__ void push_entries(uint32_t n_entries, const uint2 *__restrict__ plist,
                                              const uint32_t *__restrict__ trp, const uint32_t *__restrict__ tci,
                                              const uint8_t *__restrict__ tiles, const void *__restrict__ frontier,
-                                             void *__restrict__ next) {
+                                             void *__restrict__ next, const void *__restrict__ visited = nullptr) {
     using G = Geo<D>;
     constexpr int TPL = G::TPL;
     const uint32_t lane = lane_id();
@@ -390,7 +392,9 @@ __device__ __forceinline__ void push_entries(uint32_t n_entries, const uint2 *__
                         w |= w >> 16;
                         m = (w | (w >> 8)) & 0xFFu;
                     }
-                    if (m && tl + j >= t0 && tl + j < t1) atomic_or_word<D>(next, c[u][j], m);
+                    if (!(tl + j >= t0 && tl + j < t1)) m = 0;  // neighbours' / padding tiles of the load
+                    if (m && visited) m &= ~load_word<D>(visited, c[u][j]);
+                    if (m) atomic_or_word<D>(next, c[u][j], m);
                 }
             }
         }
@@ -426,6 +430,27 @@ __global__ void __launch_bounds__(NT, 1)
     if (listed) bbb_stream<D, true>(p0, p1, n_loads, T, alist, desc, trp, tiles, tci2, gx, next);
     else if (ctl->sparse) bbb_stream<D, false, XHot<D>, true>(p0, p1, n_loads, T, nullptr, desc, trp, tiles, tci2, gx, next);
     else bbb_stream<D, false>(p0, p1, n_loads, T, nullptr, desc, trp, tiles, tci2, gx, next);
+}
+
+// Push-only level (BFS without a transpose): every level top-down over a.
+template <int D>
+__global__ void __launch_bounds__(256) k_bfs_push_level(const BfsCtl *__restrict__ ctl, const uint2 *__restrict__ plist,
+                                                        const uint32_t *__restrict__ trp, const uint32_t *__restrict__ tci,
+                                                        const uint8_t *__restrict__ tiles, const void *__restrict__ frontier,
+                                                        const void *__restrict__ visited, void *__restrict__ next) {
+    if (ctl->mode != BFS_PUSH) return;
+    push_entries<D>(ctl->list_n, plist, trp, tci, tiles, frontier, next, visited);
+}
+
+void launch_bfs_push_level(const b2sr_matrix *a, const BfsCtl *ctl, const uint2 *push_list, const void *frontier,
+                           const void *visited, void *next, cudaStream_t s) {
+    const unsigned g = (unsigned)num_sms() * 8;
+    if (a->dim == 4)
+        LAUNCH(k_bfs_push_level<4>, g, 256, 0, s, ctl, push_list, a->trp, a->tci, (const uint8_t *)a->tiles, frontier,
+               visited, next);
+    else
+        LAUNCH(k_bfs_push_level<8>, g, 256, 0, s, ctl, push_list, a->trp, a->tci, (const uint8_t *)a->tiles, frontier,
+               visited, next);
 }
 
 void launch_bfs_level(b2sr_matrix *at, const b2sr_matrix *a, BfsCtl *ctl, const uint2 *push_list,

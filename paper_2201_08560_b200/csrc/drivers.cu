@@ -720,7 +720,8 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
         uint4 nv = next[c];
         if (zero_buf) zero_buf[c] = make_uint4(0, 0, 0, 0);  // recycled as the next level's output
         if (!(nv.x | nv.y | nv.z | nv.w)) continue;
-        const uint4 vv = visited[c], lv = live_at[c];
+        const uint4 vv = visited[c];
+        const uint4 lv = live_at ? live_at[c] : make_uint4(~0u, ~0u, ~0u, ~0u);
         if (mask) {
             uint4 mv = make_uint4(nv.x & ~vv.x & lv.x, nv.y & ~vv.y & lv.y, nv.z & ~vv.z & lv.z, nv.w & ~vv.w & lv.w);
             if (mv.x != nv.x || mv.y != nv.y || mv.z != nv.z || mv.w != nv.w) next[c] = mv;
@@ -744,7 +745,7 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
                 levels[(size_t)I * D + kk] = level;
             }
             const uint32_t old = vw[j], l = lw[j];
-            if ((~old & l) && !(~(old | w) & l)) rt += __ldg(trp_at + I + 1) - __ldg(trp_at + I);
+            if (trp_at && (~old & l) && !(~(old | w) & l)) rt += __ldg(trp_at + I + 1) - __ldg(trp_at + I);
             if (trp_a) ft += __ldg(trp_a + I + 1) - __ldg(trp_a + I);
         }
     }
@@ -959,6 +960,67 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     *iterations = sweeps;
 }
 
+// BFS without a transpose (b2sr_bfs with at == NULL; d = 4, 8): every level
+// top-down over a -- each tile row is read once per level its frontier bits
+// fall in, and visited targets are filtered before the scatter.  A matrix that
+// has no transpose yet pays the traversal only, not the (~10x longer) K3
+// transpose the pull levels need; the Python driver switches to the
+// direction-optimizing path once the transpose exists.
+template <int D>
+static void bfs_push_only(const b2sr_matrix *a, uint32_t src, double *d_levels, int64_t *iterations,
+                          cudaStream_t s) {
+    const uint32_t n = a->n, ntr = a->ntr;
+    const size_t vb = padded_vec_bytes(ntr, D);
+    const uint32_t n16 = (uint32_t)((vb + 15) / 16);
+    Buf<uint8_t> visited(n16 * 16, s), fa(n16 * 16, s), fb(n16 * 16, s);
+    Buf<BfsCtl> ctl(1, s);
+    Buf<uint2> list((size_t)ntr + a->num_tiles / PUSH_CH + 1, s);
+    const bool trace = getenv("B2SR_BFS_TRACE") != nullptr;
+    LAUNCH(k_fill_f64, grid_for(n), 256, 0, s, d_levels, (size_t)n, HUGE_VAL);
+    CK(cudaMemsetAsync(visited.p, 0, n16 * 16, s));
+    CK(cudaMemsetAsync(fb.p, 0, n16 * 16, s));
+    CK(cudaMemsetAsync(fa.p, 0, n16 * 16, s));
+    LAUNCH(k_bfs_seed, 1, 1, 0, s, src, (uint32_t)D, d_levels, fa.p, fb.p);
+    CK(cudaMemsetAsync(fa.p, 0, n16 * 16, s));
+    LAUNCH(k_bfs_ctl_init, 1, 1, 0, s, ctl.p, 1ull);  // alpha = 0 below: every level is a push
+    const unsigned gu = grid_for(ntr);
+    BfsSnapshots &snaps = bfs_snapshots();
+    snaps.reset();
+    LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)fb.p, (uint4 *)visited.p, d_levels, 0.0, a->trp, nullptr,
+           nullptr, ctl.p, nullptr, 0, 0.0, (unsigned long long)a->num_tiles, 1, snaps.dev, 0u);
+    void *frontier = fb.p, *next = fa.p;
+    const unsigned gp = (unsigned)num_sms() * 8;
+    int done = 0;
+    long long sweeps = 0;
+    for (uint32_t L = 1;; L++) {
+        LAUNCH(k_bfs_prep<D>, gp, 256, 0, s, ctl.p, ntr, a->trp, list.p, 0u, nullptr, frontier, nullptr, 0u, nullptr,
+               visited.p, nullptr, nullptr);
+        launch_bfs_push_level(a, ctl.p, list.p, frontier, visited.p, next, s);
+        LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L, a->trp,
+               nullptr, nullptr, ctl.p, (uint4 *)frontier, 1, 0.0, (unsigned long long)a->num_tiles, 1, snaps.dev, L);
+        std::swap(frontier, next);
+        if (trace || L > LOOKAHEAD) {
+            const uint32_t Lc = trace ? L : L - LOOKAHEAD;
+            const volatile BfsSnap *sn = snaps.slot(Lc);
+            while (sn->level != Lc) {
+                const cudaError_t q = cudaStreamQuery(s);
+                if (q != cudaErrorNotReady && sn->level != Lc) {
+                    CK(q);
+                    B2SR_THROW(B2SR_ECUDA, "BFS level %u finished without its outcome", Lc);
+                }
+                std::this_thread::yield();
+            }
+            done = sn->done;
+            sweeps = sn->sweeps;
+            if (trace) fprintf(stderr, "[b2sr bfs push] after level %u: done=%d sweeps=%lld\n", Lc, done, sweeps);
+            if (done) break;
+        }
+        if (L > n + 2 + LOOKAHEAD) B2SR_THROW(B2SR_ENOCONV, "BFS failed to drain its frontier");
+    }
+    CK(cudaStreamSynchronize(s));
+    *iterations = sweeps;
+}
+
 static bool bfs_devctl_enabled(const b2sr_matrix *at) {
     const char *e = getenv("B2SR_BFS_DEVCTL");  // B2SR_BFS_DEVCTL=0: host-controlled levels (A/B)
     return pull_stream(at) && !(e && e[0] == '0');
@@ -976,6 +1038,15 @@ int b2sr_bfs(const b2sr_matrix *a_c, const b2sr_matrix *at_c, uint32_t src, doub
     cudaStream_t s = (cudaStream_t)stream;
     b2sr_matrix *at = const_cast<b2sr_matrix *>(at_c);
     const b2sr_matrix *a = a_c;
+    if (!at) {  // no transpose: push-only levels over a
+        if (!a) B2SR_THROW(B2SR_EINVAL, "bfs needs a or its transpose");
+        if (a->row0 != 0 || a->ntr != tile_rows(a->n, a->dim)) B2SR_THROW(B2SR_EINVAL, "bfs needs a full matrix");
+        if (a->dim > 8) B2SR_THROW(B2SR_EINVAL, "push-only bfs supports tile dims 4 and 8");
+        if (src >= a->n) B2SR_THROW(B2SR_EINVAL, "source vertex %u out of range for n=%u", src, a->n);
+        if (a->dim == 4) bfs_push_only<4>(a, src, d_levels, iterations, s);
+        else bfs_push_only<8>(a, src, d_levels, iterations, s);
+        return B2SR_OK;
+    }
     if (at->row0 != 0 || at->ntr != tile_rows(at->n, at->dim)) B2SR_THROW(B2SR_EINVAL, "bfs needs a full matrix");
     if (a && (a->n != at->n || a->dim != at->dim || a->row0 != 0 || a->ntr != at->ntr))
         B2SR_THROW(B2SR_EINVAL, "a and at must be the same full matrix and its transpose");

@@ -298,7 +298,7 @@ class B2srMatrix:
     """
 
     __slots__ = ("n", "tile_dim", "_trp", "_tci", "_tiles", "_h", "_num_tiles", "_transpose", "_nodiag",
-                 "__weakref__")
+                 "_bfs_push", "__weakref__")
 
     def __init__(self, n, tile_dim, tile_row_ptr, tile_col_ind, bit_tiles):
         n = int(n)
@@ -340,6 +340,7 @@ class B2srMatrix:
         self._num_tiles = T
         self._transpose = None
         self._nodiag = None
+        self._bfs_push = 0  # push-only BFS calls made without a transpose (algorithms.bfs)
 
     @classmethod
     def _wrap(cls, h: _Handle) -> "B2srMatrix":
@@ -351,6 +352,7 @@ class B2srMatrix:
         self._num_tiles = h.num_tiles
         self._transpose = None
         self._nodiag = None
+        self._bfs_push = 0  # push-only BFS calls made without a transpose (algorithms.bfs)
         return self
 
     # device mirror ---------------------------------------------------

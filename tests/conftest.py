@@ -55,3 +55,15 @@ def random_pattern(rng, n, density, symmetric=False):
     rp = np.zeros(n + 1, np.int64)
     np.add.at(rp, r + 1, 1)
     return np.cumsum(rp).astype(np.uint32), c.astype(np.uint32)
+
+
+def bfs_all_paths(b2, m, src):
+    """bfs() through both device paths: push-only levels on a matrix without a
+    transpose (d = 4, 8), then the direction-optimizing push/pull driver once
+    the transpose is cached.  Both must agree bit for bit; returns the latter."""
+    first = b2.bfs(m, src)
+    b2.b2sr_transpose(m)  # cached on m: the next call takes the transposed path
+    second = b2.bfs(m, src)
+    assert first.per_vertex.tobytes() == second.per_vertex.tobytes()
+    assert first.iterations == second.iterations
+    return second

@@ -6,6 +6,7 @@ import pytest
 
 import paper_2201_08560_b200 as b2
 from paper_2201_08560_b200 import rmat
+from conftest import bfs_all_paths
 from oracle import oracle as orc
 
 pytestmark = pytest.mark.gpu
@@ -54,7 +55,7 @@ def test_scale20_properties():
         assert b2.bmm_bin_bin_sum(m, m) == int((deg * deg).sum()) if n ** 3 < 2 ** 63 else True
         # BFS levels: |level(u) - level(v)| <= 1 on every edge; src level 0
         src = int(np.argmax(deg))
-        lv = b2.bfs(m, src).per_vertex
+        lv = bfs_all_paths(b2, m, src).per_vertex
         rows = np.repeat(np.arange(n), deg)
         cols = csr.col_ind.astype(np.int64)
         a, bb = lv[rows], lv[cols]
@@ -82,7 +83,7 @@ def test_scale21_against_oracle(d):
     assert np.array_equal(got.words, orc.bmv_bbb(ref, xw, kw))
     src = int(np.argmax(np.diff(rp.astype(np.int64))))
     lv, it = orc.bfs(ref, src)
-    r = b2.bfs(m, src)
+    r = bfs_all_paths(b2, m, src)
     assert r.per_vertex.tobytes() == lv.tobytes() and r.iterations == it
 
 
