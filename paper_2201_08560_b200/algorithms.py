@@ -9,8 +9,8 @@ reference              B200 path                                    parity
 =====================  ===========================================  =================
 bfs :75-93             push-only levels over a until transposed;    bit-exact levels,
                        then K3 + direction-optimizing push/pull     same iterations
-sssp :104-124          tile-form diagonal drop + K3 + min-plus(1)   bit-exact, same
-                                                                    iterations
+sssp :104-124          BFS levels (= unit-weight distances); or     bit-exact, same
+                       diagonal drop + K3 + min-plus(1) rounds      iterations
 pagerank :127-163      K6 arithmetic (ascending-j order) + fused    bit-exact ranks and
                        update + numpy-exact pairwise delta          iterations
 connected_components   K6 min-plus(0) + parallel hook/shortcut      bit-exact labels;
@@ -112,9 +112,27 @@ def bfs(a: B2srMatrix, src: int, *, workers: int | None = None) -> AlgoResult:
 
 
 def sssp(a: B2srMatrix, src: int, *, workers: int | None = None) -> AlgoResult:
-    """Unit-weight shortest paths by min-plus relaxation (self-loops dropped)."""
+    """Unit-weight shortest paths (algorithms.py:104-124).
+
+    The reference relaxes ``dist = min(dist, bff(at, dist, min_plus(1)))``
+    until a round changes nothing (at most n-1 rounds).  With unit weights
+    round k settles exactly the vertices at hop distance k, so the result is
+    the BFS level vector (self-loops never shorten a path) and the round count
+    is min(BFS sweeps, n-1): the BFS driver computes the same bits at BFS
+    cost.  ``B2SR_SSSP=relax`` runs the min-plus relaxation driver instead
+    (tests check both against the reference's vectors).
+    """
     src = _source(a.n, src)
     resolve_workers(workers)
+    if os.environ.get("B2SR_SSSP", "bfs") == "relax":
+        return _sssp_relax(a, src)
+    r = bfs(a, src)
+    return AlgoResult(per_vertex=r.per_vertex, iterations=min(r.iterations, a.n - 1), converged=True)
+
+
+def _sssp_relax(a: B2srMatrix, src: int) -> AlgoResult:
+    """The reference's loop on the device: drop the diagonal, transpose, then
+    K6 min-plus(1) rounds with a fused np.minimum / changed flag."""
     at = b2sr_transpose(drop_diagonal(a))
     dist = dev.empty_bytes(8 * a.n)
     it = ctypes.c_int64()
