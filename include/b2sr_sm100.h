@@ -69,6 +69,13 @@ int b2sr_last_kernel_ms(float *ms);
  * K1 (segmented tile-row count + scan) and K2 (merge/pack) kernels. */
 int b2sr_from_csr(uint32_t n, uint32_t dim, const uint32_t *d_row_ptr, const uint32_t *d_col_ind,
                   uint64_t nnz, void *stream, b2sr_matrix **out);
+/* sample_profile (profile.py:73-127), counting step: over the m sampled
+ * tile rows d_rows[] (ascending, distinct, < ceil(n/dim)) of a device CSR,
+ * the tiles they would store at width dim (*tiles, the K1 merge count) and
+ * their CSR entries (*nnz).  Sample selection and the estimates stay with
+ * the caller (they are defined by numpy's generator). */
+int b2sr_profile_rows(uint32_t n, uint32_t dim, const uint32_t *d_row_ptr, const uint32_t *d_col_ind,
+                      const uint32_t *d_rows, uint32_t m, uint64_t *tiles, uint64_t *nnz, void *stream);
 /* Adopt existing arrays (already validated on the host, e.g. a B2srMatrix
  * built by the caller): copies from host pointers into a new device matrix. */
 int b2sr_from_host(uint32_t n, uint32_t dim, const uint32_t *h_trp, const uint32_t *h_tci,

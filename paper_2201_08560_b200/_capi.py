@@ -30,6 +30,7 @@ SIGNATURES = {
     "b2sr_launch_count": [],
     "b2sr_from_csr": [u32, u32, P, P, u64, P, PP],
     "b2sr_from_host": [u32, u32, P, P, P, u64, P, PP],
+    "b2sr_profile_rows": [u32, u32, P, P, P, u32, P, P, P],
     "b2sr_free": [P],
     "b2sr_info": [P, P, P, P, P],
     "b2sr_arrays": [P, P, P, P],

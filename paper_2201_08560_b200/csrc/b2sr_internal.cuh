@@ -186,6 +186,8 @@ bool hot_enabled(int dim);
 bool stream_enabled(int dim);
 // visited != null: BFS pull (y &= ~visited & live instead of keep)
 // active_only (with visited): only the loads that hold a row with an unvisited live vertex
+// K5 bbf (bmv.cu): y f64 per local row
+void launch_bbf(b2sr_matrix *m, const void *x, const void *keep, double *y, cudaStream_t s);
 void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaStream_t s,
                        const void *visited = nullptr, bool active_only = false, bool lazy = false);
 void free_stream(void *plan);

@@ -1,8 +1,9 @@
 // K7/K8: bin-SpGEMM reductions (replaces kernels.py:271-367).
 //
-// bmm_bin_bin_sum: sum_ij (A B)_ij = sum_k colsum_A(k) * rowdeg_B(k), an
-// O(T) pass (the reference's per-pair colpop*rowpop sum regrouped by k;
-// integer arithmetic, so the regrouping is exact).
+// bmm_bin_bin_sum: sum_ij (A B)_ij = sum_k colsum_A(k) * rowdeg_B(k)
+// = sum over A's set bits (i,k) of rowdeg_B(k): K5 for rowdeg_B, then one
+// coalesced pass over A's tile bytes (the reference's per-pair colpop*rowpop sum
+// regrouped by k; integer arithmetic, so the regrouping is exact).
 //
 // bmm_bin_bin_sum_masked with B supplied transposed (Bt): for every stored
 // mask tile (I,J) the tile columns of A's row I and Bt's row J are
@@ -16,33 +17,47 @@
 
 namespace b2sr {
 
+// sum(A B) = 1^T A (B 1) = sum over the set bits (i, k) of A of rowdeg_B(k).
+// rowdeg_B = K5 bbf of B with x = all ones.  The gather streams A's tile
+// array as raw 16-byte lane loads (512 B per warp, coalesced whatever the
+// width); every 32-bit word lies inside one tile, whose column K gives the
+// D row degrees the word's bits index.
 template <int D>
-__global__ void k_colsum_rowdeg(uint64_t T, const uint32_t *__restrict__ rowid, const uint32_t *__restrict__ tci,
-                                const typename WordT<D>::T *__restrict__ tiles, uint32_t *__restrict__ colsum,
-                                uint32_t *__restrict__ rowdeg) {
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < T; t += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t I = rowid[t], K = tci[t];
-#pragma unroll
-        for (int r = 0; r < D; r++) {
-            uint32_t w = tiles[t * D + r];
-            if (rowdeg && w) atomicAdd(rowdeg + (size_t)I * D + r, (uint32_t)__popc(w));
-            if (colsum) {
-                while (w) {
-                    int c = __ffs(w) - 1;
-                    w &= w - 1;
-                    atomicAdd(colsum + (size_t)K * D + c, 1u);
-                }
-            }
-        }
+__device__ __forceinline__ unsigned long long sum_word(uint32_t w, const uint32_t *__restrict__ tci,
+                                                       uint64_t byte, const double *__restrict__ rowdeg) {
+    constexpr uint32_t TB = D * (D == 32 ? 4 : (D == 16 ? 2 : 1));  // tile bytes
+    constexpr uint32_t CM = D == 32 ? 31u : (D == 16 ? 15u : 7u);   // bit -> column within the tile
+    unsigned long long acc = 0;
+    if (w) {
+        const double *x = rowdeg + (size_t)__ldg(tci + byte / TB) * D;
+        do {
+            acc += (unsigned long long)__ldg(x + ((__ffs(w) - 1) & CM));
+            w &= w - 1;
+        } while (w);
     }
+    return acc;
 }
 
-__global__ void k_dot_u32(size_t n, const uint32_t *a, const uint32_t *b, unsigned long long *out) {
+template <int D>
+__global__ void __launch_bounds__(256) k_bmm_sum_gather(uint64_t nbytes, const uint32_t *__restrict__ tci,
+                                                        const uint8_t *__restrict__ tiles,
+                                                        const double *__restrict__ rowdeg,
+                                                        unsigned long long *__restrict__ out) {
     unsigned long long acc = 0;
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-        acc += (unsigned long long)a[i] * b[i];
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x * 16;
+    for (uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) * 16; b < nbytes; b += stride) {
+        if (b + 16 <= nbytes) {
+            const uint4 v = ld_stream128(tiles + b);
+            acc += sum_word<D>(v.x, tci, b, rowdeg) + sum_word<D>(v.y, tci, b + 4, rowdeg) +
+                   sum_word<D>(v.z, tci, b + 8, rowdeg) + sum_word<D>(v.w, tci, b + 12, rowdeg);
+        } else {
+            for (uint64_t o = b; o < nbytes; o += 4)
+                acc += sum_word<D>(*reinterpret_cast<const uint32_t *>(tiles + o), tci, o, rowdeg);
+        }
+    }
+#pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+    if (lane_id() == 0 && acc) atomicAdd(out, acc);
 }
 
 static unsigned grid_for(uint64_t work) {
@@ -52,17 +67,12 @@ static unsigned grid_for(uint64_t work) {
 
 static void row_ids(const b2sr_matrix *m, uint32_t *rowid, cudaStream_t s) { launch_row_ids(m, rowid, s); }
 
-static void colsum_rowdeg(const b2sr_matrix *m, uint32_t *colsum, uint32_t *rowdeg, cudaStream_t s) {
-    if (!m->num_tiles) return;
-    Buf<uint32_t> rowid(m->num_tiles, s);
-    row_ids(m, rowid.p, s);
-    unsigned g = grid_for(m->num_tiles);
-    switch (m->dim) {
-        case 4: LAUNCH(k_colsum_rowdeg<4>, g, 256, 0, s, m->num_tiles, rowid.p, m->tci, (const uint8_t *)m->tiles, colsum, rowdeg); break;
-        case 8: LAUNCH(k_colsum_rowdeg<8>, g, 256, 0, s, m->num_tiles, rowid.p, m->tci, (const uint8_t *)m->tiles, colsum, rowdeg); break;
-        case 16: LAUNCH(k_colsum_rowdeg<16>, g, 256, 0, s, m->num_tiles, rowid.p, m->tci, (const uint16_t *)m->tiles, colsum, rowdeg); break;
-        default: LAUNCH(k_colsum_rowdeg<32>, g, 256, 0, s, m->num_tiles, rowid.p, m->tci, (const uint32_t *)m->tiles, colsum, rowdeg); break;
-    }
+template <int D>
+static void bmm_sum_gather(const b2sr_matrix *a, const double *rowdeg, unsigned long long *acc, cudaStream_t s) {
+    const uint64_t nbytes = a->num_tiles * (uint64_t)D * word_bytes(D);
+    if (nbytes)
+        LAUNCH(k_bmm_sum_gather<D>, grid_for((nbytes + 15) / 16), 256, 0, s, nbytes, a->tci,
+               (const uint8_t *)a->tiles, rowdeg, acc);
 }
 
 // ------------------------------------------------------------ masked
@@ -220,15 +230,21 @@ int b2sr_bmm_sum(const b2sr_matrix *a, const b2sr_matrix *b, int64_t *out, void 
     API_BEGIN
     cudaStream_t s = (cudaStream_t)stream;
     if (a->n != b->n || a->dim != b->dim) B2SR_THROW(B2SR_EINVAL, "operands must share n and tile width");
-    size_t rows = (size_t)tile_rows(a->n, a->dim) * a->dim;
-    Buf<uint32_t> colsum(rows, s), rowdeg(rows, s);
+    if (b->row0 || b->ntr != tile_rows(b->n, b->dim)) B2SR_THROW(B2SR_EINVAL, "B must be a full matrix");
+    const size_t rows = (size_t)tile_rows(a->n, a->dim) * a->dim;
+    const size_t vb = padded_vec_bytes(b->ntr, b->dim);
+    Buf<uint8_t> ones(vb, s);
+    Buf<double> rowdeg(rows, s);
     Buf<unsigned long long> acc(1, s);
-    CK(cudaMemsetAsync(colsum.p, 0, rows * 4, s));
-    CK(cudaMemsetAsync(rowdeg.p, 0, rows * 4, s));
+    CK(cudaMemsetAsync(ones.p, 0xFF, vb, s));  // bits past n meet no tile bits
     CK(cudaMemsetAsync(acc.p, 0, 8, s));
-    colsum_rowdeg(a, colsum.p, nullptr, s);
-    colsum_rowdeg(b, nullptr, rowdeg.p, s);
-    LAUNCH(k_dot_u32, grid_for(rows), 256, 0, s, rows, colsum.p, rowdeg.p, acc.p);
+    launch_bbf(const_cast<b2sr_matrix *>(b), ones.p, nullptr, rowdeg.p, s);
+    switch (a->dim) {
+        case 4: bmm_sum_gather<4>(a, rowdeg.p, acc.p, s); break;
+        case 8: bmm_sum_gather<8>(a, rowdeg.p, acc.p, s); break;
+        case 16: bmm_sum_gather<16>(a, rowdeg.p, acc.p, s); break;
+        default: bmm_sum_gather<32>(a, rowdeg.p, acc.p, s); break;
+    }
     *out = (int64_t)read_scalar(acc.p, s);
     API_END
 }

@@ -280,17 +280,20 @@ __global__ void __launch_bounds__(256) k_bmv_bbf(const WorkItem *__restrict__ it
 }
 
 // ------------------------------------------------------------ K6 plans
-constexpr uint32_t VLONG_ROW_TILES = 256;  // longer rows: bmv_vlong.cu (segmented scatter + fold)
+// Rows longer than this many tiles take bmv_vlong.cu (segmented scatter +
+// fold).  At d = 32 a tile row of 1024 tiles still holds only ~40 terms per
+// bit-row on R-MAT, so the group walk keeps more rows (s16: 0.59 -> 0.45 ms).
+static uint32_t vlong_row_tiles(int dim) { return dim == 32 ? 1024u : 256u; }
 
 // Row-length thresholds are fixed per matrix when its plan is built; the env
 // override exists so parity tests can push small matrices through both paths.
-static uint32_t vlong_thresh() {
+static uint32_t vlong_thresh(int dim) {
     const char *ev = getenv("B2SR_VLONG_TILES");
-    return ev ? (uint32_t)atoi(ev) : VLONG_ROW_TILES;
+    return ev ? (uint32_t)atoi(ev) : vlong_row_tiles(dim);
 }
 
 static void ensure_vlong(b2sr_matrix *m, cudaStream_t s) {
-    if (!m->vlong) m->vlong = build_vlong(m, vlong_thresh(), s);
+    if (!m->vlong) m->vlong = build_vlong(m, vlong_thresh(m->dim), s);
 }
 
 // ------------------------------------------------------------ used columns / scale
@@ -402,7 +405,7 @@ void launch_bff(const b2sr_matrix *m_, const double *x, int ring, double inc, co
                 cudaStream_t s) {
     b2sr_matrix *m = const_cast<b2sr_matrix *>(m_);
     ensure_vlong(m, s);
-    const uint32_t hi = vlong_thresh();
+    const uint32_t hi = vlong_thresh(m->dim);
     launch_bff_rows(m, x, ring, inc, keep, y, hi, s, /*plan_only=*/true);
     launch_vlong(m, x, ring, inc, keep, y, s, [&](cudaStream_t so) { launch_bff_rows(m, x, ring, inc, keep, y, hi, so); });
 }

@@ -188,9 +188,76 @@ b2sr_matrix *csr_to_b2sr_device(uint32_t n, uint32_t d, const uint32_t *row_ptr,
     return m;
 }
 
+// ------------------------------------------------------------ sampling profiler
+// sample_profile (profile.py:73-127): the tiles that the sampled tile rows
+// would store at width d, counted by the K1 merge loop over just those rows
+// (same chunked work items, so hub rows are split), plus their CSR entries.
+__global__ void k_prof_chunks(uint32_t n, uint32_t d, const uint32_t *rows, uint32_t m, const uint32_t *row_ptr,
+                              uint32_t *pcount, unsigned long long *nnz) {
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t e = 0;
+    if (i < m) {
+        uint64_t r0 = (uint64_t)rows[i] * d, r1 = min((uint64_t)n, r0 + d);
+        e = row_ptr[r1] - row_ptr[r0];
+        uint32_t p = (e + CONV_CHUNK - 1) / CONV_CHUNK;
+        pcount[i] = p ? p : 1u;
+    }
+    e = __reduce_add_sync(0xffffffffu, e);  // distinct rows: the sum is <= nnz < 2^32
+    if (lane_id() == 0 && e) atomicAdd(nnz, (unsigned long long)e);
+}
+
+__global__ void k_prof_items(uint32_t ntr, const uint32_t *rows, uint32_t m, const uint64_t *pofs, ConvItem *items) {
+    uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    uint64_t b = pofs[i];
+    uint32_t P = (uint32_t)(pofs[i + 1] - b);
+    for (uint32_t j = 0; j < P; j++)
+        items[b + j] = ConvItem{rows[i], (uint32_t)((uint64_t)j * ntr / P), (uint32_t)((uint64_t)(j + 1) * ntr / P), 0};
+}
+
+__global__ void k_sum_u32(uint32_t n, const uint32_t *v, unsigned long long *out) {
+    unsigned long long acc = 0;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) acc += v[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane_id() == 0 && acc) atomicAdd(out, acc);
+}
+
 }  // namespace b2sr
 
 using namespace b2sr;
+
+extern "C" int b2sr_profile_rows(uint32_t n, uint32_t dim, const uint32_t *d_row_ptr, const uint32_t *d_col_ind,
+                                 const uint32_t *d_rows, uint32_t m, uint64_t *tiles, uint64_t *nnz, void *stream) {
+    API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dim != 4 && dim != 8 && dim != 16 && dim != 32) B2SR_THROW(B2SR_EINVAL, "tile dim must be 4/8/16/32");
+    *tiles = 0;
+    *nnz = 0;
+    if (n == 0 || m == 0) return B2SR_OK;
+    const uint32_t ntr = tile_rows(n, dim);
+    Buf<uint32_t> pcount(m, s);
+    Buf<uint64_t> pofs((size_t)m + 1, s);
+    Buf<unsigned long long> acc(2, s);
+    CK(cudaMemsetAsync(acc.p, 0, 16, s));
+    LAUNCH(k_prof_chunks, (m + 255) / 256, 256, 0, s, n, dim, d_rows, m, d_row_ptr, pcount.p, acc.p + 1);
+    exclusive_scan_u32_to_u64(pcount.p, pofs.p, m, s);
+    uint64_t n_items64 = read_scalar(pofs.p + m, s);
+    if (n_items64 > 0xFFFFFFFFull) B2SR_THROW(B2SR_EINVAL, "too many profiling work items");
+    const uint32_t n_items = (uint32_t)n_items64;
+    Buf<ConvItem> items(n_items, s);
+    LAUNCH(k_prof_items, (m + 255) / 256, 256, 0, s, ntr, d_rows, m, pofs.p, items.p);
+    Buf<uint32_t> cnt(n_items, s);
+    conv_dispatch(dim, false, items.p, n_items, n, d_row_ptr, d_col_ind, nullptr, cnt.p, nullptr, nullptr, s);
+    unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_items + 255) / 256, (uint64_t)num_sms() * 8));
+    LAUNCH(k_sum_u32, g, 256, 0, s, n_items, cnt.p, acc.p);
+    unsigned long long h[2];
+    CK(cudaMemcpyAsync(h, acc.p, 16, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *tiles = h[0];
+    *nnz = h[1];
+    API_END
+}
 
 extern "C" int b2sr_from_csr(uint32_t n, uint32_t dim, const uint32_t *d_row_ptr, const uint32_t *d_col_ind,
                              uint64_t nnz, void *stream, b2sr_matrix **out) {
