@@ -915,7 +915,7 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     LAUNCH(k_bfs_seed, 1, 1, 0, s, src, (uint32_t)D, d_levels, fa.p, fb.p);
     CK(cudaMemsetAsync(fa.p, 0, n16 * 16, s));
     LAUNCH(k_bfs_ctl_init, 1, 1, 0, s, ctl.p, (unsigned long long)at->live_tiles);
-    const unsigned gu = grid_for(ntr);
+    const unsigned gu = grid_for(n16);  // one thread per 16-byte chunk: the last-block plan waits on every block
     const uint32_t *ta = a ? a->trp : nullptr;
     BfsSnapshots &snaps = bfs_snapshots();
     snaps.reset();
@@ -983,7 +983,7 @@ static void bfs_push_only(const b2sr_matrix *a, uint32_t src, double *d_levels, 
     LAUNCH(k_bfs_seed, 1, 1, 0, s, src, (uint32_t)D, d_levels, fa.p, fb.p);
     CK(cudaMemsetAsync(fa.p, 0, n16 * 16, s));
     LAUNCH(k_bfs_ctl_init, 1, 1, 0, s, ctl.p, 1ull);  // alpha = 0 below: every level is a push
-    const unsigned gu = grid_for(ntr);
+    const unsigned gu = grid_for(n16);  // one thread per 16-byte chunk: the last-block plan waits on every block
     BfsSnapshots &snaps = bfs_snapshots();
     snaps.reset();
     LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)fb.p, (uint4 *)visited.p, d_levels, 0.0, a->trp, nullptr,
