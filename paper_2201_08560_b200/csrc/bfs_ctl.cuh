@@ -38,12 +38,13 @@ struct BfsSnap {
     long long sweeps;
 };
 
-// Top-down sweep over the non-transposed matrix a (bmv_stream.cu): OR of the
-// frontier bit-rows of every listed tile-row chunk scattered into next.
-// Raw: already-visited vertices are masked by the update kernel.
+// One fused level (bmv_stream.cu): push levels scatter the OR of the frontier
+// bit-rows of every listed chunk of a into next (visited != null: bits of
+// visited vertices dropped first; the update masks them either way); pull
+// levels stream at.
 void launch_bfs_level(b2sr_matrix *at, const b2sr_matrix *a, BfsCtl *ctl, const uint2 *push_list,
                       const uint32_t *active_list, const void *hx, size_t hb, const void *frontier, void *next,
-                      cudaStream_t s);
+                      const void *visited, cudaStream_t s);
 // Top-down level of the push-only BFS (no transpose; d = 4, 8): the listed
 // chunks of a, bits of visited vertices dropped before the scatter.
 void launch_bfs_push_level(const b2sr_matrix *a, const BfsCtl *ctl, const uint2 *push_list, const void *frontier,

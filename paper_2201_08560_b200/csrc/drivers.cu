@@ -908,6 +908,10 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     Buf<uint32_t> alist(std::max<uint32_t>(n_loads, 1), s);
     const double alpha = bfs_alpha();
     const bool trace = getenv("B2SR_BFS_TRACE") != nullptr;
+    // visited filter in the push levels: measured slower here, where push
+    // levels are the sparse ones (92.9 vs 97.6 GTEPS at s22), so off
+    const char *pve = getenv("B2SR_PUSH_VISITED");
+    const bool push_vis = pve && pve[0] == '1';
     LAUNCH(k_fill_f64, grid_for(n), 256, 0, s, d_levels, (size_t)n, HUGE_VAL);
     CK(cudaMemsetAsync(visited.p, 0, n16 * 16, s));
     CK(cudaMemsetAsync(fb.p, 0, n16 * 16, s));
@@ -930,7 +934,7 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     for (uint32_t L = 1;; L++) {
         LAUNCH(k_bfs_prep<D>, gp, 256, 0, s, ctl.p, ntr, ta, list.p, hv.S, hv.cols, frontier, hx.p, n_loads, desc,
                visited.p, at->live, alist.p);
-        launch_bfs_level(at, a, ctl.p, list.p, alist.p, hx.p, hb, frontier, next, s);
+        launch_bfs_level(at, a, ctl.p, list.p, alist.p, hx.p, hb, frontier, next, push_vis ? visited.p : nullptr, s);
         LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L, ta,
                at->trp, (const uint4 *)at->live, ctl.p, (uint4 *)frontier, 1, alpha,
                (unsigned long long)at->num_tiles, a ? 1 : 0, snaps.dev, L);
@@ -976,6 +980,8 @@ static void bfs_push_only(const b2sr_matrix *a, uint32_t src, double *d_levels, 
     Buf<BfsCtl> ctl(1, s);
     Buf<uint2> list((size_t)ntr + a->num_tiles / PUSH_CH + 1, s);
     const bool trace = getenv("B2SR_BFS_TRACE") != nullptr;
+    const char *pve = getenv("B2SR_PUSH_VISITED");  // A/B (default on: every level is a push here)
+    const bool push_vis = !(pve && pve[0] == '0');
     LAUNCH(k_fill_f64, grid_for(n), 256, 0, s, d_levels, (size_t)n, HUGE_VAL);
     CK(cudaMemsetAsync(visited.p, 0, n16 * 16, s));
     CK(cudaMemsetAsync(fb.p, 0, n16 * 16, s));
@@ -995,7 +1001,7 @@ static void bfs_push_only(const b2sr_matrix *a, uint32_t src, double *d_levels, 
     for (uint32_t L = 1;; L++) {
         LAUNCH(k_bfs_prep<D>, gp, 256, 0, s, ctl.p, ntr, a->trp, list.p, 0u, nullptr, frontier, nullptr, 0u, nullptr,
                visited.p, nullptr, nullptr);
-        launch_bfs_push_level(a, ctl.p, list.p, frontier, visited.p, next, s);
+        launch_bfs_push_level(a, ctl.p, list.p, frontier, push_vis ? visited.p : nullptr, next, s);
         LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L, a->trp,
                nullptr, nullptr, ctl.p, (uint4 *)frontier, 1, 0.0, (unsigned long long)a->num_tiles, 1, snaps.dev, L);
         std::swap(frontier, next);
