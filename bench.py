@@ -687,7 +687,7 @@ def run_reference(args, rank, world):
     deg = np.diff(rp.astype(np.int64))
     roots = pick_roots(deg, args.warmup + args.steps + 8, seed=args.seed + 7)
     budget_s = 150.0
-    for r in roots[: min(args.warmup, 1)]:
+    for r in roots[: args.warmup]:  # untimed warm-up roots (page-in, thread pool)
         orc.bfs(m, r, workers=threads)
     edges, secs, done = 0, 0.0, 0
     for r in roots[args.warmup: args.warmup + args.steps]:
@@ -700,13 +700,13 @@ def run_reference(args, rank, world):
             break
     v = edges / secs / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GTEPS", "n_gpus": world,
-            "steps": done, "warmup": min(args.warmup, 1), "ms_per_step": round(1e3 * secs / done, 2),
+            "steps": done, "warmup": args.warmup, "ms_per_step": round(1e3 * secs / done, 2),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 bit-words",
             "data": f"synthetic R-MAT seed {args.seed} (CPU twin of the device generator)",
             "config": {"workload": f"BFS via masked bin-SpMV, undirected R-MAT scale {scale} "
                                    f"edgefactor {args.edgefactor}, B2SR-{d}", "scale": scale, "tile_dim": d},
             "cpu_baseline": {"value": round(v, 6), "unit": "GTEPS", "cores": threads, "kind": "port",
-                             "sample": f"{done} BFS roots incl. transpose; stopped after {budget_s:.0f}s"},
+                             "sample": f"{done} BFS roots incl. transpose (timed budget {budget_s:.0f} s)"},
             "e2e": {"value": round(v, 6), "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "setup_s": round(setup, 2)}
     print(json.dumps(line), flush=True)
