@@ -105,7 +105,9 @@ struct XHot {
         if (c < S) {
             if constexpr (D == 4 && HOT_NIBBLES) {  // two 4-bit words per byte (hot.cu packs them)
                 asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(sbase + (c >> 1)));
-                return (v >> ((c & 1u) * 4u)) & 0xFu;
+                // the other column's nibble may stay in bits 4-7: every consumer
+                // ANDs with 4-wide tile bytes, whose high nibbles are clear
+                return v >> ((c & 1u) * 4u);
             } else if constexpr (sizeof(typename WordT<D>::T) == 1) {
                 asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(sbase + c));
             } else if constexpr (sizeof(typename WordT<D>::T) == 2) {
