@@ -56,7 +56,7 @@ __global__ void k_stream_desc(uint32_t n_loads, uint32_t tpw, uint64_t T, uint32
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k <= n_loads; k += gridDim.x * blockDim.x) {
         uint64_t t = std::min<uint64_t>((uint64_t)k * tpw, T - 1);
         uint32_t ra = row_of(trp, 0, ntr - 1, t);
-        uint4 o = make_uint4(ra, 0xFFFFFFFFu, 0xFFFFFFFFu, 0);
+        uint4 o = make_uint4(ra, 0x80808080u, 0x80808080u, 0);  // unused offset bytes: 128 (never <= p)
         if (k < n_loads) {
             uint64_t tn = std::min<uint64_t>((uint64_t)(k + 1) * tpw, T - 1);
             uint32_t rb = row_of(trp, ra, ntr - 1, tn), span = rb - ra;
@@ -138,11 +138,15 @@ __device__ __forceinline__ void or_row(void *__restrict__ y, uint32_t row, uint3
     if (acc) atomic_or_word<D>(y, row, acc);
 }
 
-// row of offset p (0..LT-1) relative to ra: #{i : off[i] <= p}
-__device__ __forceinline__ uint32_t rel_row(uint32_t p, uint32_t oa, uint32_t ob) {
-    uint32_t pp = p * 0x01010101u;
-    return (__popc(__vcmpgeu4(pp, oa)) + __popc(__vcmpgeu4(pp, ob))) >> 3;
+// row of offset p (0..LT-1) relative to ra: #{i : off[i] <= p}.  Offsets are
+// bytes in 1..128, so per byte (p + 128) - off lies in 0..254: the subtraction
+// never borrows across bytes and bit 7 of a byte is set iff p >= off (three
+// integer ops per word instead of the emulated __vcmpgeu4).  pp = p * 0x01010101
+// + 0x80808080 is lane-constant at the call sites.
+__device__ __forceinline__ uint32_t rel_row_pp(uint32_t pp, uint32_t oa, uint32_t ob) {
+    return __popc((pp - oa) & 0x80808080u) + __popc((pp - ob) & 0x80808080u);
 }
+__device__ __forceinline__ uint32_t row_pp(uint32_t p) { return p * 0x01010101u + 0x80808080u; }
 
 // Streams the loads at positions [p0, p1): load k = list[p] with a list (BFS
 // pull over the loads that still hold an unvisited vertex), else k = p.
@@ -261,7 +265,7 @@ __device__ __forceinline__ void bbb_stream(uint32_t p0, uint32_t p1, uint32_t n_
 #pragma unroll
             for (int g = 0; g < NG; g++) {
                 const uint32_t q0 = SG::pos(lane, g);
-                const uint32_t qa = rel_row(q0, oa, ob), qb = rel_row(q0 + GT - 1, oa, ob);
+                const uint32_t qa = rel_row_pp(row_pp(q0), oa, ob), qb = rel_row_pp(row_pp(q0 + GT - 1), oa, ob);
                 if (qa == qb) {  // the group's tiles share one row
                     uint32_t h = group_hits<D>(m[g]);
 #pragma unroll
@@ -269,7 +273,7 @@ __device__ __forceinline__ void bbb_stream(uint32_t p0, uint32_t p1, uint32_t n_
                 } else {
 #pragma unroll
                     for (int j = 0; j < GT; j++) {
-                        uint32_t q = rel_row(q0 + j, oa, ob), h = tile_hits<D>(m[g], j);
+                        uint32_t q = rel_row_pp(row_pp(q0 + j), oa, ob), h = tile_hits<D>(m[g], j);
 #pragma unroll
                         for (int u = 0; u < NW; u++) acc[u] |= (q / SPW == (uint32_t)u) ? h << (D * (q % SPW)) : 0u;
                     }
