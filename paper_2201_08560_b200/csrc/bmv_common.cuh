@@ -17,17 +17,16 @@ template <int D> struct Geo {
     static constexpr uint32_t CHUNK = 64 * TPW;          // tiles per work item
 };
 
-// d=4: bit r set when byte r of v is non-zero (bytes carry a low nibble only)
+// d=4: bit r set when byte r of v is non-zero (bytes carry a low nibble only:
+// byte + 0x0F sets bit 4 iff the byte is non-zero and never carries into the
+// next byte; the multiply moves bits 4/12/20/28 to 28..31 without collisions)
 __device__ __forceinline__ uint32_t nz_nibble_bytes(uint32_t v) {
-    v = (v | (v >> 1) | (v >> 2) | (v >> 3)) & 0x01010101u;
-    return (v * 0x10204080u) >> 28;
+    return (((v + 0x0F0F0F0Fu) & 0x10101010u) * 0x01020408u) >> 28;
 }
-// full-byte variant (d=8 rows)
+// full-byte variant (d=8 rows): bit 7 of ((b & 0x7F) + 0x7F) | b is set iff
+// b != 0; bits 7/15/23/31 -> 28..31
 __device__ __forceinline__ uint32_t nz_bytes(uint32_t v) {
-    v = (v | (v >> 4)) & 0x0F0F0F0Fu;
-    v = (v | (v >> 2)) & 0x03030303u;
-    v = (v | (v >> 1)) & 0x01010101u;
-    return (v * 0x10204080u) >> 28;
+    return (((((v & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | v) & 0x80808080u) * 0x00204081u) >> 28;
 }
 // per-byte popcounts packed in the bytes of a u32
 __device__ __forceinline__ uint32_t popc_bytes(uint32_t v) {
