@@ -251,30 +251,6 @@ __device__ __forceinline__ uint32_t load_word(const void *v, uint32_t i) {
 }
 
 // x-vector gather with a selectable cache policy (A/B experiments):
-// XG 0 = default global load, 1 = ld.global.cg (L2 only), 2 = L1::no_allocate
-template <int D, int XG>
-__device__ __forceinline__ uint32_t load_x(const void *v, uint32_t i) {
-    if constexpr (XG == 0) {
-        return load_word<D>(v, i);
-    } else {
-        using W = typename WordT<D>::T;
-        const W *p = reinterpret_cast<const W *>(v) + i;
-        uint32_t r;
-        if constexpr (sizeof(W) == 1) {
-            if constexpr (XG == 1) asm("ld.global.cg.u8 %0, [%1];" : "=r"(r) : "l"(p));
-            else asm("ld.global.nc.L1::no_allocate.u8 %0, [%1];" : "=r"(r) : "l"(p));
-        } else if constexpr (sizeof(W) == 2) {
-            unsigned short h;
-            if constexpr (XG == 1) asm("ld.global.cg.u16 %0, [%1];" : "=h"(h) : "l"(p));
-            else asm("ld.global.nc.L1::no_allocate.u16 %0, [%1];" : "=h"(h) : "l"(p));
-            r = h;
-        } else {
-            if constexpr (XG == 1) asm("ld.global.cg.u32 %0, [%1];" : "=r"(r) : "l"(p));
-            else asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
-        }
-        return r;
-    }
-}
 
 // OR `val` into bit-vector word i of width D using a 32-bit atomic.
 template <int D>

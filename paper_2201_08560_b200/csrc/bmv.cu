@@ -162,12 +162,12 @@ __device__ __forceinline__ void bbb_items(const WorkItem *__restrict__ items, ui
     }
 }
 
-template <int D, int XG>
+template <int D>
 __global__ void __launch_bounds__(256) k_bmv_bbb(const WorkItem *__restrict__ items, uint32_t n_items,
                                                  const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci,
                                                  const void *__restrict__ x, const void *__restrict__ keep,
                                                  void *__restrict__ y, uint32_t row0) {
-    bbb_items<D>(items, n_items, tiles, tci, XGlobal<D, XG>{x}, keep, y, row0);
+    bbb_items<D>(items, n_items, tiles, tci, XGlobal<D>{x}, keep, y, row0);
 }
 
 // ------------------------------------------------------------ K5 bbf
@@ -367,7 +367,7 @@ void launch_bbb(b2sr_matrix *m, const void *x, const void *keep, void *y, cudaSt
     kernel_timer().begin(s);
 #define BBB_CASE(DD)                                                                                              \
     case DD:                                                                                                      \
-        LAUNCH((k_bmv_bbb<DD, 0>), g, 256, 0, s, m->items, m->n_items, tl, m->tci, x, keep, y, m->row0);          \
+        LAUNCH((k_bmv_bbb<DD>), g, 256, 0, s, m->items, m->n_items, tl, m->tci, x, keep, y, m->row0);          \
         break;
     switch (m->dim) {
         BBB_CASE(4)

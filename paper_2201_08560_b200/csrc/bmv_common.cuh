@@ -1,4 +1,4 @@
-// Shared device helpers of the bin-SpMV family (bmv.cu, bmv_blocked.cu, drivers.cu).
+// Shared device helpers of the bin-SpMV family (bmv.cu, bmv_stream.cu, drivers.cu).
 #pragma once
 
 #include <algorithm>
@@ -75,10 +75,10 @@ inline void hot_smem_attr(K kernel, size_t bytes) {
 
 // x-word gathers used by the streaming kernels: plain global loads with a
 // selectable cache policy, or the hot-column cache (hot.cu) in shared memory
-template <int D, int XG = 0>
+template <int D>
 struct XGlobal {
     const void *x;
-    __device__ __forceinline__ uint32_t operator()(uint32_t c) const { return load_x<D, XG>(x, c); }
+    __device__ __forceinline__ uint32_t operator()(uint32_t c) const { return load_word<D>(x, c); }
 };
 // The hot words live in the kernel's dynamic shared memory; indexing the
 // extern array directly lets ptxas address it with LDS immediates instead of

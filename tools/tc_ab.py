@@ -12,4 +12,4 @@ for orient in ("id", "degree"):
         for _ in range(3):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(); c = b2.algorithms._tc_count(lo); e1.record(); torch.cuda.synchronize(); ts.append(e0.elapsed_time(e1))
-        print(os.environ.get("B2SR_TC_ALG", "items"), orient, d, c, round(min(ts), 2), "ms", flush=True)
+        print(orient, d, c, round(min(ts), 2), "ms", flush=True)
