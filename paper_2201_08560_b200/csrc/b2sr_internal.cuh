@@ -250,8 +250,6 @@ __device__ __forceinline__ uint32_t load_word(const void *v, uint32_t i) {
     return (uint32_t)(reinterpret_cast<const typename WordT<D>::T *>(v))[i];
 }
 
-// x-vector gather with a selectable cache policy (A/B experiments):
-
 // OR `val` into bit-vector word i of width D using a 32-bit atomic.
 template <int D>
 __device__ __forceinline__ void atomic_or_word(void *v, uint32_t i, uint32_t val) {
