@@ -152,6 +152,7 @@ struct b2sr_matrix {
     void *hot = nullptr;              // hot-column x cache plan (hot.cu)
     void *stream = nullptr;           // flat tile-stream row hints (bmv_stream.cu)
     void *bff = nullptr;              // float-gather row order (bmv_bff.cu)
+    void *xperm = nullptr;            // hot-first x relabelling for the float gather (bmv_xperm.cu)
 };
 
 namespace b2sr {
@@ -168,7 +169,7 @@ void launch_row_ids(const b2sr_matrix *m, uint32_t *rowid, cudaStream_t s);  // 
 void free_vlong(void *plan);
 void *build_vlong(b2sr_matrix *m, uint32_t thresh, cudaStream_t s);
 void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
-                  cudaStream_t s, const std::function<void(cudaStream_t)> &overlap = {});
+                  cudaStream_t s, const std::function<void(cudaStream_t)> &overlap = {}, const uint32_t *gtci = nullptr);
 // hot.cu: the S most referenced tile columns' x words live in shared memory
 constexpr uint32_t HOT_SMEM_BYTES = 196608;
 constexpr bool HOT_NIBBLES = true;   // d=4: pack two 4-bit x words per byte (2x the slots, more ALU per gather)
@@ -192,9 +193,15 @@ void launch_bbb_stream(b2sr_matrix *m, const void *x, const void *keep, void *y,
                        const void *visited = nullptr, bool active_only = false, bool lazy = false);
 void free_stream(void *plan);
 // bmv_bff.cu: float gather over the rows with <= thresh tiles
+// gtci: the column array the gathers index x with (m->tci, or the relabelled
+// one of bmv_xperm.cu with x relabelled to match)
 void launch_bff_rows(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
-                     uint32_t thresh, cudaStream_t s, bool plan_only = false);
+                     uint32_t thresh, cudaStream_t s, bool plan_only = false, const uint32_t *gtci = nullptr);
 void free_bff(void *plan);
+// bmv_xperm.cu: hot-first relabelling of x for the float gather
+bool xperm_enabled(const b2sr_matrix *m);
+const uint32_t *xperm_apply(b2sr_matrix *m, const double *x, double *xp, cudaStream_t s);
+void free_xperm(void *plan);
 const uint4 *stream_desc(b2sr_matrix *m, cudaStream_t s, uint32_t *n_loads);  // per-load row descriptors
 void launch_stream_sweep(b2sr_matrix *m, const uint32_t *list, const uint32_t *list_n, const void *hx, size_t hb,
                          const void *x, void *y, const int *gate, int want, cudaStream_t s, bool lazy = false);

@@ -407,7 +407,17 @@ void launch_bff(const b2sr_matrix *m_, const double *x, int ring, double inc, co
     ensure_vlong(m, s);
     const uint32_t hi = vlong_thresh(m->dim);
     launch_bff_rows(m, x, ring, inc, keep, y, hi, s, /*plan_only=*/true);
-    launch_vlong(m, x, ring, inc, keep, y, s, [&](cudaStream_t so) { launch_bff_rows(m, x, ring, inc, keep, y, hi, so); });
+    // large x: gather from a hot-first relabelled copy (bmv_xperm.cu)
+    Buf<double> xp;
+    const uint32_t *gtci = nullptr;
+    if (xperm_enabled(m)) {
+        const size_t xbytes = (size_t)tile_rows(m->n, m->dim) * m->dim * sizeof(double);
+        xp = Buf<double>(xbytes / sizeof(double), s);
+        gtci = xperm_apply(m, x, xp.p, s);
+        x = xp.p;
+    }
+    launch_vlong(m, x, ring, inc, keep, y, s,
+                 [&](cudaStream_t so) { launch_bff_rows(m, x, ring, inc, keep, y, hi, so, false, gtci); }, gtci);
 }
 }  // namespace b2sr
 

@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(BFF_THREADS, 4) k_bff_rows(uint32_t n_rows, co
 
 template <int D>
 static void bff_rows_ring(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
-                          uint32_t thresh, cudaStream_t s) {
+                          uint32_t thresh, cudaStream_t s, const uint32_t *gtci) {
     BffPlan *p = static_cast<BffPlan *>(m->bff);  // built by a plan_only call on the caller's stream
     if (!p || !p->n_rows) return;
     constexpr uint32_t GPW = 32 / D;
@@ -193,25 +193,26 @@ static void bff_rows_ring(b2sr_matrix *m, const double *x, int ring, double inc,
                                               (uint64_t)num_sms() * 8);
     const uint8_t *tl = (const uint8_t *)m->tiles;
     if (ring == B2SR_RING_ARITHMETIC)
-        LAUNCH((k_bff_rows<D, B2SR_RING_ARITHMETIC>), g, BFF_THREADS, 0, s, p->n_rows, p->rows, m->n, m->trp, m->tci, tl,
+        LAUNCH((k_bff_rows<D, B2SR_RING_ARITHMETIC>), g, BFF_THREADS, 0, s, p->n_rows, p->rows, m->n, m->trp, gtci, tl,
                x, inc, keep, y, m->row0);
     else if (ring == B2SR_RING_MINPLUS)
-        LAUNCH((k_bff_rows<D, B2SR_RING_MINPLUS>), g, BFF_THREADS, 0, s, p->n_rows, p->rows, m->n, m->trp, m->tci, tl,
+        LAUNCH((k_bff_rows<D, B2SR_RING_MINPLUS>), g, BFF_THREADS, 0, s, p->n_rows, p->rows, m->n, m->trp, gtci, tl,
                x, inc, keep, y, m->row0);
     else
-        LAUNCH((k_bff_rows<D, B2SR_RING_MAXTIMES>), g, BFF_THREADS, 0, s, p->n_rows, p->rows, m->n, m->trp, m->tci, tl,
+        LAUNCH((k_bff_rows<D, B2SR_RING_MAXTIMES>), g, BFF_THREADS, 0, s, p->n_rows, p->rows, m->n, m->trp, gtci, tl,
                x, inc, keep, y, m->row0);
 }
 
 void launch_bff_rows(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
-                     uint32_t thresh, cudaStream_t s, bool plan_only) {
+                     uint32_t thresh, cudaStream_t s, bool plan_only, const uint32_t *gtci) {
     bff_plan(m, thresh, s);
     if (plan_only) return;
+    if (!gtci) gtci = m->tci;
     switch (m->dim) {
-        case 4: bff_rows_ring<4>(m, x, ring, inc, keep, y, thresh, s); break;
-        case 8: bff_rows_ring<8>(m, x, ring, inc, keep, y, thresh, s); break;
-        case 16: bff_rows_ring<16>(m, x, ring, inc, keep, y, thresh, s); break;
-        default: bff_rows_ring<32>(m, x, ring, inc, keep, y, thresh, s); break;
+        case 4: bff_rows_ring<4>(m, x, ring, inc, keep, y, thresh, s, gtci); break;
+        case 8: bff_rows_ring<8>(m, x, ring, inc, keep, y, thresh, s, gtci); break;
+        case 16: bff_rows_ring<16>(m, x, ring, inc, keep, y, thresh, s, gtci); break;
+        default: bff_rows_ring<32>(m, x, ring, inc, keep, y, thresh, s, gtci); break;
     }
 }
 

@@ -540,7 +540,8 @@ static cudaStream_t side_stream(int which = 0) {
 // Scatter, then the folds; `overlap` runs while the hub folds proceed on the
 // side stream (the main stream waits for them before returning).
 void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
-                  cudaStream_t s, const std::function<void(cudaStream_t)> &overlap) {
+                  cudaStream_t s, const std::function<void(cudaStream_t)> &overlap, const uint32_t *gtci) {
+    const uint32_t *tci = gtci ? gtci : m->tci;  // gather columns (relabelled with x, or the matrix's)
     VLongPlan *v = static_cast<VLongPlan *>(m->vlong);
     if (!v || !v->n_rows) {
         if (overlap) overlap(s);
@@ -554,10 +555,10 @@ void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const v
         const uint4 *un = v->units + u0;
         const uint32_t *uo = v->unit_off + (size_t)u0 * m->dim;
         switch (m->dim) {
-            case 4: LAUNCH(k_vlong_scatter_w<4>, gw, 256, 0, s, nu, un, uo, v->base, m->tci, (const uint8_t *)m->tiles, x, v->terms); break;
-            case 8: LAUNCH(k_vlong_scatter_w<8>, gw, 256, 0, s, nu, un, uo, v->base, m->tci, (const uint8_t *)m->tiles, x, v->terms); break;
-            case 16: LAUNCH(k_vlong_scatter<16>, gu, VTHREADS, 0, s, nu, un, uo, v->base, m->tci, (const uint16_t *)m->tiles, x, v->terms); break;
-            default: LAUNCH(k_vlong_scatter<32>, gu, VTHREADS, 0, s, nu, un, uo, v->base, m->tci, (const uint32_t *)m->tiles, x, v->terms); break;
+            case 4: LAUNCH(k_vlong_scatter_w<4>, gw, 256, 0, s, nu, un, uo, v->base, tci, (const uint8_t *)m->tiles, x, v->terms); break;
+            case 8: LAUNCH(k_vlong_scatter_w<8>, gw, 256, 0, s, nu, un, uo, v->base, tci, (const uint8_t *)m->tiles, x, v->terms); break;
+            case 16: LAUNCH(k_vlong_scatter<16>, gu, VTHREADS, 0, s, nu, un, uo, v->base, tci, (const uint16_t *)m->tiles, x, v->terms); break;
+            default: LAUNCH(k_vlong_scatter<32>, gu, VTHREADS, 0, s, nu, un, uo, v->base, tci, (const uint32_t *)m->tiles, x, v->terms); break;
         }
     };
     // 1. the top rows' terms, then their big vertices' chains on the side stream

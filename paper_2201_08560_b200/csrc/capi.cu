@@ -121,6 +121,7 @@ void free_matrix(b2sr_matrix *m) {
     free_hot(m->hot);
     free_stream(m->stream);
     free_bff(m->bff);
+    free_xperm(m->xperm);
     if (cur != m->device) cudaSetDevice(cur);
     delete m;
 }
