@@ -90,7 +90,6 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t *__restrict__
 // warp for milliseconds; split every mask tile into chunks of TC_CHUNK
 // entries of its shorter tile row so such pairs spread over many warps.
 constexpr uint32_t TC_CHUNK = 256;
-constexpr uint32_t TC_STAGE = 512;  // longer-row entries a warp stages in shared memory (2 KB)
 
 __global__ void k_tc_item_counts(uint64_t TM, const uint32_t *__restrict__ m_rowid, const uint32_t *__restrict__ m_tci,
                                  uint32_t m_row0, const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ b_trp,
@@ -122,11 +121,7 @@ __global__ void __launch_bounds__(256) k_bmm_masked_items(uint64_t n_items, cons
                                                           const typename WordT<D>::T *__restrict__ b_tiles,
                                                           uint32_t m_row0, unsigned long long *__restrict__ out,
                                                           unsigned long long *__restrict__ work) {
-    // per warp: the longer tile row's columns, when it fits, so the lanes'
-    // binary searches run in shared memory instead of chains of global loads
-    __shared__ uint32_t srow[256 / 32][TC_STAGE];
     const uint32_t lane = lane_id();
-    uint32_t *const sr = srow[threadIdx.x >> 5];
     const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long acc = 0, units = 0;
     for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_items; w += warps) {
@@ -142,42 +137,19 @@ __global__ void __launch_bounds__(256) k_bmm_masked_items(uint64_t n_items, cons
         const uint32_t *stci = a_short ? a_tci : b_tci;
         const uint32_t *ltci = a_short ? b_tci : a_tci;
         uint32_t c0 = s0 + it.y * TC_CHUNK, c1 = min(s1, c0 + TC_CHUNK);
-        if (rows_used == 0) continue;
-        const bool staged = l1 - l0 <= TC_STAGE;
-        uint32_t lo, hi;
-        if (staged) {  // stage the long row (coalesced), search it in shared memory
-            __syncwarp();  // the previous item's searches are done with sr
-            for (uint32_t i = lane; i < l1 - l0; i += 32) sr[i] = __ldg(ltci + l0 + i);
-            __syncwarp();
-            lo = 0;
-            hi = l1 - l0;
-        } else {  // narrow the long row to the chunk's value range once per warp
-            uint32_t first = __ldg(stci + c0), last = __ldg(stci + c1 - 1);
-            lo = lower_bound_u32(ltci, l0, l1, first);
-            hi = lower_bound_u32(ltci, lo, l1, last + 1);
-            if (lo == hi) continue;
-        }
+        // narrow the long row to the chunk's value range once per warp
+        uint32_t first = __ldg(stci + c0), last = __ldg(stci + c1 - 1);
+        uint32_t lo = lower_bound_u32(ltci, l0, l1, first);
+        uint32_t hi = lower_bound_u32(ltci, lo, l1, last + 1);
+        if (lo == hi || rows_used == 0) continue;
         for (uint32_t base = c0; base < c1; base += 32) {
             uint32_t si = base + lane;
             uint32_t ta = 0, tb = 0;
             bool hit = false;
             if (si < c1) {
                 uint32_t K = __ldg(stci + si);
-                uint32_t li;
-                bool found;
-                if (staged) {
-                    uint32_t a = lo, b = hi;
-                    while (a < b) {
-                        uint32_t mid = (a + b) >> 1;
-                        if (sr[mid] < K) a = mid + 1; else b = mid;
-                    }
-                    found = a < hi && sr[a] == K;
-                    li = l0 + a;
-                } else {
-                    li = lower_bound_u32(ltci, lo, hi, K);
-                    found = li < hi && __ldg(ltci + li) == K;
-                }
-                if (found) {
+                uint32_t li = lower_bound_u32(ltci, lo, hi, K);
+                if (li < hi && __ldg(ltci + li) == K) {
                     hit = true;
                     ta = a_short ? si : li;
                     tb = a_short ? li : si;
