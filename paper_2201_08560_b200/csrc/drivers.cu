@@ -753,14 +753,17 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
     rt = __reduce_add_sync(0xffffffffu, (uint32_t)rt);
     fv = __reduce_add_sync(0xffffffffu, (uint32_t)fv);
     BfsCounters *cnt = &ctl->cnt;
+    const bool any = __any_sync(0xffffffffu, found);
     if (lane == 0) {
         if (ft) atomicAdd(&cnt->frontier_tiles, ft);
         if (rt) atomicAdd(&cnt->removed_tiles, rt);
         if (fv) atomicAdd(&cnt->frontier_vertices, fv);
+        if (any) atomicOr(&cnt->any, 1);
+        // the warp's counter updates are performed before the block retires;
+        // only the warp leaders fence (a fence in every thread stalls them all)
+        __threadfence();
     }
-    if (__any_sync(0xffffffffu, found) && lane == 0) atomicOr(&cnt->any, 1);
     __shared__ bool last;
-    __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) last = atomicAdd(&ctl->blocks_done, 1u) == gridDim.x - 1;
     __syncthreads();
@@ -789,9 +792,8 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
             volatile BfsSnap *hs = snap + level_no % 8;
             hs->done = cv->done;
             hs->sweeps = cv->sweeps;
-            __threadfence_system();
-            hs->level = level_no;
-            __threadfence_system();
+            __threadfence_system();  // done/sweeps land before the level that publishes them
+            hs->level = level_no;    // no fence after: the kernel's completion flushes it
         }
     }
 }
