@@ -769,29 +769,37 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
     __syncthreads();
     if (last && threadIdx.x == 0) {  // the last block plans the next level
         __threadfence();
-        volatile BfsCtl *cv = ctl;
-        cv->blocks_done = 0;
-        if (cv->done || !cv->cnt.any) {  // this sweep found nothing: BFS is over
-            cv->done = 1;
-            cv->mode = BFS_NONE;
+        // one batch of independent L2 reads (a chain of volatile accesses costs
+        // a round trip each), then plain stores: later kernels see them
+        const int done0 = __ldcg(&ctl->done), any_all = __ldcg(&ctl->cnt.any);
+        const unsigned long long unv = __ldcg(&ctl->unvisited), rtn = __ldcg(&ctl->cnt.removed_tiles);
+        const unsigned long long ftn = __ldcg(&ctl->cnt.frontier_tiles), fvn = __ldcg(&ctl->cnt.frontier_vertices);
+        long long sweeps = __ldcg(&ctl->sweeps);
+        int done = done0;
+        ctl->blocks_done = 0;
+        if (done0 || !any_all) {  // this sweep found nothing: BFS is over
+            done = 1;
+            ctl->done = 1;
+            ctl->mode = BFS_NONE;
         } else {
-            cv->unvisited -= cv->cnt.removed_tiles;
-            bool push = has_a && (double)cv->cnt.frontier_tiles * alpha < (double)cv->unvisited;
-            cv->mode = push ? BFS_PUSH : (cv->unvisited * 2 < tiles_at ? BFS_PULL_ACTIVE : BFS_PULL);
+            const unsigned long long u = unv - rtn;
+            ctl->unvisited = u;
+            const bool push = has_a && (double)ftn * alpha < (double)u;
+            ctl->mode = push ? BFS_PUSH : (u * 2 < tiles_at ? BFS_PULL_ACTIVE : BFS_PULL);
             // a frontier of < 1/16 of the vertices: most 4-tile groups see all-zero x words
-            cv->sparse = cv->cnt.frontier_vertices * 16 < (unsigned long long)ntr * D;
-            cv->list_n = 0;
-            cv->active_n = 0;
-            cv->sweeps = cv->sweeps + 1;
-            cv->cnt.any = 0;
-            cv->cnt.frontier_tiles = 0;
-            cv->cnt.removed_tiles = 0;
-            cv->cnt.frontier_vertices = 0;
+            ctl->sparse = fvn * 16 < (unsigned long long)ntr * D;
+            ctl->list_n = 0;
+            ctl->active_n = 0;
+            ctl->sweeps = ++sweeps;
+            ctl->cnt.any = 0;
+            ctl->cnt.frontier_tiles = 0;
+            ctl->cnt.removed_tiles = 0;
+            ctl->cnt.frontier_vertices = 0;
         }
         if (snap) {  // the level's outcome, straight into mapped host memory
             volatile BfsSnap *hs = snap + level_no % 8;
-            hs->done = cv->done;
-            hs->sweeps = cv->sweeps;
+            hs->done = done;
+            hs->sweeps = sweeps;
             __threadfence_system();  // done/sweeps land before the level that publishes them
             hs->level = level_no;    // no fence after: the kernel's completion flushes it
         }
