@@ -115,28 +115,35 @@ class _PinnedPool:
         self.lock = threading.Lock()
 
     def lease(self, nbytes: int):
-        """A free block of at least nbytes (None: over the bound)."""
+        """(block, view of its first nbytes) of a free block, or None (over the
+        bound).  The view is taken under the lock: it is the reference that
+        marks the block busy, so no other thread can lease it meanwhile."""
         with self.lock:
-            best = None
-            for b in self.blocks:
-                if nbytes <= b.size <= 2 * nbytes + self.GRAIN and b.free() and (best is None or b.size < best.size):
-                    best = b
-            if best is not None:
-                return best
-            size = (nbytes + self.GRAIN - 1) // self.GRAIN * self.GRAIN
+            b = self._pick(nbytes)
+            return None if b is None else (b, b.root[:nbytes])
+
+    def _pick(self, nbytes: int):
+        """Smallest free block that fits (caller holds the lock), else a new one."""
+        best = None
+        for b in self.blocks:
+            if nbytes <= b.size <= 2 * nbytes + self.GRAIN and b.free() and (best is None or b.size < best.size):
+                best = b
+        if best is not None:
+            return best
+        size = (nbytes + self.GRAIN - 1) // self.GRAIN * self.GRAIN
+        if self.bytes + size > self.cap:
+            for b in list(self.blocks):  # make room from free blocks of other sizes
+                if self.bytes + size <= self.cap:
+                    break
+                if b.free():
+                    self.blocks.remove(b)
+                    self.bytes -= b.size
             if self.bytes + size > self.cap:
-                for b in list(self.blocks):  # make room from free blocks of other sizes
-                    if self.bytes + size <= self.cap:
-                        break
-                    if b.free():
-                        self.blocks.remove(b)
-                        self.bytes -= b.size
-                if self.bytes + size > self.cap:
-                    return None
-            b = _PinnedBlock(size)
-            self.blocks.append(b)
-            self.bytes += size
-            return b
+                return None
+        b = _PinnedBlock(size)
+        self.blocks.append(b)
+        self.bytes += size
+        return b
 
 
 _pool = _PinnedPool()
@@ -156,10 +163,11 @@ def to_host(tensor, dtype, count: int) -> np.ndarray:
     if nbytes == 0:
         return np.empty(count, dt)
     src = tensor.detach().view(t.uint8)[:nbytes]
-    blk = _pool.lease(nbytes)
-    if blk is not None:
+    leased = _pool.lease(nbytes)
+    if leased is not None:
+        blk, view = leased
         blk.tensor[:nbytes].copy_(src)
-        return blk.root[:nbytes].view(dt)
+        return view.view(dt)
     out = np.empty(count, dt)
     with _bounce_lock:
         if _bounce is None or _bounce.numel() < nbytes:

@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <functional>
+#include <mutex>
 #include <string>
 
 #include "b2sr_sm100.h"
@@ -129,6 +130,10 @@ struct WorkItem {      // one bin-SpMV work unit: tiles [t0, t1) of local tile r
 }  // namespace b2sr
 
 struct b2sr_matrix {
+    // lazily built per-matrix plans (items, stream, hot, bff, vlong, xperm,
+    // live) are created under this lock: the C ABI is re-entrant and callers
+    // may share a matrix across host threads
+    std::recursive_mutex plan_mu;
     uint32_t n = 0;          // logical dimension (global)
     uint32_t dim = 0;        // tile width 4/8/16/32
     uint32_t ntr = 0;        // tile rows stored here (== ceil(n/dim) unless a row block)
@@ -242,6 +247,8 @@ __device__ __forceinline__ uint32_t ld_stream32(const void *p) {
     asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
+
+#define B2SR_PLAN_LOCK(m) std::lock_guard<std::recursive_mutex> b2sr_plan_guard_((m)->plan_mu)
 
 // Valid-bit mask of bit-vector word w (formats.py:433-441).
 __device__ __forceinline__ uint32_t valid_mask(uint32_t w, uint32_t n, int d) {

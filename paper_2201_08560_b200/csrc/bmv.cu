@@ -51,6 +51,7 @@ __global__ void k_ofs_u32(uint32_t n, const uint64_t *in, uint32_t *out) {
 }
 
 void ensure_items(b2sr_matrix *m, cudaStream_t s) {
+    B2SR_PLAN_LOCK(m);
     if (m->items) return;
     uint32_t chunk = m->dim == 4 ? Geo<4>::CHUNK : m->dim == 8 ? Geo<8>::CHUNK
                    : m->dim == 16 ? Geo<16>::CHUNK : Geo<32>::CHUNK;
@@ -293,6 +294,7 @@ static uint32_t vlong_thresh(int dim) {
 }
 
 static void ensure_vlong(b2sr_matrix *m, cudaStream_t s) {
+    B2SR_PLAN_LOCK(m);
     if (!m->vlong) m->vlong = build_vlong(m, vlong_thresh(m->dim), s);
 }
 

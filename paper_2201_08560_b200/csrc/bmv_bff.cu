@@ -45,6 +45,7 @@ __global__ void k_bff_keys(uint32_t ntr, const uint32_t *__restrict__ trp, uint3
 }
 
 static BffPlan *bff_plan(b2sr_matrix *m, uint32_t thresh, cudaStream_t s) {
+    B2SR_PLAN_LOCK(m);
     if (!m->bff) {
         BffPlan *b = new BffPlan();
         try {

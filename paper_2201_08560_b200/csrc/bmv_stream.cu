@@ -74,6 +74,7 @@ __global__ void k_stream_desc(uint32_t n_loads, uint32_t tpw, uint64_t T, uint32
 }
 
 static StreamPlan *stream_plan(b2sr_matrix *m, uint32_t tpw, cudaStream_t s) {
+    B2SR_PLAN_LOCK(m);
     if (!m->stream) {
         StreamPlan *sp = new StreamPlan();
         sp->n_loads = (uint32_t)((m->num_tiles + tpw - 1) / tpw);

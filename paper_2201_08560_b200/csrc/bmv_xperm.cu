@@ -84,6 +84,7 @@ bool xperm_enabled(const b2sr_matrix *m) {
 }
 
 static XPerm *xperm_plan(b2sr_matrix *m, cudaStream_t s) {
+    B2SR_PLAN_LOCK(m);
     if (!m->xperm) {
         XPerm *p = new XPerm();
         try {

@@ -410,6 +410,7 @@ __global__ void k_live_tiles(uint32_t ntr, const uint32_t *__restrict__ trp, con
 }
 
 void ensure_live(b2sr_matrix *m, cudaStream_t s) {
+    B2SR_PLAN_LOCK(m);
     if (m->live) return;
     Buf<uint8_t> lv(padded_vec_bytes(m->ntr, m->dim), s);
     CK(cudaMemsetAsync(lv.p, 0, padded_vec_bytes(m->ntr, m->dim), s));

@@ -75,6 +75,7 @@ static unsigned hgrid(uint64_t work) {
 }
 
 HotView hot_view(b2sr_matrix *m, cudaStream_t s) {
+    B2SR_PLAN_LOCK(m);
     if (!m->hot) {
         const uint32_t nc = tile_rows(m->n, m->dim);  // column tile space is global for row blocks
         const uint32_t wb = (uint32_t)word_bytes((int)m->dim);
