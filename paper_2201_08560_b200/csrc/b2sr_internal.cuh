@@ -206,6 +206,7 @@ void free_bff(void *plan);
 // bmv_xperm.cu: hot-first relabelling of x for the float gather
 bool xperm_enabled(const b2sr_matrix *m);
 const uint32_t *xperm_apply(b2sr_matrix *m, const double *x, double *xp, cudaStream_t s);
+const uint32_t *xperm_apply_u32(b2sr_matrix *m, const uint32_t *x, uint32_t *xp, cudaStream_t s);  // d = 4, 8
 void free_xperm(void *plan);
 const uint4 *stream_desc(b2sr_matrix *m, cudaStream_t s, uint32_t *n_loads);  // per-load row descriptors
 void launch_stream_sweep(b2sr_matrix *m, const uint32_t *list, const uint32_t *list_n, const void *hx, size_t hb,

@@ -75,6 +75,16 @@ __global__ void k_xp_permute(uint32_t ncols, uint32_t n, const uint32_t *__restr
     }
 }
 
+// u32 vectors (CC labels): lab'[rank[c]*D + b] = lab[c*D + b]
+template <int D>
+__global__ void k_xp_permute_u32(uint32_t ncols, uint32_t n, const uint32_t *__restrict__ rank,
+                                 const uint32_t *__restrict__ x, uint32_t *__restrict__ xp) {
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x) {
+        const size_t src = (size_t)c * D, dst = (size_t)rank[c] * D;
+        for (int b = 0; b < D; b++) xp[dst + b] = src + b < n ? __ldg(x + src + b) : 0xFFFFFFFFu;
+    }
+}
+
 // Relabel when x' would not stay L2-resident anyway (B2SR_XPERM=1 / 0 forces).
 bool xperm_enabled(const b2sr_matrix *m) {
     const char *e = getenv("B2SR_XPERM");
@@ -121,6 +131,13 @@ const uint32_t *xperm_apply(b2sr_matrix *m, const double *x, double *xp, cudaStr
         case 16: LAUNCH(k_xp_permute<16>, xgrid(p->ncols), 256, 0, s, p->ncols, m->n, p->rank, x, xp); break;
         default: LAUNCH(k_xp_permute<32>, xgrid(p->ncols), 256, 0, s, p->ncols, m->n, p->rank, x, xp); break;
     }
+    return p->tci_p;
+}
+
+const uint32_t *xperm_apply_u32(b2sr_matrix *m, const uint32_t *x, uint32_t *xp, cudaStream_t s) {
+    XPerm *p = xperm_plan(m, s);
+    if (m->dim == 4) LAUNCH(k_xp_permute_u32<4>, xgrid(p->ncols), 256, 0, s, p->ncols, m->n, p->rank, x, xp);
+    else LAUNCH(k_xp_permute_u32<8>, xgrid(p->ncols), 256, 0, s, p->ncols, m->n, p->rank, x, xp);
     return p->tci_p;
 }
 

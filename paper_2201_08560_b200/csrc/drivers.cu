@@ -647,6 +647,81 @@ __global__ void k_cc_init(uint32_t n, double *labels, uint32_t *lab_u) {
     }
 }
 
+// CC's gather m = bff(a, f, min_plus(0)) (algorithms.py:176) on d = 4, 8.  The
+// labels are non-negative integers, so min(f_j + 0.0) over a row is exact and
+// independent of the order the terms are visited in: no reference-order walk
+// is needed, and the labels are read as u32 (64 MB at s24 instead of 134).
+// Warp per work item (chunk of one tile row); lanes stride the tiles, keep a
+// per-bit-row minimum, reduce with redux.sync min; split rows combine with
+// atomicMin.  mu = 0xFFFFFFFF where a vertex has no neighbour (bff's +inf).
+template <int D>
+__global__ void __launch_bounds__(256) k_cc_min(const WorkItem *__restrict__ items, uint32_t n_items, uint32_t n,
+                                                const uint32_t *__restrict__ tci, const uint8_t *__restrict__ tiles,
+                                                const uint32_t *__restrict__ lab, uint32_t *__restrict__ mu) {
+    static_assert(D == 4 || D == 8, "one 32/64-bit word per tile");
+    const uint32_t lane = lane_id(), warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_items; w += warps) {
+        const WorkItem it = items[w];
+        uint32_t mn[D];
+#pragma unroll
+        for (int r = 0; r < D; r++) mn[r] = 0xFFFFFFFFu;
+        constexpr int U = 4;  // tiles per lane per step, their loads issued together
+        for (uint32_t t = it.t0 + lane; t < it.t1; t += 32 * U) {
+            uint32_t k[U], wd[U][D / 4];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t tu = t + 32 * u;
+                const bool ok = tu < it.t1;
+                k[u] = ok ? ld_stream32(tci + tu) : 0u;
+                if constexpr (D == 4) {
+                    wd[u][0] = ok ? ld_stream32(tiles + (size_t)tu * 4) : 0u;
+                } else {
+                    wd[u][0] = ok ? ld_stream32(tiles + (size_t)tu * 8) : 0u;
+                    wd[u][1] = ok ? ld_stream32(tiles + (size_t)tu * 8 + 4) : 0u;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t *xs = lab + (size_t)k[u] * D;
+#pragma unroll
+                for (int r = 0; r < D; r++) {
+                    uint32_t b = (wd[u][r / 4] >> (8 * (r % 4))) & 0xFFu;
+                    while (b) {
+                        mn[r] = min(mn[r], __ldg(xs + __ffs(b) - 1));
+                        b &= b - 1;
+                    }
+                }
+            }
+        }
+        uint32_t mine = 0xFFFFFFFFu;
+#pragma unroll
+        for (int r = 0; r < D; r++) {
+            const uint32_t v = __reduce_min_sync(0xffffffffu, mn[r]);
+            if (lane == (uint32_t)r) mine = v;
+        }
+        const uint64_t v = (uint64_t)it.row * D + lane;
+        if (lane < (uint32_t)D && v < n) {
+            if (it.split) {
+                if (mine != 0xFFFFFFFFu) atomicMin(mu + v, mine);
+            } else {
+                mu[v] = mine;
+            }
+        }
+    }
+}
+
+// hook on the u32 minima: nxt[labels[i]] = min(nxt[labels[i]], mu_i)
+__global__ void k_cc_hook_u(uint32_t n, const uint32_t *__restrict__ mu, const uint32_t *__restrict__ lab_u,
+                            uint32_t *__restrict__ nxt) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t v = mu[i];
+        if (v != 0xFFFFFFFFu) {  // a neighbour exists (bff's minimum is finite)
+            const uint32_t t = lab_u[i];
+            if (v < nxt[t]) atomicMin(nxt + t, v);
+        }
+    }
+}
+
 // hook: nxt[labels[i]] = min(nxt[labels[i]], m_i)  (parallel form of algorithms.py:181-185)
 __global__ void k_cc_hook(uint32_t n, const double *__restrict__ m, const uint32_t *__restrict__ lab_u,
                           uint32_t *__restrict__ nxt) {
@@ -1307,16 +1382,41 @@ int b2sr_cc(const b2sr_matrix *a, double *d_labels, int64_t *iterations, void *s
     cudaStream_t s = (cudaStream_t)stream;
     if (a->row0 != 0) B2SR_THROW(B2SR_EINVAL, "connected components needs a full matrix");
     uint32_t n = a->n;
-    Buf<double> m(n, s);
-    Buf<uint32_t> lab_u(n, s), nxt(n, s);
+    const char *ue = getenv("B2SR_CC_U32");  // B2SR_CC_U32=0: the generic float gather (A/B)
+    const bool u32 = (a->dim == 4 || a->dim == 8) && !(ue && ue[0] == '0');
+    Buf<double> m(u32 ? 1 : n, s);
+    Buf<uint32_t> lab_u(n, s), nxt(n, s), mu(u32 ? n : 1, s);
     Buf<int> flag(1, s);
     LAUNCH(k_cc_init, grid_for(n), 256, 0, s, n, d_labels, lab_u.p);
+    b2sr_matrix *am = const_cast<b2sr_matrix *>(a);
+    if (u32) ensure_items(am, s);
+    // large label vectors: gather from the hot-first relabelled copy (bmv_xperm.cu)
+    const bool perm = u32 && xperm_enabled(am);
+    Buf<uint32_t> labp(perm ? (size_t)tile_rows(n, a->dim) * a->dim : 1, s);
     int64_t sweeps = 0;
     for (;;) {
-        launch_bff(a, d_labels, B2SR_RING_MINPLUS, 0.0, nullptr, m.p, s);
+        if (u32) {
+            CK(cudaMemsetAsync(mu.p, 0xFF, (size_t)n * 4, s));
+            const uint32_t *gl = lab_u.p, *gtci = a->tci;
+            if (perm) {
+                gtci = xperm_apply_u32(am, lab_u.p, labp.p, s);
+                gl = labp.p;
+            }
+            const unsigned gi = (unsigned)std::max<uint64_t>(
+                1, std::min<uint64_t>(((uint64_t)am->n_items + 7) / 8, (uint64_t)num_sms() * 16));
+            if (a->dim == 4)
+                LAUNCH(k_cc_min<4>, gi, 256, 0, s, am->items, am->n_items, n, gtci, (const uint8_t *)a->tiles, gl,
+                       mu.p);
+            else
+                LAUNCH(k_cc_min<8>, gi, 256, 0, s, am->items, am->n_items, n, gtci, (const uint8_t *)a->tiles, gl,
+                       mu.p);
+        } else {
+            launch_bff(a, d_labels, B2SR_RING_MINPLUS, 0.0, nullptr, m.p, s);
+        }
         sweeps++;
         CK(cudaMemcpyAsync(nxt.p, lab_u.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
-        LAUNCH(k_cc_hook, grid_for(n), 256, 0, s, n, m.p, lab_u.p, nxt.p);
+        if (u32) LAUNCH(k_cc_hook_u, grid_for(n), 256, 0, s, n, mu.p, lab_u.p, nxt.p);
+        else LAUNCH(k_cc_hook, grid_for(n), 256, 0, s, n, m.p, lab_u.p, nxt.p);
         for (;;) {
             CK(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
             LAUNCH(k_cc_jump, grid_for(n), 256, 0, s, n, nxt.p, flag.p);
