@@ -784,7 +784,7 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
                                 const uint32_t *__restrict__ trp_at, const uint4 *__restrict__ live_at,
                                 BfsCtl *__restrict__ ctl, uint4 *__restrict__ zero_buf, int mask, double alpha,
                                 unsigned long long tiles_at, int has_a, BfsSnap *__restrict__ snap,
-                                uint32_t level_no) {
+                                uint32_t level_no, double active_frac) {
     using W = typename WordT<D>::T;
     if (ctl->mode == BFS_NONE && mask) return;  // BFS already over
     constexpr int WPC = 16 / sizeof(W);
@@ -861,7 +861,7 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
             const unsigned long long u = unv - rtn;
             ctl->unvisited = u;
             const bool push = has_a && (double)ftn * alpha < (double)u;
-            ctl->mode = push ? BFS_PUSH : (u * 2 < tiles_at ? BFS_PULL_ACTIVE : BFS_PULL);
+            ctl->mode = push ? BFS_PUSH : ((double)u < active_frac * (double)tiles_at ? BFS_PULL_ACTIVE : BFS_PULL);
             // a frontier of < 1/16 of the vertices: most 4-tile groups see all-zero x words
             ctl->sparse = fvn * 16 < (unsigned long long)ntr * D;
             ctl->list_n = 0;
@@ -993,6 +993,8 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     const uint4 *desc = stream_desc(at, s, &n_loads);
     Buf<uint32_t> alist(std::max<uint32_t>(n_loads, 1), s);
     const double alpha = bfs_alpha();
+    const char *afe = getenv("B2SR_BFS_ACTIVE");  // pull only the loads of unvisited rows below this tile fraction
+    const double active_frac = afe ? atof(afe) : 0.5;
     const bool trace = getenv("B2SR_BFS_TRACE") != nullptr;
     // visited filter in the push levels: measured slower here, where push
     // levels are the sparse ones (92.9 vs 97.6 GTEPS at s22), so off
@@ -1012,7 +1014,7 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     // level 0 = {src}: visited, levels, counters, the push list of level 1 and its plan
     LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)fb.p, (uint4 *)visited.p, d_levels, 0.0, ta, at->trp,
            (const uint4 *)at->live, ctl.p, nullptr, 0, alpha, (unsigned long long)at->num_tiles, a ? 1 : 0,
-           snaps.dev, 0u);
+           snaps.dev, 0u, active_frac);
     void *frontier = fb.p, *next = fa.p;
     const unsigned gp = (unsigned)num_sms() * 8;
     int done = 0;
@@ -1023,7 +1025,7 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
         launch_bfs_level(at, a, ctl.p, list.p, alist.p, hx.p, hb, frontier, next, push_vis ? visited.p : nullptr, s);
         LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L, ta,
                at->trp, (const uint4 *)at->live, ctl.p, (uint4 *)frontier, 1, alpha,
-               (unsigned long long)at->num_tiles, a ? 1 : 0, snaps.dev, L);
+               (unsigned long long)at->num_tiles, a ? 1 : 0, snaps.dev, L, active_frac);
         std::swap(frontier, next);
         // the host checks level L-LOOKAHEAD's outcome while levels up to L are
         // already enqueued (levels past the end are gated no-ops): no poll
@@ -1066,6 +1068,7 @@ static void bfs_push_only(const b2sr_matrix *a, uint32_t src, double *d_levels, 
     Buf<BfsCtl> ctl(1, s);
     Buf<uint2> list((size_t)ntr + a->num_tiles / PUSH_CH + 1, s);
     const bool trace = getenv("B2SR_BFS_TRACE") != nullptr;
+    const double active_frac = 0.0;  // every level is a push here
     const char *pve = getenv("B2SR_PUSH_VISITED");  // A/B (default on: every level is a push here)
     const bool push_vis = !(pve && pve[0] == '0');
     LAUNCH(k_fill_f64, grid_for(n), 256, 0, s, d_levels, (size_t)n, HUGE_VAL);
@@ -1079,7 +1082,7 @@ static void bfs_push_only(const b2sr_matrix *a, uint32_t src, double *d_levels, 
     BfsSnapshots &snaps = bfs_snapshots();
     snaps.reset();
     LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)fb.p, (uint4 *)visited.p, d_levels, 0.0, a->trp, nullptr,
-           nullptr, ctl.p, nullptr, 0, 0.0, (unsigned long long)a->num_tiles, 1, snaps.dev, 0u);
+           nullptr, ctl.p, nullptr, 0, 0.0, (unsigned long long)a->num_tiles, 1, snaps.dev, 0u, active_frac);
     void *frontier = fb.p, *next = fa.p;
     const unsigned gp = (unsigned)num_sms() * 8;
     int done = 0;
@@ -1089,7 +1092,7 @@ static void bfs_push_only(const b2sr_matrix *a, uint32_t src, double *d_levels, 
                visited.p, nullptr, nullptr);
         launch_bfs_push_level(a, ctl.p, list.p, frontier, push_vis ? visited.p : nullptr, next, s);
         LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L, a->trp,
-               nullptr, nullptr, ctl.p, (uint4 *)frontier, 1, 0.0, (unsigned long long)a->num_tiles, 1, snaps.dev, L);
+               nullptr, nullptr, ctl.p, (uint4 *)frontier, 1, 0.0, (unsigned long long)a->num_tiles, 1, snaps.dev, L, active_frac);
         std::swap(frontier, next);
         if (trace || L > LOOKAHEAD) {
             const uint32_t Lc = trace ? L : L - LOOKAHEAD;
