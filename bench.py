@@ -663,6 +663,7 @@ def run_dist(args, rank, world, local_rank):
                         "includes": "H2D of every rank's B2SR row block from pinned memory, distributed BFS, "
                                     "D2H of the levels on rank 0"},
                 "roofline": roofline, "gpu_launches": int(launches), "bfs_sweeps_per_root": iters[:4],
+                "per_gpu_gteps": round(value / world, 4),  # BASELINE north_star: per-GPU GTEPS at N GPUs
                 "clocks": clk.summary(), "tc": tc, "graph_gen_s": round(gen_s, 3)}
         print(json.dumps(line), flush=True)
     tdist.destroy_process_group()
