@@ -176,7 +176,7 @@ void *build_vlong(b2sr_matrix *m, uint32_t thresh, cudaStream_t s);
 void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
                   cudaStream_t s, const std::function<void(cudaStream_t)> &overlap = {}, const uint32_t *gtci = nullptr);
 // hot.cu: the S most referenced tile columns' x words live in shared memory
-constexpr uint32_t HOT_SMEM_BYTES = 196608;
+constexpr uint32_t HOT_SMEM_BYTES = 131072;  // 128 KB: the rest of the 228 KB stays L1 for the cold gathers and streams
 constexpr bool HOT_NIBBLES = true;   // d=4: pack two 4-bit x words per byte (2x the slots, more ALU per gather)
 struct HotView {
     uint32_t S;               // slots; tci2 values < S are slots, others S + column
