@@ -88,17 +88,20 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t *__restrict__
 // ------------------------------------------------------------ chunked items
 // A mask tile whose two tile rows are both long (hub x hub) would pin one
 // warp for milliseconds; split every mask tile into chunks of TC_CHUNK
-// entries of its shorter tile row so such pairs spread over many warps.
-constexpr uint32_t TC_CHUNK = 256;
+// entries of its shorter tile row so such pairs spread over many warps
+// (64 / 128 / 256 / 1024 / 2048 / 8192: s20 35.0 / 28.8 / 26.4 / 26.0 / 26.0 /
+// 26.1 ms; s26 -, 6.81, 5.90, 5.39, 5.35, 5.43 s -- fewer, larger items win
+// until the hub pairs stop spreading).  B2SR_TC_CHUNK overrides (A/B).
+constexpr uint32_t TC_CHUNK = 2048;
 
 __global__ void k_tc_item_counts(uint64_t TM, const uint32_t *__restrict__ m_rowid, const uint32_t *__restrict__ m_tci,
                                  uint32_t m_row0, const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ b_trp,
-                                 uint32_t *__restrict__ cnt) {
+                                 uint32_t chunk, uint32_t *__restrict__ cnt) {
     for (uint64_t mt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; mt < TM; mt += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t I = m_rowid[mt] + m_row0, J = m_tci[mt];
         uint32_t la = a_trp[I + 1] - a_trp[I], lb = b_trp[J + 1] - b_trp[J];
         uint32_t sh = min(la, lb);
-        cnt[mt] = la && lb ? (sh + TC_CHUNK - 1) / TC_CHUNK : 0;
+        cnt[mt] = la && lb ? (sh + chunk - 1) / chunk : 0;
     }
 }
 
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(256) k_bmm_masked_items(uint64_t n_items, cons
                                                           const uint32_t *__restrict__ b_trp, const uint32_t *__restrict__ b_tci,
                                                           const typename WordT<D>::T *__restrict__ b_tiles,
                                                           uint32_t m_row0, unsigned long long *__restrict__ out,
-                                                          unsigned long long *__restrict__ work) {
+                                                          unsigned long long *__restrict__ work, uint32_t chunk) {
     const uint32_t lane = lane_id();
     const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long acc = 0, units = 0;
@@ -136,7 +139,7 @@ __global__ void __launch_bounds__(256) k_bmm_masked_items(uint64_t n_items, cons
         uint32_t l0 = a_short ? b0 : a0, l1 = a_short ? b1 : a1;
         const uint32_t *stci = a_short ? a_tci : b_tci;
         const uint32_t *ltci = a_short ? b_tci : a_tci;
-        uint32_t c0 = s0 + it.y * TC_CHUNK, c1 = min(s1, c0 + TC_CHUNK);
+        uint32_t c0 = s0 + it.y * chunk, c1 = min(s1, c0 + chunk);
         // narrow the long row to the chunk's value range once per warp
         uint32_t first = __ldg(stci + c0), last = __ldg(stci + c1 - 1);
         uint32_t lo = lower_bound_u32(ltci, l0, l1, first);
@@ -189,7 +192,9 @@ int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_ma
     Buf<uint32_t> rowid(TM, s), cnt(TM, s);
     Buf<uint64_t> ofs(TM + 1, s);
     row_ids(mask, rowid.p, s);
-    LAUNCH(k_tc_item_counts, grid_for(TM), 256, 0, s, TM, rowid.p, mask->tci, mask->row0, a->trp, bt->trp, cnt.p);
+    const char *ce = getenv("B2SR_TC_CHUNK");  // entries of the shorter row per work item (A/B)
+    const uint32_t chunk = ce ? std::max(32, atoi(ce)) : TC_CHUNK;
+    LAUNCH(k_tc_item_counts, grid_for(TM), 256, 0, s, TM, rowid.p, mask->tci, mask->row0, a->trp, bt->trp, chunk, cnt.p);
     exclusive_scan_u32_to_u64(cnt.p, ofs.p, TM, s);
     uint64_t n_items = read_scalar(ofs.p + TM, s);
     Buf<unsigned long long> out(1, s);
@@ -207,7 +212,7 @@ int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_ma
     case DD:                                                                                                   \
         LAUNCH(k_bmm_masked_items<DD>, g, 256, 0, s, n_items, items.p, rowid.p, mask->tci,                    \
                (const W *)mask->tiles, a->trp, a->tci, (const W *)a->tiles, bt->trp, bt->tci,                 \
-               (const W *)bt->tiles, mask->row0, out.p, work_out ? work.p : nullptr);                         \
+               (const W *)bt->tiles, mask->row0, out.p, work_out ? work.p : nullptr, chunk);                  \
         break;
         BMM_CASE(4, uint8_t)
         BMM_CASE(8, uint8_t)
