@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(256) k_bmv_bbf(const WorkItem *__restrict__ it
 // Rows longer than this many tiles take bmv_vlong.cu (segmented scatter +
 // fold).  At d = 32 a tile row of 1024 tiles still holds only ~40 terms per
 // bit-row on R-MAT, so the group walk keeps more rows (s16: 0.59 -> 0.45 ms).
-static uint32_t vlong_row_tiles(int dim) { return dim == 32 ? 1024u : 256u; }
+static uint32_t vlong_row_tiles(int dim) { return dim == 32 ? 1024u : (dim == 4 ? 512u : 256u); }  // s24 d=4 PR: 512 -> 96.8 vs 98.8 ms at 256
 
 // Row-length thresholds are fixed per matrix when its plan is built; the env
 // override exists so parity tests can push small matrices through both paths.
