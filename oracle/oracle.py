@@ -226,9 +226,12 @@ def pairwise_sum(a):
 
 
 # --------------------------------------------------------------- drivers
-def bfs(m, src, workers=None):
-    """algorithms.py:75-93 (transposes first, as the reference does)."""
-    at = transpose(m)
+def bfs(m, src, workers=None, symmetric=False):
+    """algorithms.py:75-93 (transposes first, as the reference does).  With
+    ``symmetric=True`` the caller asserts m == transpose(m) (an undirected
+    graph) and the matrix is passed as its own transpose -- the restatement
+    rule of SURVEY.md §8c for sizes where the transpose dominates."""
+    at = m if symmetric else transpose(m)
     n, d = m[0], m[1]
     levels = np.zeros(n, np.float64)
     it = lib().orc_bfs(n, d, _p(at[2]), _p(at[3]), _p(at[4]), int(src), _p(levels), _workers(workers))
@@ -251,9 +254,11 @@ def drop_diagonal_b2sr(m):
     return csr_to_b2sr(n, np.cumsum(rp2).astype(np.uint32), ci, d)
 
 
-def sssp(m, src, workers=None):
-    """algorithms.py:104-124."""
-    at = transpose(drop_diagonal_b2sr(m))
+def sssp(m, src, workers=None, at=None):
+    """algorithms.py:104-124.  ``at`` = transpose(drop_diagonal(m)) when the
+    caller already has it (e.g. a loop-free symmetric m is its own)."""
+    if at is None:
+        at = transpose(drop_diagonal_b2sr(m))
     n, d = m[0], m[1]
     dist = np.zeros(n, np.float64)
     it = lib().orc_sssp(n, d, _p(at[2]), _p(at[3]), _p(at[4]), int(src), _p(dist), _workers(workers))
