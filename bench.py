@@ -52,13 +52,17 @@ def parse():
     p.add_argument("--scale", type=int, default=22)
     p.add_argument("--edgefactor", type=int, default=16)
     p.add_argument("--dims", default="4,8,16,32", help="tile widths in the sweep")
-    p.add_argument("--dim", type=int, default=0, help="headline tile width (0 = best of the sweep)")
+    p.add_argument("--dim", type=int, default=4, help="headline tile width (0 = best of the sweep)")
     p.add_argument("--tc-scale", type=int, default=20)
     p.add_argument("--no-tc", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--drivers-scale", type=int, default=24, help="PR/SSSP/CC scale (BASELINE configs[3])")
     p.add_argument("--no-drivers", action="store_true")
     p.add_argument("--seed", type=int, default=1)
+    p.add_argument("--workload", choices=("auto", "s22", "s26"), default="auto",
+                   help="auto: configs[1] (s22 BFS) on one GPU, configs[4] (s26 strong scaling) under torchrun N>1")
+    p.add_argument("--scale5", type=int, default=26, help="configs[4] graph scale")
+    p.add_argument("--no-config5", action="store_true", help="skip the configs[4] N=1 point in the s22 run")
     return p.parse_args()
 
 
@@ -338,15 +342,10 @@ def run_ours(args, rank, world, local_rank):
                          "call_ms: the whole b2sr_bmv_bbb call incl. memset, hot fill and keep AND kernels"}
 
     # ---- e2e: public API with host inputs ----
+    # the caller's B2srMatrix holds ordinary (pageable) numpy arrays; the
+    # library stages the upload through its own page-locked chunks (staging.cu)
     host = (m.tile_row_ptr.copy(), m.tile_col_ind.copy(), m.bit_tiles.copy())
-    pinned = []
-    for a in host:  # pinned host copies of the caller's arrays
-        pt = torch.empty(a.nbytes, dtype=torch.uint8, pin_memory=True)
-        pt.numpy()[:] = a.view(np.uint8).reshape(-1)
-        pinned.append((pt, pt.numpy().view(a.dtype).reshape(a.shape)))
-    hm = b2.B2srMatrix(n, d, pinned[0][1], pinned[1][1], pinned[2][1])
-    # the constructor validated (and copied) them; point it back at the pinned buffers
-    hm._trp, hm._tci, hm._tiles = pinned[0][1], pinned[1][1], pinned[2][1]
+    hm = b2.B2srMatrix(n, d, *host)
     e2e_steps = max(3, min(args.steps, 6))
     e2e_edges = 0
     # untimed warm-up of the same loop (the result arrays are kept alive, as in
@@ -382,8 +381,8 @@ def run_ours(args, rank, world, local_rank):
     e2e = {"value": round(e2e_edges / (e2e_ms / 1e3) / 1e9, 4), "unit": "GTEPS",
            "h2d_bytes_per_step": int(sum(a.nbytes for a in host)), "d2h_bytes_per_step": 8 * n,
            "ms_per_step": round(e2e_ms / e2e_steps, 3),
-           "includes": "H2D of B2SR arrays from pinned memory, BFS (a fresh matrix has no transpose: "
-                       "push-only levels), D2H of levels into the pinned result pool",
+           "includes": "H2D of the B2SR arrays from the caller's pageable numpy arrays (staged by the library), "
+                       "BFS (a fresh matrix has no transpose: push-only levels), D2H of the levels",
            "breakdown_ms": breakdown}
 
     # ---- TC on the scale-20 graph ----
@@ -400,16 +399,21 @@ def run_ours(args, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32 bit-words (b1 tiles)",
             "data": f"synthetic R-MAT (Graph500 a,b,c=.57,.19,.19) generated on device, seed {args.seed}",
-            "config": {"workload": f"BFS via masked bin-SpMV, undirected R-MAT scale {args.scale} "
-                                   f"edgefactor {args.edgefactor}, B2SR-{d}",
-                       "scale": args.scale, "n": n, "nnz": int(csr.nnz), "tile_dim": d, "roots": args.steps,
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
-                       "l2": "inputs larger than L2 (B2SR %.2f GB > 126 MB)" % b2sr_gb},
+            "config": workload_config("s22", args, args.scale, n, int(csr.nnz), d, world, int(b2sr_gb * 1e9)),
             "e2e": e2e, "roofline": roofline, "gpu_launches": int(launches), "bfs_sweeps_per_root": iters[:4],
             "clocks": clk.summary(), "sweep": {str(k): v for k, v in sweep.items()}, "tc": tc, "drivers": drivers,
             "graph_gen_s": round(gen_s, 3)}
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(csr, d, roots[args.warmup])
+        line["cpu_baseline"], lv_cpu = cpu_baseline(csr, d, roots[args.warmup])
+        # parity of the headline: the oracle's levels for that root vs the device's
+        lv_gpu = b2.bfs(b2.csr_to_b2sr(csr, d), roots[args.warmup]).per_vertex
+        line["parity"] = {"bfs_levels_vs_oracle": bool(lv_gpu.tobytes() == lv_cpu.tobytes()),
+                          "root": roots[args.warmup],
+                          "full_size_tests": "tests/test_gpu_configs.py (configs 0-3 vs the oracle)"}
+    if not args.no_config5:
+        del csr
+        torch.cuda.empty_cache()
+        line["config5_n1"] = run_strong(args, 0, 1, local_rank, tdist=None, headline=False)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -420,7 +424,10 @@ def _fresh(hm):
     """Same host arrays, no device mirror (forces the H2D copy)."""
     import copy
 
+    import threading
+
     c = copy.copy(hm)
+    c._lock = threading.RLock()
     c._h = None
     c._transpose = None
     c._nodiag = None
@@ -517,169 +524,230 @@ def cpu_baseline(csr, d, root):
     e = traversed_edges(lv, deg)
     return {"value": round(e / dt / 1e9, 6), "unit": "GTEPS", "cores": threads, "kind": "port",
             "sample": f"1 BFS root (transpose included, as bfs() does) on the same scale graph, B2SR-{d}",
-            "seconds": round(dt, 3)}
+            "seconds": round(dt, 3)}, lv
 
 
-# ---------------------------------------------------------------- multi-GPU arm
-def run_dist(args, rank, world, local_rank):
-    """N > 1: row-partitioned BFS (dist.py), Graph500-style weak scaling: the
-    graph has scale + log2(N) (per-GPU vertices fixed), each rank owns an equal
-    block of tile rows of the transposed adjacency, and one all-gather of
-    frontier words per level joins the blocks.  value = traversed edges of the
-    whole job / max-over-ranks device time."""
+def cpu_baseline_s26(args):
+    """configs[4] at N=1: the C oracle on the same s26 graph (its CSR copied
+    down from the device), one root, the undirected matrix as its own
+    transpose (SURVEY.md §8c restatement rule; the transpose alone would
+    dominate)."""
+    from oracle import oracle as orc
+
+    from paper_2201_08560_b200 import rmat
+
+    d = args.dim or 4
+    csr = rmat.rmat_csr(args.scale5, args.edgefactor, seed=args.seed)
+    n, rp, ci = csr.n, csr.row_ptr, csr.col_ind
+    del csr
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    m = orc.csr_to_b2sr(n, rp, ci, d, workers=threads)
+    conv = time.perf_counter() - t0
+    deg = np.diff(rp.astype(np.int64))
+    root = pick_roots(deg, args.warmup + args.steps + 8, seed=args.seed + 7)[args.warmup]
+    t0 = time.perf_counter()
+    lv, _ = orc.bfs(m, root, workers=threads, symmetric=True)
+    dt = time.perf_counter() - t0
+    return {"value": round(traversed_edges(lv, deg) / dt / 1e9, 6), "unit": "GTEPS", "cores": threads, "kind": "port",
+            "sample": f"1 BFS root on the same s{args.scale5} graph, B2SR-{d}, matrix as its own transpose",
+            "seconds": round(dt, 3), "oracle_convert_s": round(conv, 2)}
+
+
+# ---------------------------------------------------------------- configs[4]: strong scaling
+def run_strong(args, rank, world, local_rank, tdist=None, headline=True):
+    """BASELINE configs[4]: row-partitioned BFS + TC on undirected R-MAT scale
+    26 (B2SR-4) over N GPUs -- strong scaling, the same graph and the same
+    native driver (b2sr_dist_bfs_*, NCCL) at every N including 1.  Each rank
+    builds the graph on its GPU, cuts its rows of a and at (balanced by at's
+    tiles) and drops the rest; per level the ranks exchange row contributions
+    (all-to-all-v) and the merged rows (all-gather-v) inside the library.
+    value = traversed edges of the whole job / max-over-ranks device time.
+    Returns the JSON line (headline) or a summary dict."""
     import torch
-    import torch.distributed as tdist
 
     import paper_2201_08560_b200 as b2
     from paper_2201_08560_b200 import _capi, rmat
     from paper_2201_08560_b200 import _device as dev
     from paper_2201_08560_b200 import dist as bdist
 
-    local_rank %= max(1, torch.cuda.device_count())  # several ranks may share a GPU in gloo tests
-    torch.cuda.set_device(local_rank)
-    backend = os.environ.get("B2SR_DIST_BACKEND", "nccl")  # gloo: several ranks on one GPU (tests)
-    if backend == "nccl":
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    else:
-        tdist.init_process_group(backend)
     sp = torch.cuda.current_stream().cuda_stream
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
 
     def barrier():
-        tdist.barrier()
+        if tdist is not None:
+            tdist.barrier()
         torch.cuda.synchronize()
 
-    scale = args.scale + max(0, int(round(np.log2(world))))
-    d = args.dim or 4
+    def max_over_ranks(v):
+        if tdist is None:
+            return float(v)
+        t = torch.tensor([float(v)], device="cuda", dtype=torch.float64)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
+
+    scale, d = args.scale5, args.dim or 4
     t0 = time.time()
     csr = rmat.rmat_csr(scale, args.edgefactor, seed=args.seed)
-    n = csr.n
+    n, nnz = csr.n, int(csr.nnz)
     deg = np.diff(csr.row_ptr.astype(np.int64))
     m = b2.csr_to_b2sr(csr, d)
     at = b2.b2sr_transpose(m)
-    del csr
-    b, e = bdist.partition(at.n_tile_rows, world, d)[rank]
-    blk = b2.formats._new_handle("b2sr_row_block", at.handle().ptr, b, e, dev.stream())
-    host_blk = bdist.block_to_host(blk)  # the caller's copy of this rank's block (e2e leg)
-    b2sr_bytes = b2.storage_bytes(m)
-    del m, at
+    b2sr_bytes = int(b2.storage_bytes(m))
+    comm = bdist.Comm.from_torch(tdist) if tdist is not None else bdist.Comm.nccl_single()
+    plan = bdist.NativeDistributedBfs.from_matrices(comm, m, at)
+    rb, re_ = plan.rows
+    # this rank's rows as the caller's host arrays (pageable numpy), for the e2e leg
+    blk_a = b2.formats._new_handle("b2sr_row_block", m.handle().ptr, rb, re_, sp)
+    blk_at = b2.formats._new_handle("b2sr_row_block", at.handle().ptr, rb, re_, sp)
+    host_a, host_at = bdist.block_to_host(blk_a, pinned=False), bdist.block_to_host(blk_at, pinned=False)
+    trp_a, trp_at = m.tile_row_ptr.copy(), at.tile_row_ptr.copy()
+    del blk_a, m, at
     torch.cuda.empty_cache()
-    gen_s = time.time() - t0
-    db = bdist.DistributedBfs.from_block(blk, n, d, tdist)
+    setup_s = time.time() - t0
     roots = pick_roots(deg, args.warmup + args.steps + 8, seed=args.seed + 7)
     degt = torch.from_numpy(deg).to("cuda")
+    lev = dev.empty_bytes(8 * n)
     for r in roots[: args.warmup]:
-        db.run(r, to_host=False)
+        plan.run(r, to_host=False, levels=lev)
     barrier()
     launches0 = _capi.launch_count()
-    outs, iters = [], []
+    iters, edges = [], 0
+    t_total = 0.0
     with Clocks(local_rank) as clk:
-        e0, e1 = ev(), ev()
-        e0.record()
         for r in roots[args.warmup: args.warmup + args.steps]:
-            lv, it = db.run(r, to_host=False)
-            outs.append(lv.clone())
+            e0, e1 = ev(), ev()
+            e0.record()
+            _, it = plan.run(r, to_host=False, levels=lev)
+            e1.record()
+            torch.cuda.synchronize()
+            t_total += e0.elapsed_time(e1)
             iters.append(it)
-        e1.record()
+            lv = lev.view(torch.float64)[:n]
+            edges += int(degt[torch.isfinite(lv)].sum().item()) // 2  # outside the timed region
         barrier()
     launches = _capi.launch_count() - launches0
-    ms = torch.tensor([e0.elapsed_time(e1)], device="cuda")
-    tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
-    ms = float(ms.item())
-    edges = sum(int(degt[torch.isfinite(lv)].sum().item()) // 2 for lv in outs)
-    del outs
+    ms = max_over_ranks(t_total)
     value = edges / (ms / 1e3) / 1e9
 
-    # e2e: every step each rank uploads its own block from pinned host memory,
-    # runs the distributed BFS and rank 0 reads the levels back
-    e2e_steps = max(3, min(args.steps, 6))
-    barrier()
-    f0, f1 = ev(), ev()
-    f0.record()
-    e2e_edges = 0
-    for r in roots[args.warmup: args.warmup + e2e_steps]:
-        hb = bdist.block_from_host(n, d, b, e, host_blk)
-        lv, _ = bdist.DistributedBfs.from_block(hb, n, d, tdist).run(r, to_host=(rank == 0))
-        if rank == 0:
-            e2e_edges += traversed_edges(lv, deg)
-        del hb
-    f1.record()
-    barrier()
-    e2e_ms = torch.tensor([f0.elapsed_time(f1)], device="cuda")
-    tdist.all_reduce(e2e_ms, op=tdist.ReduceOp.MAX)
-    e2e_ms = float(e2e_ms.item())
-    h2d = int(sum(h[1].nbytes for h in host_blk)) * world
-    # TC with the mask rows of the degree-oriented DAG partitioned, one int64 all-reduce
-    tc = None
-    if not args.no_tc:
-        tscale = args.tc_scale + max(0, int(round(np.log2(world))))
-        tcsr = rmat.rmat_csr(tscale, args.edgefactor, seed=args.seed)
-        lo = b2.csr_to_b2sr(b2.algorithms._degree_oriented(tcsr), d)
-        bdist.distributed_triangle_count(lo, tdist)  # warm
-        barrier()
-        t0_, t1_ = ev(), ev()
-        t0_.record()
-        tri = bdist.distributed_triangle_count(lo, tdist)
-        t1_.record()
-        barrier()
-        tms = torch.tensor([t0_.elapsed_time(t1_)], device="cuda")
-        tdist.all_reduce(tms, op=tdist.ReduceOp.MAX)
-        tms = float(tms.item())
-        tc = {"scale": tscale, "nnz": int(tcsr.nnz), "triangles": int(tri), "ms": round(tms, 3),
-              "edges_per_s": round((tcsr.nnz // 2) / (tms / 1e3), 1),
-              "parallelism": f"mask tile rows x{world}, L replicated, int64 all-reduce"}
-        del lo, tcsr
-        torch.cuda.empty_cache()
+    # K4 roofline of rank 0's block of at (masked sweep, 50 % random x / keep)
     roofline = None
-    if rank == 0:  # K4 masked sweep over this rank's block (x, keep: global 50 % random)
+    if rank == 0:
         pk, pk_kind = peaks()
         rng = np.random.default_rng(11)
         gb = dev.padded_vec_bytes(-(-n // d), d)
         xd = dev.to_device(b2.BitVector.from_bools(rng.random(n) < 0.5, d).words, gb)
         kd = dev.to_device(b2.BitVector.from_bools(rng.random(n) < 0.5, d).words, gb)
-        yd = dev.empty_bytes(dev.padded_vec_bytes(blk.ntr, d) + 16)
+        yd = dev.empty_bytes(dev.padded_vec_bytes(blk_at.ntr, d) + 16)
         flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-        kms, call_ms = k4_time(_capi, dev, torch, blk, xd, kd, yd, flush, sp, reps=8)
-        ab = bmv_alg_bytes(blk.ntr, blk.num_tiles, d)
-        roofline = {"bound": "hbm", "kernel": f"k_bmv_bbb_stream<{d}> (masked sweep of rank 0's block)",
+        kms, call_ms = k4_time(_capi, dev, torch, blk_at, xd, kd, yd, flush, sp, reps=8)
+        ab = bmv_alg_bytes(blk_at.ntr, blk_at.num_tiles, d)
+        roofline = {"bound": "hbm", "kernel": f"k_bmv_bbb_stream<{d}> (masked sweep of rank 0's rows of at, s{scale})",
                     "achieved": round(ab / kms / 1e6, 1), "peak": pk["hbm_gbs"], "peak_kind": pk_kind, "unit": "GB/s",
                     "frac": round(ab / kms / 1e6 / pk["hbm_gbs"], 4), "alg_bytes": ab,
                     "traffic": measured_traffic(f"k_bmv_bbb_stream<{d}>", scale, d), "kernel_ms": round(kms, 4),
                     "call_ms": round(call_ms, 4),
                     "timed": "CUDA events around the streaming kernel on its launch stream (b2sr_set_kernel_timing)"}
+        del xd, kd, yd, flush
+    del blk_at
+    torch.cuda.empty_cache()
+
+    # e2e: every rank uploads its rows of a and at from pageable host arrays
+    # (+ the global tile_row_ptr), plans, runs; rank 0 reads the levels back
+    e2e_steps = 2
+    barrier()
+    f0, f1 = ev(), ev()
+    f0.record()
+    e2e_edges = 0
+    for r in roots[args.warmup: args.warmup + e2e_steps]:
+        ha = bdist.block_from_host(n, d, rb, re_, host_a)
+        hat = bdist.block_from_host(n, d, rb, re_, host_at)
+        p2 = bdist.NativeDistributedBfs.from_blocks(comm, ha, hat, trp_a, trp_at)
+        lv, _ = p2.run(r, to_host=(rank == 0))
+        if rank == 0:
+            e2e_edges += traversed_edges(lv, deg)
+        del p2, ha, hat, lv
+    f1.record()
+    barrier()
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1))
+    h2d = sum(int(h[1].nbytes) for h in host_a + host_at) + trp_a.nbytes + trp_at.nbytes
+    if tdist is not None:
+        t = torch.tensor([h2d], device="cuda", dtype=torch.float64)
+        tdist.all_reduce(t)
+        h2d = int(t.item())
+    del plan, lev, host_a, host_at
+    torch.cuda.empty_cache()
+
+    # TC: L (degree-oriented DAG) replicated, mask rows cut by estimated work
+    tc = None
+    if not args.no_tc:
+        lower = b2.csr_to_b2sr(b2.algorithms._degree_oriented(csr), d)
+        bdist.native_triangle_count(comm, lower)  # warm (plans)
+        barrier()
+        t0_, t1_ = ev(), ev()
+        t0_.record()
+        tri, cuts = bdist.native_triangle_count(comm, lower)
+        t1_.record()
+        barrier()
+        tms = max_over_ranks(t0_.elapsed_time(t1_))
+        tc = {"scale": scale, "nnz": nnz, "triangles": int(tri), "ms": round(tms, 3),
+              "edges_per_s": round((nnz // 2) / (tms / 1e3), 1), "edges_per_s_per_gpu": round((nnz // 2) / (tms / 1e3) / world, 1),
+              "mask_row_cuts": cuts, "lower_tiles": int(lower.num_tiles),
+              "parallelism": f"mask tile rows x{world} (equal estimated work), L replicated, NCCL int64 all-reduce"}
+        del lower
+    del csr
+    torch.cuda.empty_cache()
+    e2e = {"value": round(e2e_edges / (e2e_ms / 1e3) / 1e9, 4), "unit": "GTEPS", "h2d_bytes_per_step": h2d,
+           "d2h_bytes_per_step": 8 * n, "ms_per_step": round(e2e_ms / e2e_steps, 3),
+           "includes": "every rank: H2D of its rows of a and at from pageable numpy arrays (staged by the "
+                       "library) + the global tile_row_ptr, plan, distributed BFS; D2H of the levels on rank 0"}
+    summary = {"workload": f"row-partitioned BFS, undirected R-MAT scale {scale} edgefactor {args.edgefactor}, "
+                           f"B2SR-{d}, strong scaling", "scale": scale, "n": n, "nnz": nnz, "tile_dim": d,
+               "n_gpus": world, "bfs_gteps": round(value, 4), "per_gpu_gteps": round(value / world, 4),
+               "ms_per_root": round(ms / args.steps, 4), "roots": args.steps, "bfs_sweeps_per_root": iters[:4],
+               "rows": [rb, re_], "tc": tc, "roofline": roofline, "e2e": e2e, "setup_s": round(setup_s, 2),
+               "b2sr_bytes": b2sr_bytes}
+    if not headline:
+        return summary
+    line = {"metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32 bit-words (b1 tiles)",
+            "data": f"synthetic R-MAT (Graph500 a,b,c=.57,.19,.19) generated on device, seed {args.seed}",
+            "config": workload_config("s26", args, scale, n, nnz, d, world, b2sr_bytes),
+            "e2e": e2e, "roofline": roofline, "gpu_launches": int(launches), "bfs_sweeps_per_root": iters[:4],
+            "per_gpu_gteps": round(value / world, 4), "clocks": clk.summary(), "tc": tc,
+            "setup_s": round(setup_s, 2)}
+    return line
+
+
+def run_dist(args, rank, world, local_rank):
+    """torchrun entry (N >= 1 processes, one GPU each) of the configs[4] workload."""
+    import torch
+    import torch.distributed as tdist
+
+    torch.cuda.set_device(local_rank)
+    tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    line = run_strong(args, rank, world, local_rank, tdist=tdist, headline=True)
     if rank == 0:
-        line = {"metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u32 bit-words (b1 tiles)",
-                "data": f"synthetic R-MAT (Graph500 a,b,c=.57,.19,.19) generated on device, seed {args.seed}",
-                "config": {"workload": f"row-partitioned BFS, undirected R-MAT scale {scale} (= {args.scale} + "
-                                       f"log2 N) edgefactor {args.edgefactor}, B2SR-{d}",
-                           "scale": scale, "n": n, "tile_dim": d, "roots": args.steps,
-                           "parallelism": f"row-partitioned x{world}, frontier all-gather ({backend})",
-                           "l2": "inputs larger than L2 (B2SR %.2f GB)" % (b2sr_bytes / 1e9)},
-                "e2e": {"value": round(e2e_edges / (e2e_ms / 1e3) / 1e9, 4), "unit": "GTEPS",
-                        "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * n,
-                        "ms_per_step": round(e2e_ms / e2e_steps, 3),
-                        "includes": "H2D of every rank's B2SR row block from pinned memory, distributed BFS, "
-                                    "D2H of the levels on rank 0"},
-                "roofline": roofline, "gpu_launches": int(launches), "bfs_sweeps_per_root": iters[:4],
-                "per_gpu_gteps": round(value / world, 4),  # BASELINE north_star: per-GPU GTEPS at N GPUs
-                "clocks": clk.summary(), "tc": tc, "graph_gen_s": round(gen_s, 3)}
+        if world == 1 and not args.no_cpu:
+            line["cpu_baseline"] = None  # the s26 CPU leg is the --impl reference arm
         print(json.dumps(line), flush=True)
     tdist.destroy_process_group()
 
 
 # ---------------------------------------------------------------- reference arm
-def run_reference(args, rank, world):
+def run_reference(args, rank, world, workload):
     """The reference algorithm on host cores: the C restatement in oracle/ (the
-    reference is pure Python/numpy and cannot travel)."""
+    reference is pure Python/numpy and cannot travel), on our
+    arm's workload (s22 at one GPU, s26 for the strong-scaling runs), its
+    BFS transposing per call as algorithms.py:78 does."""
     if rank != 0:
         return
     from oracle import oracle as orc
 
     threads = os.cpu_count() or 1
     t0 = time.perf_counter()
-    scale = args.scale + (max(0, int(round(np.log2(world)))) if world > 1 else 0)  # our arm's graph
+    scale = args.scale5 if workload == "s26" else args.scale
     rp, ci = orc.rmat_csr(scale, args.edgefactor, seed=args.seed)
     n = 1 << scale
     d = args.dim or 4
@@ -688,7 +756,8 @@ def run_reference(args, rank, world):
     deg = np.diff(rp.astype(np.int64))
     roots = pick_roots(deg, args.warmup + args.steps + 8, seed=args.seed + 7)
     budget_s = 150.0
-    for r in roots[: args.warmup]:  # untimed warm-up roots (page-in, thread pool)
+    warm = args.warmup if workload == "s22" else 0  # s26: one root already takes about a minute
+    for r in roots[:warm]:  # untimed warm-up roots (page-in, thread pool)
         orc.bfs(m, r, workers=threads)
     edges, secs, done = 0, 0.0, 0
     for r in roots[args.warmup: args.warmup + args.steps]:
@@ -700,17 +769,35 @@ def run_reference(args, rank, world):
         if secs > budget_s:
             break
     v = edges / secs / 1e9
+    tb = d * (4 if d == 32 else 2 if d == 16 else 1)
+    b2sr_bytes = 4 * (len(m[2])) + len(m[3]) * (4 + tb)
+    cfg = workload_config(workload, args, scale, n, int(len(ci)), d, world, b2sr_bytes)
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GTEPS", "n_gpus": world,
-            "steps": done, "warmup": args.warmup, "ms_per_step": round(1e3 * secs / done, 2),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 bit-words",
-            "data": f"synthetic R-MAT seed {args.seed} (CPU twin of the device generator)",
-            "config": {"workload": f"BFS via masked bin-SpMV, undirected R-MAT scale {scale} "
-                                   f"edgefactor {args.edgefactor}, B2SR-{d}", "scale": scale, "tile_dim": d},
+            "steps": done, "warmup": warm, "ms_per_step": round(1e3 * secs / done, 2),
+            "higher_is_better": True, "scaling": "strong" if workload == "s26" else "weak", "vs_baseline": None,
+            "dtype": "u32 bit-words (b1 tiles)",
+            "data": f"synthetic R-MAT (Graph500 a,b,c=.57,.19,.19), seed {args.seed} (CPU twin of the device generator)",
+            "config": cfg,
             "cpu_baseline": {"value": round(v, 6), "unit": "GTEPS", "cores": threads, "kind": "port",
-                             "sample": f"{done} BFS roots incl. transpose (timed budget {budget_s:.0f} s)"},
+                             "sample": f"{done} BFS roots incl. the per-call transpose (timed budget {budget_s:.0f} s)"},
             "e2e": {"value": round(v, 6), "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "setup_s": round(setup, 2)}
     print(json.dumps(line), flush=True)
+
+
+def workload_config(workload, args, scale, n, nnz, d, world, b2sr_bytes):
+    """The config dict both arms print for a workload (identical keys and values)."""
+    if workload == "s26":
+        return {"workload": f"row-partitioned BFS, undirected R-MAT scale {scale} edgefactor {args.edgefactor}, "
+                            f"B2SR-{d}, strong scaling", "scale": scale, "n": n, "nnz": nnz, "tile_dim": d,
+                "roots": args.steps,
+                "parallelism": f"row-partitioned x{world}: a/at tile-row blocks balanced by tiles, "
+                               "all-to-all-v + all-gather-v of frontier words per level (NCCL)",
+                "l2": "inputs larger than L2 (B2SR %.2f GB)" % (b2sr_bytes / 1e9)}
+    return {"workload": f"BFS via masked bin-SpMV, undirected R-MAT scale {scale} edgefactor {args.edgefactor}, "
+                        f"B2SR-{d}", "scale": scale, "n": n, "nnz": nnz, "tile_dim": d, "roots": args.steps,
+            "parallelism": "single",
+            "l2": "inputs larger than L2 (B2SR %.2f GB > 126 MB)" % (b2sr_bytes / 1e9)}
 
 
 def main():
@@ -718,11 +805,21 @@ def main():
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    workload = args.workload if args.workload != "auto" else ("s26" if world > 1 else "s22")
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        run_reference(args, rank, world, workload)
         return
-    if world > 1:
-        run_dist(args, rank, world, local_rank)
+    if workload == "s26":
+        if "MASTER_ADDR" in os.environ:
+            run_dist(args, rank, world, local_rank)
+        else:  # one GPU without torchrun: the same native driver, NCCL world of one
+            import torch
+
+            torch.cuda.set_device(local_rank)
+            line = run_strong(args, 0, 1, local_rank, tdist=None, headline=True)
+            if not args.no_cpu:
+                line["cpu_baseline"] = cpu_baseline_s26(args)
+            print(json.dumps(line), flush=True)
         return
     run_ours(args, rank, world, local_rank)
 

@@ -50,6 +50,8 @@ enum {
 enum { B2SR_RING_BOOLEAN = 0, B2SR_RING_ARITHMETIC = 1, B2SR_RING_MINPLUS = 2, B2SR_RING_MAXTIMES = 3 };
 
 typedef struct b2sr_matrix b2sr_matrix;
+typedef struct b2sr_comm b2sr_comm;          /* one rank's communicator (multi-GPU) */
+typedef struct b2sr_dist_bfs b2sr_dist_bfs;  /* one rank's row-partitioned BFS plan */
 
 /* ---- library ----------------------------------------------------------- */
 const char *b2sr_last_error(void);
@@ -78,6 +80,12 @@ int b2sr_profile_rows(uint32_t n, uint32_t dim, const uint32_t *d_row_ptr, const
                       const uint32_t *d_rows, uint32_t m, uint64_t *tiles, uint64_t *nnz, void *stream);
 /* Adopt existing arrays (already validated on the host, e.g. a B2srMatrix
  * built by the caller): copies from host pointers into a new device matrix. */
+/* Host -> device copy of `bytes` from h_src (any host memory).  Pageable
+ * sources are staged through the library's page-locked chunks, filled by
+ * several host threads while the previous chunk's DMA runs; h_src may be
+ * reused once the call returns.  b2sr_from_host / b2sr_block_from_host
+ * upload this way. */
+int b2sr_h2d(void *d_dst, const void *h_src, uint64_t bytes, void *stream);
 int b2sr_from_host(uint32_t n, uint32_t dim, const uint32_t *h_trp, const uint32_t *h_tci,
                    const void *h_tiles, uint64_t num_tiles, void *stream, b2sr_matrix **out);
 int b2sr_free(b2sr_matrix *m);
@@ -126,6 +134,12 @@ int b2sr_bmv_bbf(const b2sr_matrix *m, const void *d_x, const void *d_keep, doub
  * A zero scale at a used column fails with B2SR_EINVAL and *bad_col = j. */
 int b2sr_bmv_bff(const b2sr_matrix *m, const double *d_x, int ring, double inc, const double *d_scale,
                  const void *d_keep, double *d_y, int64_t *bad_col, void *stream);
+/* As b2sr_bmv_bff with the semiring's add identity given explicitly
+ * (Semiring.add_identity, semirings.py:18-21): every output element starts
+ * from it and masked-off positions hold it (kernels.py:176, 249).
+ * b2sr_bmv_bff uses the built-in identities (+inf min-plus, else 0). */
+int b2sr_bmv_bff_ex(const b2sr_matrix *m, const double *d_x, int ring, double inc, double add_identity,
+                    const double *d_scale, const void *d_keep, double *d_y, int64_t *bad_col, void *stream);
 
 /* ---- bin-SpGEMM (kernels.py:298-367) ----------------------------------- */
 /* bmm_bin_bin_sum: sum of all entries of A @ B (int64). */
@@ -215,6 +229,52 @@ int b2sr_rmat_edges(int scale, uint64_t m, uint64_t seed, uint32_t *d_src, uint3
  * d_col_ind must hold (symmetrize ? 2m : m) entries; *nnz returned. */
 int b2sr_coo_to_csr(uint32_t n, uint64_t m, const uint32_t *d_src, const uint32_t *d_dst, int symmetrize,
                     int drop_loops, uint32_t *d_row_ptr, uint32_t *d_col_ind, uint64_t *nnz, void *stream);
+
+
+/* ---- multi-GPU: row-partitioned drivers ---------------- */
+/* The reference's only parallelism is contiguous tile-row chunks
+ * (kernels.py:44-57); here the chunks are GPUs.  One communicator per rank
+ * (one process per GPU, or one host thread per GPU):
+ *   b2sr_comm_unique_id  rank 0 makes the NCCL id (128 bytes), the caller
+ *                        ships it to the other ranks (e.g. torch.distributed)
+ *   b2sr_comm_init       NCCL communicator of `rank` of `world` on the
+ *                        current device (libnccl opened at run time)
+ *   b2sr_comm_init_local `world` thread-ranks sharing the current device,
+ *                        exchanging through device copies (tests: the same
+ *                        level loop with N ranks on one GPU); outs[world]
+ * Every collective is enqueued on the caller's stream. */
+int b2sr_comm_unique_id(uint8_t *out128);
+int b2sr_comm_init(const uint8_t *id128, int world, int rank, b2sr_comm **out);
+int b2sr_comm_init_local(int world, b2sr_comm **outs);
+int b2sr_comm_free(b2sr_comm *comm);
+/* In-place int64 sum over ranks (NCCL all-reduce). */
+int b2sr_comm_allreduce_sum_i64(b2sr_comm *comm, int64_t *d, uint64_t count, void *stream);
+/* bfs (algorithms.py:75-93) over row blocks, direction-optimizing and
+ * device-controlled like b2sr_bfs (d = 4, 8).  Each rank holds the rows
+ * [begin, end) of a (push) and of at (pull), cut where at's tile prefix
+ * crosses k/world of its tiles; frontier, visited and levels are global on
+ * every rank.  Per level: push/pull over the blocks, an all-to-all-v of the
+ * row contributions, OR-merge, an all-gather-v of the merged rows; the level
+ * plan runs on the device from global counters, identically on every rank,
+ * and the host polls a mapped snapshot ring (no sync per level).
+ *   b2sr_dist_bfs_plan         from the full a / at on every rank's device
+ *   b2sr_dist_bfs_plan_blocks  from this rank's blocks (not copied: keep them
+ *                              alive) and the global tile_row_ptr of a / at
+ *                              (device or host pointers, ntr+1 entries)
+ * b2sr_dist_bfs_run: levels f64[n] on every rank, *iterations as b2sr_bfs. */
+int b2sr_dist_bfs_plan(b2sr_comm *comm, const b2sr_matrix *a, const b2sr_matrix *at, void *stream,
+                       b2sr_dist_bfs **out);
+int b2sr_dist_bfs_plan_blocks(b2sr_comm *comm, const b2sr_matrix *a_block, const b2sr_matrix *at_block,
+                              const uint32_t *tile_row_ptr_a, const uint32_t *tile_row_ptr_at, void *stream,
+                              b2sr_dist_bfs **out);
+int b2sr_dist_bfs_rows(const b2sr_dist_bfs *plan, uint32_t *begin, uint32_t *end);
+int b2sr_dist_bfs_run(b2sr_dist_bfs *plan, uint32_t src, double *d_levels, int64_t *iterations, void *stream);
+int b2sr_dist_bfs_free(b2sr_dist_bfs *plan);
+/* triangle_count's masked SpGEMM (algorithms.py:199-215, kernels.py:323-367)
+ * with the lower triangle L replicated and its tile rows (the mask) cut into
+ * blocks of equal estimated work; one int64 all-reduce.  rows_out (world+1,
+ * may be NULL) receives the cuts. */
+int b2sr_dist_tc(b2sr_comm *comm, const b2sr_matrix *lower, int64_t *count, uint32_t *rows_out, void *stream);
 
 #ifdef __cplusplus
 }

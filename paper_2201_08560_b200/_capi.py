@@ -49,6 +49,19 @@ SIGNATURES = {
     "b2sr_bmv_bbb": [P, P, P, P, P],
     "b2sr_bmv_bbf": [P, P, P, P, P],
     "b2sr_bmv_bff": [P, P, i32, f64, P, P, P, P, P],
+    "b2sr_bmv_bff_ex": [P, P, i32, f64, f64, P, P, P, P, P],
+    "b2sr_h2d": [P, P, u64, P],
+    "b2sr_comm_unique_id": [P],
+    "b2sr_comm_init": [P, i32, i32, PP],
+    "b2sr_comm_init_local": [i32, P],
+    "b2sr_comm_free": [P],
+    "b2sr_comm_allreduce_sum_i64": [P, P, u64, P],
+    "b2sr_dist_bfs_plan": [P, P, P, P, PP],
+    "b2sr_dist_bfs_plan_blocks": [P, P, P, P, P, P, PP],
+    "b2sr_dist_bfs_rows": [P, P, P],
+    "b2sr_dist_bfs_run": [P, u32, P, P, P],
+    "b2sr_dist_bfs_free": [P],
+    "b2sr_dist_tc": [P, P, P, P, P],
     "b2sr_bmm_sum": [P, P, P, P],
     "b2sr_bmm_sum_masked_bt": [P, P, P, P, P],
     "b2sr_bfs": [P, P, u32, P, P, P],

@@ -162,6 +162,13 @@ struct b2sr_matrix {
 
 namespace b2sr {
 
+// The built-in add identity of a semiring (semirings.py:54-63): +inf for
+// min-plus, 0 otherwise.  Public Semiring objects may carry any identity
+// (b2sr_bmv_bff_ex passes it through).
+inline double ring_identity(int ring) {
+    return ring == B2SR_RING_MINPLUS ? __builtin_huge_val() : 0.0;
+}
+
 inline int word_bytes(int d) { return d == 32 ? 4 : (d == 16 ? 2 : 1); }
 inline uint32_t tile_rows(uint32_t n, uint32_t d) { return (n + d - 1) / d; }
 inline size_t padded_vec_bytes(uint32_t ntr, int d) { return ((size_t)ntr * word_bytes(d) + 3) / 4 * 4; }
@@ -170,10 +177,13 @@ b2sr_matrix *new_matrix(uint32_t n, uint32_t dim, uint32_t ntr, uint64_t T, cuda
 void free_matrix(b2sr_matrix *m);
 void ensure_items(b2sr_matrix *m, cudaStream_t s);  // bin-SpMV work partition
 int num_sms();
+// host -> device copy; pageable sources are staged through page-locked
+// chunks at the link rate (staging.cu)
+void h2d(void *dst, const void *src, size_t bytes, cudaStream_t s);
 void launch_row_ids(const b2sr_matrix *m, uint32_t *rowid, cudaStream_t s);  // rowid[t] = tile row of t
 void free_vlong(void *plan);
 void *build_vlong(b2sr_matrix *m, uint32_t thresh, cudaStream_t s);
-void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
+void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, double ident, const void *keep, double *y,
                   cudaStream_t s, const std::function<void(cudaStream_t)> &overlap = {}, const uint32_t *gtci = nullptr);
 // hot.cu: the S most referenced tile columns' x words live in shared memory
 constexpr uint32_t HOT_SMEM_BYTES = 131072;  // 128 KB: the rest of the 228 KB stays L1 for the cold gathers and streams
@@ -200,7 +210,7 @@ void free_stream(void *plan);
 // bmv_bff.cu: float gather over the rows with <= thresh tiles
 // gtci: the column array the gathers index x with (m->tci, or the relabelled
 // one of bmv_xperm.cu with x relabelled to match)
-void launch_bff_rows(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
+void launch_bff_rows(b2sr_matrix *m, const double *x, int ring, double inc, double ident, const void *keep, double *y,
                      uint32_t thresh, cudaStream_t s, bool plan_only = false, const uint32_t *gtci = nullptr);
 void free_bff(void *plan);
 // bmv_xperm.cu: hot-first relabelling of x for the float gather

@@ -42,9 +42,13 @@ struct BfsSnap {
 // bit-rows of every listed chunk of a into next (visited != null: bits of
 // visited vertices dropped first; the update masks them either way); pull
 // levels stream at.
+// Row blocks (multi-GPU): push reads the frontier words of a's rows at
+// `pfrontier` (the global frontier shifted to the block) and scatters into
+// the global-length `pnext`; pull writes the block's rows at `next`.  NULL:
+// pfrontier = frontier, pnext = next (one GPU).
 void launch_bfs_level(b2sr_matrix *at, const b2sr_matrix *a, BfsCtl *ctl, const uint2 *push_list,
                       const uint32_t *active_list, const void *hx, size_t hb, const void *frontier, void *next,
-                      const void *visited, cudaStream_t s);
+                      const void *visited, cudaStream_t s, const void *pfrontier = nullptr, void *pnext = nullptr);
 // Top-down level of the push-only BFS (no transpose; d = 4, 8): the listed
 // chunks of a, bits of visited vertices dropped before the scatter.
 void launch_bfs_push_level(const b2sr_matrix *a, const BfsCtl *ctl, const uint2 *push_list, const void *frontier,

@@ -279,3 +279,84 @@ int b2sr_tc_work(const b2sr_matrix *lower, int64_t *count, uint64_t *work, void 
 }
 
 }  // extern "C"
+
+// ================================================================ row-partitioned triangle count
+// L replicated on every rank, the mask (L's tile rows) cut into
+// contiguous blocks of equal estimated work -- per mask tile (I, J) the
+// shorter of rows I and J (the intersection's search length) plus one -- each
+// rank counts its block with K8, and one int64 all-reduce sums the counts.
+namespace b2sr {
+
+__global__ void k_tc_row_work(uint32_t ntr, const uint32_t *__restrict__ trp, const uint32_t *__restrict__ tci,
+                              unsigned long long *__restrict__ work) {
+    const uint32_t lane = lane_id(), warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t I = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; I < ntr; I += warps) {
+        const uint32_t t0 = trp[I], t1 = trp[I + 1], li = t1 - t0;
+        unsigned long long w = 0;
+        for (uint32_t t = t0 + lane; t < t1; t += 32) {
+            const uint32_t J = tci[t], lj = trp[J + 1] - trp[J];
+            w += (li < lj ? li : lj) + 1;
+        }
+        for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        if (lane == 0) work[I] = w;
+    }
+}
+
+__global__ void k_work_cuts(const uint64_t *__restrict__ pre, uint32_t ntr, int world, uint32_t *__restrict__ cuts) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k > world) return;
+    if (k == 0 || k == world) {
+        cuts[k] = k ? ntr : 0;
+        return;
+    }
+    const unsigned long long target = (unsigned long long)pre[ntr] * k / world;
+    uint32_t lo = 0, hi = ntr;
+    while (lo < hi) {
+        uint32_t mid = lo + (hi - lo) / 2;
+        if (pre[mid] < target) lo = mid + 1;
+        else hi = mid;
+    }
+    cuts[k] = lo;
+}
+
+}  // namespace b2sr
+
+#include "dist_comm.cuh"
+
+extern "C" int b2sr_dist_tc(b2sr_comm *comm, const b2sr_matrix *lower, int64_t *count, uint32_t *rows_out,
+                            void *stream) {
+    API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    if (lower->row0 || lower->ntr != tile_rows(lower->n, lower->dim))
+        B2SR_THROW(B2SR_EINVAL, "b2sr_dist_tc needs the full (replicated) lower triangle");
+    Exchange *ex = comm->ex;
+    const int W = ex->world, R = ex->rank;
+    const uint32_t ntr = lower->ntr;
+    Buf<unsigned long long> work(ntr + 1, s);
+    Buf<uint64_t> pre(ntr + 1, s);
+    Buf<uint32_t> cuts(W + 1, s);
+    CK(cudaMemsetAsync(work.p, 0, 8 * ((size_t)ntr + 1), s));
+    LAUNCH(k_tc_row_work, grid_for((uint64_t)ntr * 32), 256, 0, s, ntr, lower->trp, lower->tci, work.p);
+    exclusive_scan_u64(reinterpret_cast<const uint64_t *>(work.p), pre.p, (size_t)ntr + 1, s);
+    LAUNCH(k_work_cuts, 1, 64 * ((W + 64) / 64), 0, s, pre.p, ntr, W, cuts.p);
+    std::vector<uint32_t> rows(W + 1);
+    CK(cudaMemcpyAsync(rows.data(), cuts.p, 4 * (W + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (rows_out) std::copy(rows.begin(), rows.end(), rows_out);
+    b2sr_matrix *blk = nullptr;
+    int rc = b2sr_row_block(lower, rows[R], rows[R + 1], s, &blk);
+    if (rc) throw Error{rc, std::string()};
+    int64_t mine = 0;
+    try {
+        mine = bmm_masked_bt(lower, lower, blk, s);
+    } catch (...) {
+        free_matrix(blk);
+        throw;
+    }
+    free_matrix(blk);
+    Buf<int64_t> tot(1, s);
+    CK(cudaMemcpyAsync(tot.p, &mine, 8, cudaMemcpyHostToDevice, s));
+    ex->allreduce_sum_i64(tot.p, 1, s);
+    *count = read_scalar(tot.p, s);
+    API_END
+}

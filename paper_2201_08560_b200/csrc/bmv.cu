@@ -404,11 +404,11 @@ void launch_bbf(b2sr_matrix *m, const void *x, const void *keep, double *y, cuda
 // (bmv_bff.cu), overlapped with the hub rows' segmented scatter + warp folds
 // (bmv_vlong.cu).
 void launch_bff(const b2sr_matrix *m_, const double *x, int ring, double inc, const void *keep, double *y,
-                cudaStream_t s) {
+                cudaStream_t s, double ident) {
     b2sr_matrix *m = const_cast<b2sr_matrix *>(m_);
     ensure_vlong(m, s);
     const uint32_t hi = vlong_thresh(m->dim);
-    launch_bff_rows(m, x, ring, inc, keep, y, hi, s, /*plan_only=*/true);
+    launch_bff_rows(m, x, ring, inc, ident, keep, y, hi, s, /*plan_only=*/true);
     // large x: gather from a hot-first relabelled copy (bmv_xperm.cu)
     Buf<double> xp;
     const uint32_t *gtci = nullptr;
@@ -418,8 +418,8 @@ void launch_bff(const b2sr_matrix *m_, const double *x, int ring, double inc, co
         gtci = xperm_apply(m, x, xp.p, s);
         x = xp.p;
     }
-    launch_vlong(m, x, ring, inc, keep, y, s,
-                 [&](cudaStream_t so) { launch_bff_rows(m, x, ring, inc, keep, y, hi, so, false, gtci); }, gtci);
+    launch_vlong(m, x, ring, inc, ident, keep, y, s,
+                 [&](cudaStream_t so) { launch_bff_rows(m, x, ring, inc, ident, keep, y, hi, so, false, gtci); }, gtci);
 }
 }  // namespace b2sr
 
@@ -441,6 +441,11 @@ int b2sr_bmv_bbf(const b2sr_matrix *m, const void *d_x, const void *d_keep, doub
 
 int b2sr_bmv_bff(const b2sr_matrix *m, const double *d_x, int ring, double inc, const double *d_scale,
                  const void *d_keep, double *d_y, int64_t *bad_col, void *stream) {
+    return b2sr_bmv_bff_ex(m, d_x, ring, inc, ring_identity(ring), d_scale, d_keep, d_y, bad_col, stream);
+}
+
+int b2sr_bmv_bff_ex(const b2sr_matrix *m, const double *d_x, int ring, double inc, double add_identity,
+                    const double *d_scale, const void *d_keep, double *d_y, int64_t *bad_col, void *stream) {
     API_BEGIN
     cudaStream_t s = (cudaStream_t)stream;
     if (ring == B2SR_RING_BOOLEAN)
@@ -459,7 +464,7 @@ int b2sr_bmv_bff(const b2sr_matrix *m, const double *d_x, int ring, double inc, 
         }
         x = xs.p;
     }
-    launch_bff(m, x, ring, inc, d_keep, d_y, s);
+    launch_bff(m, x, ring, inc, d_keep, d_y, s, add_identity);
     API_END
 }
 

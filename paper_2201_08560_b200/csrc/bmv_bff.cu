@@ -150,11 +150,10 @@ template <int D, int RING>
 __global__ void __launch_bounds__(BFF_THREADS, 4) k_bff_rows(uint32_t n_rows, const uint32_t *__restrict__ rows, uint32_t n,
                                                          const uint32_t *__restrict__ trp, const uint32_t *__restrict__ tci,
                                                          const uint8_t *__restrict__ tiles, const double *__restrict__ x,
-                                                         double inc, const void *__restrict__ keep,
+                                                         double inc, double ident, const void *__restrict__ keep,
                                                          double *__restrict__ y, uint32_t row0) {
     constexpr uint32_t GPW = 32 / D;
     const uint32_t lane = lane_id(), r = lane % D;
-    const double ident = RING == B2SR_RING_MINPLUS ? __longlong_as_double(0x7FF0000000000000ll) : 0.0;
     const uint32_t groups = ((gridDim.x * blockDim.x) >> 5) * GPW;
     for (uint32_t i = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * GPW + lane / D; i < n_rows; i += groups) {
         const uint32_t I = rows[i];
@@ -184,7 +183,7 @@ __global__ void __launch_bounds__(BFF_THREADS, 4) k_bff_rows(uint32_t n_rows, co
 }
 
 template <int D>
-static void bff_rows_ring(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
+static void bff_rows_ring(b2sr_matrix *m, const double *x, int ring, double inc, double ident, const void *keep, double *y,
                           uint32_t thresh, cudaStream_t s, const uint32_t *gtci) {
     BffPlan *p = static_cast<BffPlan *>(m->bff);  // built by a plan_only call on the caller's stream
     if (!p || !p->n_rows) return;
@@ -195,25 +194,25 @@ static void bff_rows_ring(b2sr_matrix *m, const double *x, int ring, double inc,
     const uint8_t *tl = (const uint8_t *)m->tiles;
     if (ring == B2SR_RING_ARITHMETIC)
         LAUNCH((k_bff_rows<D, B2SR_RING_ARITHMETIC>), g, BFF_THREADS, 0, s, p->n_rows, p->rows, m->n, m->trp, gtci, tl,
-               x, inc, keep, y, m->row0);
+               x, inc, ident, keep, y, m->row0);
     else if (ring == B2SR_RING_MINPLUS)
         LAUNCH((k_bff_rows<D, B2SR_RING_MINPLUS>), g, BFF_THREADS, 0, s, p->n_rows, p->rows, m->n, m->trp, gtci, tl,
-               x, inc, keep, y, m->row0);
+               x, inc, ident, keep, y, m->row0);
     else
         LAUNCH((k_bff_rows<D, B2SR_RING_MAXTIMES>), g, BFF_THREADS, 0, s, p->n_rows, p->rows, m->n, m->trp, gtci, tl,
-               x, inc, keep, y, m->row0);
+               x, inc, ident, keep, y, m->row0);
 }
 
-void launch_bff_rows(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
+void launch_bff_rows(b2sr_matrix *m, const double *x, int ring, double inc, double ident, const void *keep, double *y,
                      uint32_t thresh, cudaStream_t s, bool plan_only, const uint32_t *gtci) {
     bff_plan(m, thresh, s);
     if (plan_only) return;
     if (!gtci) gtci = m->tci;
     switch (m->dim) {
-        case 4: bff_rows_ring<4>(m, x, ring, inc, keep, y, thresh, s, gtci); break;
-        case 8: bff_rows_ring<8>(m, x, ring, inc, keep, y, thresh, s, gtci); break;
-        case 16: bff_rows_ring<16>(m, x, ring, inc, keep, y, thresh, s, gtci); break;
-        default: bff_rows_ring<32>(m, x, ring, inc, keep, y, thresh, s, gtci); break;
+        case 4: bff_rows_ring<4>(m, x, ring, inc, ident, keep, y, thresh, s, gtci); break;
+        case 8: bff_rows_ring<8>(m, x, ring, inc, ident, keep, y, thresh, s, gtci); break;
+        case 16: bff_rows_ring<16>(m, x, ring, inc, ident, keep, y, thresh, s, gtci); break;
+        default: bff_rows_ring<32>(m, x, ring, inc, ident, keep, y, thresh, s, gtci); break;
     }
 }
 

@@ -416,11 +416,12 @@ __global__ void __launch_bounds__(NT, 1)
                 const uint32_t *__restrict__ alist, uint64_t T, const uint4 *__restrict__ desc,
                 const uint32_t *__restrict__ trp, const uint8_t *__restrict__ tiles, const uint32_t *__restrict__ tci2,
                 const void *__restrict__ hx, uint32_t hx_bytes16, uint32_t S, const void *__restrict__ frontier,
-                void *__restrict__ next, const void *__restrict__ visited) {
+                void *__restrict__ next, const void *__restrict__ visited, const void *__restrict__ pfrontier,
+                void *__restrict__ pnext) {
     const int mode = ctl->mode;
     if (mode == BFS_NONE) return;
     if (mode == BFS_PUSH) {
-        push_entries<D>(ctl->list_n, plist, a_trp, a_tci, a_tiles, frontier, next, visited);
+        push_entries<D>(ctl->list_n, plist, a_trp, a_tci, a_tiles, pfrontier, pnext, visited);
         return;
     }
     const bool listed = mode == BFS_PULL_ACTIVE;
@@ -460,7 +461,9 @@ void launch_bfs_push_level(const b2sr_matrix *a, const BfsCtl *ctl, const uint2 
 
 void launch_bfs_level(b2sr_matrix *at, const b2sr_matrix *a, BfsCtl *ctl, const uint2 *push_list,
                       const uint32_t *active_list, const void *hx, size_t hb, const void *frontier, void *next,
-                      const void *visited, cudaStream_t s) {
+                      const void *visited, cudaStream_t s, const void *pfrontier, void *pnext) {
+    if (!pfrontier) pfrontier = frontier;
+    if (!pnext) pnext = next;
     StreamPlan *sp = stream_plan(at, LT, s);
     HotView hv = hot_view(at, s);
     const unsigned g = (unsigned)num_sms();
@@ -470,12 +473,12 @@ void launch_bfs_level(b2sr_matrix *at, const b2sr_matrix *a, BfsCtl *ctl, const 
         hot_smem_attr(k_bfs_level<4, 1024>, hb);
         LAUNCH((k_bfs_level<4, 1024>), g, 1024, hb, s, ctl, push_list, atrp, atci, atl, sp->n_loads, active_list,
                at->num_tiles, sp->desc, at->trp, (const uint8_t *)at->tiles, hv.tci2, hx, (uint32_t)hb, hv.S,
-               frontier, next, visited);
+               frontier, next, visited, pfrontier, pnext);
     } else {
         hot_smem_attr(k_bfs_level<8, 768>, hb);
         LAUNCH((k_bfs_level<8, 768>), g, 768, hb, s, ctl, push_list, atrp, atci, atl, sp->n_loads, active_list,
                at->num_tiles, sp->desc, at->trp, (const uint8_t *)at->tiles, hv.tci2, hx, (uint32_t)hb, hv.S,
-               frontier, next, visited);
+               frontier, next, visited, pfrontier, pnext);
     }
 }
 

@@ -403,9 +403,9 @@ __device__ __forceinline__ double vring_op(double cur, double term, double inc) 
 }
 
 template <int D, int RING>
-__device__ __forceinline__ void vlong_store(uint32_t k, double acc, const uint32_t *__restrict__ rows, uint32_t n,
-                                            const void *__restrict__ keep, double *__restrict__ y, uint32_t row0) {
-    const double ident = RING == B2SR_RING_MINPLUS ? __longlong_as_double(0x7FF0000000000000ll) : 0.0;
+__device__ __forceinline__ void vlong_store(uint32_t k, double acc, double ident, const uint32_t *__restrict__ rows,
+                                            uint32_t n, const void *__restrict__ keep, double *__restrict__ y,
+                                            uint32_t row0) {
     const uint32_t I = rows[k / D], r = k % D, grow = row0 + I;
     if ((uint64_t)grow * D + r < n) {
         if (keep && !((load_word<D>(keep, grow) >> r) & 1u)) acc = ident;
@@ -421,10 +421,9 @@ __global__ void __launch_bounds__(256) k_vlong_fold_lanes(uint32_t n_small, cons
                                                           const uint32_t *__restrict__ rows,
                                                           const uint64_t *__restrict__ base,
                                                           const uint32_t *__restrict__ total,
-                                                          const double *__restrict__ terms, double inc, uint32_t n,
+                                                          const double *__restrict__ terms, double inc, double ident, uint32_t n,
                                                           const void *__restrict__ keep, double *__restrict__ y,
                                                           uint32_t row0) {
-    const double ident = RING == B2SR_RING_MINPLUS ? __longlong_as_double(0x7FF0000000000000ll) : 0.0;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_small; i += gridDim.x * blockDim.x) {
         const uint32_t k = order[i];
         const uint64_t b0 = base[k];
@@ -442,7 +441,7 @@ __global__ void __launch_bounds__(256) k_vlong_fold_lanes(uint32_t n_small, cons
             acc = vring_op<RING>(acc, e.x, inc); acc = vring_op<RING>(acc, e.y, inc);
         }
         for (; q < nt; q++) acc = vring_op<RING>(acc, p[q], inc);
-        vlong_store<D, RING>(k, acc, rows, n, keep, y, row0);
+        vlong_store<D, RING>(k, acc, ident, rows, n, keep, y, row0);
     }
 }
 
@@ -462,12 +461,11 @@ __global__ void __launch_bounds__(256) k_vlong_fold(uint32_t n_big, const uint32
                                                     const uint32_t *__restrict__ rows,
                                                     const uint64_t *__restrict__ base,
                                                     const uint32_t *__restrict__ total,
-                                                    const double *__restrict__ terms, double inc, uint32_t n,
+                                                    const double *__restrict__ terms, double inc, double ident, uint32_t n,
                                                     const void *__restrict__ keep, double *__restrict__ y,
                                                     uint32_t row0) {
     __shared__ double2 sbuf[256 / 32][16];
-    const double ident = RING == B2SR_RING_MINPLUS ? __longlong_as_double(0x7FF0000000000000ll) : 0.0;
-    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n_big; i += warps) {
         const uint32_t k = order[n_big - 1 - i];  // largest first: the longest chain starts at once
@@ -522,7 +520,7 @@ __global__ void __launch_bounds__(256) k_vlong_fold(uint32_t n_big, const uint32
                 if (lane + o < 32) acc = vring_op<RING == B2SR_RING_MINPLUS ? RING_MIN_COMBINE : RING>(acc, other, 0.0);
             }
         }
-        if (lane == 0) vlong_store<D, RING>(k, acc, rows, n, keep, y, row0);
+        if (lane == 0) vlong_store<D, RING>(k, acc, ident, rows, n, keep, y, row0);
     }
 }
 
@@ -539,7 +537,7 @@ static cudaStream_t side_stream(int which = 0) {
 
 // Scatter, then the folds; `overlap` runs while the hub folds proceed on the
 // side stream (the main stream waits for them before returning).
-void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
+void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, double ident, const void *keep, double *y,
                   cudaStream_t s, const std::function<void(cudaStream_t)> &overlap, const uint32_t *gtci) {
     const uint32_t *tci = gtci ? gtci : m->tci;  // gather columns (relabelled with x, or the matrix's)
     VLongPlan *v = static_cast<VLongPlan *>(m->vlong);
@@ -580,15 +578,15 @@ void launch_vlong(b2sr_matrix *m, const double *x, int ring, double inc, const v
         if (s2) {                                                                                                   \
             hot_smem_attr(k_vlong_fold<DD, RR>, top_smem);                                                          \
             LAUNCH((k_vlong_fold<DD, RR>), std::min<uint32_t>(v->n_big_top, (uint32_t)num_sms()), 32, top_smem, s2, \
-                   v->n_big_top, v->big_top, v->rows, v->base, v->total, v->terms, inc, m->n, keep, y, m->row0);    \
+                   v->n_big_top, v->big_top, v->rows, v->base, v->total, v->terms, inc, ident, m->n, keep, y, m->row0);    \
         }                                                                                                           \
         scatter(v->top_units, v->n_units);                                                                          \
         if (v->n_big_rest)                                                                                          \
             LAUNCH((k_vlong_fold<DD, RR>), gr, 256, 0, s, v->n_big_rest, v->big_rest, v->rows, v->base, v->total,   \
-                   v->terms, inc, m->n, keep, y, m->row0);                                                          \
+                   v->terms, inc, ident, m->n, keep, y, m->row0);                                                          \
         if (v->n_small)                                                                                             \
             LAUNCH((k_vlong_fold_lanes<DD, RR>), gl, 256, 0, s, v->n_small, v->order, v->rows, v->base, v->total,   \
-                   v->terms, inc, m->n, keep, y, m->row0);                                                          \
+                   v->terms, inc, ident, m->n, keep, y, m->row0);                                                          \
     } while (0)
 #define VL_DIM(DD)                                                                                                  \
     do {                                                                                                            \

@@ -111,6 +111,10 @@ void free_matrix(b2sr_matrix *m) {
     int cur = 0;
     cudaGetDevice(&cur);
     if (cur != m->device) cudaSetDevice(m->device);
+    // Kernels reading this matrix may still be queued on a caller's
+    // non-blocking stream, which the NULL-stream frees below are not ordered
+    // after: wait for the device first (what a plain cudaFree would do).
+    cudaDeviceSynchronize();
     dfree(m->trp, nullptr);
     dfree(m->tci, nullptr);
     dfree(m->tiles, nullptr);
@@ -215,10 +219,10 @@ int b2sr_from_host(uint32_t n, uint32_t dim, const uint32_t *h_trp, const uint32
     uint32_t ntr = tile_rows(n, dim);
     b2sr_matrix *m = new_matrix(n, dim, ntr, num_tiles, s);
     try {
-        CK(cudaMemcpyAsync(m->trp, h_trp, ((size_t)ntr + 1) * 4, cudaMemcpyHostToDevice, s));
+        h2d(m->trp, h_trp, ((size_t)ntr + 1) * 4, s);
         if (num_tiles) {
-            CK(cudaMemcpyAsync(m->tci, h_tci, num_tiles * 4, cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(m->tiles, h_tiles, num_tiles * dim * word_bytes(dim), cudaMemcpyHostToDevice, s));
+            h2d(m->tci, h_tci, num_tiles * 4, s);
+            h2d(m->tiles, h_tiles, num_tiles * dim * word_bytes(dim), s);
         }
     } catch (...) {
         free_matrix(m);
@@ -294,10 +298,10 @@ int b2sr_block_from_host(uint32_t n, uint32_t dim, uint32_t tr_begin, uint32_t t
     b2sr_matrix *m = new_matrix(n, dim, rows, num_tiles, s);
     m->row0 = tr_begin;
     try {
-        CK(cudaMemcpyAsync(m->trp, h_trp, ((size_t)rows + 1) * 4, cudaMemcpyHostToDevice, s));
+        h2d(m->trp, h_trp, ((size_t)rows + 1) * 4, s);
         if (num_tiles) {
-            CK(cudaMemcpyAsync(m->tci, h_tci, num_tiles * 4, cudaMemcpyHostToDevice, s));
-            CK(cudaMemcpyAsync(m->tiles, h_tiles, num_tiles * dim * word_bytes(dim), cudaMemcpyHostToDevice, s));
+            h2d(m->tci, h_tci, num_tiles * 4, s);
+            h2d(m->tiles, h_tiles, num_tiles * dim * word_bytes(dim), s);
         }
     } catch (...) {
         free_matrix(m);

@@ -22,11 +22,12 @@
 
 #include "bfs_ctl.cuh"
 #include "bmv_common.cuh"
+#include "dist_comm.cuh"
 
 namespace b2sr {
 
 void launch_bff(const b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
-                cudaStream_t s);
+                cudaStream_t s, double ident);
 void used_column_words(const b2sr_matrix *m, uint32_t *colw, cudaStream_t s);
 
 static unsigned grid_for(uint64_t work) {
@@ -890,7 +891,9 @@ __global__ void k_bfs_prep(BfsCtl *__restrict__ c, uint32_t ntr, const uint32_t 
                            const uint32_t *__restrict__ cols, const void *__restrict__ frontier,
                            uint8_t *__restrict__ hx, uint32_t n_loads, const uint4 *__restrict__ desc,
                            const void *__restrict__ visited, const void *__restrict__ live,
-                           uint32_t *__restrict__ alist) {
+                           uint32_t *__restrict__ alist, const void *__restrict__ pfrontier) {
+    // row blocks: pfrontier / visited are shifted to the block's first row
+    // (a and at blocks share the row range); frontier stays global (hot fill)
     const int mode = c->mode;
     if (mode == BFS_NONE) return;
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
@@ -899,7 +902,7 @@ __global__ void k_bfs_prep(BfsCtl *__restrict__ c, uint32_t ntr, const uint32_t 
         const uint32_t iters = (ntr + stride - 1) / stride;
         for (uint32_t it = 0; it < iters; it++) {
             uint32_t I = tid + it * stride, nch = 0, len = 0;
-            if (I < ntr && load_word<D>(frontier, I)) {
+            if (I < ntr && load_word<D>(pfrontier, I)) {
                 len = a_trp[I + 1] - a_trp[I];
                 nch = (len + PUSH_CH - 1) / PUSH_CH;
             }
@@ -1021,7 +1024,7 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     long long sweeps = 0;
     for (uint32_t L = 1;; L++) {
         LAUNCH(k_bfs_prep<D>, gp, 256, 0, s, ctl.p, ntr, ta, list.p, hv.S, hv.cols, frontier, hx.p, n_loads, desc,
-               visited.p, at->live, alist.p);
+               visited.p, at->live, alist.p, frontier);
         launch_bfs_level(at, a, ctl.p, list.p, alist.p, hx.p, hb, frontier, next, push_vis ? visited.p : nullptr, s);
         LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L, ta,
                at->trp, (const uint4 *)at->live, ctl.p, (uint4 *)frontier, 1, alpha,
@@ -1089,7 +1092,7 @@ static void bfs_push_only(const b2sr_matrix *a, uint32_t src, double *d_levels, 
     long long sweeps = 0;
     for (uint32_t L = 1;; L++) {
         LAUNCH(k_bfs_prep<D>, gp, 256, 0, s, ctl.p, ntr, a->trp, list.p, 0u, nullptr, frontier, nullptr, 0u, nullptr,
-               visited.p, nullptr, nullptr);
+               visited.p, nullptr, nullptr, frontier);
         launch_bfs_push_level(a, ctl.p, list.p, frontier, push_vis ? visited.p : nullptr, next, s);
         LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L, a->trp,
                nullptr, nullptr, ctl.p, (uint4 *)frontier, 1, 0.0, (unsigned long long)a->num_tiles, 1, snaps.dev, L, active_frac);
@@ -1119,6 +1122,193 @@ static void bfs_push_only(const b2sr_matrix *a, uint32_t src, double *d_levels, 
 static bool bfs_devctl_enabled(const b2sr_matrix *at) {
     const char *e = getenv("B2SR_BFS_DEVCTL");  // B2SR_BFS_DEVCTL=0: host-controlled levels (A/B)
     return pull_stream(at) && !(e && e[0] == '0');
+}
+
+
+// ================================================================ row-partitioned BFS (multi-GPU)
+// both a and at are cut into the same contiguous tile-row
+// blocks, balanced by at's tile count (the pull work); every rank keeps the
+// global frontier / visited / levels and the global row lengths of a and at
+// plus at's row-liveness words (small next to its block), so each rank
+// evaluates the single-GPU driver's level plan on identical data -- the
+// direction of every level is chosen on the device, identically on every
+// rank, with no collective and no host round trip.  Per level:
+//   prep     push list over the block's rows of a / hot x words + active loads
+//   level    push: the block's frontier rows of a scatter into a global-length
+//            contribution; pull: the block's rows of at (K4 flat stream)
+//   exchange each rank's contribution to every other rank's rows
+//            (grouped send/recv: an all-to-all-v of bit words)
+//   merge    own rows = own contribution | the received ones
+//   gather   all-gather-v of the merged row blocks -> global next
+//   update   the single-GPU level update + plan on the global next
+// Levels and sweep counts equal the single-GPU driver's bit for bit (the
+// per-level vertex set is the same OR of the same bits).
+}  // namespace b2sr
+
+struct b2sr_dist_bfs {
+    b2sr::Exchange *ex = nullptr;       // not owned
+    b2sr_matrix *a = nullptr, *at = nullptr;
+    bool owns_blocks = false;
+    uint32_t n = 0, dim = 0, ntr = 0;   // global
+    uint32_t *trp_a = nullptr, *trp_at = nullptr;  // global tile-row offsets (device)
+    void *live_at = nullptr;            // global row-liveness words (n16 * 16 bytes)
+    uint64_t live_tiles = 0, tiles_at = 0;
+    std::vector<uint32_t> rows;         // world + 1 tile-row boundaries
+    std::vector<size_t> off, len;       // byte ranges of the blocks in a global bit vector
+    size_t n16 = 0, maxlen = 0;
+    ~b2sr_dist_bfs() {
+        if (owns_blocks) {
+            b2sr::free_matrix(a);
+            b2sr::free_matrix(at);
+        }
+        b2sr::dfree(trp_a, nullptr);
+        b2sr::dfree(trp_at, nullptr);
+        b2sr::dfree(live_at, nullptr);
+    }
+};
+
+namespace b2sr {
+
+// rows = multiple of `align`, boundaries where at's tile prefix crosses k*T/world
+__global__ void k_balanced_cuts(const uint32_t *__restrict__ trp, uint32_t ntr, int world, uint32_t align,
+                                uint32_t *__restrict__ cuts) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k > world) return;
+    if (k == 0 || k == world) {
+        cuts[k] = k ? ntr : 0;
+        return;
+    }
+    const unsigned long long target = (unsigned long long)trp[ntr] * k / world;
+    uint32_t lo = 0, hi = ntr;  // first row whose prefix reaches the target
+    while (lo < hi) {
+        uint32_t mid = lo + (hi - lo) / 2;
+        if ((unsigned long long)trp[mid] < target) lo = mid + 1;
+        else hi = mid;
+    }
+    uint32_t r = (lo + align / 2) / align * align;
+    cuts[k] = r < ntr ? r : ntr;
+}
+
+// own rows of the global next = own contribution | every peer's contribution
+__global__ void k_or_merge(uint4 *__restrict__ dst, const uint4 *__restrict__ own, const uint4 *__restrict__ recv,
+                           uint32_t n16, uint32_t stride16, int parts) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x) {
+        uint4 v = own[i];
+        for (int p = 0; p < parts; p++) {
+            uint4 w = recv[(size_t)p * stride16 + i];
+            v.x |= w.x; v.y |= w.y; v.z |= w.z; v.w |= w.w;
+        }
+        dst[i] = v;
+    }
+}
+
+static void dist_layout(b2sr_dist_bfs *p) {
+    const int W = p->ex->world;
+    const int wb = word_bytes(p->dim);
+    const size_t vb = padded_vec_bytes(p->ntr, p->dim);
+    p->n16 = (vb + 15) / 16;
+    p->off.assign(W, 0);
+    p->len.assign(W, 0);
+    p->maxlen = 0;
+    for (int r = 0; r < W; r++) {  // a block at the very end may be empty
+        p->off[r] = p->rows[r] >= p->ntr ? p->n16 * 16 : (size_t)p->rows[r] * wb;
+        size_t end = (r + 1 == W || p->rows[r + 1] >= p->ntr) ? p->n16 * 16 : (size_t)p->rows[r + 1] * wb;
+        if (p->off[r] % 16 || end % 16) B2SR_THROW(B2SR_EINVAL, "row blocks must start on 16-byte words");
+        p->len[r] = end - p->off[r];
+        p->maxlen = std::max(p->maxlen, p->len[r]);
+    }
+}
+
+static uint32_t row_align(int dim) { return 16 / word_bytes(dim); }
+
+template <int D>
+static void dist_bfs_run(b2sr_dist_bfs *p, uint32_t src, double *d_levels, int64_t *iterations, cudaStream_t s) {
+    Exchange &ex = *p->ex;
+    const int W = ex.world, R = ex.rank;
+    const uint32_t n = p->n, ntr = p->ntr;
+    b2sr_matrix *a = p->a, *at = p->at;
+    const size_t vbytes = p->n16 * 16, off = p->off[R];
+    Buf<uint8_t> visited(vbytes, s), fa(vbytes, s), fb(vbytes, s), contrib(vbytes, s);
+    Buf<uint8_t> recv(std::max<size_t>(1, (size_t)(W - 1) * p->maxlen), s);
+    Buf<BfsCtl> ctl(1, s);
+    Buf<uint2> list((size_t)a->ntr + a->num_tiles / PUSH_CH + 1, s);
+    ensure_live(at, s);  // block-local liveness (active-load lists)
+    HotView hv = at->num_tiles ? hot_view(at, s) : HotView{0, nullptr, nullptr};
+    const size_t hb = hot_fill_bytes(hv, D);
+    Buf<uint8_t> hx(hb, s);
+    CK(cudaMemsetAsync(hx.p, 0, hb, s));
+    uint32_t n_loads = 0;
+    const uint4 *desc = at->num_tiles ? stream_desc(at, s, &n_loads) : nullptr;
+    Buf<uint32_t> alist(std::max<uint32_t>(n_loads, 1), s);
+    const double alpha = bfs_alpha();
+    const char *afe = getenv("B2SR_BFS_ACTIVE");
+    const double active_frac = afe ? atof(afe) : 0.5;
+    const bool trace = getenv("B2SR_BFS_TRACE") != nullptr;
+    LAUNCH(k_fill_f64, grid_for(n), 256, 0, s, d_levels, (size_t)n, HUGE_VAL);
+    CK(cudaMemsetAsync(visited.p, 0, vbytes, s));
+    CK(cudaMemsetAsync(fb.p, 0, vbytes, s));
+    CK(cudaMemsetAsync(fa.p, 0, vbytes, s));
+    CK(cudaMemsetAsync(contrib.p, 0, vbytes, s));
+    LAUNCH(k_bfs_seed, 1, 1, 0, s, src, (uint32_t)D, d_levels, fa.p, fb.p);
+    CK(cudaMemsetAsync(fa.p, 0, vbytes, s));
+    LAUNCH(k_bfs_ctl_init, 1, 1, 0, s, ctl.p, (unsigned long long)p->live_tiles);
+    const unsigned gu = grid_for(p->n16);
+    BfsSnapshots &snaps = bfs_snapshots();
+    snaps.reset();
+    LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)fb.p, (uint4 *)visited.p, d_levels, 0.0, p->trp_a,
+           p->trp_at, (const uint4 *)p->live_at, ctl.p, nullptr, 0, alpha, (unsigned long long)p->tiles_at, 1,
+           snaps.dev, 0u, active_frac);
+    // the exchange pattern is the same every level
+    std::vector<Xfer> sends, recvs;
+    for (int q = 0, k = 0; q < W; q++) {
+        if (q == R) continue;
+        if (p->len[q]) sends.push_back({q, contrib.p + p->off[q], p->len[q]});
+        if (p->len[R]) recvs.push_back({q, recv.p + (size_t)k * p->maxlen, p->len[R]});
+        k++;
+    }
+    const uint32_t own16 = (uint32_t)(p->len[R] / 16);
+    const unsigned gm = grid_for(own16);
+    void *frontier = fb.p, *next = fa.p;
+    const unsigned gp = (unsigned)num_sms() * 8;
+    const uint8_t *vis_blk = visited.p + off;
+    int done = 0;
+    long long sweeps = 0;
+    for (uint32_t L = 1;; L++) {
+        const uint8_t *fr = static_cast<const uint8_t *>(frontier);
+        LAUNCH(k_bfs_prep<D>, gp, 256, 0, s, ctl.p, a->ntr, a->trp, list.p, hv.S, hv.cols, frontier, hx.p, n_loads,
+               desc, vis_blk, at->live, alist.p, fr + off);
+        if (at->num_tiles || a->num_tiles)
+            launch_bfs_level(at, a, ctl.p, list.p, alist.p, hx.p, hb, frontier, contrib.p + off, nullptr, s, fr + off,
+                             contrib.p);
+        ex.sendrecv(sends, recvs, s);
+        LAUNCH(k_or_merge, gm, 256, 0, s, reinterpret_cast<uint4 *>(static_cast<uint8_t *>(next) + off),
+               reinterpret_cast<const uint4 *>(contrib.p + off), reinterpret_cast<const uint4 *>(recv.p), own16,
+               (uint32_t)(p->maxlen / 16), W - 1);
+        ex.allgatherv(next, p->off, p->len, s);
+        LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L,
+               p->trp_a, p->trp_at, (const uint4 *)p->live_at, ctl.p, (uint4 *)contrib.p, 1, alpha,
+               (unsigned long long)p->tiles_at, 1, snaps.dev, L, active_frac);
+        std::swap(frontier, next);
+        if (trace || L > LOOKAHEAD) {
+            const uint32_t Lc = trace ? L : L - LOOKAHEAD;
+            const volatile BfsSnap *sn = snaps.slot(Lc);
+            while (sn->level != Lc) {
+                const cudaError_t q = cudaStreamQuery(s);
+                if (q != cudaErrorNotReady && sn->level != Lc) {
+                    CK(q);
+                    B2SR_THROW(B2SR_ECUDA, "BFS level %u finished without its outcome", Lc);
+                }
+                std::this_thread::yield();
+            }
+            done = sn->done;
+            sweeps = sn->sweeps;
+            if (trace) fprintf(stderr, "[b2sr dist bfs r%d] after level %u: done=%d sweeps=%lld\n", R, Lc, done, sweeps);
+            if (done) break;
+        }
+        if (L > n + 2 + LOOKAHEAD) B2SR_THROW(B2SR_ENOCONV, "BFS failed to drain its frontier");
+    }
+    CK(cudaStreamSynchronize(s));
+    *iterations = sweeps;
 }
 
 }  // namespace b2sr
@@ -1292,7 +1482,7 @@ int b2sr_sssp(const b2sr_matrix *at, uint32_t src, double *d_dist, int64_t *iter
     CK(cudaMemsetAsync(d_dist + src, 0, sizeof(double), s));
     int64_t sweeps = 0;
     for (uint32_t it = 0; it + 1 < n; it++) {  // for _ in range(n - 1)
-        launch_bff(at, d_dist, B2SR_RING_MINPLUS, 1.0, nullptr, y.p, s);
+        launch_bff(at, d_dist, B2SR_RING_MINPLUS, 1.0, nullptr, y.p, s, ring_identity(B2SR_RING_MINPLUS));
         CK(cudaMemsetAsync(changed.p, 0, sizeof(int), s));
         LAUNCH(k_relax, grid_for(n), 256, 0, s, (size_t)n, d_dist, y.p, changed.p);
         sweeps++;
@@ -1360,7 +1550,7 @@ int b2sr_pagerank(const b2sr_matrix *a, const double *d_out_degree, double alpha
         for (auto &e : ev) CK(cudaEventCreate(&e));
     while (sweeps < max_iter) {
         if (trace) CK(cudaEventRecord(ev[0], s));
-        launch_bff(a, xs.p, B2SR_RING_ARITHMETIC, 0.0, nullptr, g.p, s);
+        launch_bff(a, xs.p, B2SR_RING_ARITHMETIC, 0.0, nullptr, g.p, s, 0.0);
         if (trace) CK(cudaEventRecord(ev[1], s));
         LAUNCH(k_pr_update, grid_for(n), 256, 0, s, n, teleport, alpha, g.p, d_out_degree, d_rank, xs.p, diff.p);
         pw.run(diff.p, s);
@@ -1414,7 +1604,7 @@ int b2sr_cc(const b2sr_matrix *a, double *d_labels, int64_t *iterations, void *s
                 LAUNCH(k_cc_min<8>, gi, 256, 0, s, am->items, am->n_items, n, gtci, (const uint8_t *)a->tiles, gl,
                        mu.p);
         } else {
-            launch_bff(a, d_labels, B2SR_RING_MINPLUS, 0.0, nullptr, m.p, s);
+            launch_bff(a, d_labels, B2SR_RING_MINPLUS, 0.0, nullptr, m.p, s, ring_identity(B2SR_RING_MINPLUS));
         }
         sweeps++;
         CK(cudaMemcpyAsync(nxt.p, lab_u.p, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
@@ -1431,6 +1621,161 @@ int b2sr_cc(const b2sr_matrix *a, double *d_labels, int64_t *iterations, void *s
         if (sweeps > (int64_t)n + 1) B2SR_THROW(B2SR_ENOCONV, "component labels failed to stabilise");
     }
     *iterations = sweeps;
+    API_END
+}
+
+}  // extern "C"
+
+// ================================================================ row-partitioned drivers: C ABI
+namespace b2sr {
+
+static void check_block_pair(const b2sr_matrix *a, const b2sr_matrix *at) {
+    if (!a || !at) B2SR_THROW(B2SR_EINVAL, "distributed bfs needs a and its transpose");
+    if (a->n != at->n || a->dim != at->dim) B2SR_THROW(B2SR_EINVAL, "a and at must share n and tile width");
+    if (a->dim > 8) B2SR_THROW(B2SR_EINVAL, "the device-controlled distributed bfs supports tile dims 4 and 8");
+}
+
+static b2sr_matrix *block_of(const b2sr_matrix *m, uint32_t b, uint32_t e, cudaStream_t s) {
+    b2sr_matrix *out = nullptr;
+    int rc = b2sr_row_block(m, b, e, s, &out);
+    if (rc) throw Error{rc, std::string()};
+    return out;
+}
+
+static uint32_t *copy_u32(const uint32_t *src, size_t count, cudaStream_t s) {
+    uint32_t *d = static_cast<uint32_t *>(dalloc(count * 4 + 16, s));
+    CK(cudaMemcpyAsync(d, src, count * 4, cudaMemcpyDefault, s));
+    return d;
+}
+
+}  // namespace b2sr
+
+extern "C" {
+
+int b2sr_dist_bfs_plan(b2sr_comm *comm, const b2sr_matrix *a_c, const b2sr_matrix *at_c, void *stream,
+                       b2sr_dist_bfs **out) {
+    API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    check_block_pair(a_c, at_c);
+    b2sr_matrix *a = const_cast<b2sr_matrix *>(a_c), *at = const_cast<b2sr_matrix *>(at_c);
+    if (a->row0 || at->row0 || a->ntr != tile_rows(a->n, a->dim) || at->ntr != a->ntr)
+        B2SR_THROW(B2SR_EINVAL, "b2sr_dist_bfs_plan needs the full matrices (see b2sr_dist_bfs_plan_blocks)");
+    Exchange *ex = comm->ex;
+    auto *p = new b2sr_dist_bfs();
+    try {
+        p->ex = ex;
+        p->n = at->n;
+        p->dim = at->dim;
+        p->ntr = at->ntr;
+        ensure_live(at, s);
+        p->live_tiles = at->live_tiles;
+        p->tiles_at = at->num_tiles;
+        // cuts balanced by at's tiles, on 16-byte word boundaries of the bit vectors
+        Buf<uint32_t> cuts(ex->world + 1, s);
+        LAUNCH(k_balanced_cuts, 1, 64 * ((ex->world + 64) / 64), 0, s, at->trp, at->ntr, ex->world,
+               row_align(at->dim), cuts.p);
+        p->rows.resize(ex->world + 1);
+        CK(cudaMemcpyAsync(p->rows.data(), cuts.p, 4 * (ex->world + 1), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        dist_layout(p);
+        const uint32_t b = p->rows[ex->rank], e = p->rows[ex->rank + 1];
+        p->a = block_of(a, b, e, s);
+        p->at = block_of(at, b, e, s);
+        p->owns_blocks = true;
+        p->trp_a = copy_u32(a->trp, (size_t)p->ntr + 1, s);
+        p->trp_at = copy_u32(at->trp, (size_t)p->ntr + 1, s);
+        p->live_at = dalloc(p->n16 * 16, s);
+        CK(cudaMemsetAsync(p->live_at, 0, p->n16 * 16, s));
+        CK(cudaMemcpyAsync(p->live_at, at->live, padded_vec_bytes(p->ntr, p->dim), cudaMemcpyDeviceToDevice, s));
+        CK(cudaStreamSynchronize(s));
+    } catch (...) {
+        delete p;
+        throw;
+    }
+    *out = p;
+    API_END
+}
+
+int b2sr_dist_bfs_plan_blocks(b2sr_comm *comm, const b2sr_matrix *a_blk, const b2sr_matrix *at_blk,
+                              const uint32_t *trp_a, const uint32_t *trp_at, void *stream, b2sr_dist_bfs **out) {
+    API_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    check_block_pair(a_blk, at_blk);
+    if (a_blk->row0 != at_blk->row0 || a_blk->ntr != at_blk->ntr)
+        B2SR_THROW(B2SR_EINVAL, "a and at blocks must cover the same tile rows");
+    Exchange *ex = comm->ex;
+    const int W = ex->world, R = ex->rank;
+    auto *p = new b2sr_dist_bfs();
+    try {
+        p->ex = ex;
+        p->n = at_blk->n;
+        p->dim = at_blk->dim;
+        p->ntr = tile_rows(p->n, p->dim);
+        p->a = const_cast<b2sr_matrix *>(a_blk);
+        p->at = const_cast<b2sr_matrix *>(at_blk);
+        ensure_live(p->at, s);
+        // every rank's (first row, rows, live tiles): an all-reduce of one-hot slots
+        Buf<int64_t> meta(3 * (size_t)W, s);
+        std::vector<int64_t> h(3 * (size_t)W, 0);
+        h[3 * R] = at_blk->row0;
+        h[3 * R + 1] = at_blk->ntr;
+        h[3 * R + 2] = (int64_t)p->at->live_tiles;
+        CK(cudaMemcpyAsync(meta.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, s));
+        ex->allreduce_sum_i64(meta.p, h.size(), s);
+        CK(cudaMemcpyAsync(h.data(), meta.p, h.size() * 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        p->rows.resize(W + 1);
+        for (int r = 0; r < W; r++) {
+            if (h[3 * r] != (r ? (int64_t)p->rows[r] : 0))
+                B2SR_THROW(B2SR_EINVAL, "row blocks must be contiguous and in rank order");
+            p->rows[r] = (uint32_t)h[3 * r];
+            p->rows[r + 1] = (uint32_t)(h[3 * r] + h[3 * r + 1]);
+            p->live_tiles += (uint64_t)h[3 * r + 2];
+        }
+        if (p->rows[W] != p->ntr) B2SR_THROW(B2SR_EINVAL, "row blocks must cover every tile row");
+        dist_layout(p);
+        p->trp_a = copy_u32(trp_a, (size_t)p->ntr + 1, s);
+        p->trp_at = copy_u32(trp_at, (size_t)p->ntr + 1, s);
+        CK(cudaMemcpyAsync(&p->tiles_at, p->trp_at + p->ntr, 4, cudaMemcpyDeviceToHost, s));
+        // global liveness: every block's words at its offset, then all-gathered
+        p->live_at = dalloc(p->n16 * 16, s);
+        CK(cudaMemsetAsync(p->live_at, 0, p->n16 * 16, s));
+        const size_t own = (size_t)at_blk->ntr * word_bytes(p->dim);
+        if (own) CK(cudaMemcpyAsync(static_cast<char *>(p->live_at) + p->off[R], p->at->live, own,
+                                    cudaMemcpyDeviceToDevice, s));
+        ex->allgatherv(p->live_at, p->off, p->len, s);
+        CK(cudaStreamSynchronize(s));
+        p->tiles_at &= 0xFFFFFFFFull;
+    } catch (...) {
+        p->a = p->at = nullptr;
+        delete p;
+        throw;
+    }
+    *out = p;
+    API_END
+}
+
+int b2sr_dist_bfs_rows(const b2sr_dist_bfs *p, uint32_t *begin, uint32_t *end) {
+    API_BEGIN
+    *begin = p->rows[p->ex->rank];
+    *end = p->rows[p->ex->rank + 1];
+    API_END
+}
+
+int b2sr_dist_bfs_run(b2sr_dist_bfs *p, uint32_t src, double *d_levels, int64_t *iterations, void *stream) {
+    API_BEGIN
+    if (src >= p->n) B2SR_THROW(B2SR_EINVAL, "source vertex %u out of range for n=%u", src, p->n);
+    if (p->dim == 4) dist_bfs_run<4>(p, src, d_levels, iterations, (cudaStream_t)stream);
+    else dist_bfs_run<8>(p, src, d_levels, iterations, (cudaStream_t)stream);
+    API_END
+}
+
+int b2sr_dist_bfs_free(b2sr_dist_bfs *p) {
+    API_BEGIN
+    if (p) {
+        cudaDeviceSynchronize();
+        delete p;
+    }
     API_END
 }
 

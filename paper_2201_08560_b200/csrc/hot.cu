@@ -17,6 +17,7 @@
 // whole x fits (S = number of tile columns), cols is the identity and tci2 is
 // the matrix's own tci.  Nothing about the tiles or their order changes, so
 // the outputs are exactly those of the plain kernels.
+#include <map>
 #include <mutex>
 #include <unordered_map>
 
@@ -159,9 +160,13 @@ void hot_fill(const HotView &hv, int dim, const void *x, void *hx, cudaStream_t 
 
 void hot_smem_attr_raw(const void *kernel, size_t bytes) {
     static std::mutex mu;
-    static std::unordered_map<const void *, size_t> set;  // kernel -> dynamic smem limit already set
+    // (device, kernel) -> dynamic smem limit already set: the attribute is per
+    // device context, so a second GPU in the same process sets its own
+    static std::map<std::pair<int, const void *>, size_t> set;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(mu);
-    size_t &cur = set[kernel];
+    size_t &cur = set[{dev, kernel}];
     if (bytes <= cur) return;
     size_t b = std::max<size_t>(bytes, HOT_SMEM_BYTES + 16);
     CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)b));

@@ -169,6 +169,120 @@ def block_from_host(n: int, dim: int, begin: int, end: int, host) -> _Handle:
                        tiles.ctypes.data, len(tci), dev.stream())
 
 
+# ---------------------------------------------------------------- native multi-GPU drivers
+class Comm:
+    """One rank's communicator inside the C library (b2sr_comm_*).
+
+    ``Comm.from_torch(dist)``: NCCL over NVLink / NVSwitch, one process per
+    GPU; rank 0 makes the NCCL id and ``torch.distributed`` ships it.
+    ``Comm.nccl_single()``: a world of one (same code path, one GPU).
+    ``Comm.local(world)``: ``world`` thread-ranks sharing the current GPU
+    (the multi-rank level loop testable on one device)."""
+
+    def __init__(self, ptr: int, rank: int, world: int):
+        self.ptr, self.rank, self.world = ptr, rank, world
+
+    @classmethod
+    def from_torch(cls, dist) -> "Comm":
+        rank, world = dist.get_rank(), dist.get_world_size()
+        box = [None]
+        if rank == 0:
+            uid = (ctypes.c_uint8 * 128)()
+            _capi.call("b2sr_comm_unique_id", ctypes.addressof(uid))
+            box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0)
+        uid = (ctypes.c_uint8 * 128).from_buffer_copy(box[0])
+        out = ctypes.c_void_p()
+        _capi.call("b2sr_comm_init", ctypes.addressof(uid), world, rank, ctypes.byref(out))
+        return cls(out.value, rank, world)
+
+    @classmethod
+    def nccl_single(cls) -> "Comm":
+        uid = (ctypes.c_uint8 * 128)()
+        _capi.call("b2sr_comm_unique_id", ctypes.addressof(uid))
+        out = ctypes.c_void_p()
+        _capi.call("b2sr_comm_init", ctypes.addressof(uid), 1, 0, ctypes.byref(out))
+        return cls(out.value, 0, 1)
+
+    @classmethod
+    def local(cls, world: int) -> list:
+        outs = (ctypes.c_void_p * world)()
+        _capi.call("b2sr_comm_init_local", world, ctypes.addressof(outs))
+        return [cls(outs[r], r, world) for r in range(world)]
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and _capi._lib is not None:
+            _capi._lib.b2sr_comm_free(self.ptr)
+            self.ptr = None
+
+
+class NativeDistributedBfs:
+    """bfs (algorithms.py:75-93) over row blocks of a and at, direction-
+    optimizing and device-controlled (b2sr_dist_bfs_*; d = 4, 8): the level
+    loop, its exchanges (all-to-all-v of row contributions + all-gather-v of
+    the merged rows) and the level plan run in the library on the caller's
+    stream, with no host sync per level.  Levels end up on every rank."""
+
+    def __init__(self, comm: Comm, plan: int, n: int, keep=()):
+        self.comm, self.plan, self.n = comm, plan, n
+        self._keep = keep  # blocks a plan_blocks plan points into
+
+    @classmethod
+    def from_matrices(cls, comm: Comm, a: B2srMatrix, at: B2srMatrix) -> "NativeDistributedBfs":
+        """Every rank holds the full a and at; the plan cuts its blocks
+        (balanced by at's tiles) -- the full matrices may be dropped after."""
+        out = ctypes.c_void_p()
+        ha, hat = a.handle(), at.handle()
+        _capi.call("b2sr_dist_bfs_plan", comm.ptr, ha.ptr, hat.ptr, dev.stream(), ctypes.byref(out))
+        return cls(comm, out.value, a.n)
+
+    @classmethod
+    def from_blocks(cls, comm: Comm, a_block: _Handle, at_block: _Handle, trp_a, trp_at) -> "NativeDistributedBfs":
+        """This rank's blocks (e.g. uploaded with block_from_host) and the
+        global tile_row_ptr arrays of a and at (host numpy or device tensors)."""
+        def ptr(x):
+            return x.data_ptr() if dev.is_cuda_tensor(x) else np.ascontiguousarray(x, np.uint32).ctypes.data
+
+        keep = [np.ascontiguousarray(x, np.uint32) if not dev.is_cuda_tensor(x) else x for x in (trp_a, trp_at)]
+        out = ctypes.c_void_p()
+        _capi.call("b2sr_dist_bfs_plan_blocks", comm.ptr, a_block.ptr, at_block.ptr, ptr(keep[0]), ptr(keep[1]),
+                   dev.stream(), ctypes.byref(out))
+        return cls(comm, out.value, a_block.n, keep=(a_block, at_block))
+
+    @property
+    def rows(self):
+        b, e = ctypes.c_uint32(), ctypes.c_uint32()
+        _capi.call("b2sr_dist_bfs_rows", self.plan, ctypes.addressof(b), ctypes.addressof(e))
+        return b.value, e.value
+
+    def run(self, src: int, to_host: bool = True, levels=None, stream=None):
+        """(levels float64[n], sweeps); ``to_host=False`` keeps the levels on
+        the device (a CUDA tensor view)."""
+        lv = levels if levels is not None else dev.empty_bytes(8 * self.n)
+        it = ctypes.c_int64()
+        _capi.call("b2sr_dist_bfs_run", self.plan, int(src), dev.ptr(lv), ctypes.addressof(it),
+                   stream if stream is not None else dev.stream())
+        if not to_host:
+            return lv.view(dev.torch().float64)[: self.n], int(it.value)
+        return dev.to_host(lv, np.float64, self.n), int(it.value)
+
+    def __del__(self):
+        if getattr(self, "plan", None) and _capi._lib is not None:
+            _capi._lib.b2sr_dist_bfs_free(self.plan)
+            self.plan = None
+
+
+def native_triangle_count(comm: Comm, lower: B2srMatrix, stream=None):
+    """(count, cuts): the masked SpGEMM of triangle_count with L replicated and
+    its mask rows cut by estimated work (b2sr_dist_tc); one int64 all-reduce."""
+    out = ctypes.c_int64()
+    cuts = (ctypes.c_uint32 * (comm.world + 1))()
+    h = lower.handle()
+    _capi.call("b2sr_dist_tc", comm.ptr, h.ptr, ctypes.addressof(out), ctypes.addressof(cuts),
+               stream if stream is not None else dev.stream())
+    return int(out.value), list(cuts)
+
+
 # ---------------------------------------------------------------- float-gather drivers
 def _slices(n: int, dim: int, world: int, rank: int):
     """(vertex begin, valid count, padded slice length) of this rank's rows."""
@@ -196,6 +310,20 @@ def distributed_pagerank(at: B2srMatrix, out_degree, dist, alpha: float = 0.85, 
     t = dev.torch()
     rank, world = dist.get_rank(), dist.get_world_size()
     n, d = at.n, at.dim
+    out_degree = np.asarray(out_degree, dtype=np.float64).reshape(-1)
+    if out_degree.shape != (n,):
+        raise ValueError(f"expected a length-{n} out-degree vector")
+    # the check of algorithms.py:143-148 (and of the single-GPU driver): a
+    # vertex with out-edges (a used column of the transposed matrix) must not
+    # have a zero out-degree -- every rank sees the whole matrix, so every
+    # rank raises the same error
+    ud = dev.empty_bytes(max(n, 16))
+    _capi.call("b2sr_used_columns", at.handle().ptr, dev.ptr(ud), dev.stream())
+    used = dev.to_host(ud, np.uint8, n).astype(bool)
+    bad = np.flatnonzero(used & (out_degree == 0.0))
+    if bad.size:
+        j = int(bad[0])
+        raise ValueError(f"out_degree[{j}] is zero but vertex {j} has out-edges")
     b, e, v0, cnt, per = _slices(n, d, world, rank)
     blk = _new_handle("b2sr_row_block", at.handle().ptr, b, e, dev.stream())
     full = per * world

@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes
 import struct
+import threading
 import weakref
 from dataclasses import dataclass
 
@@ -298,7 +299,7 @@ class B2srMatrix:
     """
 
     __slots__ = ("n", "tile_dim", "_trp", "_tci", "_tiles", "_h", "_num_tiles", "_transpose", "_nodiag",
-                 "_bfs_push", "__weakref__")
+                 "_bfs_push", "_lock", "__weakref__")
 
     def __init__(self, n, tile_dim, tile_row_ptr, tile_col_ind, bit_tiles):
         n = int(n)
@@ -341,6 +342,10 @@ class B2srMatrix:
         self._transpose = None
         self._nodiag = None
         self._bfs_push = 0  # push-only BFS calls made without a transpose (algorithms.bfs)
+        # guards the lazily created device mirror, host arrays and cached
+        # transpose / diagonal-free twin: each is created once and never
+        # replaced, so a handle read from the matrix stays alive with it
+        self._lock = threading.RLock()
 
     @classmethod
     def _wrap(cls, h: _Handle) -> "B2srMatrix":
@@ -353,20 +358,32 @@ class B2srMatrix:
         self._transpose = None
         self._nodiag = None
         self._bfs_push = 0  # push-only BFS calls made without a transpose (algorithms.bfs)
+        # guards the lazily created device mirror, host arrays and cached
+        # transpose / diagonal-free twin: each is created once and never
+        # replaced, so a handle read from the matrix stays alive with it
+        self._lock = threading.RLock()
         return self
 
     # device mirror ---------------------------------------------------
     def handle(self) -> _Handle:
-        if self._h is None:
-            d = self.dim
-            self._h = _new_handle(
-                "b2sr_from_host", self.n, d, self._trp.ctypes.data, self._tci.ctypes.data,
-                self._tiles.ctypes.data, self._num_tiles, dev.stream())
-        return self._h
+        h = self._h
+        if h is None:
+            with self._lock:  # two threads' first kernel calls upload once
+                if self._h is None:
+                    self._h = _new_handle(
+                        "b2sr_from_host", self.n, self.dim, self._trp.ctypes.data, self._tci.ctypes.data,
+                        self._tiles.ctypes.data, self._num_tiles, dev.stream())
+                h = self._h
+        return h
 
     def _materialise(self):
         if self._trp is not None:
             return
+        with self._lock:
+            if self._trp is None:
+                self._download()
+
+    def _download(self):
         h = self._h
         trp = np.zeros(h.ntr + 1, np.uint32)
         tci = np.zeros(h.num_tiles, np.uint32)
@@ -589,14 +606,20 @@ def b2sr_transpose(m: B2srMatrix) -> B2srMatrix:
     Matrices are immutable, so the result is cached on ``m`` (and ``m`` on
     the result): repeated ``bfs``/``sssp`` calls transpose once.
     """
-    cached = m._transpose
-    if cached is not None:
-        t = cached() if isinstance(cached, weakref.ref) else cached
-        if t is not None:
-            return t
-    t = B2srMatrix._wrap(_new_handle("b2sr_transpose", m.handle().ptr, dev.stream()))
-    m._transpose = t
-    t._transpose = weakref.ref(m)  # no reference cycle: device memory is freed by refcounting
+    def cached():
+        c = m._transpose
+        return c() if isinstance(c, weakref.ref) else c
+
+    t = cached()
+    if t is not None:
+        return t
+    with m._lock:
+        t = cached()
+        if t is None:
+            h = m.handle()
+            t = B2srMatrix._wrap(_new_handle("b2sr_transpose", h.ptr, dev.stream()))
+            t._transpose = weakref.ref(m)  # no reference cycle: device memory is freed by refcounting
+            m._transpose = t
     return t
 
 
@@ -604,7 +627,10 @@ def drop_diagonal(m: B2srMatrix) -> B2srMatrix:
     """csr_to_b2sr(_drop_diagonal(b2sr_to_csr(m))) done in tile form (algorithms.py:96-101, 111).
     Matrices are immutable, so the result is cached on ``m`` (as transposes are)."""
     if m._nodiag is None:
-        m._nodiag = B2srMatrix._wrap(_new_handle("b2sr_drop_diagonal", m.handle().ptr, dev.stream()))
+        with m._lock:
+            if m._nodiag is None:
+                h = m.handle()
+                m._nodiag = B2srMatrix._wrap(_new_handle("b2sr_drop_diagonal", h.ptr, dev.stream()))
     return m._nodiag
 
 

@@ -161,9 +161,11 @@ def _bff(a: B2srMatrix, x, semiring: Semiring, scale, keep: BitVector | None) ->
     kd = _words_to_device(keep) if keep is not None else None
     y = dev.empty_bytes(8 * a.n)
     bad = ctypes.c_int64(-1)
-    _capi.call("b2sr_bmv_bff", h.ptr, dev.ptr(xd), _capi.RING[semiring.name], float(semiring.edge_increment),
-               dev.ptr(sd) if sd is not None else None, dev.ptr(kd) if kd is not None else None, dev.ptr(y),
-               ctypes.addressof(bad), dev.stream())
+    # the semiring's own add identity (kernels.py:176, 249): any float the
+    # public Semiring constructor accepts, e.g. Semiring("maxtimes", -inf)
+    _capi.call("b2sr_bmv_bff_ex", h.ptr, dev.ptr(xd), _capi.RING[semiring.name], float(semiring.edge_increment),
+               float(semiring.add_identity), dev.ptr(sd) if sd is not None else None,
+               dev.ptr(kd) if kd is not None else None, dev.ptr(y), ctypes.addressof(bad), dev.stream())
     return dev.to_host(y, np.float64, a.n)
 
 
