@@ -93,6 +93,14 @@ int b2sr_info(const b2sr_matrix *m, uint32_t *n, uint32_t *dim, uint32_t *ntr, u
 /* Device pointers of the three arrays (borrowed; valid until b2sr_free). */
 int b2sr_arrays(const b2sr_matrix *m, const uint32_t **trp, const uint32_t **tci, const void **tiles);
 /* Copy the three arrays to host buffers (sizes from b2sr_info). */
+/* from_host with the B2SR invariants of formats.py:242-295 checked on the
+ * device (b2sr_validate): B2SR_EFORMAT with the reference's message for the
+ * first violated one (row pointer start / monotone / last, column range,
+ * column order, empty tile, d=4 high nibble, padding rows, padding
+ * columns).  Used by load_b2sr (the .b2sr container, formats.py:533-554). */
+int b2sr_from_host_checked(uint32_t n, uint32_t dim, const uint32_t *h_trp, const uint32_t *h_tci,
+                           const void *h_tiles, uint64_t num_tiles, void *stream, b2sr_matrix **out);
+int b2sr_validate(const b2sr_matrix *m, void *stream);
 int b2sr_to_host(const b2sr_matrix *m, uint32_t *h_trp, uint32_t *h_tci, void *h_tiles, void *stream);
 /* b2sr_transpose (formats.py:477-489): K3, radix sort by tile column +
  * in-register bit transpose. */

@@ -51,6 +51,8 @@ SIGNATURES = {
     "b2sr_bmv_bff": [P, P, i32, f64, P, P, P, P, P],
     "b2sr_bmv_bff_ex": [P, P, i32, f64, f64, P, P, P, P, P],
     "b2sr_h2d": [P, P, u64, P],
+    "b2sr_from_host_checked": [u32, u32, P, P, P, u64, P, PP],
+    "b2sr_validate": [P, P],
     "b2sr_comm_unique_id": [P],
     "b2sr_comm_init": [P, i32, i32, PP],
     "b2sr_comm_init_local": [i32, P],

@@ -400,6 +400,30 @@ void launch_bbf(b2sr_matrix *m, const void *x, const void *keep, double *y, cuda
     }
 }
 
+// ARITHMETIC with add identity -0.0 (a public Semiring may carry it): the
+// reference adds +0.0 for every unset bit it walks (kernels.py:201-207,
+// cur + where(bit, term, 0.0)), which turns a -0.0 accumulator into +0.0; the
+// set-bit fold keeps -0.0.  They differ only where the fold ends at -0.0, so
+// those positions -- rare: every term was -0.0 -- are rescanned: if the
+// bit-row meets an unset bit in any tile of its tile row, the reference holds
+// +0.0.  Masked-off positions keep the identity.
+template <int D>
+__global__ void k_fix_negzero(uint32_t n, const uint32_t *__restrict__ trp, const typename WordT<D>::T *__restrict__ tiles,
+                              const void *__restrict__ keep, double *__restrict__ y, uint32_t row0, uint32_t nrows) {
+    constexpr uint32_t FULL = D == 32 ? 0xFFFFFFFFu : ((1u << D) - 1u);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nrows * D; i += gridDim.x * blockDim.x) {
+        const double v = y[i];
+        if (v != 0.0 || !signbit(v)) continue;
+        const uint32_t I = i / D, r = i % D, grow = row0 + I;
+        if ((uint64_t)grow * D + r >= n) continue;
+        if (keep && !((load_word<D>(keep, grow) >> r) & 1u)) continue;
+        const uint32_t t0 = trp[I], t1 = trp[I + 1];
+        uint32_t walked_unset = 0;
+        for (uint32_t t = t0; t < t1 && !walked_unset; t++) walked_unset = (uint32_t)tiles[(size_t)t * D + r] != FULL;
+        if (walked_unset) y[i] = 0.0;
+    }
+}
+
 // Rows up to the segmented-plan threshold: pipelined group-per-row walk
 // (bmv_bff.cu), overlapped with the hub rows' segmented scatter + warp folds
 // (bmv_vlong.cu).
@@ -420,6 +444,16 @@ void launch_bff(const b2sr_matrix *m_, const double *x, int ring, double inc, co
     }
     launch_vlong(m, x, ring, inc, ident, keep, y, s,
                  [&](cudaStream_t so) { launch_bff_rows(m, x, ring, inc, ident, keep, y, hi, so, false, gtci); }, gtci);
+    if (ring == B2SR_RING_ARITHMETIC && ident == 0.0 && std::signbit(ident) && m->ntr) {
+        unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)m->ntr * m->dim + 255) / 256,
+                                                                          (uint64_t)num_sms() * 8));
+        switch (m->dim) {
+            case 4: LAUNCH(k_fix_negzero<4>, g, 256, 0, s, m->n, m->trp, (const uint8_t *)m->tiles, keep, y, m->row0, m->ntr); break;
+            case 8: LAUNCH(k_fix_negzero<8>, g, 256, 0, s, m->n, m->trp, (const uint8_t *)m->tiles, keep, y, m->row0, m->ntr); break;
+            case 16: LAUNCH(k_fix_negzero<16>, g, 256, 0, s, m->n, m->trp, (const uint16_t *)m->tiles, keep, y, m->row0, m->ntr); break;
+            default: LAUNCH(k_fix_negzero<32>, g, 256, 0, s, m->n, m->trp, (const uint32_t *)m->tiles, keep, y, m->row0, m->ntr); break;
+        }
+    }
 }
 }  // namespace b2sr
 

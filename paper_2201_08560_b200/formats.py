@@ -85,15 +85,16 @@ def _index_array(a, what: str) -> np.ndarray:
     return out
 
 
-def _check_ptr(ptr: np.ndarray, length: int, total: int, what: str):
+def _check_ptr(ptr: np.ndarray, length: int, total: int, what: str, length_msg: str, last_msg: str):
+    """The row-pointer checks of formats.py:119-127 / 257-263, same messages."""
     if ptr.shape != (length,):
-        raise FormatError(f"{what} must have length {length}")
+        raise FormatError(length_msg)
     if ptr[0] != 0:
         raise FormatError(f"{what} must start at 0")
     if length > 1 and np.any(ptr[1:] < ptr[:-1]):
         raise FormatError(f"{what} must be non-decreasing")
     if int(ptr[-1]) != total:
-        raise FormatError(f"{what}[-1] must equal the entry count")
+        raise FormatError(last_msg)
 
 
 def _strictly_increasing_in_segments(ptr: np.ndarray, idx: np.ndarray) -> bool:
@@ -138,7 +139,8 @@ class CsrMatrix:
             raise FormatError("matrix dimension must be non-negative")
         rp = _index_array(row_ptr, "row_ptr")
         ci = _index_array(col_ind, "col_ind")
-        _check_ptr(rp, n + 1, len(ci), "row_ptr")
+        _check_ptr(rp, n + 1, len(ci), "row_ptr", f"row_ptr must have length n+1 = {n + 1}",
+                   "row_ptr[-1] must equal nnz")
         if len(ci) and int(ci.max()) >= n:
             raise FormatError("column index out of range")
         if not _strictly_increasing_in_segments(rp, ci):
@@ -310,7 +312,8 @@ class B2srMatrix:
         trp = _index_array(tile_row_ptr, "tile_row_ptr")
         tci = _index_array(tile_col_ind, "tile_col_ind")
         T = len(tci)
-        _check_ptr(trp, ntr + 1, T, "tile_row_ptr")
+        _check_ptr(trp, ntr + 1, T, "tile_row_ptr", f"tile_row_ptr must have length {ntr + 1}",
+                   "tile_row_ptr[-1] must equal the tile count")
         if T and int(tci.max()) >= ntr:
             raise FormatError("tile column index out of range")
         if not _strictly_increasing_in_segments(trp, tci):
@@ -657,15 +660,34 @@ def nonzero_density(csr: CsrMatrix) -> float:
 
 # ---------------------------------------------------------------- container
 def save_b2sr(m: B2srMatrix, path) -> None:
-    """Little-endian container: 28-byte header then the three raw arrays."""
+    """Little-endian container (formats.py:517-531): 28-byte header then the
+    three raw arrays.  A device-resident matrix is written straight from HBM
+    (one D2H per array into page-locked memory) without materialising -- and
+    caching -- host copies on the matrix."""
     with open(path, "wb") as fh:
         fh.write(_HEADER.pack(_MAGIC, _VERSION, m.n, m.dim, m.n_tile_rows, m.num_tiles))
-        fh.write(np.ascontiguousarray(m.tile_row_ptr, "<u4").tobytes())
-        fh.write(np.ascontiguousarray(m.tile_col_ind, "<u4").tobytes())
-        fh.write(np.ascontiguousarray(m.bit_tiles, m.tile_dim.word_dtype).tobytes())
+        if m._trp is not None:
+            fh.write(np.ascontiguousarray(m._trp, "<u4").tobytes())
+            fh.write(np.ascontiguousarray(m._tci, "<u4").tobytes())
+            fh.write(np.ascontiguousarray(m._tiles, m.tile_dim.word_dtype).tobytes())
+            return
+        h = m.handle()
+        t = dev.torch()
+        sizes = (4 * (h.ntr + 1), 4 * m.num_tiles, m.num_tiles * m.dim * m.tile_dim.word_dtype.itemsize)
+        bufs = [t.empty(max(b, 1), dtype=t.uint8, pin_memory=True) for b in sizes]
+        _capi.call("b2sr_to_host", h.ptr, bufs[0].data_ptr(), bufs[1].data_ptr(), bufs[2].data_ptr(), dev.stream())
+        for b, nbytes in zip(bufs, sizes):
+            if nbytes:
+                fh.write(memoryview(b.numpy()[:nbytes]))
 
 
 def load_b2sr(path) -> B2srMatrix:
+    """Read a container written by save_b2sr (formats.py:533-554).  The header
+    and size checks run on the host (same FormatError cases and messages);
+    the arrays go straight from the file buffer to HBM and the tile
+    invariants of formats.py:242-295 are checked there (b2sr_from_host_checked)
+    -- no O(T*d) host pass.  The returned matrix keeps read-only host views
+    of the file buffer, so touching its arrays costs no copy back."""
     with open(path, "rb") as fh:
         raw = fh.read()
     if len(raw) < _HEADER.size:
@@ -689,4 +711,8 @@ def load_b2sr(path) -> B2srMatrix:
     tci = np.frombuffer(raw, "<u4", T, o)
     o += 4 * T
     tiles = np.frombuffer(raw, td.word_dtype, T * dim, o).reshape(T, dim)
-    return B2srMatrix(n, td, trp, tci, tiles)
+    h = _new_handle("b2sr_from_host_checked", n, dim, trp.ctypes.data, tci.ctypes.data, tiles.ctypes.data, T,
+                    dev.stream())
+    m = B2srMatrix._wrap(h)
+    m._trp, m._tci, m._tiles = trp, tci, tiles  # read-only views of the file buffer
+    return m
