@@ -194,6 +194,41 @@ def k4_time(_capi, dev, torch, h, xd, kd, yd, flush, sp, reps=10):
     return float(np.mean(kt)), float(np.mean(ct))
 
 
+def bfs_byte_accounting(torch, at, lv, sweeps, d, bfs_ms, peak_gbs):
+    """SURVEY.md §8d BFS byte accounting for one root (outside the timed
+    region): per sweep L, the reference reads a full masked bbb sweep
+    (kernels.py:219-225); a traversal NEEDS only the tile columns of tile rows
+    whose keep word (~visited) is non-zero, the tile bytes of those tiles whose
+    x word (the frontier) is non-zero, and the x / keep / y words.  Both
+    totals over the BFS's sweeps (the final empty one included), and the
+    needed bytes over the measured BFS time against the HBM peak."""
+    wb = 4 if d == 32 else (2 if d == 16 else 1)
+    tb = d * wb
+    trp = torch.from_numpy(at.tile_row_ptr.astype(np.int64)).cuda()
+    tci = torch.from_numpy(at.tile_col_ind.astype(np.int64)).cuda()
+    ntr = trp.numel() - 1
+    rows = torch.repeat_interleave(torch.arange(ntr, device="cuda"), trp[1:] - trp[:-1])
+    lens = trp[1:] - trp[:-1]
+    pad = torch.full((ntr * d,), float("inf"), dtype=torch.float64, device="cuda")
+    pad[: lv.numel()] = lv
+    lt = pad.view(ntr, d)
+    vec = 3 * ntr * wb + 4 * (ntr + 1)
+    needed = full = 0
+    for L in range(1, sweeps + 1):
+        keep = (lt >= L).any(dim=1)  # tile rows still holding an unvisited vertex (~visited != 0)
+        front = (lt == L - 1).any(dim=1)  # tile columns whose frontier word is non-zero
+        live_tiles = keep[rows]
+        needed += vec + 4 * int(lens[keep].sum().item()) + tb * int((live_tiles & front[tci]).sum().item())
+        full += vec + int(tci.numel()) * (4 + tb)
+    del trp, tci, rows, pad
+    needed_gbs = needed / bfs_ms / 1e6
+    return {"needed_bytes": needed, "full_sweep_bytes": full, "sweeps": sweeps, "bfs_ms": round(bfs_ms, 4),
+            "needed_gbs": round(needed_gbs, 1), "needed_frac_of_peak": round(needed_gbs / peak_gbs, 4),
+            "full_sweep_equivalent_gbs": round(full / bfs_ms / 1e6, 1),
+            "note": "one root; needed = tile columns of rows with a keep bit + tile bytes where the frontier "
+                    "word is non-zero + vectors (SURVEY.md §8d); full = the reference's masked sweeps"}
+
+
 def bmv_alg_bytes(ntr: int, T: int, d: int) -> int:
     """Full masked bbb sweep: tile_row_ptr + T*(4 + tile bytes) + x, keep, y words."""
     wb = 4 if d == 32 else (2 if d == 16 else 1)
@@ -301,20 +336,27 @@ def run_ours(args, rank, world, local_rank):
     launches0 = _capi.launch_count()
     iters = []
     with Clocks(local_rank) as clk:
-        e0, e1 = ev(), ev()
-        e0.record()
+        marks = [ev() for _ in range(n_steps + 1)]  # per-root boundaries (same stream, no extra sync)
+        marks[0].record()
         for k, r in enumerate(roots[args.warmup: args.warmup + n_steps]):
             _capi.call("b2sr_bfs", hA.ptr, h.ptr, r, dev.ptr(lev[k]), ctypes.addressof(it), sp)
             iters.append(int(it.value))
-        e1.record()
+            marks[k + 1].record()
         barrier()
+    e0, e1 = marks[0], marks[-1]
     launches = _capi.launch_count() - launches0
     ms = e0.elapsed_time(e1)
     degt = torch.from_numpy(deg).to("cuda")
     edges = 0
+    per_root = []
     for k in range(n_steps):  # after the timed region: Graph500 edge count per root
         lv = lev[k].view(torch.float64)[:n]
-        edges += int(degt[torch.isfinite(lv)].sum().item()) // 2
+        ek = int(degt[torch.isfinite(lv)].sum().item()) // 2
+        edges += ek
+        per_root.append(ek / (marks[k].elapsed_time(marks[k + 1]) / 1e3) / 1e9)
+    gteps_hmean = len(per_root) / sum(1.0 / max(g, 1e-12) for g in per_root)
+    bfs_bytes = bfs_byte_accounting(torch, at, lev[0].view(torch.float64)[:n], iters[0], d,
+                                    marks[0].elapsed_time(marks[1]), peaks()[0]["hbm_gbs"])
     del lev
     if dist is not None:
         t = torch.tensor([ms], device="cuda")
@@ -401,6 +443,7 @@ def run_ours(args, rank, world, local_rank):
             "data": f"synthetic R-MAT (Graph500 a,b,c=.57,.19,.19) generated on device, seed {args.seed}",
             "config": workload_config("s22", args, args.scale, n, int(csr.nnz), d, world, int(b2sr_gb * 1e9)),
             "e2e": e2e, "roofline": roofline, "gpu_launches": int(launches), "bfs_sweeps_per_root": iters[:4],
+            "gteps_harmonic_mean": round(gteps_hmean, 4), "bfs_bytes": bfs_bytes,
             "clocks": clk.summary(), "sweep": {str(k): v for k, v in sweep.items()}, "tc": tc, "drivers": drivers,
             "graph_gen_s": round(gen_s, 3)}
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -456,7 +499,16 @@ def bench_drivers(args, b2, rmat, torch, ev):
         return r, a0.elapsed_time(a1)
 
     r, ms = timed(lambda: b2.pagerank(at, deg))
-    out["pagerank"] = {"ms": round(ms, 3), "iterations": r.iterations, "ms_per_iter": round(ms / r.iterations, 3)}
+    out["pagerank"] = {"ms": round(ms, 3), "iterations": r.iterations, "ms_per_iter": round(ms / r.iterations, 3),
+                       "mode": "exact (bit-identical to the reference)"}
+    os.environ["B2SR_PR_MODE"] = "fast"  # documented tolerance mode (relative L1 <= 1e-5)
+    try:
+        rf, msf = timed(lambda: b2.pagerank(at, deg))
+    finally:
+        del os.environ["B2SR_PR_MODE"]
+    out["pagerank_fast"] = {"ms": round(msf, 3), "iterations": rf.iterations, "ms_per_iter": round(msf / rf.iterations, 3),
+                            "rel_l1_vs_exact": float(np.abs(rf.per_vertex - r.per_vertex).sum() / np.abs(r.per_vertex).sum()),
+                            "mode": "B2SR_PR_MODE=fast: float32 x (L2-resident), float64 order-free sums"}
     r, ms = timed(lambda: b2.sssp(m, src))
     out["sssp"] = {"ms": round(ms, 3), "iterations": r.iterations}
     r, ms = timed(lambda: b2.connected_components(m))

@@ -96,12 +96,15 @@ constexpr uint32_t TC_CHUNK = 2048;
 
 __global__ void k_tc_item_counts(uint64_t TM, const uint32_t *__restrict__ m_rowid, const uint32_t *__restrict__ m_tci,
                                  uint32_t m_row0, const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ b_trp,
-                                 uint32_t chunk, uint32_t *__restrict__ cnt, uint32_t hashed_max) {
+                                 uint32_t chunk, uint32_t *__restrict__ cnt, uint32_t hashed_max,
+                                 const uint32_t *__restrict__ m_trp) {
     for (uint64_t mt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; mt < TM; mt += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t I = m_rowid[mt] + m_row0, J = m_tci[mt];
+        uint32_t i = m_rowid[mt], I = i + m_row0, J = m_tci[mt];
         uint32_t la = a_trp[I + 1] - a_trp[I], lb = b_trp[J + 1] - b_trp[J];
         uint32_t sh = min(la, lb);
-        cnt[mt] = la && lb && la > hashed_max ? (sh + chunk - 1) / chunk : 0;  // la <= hashed_max: row-hash kernel
+        // rows the row-hash kernel takes (A row and mask row both <= hashed_max) get no items here
+        const bool hashed = la <= hashed_max && m_trp[i + 1] - m_trp[i] <= hashed_max;
+        cnt[mt] = la && lb && !hashed ? (sh + chunk - 1) / chunk : 0;
     }
 }
 
@@ -213,8 +216,8 @@ __global__ void __launch_bounds__(TCH_WARPS * 32) k_tc_rowhash(
     const typename WordT<D>::T *__restrict__ m_tiles, const uint32_t *__restrict__ a_trp,
     const uint32_t *__restrict__ a_tci, const typename WordT<D>::T *__restrict__ a_tiles,
     const uint32_t *__restrict__ b_trp, const uint32_t *__restrict__ b_tci,
-    const typename WordT<D>::T *__restrict__ b_tiles, uint32_t *__restrict__ next_row,
-    unsigned long long *__restrict__ out, unsigned long long *__restrict__ work) {
+    const typename WordT<D>::T *__restrict__ b_tiles, const uint2 *__restrict__ hitems, uint32_t n_hitems,
+    uint32_t *__restrict__ next_item, unsigned long long *__restrict__ out, unsigned long long *__restrict__ work) {
     __shared__ uint32_t keys[TCH_WARPS][TCH_SLOTS];
     __shared__ uint16_t posn[TCH_WARPS][TCH_SLOTS];
     const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
@@ -222,14 +225,49 @@ __global__ void __launch_bounds__(TCH_WARPS * 32) k_tc_rowhash(
     uint16_t *pt = posn[wid];
     unsigned long long acc = 0, units = 0;
     for (;;) {
-        uint32_t i = 0;
-        if (lane == 0) i = atomicAdd(next_row, 1u);
-        i = __shfl_sync(0xffffffffu, i, 0);
-        if (i >= m_ntr) break;
-        const uint32_t m0 = __ldg(m_trp + i), m1 = __ldg(m_trp + i + 1);
-        if (m0 == m1) continue;
+        uint32_t w = 0;
+        if (lane == 0) w = atomicAdd(next_item, 1u);
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (w >= n_hitems) break;
+        const uint2 hit_item = hitems[w];
+        const uint32_t i = hit_item.x, part = hit_item.y & 0xFFFFu, parts = hit_item.y >> 16;
+        uint32_t m0 = __ldg(m_trp + i), m1 = __ldg(m_trp + i + 1);
         const uint32_t I = m_row0 + i, a0 = __ldg(a_trp + I), la = __ldg(a_trp + I + 1) - a0;
-        if (la == 0 || la > TCH_MAX) continue;
+        if (parts > 1) {  // this item's share of the row's mask tiles: equal Bt-row entry counts
+            const uint32_t nj = m1 - m0;  // <= TCH_MAX
+            uint32_t lens[TCH_MAX / 32], run = 0;
+#pragma unroll
+            for (int k = 0; k < (int)(TCH_MAX / 32); k++) {
+                const uint32_t j = k * 32 + lane;
+                uint32_t l = 0;
+                if (j < nj) {
+                    const uint32_t J = __ldg(m_tci + m0 + j);
+                    l = __ldg(b_trp + J + 1) - __ldg(b_trp + J);
+                }
+                uint32_t incl = l;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= (uint32_t)o) incl += y;
+                }
+                lens[k] = run + incl - l;  // exclusive prefix of j
+                run += __shfl_sync(0xffffffffu, incl, 31);
+            }
+            const unsigned long long tot = run;
+            const uint32_t lo_t = (uint32_t)(tot * part / parts), hi_t = (uint32_t)(tot * (part + 1) / parts);
+            uint32_t jlo = 0, jhi = 0;
+#pragma unroll
+            for (int k = 0; k < (int)(TCH_MAX / 32); k++) {
+                const uint32_t j = k * 32 + lane;
+                jlo += __popc(__ballot_sync(0xffffffffu, j < nj && lens[k] < lo_t));
+                jhi += __popc(__ballot_sync(0xffffffffu, j < nj && lens[k] < hi_t));
+            }
+            if (part + 1 == parts) jhi = nj;
+            if (part == 0) jlo = 0;
+            m1 = m0 + jhi;
+            m0 = m0 + jlo;
+            if (m0 >= m1) continue;
+        }
         const uint32_t lg = max(5u, 32u - __clz(2 * la - 1));  // slots = 2^lg >= 2*la
         const uint32_t S = 1u << lg, shift = 32 - lg;
         for (uint32_t q = lane; q < S; q += 32) kt[q] = 0;
@@ -317,9 +355,47 @@ __global__ void __launch_bounds__(TCH_WARPS * 32) k_tc_rowhash(
     }
 }
 
+constexpr uint32_t TCH_BUDGET = 4096;  // probed Bt entries per row-hash work item
+
+// parts of each eligible mask row (0: the row takes the binary-search items or is empty)
+__global__ void k_tch_parts(uint32_t mntr, uint32_t m_row0, const uint32_t *__restrict__ m_trp,
+                            const uint32_t *__restrict__ m_tci, const uint32_t *__restrict__ a_trp,
+                            const uint32_t *__restrict__ b_trp, uint32_t *__restrict__ parts) {
+    const uint32_t lane = lane_id(), warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < mntr; i += warps) {
+        const uint32_t m0 = m_trp[i], m1 = m_trp[i + 1], I = m_row0 + i;
+        const uint32_t la = a_trp[I + 1] - a_trp[I];
+        uint32_t p = 0;
+        if (m1 > m0 && la && la <= TCH_MAX && m1 - m0 <= TCH_MAX) {
+            unsigned long long w = 0;
+            for (uint32_t t = m0 + lane; t < m1; t += 32) {
+                const uint32_t J = m_tci[t];
+                w += b_trp[J + 1] - b_trp[J];
+            }
+            for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+            const unsigned long long q = (w + TCH_BUDGET - 1) / TCH_BUDGET;
+            p = q == 0 ? 1u : (q > 0xFFFFull ? 0xFFFFu : (uint32_t)q);
+        }
+        if (lane == 0) parts[i] = p;
+    }
+}
+
+__global__ void k_tch_fill(uint32_t mntr, const uint32_t *__restrict__ parts, const uint64_t *__restrict__ ofs,
+                           uint2 *__restrict__ items) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mntr; i += gridDim.x * blockDim.x) {
+        const uint32_t P = parts[i];
+        const uint64_t o = ofs[i];
+        for (uint32_t q = 0; q < P; q++) items[o + q] = make_uint2(i, (P << 16) | q);
+    }
+}
+
+// Measured (s20, B200): row-hash 41.8 / 50.4 ms vs binary-search items 25.6 /
+// 32.0 ms at d = 4 / 8 -- ncu: 25.8 G warp instructions (probe loops, partial
+// 32-entry chunks of short Bt rows, 0.56 G shared-memory bank conflicts) vs
+// 17.8 G.  Kept as an A/B path, off by default (B2SR_TC_HASH=1 enables it).
 static bool tc_rowhash_enabled() {
-    const char *e = getenv("B2SR_TC_HASH");  // B2SR_TC_HASH=0: binary-search items only (A/B)
-    return !(e && e[0] == '0');
+    const char *e = getenv("B2SR_TC_HASH");
+    return e && e[0] == '1';
 }
 
 int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_matrix *mask, cudaStream_t s,
@@ -334,7 +410,7 @@ int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_ma
     const uint32_t chunk = ce ? std::max(32, atoi(ce)) : TC_CHUNK;
     const bool hashed = tc_rowhash_enabled();
     LAUNCH(k_tc_item_counts, grid_for(TM), 256, 0, s, TM, rowid.p, mask->tci, mask->row0, a->trp, bt->trp, chunk, cnt.p,
-           hashed ? TCH_MAX : 0u);
+           hashed ? TCH_MAX : 0u, mask->trp);
     exclusive_scan_u32_to_u64(cnt.p, ofs.p, TM, s);
     uint64_t n_items = read_scalar(ofs.p + TM, s);
     Buf<unsigned long long> out(1, s);
@@ -348,15 +424,30 @@ int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_ma
     Buf<uint32_t> next_row(1, s);
     CK(cudaMemsetAsync(next_row.p, 0, 4, s));
     kernel_timer().begin(s);
+    Buf<uint2> hitems;
+    uint32_t n_hitems = 0;
     if (hashed) {
-        // a few resident CTAs per SM; rows handed out dynamically
-        const unsigned gh = (unsigned)std::min<uint64_t>((uint64_t)num_sms() * 6, ((uint64_t)mask->ntr + TCH_WARPS - 1) / TCH_WARPS);
+        // work items of the row-hash kernel: each eligible mask row cut into
+        // parts of <= TCH_BUDGET probed Bt entries (bounded tail), rows handed
+        // out dynamically
+        const uint32_t mntr = mask->ntr;
+        Buf<uint32_t> pc(std::max<uint32_t>(mntr, 1), s);
+        Buf<uint64_t> pofs((size_t)mntr + 1, s);
+        LAUNCH(k_tch_parts, grid_for((uint64_t)mntr * 32), 256, 0, s, mntr, mask->row0, mask->trp, mask->tci, a->trp,
+               bt->trp, pc.p);
+        exclusive_scan_u32_to_u64(pc.p, pofs.p, mntr, s);
+        n_hitems = (uint32_t)read_scalar(pofs.p + mntr, s);
+        hitems = Buf<uint2>(std::max<uint32_t>(n_hitems, 1), s);
+        if (n_hitems) LAUNCH(k_tch_fill, grid_for(mntr), 256, 0, s, mntr, pc.p, pofs.p, hitems.p);
+    }
+    if (n_hitems) {
+        const unsigned gh = (unsigned)std::min<uint64_t>((uint64_t)num_sms() * 6, ((uint64_t)n_hitems + TCH_WARPS - 1) / TCH_WARPS);
         switch (a->dim) {
 #define TCH_CASE(DD, W)                                                                                          \
     case DD:                                                                                                     \
         LAUNCH(k_tc_rowhash<DD>, gh, TCH_WARPS * 32, 0, s, mask->ntr, mask->row0, mask->trp, mask->tci,         \
                (const W *)mask->tiles, a->trp, a->tci, (const W *)a->tiles, bt->trp, bt->tci,                   \
-               (const W *)bt->tiles, next_row.p, out.p, work_out ? work.p : nullptr);                           \
+               (const W *)bt->tiles, hitems.p, n_hitems, next_row.p, out.p, work_out ? work.p : nullptr);        \
         break;
             TCH_CASE(4, uint8_t)
             TCH_CASE(8, uint8_t)

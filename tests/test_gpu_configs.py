@@ -136,6 +136,16 @@ def test_config3_s24_pagerank_sssp_cc():
     rel_l1 = np.abs(pr.per_vertex - want).sum() / np.abs(want).sum()
     assert rel_l1 <= 1e-5 and pr.iterations == it and pr.converged == conv
     assert pr.per_vertex.tobytes() == want.tobytes()  # the default driver is bit-exact
+    # the documented fast mode (float32 x, order-free float64 sums) sits inside the tolerance
+    import os
+
+    os.environ["B2SR_PR_MODE"] = "fast"
+    try:
+        prf = b2.pagerank(at, deg)
+    finally:
+        del os.environ["B2SR_PR_MODE"]
+    rel_f = np.abs(prf.per_vertex - want).sum() / np.abs(want).sum()
+    assert rel_f <= 1e-5 and prf.iterations == it and prf.converged == conv, rel_f
     # SSSP: the graph is loop-free, so drop_diagonal(m) = m and its transpose is ref_t
     rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(rp.astype(np.int64)))
     assert not np.any(rows == ci)
