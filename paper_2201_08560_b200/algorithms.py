@@ -89,16 +89,32 @@ def _cached_transpose(a: B2srMatrix):
     return t() if isinstance(t, weakref.ref) else t
 
 
-def bfs(a: B2srMatrix, src: int, *, workers: int | None = None) -> AlgoResult:
+def bfs(a: B2srMatrix, src: int, *, workers: int | None = None, devices=None) -> AlgoResult:
     """Level-synchronous BFS; hop counts, +inf where unreachable.
 
     The reference transposes on every call (algorithms.py:78).  Here the
     transpose is cached on the matrix; until one exists (and for the first
     BFS_PUSH_CALLS calls) d = 4/8 matrices run push-only levels over ``a``,
     which need no transpose at all.  Levels and iterations are identical.
+
+    ``devices`` (or env B2SR_GPUS): spread the traversal over several GPUs
+    from this process -- a's and at's tile rows cut into blocks, one rank per
+    GPU, NCCL between them (dist.multi_gpu_bfs, b2sr_dist_bfs_*; d = 4, 8).
+    Same levels and iterations.  ``workers`` stays the reference's thread
+    count knob (validated, results independent of it).
     """
     src = _source(a.n, src)
     resolve_workers(workers)
+    from . import dist
+
+    devs = dist.resolve_devices(devices)
+    if len(devs) > 1:
+        if a.dim > 8:
+            raise ValueError("multi-GPU bfs supports tile dims 4 and 8")
+        at = _cached_transpose(a)
+        at = at if at is not None else b2sr_transpose(a)
+        lv, it = dist.multi_gpu_bfs(a, at, src, devs)
+        return AlgoResult(per_vertex=lv, iterations=int(it), converged=True)
     levels = dev.empty_bytes(8 * a.n)
     it = ctypes.c_int64()
     at = _cached_transpose(a)

@@ -11,6 +11,10 @@
 //     their run and build their row word, and one tile is emitted;
 //   * K1 runs the loop counting tiles -> exclusive scan -> tile_row_ptr;
 //     K2 re-runs it writing tile_col_ind and the bit rows.
+// (Staging each warp's runs in shared memory first -- coalesced loads, merge
+// steps on shared memory -- measured no faster at d = 4 (10.6 ms at s22 either
+// way) and 8-10x slower at d = 16/32 (a third of the resident warps), so the
+// merge reads its runs from global memory.)
 // Long tile rows (hubs) are split into column ranges of ~CONV_CHUNK entries
 // so no group walks a hub alone; the split points are found by binary
 // search and the ranges' counts are scanned in order, so the layout is
@@ -18,8 +22,6 @@
 #include "b2sr_internal.cuh"
 
 namespace b2sr {
-
-void hot_smem_attr_raw(const void *kernel, size_t bytes);  // hot.cu: opt-in dynamic smem, per (device, kernel)
 
 constexpr uint32_t CONV_CHUNK = 1024;  // CSR entries per work item (target)
 constexpr uint32_t INF32 = 0xFFFFFFFFu;
@@ -66,24 +68,14 @@ __device__ __forceinline__ uint32_t group_min(uint32_t v) {
     }
 }
 
-// The merge's per-step loads are staged: a warp first copies the CSR runs of
-// its GPW items into shared memory with coalesced loads (CONV_STAGE words
-// per warp; items whose runs do not fit read global memory as before), so
-// the merge steps -- one group min + one run read each -- wait on shared
-// memory instead of a dependent global load per step.
-constexpr uint32_t CONV_WARPS = 8;
-constexpr uint32_t CONV_STAGE = 2048;  // staged col_ind words per warp (64 KB per CTA)
-
 template <int D, bool PACK>
-__global__ void __launch_bounds__(CONV_WARPS * 32) k_conv(const ConvItem *__restrict__ items, uint32_t n_items, uint32_t n,
+__global__ void __launch_bounds__(256) k_conv(const ConvItem *__restrict__ items, uint32_t n_items, uint32_t n,
                                               const uint32_t *__restrict__ row_ptr,
                                               const uint32_t *__restrict__ col_ind, const uint64_t *__restrict__ iofs,
                                               uint32_t *__restrict__ cnt, uint32_t *__restrict__ tci,
                                               typename WordT<D>::T *__restrict__ tiles) {
-    extern __shared__ uint32_t conv_stage[];
     constexpr uint32_t GPW = 32 / D;  // groups (items) per warp
     const uint32_t lane = lane_id(), r = lane % D;
-    uint32_t *stage = conv_stage + (threadIdx.x >> 5) * CONV_STAGE;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t wb = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wb * GPW < n_items; wb += warps) {
         uint32_t item = wb * GPW + lane / D;
@@ -102,62 +94,11 @@ __global__ void __launch_bounds__(CONV_WARPS * 32) k_conv(const ConvItem *__rest
                 }
                 p = a;
             }
-            if (it.khi < (n + D - 1) / D) {  // split range: stop before c >= khi*D (bounds the staged run)
-                uint32_t key = it.khi * (uint32_t)D, a = p, b = end;
-                while (a < b) {
-                    uint32_t mid = (a + b) >> 1;
-                    if (col_ind[mid] < key) a = mid + 1; else b = mid;
-                }
-                end = a;
-            }
         }
-        // stage the warp's runs: exclusive offsets of the 32 run lengths
-        const uint32_t len = end - p;
-        uint32_t off = len;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, off, o);
-            if (lane >= (uint32_t)o) off += y;
-        }
-        const uint32_t total = __shfl_sync(0xffffffffu, off, 31);
-        off -= len;
-        const bool staged = total <= CONV_STAGE;
-        if (staged) {
-            // entry f of the warp's runs belongs to the last lane whose offset
-            // is <= f: every lane stages entries f = lane, lane+32, ... with
-            // independent loads (4 in flight), runs located by binary search
-            uint32_t *soff = conv_stage + CONV_WARPS * CONV_STAGE + (threadIdx.x >> 5) * 64, *sbase = soff + 32;
-            soff[lane] = off;
-            sbase[lane] = p;
-            __syncwarp();
-            for (uint32_t f0 = 0; f0 < total; f0 += 128) {
-                uint32_t v[4];
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const uint32_t f = f0 + u * 32 + lane;
-                    v[u] = 0;
-                    if (f < total) {
-                        uint32_t lo = 0, hi = 31;
-                        while (lo < hi) {
-                            const uint32_t mid = (lo + hi + 1) >> 1;
-                            if (soff[mid] <= f) lo = mid; else hi = mid - 1;
-                        }
-                        v[u] = __ldg(col_ind + sbase[lo] + (f - soff[lo]));
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    const uint32_t f = f0 + u * 32 + lane;
-                    if (f < total) stage[f] = v[u];
-                }
-            }
-            __syncwarp();
-        }
-        const uint32_t *run = staged ? stage + off : col_ind + p;
-        uint32_t q = 0, c = 0, cur = INF32;
-        if (q < len) {
-            c = run[q];
-            cur = c / D;
+        uint32_t c = 0, cur = INF32;
+        if (p < end) {
+            c = col_ind[p];
+            if (c / D < it.khi) cur = c / D;
         }
         uint64_t t = (PACK && valid) ? iofs[item] : 0;
         uint32_t count = 0;
@@ -166,11 +107,12 @@ __global__ void __launch_bounds__(CONV_WARPS * 32) k_conv(const ConvItem *__rest
             uint32_t word = 0;
             while (cur == K && K != INF32) {  // consume this lane's run inside tile column K
                 word |= 1u << (c % D);
-                ++q;
+                ++p;
                 cur = INF32;
-                if (q < len) {
-                    c = run[q];
-                    cur = c / D;
+                if (p < end) {
+                    c = col_ind[p];
+                    uint32_t k = c / D;
+                    if (k < it.khi) cur = k;
                 }
             }
             if (K != INF32) {
@@ -185,7 +127,6 @@ __global__ void __launch_bounds__(CONV_WARPS * 32) k_conv(const ConvItem *__rest
         if constexpr (!PACK) {
             if (valid && r == 0) cnt[item] = count;
         }
-        __syncwarp();  // the stage is rewritten by the next iteration
     }
 }
 
@@ -200,19 +141,15 @@ static void conv_launch(bool pack, const ConvItem *items, uint32_t n_items, uint
                         cudaStream_t s) {
     constexpr uint32_t GPW = 32 / D;
     uint64_t warps = (n_items + GPW - 1) / GPW;
-    uint64_t blocks = (warps + CONV_WARPS - 1) / CONV_WARPS;
-    uint64_t cap = (uint64_t)num_sms() * 3;  // 3 CTAs (64 KB stage each) per SM, grid-stride beyond
+    uint64_t blocks = (warps + 7) / 8;
+    uint64_t cap = (uint64_t)num_sms() * 8;  // 8 CTAs x 8 warps per SM, grid-stride beyond
     unsigned g = (unsigned)(blocks < cap ? blocks : cap);
-    const size_t smem = (size_t)CONV_WARPS * (CONV_STAGE + 64) * 4;
-    if (pack) {
-        hot_smem_attr_raw((const void *)k_conv<D, true>, smem);
-        LAUNCH((k_conv<D, true>), g, CONV_WARPS * 32, smem, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
+    if (pack)
+        LAUNCH((k_conv<D, true>), g, 256, 0, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
                (typename WordT<D>::T *)tiles);
-    } else {
-        hot_smem_attr_raw((const void *)k_conv<D, false>, smem);
-        LAUNCH((k_conv<D, false>), g, CONV_WARPS * 32, smem, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
+    else
+        LAUNCH((k_conv<D, false>), g, 256, 0, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
                (typename WordT<D>::T *)tiles);
-    }
 }
 
 static void conv_dispatch(uint32_t d, bool pack, const ConvItem *items, uint32_t n_items, uint32_t n,

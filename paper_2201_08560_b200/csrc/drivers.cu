@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -713,6 +714,45 @@ __global__ void k_pr_fold_parts(uint32_t ntr, uint32_t n, const uint32_t *__rest
 __global__ void k_to_f32(uint32_t n, const double *__restrict__ a, float *__restrict__ b) {
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) b[j] = __double2float_rn(a[j]);
 }
+
+// Keeps the float32 x of the fast PageRank gather resident in L2 while the
+// tile stream (4.2 GB per sweep at s24) passes through: an access-policy
+// window marks x persisting (set-aside capped by the device limit), the
+// stream's other accesses streaming.  Restored on destruction.
+struct L2Persist {
+    cudaStream_t s = nullptr;
+    bool on = false;
+    size_t old_limit = 0;
+    L2Persist(cudaStream_t st, const void *base, size_t bytes) : s(st) {
+        const char *e = getenv("B2SR_PR_L2PERSIST");
+        if (e && e[0] == '0') return;
+        int dev = 0, max_persist = 0, max_window = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev));
+        CK(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+        if (max_persist <= 0 || max_window <= 0) return;
+        CK(cudaDeviceGetLimit(&old_limit, cudaLimitPersistingL2CacheSize));
+        const size_t set_aside = std::min<size_t>(bytes, (size_t)max_persist);
+        CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, set_aside));
+        cudaStreamAttrValue v = {};
+        v.accessPolicyWindow.base_ptr = const_cast<void *>(base);
+        v.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, (size_t)max_window);
+        v.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)set_aside / (double)v.accessPolicyWindow.num_bytes);
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        CK(cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v));
+        on = true;
+    }
+    ~L2Persist() {
+        if (!on) return;
+        cudaStreamAttrValue v = {};
+        v.accessPolicyWindow.num_bytes = 0;
+        cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
+        cudaStreamSynchronize(s);
+        cudaCtxResetPersistingL2Cache();
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, old_limit);
+    }
+};
 
 static bool pr_fast_mode(int dim) {
     const char *e = getenv("B2SR_PR_MODE");
@@ -1648,6 +1688,8 @@ int b2sr_pagerank(const b2sr_matrix *a, const double *d_out_degree, double alpha
         part = Buf<double>((size_t)a->n_items * d, s);
         CK(cudaMemsetAsync(x32.p, 0, (size_t)a->ntr * d * 4, s));
     }
+    std::unique_ptr<L2Persist> persist;
+    if (fast) persist.reset(new L2Persist(s, x32.p, (size_t)a->ntr * d * 4));
     while (sweeps < max_iter) {
         if (trace) CK(cudaEventRecord(ev[0], s));
         if (fast) {

@@ -29,6 +29,8 @@ are the CUDA kernels below.
 from __future__ import annotations
 
 import ctypes
+import os
+import threading
 
 import numpy as np
 
@@ -281,6 +283,135 @@ def native_triangle_count(comm: Comm, lower: B2srMatrix, stream=None):
     _capi.call("b2sr_dist_tc", comm.ptr, h.ptr, ctypes.addressof(out), ctypes.addressof(cuts),
                stream if stream is not None else dev.stream())
     return int(out.value), list(cuts)
+
+
+# ---------------------------------------------------------------- one process, several GPUs
+def resolve_devices(devices=None) -> list:
+    """The GPUs a drop-in call spreads over: ``devices`` (a count N -> cuda:0..N-1,
+    or an explicit list of device ordinals), else env B2SR_GPUS (a count or
+    "0,1,..."), else one GPU.  A list may repeat an ordinal: those ranks
+    share that GPU (thread-ranks exchanging through device copies -- how the
+    multi-rank path is tested on one device)."""
+    if devices is None:
+        env = os.environ.get("B2SR_GPUS", "").strip()
+        if not env:
+            return [None]
+        devices = [int(x) for x in env.split(",")] if "," in env else int(env)
+    if isinstance(devices, (int, np.integer)):
+        if devices < 1:
+            raise ValueError("devices must be at least 1")
+        devices = list(range(int(devices)))
+    devices = [int(d) for d in devices]
+    if not devices or any(d < 0 for d in devices):
+        raise ValueError("devices must be a positive count or a list of device ordinals")
+    return devices
+
+
+def _row_cuts(trp: np.ndarray, world: int, dim: int) -> list:
+    """Tile-row blocks balanced by tile count, on 16-byte word boundaries of
+    the bit vectors (the rule of b2sr_dist_bfs_plan's k_balanced_cuts)."""
+    ntr = len(trp) - 1
+    align = 16 // (4 if dim == 32 else 2 if dim == 16 else 1)
+    T = int(trp[-1])
+    cuts = [0]
+    for k in range(1, world):
+        r = int(np.searchsorted(trp, T * k // world, side="left"))
+        cuts.append(min(ntr, (r + align // 2) // align * align))
+    cuts.append(ntr)
+    return [max(c, cuts[i - 1]) if i else c for i, c in enumerate(cuts)]
+
+
+class _MultiGpuBfs:
+    """Per-matrix state of bfs(a, src, devices=...): one rank per listed
+    device, each holding its rows of a and at (uploaded once from the host
+    arrays) and a b2sr_dist_bfs plan; every call runs the ranks' level loops
+    concurrently on host threads (the C calls release the GIL)."""
+
+    def __init__(self, a: B2srMatrix, at: B2srMatrix, devs: list):
+        t = dev.torch()
+        self.n, self.devs = a.n, devs
+        world = len(devs)
+        trp_a, trp_at = np.ascontiguousarray(a.tile_row_ptr), np.ascontiguousarray(at.tile_row_ptr)
+        cuts = _row_cuts(trp_at, world, a.dim)
+        host = []
+        for mat, trp in ((a, trp_a), (at, trp_at)):
+            tci, tiles = mat.tile_col_ind, mat.bit_tiles
+            parts = []
+            for r in range(world):
+                b, e = cuts[r], cuts[r + 1]
+                t0, t1 = int(trp[b]), int(trp[e])
+                parts.append(((None, (trp[b:e + 1] - trp[b]).astype(np.uint32)), (None, tci[t0:t1]),
+                              (None, np.ascontiguousarray(tiles[t0:t1]))))
+            host.append(parts)
+        if len(set(devs)) == len(devs):  # distinct GPUs: NCCL, ranks initialised together
+            uid = (ctypes.c_uint8 * 128)()
+            _capi.call("b2sr_comm_unique_id", ctypes.addressof(uid))
+            comms = [None] * world
+        else:  # repeated ordinals: thread-ranks sharing devices
+            t.cuda.set_device(devs[0])
+            comms = Comm.local(world)
+            uid = None
+        self.ranks = [None] * world
+
+        def setup(r):
+            t.cuda.set_device(devs[r])
+            if uid is not None:
+                out = ctypes.c_void_p()
+                _capi.call("b2sr_comm_init", ctypes.addressof(uid), world, r, ctypes.byref(out))
+                comms[r] = Comm(out.value, r, world)
+            b, e = cuts[r], cuts[r + 1]
+            ab = block_from_host(a.n, a.dim, b, e, host[0][r])
+            atb = block_from_host(a.n, a.dim, b, e, host[1][r])
+            self.ranks[r] = NativeDistributedBfs.from_blocks(comms[r], ab, atb, trp_a, trp_at)
+
+        self._each(setup)
+        self.cuts = cuts
+
+    def _each(self, fn):
+        err, threads = [], []
+
+        def body(r):
+            try:
+                fn(r)
+            except BaseException as e:  # noqa: BLE001 -- re-raised on the caller's thread
+                err.append(e)
+
+        for r in range(len(self.devs)):
+            threads.append(threading.Thread(target=body, args=(r,)))
+            threads[-1].start()
+        for th in threads:
+            th.join()
+        if err:
+            raise err[0]
+
+    def run(self, src: int):
+        t = dev.torch()
+        out = [None] * len(self.devs)
+
+        def go(r):
+            t.cuda.set_device(self.devs[r])
+            st = t.cuda.Stream()
+            with t.cuda.stream(st):
+                out[r] = self.ranks[r].run(src, to_host=(r == 0), stream=st.cuda_stream)
+                st.synchronize()
+
+        self._each(go)
+        return out[0]
+
+
+_multi_lock = threading.Lock()
+
+
+def multi_gpu_bfs(a: B2srMatrix, at: B2srMatrix, src: int, devs: list):
+    """bfs over several GPUs from one process; plans cached on ``a``."""
+    key = tuple(devs)
+    with _multi_lock:
+        cache = a._dist if a._dist is not None else {}
+        a._dist = cache
+        state = cache.get(key)
+        if state is None:
+            state = cache[key] = _MultiGpuBfs(a, at, devs)
+    return state.run(src)
 
 
 # ---------------------------------------------------------------- float-gather drivers

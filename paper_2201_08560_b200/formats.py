@@ -301,7 +301,7 @@ class B2srMatrix:
     """
 
     __slots__ = ("n", "tile_dim", "_trp", "_tci", "_tiles", "_h", "_num_tiles", "_transpose", "_nodiag",
-                 "_bfs_push", "_lock", "__weakref__")
+                 "_bfs_push", "_lock", "_dist", "__weakref__")
 
     def __init__(self, n, tile_dim, tile_row_ptr, tile_col_ind, bit_tiles):
         n = int(n)
@@ -349,6 +349,7 @@ class B2srMatrix:
         # transpose / diagonal-free twin: each is created once and never
         # replaced, so a handle read from the matrix stays alive with it
         self._lock = threading.RLock()
+        self._dist = None  # per-device-list multi-GPU BFS plans (dist.multi_gpu_bfs)
 
     @classmethod
     def _wrap(cls, h: _Handle) -> "B2srMatrix":
@@ -365,6 +366,7 @@ class B2srMatrix:
         # transpose / diagonal-free twin: each is created once and never
         # replaced, so a handle read from the matrix stays alive with it
         self._lock = threading.RLock()
+        self._dist = None  # per-device-list multi-GPU BFS plans (dist.multi_gpu_bfs)
         return self
 
     # device mirror ---------------------------------------------------

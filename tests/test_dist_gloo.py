@@ -150,3 +150,31 @@ def test_partition_properties():
                 assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
                 wb = 4 if d == 32 else (2 if d == 16 else 1)
                 assert (bdist.block_rows(ntr, world, d) * wb) % 4 == 0
+
+
+def test_resolve_devices_and_row_cuts(monkeypatch):
+    import numpy as np
+
+    from paper_2201_08560_b200 import dist as bdist
+
+    monkeypatch.delenv("B2SR_GPUS", raising=False)
+    assert bdist.resolve_devices(None) == [None]
+    assert bdist.resolve_devices(3) == [0, 1, 2]
+    assert bdist.resolve_devices([1, 0]) == [1, 0]
+    monkeypatch.setenv("B2SR_GPUS", "4")
+    assert bdist.resolve_devices(None) == [0, 1, 2, 3]
+    monkeypatch.setenv("B2SR_GPUS", "0,0")
+    assert bdist.resolve_devices(None) == [0, 0]
+    for bad in (0, [], [-1]):
+        with pytest.raises(ValueError):
+            bdist.resolve_devices(bad)
+    rng = np.random.default_rng(0)
+    lens = rng.integers(0, 50, 1000)
+    trp = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint32)
+    for world, dim in ((2, 4), (3, 8), (8, 16), (5, 32)):
+        cuts = bdist._row_cuts(trp, world, dim)
+        align = 16 // (4 if dim == 32 else 2 if dim == 16 else 1)
+        assert cuts[0] == 0 and cuts[-1] == 1000 and cuts == sorted(cuts) and len(cuts) == world + 1
+        assert all(c % align == 0 or c == 1000 for c in cuts)
+        tiles = [int(trp[cuts[r + 1]] - trp[cuts[r]]) for r in range(world)]
+        assert max(tiles) - min(tiles) <= 2 * align * 50 + 1  # balanced up to the alignment granule

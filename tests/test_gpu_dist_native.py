@@ -150,3 +150,20 @@ def test_dist_tc_thread_ranks(world, d):
     for cnt, cuts in res:
         assert cnt == want
         assert cuts[0] == 0 and cuts[-1] == lower.n_tile_rows and cuts == sorted(cuts)
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0]])
+@pytest.mark.parametrize("d", [4, 8])
+def test_bfs_devices_keyword(devices, d):
+    """The drop-in bfs(a, src, devices=...) -- one process, one rank per listed
+    device (repeated ordinals: thread-ranks on one GPU) -- equals the oracle,
+    and a second call reuses the cached per-device plans."""
+    csr = _graph(13, False, seed=11)
+    m = b2.csr_to_b2sr(csr, d)
+    ref = (csr.n, d, m.tile_row_ptr, m.tile_col_ind, m.bit_tiles)
+    deg = np.diff(csr.row_ptr.astype(np.int64))
+    for src in (int(np.argmax(deg)), int(np.flatnonzero(deg > 0)[3])):
+        lv, it = orc.bfs(ref, src)
+        r = b2.bfs(m, src, devices=devices)
+        assert r.per_vertex.tobytes() == lv.tobytes() and r.iterations == it
+    assert len(m._dist) == 1
