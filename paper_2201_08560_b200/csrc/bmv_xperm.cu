@@ -75,6 +75,17 @@ __global__ void k_xp_permute(uint32_t ncols, uint32_t n, const uint32_t *__restr
     }
 }
 
+// float32 copy for the fast PageRank gather: x'[rank[c]*D + b] = (float)x[c*D + b]
+template <int D>
+__global__ void k_xp_permute_f32(uint32_t ncols, uint32_t n, const uint32_t *__restrict__ rank,
+                                 const double *__restrict__ x, float *__restrict__ xp) {
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < ncols; c += gridDim.x * blockDim.x) {
+        const size_t src = (size_t)c * D, dst = (size_t)rank[c] * D;
+#pragma unroll
+        for (int b = 0; b < D; b++) xp[dst + b] = src + b < n ? __double2float_rn(__ldg(x + src + b)) : 0.0f;
+    }
+}
+
 // u32 vectors (CC labels): lab'[rank[c]*D + b] = lab[c*D + b]
 template <int D>
 __global__ void k_xp_permute_u32(uint32_t ncols, uint32_t n, const uint32_t *__restrict__ rank,
@@ -138,6 +149,14 @@ const uint32_t *xperm_apply_u32(b2sr_matrix *m, const uint32_t *x, uint32_t *xp,
     XPerm *p = xperm_plan(m, s);
     if (m->dim == 4) LAUNCH(k_xp_permute_u32<4>, xgrid(p->ncols), 256, 0, s, p->ncols, m->n, p->rank, x, xp);
     else LAUNCH(k_xp_permute_u32<8>, xgrid(p->ncols), 256, 0, s, p->ncols, m->n, p->rank, x, xp);
+    return p->tci_p;
+}
+
+// float32 x' for the fast PageRank gather (d = 4, 8); returns the gather column array
+const uint32_t *xperm_apply_f32(b2sr_matrix *m, const double *x, float *xp, cudaStream_t s) {
+    XPerm *p = xperm_plan(m, s);
+    if (m->dim == 4) LAUNCH(k_xp_permute_f32<4>, xgrid(p->ncols), 256, 0, s, p->ncols, m->n, p->rank, x, xp);
+    else LAUNCH(k_xp_permute_f32<8>, xgrid(p->ncols), 256, 0, s, p->ncols, m->n, p->rank, x, xp);
     return p->tci_p;
 }
 

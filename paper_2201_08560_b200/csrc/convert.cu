@@ -73,13 +73,15 @@ __global__ void __launch_bounds__(256) k_conv(const ConvItem *__restrict__ items
                                               const uint32_t *__restrict__ row_ptr,
                                               const uint32_t *__restrict__ col_ind, const uint64_t *__restrict__ iofs,
                                               uint32_t *__restrict__ cnt, uint32_t *__restrict__ tci,
-                                              typename WordT<D>::T *__restrict__ tiles) {
+                                              typename WordT<D>::T *__restrict__ tiles,
+                                              const uint32_t *__restrict__ order) {
     constexpr uint32_t GPW = 32 / D;  // groups (items) per warp
     const uint32_t lane = lane_id(), r = lane % D;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t wb = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; wb * GPW < n_items; wb += warps) {
-        uint32_t item = wb * GPW + lane / D;
-        bool valid = item < n_items;
+        const uint32_t slot = wb * GPW + lane / D;
+        bool valid = slot < n_items;
+        uint32_t item = valid ? (order ? order[slot] : slot) : slot;
         ConvItem it = valid ? items[item] : ConvItem{0, 0, 0, 0};
         uint64_t row = (uint64_t)it.row * D + r;
         uint32_t p = 0, end = 0;
@@ -138,7 +140,7 @@ __global__ void k_conv_trp(uint32_t ntr, const uint64_t *pofs, const uint64_t *i
 template <int D>
 static void conv_launch(bool pack, const ConvItem *items, uint32_t n_items, uint32_t n, const uint32_t *row_ptr,
                         const uint32_t *col_ind, const uint64_t *iofs, uint32_t *cnt, uint32_t *tci, void *tiles,
-                        cudaStream_t s) {
+                        cudaStream_t s, const uint32_t *order) {
     constexpr uint32_t GPW = 32 / D;
     uint64_t warps = (n_items + GPW - 1) / GPW;
     uint64_t blocks = (warps + 7) / 8;
@@ -146,21 +148,48 @@ static void conv_launch(bool pack, const ConvItem *items, uint32_t n_items, uint
     unsigned g = (unsigned)(blocks < cap ? blocks : cap);
     if (pack)
         LAUNCH((k_conv<D, true>), g, 256, 0, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
-               (typename WordT<D>::T *)tiles);
+               (typename WordT<D>::T *)tiles, order);
     else
         LAUNCH((k_conv<D, false>), g, 256, 0, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
-               (typename WordT<D>::T *)tiles);
+               (typename WordT<D>::T *)tiles, order);
 }
 
 static void conv_dispatch(uint32_t d, bool pack, const ConvItem *items, uint32_t n_items, uint32_t n,
                           const uint32_t *row_ptr, const uint32_t *col_ind, const uint64_t *iofs, uint32_t *cnt,
-                          uint32_t *tci, void *tiles, cudaStream_t s) {
+                          uint32_t *tci, void *tiles, cudaStream_t s, const uint32_t *order = nullptr) {
     switch (d) {
-        case 4: conv_launch<4>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s); break;
-        case 8: conv_launch<8>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s); break;
-        case 16: conv_launch<16>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s); break;
-        default: conv_launch<32>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s); break;
+        case 4: conv_launch<4>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order); break;
+        case 8: conv_launch<8>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order); break;
+        case 16: conv_launch<16>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order); break;
+        default: conv_launch<32>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order); break;
     }
+}
+
+// Optionally, items sorted by their (estimated) CSR entry count, so the GPW items a warp
+// merges in lock-step have similar lengths: the warp loops until its LONGEST
+// item is done, and on R-MAT a random group of 8 tile rows (d = 4) is
+// dominated by one long row (ncu, s22 d=4: 2.13 G warp instructions for the
+// count pass, issue-bound).  Output offsets follow the items' own order, so
+// the layout does not depend on the processing order.
+__global__ void k_conv_item_len(uint32_t n_items, uint32_t n, uint32_t d, const ConvItem *__restrict__ items,
+                                const uint32_t *__restrict__ row_ptr, const uint64_t *__restrict__ pofs,
+                                uint32_t *__restrict__ key, uint32_t *__restrict__ val) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_items; i += gridDim.x * blockDim.x) {
+        const ConvItem it = items[i];
+        const uint64_t r0 = (uint64_t)it.row * d, r1 = min((uint64_t)n, r0 + d);
+        const uint32_t e = row_ptr[r1] - row_ptr[r0];
+        const uint32_t P = (uint32_t)(pofs[it.row + 1] - pofs[it.row]);
+        key[i] = min(0xFFFFu, e / P);
+        val[i] = i;
+    }
+}
+
+// Measured slower (s22 d=4: 8.6 vs 6.3 ms): the sort costs more than the
+// imbalance it removes, and neighbouring tile rows no longer share cache
+// lines.  Off by default; B2SR_CONV_SORT=1 enables it (A/B).
+static bool conv_sorted() {
+    const char *e = getenv("B2SR_CONV_SORT");
+    return e && e[0] == '1';
 }
 
 b2sr_matrix *csr_to_b2sr_device(uint32_t n, uint32_t d, const uint32_t *row_ptr, const uint32_t *col_ind,
@@ -175,16 +204,27 @@ b2sr_matrix *csr_to_b2sr_device(uint32_t n, uint32_t d, const uint32_t *row_ptr,
     uint32_t n_items = (uint32_t)n_items64;
     Buf<ConvItem> items(n_items, s);
     LAUNCH(k_conv_items, (ntr + 255) / 256, 256, 0, s, ntr, pofs.p, items.p);
+    Buf<uint32_t> order_k, order_v, kalt, valt;
+    uint32_t *order = nullptr;
+    if (conv_sorted() && n_items > 1) {
+        order_k = Buf<uint32_t>(n_items, s);
+        order_v = Buf<uint32_t>(n_items, s);
+        LAUNCH(k_conv_item_len, (unsigned)std::min<uint64_t>((n_items + 255) / 256, (uint64_t)num_sms() * 8), 256, 0, s,
+               n_items, n, d, items.p, row_ptr, pofs.p, order_k.p, order_v.p);
+        uint32_t *ko = nullptr, *vo = nullptr;
+        radix_sort_pairs_u32(order_k.p, order_v.p, n_items, 16, s, &ko, &vo, &kalt, &valt);
+        order = vo;
+    }
     Buf<uint32_t> cnt(n_items, s);
     Buf<uint64_t> iofs((size_t)n_items + 1, s);
-    conv_dispatch(d, false, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, nullptr, nullptr, s);
+    conv_dispatch(d, false, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, nullptr, nullptr, s, order);
     exclusive_scan_u32_to_u64(cnt.p, iofs.p, n_items, s);
     uint64_t T = read_scalar(iofs.p + n_items, s);
     if (T > 0xFFFFFFFFull) B2SR_THROW(B2SR_EFORMAT, "tile count exceeds 32-bit index range");
     b2sr_matrix *m = new_matrix(n, d, ntr, T, s);
     try {
         LAUNCH(k_conv_trp, (ntr + 256) / 256, 256, 0, s, ntr, pofs.p, iofs.p, m->trp);
-        if (T) conv_dispatch(d, true, items.p, n_items, n, row_ptr, col_ind, iofs.p, nullptr, m->tci, m->tiles, s);
+        if (T) conv_dispatch(d, true, items.p, n_items, n, row_ptr, col_ind, iofs.p, nullptr, m->tci, m->tiles, s, order);
     } catch (...) {
         free_matrix(m);
         throw;

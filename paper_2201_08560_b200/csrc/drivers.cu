@@ -20,6 +20,7 @@
 #include <memory>
 #include <mutex>
 #include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "bfs_ctl.cuh"
@@ -30,6 +31,7 @@ namespace b2sr {
 
 void launch_bff(const b2sr_matrix *m, const double *x, int ring, double inc, const void *keep, double *y,
                 cudaStream_t s, double ident);
+const uint32_t *xperm_apply_f32(b2sr_matrix *m, const double *x, float *xp, cudaStream_t s);
 void used_column_words(const b2sr_matrix *m, uint32_t *colw, cudaStream_t s);
 
 static unsigned grid_for(uint64_t work) {
@@ -643,57 +645,71 @@ __global__ void k_pr_init(uint32_t n, double r0, const double *deg, double *rank
 // x, so ranks differ from the exact ones by ~1e-7 relative (checked <= 1e-5
 // against the oracle at s24, same iteration count).
 template <int D>
+__device__ __forceinline__ void pr_add(double (&acc)[D], uint32_t r, double v) {
+#pragma unroll
+    for (int q = 0; q < D; q++) acc[q] = __dadd_rn(acc[q], q == (int)r ? v : 0.0);
+}
+
+template <int D>
 __global__ void __launch_bounds__(256) k_pr_gather32(const WorkItem *__restrict__ items, uint32_t n_items, uint32_t n,
                                                      const uint32_t *__restrict__ tci, const uint8_t *__restrict__ tiles,
                                                      const float *__restrict__ x, double *__restrict__ y,
                                                      double *__restrict__ part) {
     static_assert(D == 4 || D == 8, "one 32/64-bit word per tile");
+    using TW = typename std::conditional<D == 4, uint32_t, unsigned long long>::type;  // row r in byte r
     const uint32_t lane = lane_id(), warps = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n_items; w += warps) {
         const WorkItem it = items[w];
         double acc[D];
 #pragma unroll
         for (int r = 0; r < D; r++) acc[r] = 0.0;
-        constexpr int U = 4;  // tiles per lane per step, their loads issued together
+        // U tiles per lane per step: tile loads, then every tile's FIRST set bit
+        // gathered unconditionally (R-MAT: ~1 bit per tile), all in flight
+        // together; further bits of a tile are the rare tail
+        constexpr int U = 8;
         for (uint32_t t = it.t0 + lane; t < it.t1; t += 32 * U) {
-            uint32_t k[U], wd[U][D / 4];
+            uint32_t k[U];
+            TW wd[U];
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 const uint32_t tu = t + 32 * u;
                 const bool ok = tu < it.t1;
                 k[u] = ok ? ld_stream32(tci + tu) : 0u;
-                if constexpr (D == 4) {
-                    wd[u][0] = ok ? ld_stream32(tiles + (size_t)tu * 4) : 0u;
-                } else {
-                    wd[u][0] = ok ? ld_stream32(tiles + (size_t)tu * 8) : 0u;
-                    wd[u][1] = ok ? ld_stream32(tiles + (size_t)tu * 8 + 4) : 0u;
-                }
+                if constexpr (D == 4) wd[u] = ok ? ld_stream32(tiles + (size_t)tu * 4) : 0u;
+                else wd[u] = ok ? ((TW)ld_stream32(tiles + (size_t)tu * 8 + 4) << 32) | ld_stream32(tiles + (size_t)tu * 8) : 0ull;
+            }
+            float v[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const int p = wd[u] ? (D == 4 ? __ffs((uint32_t)wd[u]) : __ffsll((long long)wd[u])) - 1 : 0;
+                v[u] = wd[u] ? __ldg(x + (size_t)k[u] * D + (p & 7)) : 0.0f;
             }
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                const float *xs = x + (size_t)k[u] * D;
-#pragma unroll
-                for (int r = 0; r < D; r++) {
-                    uint32_t b = (wd[u][r / 4] >> (8 * (r % 4))) & 0xFFu;
-                    while (b) {
-                        acc[r] = __dadd_rn(acc[r], (double)__ldg(xs + __ffs(b) - 1));
-                        b &= b - 1;
-                    }
+                TW b = wd[u];
+                if (!b) continue;
+                int p = (D == 4 ? __ffs((uint32_t)b) : __ffsll((long long)b)) - 1;
+                pr_add<D>(acc, (uint32_t)p >> 3, (double)v[u]);
+                b &= b - 1;
+                while (b) {
+                    p = (D == 4 ? __ffs((uint32_t)b) : __ffsll((long long)b)) - 1;
+                    b &= b - 1;
+                    pr_add<D>(acc, (uint32_t)p >> 3, (double)__ldg(x + (size_t)k[u] * D + (p & 7)));
                 }
             }
         }
         double mine = 0.0;
 #pragma unroll
         for (int r = 0; r < D; r++) {
-            double v = acc[r];
+            double val = acc[r];
 #pragma unroll
-            for (int o = 16; o; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
-            if (lane == (uint32_t)r) mine = v;
+            for (int o = 16; o; o >>= 1) val = __dadd_rn(val, __shfl_xor_sync(0xffffffffu, val, o));
+            if (lane == (uint32_t)r) mine = val;
         }
-        const uint64_t v = (uint64_t)it.row * D + lane;
+        const uint64_t vrow = (uint64_t)it.row * D + lane;
         if (lane < (uint32_t)D) {
             if (it.split) part[(size_t)w * D + lane] = mine;
-            else if (v < n) y[v] = mine;
+            else if (vrow < n) y[vrow] = mine;
         }
     }
 }
@@ -1681,6 +1697,8 @@ int b2sr_pagerank(const b2sr_matrix *a, const double *d_out_degree, double alpha
     if (trace)
         for (auto &e : ev) CK(cudaEventCreate(&e));
     const bool fast = pr_fast_mode(d);
+    const char *pxe = getenv("B2SR_PR_XPERM");  // fast mode: relabelled x' (default on; 0 = plain x)
+    const bool pr_xperm = fast && !(pxe && pxe[0] == '0');
     Buf<float> x32(fast ? (size_t)a->ntr * d : 1, s);
     Buf<double> part;
     if (fast) {
@@ -1693,15 +1711,18 @@ int b2sr_pagerank(const b2sr_matrix *a, const double *d_out_degree, double alpha
     while (sweeps < max_iter) {
         if (trace) CK(cudaEventRecord(ev[0], s));
         if (fast) {
-            LAUNCH(k_to_f32, grid_for(n), 256, 0, s, n, xs.p, x32.p);
+            // hot-first relabelled float32 x' (bmv_xperm.cu): hot columns share
+            // cache lines, so more of the random gathers hit L1 / L2
+            const uint32_t *gtci = pr_xperm ? xperm_apply_f32(const_cast<b2sr_matrix *>(a), xs.p, x32.p, s) : a->tci;
+            if (!pr_xperm) LAUNCH(k_to_f32, grid_for(n), 256, 0, s, n, xs.p, x32.p);
             const unsigned gi = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)a->n_items + 7) / 8,
                                                                                     (uint64_t)num_sms() * 16));
             kernel_timer().begin(s);
             if (d == 4)
-                LAUNCH(k_pr_gather32<4>, gi, 256, 0, s, a->items, a->n_items, n, a->tci, (const uint8_t *)a->tiles, x32.p,
+                LAUNCH(k_pr_gather32<4>, gi, 256, 0, s, a->items, a->n_items, n, gtci, (const uint8_t *)a->tiles, x32.p,
                        g.p, part.p);
             else
-                LAUNCH(k_pr_gather32<8>, gi, 256, 0, s, a->items, a->n_items, n, a->tci, (const uint8_t *)a->tiles, x32.p,
+                LAUNCH(k_pr_gather32<8>, gi, 256, 0, s, a->items, a->n_items, n, gtci, (const uint8_t *)a->tiles, x32.p,
                        g.p, part.p);
             kernel_timer().end(s);
             if (a->any_split) {
