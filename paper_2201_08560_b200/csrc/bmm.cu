@@ -93,7 +93,6 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t *__restrict__
 // 26.1 ms; s26 -, 6.81, 5.90, 5.39, 5.35, 5.43 s -- fewer, larger items win
 // until the hub pairs stop spreading).  B2SR_TC_CHUNK overrides (A/B).
 constexpr uint32_t TC_CHUNK = 2048;
-constexpr uint32_t TC_STAGE = 256;  // words of the longer row staged per warp
 
 __global__ void k_tc_item_counts(uint64_t TM, const uint32_t *__restrict__ m_rowid, const uint32_t *__restrict__ m_tci,
                                  uint32_t m_row0, const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ b_trp,
@@ -118,7 +117,7 @@ __global__ void k_tc_item_fill(uint64_t TM, const uint32_t *__restrict__ cnt, co
 }
 
 template <int D>
-__global__ void __launch_bounds__(256, 8) k_bmm_masked_items(uint64_t n_items, const uint2 *__restrict__ items,
+__global__ void __launch_bounds__(256) k_bmm_masked_items(uint64_t n_items, const uint2 *__restrict__ items,
                                                           const uint32_t *__restrict__ m_rowid,
                                                           const uint32_t *__restrict__ m_tci,
                                                           const typename WordT<D>::T *__restrict__ m_tiles,
@@ -128,13 +127,6 @@ __global__ void __launch_bounds__(256, 8) k_bmm_masked_items(uint64_t n_items, c
                                                           const typename WordT<D>::T *__restrict__ b_tiles,
                                                           uint32_t m_row0, unsigned long long *__restrict__ out,
                                                           unsigned long long *__restrict__ work, uint32_t chunk) {
-    // the narrowed range of the longer row, staged per warp when short enough:
-    // the per-lane binary searches then wait on shared memory, not on a
-    // chain of dependent L2 loads (TC_STAGE words: 8 KB per 256-thread CTA,
-    // no occupancy cost -- r01's staging of whole rows up to 2048 entries
-    // cost a quarter of the occupancy and was slower at s26)
-    __shared__ uint32_t lstage[8][TC_STAGE];
-    uint32_t *ls = lstage[threadIdx.x >> 5];
     const uint32_t lane = lane_id();
     const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long acc = 0, units = 0;
@@ -156,33 +148,14 @@ __global__ void __launch_bounds__(256, 8) k_bmm_masked_items(uint64_t n_items, c
         uint32_t lo = lower_bound_u32(ltci, l0, l1, first);
         uint32_t hi = lower_bound_u32(ltci, lo, l1, last + 1);
         if (lo == hi || rows_used == 0) continue;
-        const bool staged = hi - lo <= TC_STAGE;
-        if (staged) {
-            __syncwarp();
-            for (uint32_t q = lane; q < hi - lo; q += 32) ls[q] = __ldg(ltci + lo + q);
-            __syncwarp();
-        }
         for (uint32_t base = c0; base < c1; base += 32) {
             uint32_t si = base + lane;
             uint32_t ta = 0, tb = 0;
             bool hit = false;
             if (si < c1) {
                 uint32_t K = __ldg(stci + si);
-                uint32_t li;
-                bool eq;
-                if (staged) {
-                    uint32_t a = 0, b = hi - lo;
-                    while (a < b) {
-                        const uint32_t mid = (a + b) >> 1;
-                        if (ls[mid] < K) a = mid + 1; else b = mid;
-                    }
-                    eq = a < hi - lo && ls[a] == K;
-                    li = lo + a;
-                } else {
-                    li = lower_bound_u32(ltci, lo, hi, K);
-                    eq = li < hi && __ldg(ltci + li) == K;
-                }
-                if (eq) {
+                uint32_t li = lower_bound_u32(ltci, lo, hi, K);
+                if (li < hi && __ldg(ltci + li) == K) {
                     hit = true;
                     ta = a_short ? si : li;
                     tb = a_short ? li : si;
