@@ -259,6 +259,37 @@ __device__ __forceinline__ uint32_t ld_stream32(const void *p) {
     return v;
 }
 
+// 32-bit shared-window addresses kept in registers: ptxas otherwise re-derives
+// the base of every static __shared__ array (S2R CgaCtaId + LEA) inside hot
+// loops.  The accessors are volatile with a memory clobber, so they stay
+// ordered with barriers and with each other.
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+    uint32_t a;
+    asm volatile("{ .reg .u64 t; cvta.to.shared.u64 t, %1; cvt.u32.u64 %0, t; }" : "=r"(a) : "l"(p));
+    return a;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned long long lds_u64(uint32_t a) {
+    unsigned long long v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+
 #define B2SR_PLAN_LOCK(m) std::lock_guard<std::recursive_mutex> b2sr_plan_guard_((m)->plan_mu)
 
 // Valid-bit mask of bit-vector word w (formats.py:433-441).

@@ -96,15 +96,15 @@ constexpr uint32_t TC_CHUNK = 2048;
 
 __global__ void k_tc_item_counts(uint64_t TM, const uint32_t *__restrict__ m_rowid, const uint32_t *__restrict__ m_tci,
                                  uint32_t m_row0, const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ b_trp,
-                                 uint32_t chunk, uint32_t *__restrict__ cnt, uint32_t hashed_max,
-                                 const uint32_t *__restrict__ m_trp) {
+                                 uint32_t chunk, uint32_t *__restrict__ cnt,
+                                 const uint32_t *__restrict__ fparts) {
     for (uint64_t mt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; mt < TM; mt += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t i = m_rowid[mt], I = i + m_row0, J = m_tci[mt];
         uint32_t la = a_trp[I + 1] - a_trp[I], lb = b_trp[J + 1] - b_trp[J];
         uint32_t sh = min(la, lb);
-        // rows the row-hash kernel takes (A row and mask row both <= hashed_max) get no items here
-        const bool hashed = la <= hashed_max && m_trp[i + 1] - m_trp[i] <= hashed_max;
-        cnt[mt] = la && lb && !hashed ? (sh + chunk - 1) / chunk : 0;
+        // rows the filter kernel takes get no items here
+        const bool filtered = fparts && fparts[i] != 0;
+        cnt[mt] = la && lb && !filtered ? (sh + chunk - 1) / chunk : 0;
     }
 }
 
@@ -187,165 +187,229 @@ __global__ void __launch_bounds__(256) k_bmm_masked_items(uint64_t n_items, cons
     }
 }
 
-// ------------------------------------------------------------ row-hash items
-// Mask rows whose A row is short enough (<= TCH_MAX tiles): one warp per mask
-// row I stages A's row I once as an open-addressing table in shared memory
-// (tile column -> position; load factor <= 1/2), then for every mask tile
-// (I, J) streams Bt's row J with coalesced loads and probes the table -- O(1)
-// per entry instead of a binary search of the longer row per entry of the
-// shorter one (s20 d=4: 2.5 G searched entries x ~8 dependent steps).  Hits
-// do the AND+POPC of the pair's tiles exactly as below; the sum over common K
-// is order-free integer arithmetic.  Longer A rows keep the chunked
-// binary-search items.
-constexpr uint32_t TCH_SLOTS = 1024;             // per warp
-constexpr uint32_t TCH_MAX = TCH_SLOTS / 2;      // longest A row staged
-constexpr uint32_t TCH_WARPS = 8;
-
-__device__ __forceinline__ uint32_t tch_hash(uint32_t k, uint32_t shift) { return (k * 0x9E3779B1u) >> shift; }
+// ------------------------------------------------------------ row-filter items
+// Mask rows whose A row and mask row are both short enough (<= TCB_CAP tiles,
+// every row of the degree-oriented DAG at R-MAT s20) and D <= 8: one CTA per
+// work item (mask row I, part p of P) stages A's row I in shared memory --
+// its tile columns, its tiles, and a one-bit-per-column filter indexed by the
+// low TCB_BITS_LG bits of the column -- plus mask row I's tiles, the row
+// starts of the Bt rows J it names and the exclusive prefix of their lengths.
+// The concatenation of those Bt rows is the item's flat probe space; the 8
+// warps stride it 32 entries at a time (no lane idles on a short row J, and
+// the split across items is by equal probe counts, not by whole rows).  Per
+// entry: one coalesced load of the column K, one shared-memory filter test;
+// only on a filter hit (~8 % at s20) a binary search of A's staged columns
+// confirms K and gives its position, and the AND+POPC of the tile pair is
+// done with byte-parallel masks.  Replaces the per-lane binary search of the
+// longer row for every entry of the shorter one (~40 warp instructions per
+// AND+POPC unit).  The sum over common K is order-free integer arithmetic, so
+// the count is the item kernel's bit for bit.
+constexpr uint32_t TCB_CAP = 1024;       // longest A row / mask row staged
+constexpr uint32_t TCB_BITS_LG = 16;     // filter: 2^16 bits = 8 KB (false hits <= 1024 / 2^16)
+constexpr uint32_t TCB_THREADS = 256;
+constexpr uint32_t TCB_BUDGET = 16384;   // probed Bt entries per work item (B2SR_TC_BUDGET overrides)
+constexpr uint32_t TCB_MAXCH = 1024;     // 32-probe chunks per item: budget <= 32 * (TCB_MAXCH - 2)
 
 template <int D>
-__device__ __forceinline__ uint64_t tile_bits(const typename WordT<D>::T *__restrict__ tiles, size_t t) {
+using TileBits = typename std::conditional<D == 4, uint32_t, unsigned long long>::type;
+
+template <int D>
+__device__ __forceinline__ TileBits<D> tile_bits(const typename WordT<D>::T *__restrict__ tiles, size_t t) {
     // D <= 8: the whole tile in one load (row r in byte r; d = 4 keeps the high nibble clear)
-    if constexpr (D == 4) return __ldg(reinterpret_cast<const uint32_t *>(tiles) + t);
-    else return __ldg(reinterpret_cast<const unsigned long long *>(tiles) + t);
+    return __ldg(reinterpret_cast<const TileBits<D> *>(tiles) + t);
+}
+
+// bytes of x (< 256) replicated: byte c of the result is 0xFF iff bit c of m is set
+__device__ __forceinline__ unsigned long long expand_bits8(uint32_t m) {
+    unsigned long long e = ((unsigned long long)m * 0x0101010101010101ull) & 0x8040201008040201ull;
+    e = ((e + 0x7F7F7F7F7F7F7F7Full) | e) & 0x8080808080808080ull;
+    return (e >> 7) * 0xFFull;
+}
+
+// sum over mask bits (r, c) of popc(A[r] & B[c]); units: sum over rows r with
+// A[r] != 0 of popc(M[r]) (the item kernel's AND+POPC unit count)
+template <int D>
+__device__ __forceinline__ void tc_tile_pair(TileBits<D> m, TileBits<D> a, TileBits<D> b, unsigned long long &acc,
+                                             unsigned long long &units, bool count_units) {
+    while (m) {
+        const uint32_t r = (uint32_t)(__ffsll((long long)m) - 1) >> 3;
+        const uint32_t mw = (uint32_t)(m >> (8 * r)) & 0xFFu, aw = (uint32_t)(a >> (8 * r)) & 0xFFu;
+        m &= ~((TileBits<D>)0xFF << (8 * r));
+        if (!aw) continue;
+        if (count_units) units += __popc(mw);
+        const unsigned long long sel = expand_bits8(mw) & ((unsigned long long)aw * 0x0101010101010101ull);
+        if constexpr (D == 4) acc += __popc((uint32_t)sel & (uint32_t)b);
+        else acc += __popcll(sel & (unsigned long long)b);
+    }
+}
+
+// a queued filter hit: confirm K in A's staged row (binary search), then the tile pair
+// (s_*: 32-bit shared addresses of the staged arrays)
+template <int D>
+__device__ __forceinline__ void tc_resolve(uint32_t t, uint32_t j, uint32_t la, uint32_t s_acol, uint32_t s_atile,
+                                           uint32_t s_mtile, const uint32_t *__restrict__ b_tci,
+                                           const typename WordT<D>::T *__restrict__ b_tiles, unsigned long long &acc,
+                                           unsigned long long &units, bool count_units) {
+    constexpr uint32_t TBY = sizeof(TileBits<D>);
+    const uint32_t K = __ldg(b_tci + t);
+    uint32_t pl = 0, ph = la;
+    while (pl < ph) {
+        const uint32_t mid = (pl + ph) >> 1;
+        if (lds_u32(s_acol + 4 * mid) < K) pl = mid + 1; else ph = mid;
+    }
+    if (pl < la && lds_u32(s_acol + 4 * pl) == K) {
+        TileBits<D> m, a;
+        if constexpr (D == 4) { m = lds_u32(s_mtile + 4 * j); a = lds_u32(s_atile + 4 * pl); }
+        else { m = lds_u64(s_mtile + TBY * j); a = lds_u64(s_atile + TBY * pl); }
+        tc_tile_pair<D>(m, a, tile_bits<D>(b_tiles, t), acc, units, count_units);
+    }
 }
 
 template <int D>
-__global__ void __launch_bounds__(TCH_WARPS * 32) k_tc_rowhash(
-    uint32_t m_ntr, uint32_t m_row0, const uint32_t *__restrict__ m_trp, const uint32_t *__restrict__ m_tci,
+__global__ void __launch_bounds__(TCB_THREADS) k_tc_filter(
+    uint32_t m_row0, const uint32_t *__restrict__ m_trp, const uint32_t *__restrict__ m_tci,
     const typename WordT<D>::T *__restrict__ m_tiles, const uint32_t *__restrict__ a_trp,
     const uint32_t *__restrict__ a_tci, const typename WordT<D>::T *__restrict__ a_tiles,
     const uint32_t *__restrict__ b_trp, const uint32_t *__restrict__ b_tci,
-    const typename WordT<D>::T *__restrict__ b_tiles, const uint2 *__restrict__ hitems, uint32_t n_hitems,
+    const typename WordT<D>::T *__restrict__ b_tiles, const uint2 *__restrict__ items, uint32_t n_items,
     uint32_t *__restrict__ next_item, unsigned long long *__restrict__ out, unsigned long long *__restrict__ work) {
-    __shared__ uint32_t keys[TCH_WARPS][TCH_SLOTS];
-    __shared__ uint16_t posn[TCH_WARPS][TCH_SLOTS];
-    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
-    uint32_t *kt = keys[wid];
-    uint16_t *pt = posn[wid];
+    using TB = TileBits<D>;
+    constexpr uint32_t FW = 1u << (TCB_BITS_LG - 5), FM = (1u << TCB_BITS_LG) - 1;
+    constexpr uint32_t NW = TCB_THREADS / 32, PER = TCB_CAP / TCB_THREADS;
+    __shared__ uint32_t filt[FW];
+    __shared__ uint32_t acol[TCB_CAP];
+    __shared__ TB atile[TCB_CAP];
+    __shared__ TB mtile[TCB_CAP];
+    __shared__ uint32_t jst[TCB_CAP];
+    __shared__ uint32_t pre[TCB_CAP + 1];
+    __shared__ uint16_t jfirst[TCB_MAXCH];
+    __shared__ uint32_t ring_t[NW][64];
+    __shared__ uint16_t ring_j[NW][64];
+    __shared__ uint32_t wtot[NW];
+    __shared__ uint32_t s_item;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5, lt_mask = (1u << lane) - 1u;
+    for (uint32_t q = tid; q < FW; q += TCB_THREADS) filt[q] = 0;
     unsigned long long acc = 0, units = 0;
     for (;;) {
-        uint32_t w = 0;
-        if (lane == 0) w = atomicAdd(next_item, 1u);
-        w = __shfl_sync(0xffffffffu, w, 0);
-        if (w >= n_hitems) break;
-        const uint2 hit_item = hitems[w];
-        const uint32_t i = hit_item.x, part = hit_item.y & 0xFFFFu, parts = hit_item.y >> 16;
-        uint32_t m0 = __ldg(m_trp + i), m1 = __ldg(m_trp + i + 1);
+        if (tid == 0) s_item = atomicAdd(next_item, 1u);
+        __syncthreads();  // also orders the previous item's filter clear before this item's staging
+        const uint32_t w = s_item;
+        if (w >= n_items) break;
+        const uint2 it = __ldg(items + w);
+        const uint32_t i = it.x, part = it.y & 0xFFFFu, parts = it.y >> 16;
+        const uint32_t m0 = __ldg(m_trp + i), nm = __ldg(m_trp + i + 1) - m0;
         const uint32_t I = m_row0 + i, a0 = __ldg(a_trp + I), la = __ldg(a_trp + I + 1) - a0;
-        if (parts > 1) {  // this item's share of the row's mask tiles: equal Bt-row entry counts
-            const uint32_t nj = m1 - m0;  // <= TCH_MAX
-            uint32_t lens[TCH_MAX / 32], run = 0;
-#pragma unroll
-            for (int k = 0; k < (int)(TCH_MAX / 32); k++) {
-                const uint32_t j = k * 32 + lane;
-                uint32_t l = 0;
-                if (j < nj) {
-                    const uint32_t J = __ldg(m_tci + m0 + j);
-                    l = __ldg(b_trp + J + 1) - __ldg(b_trp + J);
-                }
-                uint32_t incl = l;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= (uint32_t)o) incl += y;
-                }
-                lens[k] = run + incl - l;  // exclusive prefix of j
-                run += __shfl_sync(0xffffffffu, incl, 31);
-            }
-            const unsigned long long tot = run;
-            const uint32_t lo_t = (uint32_t)(tot * part / parts), hi_t = (uint32_t)(tot * (part + 1) / parts);
-            uint32_t jlo = 0, jhi = 0;
-#pragma unroll
-            for (int k = 0; k < (int)(TCH_MAX / 32); k++) {
-                const uint32_t j = k * 32 + lane;
-                jlo += __popc(__ballot_sync(0xffffffffu, j < nj && lens[k] < lo_t));
-                jhi += __popc(__ballot_sync(0xffffffffu, j < nj && lens[k] < hi_t));
-            }
-            if (part + 1 == parts) jhi = nj;
-            if (part == 0) jlo = 0;
-            m1 = m0 + jhi;
-            m0 = m0 + jlo;
-            if (m0 >= m1) continue;
-        }
-        const uint32_t lg = max(5u, 32u - __clz(2 * la - 1));  // slots = 2^lg >= 2*la
-        const uint32_t S = 1u << lg, shift = 32 - lg;
-        for (uint32_t q = lane; q < S; q += 32) kt[q] = 0;
-        __syncwarp();
-        for (uint32_t q = lane; q < la; q += 32) {
+        for (uint32_t q = tid; q < la; q += TCB_THREADS) {
             const uint32_t K = __ldg(a_tci + a0 + q);
-            uint32_t h = tch_hash(K, shift);
-            while (atomicCAS(kt + h, 0u, K + 1) != 0u) h = (h + 1) & (S - 1);
-            pt[h] = (uint16_t)q;
+            acol[q] = K;
+            atile[q] = tile_bits<D>(a_tiles, (size_t)a0 + q);
+            atomicOr(filt + ((K & FM) >> 5), 1u << (K & 31u));
+        }
+        // mask row: Bt row starts, mask tiles, block-exclusive prefix of the Bt row lengths
+        uint32_t len[PER], run = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < PER; k++) {
+            const uint32_t q = tid * PER + k;
+            len[k] = 0;
+            if (q < nm) {
+                const uint32_t J = __ldg(m_tci + m0 + q), b0 = __ldg(b_trp + J);
+                len[k] = __ldg(b_trp + J + 1) - b0;
+                jst[q] = b0;
+                mtile[q] = tile_bits<D>(m_tiles, (size_t)m0 + q);
+            }
+            run += len[k];
+        }
+        uint32_t incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+        }
+        if (lane == 31) wtot[wid] = incl;
+        __syncthreads();
+        uint32_t off = incl - run;
+        for (uint32_t v = 0; v < wid; v++) off += wtot[v];
+#pragma unroll
+        for (uint32_t k = 0; k < PER; k++) {
+            const uint32_t q = tid * PER + k;
+            if (q <= nm) pre[q] = off;  // q == nm: the total
+            off += len[k];
+        }
+        if (tid == TCB_THREADS - 1 && nm == TCB_CAP) pre[TCB_CAP] = off;
+        __syncthreads();
+        const uint32_t total = pre[nm];
+        const uint32_t lo = (uint32_t)((unsigned long long)total * part / parts);
+        const uint32_t hi = (uint32_t)((unsigned long long)total * (part + 1) / parts);
+        // chunk (32 probes) -> the row j holding its first entry
+        for (uint32_t j = tid; j < nm; j += TCB_THREADS) {
+            const uint32_t s0 = max(pre[j], lo), s1 = min(pre[j + 1], hi);
+            if (s0 < s1)
+                for (uint32_t c = (s0 - lo + 31) >> 5, ce = (s1 - lo + 31) >> 5; c < ce; c++) jfirst[c] = (uint16_t)j;
+        }
+        __syncthreads();
+        // filter hits are queued per warp (ring of 64) and resolved 32 at a
+        // time with every lane busy: ~1 lane in 12 hits, so resolving them
+        // in place would run the search of A's row on nearly every chunk
+        uint32_t qh = 0, qtl = 0;
+        const uint32_t s_rt = smem_addr(&ring_t[wid][0]), s_rj = smem_addr(&ring_j[wid][0]);
+        const uint32_t s_pre = smem_addr(pre), s_jst = smem_addr(jst), s_jf = smem_addr(jfirst);
+        const uint32_t s_filt = smem_addr(filt), s_acol = smem_addr(acol), s_atile = smem_addr(atile);
+        const uint32_t s_mtile = smem_addr(mtile);
+        for (uint32_t base = lo + wid * 32; base < hi; base += TCB_THREADS) {
+            const bool valid = base + lane < hi;
+            const uint32_t e = valid ? base + lane : hi - 1;
+            // j = largest row with pre[j] <= e: the chunk's first row plus the
+            // number of the next 32 row starts <= e
+            const uint32_t j0 = lds_u16(s_jf + 2 * ((base - lo) >> 5));
+            const uint32_t q = j0 + 1 + lane;
+            const uint32_t v = q <= nm ? lds_u32(s_pre + 4 * q) : 0xFFFFFFFFu;
+            uint32_t j = j0;
+            if (__shfl_sync(0xffffffffu, v, 0) <= min(base + 31, hi - 1)) {  // the chunk crosses a row start
+                uint32_t c = 0;
+#pragma unroll
+                for (uint32_t st = 16; st; st >>= 1)
+                    if (__shfl_sync(0xffffffffu, v, c + st - 1) <= e) c += st;
+                j = j0 + c;
+                if (c == 31 && __shfl_sync(0xffffffffu, v, 31) <= e) {  // > 31 (empty) rows crossed
+                    uint32_t jl = j0 + 32, jh = nm;  // pre[jl] <= e < pre[jh]
+                    while (jh - jl > 1) {
+                        const uint32_t mid = (jl + jh) >> 1;
+                        if (lds_u32(s_pre + 4 * mid) <= e) jl = mid; else jh = mid;
+                    }
+                    j = jl;
+                }
+            }
+            bool hit = false;
+            uint32_t t = 0;
+            if (valid) {
+                t = lds_u32(s_jst + 4 * j) + (e - lds_u32(s_pre + 4 * j));
+                const uint32_t K = __ldg(b_tci + t);
+                hit = (lds_u32(s_filt + 4 * ((K & FM) >> 5)) >> (K & 31u)) & 1u;
+            }
+            const uint32_t hm = __ballot_sync(0xffffffffu, hit);
+            if (hit) {
+                const uint32_t pos = (qtl + __popc(hm & lt_mask)) & 63u;
+                sts_u32(s_rt + 4 * pos, t);
+                sts_u16(s_rj + 2 * pos, j);
+            }
+            qtl += __popc(hm);
+            if (qtl - qh >= 32) {
+                __syncwarp();
+                const uint32_t pos = (qh + lane) & 63u;
+                tc_resolve<D>(lds_u32(s_rt + 4 * pos), lds_u16(s_rj + 2 * pos), la, s_acol, s_atile, s_mtile, b_tci,
+                              b_tiles, acc, units, work != nullptr);
+                qh += 32;
+                __syncwarp();
+            }
         }
         __syncwarp();
-        for (uint32_t mt = m0; mt < m1; mt++) {
-            const uint32_t J = __ldg(m_tci + mt);
-            const uint32_t b0 = __ldg(b_trp + J), b1 = __ldg(b_trp + J + 1);
-            if (b0 == b1) continue;
-            uint64_t mbits = 0;
-            uint32_t mword = 0, rows_used = 0;
-            if constexpr (D <= 8) {
-                mbits = tile_bits<D>(m_tiles, mt);
-            } else {
-                mword = lane < (uint32_t)D ? (uint32_t)m_tiles[(size_t)mt * D + lane] : 0u;
-                rows_used = __ballot_sync(0xffffffffu, mword != 0);
-            }
-            for (uint32_t base = b0; base < b1; base += 32) {
-                const uint32_t t = base + lane;
-                uint32_t ta = 0xFFFFFFFFu;
-                if (t < b1) {
-                    const uint32_t K = __ldg(b_tci + t);
-                    uint32_t h = tch_hash(K, shift);
-                    for (;;) {
-                        const uint32_t k = kt[h];
-                        if (k == K + 1) { ta = pt[h]; break; }
-                        if (k == 0) break;
-                        h = (h + 1) & (S - 1);
-                    }
-                }
-                const bool hit = ta != 0xFFFFFFFFu;
-                if constexpr (D <= 8) {
-                    if (hit) {
-                        const uint64_t av = tile_bits<D>(a_tiles, (size_t)a0 + ta), bv = tile_bits<D>(b_tiles, t);
-                        uint64_t mm = mbits;
-                        while (mm) {  // mask bit (r, c) at bit 8r + c
-                            const int bit = __ffsll((long long)mm) - 1;
-                            const uint32_t r = bit >> 3;
-                            const uint32_t aw = (uint32_t)(av >> (8 * r)) & 0xFFu;
-                            const uint32_t mw = (uint32_t)(mm >> (8 * r)) & 0xFFu;
-                            mm &= ~(0xFFull << (8 * r));
-                            if (!aw) continue;
-                            if (work) units += __popc(mw);
-                            uint32_t cc = mw;
-                            while (cc) {
-                                const int c = __ffs(cc) - 1;
-                                cc &= cc - 1;
-                                acc += __popc(aw & ((uint32_t)(bv >> (8 * c)) & 0xFFu));
-                            }
-                        }
-                    }
-                } else {
-                    if (!__ballot_sync(0xffffffffu, hit)) continue;
-                    uint32_t ru = rows_used;
-                    while (ru) {  // warp-uniform loop over non-empty mask rows
-                        const int r = __ffs(ru) - 1;
-                        ru &= ru - 1;
-                        uint32_t mw = __shfl_sync(0xffffffffu, mword, r);
-                        if (hit) {
-                            const uint32_t aw = a_tiles[((size_t)a0 + ta) * D + r];
-                            if (work) units += aw ? __popc(mw) : 0u;
-                            while (aw && mw) {
-                                const int c = __ffs(mw) - 1;
-                                mw &= mw - 1;
-                                acc += __popc(aw & (uint32_t)b_tiles[(size_t)t * D + c]);
-                            }
-                        }
-                    }
-                }
-            }
+        if (lane < qtl - qh) {
+            const uint32_t pos = (qh + lane) & 63u;
+            tc_resolve<D>(lds_u32(s_rt + 4 * pos), lds_u16(s_rj + 2 * pos), la, s_acol, s_atile, s_mtile, b_tci,
+                          b_tiles, acc, units, work != nullptr);
         }
-        __syncwarp();
+        __syncthreads();
+        for (uint32_t q = tid; q < la; q += TCB_THREADS) filt[(acol[q] & FM) >> 5] = 0;
     }
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (lane == 0 && acc) atomicAdd(out, acc);
@@ -355,32 +419,30 @@ __global__ void __launch_bounds__(TCH_WARPS * 32) k_tc_rowhash(
     }
 }
 
-constexpr uint32_t TCH_BUDGET = 4096;  // probed Bt entries per row-hash work item
-
 // parts of each eligible mask row (0: the row takes the binary-search items or is empty)
-__global__ void k_tch_parts(uint32_t mntr, uint32_t m_row0, const uint32_t *__restrict__ m_trp,
+__global__ void k_tcb_parts(uint32_t mntr, uint32_t m_row0, const uint32_t *__restrict__ m_trp,
                             const uint32_t *__restrict__ m_tci, const uint32_t *__restrict__ a_trp,
-                            const uint32_t *__restrict__ b_trp, uint32_t *__restrict__ parts) {
+                            const uint32_t *__restrict__ b_trp, uint32_t budget, uint32_t *__restrict__ parts) {
     const uint32_t lane = lane_id(), warps = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < mntr; i += warps) {
         const uint32_t m0 = m_trp[i], m1 = m_trp[i + 1], I = m_row0 + i;
         const uint32_t la = a_trp[I + 1] - a_trp[I];
         uint32_t p = 0;
-        if (m1 > m0 && la && la <= TCH_MAX && m1 - m0 <= TCH_MAX) {
+        if (m1 > m0 && la && la <= TCB_CAP && m1 - m0 <= TCB_CAP) {
             unsigned long long w = 0;
             for (uint32_t t = m0 + lane; t < m1; t += 32) {
                 const uint32_t J = m_tci[t];
                 w += b_trp[J + 1] - b_trp[J];
             }
             for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-            const unsigned long long q = (w + TCH_BUDGET - 1) / TCH_BUDGET;
-            p = q == 0 ? 1u : (q > 0xFFFFull ? 0xFFFFu : (uint32_t)q);
+            const unsigned long long q = (w + budget - 1) / budget;
+            p = (q == 0 || w >= 0x80000000ull) ? 0u : (q > 0xFFFFull ? 0xFFFFu : (uint32_t)q);
         }
         if (lane == 0) parts[i] = p;
     }
 }
 
-__global__ void k_tch_fill(uint32_t mntr, const uint32_t *__restrict__ parts, const uint64_t *__restrict__ ofs,
+__global__ void k_tcb_fill(uint32_t mntr, const uint32_t *__restrict__ parts, const uint64_t *__restrict__ ofs,
                            uint2 *__restrict__ items) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mntr; i += gridDim.x * blockDim.x) {
         const uint32_t P = parts[i];
@@ -389,13 +451,10 @@ __global__ void k_tch_fill(uint32_t mntr, const uint32_t *__restrict__ parts, co
     }
 }
 
-// Measured (s20, B200): row-hash 41.8 / 50.4 ms vs binary-search items 25.6 /
-// 32.0 ms at d = 4 / 8 -- ncu: 25.8 G warp instructions (probe loops, partial
-// 32-entry chunks of short Bt rows, 0.56 G shared-memory bank conflicts) vs
-// 17.8 G.  Kept as an A/B path, off by default (B2SR_TC_HASH=1 enables it).
-static bool tc_rowhash_enabled() {
-    const char *e = getenv("B2SR_TC_HASH");
-    return e && e[0] == '1';
+// B2SR_TC_FILTER=0: every mask tile on the binary-search items (A/B)
+static bool tc_filter_enabled(int dim) {
+    const char *e = getenv("B2SR_TC_FILTER");
+    return dim <= 8 && !(e && e[0] == '0');
 }
 
 int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_matrix *mask, cudaStream_t s,
@@ -408,9 +467,27 @@ int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_ma
     row_ids(mask, rowid.p, s);
     const char *ce = getenv("B2SR_TC_CHUNK");  // entries of the shorter row per work item (A/B)
     const uint32_t chunk = ce ? std::max(32, atoi(ce)) : TC_CHUNK;
-    const bool hashed = tc_rowhash_enabled();
+    const bool filtered = tc_filter_enabled(a->dim);
+    Buf<uint2> fitems;
+    Buf<uint32_t> pc;
+    uint32_t n_fitems = 0;
+    if (filtered) {
+        // work items of the filter kernel: each eligible mask row cut into
+        // parts of <= budget probed Bt entries, handed out dynamically
+        const char *be = getenv("B2SR_TC_BUDGET");
+        const uint32_t budget = be ? (uint32_t)std::min(32 * (int)(TCB_MAXCH - 2), std::max(256, atoi(be))) : TCB_BUDGET;
+        const uint32_t mntr = mask->ntr;
+        pc = Buf<uint32_t>(std::max<uint32_t>(mntr, 1), s);
+        Buf<uint64_t> pofs((size_t)mntr + 1, s);
+        LAUNCH(k_tcb_parts, grid_for((uint64_t)mntr * 32), 256, 0, s, mntr, mask->row0, mask->trp, mask->tci, a->trp,
+               bt->trp, budget, pc.p);
+        exclusive_scan_u32_to_u64(pc.p, pofs.p, mntr, s);
+        n_fitems = (uint32_t)read_scalar(pofs.p + mntr, s);
+        fitems = Buf<uint2>(std::max<uint32_t>(n_fitems, 1), s);
+        if (n_fitems) LAUNCH(k_tcb_fill, grid_for(mntr), 256, 0, s, mntr, pc.p, pofs.p, fitems.p);
+    }
     LAUNCH(k_tc_item_counts, grid_for(TM), 256, 0, s, TM, rowid.p, mask->tci, mask->row0, a->trp, bt->trp, chunk, cnt.p,
-           hashed ? TCH_MAX : 0u, mask->trp);
+           filtered ? pc.p : nullptr);
     exclusive_scan_u32_to_u64(cnt.p, ofs.p, TM, s);
     uint64_t n_items = read_scalar(ofs.p + TM, s);
     Buf<unsigned long long> out(1, s);
@@ -424,36 +501,21 @@ int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_ma
     Buf<uint32_t> next_row(1, s);
     CK(cudaMemsetAsync(next_row.p, 0, 4, s));
     kernel_timer().begin(s);
-    Buf<uint2> hitems;
-    uint32_t n_hitems = 0;
-    if (hashed) {
-        // work items of the row-hash kernel: each eligible mask row cut into
-        // parts of <= TCH_BUDGET probed Bt entries (bounded tail), rows handed
-        // out dynamically
-        const uint32_t mntr = mask->ntr;
-        Buf<uint32_t> pc(std::max<uint32_t>(mntr, 1), s);
-        Buf<uint64_t> pofs((size_t)mntr + 1, s);
-        LAUNCH(k_tch_parts, grid_for((uint64_t)mntr * 32), 256, 0, s, mntr, mask->row0, mask->trp, mask->tci, a->trp,
-               bt->trp, pc.p);
-        exclusive_scan_u32_to_u64(pc.p, pofs.p, mntr, s);
-        n_hitems = (uint32_t)read_scalar(pofs.p + mntr, s);
-        hitems = Buf<uint2>(std::max<uint32_t>(n_hitems, 1), s);
-        if (n_hitems) LAUNCH(k_tch_fill, grid_for(mntr), 256, 0, s, mntr, pc.p, pofs.p, hitems.p);
-    }
-    if (n_hitems) {
-        const unsigned gh = (unsigned)std::min<uint64_t>((uint64_t)num_sms() * 6, ((uint64_t)n_hitems + TCH_WARPS - 1) / TCH_WARPS);
+    if (n_fitems) {
+        int per_sm = 1;
         switch (a->dim) {
-#define TCH_CASE(DD, W)                                                                                          \
-    case DD:                                                                                                     \
-        LAUNCH(k_tc_rowhash<DD>, gh, TCH_WARPS * 32, 0, s, mask->ntr, mask->row0, mask->trp, mask->tci,         \
-               (const W *)mask->tiles, a->trp, a->tci, (const W *)a->tiles, bt->trp, bt->tci,                   \
-               (const W *)bt->tiles, hitems.p, n_hitems, next_row.p, out.p, work_out ? work.p : nullptr);        \
+#define TCB_CASE(DD, W)                                                                                           \
+    case DD:                                                                                                      \
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_filter<DD>, TCB_THREADS, 0));               \
+        LAUNCH(k_tc_filter<DD>,                                                                                   \
+               (unsigned)std::min<uint64_t>((uint64_t)num_sms() * std::max(per_sm, 1), n_fitems), TCB_THREADS, 0, \
+               s, mask->row0, mask->trp, mask->tci, (const W *)mask->tiles, a->trp, a->tci, (const W *)a->tiles,  \
+               bt->trp, bt->tci, (const W *)bt->tiles, fitems.p, n_fitems, next_row.p, out.p,                     \
+               work_out ? work.p : nullptr);                                                                       \
         break;
-            TCH_CASE(4, uint8_t)
-            TCH_CASE(8, uint8_t)
-            TCH_CASE(16, uint16_t)
-            TCH_CASE(32, uint32_t)
-#undef TCH_CASE
+            TCB_CASE(4, uint8_t)
+            TCB_CASE(8, uint8_t)
+#undef TCB_CASE
         }
     }
     if (n_items) switch (a->dim) {

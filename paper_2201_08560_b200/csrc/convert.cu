@@ -33,12 +33,14 @@ struct ConvItem {
     uint32_t pad;
 };
 
-__global__ void k_conv_chunks(uint32_t n, uint32_t d, uint32_t ntr, const uint32_t *row_ptr, uint32_t *pcount) {
+// one item per tile row with <= whole entries, else ceil(e / chunk) column ranges
+__global__ void k_conv_chunks(uint32_t n, uint32_t d, uint32_t ntr, const uint32_t *row_ptr, uint32_t *pcount,
+                              uint32_t whole, uint32_t chunk) {
     uint32_t I = blockIdx.x * blockDim.x + threadIdx.x;
     if (I >= ntr) return;
     uint64_t r0 = (uint64_t)I * d, r1 = min((uint64_t)n, r0 + d);
     uint32_t e = row_ptr[r1] - row_ptr[r0];
-    uint32_t p = (e + CONV_CHUNK - 1) / CONV_CHUNK;
+    uint32_t p = e <= whole ? 1u : (e + chunk - 1) / chunk;
     pcount[I] = p ? p : 1u;
 }
 
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(256) k_conv(const ConvItem *__restrict__ items
                                               const uint32_t *__restrict__ col_ind, const uint64_t *__restrict__ iofs,
                                               uint32_t *__restrict__ cnt, uint32_t *__restrict__ tci,
                                               typename WordT<D>::T *__restrict__ tiles,
-                                              const uint32_t *__restrict__ order) {
+                                              const uint32_t *__restrict__ order, const uint8_t *__restrict__ only) {
     constexpr uint32_t GPW = 32 / D;  // groups (items) per warp
     const uint32_t lane = lane_id(), r = lane % D;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
@@ -82,6 +84,7 @@ __global__ void __launch_bounds__(256) k_conv(const ConvItem *__restrict__ items
         const uint32_t slot = wb * GPW + lane / D;
         bool valid = slot < n_items;
         uint32_t item = valid ? (order ? order[slot] : slot) : slot;
+        if (valid && only && !only[item]) valid = false;  // the warp merge did this item
         ConvItem it = valid ? items[item] : ConvItem{0, 0, 0, 0};
         uint64_t row = (uint64_t)it.row * D + r;
         uint32_t p = 0, end = 0;
@@ -132,6 +135,154 @@ __global__ void __launch_bounds__(256) k_conv(const ConvItem *__restrict__ items
     }
 }
 
+// ------------------------------------------------------------ warp merge (d = 4, 8)
+// One warp per item of <= CM_CAP CSR entries.  The item's d runs (one per
+// bit-row, each sorted by column) are staged in shared memory as u32 values
+// v = c << S | r (S = log2 d; needs n <= 2^(32-S)), then merged pairwise in
+// S levels -- each element finds its place in the merged pair with one binary
+// search of the partner run (values are distinct: no ties) -- which sorts
+// the item by (c, r), hence by tile column k = c >> S.  A ballot over "k
+// differs from the previous element" numbers the tiles; K1 counts them, K2
+// writes tile_col_ind at the first element of each tile and ORs every
+// element's bit into a shared-memory tile buffer that is then stored with
+// coalesced 32-bit stores.  Per element that is S searches of a ~30-entry run
+// instead of the per-step group min of the lock-step merge, whose warps loop
+// until their longest of 8 tile rows is done (ncu, s22 d=4: 2.13 G warp
+// instructions per pass).  Items over CM_CAP entries (hub rows cut into column
+// ranges that came out long) go to the lock-step merge above.
+constexpr uint32_t CM_CAP = 512;
+
+template <int D>
+struct ConvMerge {
+    static constexpr uint32_t S = D == 4 ? 2 : 3;
+    static constexpr uint32_t NW = D == 4 ? 8 : 4;        // warps per CTA (32 KB static shared memory)
+    static constexpr uint32_t TW = D == 4 ? 1 : 2;        // u32 words per tile
+    static constexpr uint32_t TBUF = D == 4 ? 0 : 2 * CM_CAP;  // d = 8: separate tile buffer
+};
+
+template <int D, bool PACK>
+__global__ void __launch_bounds__(ConvMerge<D>::NW * 32) k_conv_merge(
+    const ConvItem *__restrict__ items, uint32_t n_items, uint32_t n, const uint32_t *__restrict__ row_ptr,
+    const uint32_t *__restrict__ col_ind, const uint64_t *__restrict__ iofs, uint32_t *__restrict__ cnt,
+    uint32_t *__restrict__ tci, uint32_t *__restrict__ tiles32, uint8_t *__restrict__ big) {
+    using CMt = ConvMerge<D>;
+    constexpr uint32_t S = CMt::S, NW = CMt::NW, TW = CMt::TW;
+    __shared__ uint32_t buf[NW][2][CM_CAP];
+    __shared__ uint32_t tbuf[NW][CMt::TBUF ? CMt::TBUF : 1];
+    __shared__ uint32_t soff[NW][D + 1];
+    __shared__ uint32_t sst[NW][D];
+    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    uint32_t *off = soff[wid], *st = sst[wid];
+    for (uint32_t item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < n_items; item += warps) {
+        const ConvItem it = items[item];
+        // run r = bit-row r of tile row it.row, restricted to tile columns [klo, khi)
+        uint32_t p0 = 0, p1 = 0;
+        if (lane < (uint32_t)D) {
+            const uint64_t row = (uint64_t)it.row * D + lane;
+            if (row < n) {
+                p0 = row_ptr[row];
+                p1 = row_ptr[row + 1];
+                if (it.klo > 0) {
+                    uint32_t a = p0, b = p1;
+                    const uint32_t key = it.klo * (uint32_t)D;
+                    while (a < b) { const uint32_t m = (a + b) >> 1; if (__ldg(col_ind + m) < key) a = m + 1; else b = m; }
+                    p0 = a;
+                }
+                if ((uint64_t)it.khi * D < n) {
+                    uint32_t a = p0, b = p1;
+                    const uint32_t key = it.khi * (uint32_t)D;
+                    while (a < b) { const uint32_t m = (a + b) >> 1; if (__ldg(col_ind + m) < key) a = m + 1; else b = m; }
+                    p1 = a;
+                }
+            }
+        }
+        const uint32_t len = p1 - p0;
+        uint32_t incl = len;
+#pragma unroll
+        for (int o = 1; o < D; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+        }
+        const uint32_t E = __shfl_sync(0xffffffffu, incl, D - 1);
+        if (E > CM_CAP) {  // the lock-step merge takes it
+            if (!PACK && lane == 0) big[item] = 1;
+            continue;
+        }
+        __syncwarp();  // the previous item's readers of off/st are done
+        if (lane < (uint32_t)D) {
+            off[lane + 1] = incl;
+            st[lane] = p0;
+        }
+        if (lane == 0) off[0] = 0;
+        __syncwarp();
+        // stage: element i of run r (CSR index st[r] + i - off[r]) -> c << S | r
+        uint32_t *X = buf[wid][0], *Y = buf[wid][1];
+        for (uint32_t i = lane; i < E; i += 32) {
+            uint32_t r = 0;
+#pragma unroll
+            for (int q = 1; q < D; q++) r += off[q] <= i;
+            X[i] = (__ldg(col_ind + st[r] + (i - off[r])) << S) | r;
+        }
+        __syncwarp();
+        // S pairwise merge levels: level l merges runs of 2^l bit-rows in pairs
+#pragma unroll
+        for (uint32_t l = 0; l < S; l++) {
+            for (uint32_t i = lane; i < E; i += 32) {
+                uint32_t r = 0;
+#pragma unroll
+                for (int q = 1; q < D; q++) r += off[q] <= i;
+                const uint32_t j = r >> l;                   // level-l run of element i
+                const uint32_t a = off[j << l];              // its start
+                const uint32_t pj = j ^ 1u;                  // partner run
+                const uint32_t pa = off[pj << l], pb = off[min((pj + 1) << l, (uint32_t)D)];
+                const uint32_t ms = off[(j & ~1u) << l];     // merged run start
+                const uint32_t v = X[i];
+                uint32_t lo = pa, hi = pb;
+                while (lo < hi) { const uint32_t m = (lo + hi) >> 1; if (X[m] < v) lo = m + 1; else hi = m; }
+                Y[ms + (i - a) + (lo - pa)] = v;
+            }
+            __syncwarp();
+            uint32_t *t = X; X = Y; Y = t;
+        }
+        // X: sorted by (c, r).  Tiles = runs of equal k = v >> 2S.
+        if constexpr (PACK) {
+            uint32_t *T = CMt::TBUF ? tbuf[wid] : Y;
+            for (uint32_t q = lane; q < E * TW; q += 32) T[q] = 0;
+            __syncwarp();
+            const uint64_t tb = iofs[item];
+            uint32_t run = 0;
+            for (uint32_t base = 0; base < E; base += 32) {
+                const uint32_t i = base + lane;
+                const uint32_t v = i < E ? X[i] : 0u;
+                const uint32_t k = v >> (2 * S);
+                const bool first = i < E && (i == 0 || (X[i - 1] >> (2 * S)) != k);
+                const uint32_t fm = __ballot_sync(0xffffffffu, first);
+                const uint32_t t = run + __popc(fm & lt_mask) + (first ? 1u : 0u) - 1u;  // tile of element i
+                if (i < E) {
+                    const uint32_t r = v & (D - 1), c = (v >> S) & (D - 1);
+                    if (first) tci[tb + t] = k;
+                    // tile word: row r in byte r (d = 8: two u32 words per tile)
+                    atomicOr(T + t * TW + (r >> 2), 1u << (8 * (r & 3) + c));
+                }
+                run += __popc(fm);
+            }
+            __syncwarp();
+            uint32_t *dst = tiles32 + tb * TW;
+            for (uint32_t q = lane; q < run * TW; q += 32) dst[q] = T[q];
+        } else {
+            uint32_t run = 0;
+            for (uint32_t base = 0; base < E; base += 32) {
+                const uint32_t i = base + lane;
+                const bool first = i < E && (i == 0 || (X[i - 1] >> (2 * S)) != (X[i] >> (2 * S)));
+                run += __popc(__ballot_sync(0xffffffffu, first));
+            }
+            if (lane == 0) cnt[item] = run;
+        }
+    }
+}
+
 __global__ void k_conv_trp(uint32_t ntr, const uint64_t *pofs, const uint64_t *iofs, uint32_t *trp) {
     uint32_t I = blockIdx.x * blockDim.x + threadIdx.x;
     if (I <= ntr) trp[I] = (uint32_t)iofs[pofs[I]];
@@ -140,7 +291,7 @@ __global__ void k_conv_trp(uint32_t ntr, const uint64_t *pofs, const uint64_t *i
 template <int D>
 static void conv_launch(bool pack, const ConvItem *items, uint32_t n_items, uint32_t n, const uint32_t *row_ptr,
                         const uint32_t *col_ind, const uint64_t *iofs, uint32_t *cnt, uint32_t *tci, void *tiles,
-                        cudaStream_t s, const uint32_t *order) {
+                        cudaStream_t s, const uint32_t *order, const uint8_t *only) {
     constexpr uint32_t GPW = 32 / D;
     uint64_t warps = (n_items + GPW - 1) / GPW;
     uint64_t blocks = (warps + 7) / 8;
@@ -148,21 +299,47 @@ static void conv_launch(bool pack, const ConvItem *items, uint32_t n_items, uint
     unsigned g = (unsigned)(blocks < cap ? blocks : cap);
     if (pack)
         LAUNCH((k_conv<D, true>), g, 256, 0, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
-               (typename WordT<D>::T *)tiles, order);
+               (typename WordT<D>::T *)tiles, order, only);
     else
         LAUNCH((k_conv<D, false>), g, 256, 0, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
-               (typename WordT<D>::T *)tiles, order);
+               (typename WordT<D>::T *)tiles, order, only);
 }
 
 static void conv_dispatch(uint32_t d, bool pack, const ConvItem *items, uint32_t n_items, uint32_t n,
                           const uint32_t *row_ptr, const uint32_t *col_ind, const uint64_t *iofs, uint32_t *cnt,
-                          uint32_t *tci, void *tiles, cudaStream_t s, const uint32_t *order = nullptr) {
+                          uint32_t *tci, void *tiles, cudaStream_t s, const uint32_t *order = nullptr,
+                          const uint8_t *only = nullptr) {
     switch (d) {
-        case 4: conv_launch<4>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order); break;
-        case 8: conv_launch<8>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order); break;
-        case 16: conv_launch<16>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order); break;
-        default: conv_launch<32>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order); break;
+        case 4: conv_launch<4>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order, only); break;
+        case 8: conv_launch<8>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order, only); break;
+        case 16: conv_launch<16>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order, only); break;
+        default: conv_launch<32>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order, only); break;
     }
+}
+
+template <int D>
+static void merge_launch(bool pack, const ConvItem *items, uint32_t n_items, uint32_t n, const uint32_t *row_ptr,
+                         const uint32_t *col_ind, const uint64_t *iofs, uint32_t *cnt, uint32_t *tci, void *tiles,
+                         uint8_t *big, cudaStream_t s) {
+    constexpr uint32_t NW = ConvMerge<D>::NW;
+    int per_sm = 1;
+    if (pack) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_conv_merge<D, true>, NW * 32, 0));
+    else CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_conv_merge<D, false>, NW * 32, 0));
+    const unsigned g = (unsigned)std::min<uint64_t>(((uint64_t)n_items + NW - 1) / NW,
+                                                    (uint64_t)num_sms() * std::max(per_sm, 1));
+    if (pack)
+        LAUNCH((k_conv_merge<D, true>), g, NW * 32, 0, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
+               (uint32_t *)tiles, big);
+    else
+        LAUNCH((k_conv_merge<D, false>), g, NW * 32, 0, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
+               (uint32_t *)tiles, big);
+}
+
+// warp merge for d = 4, 8 (B2SR_CONV_MERGE=0: lock-step merge only, A/B)
+static bool conv_merge_enabled(uint32_t n, uint32_t d) {
+    const char *e = getenv("B2SR_CONV_MERGE");
+    if (e && e[0] == '0') return false;
+    return (d == 4 && n <= (1u << 30)) || (d == 8 && n <= (1u << 29));
 }
 
 // Optionally, items sorted by their (estimated) CSR entry count, so the GPW items a warp
@@ -197,7 +374,10 @@ b2sr_matrix *csr_to_b2sr_device(uint32_t n, uint32_t d, const uint32_t *row_ptr,
     uint32_t ntr = tile_rows(n, d);
     Buf<uint32_t> pcount(ntr, s);
     Buf<uint64_t> pofs((size_t)ntr + 1, s);
-    LAUNCH(k_conv_chunks, (ntr + 255) / 256, 256, 0, s, n, d, ntr, row_ptr, pcount.p);
+    const bool merge = conv_merge_enabled(n, d);
+    // warp merge: whole tile rows up to CM_CAP entries, longer ones in ranges of ~CM_CAP/2
+    LAUNCH(k_conv_chunks, (ntr + 255) / 256, 256, 0, s, n, d, ntr, row_ptr, pcount.p, merge ? CM_CAP : CONV_CHUNK,
+           merge ? CM_CAP / 2 : CONV_CHUNK);
     exclusive_scan_u32_to_u64(pcount.p, pofs.p, ntr, s);
     uint64_t n_items64 = read_scalar(pofs.p + ntr, s);
     if (n_items64 > 0xFFFFFFFFull) B2SR_THROW(B2SR_EINVAL, "too many conversion work items");
@@ -217,14 +397,27 @@ b2sr_matrix *csr_to_b2sr_device(uint32_t n, uint32_t d, const uint32_t *row_ptr,
     }
     Buf<uint32_t> cnt(n_items, s);
     Buf<uint64_t> iofs((size_t)n_items + 1, s);
-    conv_dispatch(d, false, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, nullptr, nullptr, s, order);
+    Buf<uint8_t> big;
+    if (merge) {
+        big = Buf<uint8_t>(std::max<uint32_t>(n_items, 1), s);
+        CK(cudaMemsetAsync(big.p, 0, n_items, s));
+        if (d == 4) merge_launch<4>(false, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, nullptr, nullptr, big.p, s);
+        else merge_launch<8>(false, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, nullptr, nullptr, big.p, s);
+    }
+    conv_dispatch(d, false, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, nullptr, nullptr, s, order,
+                  merge ? big.p : nullptr);
     exclusive_scan_u32_to_u64(cnt.p, iofs.p, n_items, s);
     uint64_t T = read_scalar(iofs.p + n_items, s);
     if (T > 0xFFFFFFFFull) B2SR_THROW(B2SR_EFORMAT, "tile count exceeds 32-bit index range");
     b2sr_matrix *m = new_matrix(n, d, ntr, T, s);
     try {
         LAUNCH(k_conv_trp, (ntr + 256) / 256, 256, 0, s, ntr, pofs.p, iofs.p, m->trp);
-        if (T) conv_dispatch(d, true, items.p, n_items, n, row_ptr, col_ind, iofs.p, nullptr, m->tci, m->tiles, s, order);
+        if (T && merge) {
+            if (d == 4) merge_launch<4>(true, items.p, n_items, n, row_ptr, col_ind, iofs.p, nullptr, m->tci, m->tiles, big.p, s);
+            else merge_launch<8>(true, items.p, n_items, n, row_ptr, col_ind, iofs.p, nullptr, m->tci, m->tiles, big.p, s);
+        }
+        if (T) conv_dispatch(d, true, items.p, n_items, n, row_ptr, col_ind, iofs.p, nullptr, m->tci, m->tiles, s, order,
+                             merge ? big.p : nullptr);
     } catch (...) {
         free_matrix(m);
         throw;
