@@ -175,6 +175,7 @@ inline size_t padded_vec_bytes(uint32_t ntr, int d) { return ((size_t)ntr * word
 
 b2sr_matrix *new_matrix(uint32_t n, uint32_t dim, uint32_t ntr, uint64_t T, cudaStream_t s);
 void free_matrix(b2sr_matrix *m);
+b2sr_matrix *transpose_device(const b2sr_matrix *m, cudaStream_t s);  // transpose.cu
 void ensure_items(b2sr_matrix *m, cudaStream_t s);  // bin-SpMV work partition
 int num_sms();
 // host -> device copy; pageable sources are staged through page-locked

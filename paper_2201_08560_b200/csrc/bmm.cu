@@ -97,13 +97,15 @@ constexpr uint32_t TC_CHUNK = 2048;
 __global__ void k_tc_item_counts(uint64_t TM, const uint32_t *__restrict__ m_rowid, const uint32_t *__restrict__ m_tci,
                                  uint32_t m_row0, const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ b_trp,
                                  uint32_t chunk, uint32_t *__restrict__ cnt,
-                                 const uint32_t *__restrict__ fparts) {
+                                 const uint8_t *__restrict__ elig, bool sym) {
     for (uint64_t mt = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; mt < TM; mt += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t i = m_rowid[mt], I = i + m_row0, J = m_tci[mt];
         uint32_t la = a_trp[I + 1] - a_trp[I], lb = b_trp[J + 1] - b_trp[J];
         uint32_t sh = min(la, lb);
-        // rows the filter kernel takes get no items here
-        const bool filtered = fparts && fparts[i] != 0;
+        // pairs the filter kernel takes get no items here: staged on row I
+        // (non-SYM), or on the longer of rows I and J (SYM)
+        const uint32_t X = sym && lb > la ? J - m_row0 : i;
+        const bool filtered = elig && elig[X] != 0;
         cnt[mt] = la && lb && !filtered ? (sh + chunk - 1) / chunk : 0;
     }
 }
@@ -188,26 +190,27 @@ __global__ void __launch_bounds__(256) k_bmm_masked_items(uint64_t n_items, cons
 }
 
 // ------------------------------------------------------------ row-filter items
-// Mask rows whose A row and mask row are both short enough (<= TCB_CAP tiles,
-// every row of the degree-oriented DAG at R-MAT s20) and D <= 8: one CTA per
-// work item (mask row I, part p of P) stages A's row I in shared memory --
-// its tile columns, its tiles, and a one-bit-per-column filter indexed by the
-// low TCB_BITS_LG bits of the column -- plus mask row I's tiles, the row
-// starts of the Bt rows J it names and the exclusive prefix of their lengths.
-// The concatenation of those Bt rows is the item's flat probe space; the 8
-// warps stride it 32 entries at a time (no lane idles on a short row J, and
-// the split across items is by equal probe counts, not by whole rows).  Per
-// entry: one coalesced load of the column K, one shared-memory filter test;
-// only on a filter hit (~8 % at s20) a binary search of A's staged columns
-// confirms K and gives its position, and the AND+POPC of the tile pair is
-// done with byte-parallel masks.  Replaces the per-lane binary search of the
-// longer row for every entry of the shorter one (~40 warp instructions per
-// AND+POPC unit).  The sum over common K is order-free integer arithmetic, so
-// the count is the item kernel's bit for bit.
+// Staged rows of at most TCB_CAP tiles (every row of the degree-oriented DAG
+// at R-MAT s20) and D <= 8: one CTA per work item (staged row X, partner
+// chunk, part) stages row X in shared memory -- its tile columns, its tiles,
+// a one-bit-per-column filter indexed by the low TCB_BITS_LG bits of the
+// column and the first position of each of TCB_NB column buckets -- plus, per
+// partner, the mask tile, the start and length of the streamed row and the
+// prefix of its 32-entry chunk counts.  The item's chunks (each inside one
+// streamed row) are strided over the 8 warps; per lane: one coalesced load of
+// a column K (the next chunk's loads issued before this chunk's tests), one
+// shared-memory filter test.  Filter hits go to a per-warp queue and are
+// resolved 32 at a time with every lane busy: the bucket of K gives its
+// position in row X (about one comparison), and the AND+POPC of the tile pair
+// is done with byte-parallel masks.  Replaces the per-lane binary search of
+// the longer row for every entry of the shorter one (~40 warp instructions
+// per AND+POPC unit).  The sum over common K is order-free integer
+// arithmetic, so the count is the item kernel's bit for bit.
 constexpr uint32_t TCB_CAP = 1024;       // longest A row / mask row staged
-constexpr uint32_t TCB_BITS_LG = 16;     // filter: 2^16 bits = 8 KB (false hits <= 1024 / 2^16)
+constexpr uint32_t TCB_BITS_LG = 15;     // filter: 2^15 bits = 4 KB (false hits <= 1024 / 2^15, resolved cheaply)
 constexpr uint32_t TCB_THREADS = 256;
-constexpr uint32_t TCB_BUDGET = 16384;   // probed Bt entries per work item (B2SR_TC_BUDGET overrides)
+constexpr uint32_t TCB_BUDGET = 32000;   // probed Bt entries per work item (B2SR_TC_BUDGET overrides; 16 K: +5 %)
+constexpr uint32_t TCB_NB = 1024;        // column buckets of the staged row (hit lookup)
 constexpr uint32_t TCB_MAXCH = 1024;     // 32-probe chunks per item: budget <= 32 * (TCB_MAXCH - 2)
 
 template <int D>
@@ -226,96 +229,156 @@ __device__ __forceinline__ unsigned long long expand_bits8(uint32_t m) {
     return (e >> 7) * 0xFFull;
 }
 
-// sum over mask bits (r, c) of popc(A[r] & B[c]); units: sum over rows r with
-// A[r] != 0 of popc(M[r]) (the item kernel's AND+POPC unit count)
+// byte r of x non-zero -> bit r
 template <int D>
-__device__ __forceinline__ void tc_tile_pair(TileBits<D> m, TileBits<D> a, TileBits<D> b, unsigned long long &acc,
-                                             unsigned long long &units, bool count_units) {
+__device__ __forceinline__ uint32_t nz_rows(TileBits<D> x) {
+    unsigned long long y = (unsigned long long)x;
+    y = (((y & 0x7F7F7F7F7F7F7F7Full) + 0x7F7F7F7F7F7F7F7Full) | y) & 0x8080808080808080ull;
+    return (uint32_t)(((y >> 7) * 0x0102040810204080ull) >> 56);
+}
+
+// sum over mask bits (r, c) of m of popc(S[r] & T[c]) (S: the staged row's tile,
+// T: the streamed row's tile).  units: the item kernel's AND+POPC unit count,
+// sum over rows r with A[r] != 0 of popc(M[r]) in the ORIGINAL orientation --
+// side 0: m = M, S = A; side 1: m = M^T, T = A.
+template <int D>
+__device__ __forceinline__ void tc_tile_pair(TileBits<D> m, TileBits<D> sa, TileBits<D> tb, uint32_t side,
+                                             unsigned long long &acc, unsigned long long &units, bool count_units) {
+    if (count_units) {
+        const unsigned long long mm = (unsigned long long)m;
+        units += side == 0 ? __popcll(mm & expand_bits8(nz_rows<D>(sa)))
+                           : __popcll(mm & ((unsigned long long)nz_rows<D>(tb) * 0x0101010101010101ull));
+    }
     while (m) {
         const uint32_t r = (uint32_t)(__ffsll((long long)m) - 1) >> 3;
-        const uint32_t mw = (uint32_t)(m >> (8 * r)) & 0xFFu, aw = (uint32_t)(a >> (8 * r)) & 0xFFu;
+        const uint32_t mw = (uint32_t)(m >> (8 * r)) & 0xFFu, aw = (uint32_t)(sa >> (8 * r)) & 0xFFu;
         m &= ~((TileBits<D>)0xFF << (8 * r));
         if (!aw) continue;
-        if (count_units) units += __popc(mw);
         const unsigned long long sel = expand_bits8(mw) & ((unsigned long long)aw * 0x0101010101010101ull);
-        if constexpr (D == 4) acc += __popc((uint32_t)sel & (uint32_t)b);
-        else acc += __popcll(sel & (unsigned long long)b);
+        if constexpr (D == 4) acc += __popc((uint32_t)sel & (uint32_t)tb);
+        else acc += __popcll(sel & (unsigned long long)tb);
     }
 }
 
-// a queued filter hit: confirm K in A's staged row (binary search), then the tile pair
-// (s_*: 32-bit shared addresses of the staged arrays)
+// a queued filter hit: confirm K in the staged row (binary search), then the
+// tile pair (s_*: 32-bit shared addresses of the staged arrays)
 template <int D>
-__device__ __forceinline__ void tc_resolve(uint32_t t, uint32_t j, uint32_t la, uint32_t s_acol, uint32_t s_atile,
-                                           uint32_t s_mtile, const uint32_t *__restrict__ b_tci,
+__device__ __forceinline__ void tc_resolve(uint32_t t, const uint32_t *__restrict__ b_tci, uint32_t j, uint32_t s_acol,
+                                           uint32_t s_start,
+                                           uint32_t ksh, uint32_t s_atile, uint32_t s_mtile, uint32_t s_side,
                                            const typename WordT<D>::T *__restrict__ b_tiles, unsigned long long &acc,
                                            unsigned long long &units, bool count_units) {
     constexpr uint32_t TBY = sizeof(TileBits<D>);
-    const uint32_t K = __ldg(b_tci + t);
-    uint32_t pl = 0, ph = la;
-    while (pl < ph) {
-        const uint32_t mid = (pl + ph) >> 1;
-        if (lds_u32(s_acol + 4 * mid) < K) pl = mid + 1; else ph = mid;
-    }
-    if (pl < la && lds_u32(s_acol + 4 * pl) == K) {
+    const uint32_t K = __ldg(b_tci + t);  // reloaded (L1): the queue keeps 6 bytes per hit
+    // bucket K >> ksh of the staged row: positions [start[b], start[b+1]), ~1 entry
+    const uint32_t b = K >> ksh;
+    const uint32_t ab = lds_u32(s_start + 2 * (b & ~1u));  // start[b], start[b+1] (u16 pairs)
+    uint32_t p = (b & 1u) ? (ab >> 16) : (ab & 0xFFFFu);
+    const uint32_t pe = (b & 1u) ? lds_u16(s_start + 2 * (b + 1)) : (ab >> 16);
+    while (p < pe && lds_u32(s_acol + 4 * p) < K) p++;
+    if (p < pe && lds_u32(s_acol + 4 * p) == K) {
         TileBits<D> m, a;
-        if constexpr (D == 4) { m = lds_u32(s_mtile + 4 * j); a = lds_u32(s_atile + 4 * pl); }
-        else { m = lds_u64(s_mtile + TBY * j); a = lds_u64(s_atile + TBY * pl); }
-        tc_tile_pair<D>(m, a, tile_bits<D>(b_tiles, t), acc, units, count_units);
+        if constexpr (D == 4) { m = lds_u32(s_mtile + 4 * j); a = lds_u32(s_atile + 4 * p); }
+        else { m = lds_u64(s_mtile + TBY * j); a = lds_u64(s_atile + TBY * p); }
+        const uint32_t side = count_units ? (lds_u32(s_side + 4 * (j >> 5)) >> (j & 31u)) & 1u : 0u;
+        tc_tile_pair<D>(m, a, tile_bits<D>(b_tiles, t), side, acc, units, count_units);
     }
 }
 
-template <int D>
-__global__ void __launch_bounds__(TCB_THREADS) k_tc_filter(
+// Work item {X, chunk, part, parts}: staged row X of A; its partners are
+// positions [chunk * CAP, +CAP) of the concatenation (mask row X) ++ (row X
+// of the mask's transpose MT, SYM only), and the item probes part `part` of
+// `parts` of their streamed entries.
+//   non-SYM (any A, Bt, M): partners = mask row X: (J, M_XJ), stream Bt row J.
+//   SYM (triangle counting, A = Bt = M = L, MT = L^T): each pair (I, J) of L
+//     is intersected once, staged on its LONGER row: mask row X keeps J when
+//     len J <= len X (m = M_XJ), L^T row X keeps I when len I < len X (m = the
+//     L^T tile = M_IX^T, and sum_{(r,c) in M} popc(A_I[r] & L_X[c]) =
+//     sum_{(c,r) in M^T} popc(L_X[c] & A_I[r])): sum over pairs of the SHORTER
+//     row (s20 d=4: 2.48 G probes instead of 5.0 G); excluded partners keep
+//     their slot with no probes.
+template <int D, bool SYM>
+__global__ void __launch_bounds__(TCB_THREADS, 6) k_tc_filter(
     uint32_t m_row0, const uint32_t *__restrict__ m_trp, const uint32_t *__restrict__ m_tci,
-    const typename WordT<D>::T *__restrict__ m_tiles, const uint32_t *__restrict__ a_trp,
-    const uint32_t *__restrict__ a_tci, const typename WordT<D>::T *__restrict__ a_tiles,
+    const typename WordT<D>::T *__restrict__ m_tiles, const uint32_t *__restrict__ mt_trp,
+    const uint32_t *__restrict__ mt_tci, const typename WordT<D>::T *__restrict__ mt_tiles,
+    const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ a_tci, const typename WordT<D>::T *__restrict__ a_tiles,
     const uint32_t *__restrict__ b_trp, const uint32_t *__restrict__ b_tci,
-    const typename WordT<D>::T *__restrict__ b_tiles, const uint2 *__restrict__ items, uint32_t n_items,
-    uint32_t *__restrict__ next_item, unsigned long long *__restrict__ out, unsigned long long *__restrict__ work) {
+    const typename WordT<D>::T *__restrict__ b_tiles, const uint4 *__restrict__ items, uint32_t n_items,
+    uint32_t *__restrict__ next_item, unsigned long long *__restrict__ out, unsigned long long *__restrict__ work,
+    uint32_t ksh) {
     using TB = TileBits<D>;
-    constexpr uint32_t FW = 1u << (TCB_BITS_LG - 5), FM = (1u << TCB_BITS_LG) - 1;
+    constexpr uint32_t FLG = TCB_BITS_LG;
+    constexpr uint32_t FW = 1u << (FLG - 5), FM = (1u << FLG) - 1;
     constexpr uint32_t NW = TCB_THREADS / 32, PER = TCB_CAP / TCB_THREADS;
     __shared__ uint32_t filt[FW];
     __shared__ uint32_t acol[TCB_CAP];
+    __shared__ __align__(16) uint16_t bstart[TCB_NB + 2];  // staged row: first position of each column bucket
     __shared__ TB atile[TCB_CAP];
     __shared__ TB mtile[TCB_CAP];
     __shared__ uint32_t jst[TCB_CAP];
+    __shared__ uint32_t jln[TCB_CAP];
     __shared__ uint32_t pre[TCB_CAP + 1];
+    __shared__ uint32_t pside[TCB_CAP / 32];
     __shared__ uint16_t jfirst[TCB_MAXCH];
     __shared__ uint32_t ring_t[NW][64];
     __shared__ uint16_t ring_j[NW][64];
     __shared__ uint32_t wtot[NW];
-    __shared__ uint32_t s_item;
+    __shared__ uint4 s_item;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5, lt_mask = (1u << lane) - 1u;
     for (uint32_t q = tid; q < FW; q += TCB_THREADS) filt[q] = 0;
     unsigned long long acc = 0, units = 0;
+    const uint32_t s_rt = smem_addr(&ring_t[wid][0]), s_rj = smem_addr(&ring_j[wid][0]);
+    const uint32_t s_pre = smem_addr(pre), s_jst = smem_addr(jst), s_jf = smem_addr(jfirst), s_jln = smem_addr(jln);
+    const uint32_t s_filt = smem_addr(filt), s_acol = smem_addr(acol), s_atile = smem_addr(atile);
+    const uint32_t s_mtile = smem_addr(mtile), s_side = smem_addr(pside), s_start = smem_addr(bstart);
     for (;;) {
-        if (tid == 0) s_item = atomicAdd(next_item, 1u);
+        if (tid == 0) {
+            const uint32_t w = atomicAdd(next_item, 1u);
+            s_item = w < n_items ? items[w] : make_uint4(0xFFFFFFFFu, 0, 0, 0);
+        }
         __syncthreads();  // also orders the previous item's filter clear before this item's staging
-        const uint32_t w = s_item;
-        if (w >= n_items) break;
-        const uint2 it = __ldg(items + w);
-        const uint32_t i = it.x, part = it.y & 0xFFFFu, parts = it.y >> 16;
-        const uint32_t m0 = __ldg(m_trp + i), nm = __ldg(m_trp + i + 1) - m0;
+        const uint4 it = s_item;
+        if (it.x == 0xFFFFFFFFu) break;
+        const uint32_t i = it.x, chunk = it.y, part = it.z, parts = it.w;
         const uint32_t I = m_row0 + i, a0 = __ldg(a_trp + I), la = __ldg(a_trp + I + 1) - a0;
+        const uint32_t m0 = __ldg(m_trp + i), nL = __ldg(m_trp + i + 1) - m0;
+        uint32_t t0 = 0, nT = 0;
+        if constexpr (SYM) {
+            t0 = __ldg(mt_trp + I);
+            nT = __ldg(mt_trp + I + 1) - t0;
+        }
+        const uint32_t g0 = chunk * TCB_CAP, nm = min(TCB_CAP, nL + nT - g0);
         for (uint32_t q = tid; q < la; q += TCB_THREADS) {
             const uint32_t K = __ldg(a_tci + a0 + q);
             acol[q] = K;
             atile[q] = tile_bits<D>(a_tiles, (size_t)a0 + q);
             atomicOr(filt + ((K & FM) >> 5), 1u << (K & 31u));
         }
-        // mask row: Bt row starts, mask tiles, block-exclusive prefix of the Bt row lengths
+        // partners: streamed-row starts and lengths, mask tiles, block-exclusive
+        // prefix of their 32-entry chunk counts
         uint32_t len[PER], run = 0;
 #pragma unroll
         for (uint32_t k = 0; k < PER; k++) {
             const uint32_t q = tid * PER + k;
             len[k] = 0;
             if (q < nm) {
-                const uint32_t J = __ldg(m_tci + m0 + q), b0 = __ldg(b_trp + J);
-                len[k] = __ldg(b_trp + J + 1) - b0;
+                const uint32_t g = g0 + q;
+                uint32_t J;
+                bool second = false;  // partner from MT
+                if (!SYM || g < nL) {
+                    J = __ldg(m_tci + m0 + g);
+                    mtile[q] = tile_bits<D>(m_tiles, (size_t)m0 + g);
+                } else {
+                    second = true;
+                    J = __ldg(mt_tci + t0 + (g - nL));
+                    mtile[q] = tile_bits<D>(mt_tiles, (size_t)t0 + (g - nL));
+                }
+                const uint32_t b0 = __ldg(b_trp + J), lb = __ldg(b_trp + J + 1) - b0;
+                const uint32_t kept = (SYM && (second ? lb >= la : lb > la)) ? 0u : lb;  // else staged on row J
                 jst[q] = b0;
-                mtile[q] = tile_bits<D>(m_tiles, (size_t)m0 + q);
+                jln[q] = kept;
+                len[k] = (kept + 31) >> 5;  // 32-entry chunks
             }
             run += len[k];
         }
@@ -326,6 +389,15 @@ __global__ void __launch_bounds__(TCB_THREADS) k_tc_filter(
             if (lane >= (uint32_t)o) incl += y;
         }
         if (lane == 31) wtot[wid] = incl;
+        if (tid < TCB_CAP / 32) {  // side bit q: partner q comes from MT
+            uint32_t sw = 0;
+            if (SYM) {
+                const uint32_t qb = tid * 32, first2 = nL > g0 ? nL - g0 : 0u;  // first MT partner slot
+                if (first2 <= qb) sw = 0xFFFFFFFFu;
+                else if (first2 < qb + 32) sw = 0xFFFFFFFFu << (first2 - qb);
+            }
+            pside[tid] = sw;
+        }
         __syncthreads();
         uint32_t off = incl - run;
         for (uint32_t v = 0; v < wid; v++) off += wtot[v];
@@ -336,77 +408,74 @@ __global__ void __launch_bounds__(TCB_THREADS) k_tc_filter(
             off += len[k];
         }
         if (tid == TCB_THREADS - 1 && nm == TCB_CAP) pre[TCB_CAP] = off;
+        // bucket starts of the staged row (acol is in place since the barrier above):
+        // entry q fills the buckets after its predecessor's up to its own
+        for (uint32_t q = tid; q <= la; q += TCB_THREADS) {
+            const uint32_t bq = q < la ? acol[q] >> ksh : TCB_NB + 1;
+            const uint32_t bp = q ? (acol[q - 1] >> ksh) + 1 : 0u;
+            for (uint32_t bb = bp; bb <= bq && bb <= TCB_NB + 1; bb++) bstart[bb] = (uint16_t)q;
+        }
         __syncthreads();
-        const uint32_t total = pre[nm];
+        const uint32_t total = pre[nm];  // chunks
         const uint32_t lo = (uint32_t)((unsigned long long)total * part / parts);
         const uint32_t hi = (uint32_t)((unsigned long long)total * (part + 1) / parts);
-        // chunk (32 probes) -> the row j holding its first entry
+        // chunk -> its partner (each warp chunk lies inside one partner row: R-MAT
+        // s20 pairs waste 10 % of the lanes on row tails, against a per-lane
+        // partner search for chunks that cross rows)
         for (uint32_t j = tid; j < nm; j += TCB_THREADS) {
-            const uint32_t s0 = max(pre[j], lo), s1 = min(pre[j + 1], hi);
-            if (s0 < s1)
-                for (uint32_t c = (s0 - lo + 31) >> 5, ce = (s1 - lo + 31) >> 5; c < ce; c++) jfirst[c] = (uint16_t)j;
+            const uint32_t c0 = max(pre[j], lo), c1 = min(pre[j + 1], hi);
+            for (uint32_t c = c0; c < c1; c++) jfirst[c - lo] = (uint16_t)j;
         }
         __syncthreads();
         // filter hits are queued per warp (ring of 64) and resolved 32 at a
-        // time with every lane busy: ~1 lane in 12 hits, so resolving them
-        // in place would run the search of A's row on nearly every chunk
+        // time with every lane busy: ~1 lane in 5 hits, so resolving them
+        // in place would run the lookup on nearly every chunk
         uint32_t qh = 0, qtl = 0;
-        const uint32_t s_rt = smem_addr(&ring_t[wid][0]), s_rj = smem_addr(&ring_j[wid][0]);
-        const uint32_t s_pre = smem_addr(pre), s_jst = smem_addr(jst), s_jf = smem_addr(jfirst);
-        const uint32_t s_filt = smem_addr(filt), s_acol = smem_addr(acol), s_atile = smem_addr(atile);
-        const uint32_t s_mtile = smem_addr(mtile);
-        for (uint32_t base = lo + wid * 32; base < hi; base += TCB_THREADS) {
-            const bool valid = base + lane < hi;
-            const uint32_t e = valid ? base + lane : hi - 1;
-            // j = largest row with pre[j] <= e: the chunk's first row plus the
-            // number of the next 32 row starts <= e
-            const uint32_t j0 = lds_u16(s_jf + 2 * ((base - lo) >> 5));
-            const uint32_t q = j0 + 1 + lane;
-            const uint32_t v = q <= nm ? lds_u32(s_pre + 4 * q) : 0xFFFFFFFFu;
-            uint32_t j = j0;
-            if (__shfl_sync(0xffffffffu, v, 0) <= min(base + 31, hi - 1)) {  // the chunk crosses a row start
-                uint32_t c = 0;
-#pragma unroll
-                for (uint32_t st = 16; st; st >>= 1)
-                    if (__shfl_sync(0xffffffffu, v, c + st - 1) <= e) c += st;
-                j = j0 + c;
-                if (c == 31 && __shfl_sync(0xffffffffu, v, 31) <= e) {  // > 31 (empty) rows crossed
-                    uint32_t jl = j0 + 32, jh = nm;  // pre[jl] <= e < pre[jh]
-                    while (jh - jl > 1) {
-                        const uint32_t mid = (jl + jh) >> 1;
-                        if (lds_u32(s_pre + 4 * mid) <= e) jl = mid; else jh = mid;
-                    }
-                    j = jl;
-                }
+        auto locate = [&](uint32_t c, uint32_t &t, uint32_t &j) -> bool {
+            j = lds_u16(s_jf + 2 * (c - lo));
+            const uint32_t off = (c - lds_u32(s_pre + 4 * j)) * 32 + lane;
+            t = lds_u32(s_jst + 4 * j) + off;
+            return off < lds_u32(s_jln + 4 * j);
+        };
+        // two-deep pipeline: the column loads of the next chunk are issued
+        // before the filter test of this one
+        uint32_t c = lo + wid;
+        uint32_t t_c = 0, j_c = 0, K_c = 0;
+        bool v_c = false;
+        if (c < hi) {
+            v_c = locate(c, t_c, j_c);
+            K_c = v_c ? __ldg(b_tci + t_c) : 0u;
+        }
+        for (; c < hi; c += NW) {
+            uint32_t t_n = 0, j_n = 0, K_n = 0;
+            bool v_n = false;
+            if (c + NW < hi) {
+                v_n = locate(c + NW, t_n, j_n);
+                K_n = v_n ? __ldg(b_tci + t_n) : 0u;
             }
-            bool hit = false;
-            uint32_t t = 0;
-            if (valid) {
-                t = lds_u32(s_jst + 4 * j) + (e - lds_u32(s_pre + 4 * j));
-                const uint32_t K = __ldg(b_tci + t);
-                hit = (lds_u32(s_filt + 4 * ((K & FM) >> 5)) >> (K & 31u)) & 1u;
-            }
+            const bool hit = v_c && ((lds_u32(s_filt + 4 * ((K_c & FM) >> 5)) >> (K_c & 31u)) & 1u);
             const uint32_t hm = __ballot_sync(0xffffffffu, hit);
             if (hit) {
                 const uint32_t pos = (qtl + __popc(hm & lt_mask)) & 63u;
-                sts_u32(s_rt + 4 * pos, t);
-                sts_u16(s_rj + 2 * pos, j);
+                sts_u32(s_rt + 4 * pos, t_c);
+                sts_u16(s_rj + 2 * pos, j_c);
             }
             qtl += __popc(hm);
             if (qtl - qh >= 32) {
                 __syncwarp();
                 const uint32_t pos = (qh + lane) & 63u;
-                tc_resolve<D>(lds_u32(s_rt + 4 * pos), lds_u16(s_rj + 2 * pos), la, s_acol, s_atile, s_mtile, b_tci,
-                              b_tiles, acc, units, work != nullptr);
+                tc_resolve<D>(lds_u32(s_rt + 4 * pos), b_tci, lds_u16(s_rj + 2 * pos), s_acol,
+                              s_start, ksh, s_atile, s_mtile, s_side, b_tiles, acc, units, work != nullptr);
                 qh += 32;
                 __syncwarp();
             }
+            t_c = t_n; j_c = j_n; K_c = K_n; v_c = v_n;
         }
         __syncwarp();
         if (lane < qtl - qh) {
             const uint32_t pos = (qh + lane) & 63u;
-            tc_resolve<D>(lds_u32(s_rt + 4 * pos), lds_u16(s_rj + 2 * pos), la, s_acol, s_atile, s_mtile, b_tci,
-                          b_tiles, acc, units, work != nullptr);
+            tc_resolve<D>(lds_u32(s_rt + 4 * pos), b_tci, lds_u16(s_rj + 2 * pos), s_acol,
+                          s_start, ksh, s_atile, s_mtile, s_side, b_tiles, acc, units, work != nullptr);
         }
         __syncthreads();
         for (uint32_t q = tid; q < la; q += TCB_THREADS) filt[(acol[q] & FM) >> 5] = 0;
@@ -419,35 +488,59 @@ __global__ void __launch_bounds__(TCB_THREADS) k_tc_filter(
     }
 }
 
-// parts of each eligible mask row (0: the row takes the binary-search items or is empty)
-__global__ void k_tcb_parts(uint32_t mntr, uint32_t m_row0, const uint32_t *__restrict__ m_trp,
-                            const uint32_t *__restrict__ m_tci, const uint32_t *__restrict__ a_trp,
-                            const uint32_t *__restrict__ b_trp, uint32_t budget, uint32_t *__restrict__ parts) {
-    const uint32_t lane = lane_id(), warps = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < mntr; i += warps) {
-        const uint32_t m0 = m_trp[i], m1 = m_trp[i + 1], I = m_row0 + i;
-        const uint32_t la = a_trp[I + 1] - a_trp[I];
-        uint32_t p = 0;
-        if (m1 > m0 && la && la <= TCB_CAP && m1 - m0 <= TCB_CAP) {
-            unsigned long long w = 0;
-            for (uint32_t t = m0 + lane; t < m1; t += 32) {
-                const uint32_t J = m_tci[t];
-                w += b_trp[J + 1] - b_trp[J];
-            }
-            for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
-            const unsigned long long q = (w + budget - 1) / budget;
-            p = (q == 0 || w >= 0x80000000ull) ? 0u : (q > 0xFFFFull ? 0xFFFFu : (uint32_t)q);
-        }
-        if (lane == 0) parts[i] = p;
+// Items of the filter kernel.  Per staged row X (X = mask row i, I = row0 + i):
+// eligible iff 0 < len_A(X) <= CAP (D <= 8); non-SYM also needs the mask row
+// <= CAP partners.  k_tcf_chunks: partner chunks of CAP per eligible row;
+// k_tcf_parts: per chunk, the probes it streams cut into parts of <= budget.
+__global__ void k_tcf_chunks(uint32_t mntr, uint32_t m_row0, const uint32_t *__restrict__ m_trp,
+                             const uint32_t *__restrict__ mt_trp, const uint32_t *__restrict__ a_trp,
+                             uint32_t *__restrict__ nch, uint8_t *__restrict__ elig) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mntr; i += gridDim.x * blockDim.x) {
+        const uint32_t I = m_row0 + i, la = a_trp[I + 1] - a_trp[I];
+        const uint32_t np = (m_trp[i + 1] - m_trp[i]) + (mt_trp ? mt_trp[I + 1] - mt_trp[I] : 0u);
+        const bool ok = la > 0 && la <= TCB_CAP && (mt_trp || np <= TCB_CAP);
+        elig[i] = ok;
+        nch[i] = ok ? (np + TCB_CAP - 1) / TCB_CAP : 0u;
     }
 }
 
-__global__ void k_tcb_fill(uint32_t mntr, const uint32_t *__restrict__ parts, const uint64_t *__restrict__ ofs,
-                           uint2 *__restrict__ items) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mntr; i += gridDim.x * blockDim.x) {
-        const uint32_t P = parts[i];
-        const uint64_t o = ofs[i];
-        for (uint32_t q = 0; q < P; q++) items[o + q] = make_uint2(i, (P << 16) | q);
+__global__ void k_tcf_chunk_list(uint32_t mntr, const uint32_t *__restrict__ nch, const uint64_t *__restrict__ ofs,
+                                 uint2 *__restrict__ chunks) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mntr; i += gridDim.x * blockDim.x)
+        for (uint32_t c = 0; c < nch[i]; c++) chunks[ofs[i] + c] = make_uint2(i, c);
+}
+
+// warp per chunk: probes = sum of the streamed lengths of its kept partners
+__global__ void k_tcf_parts(uint32_t nchunks, const uint2 *__restrict__ chunks, uint32_t m_row0,
+                            const uint32_t *__restrict__ m_trp, const uint32_t *__restrict__ m_tci,
+                            const uint32_t *__restrict__ mt_trp, const uint32_t *__restrict__ mt_tci,
+                            const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ b_trp, uint32_t budget,
+                            uint32_t *__restrict__ parts) {
+    const uint32_t lane = lane_id(), warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nchunks; c += warps) {
+        const uint2 ch = chunks[c];
+        const uint32_t i = ch.x, I = m_row0 + i, la = a_trp[I + 1] - a_trp[I];
+        const uint32_t m0 = m_trp[i], nL = m_trp[i + 1] - m0;
+        const uint32_t t0 = mt_trp ? mt_trp[I] : 0u, nT = mt_trp ? mt_trp[I + 1] - t0 : 0u;
+        const uint32_t g0 = ch.y * TCB_CAP, g1 = min(g0 + TCB_CAP, nL + nT);
+        unsigned long long w = 0;
+        for (uint32_t g = g0 + lane; g < g1; g += 32) {
+            const bool second = g >= nL;
+            const uint32_t J = second ? mt_tci[t0 + (g - nL)] : m_tci[m0 + g];
+            const uint32_t lb = b_trp[J + 1] - b_trp[J];
+            if (!mt_trp || (second ? lb < la : lb <= la)) w += (lb + 31) / 32;  // 32-entry chunks
+        }
+        for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        const unsigned long long q = (w + budget - 1) / budget;  // budget: chunks per item
+        if (lane == 0) parts[c] = (q == 0 || w >= 0x80000000ull) ? 0u : (q > 0xFFFFull ? 0xFFFFu : (uint32_t)q);
+    }
+}
+
+__global__ void k_tcf_fill(uint32_t nchunks, const uint2 *__restrict__ chunks, const uint32_t *__restrict__ parts,
+                           const uint64_t *__restrict__ ofs, uint4 *__restrict__ items) {
+    for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < nchunks; c += gridDim.x * blockDim.x) {
+        const uint32_t P = parts[c];
+        for (uint32_t q = 0; q < P; q++) items[ofs[c] + q] = make_uint4(chunks[c].x, chunks[c].y, q, P);
     }
 }
 
@@ -457,8 +550,9 @@ static bool tc_filter_enabled(int dim) {
     return dim <= 8 && !(e && e[0] == '0');
 }
 
+// mt: the mask's transpose (SYM triangle counting: a = bt = mask = L, mt = L^T), else null
 int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_matrix *mask, cudaStream_t s,
-                      uint64_t *work_out = nullptr) {
+                      uint64_t *work_out = nullptr, const b2sr_matrix *mt = nullptr) {
     if (work_out) *work_out = 0;
     if (!mask->num_tiles || !a->num_tiles || !bt->num_tiles) return 0;
     uint64_t TM = mask->num_tiles;
@@ -468,26 +562,38 @@ int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_ma
     const char *ce = getenv("B2SR_TC_CHUNK");  // entries of the shorter row per work item (A/B)
     const uint32_t chunk = ce ? std::max(32, atoi(ce)) : TC_CHUNK;
     const bool filtered = tc_filter_enabled(a->dim);
-    Buf<uint2> fitems;
-    Buf<uint32_t> pc;
+    const bool sym = filtered && mt != nullptr;
+    Buf<uint4> fitems;
+    Buf<uint8_t> elig;
     uint32_t n_fitems = 0;
     if (filtered) {
-        // work items of the filter kernel: each eligible mask row cut into
-        // parts of <= budget probed Bt entries, handed out dynamically
+        // work items of the filter kernel, handed out dynamically
         const char *be = getenv("B2SR_TC_BUDGET");
-        const uint32_t budget = be ? (uint32_t)std::min(32 * (int)(TCB_MAXCH - 2), std::max(256, atoi(be))) : TCB_BUDGET;
+        const uint32_t budget =  // in 32-entry chunks (the jfirst table holds TCB_MAXCH)
+            (be ? (uint32_t)std::min(32 * (int)(TCB_MAXCH - 2), std::max(256, atoi(be))) : TCB_BUDGET) / 32;
         const uint32_t mntr = mask->ntr;
-        pc = Buf<uint32_t>(std::max<uint32_t>(mntr, 1), s);
-        Buf<uint64_t> pofs((size_t)mntr + 1, s);
-        LAUNCH(k_tcb_parts, grid_for((uint64_t)mntr * 32), 256, 0, s, mntr, mask->row0, mask->trp, mask->tci, a->trp,
-               bt->trp, budget, pc.p);
-        exclusive_scan_u32_to_u64(pc.p, pofs.p, mntr, s);
-        n_fitems = (uint32_t)read_scalar(pofs.p + mntr, s);
-        fitems = Buf<uint2>(std::max<uint32_t>(n_fitems, 1), s);
-        if (n_fitems) LAUNCH(k_tcb_fill, grid_for(mntr), 256, 0, s, mntr, pc.p, pofs.p, fitems.p);
+        elig = Buf<uint8_t>(std::max<uint32_t>(mntr, 1), s);
+        Buf<uint32_t> nch(std::max<uint32_t>(mntr, 1), s);
+        Buf<uint64_t> cofs((size_t)mntr + 1, s);
+        LAUNCH(k_tcf_chunks, grid_for(mntr), 256, 0, s, mntr, mask->row0, mask->trp, sym ? mt->trp : nullptr, a->trp,
+               nch.p, elig.p);
+        exclusive_scan_u32_to_u64(nch.p, cofs.p, mntr, s);
+        const uint32_t nchunks = (uint32_t)read_scalar(cofs.p + mntr, s);
+        if (nchunks) {
+            Buf<uint2> chunks(nchunks, s);
+            Buf<uint32_t> pc(nchunks, s);
+            Buf<uint64_t> pofs((size_t)nchunks + 1, s);
+            LAUNCH(k_tcf_chunk_list, grid_for(mntr), 256, 0, s, mntr, nch.p, cofs.p, chunks.p);
+            LAUNCH(k_tcf_parts, grid_for((uint64_t)nchunks * 32), 256, 0, s, nchunks, chunks.p, mask->row0, mask->trp,
+                   mask->tci, sym ? mt->trp : nullptr, sym ? mt->tci : nullptr, a->trp, bt->trp, budget, pc.p);
+            exclusive_scan_u32_to_u64(pc.p, pofs.p, nchunks, s);
+            n_fitems = (uint32_t)read_scalar(pofs.p + nchunks, s);
+            fitems = Buf<uint4>(std::max<uint32_t>(n_fitems, 1), s);
+            if (n_fitems) LAUNCH(k_tcf_fill, grid_for(nchunks), 256, 0, s, nchunks, chunks.p, pc.p, pofs.p, fitems.p);
+        }
     }
     LAUNCH(k_tc_item_counts, grid_for(TM), 256, 0, s, TM, rowid.p, mask->tci, mask->row0, a->trp, bt->trp, chunk, cnt.p,
-           filtered ? pc.p : nullptr);
+           filtered ? elig.p : nullptr, sym);
     exclusive_scan_u32_to_u64(cnt.p, ofs.p, TM, s);
     uint64_t n_items = read_scalar(ofs.p + TM, s);
     Buf<unsigned long long> out(1, s);
@@ -503,18 +609,24 @@ int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_ma
     kernel_timer().begin(s);
     if (n_fitems) {
         int per_sm = 1;
-        switch (a->dim) {
-#define TCB_CASE(DD, W)                                                                                           \
-    case DD:                                                                                                      \
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_filter<DD>, TCB_THREADS, 0));               \
-        LAUNCH(k_tc_filter<DD>,                                                                                   \
-               (unsigned)std::min<uint64_t>((uint64_t)num_sms() * std::max(per_sm, 1), n_fitems), TCB_THREADS, 0, \
-               s, mask->row0, mask->trp, mask->tci, (const W *)mask->tiles, a->trp, a->tci, (const W *)a->tiles,  \
-               bt->trp, bt->tci, (const W *)bt->tiles, fitems.p, n_fitems, next_row.p, out.p,                     \
-               work_out ? work.p : nullptr);                                                                       \
+        const uint32_t *mtp = sym ? mt->trp : nullptr, *mtc = sym ? mt->tci : nullptr;
+        const void *mtt = sym ? mt->tiles : nullptr;
+        uint32_t ksh = 0;  // column bucket shift: (ntr - 1) >> ksh < TCB_NB
+        while (((uint64_t)(a->ntr ? a->ntr - 1 : 0) >> ksh) >= TCB_NB) ksh++;
+        switch (a->dim * 2 + (sym ? 1 : 0)) {
+#define TCB_CASE(DD, SY, W)                                                                                          \
+    case DD * 2 + SY:                                                                                                \
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_filter<DD, SY>, TCB_THREADS, 0));             \
+        LAUNCH((k_tc_filter<DD, SY>),                                                                                \
+               (unsigned)std::min<uint64_t>((uint64_t)num_sms() * std::max(per_sm, 1), n_fitems), TCB_THREADS, 0,    \
+               s, mask->row0, mask->trp, mask->tci, (const W *)mask->tiles, mtp, mtc, (const W *)mtt, a->trp, a->tci, \
+               (const W *)a->tiles, bt->trp, bt->tci, (const W *)bt->tiles, fitems.p, n_fitems, next_row.p, out.p,  \
+               work_out ? work.p : nullptr, ksh);                                                                     \
         break;
-            TCB_CASE(4, uint8_t)
-            TCB_CASE(8, uint8_t)
+            TCB_CASE(4, 0, uint8_t)
+            TCB_CASE(4, 1, uint8_t)
+            TCB_CASE(8, 0, uint8_t)
+            TCB_CASE(8, 1, uint8_t)
 #undef TCB_CASE
         }
     }
@@ -534,6 +646,25 @@ int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_ma
     kernel_timer().end(s);
     if (work_out) *work_out = read_scalar(work.p, s);
     return (int64_t)read_scalar(out.p, s);
+}
+
+// triangle counting: bmm_masked(L, transpose(L), L) -- B = transpose(L) enters
+// transposed, i.e. L.  With the filter kernel, pairs are staged on their longer
+// row, which needs L^T (one transpose of L; B2SR_TC_SYM=0 keeps row I staged).
+static int64_t tc_count(const b2sr_matrix *lower, cudaStream_t s, uint64_t *work) {
+    const char *e = getenv("B2SR_TC_SYM");
+    if (tc_filter_enabled(lower->dim) && !(e && e[0] == '0') && lower->num_tiles) {
+        b2sr_matrix *lt = transpose_device(lower, s);
+        try {
+            const int64_t c = bmm_masked_bt(lower, lower, lower, s, work, lt);
+            free_matrix(lt);
+            return c;
+        } catch (...) {
+            free_matrix(lt);
+            throw;
+        }
+    }
+    return bmm_masked_bt(lower, lower, lower, s, work);
 }
 
 }  // namespace b2sr
@@ -579,13 +710,13 @@ int b2sr_bmm_sum_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2
 int b2sr_tc(const b2sr_matrix *lower, int64_t *count, void *stream) {
     API_BEGIN
     // bmm_masked(L, transpose(L), L): B = transpose(L) enters transposed, i.e. L.
-    *count = bmm_masked_bt(lower, lower, lower, (cudaStream_t)stream);
+    *count = tc_count(lower, (cudaStream_t)stream, nullptr);
     API_END
 }
 
 int b2sr_tc_work(const b2sr_matrix *lower, int64_t *count, uint64_t *work, void *stream) {
     API_BEGIN
-    *count = bmm_masked_bt(lower, lower, lower, (cudaStream_t)stream, work);
+    *count = tc_count(lower, (cudaStream_t)stream, work);
     API_END
 }
 

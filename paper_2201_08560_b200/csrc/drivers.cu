@@ -650,8 +650,11 @@ __device__ __forceinline__ void pr_add(double (&acc)[D], uint32_t r, double v) {
     for (int q = 0; q < D; q++) acc[q] = __dadd_rn(acc[q], q == (int)r ? v : 0.0);
 }
 
-template <int D>
-__global__ void __launch_bounds__(256) k_pr_gather32(const WorkItem *__restrict__ items, uint32_t n_items, uint32_t n,
+// U: tiles per lane in flight per step; MINB: CTAs per SM (the gather is
+// latency-bound on the x loads: ncu at U = 8, 4 CTAs/SM, 64 registers: 41 %
+// warps active, long-scoreboard stalls)
+template <int D, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_pr_gather32(const WorkItem *__restrict__ items, uint32_t n_items, uint32_t n,
                                                      const uint32_t *__restrict__ tci, const uint8_t *__restrict__ tiles,
                                                      const float *__restrict__ x, double *__restrict__ y,
                                                      double *__restrict__ part) {
@@ -666,7 +669,6 @@ __global__ void __launch_bounds__(256) k_pr_gather32(const WorkItem *__restrict_
         // U tiles per lane per step: tile loads, then every tile's FIRST set bit
         // gathered unconditionally (R-MAT: ~1 bit per tile), all in flight
         // together; further bits of a tile are the rare tail
-        constexpr int U = 8;
         for (uint32_t t = it.t0 + lane; t < it.t1; t += 32 * U) {
             uint32_t k[U];
             TW wd[U];
@@ -1763,12 +1765,20 @@ int b2sr_pagerank(const b2sr_matrix *a, const double *d_out_degree, double alpha
             const unsigned gi = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)a->n_items + 7) / 8,
                                                                                     (uint64_t)num_sms() * 16));
             kernel_timer().begin(s);
-            if (d == 4)
-                LAUNCH(k_pr_gather32<4>, gi, 256, 0, s, a->items, a->n_items, n, gtci, (const uint8_t *)a->tiles, x32.p,
-                       g.p, part.p);
-            else
-                LAUNCH(k_pr_gather32<8>, gi, 256, 0, s, a->items, a->n_items, n, gtci, (const uint8_t *)a->tiles, x32.p,
-                       g.p, part.p);
+            // B2SR_PRG: gather geometry (A/B) -- 0: U=8 x 4 CTAs/SM, 1: U=4 x 6, 2: U=6 x 5, 3: U=16 x 2
+            static const int prg = [] { const char *e = getenv("B2SR_PRG"); return e ? atoi(e) : 0; }();
+#define PRG_LAUNCH(DD, UU, MB)                                                                                    \
+    LAUNCH((k_pr_gather32<DD, UU, MB>), gi, 256, 0, s, a->items, a->n_items, n, gtci, (const uint8_t *)a->tiles, \
+           x32.p, g.p, part.p)
+            if (d == 4) {
+                if (prg == 1) PRG_LAUNCH(4, 4, 6);
+                else if (prg == 2) PRG_LAUNCH(4, 6, 5);
+                else if (prg == 3) PRG_LAUNCH(4, 16, 2);
+                else PRG_LAUNCH(4, 8, 4);
+            } else {
+                PRG_LAUNCH(8, 8, 4);
+            }
+#undef PRG_LAUNCH
             kernel_timer().end(s);
             if (a->any_split) {
                 if (d == 4) LAUNCH(k_pr_fold_parts<4>, grid_for((uint64_t)a->ntr * 4), 256, 0, s, a->ntr, n, a->item_ofs, part.p, g.p);

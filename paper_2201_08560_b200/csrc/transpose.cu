@@ -139,6 +139,329 @@ __global__ void k_unpack4(uint64_t T, const uint64_t *__restrict__ keys, int cb,
     }
 }
 
+// ------------------------------------------------------------ two-level transpose (d = 4, 8)
+// A stable counting sort of the tiles by column in two levels, the column cut
+// into a high digit (HB bits: <= 2048 buckets) and a low digit (LB bits: <=
+// 2048 columns per bucket):
+//   A  each of G CTAs histograms the high digit over its contiguous tile range;
+//      one scan gives every (bucket, CTA) its output start;
+//   B  the same CTAs walk their ranges in sub-tiles of TR_SUB tiles in order:
+//      tile rows are recovered from tile_row_ptr in shared memory (row starts
+//      counted per sub-tile position, one block scan), elements (column | row
+//      | tile) are ranked stably by high digit (__match_any_sync, per-warp
+//      counters), staged by digit and written to their bucket with coalesced
+//      runs -- the bucket then holds its elements in input (row-major) order;
+//   C  one CTA per bucket: per-warp low-digit counts over its segment, one
+//      scan over the bucket's columns (which is also tile_row_ptr of the
+//      transpose), then each warp places its segment stably (match_any again)
+//      and stores the row as the new tile column and the bit-transposed tile.
+// HBM traffic: tci read twice, tiles once, 8 (d=4) / 16 (d=8) bytes per tile
+// written and read twice -- against the three 8-bit LSD passes (each a
+// histogram read plus a read and a write of 8-byte keys) plus pack and unpack
+// passes and a column histogram of global atomics.
+void hot_smem_attr_raw(const void *kernel, size_t bytes);  // hot.cu: opt-in dynamic shared memory
+
+constexpr int TR_THREADS = 256, TR_WARPS = TR_THREADS / 32;
+constexpr int TR_SUB = 2048, TR_PER = TR_SUB / TR_THREADS;  // tiles per sub-tile / per thread
+constexpr int TR_MAXB = 2048;                                 // digit range
+
+template <int D> struct TrElem;
+template <> struct TrElem<4> {  // col | row << cb | 16-bit nibble tile << 2cb
+    static constexpr bool PAY = false;
+};
+template <> struct TrElem<8> {  // key col | row << cb, payload: the 8-byte tile
+    static constexpr bool PAY = true;
+};
+
+__device__ __forceinline__ uint32_t nib16(uint32_t w) {
+    return (w & 0xFu) | ((w >> 4) & 0xF0u) | ((w >> 8) & 0xF00u) | ((w >> 12) & 0xF000u);
+}
+
+__global__ void __launch_bounds__(TR_THREADS) k_tr_hist(uint64_t T, uint32_t G, const uint32_t *__restrict__ tci,
+                                                        int lb, uint32_t nb, uint32_t *__restrict__ hcnt) {
+    __shared__ uint32_t h[TR_MAXB];
+    for (uint32_t b = threadIdx.x; b < nb; b += TR_THREADS) h[b] = 0;
+    __syncthreads();
+    const uint64_t t0 = T * blockIdx.x / G, t1 = T * (blockIdx.x + 1) / G;
+    for (uint64_t t = t0 + threadIdx.x; t < t1; t += TR_THREADS) atomicAdd(&h[__ldg(tci + t) >> lb], 1u);
+    __syncthreads();
+    for (uint32_t b = threadIdx.x; b < nb; b += TR_THREADS) hcnt[(size_t)b * G + blockIdx.x] = h[b];
+}
+
+// largest r in [0, ntr) with trp[r] <= t
+__device__ __forceinline__ uint32_t tr_row_of(const uint32_t *__restrict__ trp, uint32_t ntr, uint64_t t) {
+    uint32_t lo = 0, hi = ntr - 1;
+    while (lo < hi) {
+        const uint32_t mid = lo + (hi - lo + 1) / 2;
+        if (trp[mid] <= t) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <int D>
+__global__ void __launch_bounds__(TR_THREADS) k_tr_scatter(uint64_t T, uint32_t G, uint32_t ntr,
+                                                           const uint32_t *__restrict__ trp,
+                                                           const uint32_t *__restrict__ tci,
+                                                           const void *__restrict__ tiles, int cb, int lb, uint32_t nb,
+                                                           const uint64_t *__restrict__ hofs,
+                                                           unsigned long long *__restrict__ ekey,
+                                                           unsigned long long *__restrict__ epay) {
+    extern __shared__ __align__(16) unsigned char tr_smem[];
+    unsigned long long *skey = reinterpret_cast<unsigned long long *>(tr_smem);      // TR_SUB
+    unsigned long long *spay = skey + TR_SUB;                                         // TR_SUB (d = 8)
+    unsigned long long *pos = spay + (TrElem<D>::PAY ? TR_SUB : 0);                  // nb: next output slot
+    uint32_t *rowc = reinterpret_cast<uint32_t *>(pos + nb);                          // TR_SUB + 1
+    uint32_t *dbase = rowc + TR_SUB + 1;                                              // nb
+    uint16_t *wc = reinterpret_cast<uint16_t *>(dbase + nb);                          // TR_WARPS * nb
+    __shared__ uint32_t wsum[TR_WARPS];
+    __shared__ uint32_t s_flag, s_row;
+    const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5, lt = (1u << lane) - 1u;
+    const uint64_t t_begin = T * blockIdx.x / G, t_end = T * (blockIdx.x + 1) / G;
+    for (uint32_t b = tid; b < nb; b += TR_THREADS) pos[b] = hofs[(size_t)b * G + blockIdx.x];
+    if (tid == 0) s_row = t_begin < t_end ? tr_row_of(trp, ntr, t_begin) : 0u;
+    __syncthreads();
+    uint32_t rcur = s_row;
+    for (uint64_t t0 = t_begin; t0 < t_end; t0 += TR_SUB) {
+        const uint32_t cnt = (uint32_t)min((uint64_t)TR_SUB, t_end - t0);
+        // rows: rowc[p] = number of tile rows after rcur starting at or before t0 + p
+        for (uint32_t q = tid; q <= TR_SUB; q += TR_THREADS) rowc[q] = 0;
+        for (uint32_t b = tid; b < TR_WARPS * nb; b += TR_THREADS) wc[b] = 0;
+        __syncthreads();
+        for (uint32_t r = rcur + 1;; r += TR_THREADS) {
+            bool more = false;
+            const uint32_t rr = r + tid;
+            if (rr < ntr) {
+                const uint32_t st = __ldg(trp + rr);
+                if (st <= t0 + cnt) {
+                    atomicAdd(&rowc[st - t0], 1u);
+                    more = true;
+                }
+            }
+            if (!__syncthreads_or(more)) break;
+        }
+        // inclusive scan of rowc[0..TR_SUB] (TR_SUB + 1 entries; the last one only feeds the next rcur)
+        {
+            uint32_t v[TR_PER], run = 0;
+#pragma unroll
+            for (int k = 0; k < TR_PER; k++) { run += rowc[tid * TR_PER + k]; v[k] = run; }
+            uint32_t incl = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (uint32_t)o) incl += y;
+            }
+            if (lane == 31) wsum[w] = incl;
+            const uint32_t last = rowc[TR_SUB];
+            __syncthreads();
+            uint32_t off = incl - run;
+            for (uint32_t u = 0; u < w; u++) off += wsum[u];
+#pragma unroll
+            for (int k = 0; k < TR_PER; k++) rowc[tid * TR_PER + k] = v[k] + off;
+            if (tid == TR_THREADS - 1) s_flag = v[TR_PER - 1] + off + last;
+            __syncthreads();
+        }
+        // elements of this thread (warp w: tiles [w*256, w*256+256) in rounds of 32), stable digit rank
+        unsigned long long key[TR_PER], pay[TR_PER];
+        uint32_t rank[TR_PER], dig[TR_PER];
+#pragma unroll
+        for (int j = 0; j < TR_PER; j++) {
+            const uint32_t p = w * (TR_SUB / TR_WARPS) + j * 32 + lane;
+            const bool ok = p < cnt;
+            uint32_t dg = TR_MAXB;  // no element
+            key[j] = 0;
+            pay[j] = 0;
+            if (ok) {
+                const uint64_t t = t0 + p;
+                const uint32_t col = __ldg(tci + t), row = rcur + rowc[p];
+                dg = col >> lb;
+                key[j] = (unsigned long long)col | ((unsigned long long)row << cb);
+                if constexpr (D == 4) key[j] |= (unsigned long long)nib16(__ldg(reinterpret_cast<const uint32_t *>(tiles) + t)) << (2 * cb);
+                else pay[j] = __ldg(reinterpret_cast<const unsigned long long *>(tiles) + t);
+            }
+            dig[j] = dg;
+            const uint32_t peers = __match_any_sync(0xffffffffu, dg);
+            const uint32_t before = dg < TR_MAXB ? wc[w * nb + dg] : 0u;
+            rank[j] = before + __popc(peers & lt);
+            __syncwarp();
+            if (dg < TR_MAXB && lane == (uint32_t)(__ffs(peers) - 1)) wc[w * nb + dg] = (uint16_t)(before + __popc(peers));
+            __syncwarp();
+        }
+        __syncthreads();
+        // per digit: warp prefix (in place) and the CTA-local run start
+        for (uint32_t b = tid; b < nb; b += TR_THREADS) {
+            uint32_t run = 0;
+#pragma unroll
+            for (int u = 0; u < TR_WARPS; u++) {
+                const uint32_t c = wc[u * nb + b];
+                wc[u * nb + b] = (uint16_t)run;
+                run += c;
+            }
+            dbase[b] = run;  // digit total, scanned below
+        }
+        __syncthreads();
+        if (w == 0) {  // exclusive scan of the nb digit totals (one warp)
+            uint32_t carry = 0;
+            for (uint32_t b0 = 0; b0 < nb; b0 += 32) {
+                const uint32_t b = b0 + lane;
+                const uint32_t v = b < nb ? dbase[b] : 0u;
+                uint32_t incl = v;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= (uint32_t)o) incl += y;
+                }
+                if (b < nb) dbase[b] = carry + incl - v;
+                carry += __shfl_sync(0xffffffffu, incl, 31);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < TR_PER; j++)
+            if (dig[j] < TR_MAXB) {
+                const uint32_t lp = dbase[dig[j]] + wc[w * nb + dig[j]] + rank[j];
+                skey[lp] = key[j];
+                if constexpr (TrElem<D>::PAY) spay[lp] = pay[j];
+            }
+        __syncthreads();
+        for (uint32_t lp = tid; lp < cnt; lp += TR_THREADS) {
+            const unsigned long long k = skey[lp];
+            const uint32_t dg = (uint32_t)(k & ((1ull << cb) - 1)) >> lb;
+            const unsigned long long o = pos[dg] + (lp - dbase[dg]);
+            ekey[o] = k;
+            if constexpr (TrElem<D>::PAY) epay[o] = spay[lp];
+        }
+        __syncthreads();
+        for (uint32_t b = tid; b < nb; b += TR_THREADS) {  // advance each digit by its count in this sub-tile
+            const uint32_t nxt = b + 1 < nb ? dbase[b + 1] : cnt;
+            pos[b] += nxt - dbase[b];
+        }
+        rcur += s_flag;
+        __syncthreads();
+    }
+}
+
+template <int D>
+__global__ void __launch_bounds__(TR_THREADS) k_tr_bucket(uint32_t ntr, int cb, int lb, uint32_t G,
+                                                          const uint64_t *__restrict__ hofs, uint64_t T,
+                                                          const unsigned long long *__restrict__ ekey,
+                                                          const unsigned long long *__restrict__ epay,
+                                                          uint32_t *__restrict__ trp_out, uint32_t *__restrict__ tci_out,
+                                                          void *__restrict__ tiles_out) {
+    extern __shared__ __align__(16) unsigned char tr_smem[];
+    const uint32_t nl = 1u << lb;
+    uint32_t *wc = reinterpret_cast<uint32_t *>(tr_smem);  // TR_WARPS * nl
+    uint32_t *cs = wc + TR_WARPS * nl;                       // nl
+    const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5, lt = (1u << lane) - 1u;
+    const uint32_t b = blockIdx.x;
+    const uint64_t bs = hofs[(size_t)b * G], be = hofs[(size_t)(b + 1) * G];
+    const uint64_t s0 = bs + (be - bs) * w / TR_WARPS, s1 = bs + (be - bs) * (w + 1) / TR_WARPS;
+    const uint32_t lm = nl - 1;
+    for (uint32_t q = tid; q < TR_WARPS * nl; q += TR_THREADS) wc[q] = 0;
+    __syncthreads();
+    for (uint64_t e = s0 + lane; e < s1; e += 32) atomicAdd(&wc[w * nl + ((uint32_t)ekey[e] & lm)], 1u);
+    __syncthreads();
+    for (uint32_t c = tid; c < nl; c += TR_THREADS) {
+        uint32_t run = 0;
+#pragma unroll
+        for (int u = 0; u < TR_WARPS; u++) {
+            const uint32_t v = wc[u * nl + c];
+            wc[u * nl + c] = run;
+            run += v;
+        }
+        cs[c] = run;
+    }
+    __syncthreads();
+    if (w == 0) {  // exclusive scan of the column totals -> tile_row_ptr of the transpose
+        uint32_t carry = 0;
+        for (uint32_t c0 = 0; c0 < nl; c0 += 32) {
+            const uint32_t c = c0 + lane;
+            const uint32_t v = c < nl ? cs[c] : 0u;
+            uint32_t incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (uint32_t)o) incl += y;
+            }
+            if (c < nl) {
+                cs[c] = carry + incl - v;
+                const uint64_t col = ((uint64_t)b << lb) + c;
+                if (col < ntr) trp_out[col] = (uint32_t)(bs + carry + incl - v);
+            }
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        if (b == gridDim.x - 1 && lane == 0) trp_out[ntr] = (uint32_t)T;
+    }
+    __syncthreads();
+    const unsigned long long cm = (1ull << cb) - 1;
+    for (uint64_t e0 = s0; e0 < s1; e0 += 32) {  // warp-uniform: stable placement in order
+        const uint64_t e = e0 + lane;
+        const bool ok = e < s1;
+        unsigned long long k = ok ? ekey[e] : 0ull;
+        const uint32_t c = ok ? ((uint32_t)k & lm) : nl;
+        const uint32_t peers = __match_any_sync(0xffffffffu, c);
+        const uint32_t before = ok ? wc[w * nl + c] : 0u;
+        __syncwarp();
+        if (ok && lane == (uint32_t)(__ffs(peers) - 1)) wc[w * nl + c] = before + __popc(peers);
+        __syncwarp();
+        if (ok) {
+            const uint64_t o = bs + cs[c] + before + __popc(peers & lt);
+            tci_out[o] = (uint32_t)((k >> cb) & cm);  // the source row is the new column
+            if constexpr (D == 4) {
+                const uint32_t nib = (uint32_t)(k >> (2 * cb));
+                uint32_t a[4] = {nib & 0xFu, (nib >> 4) & 0xFu, (nib >> 8) & 0xFu, (nib >> 12) & 0xFu};
+                bit_transpose<4>(a);
+                reinterpret_cast<uint32_t *>(tiles_out)[o] = a[0] | (a[1] << 8) | (a[2] << 16) | (a[3] << 24);
+            } else {
+                const unsigned long long v = epay[e];
+                uint32_t a[8];
+#pragma unroll
+                for (int r = 0; r < 8; r++) a[r] = (uint32_t)(v >> (8 * r)) & 0xFFu;
+                bit_transpose<8>(a);
+                unsigned long long outv = 0;
+#pragma unroll
+                for (int r = 0; r < 8; r++) outv |= (unsigned long long)a[r] << (8 * r);
+                reinterpret_cast<unsigned long long *>(tiles_out)[o] = outv;
+            }
+        }
+    }
+}
+
+// Measured slower than the LSD path (s22: d=4 10.2 vs 7.0 ms, d=8 12.5 vs 11.5
+// ms): the bucket pass writes 4-byte outputs scattered over its bucket's
+// 1 MB range, and with ~700 buckets in flight the partially written sectors
+// leave L2 before they fill (ncu: k_tr_bucket at 18 % issue, long-scoreboard
+// bound).  Kept as an A/B path: B2SR_TRANSPOSE=two.
+static bool tr2_enabled() {
+    const char *e = getenv("B2SR_TRANSPOSE");
+    return e && e[0] == 't';
+}
+
+// returns false when the two-level path does not apply (d >= 16, > 22 column bits)
+template <int D>
+static bool transpose_two_level(const b2sr_matrix *m, b2sr_matrix *o, int cb, cudaStream_t s) {
+    if (cb > 22 || !tr2_enabled()) return false;
+    const uint64_t T = m->num_tiles;
+    const uint32_t ntr = m->ntr;
+    const int lb = cb / 2, hb = cb - lb;
+    const uint32_t nb = 1u << hb, nl = 1u << lb;
+    const uint32_t G = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)num_sms() * 2, (T + TR_SUB - 1) / TR_SUB));
+    Buf<uint32_t> hcnt((size_t)nb * G, s);
+    Buf<uint64_t> hofs((size_t)nb * G + 1, s);
+    LAUNCH(k_tr_hist, G, TR_THREADS, 0, s, T, G, m->tci, lb, nb, hcnt.p);
+    exclusive_scan_u32_to_u64(hcnt.p, hofs.p, (size_t)nb * G, s);
+    Buf<unsigned long long> ekey(T, s), epay(TrElem<D>::PAY ? T : 1, s);
+    const size_t smem_b = (size_t)TR_SUB * 8 * (TrElem<D>::PAY ? 2 : 1) + (size_t)nb * 8 + (TR_SUB + 1) * 4 +
+                          (size_t)nb * 4 + (size_t)TR_WARPS * nb * 2 + 16;
+    hot_smem_attr_raw(reinterpret_cast<const void *>(k_tr_scatter<D>), smem_b);
+    LAUNCH(k_tr_scatter<D>, G, TR_THREADS, smem_b, s, T, G, ntr, m->trp, m->tci, m->tiles, cb, lb, nb, hofs.p, ekey.p,
+           epay.p);
+    const size_t smem_c = (size_t)TR_WARPS * nl * 4 + (size_t)nl * 4;
+    hot_smem_attr_raw(reinterpret_cast<const void *>(k_tr_bucket<D>), smem_c);
+    LAUNCH(k_tr_bucket<D>, nb, TR_THREADS, smem_c, s, ntr, cb, lb, G, hofs.p, T, ekey.p, epay.p, o->trp, o->tci,
+           o->tiles);
+    return true;
+}
+
 void launch_row_ids(const b2sr_matrix *m, uint32_t *rowid, cudaStream_t s) {
     uint64_t b = ((uint64_t)m->ntr * 32 + 255) / 256, cap = (uint64_t)num_sms() * 16;
     LAUNCH(k_row_ids, (unsigned)std::max<uint64_t>(1, std::min(b, cap)), 256, 0, s, m->ntr, m->trp, rowid);
@@ -162,6 +485,10 @@ b2sr_matrix *transpose_device(const b2sr_matrix *m, cudaStream_t s) {
     uint64_t T = m->num_tiles;
     b2sr_matrix *o = new_matrix(m->n, m->dim, ntr, T, s);
     try {
+        const int cb0 = std::max(1, bits_for(ntr - 1));  // >= 1: the packed fields must not overlap
+        if (T && ((m->dim == 4 && transpose_two_level<4>(m, o, cb0, s)) ||
+                  (m->dim == 8 && transpose_two_level<8>(m, o, cb0, s))))
+            return o;
         Buf<uint32_t> cnt(ntr, s);
         Buf<uint64_t> ofs((size_t)ntr + 1, s);
         CK(cudaMemsetAsync(cnt.p, 0, (size_t)ntr * 4, s));
