@@ -570,9 +570,11 @@ def bench_tc(args, b2, rmat, torch, ev):
                        "popc_peak_units_per_s": popc_peak,
                        "popc_frac": round(work.value / (kms / 1e3) / popc_peak, 4)}
     return {"scale": args.tc_scale, "nnz": int(csr.nnz), "by_tile_dim": out,
-            "kernel": "k_bmm_masked_items (AND+POPC): sum over the degree-oriented DAG L of (L L^T) "
-                      "(= triangles; the reference uses the ID-ordered lower triangle)",
-            "note": "work_units = AND+POPC units W; the kernel is bound by intersection search, not POPC"}
+            "kernel": "k_tc_filter (each pair of L staged on its longer row: shared-memory filter probes, "
+                      "queued hits, AND+POPC) + k_bmm_masked_items for rows over 1024 tiles: sum over the "
+                      "degree-oriented DAG L of (L L^T) (= triangles; the reference uses the ID-ordered lower triangle)",
+            "note": "work_units = AND+POPC units W; ms = the whole b2sr_tc call (incl. the transpose of L), "
+                    "spgemm_kernel_ms = the masked SpGEMM kernels; bound by probe issue, not POPC"}
 
 
 def cpu_baseline(csr, d, root):

@@ -222,7 +222,8 @@ int b2sr_from_host(uint32_t n, uint32_t dim, const uint32_t *h_trp, const uint32
         h2d(m->trp, h_trp, ((size_t)ntr + 1) * 4, s);
         if (num_tiles) {
             h2d(m->tci, h_tci, num_tiles * 4, s);
-            h2d(m->tiles, h_tiles, num_tiles * dim * word_bytes(dim), s);
+            if (!(dim == 4 && h2d_tiles4(m->tiles, h_tiles, num_tiles, s)))
+                h2d(m->tiles, h_tiles, num_tiles * dim * word_bytes(dim), s);
         }
     } catch (...) {
         free_matrix(m);

@@ -1765,18 +1765,21 @@ int b2sr_pagerank(const b2sr_matrix *a, const double *d_out_degree, double alpha
             const unsigned gi = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)a->n_items + 7) / 8,
                                                                                     (uint64_t)num_sms() * 16));
             kernel_timer().begin(s);
-            // B2SR_PRG: gather geometry (A/B) -- 0: U=8 x 4 CTAs/SM, 1: U=4 x 6, 2: U=6 x 5, 3: U=16 x 2
-            static const int prg = [] { const char *e = getenv("B2SR_PRG"); return e ? atoi(e) : 0; }();
+            // B2SR_PRG: gather geometry (A/B; s24 gather ms) -- 5 (default): U=2 x 8 CTAs/SM (3.03),
+            // 0: U=8 x 4 (3.97), 1: U=4 x 6 (3.31), 2: U=6 x 5 (4.07), 3: U=16 x 2 (6.56), 4: U=4 x 8 (3.89, spills)
+            static const int prg = [] { const char *e = getenv("B2SR_PRG"); return e ? atoi(e) : 5; }();
 #define PRG_LAUNCH(DD, UU, MB)                                                                                    \
     LAUNCH((k_pr_gather32<DD, UU, MB>), gi, 256, 0, s, a->items, a->n_items, n, gtci, (const uint8_t *)a->tiles, \
            x32.p, g.p, part.p)
             if (d == 4) {
-                if (prg == 1) PRG_LAUNCH(4, 4, 6);
+                if (prg == 0) PRG_LAUNCH(4, 8, 4);
+                else if (prg == 1) PRG_LAUNCH(4, 4, 6);
                 else if (prg == 2) PRG_LAUNCH(4, 6, 5);
                 else if (prg == 3) PRG_LAUNCH(4, 16, 2);
-                else PRG_LAUNCH(4, 8, 4);
+                else if (prg == 4) PRG_LAUNCH(4, 4, 8);
+                else PRG_LAUNCH(4, 2, 8);
             } else {
-                PRG_LAUNCH(8, 8, 4);
+                PRG_LAUNCH(8, 8, 4);  // d = 8 (U = 4 x 6 spills there)
             }
 #undef PRG_LAUNCH
             kernel_timer().end(s);

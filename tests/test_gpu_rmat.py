@@ -192,3 +192,35 @@ def test_row_partitioned_pagerank_sssp_two_ranks_one_gpu(d, monkeypatch):
         p.join(timeout=60)
     assert got[0] == want_pr.per_vertex.tobytes() and got[1] == want_pr.iterations and got[2] == want_pr.converged
     assert got[3] == want_ss.per_vertex.tobytes() and got[4] == want_ss.iterations
+
+
+def test_large_host_upload_paths(tmp_path):
+    """Host-array uploads above the staging threshold (staging.cu): the
+    staged copy of tile_col_ind and the nibble-packed d=4 tile upload give the
+    device the caller's exact bytes; a d=4 tile with a high nibble set still
+    reaches the device check and raises the reference constructor's message."""
+    from paper_2201_08560_b200.errors import FormatError
+
+    csr = rmat.rmat_csr(18, 16, seed=4)  # ~7.7 M tiles at d=4: 31 MB of tiles, past the 16 MB threshold
+    for d in (4, 8):
+        m = b2.csr_to_b2sr(csr, d)
+        trp, tci, tiles = m.tile_row_ptr.copy(), m.tile_col_ind.copy(), m.bit_tiles.copy()
+        h = b2.B2srMatrix(csr.n, d, trp, tci, tiles)  # host-built: uploaded on first use
+        assert h == m
+        p = tmp_path / f"m{d}.b2sr"
+        b2.save_b2sr(m, p)
+        back = b2.load_b2sr(p)  # straight to HBM through the device check
+        assert back == m
+        assert back.bit_tiles.tobytes() == tiles.tobytes() and back.tile_col_ind.tobytes() == tci.tobytes()
+    m = b2.csr_to_b2sr(csr, 4)
+    trp, tci, tiles = m.tile_row_ptr.copy(), m.tile_col_ind.copy(), m.bit_tiles.copy()
+    tiles[len(tiles) // 2] |= 0x10  # a high nibble in a row byte of a 4x4 tile
+    raw = (b2.formats._HEADER.pack(b2.formats._MAGIC, b2.formats._VERSION, csr.n, 4, len(trp) - 1, len(tci))
+           + trp.astype("<u4").tobytes() + tci.astype("<u4").tobytes() + tiles.astype(np.uint8).tobytes())
+    q = tmp_path / "bad.b2sr"
+    q.write_bytes(raw)
+    with pytest.raises(FormatError) as e_dev:
+        b2.load_b2sr(q)
+    with pytest.raises(FormatError) as e_host:
+        b2.B2srMatrix(csr.n, 4, trp, tci, tiles)
+    assert str(e_dev.value) == str(e_host.value)
