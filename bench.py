@@ -286,7 +286,9 @@ def run_ours(args, rank, world, local_rank):
             s1.record()
             torch.cuda.synchronize()
         conv_ms = s0.elapsed_time(s1)
+        at = None
         for _ in range(2):
+            at = None  # the previous result's memory goes back to the pool first
             torch.cuda.synchronize()
             s0.record()
             at = b2.formats.B2srMatrix._wrap(b2.formats._new_handle("b2sr_transpose", m.handle().ptr, sp))

@@ -181,8 +181,9 @@ int num_sms();
 // host -> device copy; pageable sources are staged through page-locked
 // chunks at the link rate (staging.cu)
 void h2d(void *dst, const void *src, size_t bytes, cudaStream_t s);
-// d = 4 tiles uploaded nibble-packed (staging.cu); false: not applicable, use h2d
-bool h2d_tiles4(void *d_tiles, const void *h_tiles, uint64_t num_tiles, cudaStream_t s);
+// the arrays of a host B2SR matrix into m's device arrays in one staged upload
+// (d = 4 tiles nibble-packed on the way; staging.cu)
+void upload_b2sr(b2sr_matrix *m, const uint32_t *h_trp, const uint32_t *h_tci, const void *h_tiles, cudaStream_t s);
 void launch_row_ids(const b2sr_matrix *m, uint32_t *rowid, cudaStream_t s);  // rowid[t] = tile row of t
 void free_vlong(void *plan);
 void *build_vlong(b2sr_matrix *m, uint32_t thresh, cudaStream_t s);

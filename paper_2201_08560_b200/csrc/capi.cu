@@ -219,12 +219,7 @@ int b2sr_from_host(uint32_t n, uint32_t dim, const uint32_t *h_trp, const uint32
     uint32_t ntr = tile_rows(n, dim);
     b2sr_matrix *m = new_matrix(n, dim, ntr, num_tiles, s);
     try {
-        h2d(m->trp, h_trp, ((size_t)ntr + 1) * 4, s);
-        if (num_tiles) {
-            h2d(m->tci, h_tci, num_tiles * 4, s);
-            if (!(dim == 4 && h2d_tiles4(m->tiles, h_tiles, num_tiles, s)))
-                h2d(m->tiles, h_tiles, num_tiles * dim * word_bytes(dim), s);
-        }
+        upload_b2sr(m, h_trp, h_tci, h_tiles, s);
     } catch (...) {
         free_matrix(m);
         throw;
@@ -299,11 +294,7 @@ int b2sr_block_from_host(uint32_t n, uint32_t dim, uint32_t tr_begin, uint32_t t
     b2sr_matrix *m = new_matrix(n, dim, rows, num_tiles, s);
     m->row0 = tr_begin;
     try {
-        h2d(m->trp, h_trp, ((size_t)rows + 1) * 4, s);
-        if (num_tiles) {
-            h2d(m->tci, h_tci, num_tiles * 4, s);
-            h2d(m->tiles, h_tiles, num_tiles * dim * word_bytes(dim), s);
-        }
+        upload_b2sr(m, h_trp, h_tci, h_tiles, s);  // trp: rows + 1 entries (m->ntr = rows)
     } catch (...) {
         free_matrix(m);
         throw;

@@ -317,6 +317,92 @@ static void conv_dispatch(uint32_t d, bool pack, const ConvItem *items, uint32_t
     }
 }
 
+// K1 for the warp-merge items: the tile count of an item is the number of
+// DISTINCT tile columns among its entries, which needs no sorted order: each
+// warp inserts its item's tile columns into a 1024-slot shared-memory hash set
+// (linear probing, atomicCAS) and counts the successful inserts.  Entries of
+// one run with the same tile column as their predecessor are skipped first
+// (runs are sorted).  About a dozen instructions per entry instead of the
+// log2 d merge levels (K2 still merges: it needs the order).
+constexpr uint32_t CH_SLOTS = 1024;  // >= 2 * CM_CAP: load factor <= 1/2
+
+template <int D>
+__global__ void __launch_bounds__(256) k_conv_count_hash(const ConvItem *__restrict__ items, uint32_t n_items, uint32_t n,
+                                                        const uint32_t *__restrict__ row_ptr,
+                                                        const uint32_t *__restrict__ col_ind, uint32_t *__restrict__ cnt,
+                                                        uint8_t *__restrict__ big) {
+    constexpr uint32_t S = D == 4 ? 2 : 3;
+    __shared__ uint32_t hset[8][CH_SLOTS];
+    __shared__ uint32_t soff[8][D + 1];
+    __shared__ uint32_t sst[8][D];
+    const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+    const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+    uint32_t *H = hset[wid], *off = soff[wid], *st = sst[wid];
+    for (uint32_t q = lane; q < CH_SLOTS; q += 32) H[q] = 0;
+    for (uint32_t item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < n_items; item += warps) {
+        const ConvItem it = items[item];
+        uint32_t p0 = 0, p1 = 0;
+        if (lane < (uint32_t)D) {
+            const uint64_t row = (uint64_t)it.row * D + lane;
+            if (row < n) {
+                p0 = row_ptr[row];
+                p1 = row_ptr[row + 1];
+                if (it.klo > 0) {
+                    uint32_t a = p0, b = p1;
+                    const uint32_t key = it.klo * (uint32_t)D;
+                    while (a < b) { const uint32_t m = (a + b) >> 1; if (__ldg(col_ind + m) < key) a = m + 1; else b = m; }
+                    p0 = a;
+                }
+                if ((uint64_t)it.khi * D < n) {
+                    uint32_t a = p0, b = p1;
+                    const uint32_t key = it.khi * (uint32_t)D;
+                    while (a < b) { const uint32_t m = (a + b) >> 1; if (__ldg(col_ind + m) < key) a = m + 1; else b = m; }
+                    p1 = a;
+                }
+            }
+        }
+        const uint32_t len = p1 - p0;
+        uint32_t incl = len;
+#pragma unroll
+        for (int o = 1; o < D; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+        }
+        const uint32_t E = __shfl_sync(0xffffffffu, incl, D - 1);
+        if (E > CM_CAP) {  // the lock-step merge takes it
+            if (lane == 0) big[item] = 1;
+            continue;
+        }
+        __syncwarp();
+        if (lane < (uint32_t)D) {
+            off[lane + 1] = incl;
+            st[lane] = p0;
+        }
+        if (lane == 0) off[0] = 0;
+        __syncwarp();
+        uint32_t count = 0;
+        for (uint32_t i = lane; i < E; i += 32) {
+            uint32_t r = 0;
+#pragma unroll
+            for (int q = 1; q < D; q++) r += off[q] <= i;
+            const uint32_t g = st[r] + (i - off[r]);
+            const uint32_t k = __ldg(col_ind + g) >> S;
+            if (i > off[r] && (__ldg(col_ind + g - 1) >> S) == k) continue;  // same tile as the run's previous entry
+            uint32_t h = (k * 0x9E3779B1u) >> (32 - 10);
+            for (;;) {
+                const uint32_t old = atomicCAS(H + h, 0u, k + 1);
+                if (old == 0) { count++; break; }
+                if (old == k + 1) break;
+                h = (h + 1) & (CH_SLOTS - 1);
+            }
+        }
+        count = __reduce_add_sync(0xffffffffu, count);
+        __syncwarp();
+        for (uint32_t q = lane; q < CH_SLOTS; q += 32) H[q] = 0;
+        if (lane == 0) cnt[item] = count;
+    }
+}
+
 template <int D>
 static void merge_launch(bool pack, const ConvItem *items, uint32_t n_items, uint32_t n, const uint32_t *row_ptr,
                          const uint32_t *col_ind, const uint64_t *iofs, uint32_t *cnt, uint32_t *tci, void *tiles,
@@ -401,8 +487,17 @@ b2sr_matrix *csr_to_b2sr_device(uint32_t n, uint32_t d, const uint32_t *row_ptr,
     if (merge) {
         big = Buf<uint8_t>(std::max<uint32_t>(n_items, 1), s);
         CK(cudaMemsetAsync(big.p, 0, n_items, s));
-        if (d == 4) merge_launch<4>(false, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, nullptr, nullptr, big.p, s);
-        else merge_launch<8>(false, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, nullptr, nullptr, big.p, s);
+        // K1: distinct tile columns counted through a shared-memory hash set
+        // (B2SR_CONV_COUNT=merge: the merge kernel's count pass, A/B)
+        const char *ce = getenv("B2SR_CONV_COUNT");
+        if (ce && ce[0] == 'm') {
+            if (d == 4) merge_launch<4>(false, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, nullptr, nullptr, big.p, s);
+            else merge_launch<8>(false, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, nullptr, nullptr, big.p, s);
+        } else {
+            const unsigned g = (unsigned)std::min<uint64_t>(((uint64_t)n_items + 7) / 8, (uint64_t)num_sms() * 6);
+            if (d == 4) LAUNCH(k_conv_count_hash<4>, g, 256, 0, s, items.p, n_items, n, row_ptr, col_ind, cnt.p, big.p);
+            else LAUNCH(k_conv_count_hash<8>, g, 256, 0, s, items.p, n_items, n, row_ptr, col_ind, cnt.p, big.p);
+        }
     }
     conv_dispatch(d, false, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, nullptr, nullptr, s, order,
                   merge ? big.p : nullptr);

@@ -13,7 +13,7 @@ namespace b2sr {
 
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
-constexpr int RS_ROUNDS = 16;
+constexpr int RS_ROUNDS = 8;   // 16: 122 registers, 2 CTAs per SM
 constexpr int RS_TILE = RS_THREADS * RS_ROUNDS;  // 4096 keys per CTA
 
 template <typename K>
@@ -41,8 +41,11 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__
     __shared__ uint32_t dbase[256];            // CTA-local start of each digit run
     __shared__ K skey[RS_TILE];                // keys re-ordered by digit inside the CTA
     __shared__ uint32_t sval[VALS ? RS_TILE : 1];
+    __shared__ uint64_t goff[256];             // this CTA's global start of each digit run
     const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
     for (int b = threadIdx.x; b < RS_WARPS * 256; b += RS_THREADS) (&wc[0][0])[b] = 0;
+    // once per CTA instead of one dependent global load per key in the write loop
+    for (int b = threadIdx.x; b < 256; b += RS_THREADS) goff[b] = offs[(size_t)b * nblocks + blockIdx.x];
     __syncthreads();
     size_t base = (size_t)blockIdx.x * RS_TILE + (size_t)w * (32 * RS_ROUNDS);
     K key[RS_ROUNDS];
@@ -103,7 +106,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__
     for (uint32_t lp = threadIdx.x; lp < count; lp += RS_THREADS) {
         K k = skey[lp];
         uint32_t dg = (uint32_t)(k >> sh) & dm;
-        size_t pos = offs[(size_t)dg * nblocks + blockIdx.x] + (lp - dbase[dg]);
+        size_t pos = goff[dg] + (lp - dbase[dg]);
         kout[pos] = k;
         if constexpr (VALS) vout[pos] = sval[lp];
     }

@@ -39,7 +39,9 @@ int copy_threads() {
     static int t = [] {
         const char *e = getenv("B2SR_H2D_THREADS");
         int v = e ? atoi(e) : 0;
-        if (v <= 0) v = std::min(12, std::max(1, (int)std::thread::hardware_concurrency() * 3 / 4));
+        // 16-core GPU host, R-MAT s22 B2SR-4 host matrix (1.03 GB, tiles packed):
+        // 4 / 8 / 12 / 16 threads: 46.5 / 30.2 / 27.7 / 22.9 ms (tools/upload_probe.py)
+        if (v <= 0) v = std::min(16, std::max(1, (int)std::thread::hardware_concurrency()));
         return v;
     }();
     return t;
@@ -86,19 +88,40 @@ bool page_locked(const void *p) {
 
 }  // namespace
 
-// The staged loop: src_bytes of pageable input in chunks of kChunk * IN /
-// OUT source bytes, each turned into <= kChunk staged bytes by `fill(slot,
-// src_chunk, len) -> staged bytes` and DMA'd to dst + chunk * (kChunk).
-template <class Fill>
-static void staged(void *dst, const void *src, size_t src_bytes, size_t src_chunk, size_t dst_chunk, Fill fill,
-                   cudaStream_t s) {
+// One staged upload: a list of jobs (dst, pageable src, bytes, kind), cut
+// into chunks that fill at most one kChunk slot; T host threads take every
+// T-th chunk of the whole list, so several arrays stream without a join
+// between them.  kind COPY: memcpy; kind PACK4: d = 4 bit tiles, four row
+// bytes -> 16 bits (only the low nibbles may be set, formats.py:289).
+enum { COPY = 0, PACK4 = 1 };
+struct Job {
+    void *dst;
+    const void *src;
+    size_t bytes;  // source bytes
+    int kind;
+};
+
+static void staged(const std::vector<Job> &jobs, bool *high, cudaStream_t s) {
+    struct Chunk {
+        int job;
+        size_t off;  // source offset
+        size_t len;  // source bytes
+    };
+    std::vector<Chunk> chunks;
+    for (int j = 0; j < (int)jobs.size(); j++) {
+        const size_t step = jobs[j].kind == PACK4 ? 2 * kChunk : kChunk;
+        for (size_t off = 0; off < jobs[j].bytes; off += step)
+            chunks.push_back({j, off, std::min(step, jobs[j].bytes - off)});
+    }
+    if (chunks.empty()) return;
     int dev = 0;
     CK(cudaGetDevice(&dev));
     StagePool &P = pool(dev);
     std::lock_guard<std::mutex> lk(P.mu);
     P.init(copy_threads());
-    const size_t nchunks = (src_bytes + src_chunk - 1) / src_chunk;
+    const size_t nchunks = chunks.size();
     const int T = (int)std::min<size_t>(P.threads, nchunks);
+    std::atomic<bool> hi{false};
     std::vector<std::exception_ptr> err(T);
     std::vector<std::string> msg(T);  // the error text is thread-local: carry it to the caller's thread
     auto worker = [&](int i) {
@@ -107,10 +130,28 @@ static void staged(void *dst, const void *src, size_t src_bytes, size_t src_chun
             size_t round = 0;
             for (size_t c = i; c < nchunks; c += T, round++) {
                 const int slot = i + P.threads * (int)(round & 1);
-                const size_t off = c * src_chunk, len = std::min(src_chunk, src_bytes - off);
+                const Chunk &ch = chunks[c];
+                const Job &jb = jobs[ch.job];
+                const char *from = (const char *)jb.src + ch.off;
                 CK(cudaEventSynchronize(P.done[slot]));  // the slot's previous DMA has drained
-                const size_t out = fill(P.buf[slot], (const char *)src + off, len);
-                CK(cudaMemcpyAsync((char *)dst + c * dst_chunk, P.buf[slot], out, cudaMemcpyHostToDevice, s));
+                size_t out = ch.len, doff = ch.off;
+                if (jb.kind == COPY) {
+                    memcpy(P.buf[slot], from, ch.len);
+                } else {
+                    const uint32_t *w = reinterpret_cast<const uint32_t *>(from);
+                    uint16_t *o = static_cast<uint16_t *>(P.buf[slot]);
+                    const size_t n = ch.len / 4;
+                    uint32_t h = 0;
+                    for (size_t k = 0; k < n; k++) {
+                        const uint32_t v = w[k];
+                        h |= v;
+                        o[k] = (uint16_t)((v & 0xFu) | ((v >> 4) & 0xF0u) | ((v >> 8) & 0xF00u) | ((v >> 12) & 0xF000u));
+                    }
+                    if (h & 0xF0F0F0F0u) hi.store(true, std::memory_order_relaxed);
+                    out = n * 2;
+                    doff = ch.off / 2;
+                }
+                CK(cudaMemcpyAsync((char *)jb.dst + doff, P.buf[slot], out, cudaMemcpyHostToDevice, s));
                 CK(cudaEventRecord(P.done[slot], s));
             }
         } catch (...) {
@@ -128,6 +169,7 @@ static void staged(void *dst, const void *src, size_t src_bytes, size_t src_chun
             set_error(B2SR_ECUDA, "%s", msg[i].c_str());
             std::rethrow_exception(err[i]);
         }
+    if (high) *high = hi.load();
 }
 
 void h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
@@ -141,20 +183,12 @@ void h2d(void *dst, const void *src, size_t bytes, cudaStream_t s) {
         CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
         return;
     }
-    staged(dst, src, bytes, kChunk, kChunk,
-           [](void *slot, const char *from, size_t len) {
-               memcpy(slot, from, len);
-               return len;
-           },
-           s);
+    staged({{dst, src, bytes, COPY}}, nullptr, s);
 }
 
-// d = 4 bit tiles: four row bytes of which only the low nibbles may be set
-// (formats.py:289).  The upload packs them to 16 bits per tile on the host
-// (inside the copy the staging threads do anyway) and widens them again on
-// the device: 512 -> 256 MB over PCIe at R-MAT s22.  A tile with a high
-// nibble set (a FormatError the device check must report, with the
-// reference's message) makes the caller fall back to the plain copy.
+// d = 4 bit tiles travel nibble-packed: 512 -> 256 MB over PCIe at R-MAT s22,
+// widened again on the device.  A tile with a high nibble set (a FormatError
+// the device check reports with the reference's message) is re-sent plainly.
 __global__ void k_unpack_nibbles(uint64_t T, const uint16_t *__restrict__ in, uint32_t *__restrict__ out) {
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < T; t += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t p = in[t];
@@ -162,30 +196,37 @@ __global__ void k_unpack_nibbles(uint64_t T, const uint16_t *__restrict__ in, ui
     }
 }
 
-bool h2d_tiles4(void *d_tiles, const void *h_tiles, uint64_t T, cudaStream_t s) {
-    const size_t bytes = T * 4;
-    if (bytes < 4 * kDirect || page_locked(h_tiles)) return false;
-    Buf<uint16_t> packed(T, s);
-    std::atomic<bool> high{false};
-    staged(packed.p, h_tiles, bytes, 2 * kChunk, kChunk,
-           [&](void *slot, const char *from, size_t len) {
-               const uint32_t *w = reinterpret_cast<const uint32_t *>(from);
-               uint16_t *o = static_cast<uint16_t *>(slot);
-               const size_t n = len / 4;
-               uint32_t hi = 0;
-               for (size_t i = 0; i < n; i++) {
-                   const uint32_t v = w[i];
-                   hi |= v;
-                   o[i] = (uint16_t)((v & 0xFu) | ((v >> 4) & 0xF0u) | ((v >> 8) & 0xF00u) | ((v >> 12) & 0xF000u));
-               }
-               if (hi & 0xF0F0F0F0u) high.store(true, std::memory_order_relaxed);
-               return n * 2;
-           },
-           s);
-    if (high.load()) return false;  // the stream drains `packed` before its memory is reused
+// the three arrays of a host B2SR matrix in one staged upload
+void upload_b2sr(b2sr_matrix *m, const uint32_t *h_trp, const uint32_t *h_tci, const void *h_tiles, cudaStream_t s) {
+    const size_t trp_b = ((size_t)m->ntr + 1) * 4, tci_b = m->num_tiles * 4;
+    const size_t tile_b = m->num_tiles * (size_t)m->dim * word_bytes(m->dim);
+    const bool pinned = page_locked(h_tci);
+    if (pinned || tci_b + tile_b < 4 * kDirect) {
+        h2d(m->trp, h_trp, trp_b, s);
+        h2d(m->tci, h_tci, tci_b, s);
+        h2d(m->tiles, h_tiles, tile_b, s);
+        return;
+    }
+    static const bool pack_on = [] { const char *e = getenv("B2SR_H2D_PACK"); return !(e && e[0] == '0'); }();
+    const bool pack = pack_on && m->dim == 4 && !page_locked(h_tiles);  // B2SR_H2D_PACK=0: plain copy (A/B)
+    Buf<uint16_t> packed(pack ? m->num_tiles : 1, s);
+    std::vector<Job> jobs;
+    if (trp_b < kDirect) CK(cudaMemcpyAsync(m->trp, h_trp, trp_b, cudaMemcpyHostToDevice, s));
+    else jobs.push_back({m->trp, h_trp, trp_b, COPY});
+    jobs.push_back({m->tci, h_tci, tci_b, COPY});
+    if (pack) jobs.push_back({packed.p, h_tiles, tile_b, PACK4});
+    else if (page_locked(h_tiles)) h2d(m->tiles, h_tiles, tile_b, s);
+    else jobs.push_back({m->tiles, h_tiles, tile_b, COPY});
+    bool high = false;
+    staged(jobs, &high, s);
+    if (!pack) return;
+    if (high) {  // the stream drains `packed` before its memory is reused
+        h2d(m->tiles, h_tiles, tile_b, s);
+        return;
+    }
+    const uint64_t T = m->num_tiles;
     const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((T + 255) / 256, (uint64_t)num_sms() * 16));
-    LAUNCH(k_unpack_nibbles, g, 256, 0, s, T, packed.p, static_cast<uint32_t *>(d_tiles));
-    return true;
+    LAUNCH(k_unpack_nibbles, g, 256, 0, s, T, packed.p, static_cast<uint32_t *>(m->tiles));
 }
 
 }  // namespace b2sr

@@ -77,10 +77,6 @@ __device__ __forceinline__ void store_tile(void *tiles, size_t t, const uint32_t
     }
 }
 
-__global__ void k_col_hist(uint64_t T, const uint32_t *tci, uint32_t *cnt) {
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < T; t += (uint64_t)gridDim.x * blockDim.x)
-        atomicAdd(cnt + tci[t], 1u);
-}
 
 __global__ void k_u64_to_u32(const uint64_t *in, uint32_t *out, size_t n) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
@@ -117,20 +113,42 @@ __global__ void __launch_bounds__(256) k_transpose_gather(uint64_t T, const uint
 // d=4 fast path: a 4x4 tile is 16 bits of payload, so (column | row | tile)
 // fits one 64-bit key and a stable radix sort over the column bits carries
 // every tile to its transposed position -- no random gathers afterwards.
+// (a warp per tile row without the row-id array measured 2.8 vs 0.7 ms at s22:
+// a hub row of ~10^5 tiles serialises on one warp)
 __global__ void k_pack4(uint64_t T, const uint32_t *__restrict__ rowid, const uint32_t *__restrict__ tci,
                         const uint32_t *__restrict__ tiles, int cb, uint64_t *__restrict__ keys) {
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < T; t += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t w = tiles[t];  // four row bytes, low nibbles
-        uint32_t nib = (w & 0xFu) | ((w >> 4) & 0xF0u) | ((w >> 8) & 0xF00u) | ((w >> 12) & 0xF000u);
+        const uint32_t w = tiles[t];  // four row bytes, low nibbles
+        const uint32_t nib = (w & 0xFu) | ((w >> 4) & 0xF0u) | ((w >> 8) & 0xF00u) | ((w >> 12) & 0xF000u);
         keys[t] = (uint64_t)tci[t] | ((uint64_t)rowid[t] << cb) | ((uint64_t)nib << (2 * cb));
     }
 }
 
-__global__ void k_unpack4(uint64_t T, const uint64_t *__restrict__ keys, int cb, uint32_t *__restrict__ tci_out,
+// tile_row_ptr of the transpose from the column-sorted keys: position p starts
+// every column in (column of p-1, column of p]; the last position closes the
+// columns up to ntr (replaces a column histogram of T global atomics + scan)
+template <typename K>
+__device__ __forceinline__ void trp_bounds(uint64_t p, uint64_t T, K key, K prev, K mask, uint32_t ntr,
+                                           uint32_t *__restrict__ trp_out) {
+    const uint32_t c = (uint32_t)(key & mask);
+    const uint32_t c0 = p ? (uint32_t)(prev & mask) + 1u : 0u;
+    for (uint32_t q = c0; q <= c; q++) trp_out[q] = (uint32_t)p;
+    if (p + 1 == T)
+        for (uint32_t q = c + 1; q <= ntr; q++) trp_out[q] = (uint32_t)T;
+}
+
+__global__ void k_trp_sorted(uint64_t T, const uint32_t *__restrict__ cols, uint32_t ntr, uint32_t *__restrict__ trp_out) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < T; p += (uint64_t)gridDim.x * blockDim.x)
+        trp_bounds<uint32_t>(p, T, cols[p], p ? cols[p - 1] : 0u, 0xFFFFFFFFu, ntr, trp_out);
+}
+
+__global__ void k_unpack4(uint64_t T, const uint64_t *__restrict__ keys, int cb, uint32_t ntr,
+                          uint32_t *__restrict__ trp_out, uint32_t *__restrict__ tci_out,
                           uint32_t *__restrict__ tiles_out) {
     const uint64_t mask = (1ull << cb) - 1;
     for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < T; p += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t k = keys[p];
+        trp_bounds<uint64_t>(p, T, k, p ? keys[p - 1] : 0ull, mask, ntr, trp_out);
         tci_out[p] = (uint32_t)((k >> cb) & mask);  // the source row is the transposed column
         uint32_t nib = (uint32_t)(k >> (2 * cb));
         uint32_t a[4] = {nib & 0xFu, (nib >> 4) & 0xFu, (nib >> 8) & 0xFu, (nib >> 12) & 0xFu};
@@ -489,14 +507,10 @@ b2sr_matrix *transpose_device(const b2sr_matrix *m, cudaStream_t s) {
         if (T && ((m->dim == 4 && transpose_two_level<4>(m, o, cb0, s)) ||
                   (m->dim == 8 && transpose_two_level<8>(m, o, cb0, s))))
             return o;
-        Buf<uint32_t> cnt(ntr, s);
-        Buf<uint64_t> ofs((size_t)ntr + 1, s);
-        CK(cudaMemsetAsync(cnt.p, 0, (size_t)ntr * 4, s));
-        if (T) LAUNCH(k_col_hist, grid_for(T), 256, 0, s, T, m->tci, cnt.p);
-        exclusive_scan_u32_to_u64(cnt.p, ofs.p, ntr, s);
-        LAUNCH(k_u64_to_u32, grid_for(ntr + 1), 256, 0, s, ofs.p, o->trp, (size_t)ntr + 1);
-        const int cb = bits_for(ntr - 1);
-        if (T && m->dim == 4 && 2 * cb + 16 <= 64) {
+        const int cb = cb0;
+        if (!T) {
+            CK(cudaMemsetAsync(o->trp, 0, ((size_t)ntr + 1) * 4, s));
+        } else if (m->dim == 4 && 2 * cb + 16 <= 64) {
             Buf<uint64_t> keys(T, s), kalt;
             {
                 Buf<uint32_t> rowid(T, s);
@@ -505,14 +519,15 @@ b2sr_matrix *transpose_device(const b2sr_matrix *m, cudaStream_t s) {
             }
             uint64_t *ks = nullptr;
             radix_sort_keys_u64(keys.p, T, cb, s, &ks, &kalt);
-            LAUNCH(k_unpack4, grid_for(T), 256, 0, s, T, ks, cb, o->tci, (uint32_t *)o->tiles);
-        } else if (T) {
+            LAUNCH(k_unpack4, grid_for(T), 256, 0, s, T, ks, cb, ntr, o->trp, o->tci, (uint32_t *)o->tiles);
+        } else {
             Buf<uint32_t> keys(T, s), vals(T, s), rowid(T, s), kalt, valt;
             CK(cudaMemcpyAsync(keys.p, m->tci, T * 4, cudaMemcpyDeviceToDevice, s));
             LAUNCH(k_iota, grid_for(T), 256, 0, s, vals.p, T);
             LAUNCH(k_row_ids, grid_for((uint64_t)ntr * 32), 256, 0, s, ntr, m->trp, rowid.p);
             uint32_t *ks = nullptr, *vs = nullptr;
             radix_sort_pairs_u32(keys.p, vals.p, T, bits_for(ntr - 1), s, &ks, &vs, &kalt, &valt);
+            LAUNCH(k_trp_sorted, grid_for(T), 256, 0, s, T, ks, ntr, o->trp);
             unsigned g = grid_for(T);
             switch (m->dim) {
                 case 4: LAUNCH(k_transpose_gather<4>, g, 256, 0, s, T, vs, rowid.p, m->tiles, o->tci, o->tiles); break;
