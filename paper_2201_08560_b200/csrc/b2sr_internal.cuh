@@ -158,6 +158,7 @@ struct b2sr_matrix {
     void *stream = nullptr;           // flat tile-stream row hints (bmv_stream.cu)
     void *bff = nullptr;              // float-gather row order (bmv_bff.cu)
     void *xperm = nullptr;            // hot-first x relabelling for the float gather (bmv_xperm.cu)
+    void *csrplan = nullptr;          // CSR column lists for the wide-tile float gather (bmv_csr.cu)
 };
 
 namespace b2sr {
@@ -217,6 +218,11 @@ void free_stream(void *plan);
 void launch_bff_rows(b2sr_matrix *m, const double *x, int ring, double inc, double ident, const void *keep, double *y,
                      uint32_t thresh, cudaStream_t s, bool plan_only = false, const uint32_t *gtci = nullptr);
 void free_bff(void *plan);
+// bmv_csr.cu: the float gather at d = 16/32 over the matrix's cached CSR form
+bool bff_csr_enabled(const b2sr_matrix *m);
+void launch_bff_csr(b2sr_matrix *m, const double *x, int ring, double inc, double ident, const void *keep, double *y,
+                    cudaStream_t s);
+void free_csrplan(void *plan);
 // bmv_xperm.cu: hot-first relabelling of x for the float gather
 bool xperm_enabled(const b2sr_matrix *m);
 const uint32_t *xperm_apply(b2sr_matrix *m, const double *x, double *xp, cudaStream_t s);

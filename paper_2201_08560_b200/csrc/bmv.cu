@@ -430,20 +430,25 @@ __global__ void k_fix_negzero(uint32_t n, const uint32_t *__restrict__ trp, cons
 void launch_bff(const b2sr_matrix *m_, const double *x, int ring, double inc, const void *keep, double *y,
                 cudaStream_t s, double ident) {
     b2sr_matrix *m = const_cast<b2sr_matrix *>(m_);
-    ensure_vlong(m, s);
-    const uint32_t hi = vlong_thresh(m->dim);
-    launch_bff_rows(m, x, ring, inc, ident, keep, y, hi, s, /*plan_only=*/true);
-    // large x: gather from a hot-first relabelled copy (bmv_xperm.cu)
-    Buf<double> xp;
-    const uint32_t *gtci = nullptr;
-    if (xperm_enabled(m)) {
-        const size_t xbytes = (size_t)tile_rows(m->n, m->dim) * m->dim * sizeof(double);
-        xp = Buf<double>(xbytes / sizeof(double), s);
-        gtci = xperm_apply(m, x, xp.p, s);
-        x = xp.p;
+    if (bff_csr_enabled(m)) {  // wide tiles: the cached CSR column lists (bmv_csr.cu)
+        launch_bff_csr(m, x, ring, inc, ident, keep, y, s);
+    } else {
+        ensure_vlong(m, s);
+        const uint32_t hi = vlong_thresh(m->dim);
+        launch_bff_rows(m, x, ring, inc, ident, keep, y, hi, s, /*plan_only=*/true);
+        // large x: gather from a hot-first relabelled copy (bmv_xperm.cu)
+        Buf<double> xp;
+        const uint32_t *gtci = nullptr;
+        if (xperm_enabled(m)) {
+            const size_t xbytes = (size_t)tile_rows(m->n, m->dim) * m->dim * sizeof(double);
+            xp = Buf<double>(xbytes / sizeof(double), s);
+            gtci = xperm_apply(m, x, xp.p, s);
+            x = xp.p;
+        }
+        launch_vlong(m, x, ring, inc, ident, keep, y, s,
+                     [&](cudaStream_t so) { launch_bff_rows(m, x, ring, inc, ident, keep, y, hi, so, false, gtci); },
+                     gtci);
     }
-    launch_vlong(m, x, ring, inc, ident, keep, y, s,
-                 [&](cudaStream_t so) { launch_bff_rows(m, x, ring, inc, ident, keep, y, hi, so, false, gtci); }, gtci);
     if (ring == B2SR_RING_ARITHMETIC && ident == 0.0 && std::signbit(ident) && m->ntr) {
         unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)m->ntr * m->dim + 255) / 256,
                                                                           (uint64_t)num_sms() * 8));

@@ -118,6 +118,14 @@ struct XHot {
             }
             return v;
         }
+        if constexpr (sizeof(typename WordT<D>::T) == 1) {
+            // cold column: one IMAD.WIDE (xm + c) and the load -- the plain
+            // expression compiled to c - S, then a 64-bit add of x (4 instructions)
+            unsigned long long a;
+            asm("mad.wide.u32 %0, %1, 1, %2;" : "=l"(a) : "r"(c), "l"(reinterpret_cast<unsigned long long>(xm)));
+            asm("ld.global.nc.u8 %0, [%1];" : "=r"(v) : "l"(a));
+            return v;
+        }
         return (uint32_t)__ldg(xm + c);
     }
 };

@@ -126,6 +126,7 @@ void free_matrix(b2sr_matrix *m) {
     free_stream(m->stream);
     free_bff(m->bff);
     free_xperm(m->xperm);
+    free_csrplan(m->csrplan);
     if (cur != m->device) cudaSetDevice(cur);
     delete m;
 }
