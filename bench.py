@@ -98,6 +98,7 @@ class Clocks:
             idx = torch.cuda._get_nvml_device_index(self.cuda_index)
             self.nv, self.h = pynvml, pynvml.nvmlDeviceGetHandleByIndex(idx)
             self.max = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self._sample()  # at the start of the region, whatever the thread's scheduling
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         except Exception:
@@ -128,6 +129,11 @@ class Clocks:
             time.sleep(0.002)
 
     def __exit__(self, *a):
+        if self.t:
+            try:
+                self._sample()  # and at its end
+            except Exception as e:
+                self.errors.add(type(e).__name__)
         self._stop.set()
         if self.t:
             self.t.join(timeout=2)

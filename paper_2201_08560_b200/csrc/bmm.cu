@@ -102,9 +102,11 @@ __global__ void k_tc_item_counts(uint64_t TM, const uint32_t *__restrict__ m_row
         uint32_t i = m_rowid[mt], I = i + m_row0, J = m_tci[mt];
         uint32_t la = a_trp[I + 1] - a_trp[I], lb = b_trp[J + 1] - b_trp[J];
         uint32_t sh = min(la, lb);
-        // pairs the filter kernel takes get no items here: staged on row I
-        // (non-SYM), or on the longer of rows I and J (SYM)
-        const uint32_t X = sym && lb > la ? J - m_row0 : i;
+        // pairs the filter kernel takes get no items here: staged on mask row i
+        // (non-SYM, elig per mask row), or on the longer of rows I and J (SYM,
+        // elig per global row: with a mask row block the pair may belong to the
+        // rank that owns row J)
+        const uint32_t X = sym ? (lb > la ? J : I) : i;
         const bool filtered = elig && elig[X] != 0;
         cnt[mt] = la && lb && !filtered ? (sh + chunk - 1) / chunk : 0;
     }
@@ -504,6 +506,14 @@ __global__ void k_tcf_chunks(uint32_t mntr, uint32_t m_row0, const uint32_t *__r
     }
 }
 
+// SYM: a row can be staged iff 0 < len <= CAP (per global row)
+__global__ void k_tcf_elig_global(uint32_t ntr, const uint32_t *__restrict__ a_trp, uint8_t *__restrict__ elig) {
+    for (uint32_t I = blockIdx.x * blockDim.x + threadIdx.x; I < ntr; I += gridDim.x * blockDim.x) {
+        const uint32_t la = a_trp[I + 1] - a_trp[I];
+        elig[I] = la > 0 && la <= TCB_CAP;
+    }
+}
+
 __global__ void k_tcf_chunk_list(uint32_t mntr, const uint32_t *__restrict__ nch, const uint64_t *__restrict__ ofs,
                                  uint2 *__restrict__ chunks) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mntr; i += gridDim.x * blockDim.x)
@@ -592,8 +602,13 @@ int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_ma
             if (n_fitems) LAUNCH(k_tcf_fill, grid_for(nchunks), 256, 0, s, nchunks, chunks.p, pc.p, pofs.p, fitems.p);
         }
     }
+    Buf<uint8_t> elig_g;
+    if (sym) {
+        elig_g = Buf<uint8_t>(std::max<uint32_t>(a->ntr, 1), s);
+        LAUNCH(k_tcf_elig_global, grid_for(a->ntr), 256, 0, s, a->ntr, a->trp, elig_g.p);
+    }
     LAUNCH(k_tc_item_counts, grid_for(TM), 256, 0, s, TM, rowid.p, mask->tci, mask->row0, a->trp, bt->trp, chunk, cnt.p,
-           filtered ? elig.p : nullptr, sym);
+           sym ? elig_g.p : (filtered ? elig.p : nullptr), sym);
     exclusive_scan_u32_to_u64(cnt.p, ofs.p, TM, s);
     uint64_t n_items = read_scalar(ofs.p + TM, s);
     Buf<unsigned long long> out(1, s);
@@ -744,6 +759,22 @@ __global__ void k_tc_row_work(uint32_t ntr, const uint32_t *__restrict__ trp, co
     }
 }
 
+// SYM triangle counting: pair (I, J) costs its shorter row and is counted by the
+// owner of the longer row X when X can be staged, else by the owner of I
+__global__ void k_tc_row_work_sym(uint32_t ntr, const uint32_t *__restrict__ trp, const uint32_t *__restrict__ tci,
+                                  unsigned long long *__restrict__ work) {
+    const uint32_t lane = lane_id(), warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t I = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; I < ntr; I += warps) {
+        const uint32_t t0 = trp[I], t1 = trp[I + 1], li = t1 - t0;
+        for (uint32_t t = t0 + lane; t < t1; t += 32) {
+            const uint32_t J = tci[t], lj = trp[J + 1] - trp[J];
+            const uint32_t X = lj > li ? J : I, lx = lj > li ? lj : li;
+            const uint32_t owner = (lx > 0 && lx <= TCB_CAP) ? X : I;
+            atomicAdd(work + owner, (unsigned long long)(li < lj ? li : lj) + 1ull);
+        }
+    }
+}
+
 __global__ void k_work_cuts(const uint64_t *__restrict__ pre, uint32_t ntr, int world, uint32_t *__restrict__ cuts) {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k > world) return;
@@ -778,7 +809,10 @@ extern "C" int b2sr_dist_tc(b2sr_comm *comm, const b2sr_matrix *lower, int64_t *
     Buf<uint64_t> pre(ntr + 1, s);
     Buf<uint32_t> cuts(W + 1, s);
     CK(cudaMemsetAsync(work.p, 0, 8 * ((size_t)ntr + 1), s));
-    LAUNCH(k_tc_row_work, grid_for((uint64_t)ntr * 32), 256, 0, s, ntr, lower->trp, lower->tci, work.p);
+    const char *se = getenv("B2SR_TC_SYM");
+    const bool sym = tc_filter_enabled(lower->dim) && !(se && se[0] == '0') && lower->num_tiles;
+    if (sym) LAUNCH(k_tc_row_work_sym, grid_for((uint64_t)ntr * 32), 256, 0, s, ntr, lower->trp, lower->tci, work.p);
+    else LAUNCH(k_tc_row_work, grid_for((uint64_t)ntr * 32), 256, 0, s, ntr, lower->trp, lower->tci, work.p);
     exclusive_scan_u64(reinterpret_cast<const uint64_t *>(work.p), pre.p, (size_t)ntr + 1, s);
     LAUNCH(k_work_cuts, 1, 64 * ((W + 64) / 64), 0, s, pre.p, ntr, W, cuts.p);
     std::vector<uint32_t> rows(W + 1);
@@ -789,13 +823,17 @@ extern "C" int b2sr_dist_tc(b2sr_comm *comm, const b2sr_matrix *lower, int64_t *
     int rc = b2sr_row_block(lower, rows[R], rows[R + 1], s, &blk);
     if (rc) throw Error{rc, std::string()};
     int64_t mine = 0;
+    b2sr_matrix *lt = nullptr;  // SYM: L^T replicated, each pair counted by the owner of its staged row
     try {
-        mine = bmm_masked_bt(lower, lower, blk, s);
+        if (sym) lt = transpose_device(lower, s);
+        mine = bmm_masked_bt(lower, lower, blk, s, nullptr, lt);
     } catch (...) {
         free_matrix(blk);
+        free_matrix(lt);
         throw;
     }
     free_matrix(blk);
+    free_matrix(lt);
     Buf<int64_t> tot(1, s);
     CK(cudaMemcpyAsync(tot.p, &mine, 8, cudaMemcpyHostToDevice, s));
     ex->allreduce_sum_i64(tot.p, 1, s);

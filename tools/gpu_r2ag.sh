@@ -1,0 +1,5 @@
+set -x
+timeout -s KILL 600 python -m pytest tests/test_gpu_configs.py -q -x -p no:cacheprovider -k "config0" 2>&1 | tail -1
+timeout -s KILL 120 python tools/bff_probe.py --scale 16 --dim 32 --reps 3 --check
+timeout -s KILL 120 python tools/bff_probe.py --scale 16 --dim 16 --reps 3
+timeout -s KILL 120 python tools/bff_probe.py --scale 20 --dim 32 --reps 2
