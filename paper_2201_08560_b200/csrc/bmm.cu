@@ -287,6 +287,36 @@ __device__ __forceinline__ void tc_resolve(uint32_t t, const uint32_t *__restric
     }
 }
 
+// SYM: a staged row longer than TCB_CAP is cut into R column ranges of
+// <= TCB_CAP of its own entries, range r covering columns [c_r, c_{r+1}) with
+// c_r = the column of its entry r*CAP (c_0 = 0, c_R = infinity); a partner row
+// is streamed against range r only over its entries in those columns (two
+// binary searches of the sorted partner row), so every common column is met
+// in exactly one range and no row needs the binary-search items.
+__device__ __forceinline__ uint32_t tcf_ranges(uint32_t la) { return la ? (la + TCB_CAP - 1) / TCB_CAP : 0u; }
+
+__device__ __forceinline__ uint32_t tcf_lower(const uint32_t *__restrict__ v, uint32_t lo, uint32_t hi, uint32_t key) {
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(v + mid) < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+// the part of partner row [b0, b0 + lb) of Bt inside the columns of range r of
+// staged row a0.. (la entries, R ranges)
+__device__ __forceinline__ void tcf_restrict(const uint32_t *__restrict__ a_tci, uint32_t a0, uint32_t la,
+                                             uint32_t R, uint32_t r, const uint32_t *__restrict__ b_tci,
+                                             uint32_t &b0, uint32_t &lb) {
+    if (R <= 1) return;
+    const uint32_t b1 = b0 + lb;
+    const uint32_t lo = r ? tcf_lower(b_tci, b0, b1, __ldg(a_tci + a0 + r * TCB_CAP)) : b0;
+    const uint32_t hi = r + 1 < R ? tcf_lower(b_tci, lo, b1, __ldg(a_tci + a0 + (r + 1) * TCB_CAP)) : b1;
+    b0 = lo;
+    lb = hi - lo;
+    (void)la;
+}
+
 // Work item {X, chunk, part, parts}: staged row X of A; its partners are
 // positions [chunk * CAP, +CAP) of the concatenation (mask row X) ++ (row X
 // of the mask's transpose MT, SYM only), and the item probes part `part` of
@@ -299,7 +329,7 @@ __device__ __forceinline__ void tc_resolve(uint32_t t, const uint32_t *__restric
 //     sum_{(c,r) in M^T} popc(L_X[c] & A_I[r])): sum over pairs of the SHORTER
 //     row (s20 d=4: 2.48 G probes instead of 5.0 G); excluded partners keep
 //     their slot with no probes.
-template <int D, bool SYM>
+template <int D, bool SYM, bool RANGED>
 __global__ void __launch_bounds__(TCB_THREADS, 6) k_tc_filter(
     uint32_t m_row0, const uint32_t *__restrict__ m_trp, const uint32_t *__restrict__ m_tci,
     const typename WordT<D>::T *__restrict__ m_tiles, const uint32_t *__restrict__ mt_trp,
@@ -342,8 +372,11 @@ __global__ void __launch_bounds__(TCB_THREADS, 6) k_tc_filter(
         __syncthreads();  // also orders the previous item's filter clear before this item's staging
         const uint4 it = s_item;
         if (it.x == 0xFFFFFFFFu) break;
-        const uint32_t i = it.x, chunk = it.y, part = it.z, parts = it.w;
-        const uint32_t I = m_row0 + i, a0 = __ldg(a_trp + I), la = __ldg(a_trp + I + 1) - a0;
+        const uint32_t i = it.x, chunk = it.y & 0xFFFFu, rng = it.y >> 16, part = it.z, parts = it.w;
+        const uint32_t I = m_row0 + i, a0f = __ldg(a_trp + I), laf = __ldg(a_trp + I + 1) - a0f;
+        const uint32_t R = RANGED ? tcf_ranges(laf) : 1u;  // RANGED: the rows over TCB_CAP entries
+        // this item's range of the staged row (SYM rows over TCB_CAP entries)
+        const uint32_t a0 = a0f + rng * TCB_CAP, la = min(TCB_CAP, laf - rng * TCB_CAP);
         const uint32_t m0 = __ldg(m_trp + i), nL = __ldg(m_trp + i + 1) - m0;
         uint32_t t0 = 0, nT = 0;
         if constexpr (SYM) {
@@ -376,8 +409,10 @@ __global__ void __launch_bounds__(TCB_THREADS, 6) k_tc_filter(
                     J = __ldg(mt_tci + t0 + (g - nL));
                     mtile[q] = tile_bits<D>(mt_tiles, (size_t)t0 + (g - nL));
                 }
-                const uint32_t b0 = __ldg(b_trp + J), lb = __ldg(b_trp + J + 1) - b0;
-                const uint32_t kept = (SYM && (second ? lb >= la : lb > la)) ? 0u : lb;  // else staged on row J
+                uint32_t b0 = __ldg(b_trp + J), lb = __ldg(b_trp + J + 1) - b0;
+                const bool keep_pair = !(SYM && (second ? lb >= laf : lb > laf));  // else staged on row J
+                if (RANGED && keep_pair) tcf_restrict(a_tci, a0f, laf, R, rng, b_tci, b0, lb);
+                const uint32_t kept = keep_pair ? lb : 0u;
                 jst[q] = b0;
                 jln[q] = kept;
                 len[k] = (kept + 31) >> 5;  // 32-entry chunks
@@ -500,49 +535,61 @@ __global__ void k_tcf_chunks(uint32_t mntr, uint32_t m_row0, const uint32_t *__r
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mntr; i += gridDim.x * blockDim.x) {
         const uint32_t I = m_row0 + i, la = a_trp[I + 1] - a_trp[I];
         const uint32_t np = (m_trp[i + 1] - m_trp[i]) + (mt_trp ? mt_trp[I + 1] - mt_trp[I] : 0u);
-        const bool ok = la > 0 && la <= TCB_CAP && (mt_trp || np <= TCB_CAP);
+        // SYM: any non-empty row (long rows in column ranges); else <= CAP and <= CAP partners
+        const bool ok = la > 0 && (mt_trp || (la <= TCB_CAP && np <= TCB_CAP));
         elig[i] = ok;
-        nch[i] = ok ? (np + TCB_CAP - 1) / TCB_CAP : 0u;
+        const uint32_t R = mt_trp ? tcf_ranges(la) : 1u;
+        nch[i] = ok ? R * ((np + TCB_CAP - 1) / TCB_CAP) : 0u;
     }
 }
 
-// SYM: a row can be staged iff 0 < len <= CAP (per global row)
+// SYM: a row can be staged iff it is not empty (per global row)
 __global__ void k_tcf_elig_global(uint32_t ntr, const uint32_t *__restrict__ a_trp, uint8_t *__restrict__ elig) {
     for (uint32_t I = blockIdx.x * blockDim.x + threadIdx.x; I < ntr; I += gridDim.x * blockDim.x) {
-        const uint32_t la = a_trp[I + 1] - a_trp[I];
-        elig[I] = la > 0 && la <= TCB_CAP;
+        elig[I] = a_trp[I + 1] > a_trp[I];  // every non-empty row can be staged (column ranges)
     }
 }
 
 __global__ void k_tcf_chunk_list(uint32_t mntr, const uint32_t *__restrict__ nch, const uint64_t *__restrict__ ofs,
                                  uint2 *__restrict__ chunks) {
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < mntr; i += gridDim.x * blockDim.x)
-        for (uint32_t c = 0; c < nch[i]; c++) chunks[ofs[i] + c] = make_uint2(i, c);
+        for (uint32_t c = 0; c < nch[i]; c++) chunks[ofs[i] + c] = make_uint2(i, c);  // c = range * npc + chunk
 }
 
 // warp per chunk: probes = sum of the streamed lengths of its kept partners
-__global__ void k_tcf_parts(uint32_t nchunks, const uint2 *__restrict__ chunks, uint32_t m_row0,
+__global__ void k_tcf_parts(uint32_t nchunks, uint2 *__restrict__ chunks, uint32_t m_row0,
                             const uint32_t *__restrict__ m_trp, const uint32_t *__restrict__ m_tci,
                             const uint32_t *__restrict__ mt_trp, const uint32_t *__restrict__ mt_tci,
-                            const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ b_trp, uint32_t budget,
-                            uint32_t *__restrict__ parts) {
+                            const uint32_t *__restrict__ a_trp, const uint32_t *__restrict__ a_tci,
+                            const uint32_t *__restrict__ b_trp, const uint32_t *__restrict__ b_tci, uint32_t budget,
+                            uint32_t *__restrict__ parts, uint32_t *__restrict__ parts_ranged) {
     const uint32_t lane = lane_id(), warps = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nchunks; c += warps) {
         const uint2 ch = chunks[c];
-        const uint32_t i = ch.x, I = m_row0 + i, la = a_trp[I + 1] - a_trp[I];
+        const uint32_t i = ch.x, I = m_row0 + i, a0 = a_trp[I], la = a_trp[I + 1] - a0;
         const uint32_t m0 = m_trp[i], nL = m_trp[i + 1] - m0;
         const uint32_t t0 = mt_trp ? mt_trp[I] : 0u, nT = mt_trp ? mt_trp[I + 1] - t0 : 0u;
-        const uint32_t g0 = ch.y * TCB_CAP, g1 = min(g0 + TCB_CAP, nL + nT);
+        const uint32_t npc = (nL + nT + TCB_CAP - 1) / TCB_CAP, R = mt_trp ? tcf_ranges(la) : 1u;
+        const uint32_t rng = ch.y / npc, pc = ch.y % npc;
+        const uint32_t g0 = pc * TCB_CAP, g1 = min(g0 + TCB_CAP, nL + nT);
         unsigned long long w = 0;
         for (uint32_t g = g0 + lane; g < g1; g += 32) {
             const bool second = g >= nL;
             const uint32_t J = second ? mt_tci[t0 + (g - nL)] : m_tci[m0 + g];
-            const uint32_t lb = b_trp[J + 1] - b_trp[J];
-            if (!mt_trp || (second ? lb < la : lb <= la)) w += (lb + 31) / 32;  // 32-entry chunks
+            uint32_t b0 = b_trp[J], lb = b_trp[J + 1] - b0;
+            if (!mt_trp || (second ? lb < la : lb <= la)) {
+                if (mt_trp) tcf_restrict(a_tci, a0, la, R, rng, b_tci, b0, lb);
+                w += (lb + 31) / 32;  // 32-entry chunks
+            }
         }
         for (int o = 16; o; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
         const unsigned long long q = (w + budget - 1) / budget;  // budget: chunks per item
-        if (lane == 0) parts[c] = (q == 0 || w >= 0x80000000ull) ? 0u : (q > 0xFFFFull ? 0xFFFFu : (uint32_t)q);
+        if (lane == 0) {
+            const uint32_t P = (q == 0 || w >= 0x80000000ull) ? 0u : (q > 0xFFFFull ? 0xFFFFu : (uint32_t)q);
+            parts[c] = R > 1 ? 0u : P;         // items of the plain kernel
+            parts_ranged[c] = R > 1 ? P : 0u;  // items of the column-range kernel
+            chunks[c].y = (rng << 16) | pc;    // what the filter kernel's items carry
+        }
     }
 }
 
@@ -573,9 +620,9 @@ int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_ma
     const uint32_t chunk = ce ? std::max(32, atoi(ce)) : TC_CHUNK;
     const bool filtered = tc_filter_enabled(a->dim);
     const bool sym = filtered && mt != nullptr;
-    Buf<uint4> fitems;
+    Buf<uint4> fitems;  // plain items, then the column-range items (SYM rows over TCB_CAP)
     Buf<uint8_t> elig;
-    uint32_t n_fitems = 0;
+    uint32_t n_fitems = 0, n_ritems = 0;
     if (filtered) {
         // work items of the filter kernel, handed out dynamically
         const char *be = getenv("B2SR_TC_BUDGET");
@@ -591,15 +638,20 @@ int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_ma
         const uint32_t nchunks = (uint32_t)read_scalar(cofs.p + mntr, s);
         if (nchunks) {
             Buf<uint2> chunks(nchunks, s);
-            Buf<uint32_t> pc(nchunks, s);
-            Buf<uint64_t> pofs((size_t)nchunks + 1, s);
+            Buf<uint32_t> pc(nchunks, s), pcr(nchunks, s);
+            Buf<uint64_t> pofs((size_t)nchunks + 1, s), rofs((size_t)nchunks + 1, s);
             LAUNCH(k_tcf_chunk_list, grid_for(mntr), 256, 0, s, mntr, nch.p, cofs.p, chunks.p);
             LAUNCH(k_tcf_parts, grid_for((uint64_t)nchunks * 32), 256, 0, s, nchunks, chunks.p, mask->row0, mask->trp,
-                   mask->tci, sym ? mt->trp : nullptr, sym ? mt->tci : nullptr, a->trp, bt->trp, budget, pc.p);
+                   mask->tci, sym ? mt->trp : nullptr, sym ? mt->tci : nullptr, a->trp, a->tci, bt->trp, bt->tci,
+                   budget, pc.p, pcr.p);
             exclusive_scan_u32_to_u64(pc.p, pofs.p, nchunks, s);
+            exclusive_scan_u32_to_u64(pcr.p, rofs.p, nchunks, s);
             n_fitems = (uint32_t)read_scalar(pofs.p + nchunks, s);
-            fitems = Buf<uint4>(std::max<uint32_t>(n_fitems, 1), s);
+            n_ritems = (uint32_t)read_scalar(rofs.p + nchunks, s);
+            fitems = Buf<uint4>(std::max<uint32_t>(n_fitems + n_ritems, 1), s);
             if (n_fitems) LAUNCH(k_tcf_fill, grid_for(nchunks), 256, 0, s, nchunks, chunks.p, pc.p, pofs.p, fitems.p);
+            if (n_ritems)
+                LAUNCH(k_tcf_fill, grid_for(nchunks), 256, 0, s, nchunks, chunks.p, pcr.p, rofs.p, fitems.p + n_fitems);
         }
     }
     Buf<uint8_t> elig_g;
@@ -622,27 +674,35 @@ int64_t bmm_masked_bt(const b2sr_matrix *a, const b2sr_matrix *bt, const b2sr_ma
     Buf<uint32_t> next_row(1, s);
     CK(cudaMemsetAsync(next_row.p, 0, 4, s));
     kernel_timer().begin(s);
-    if (n_fitems) {
+    if (n_fitems || n_ritems) {
         int per_sm = 1;
         const uint32_t *mtp = sym ? mt->trp : nullptr, *mtc = sym ? mt->tci : nullptr;
         const void *mtt = sym ? mt->tiles : nullptr;
         uint32_t ksh = 0;  // column bucket shift: (ntr - 1) >> ksh < TCB_NB
         while (((uint64_t)(a->ntr ? a->ntr - 1 : 0) >> ksh) >= TCB_NB) ksh++;
-        switch (a->dim * 2 + (sym ? 1 : 0)) {
-#define TCB_CASE(DD, SY, W)                                                                                          \
-    case DD * 2 + SY:                                                                                                \
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_filter<DD, SY>, TCB_THREADS, 0));             \
-        LAUNCH((k_tc_filter<DD, SY>),                                                                                \
-               (unsigned)std::min<uint64_t>((uint64_t)num_sms() * std::max(per_sm, 1), n_fitems), TCB_THREADS, 0,    \
-               s, mask->row0, mask->trp, mask->tci, (const W *)mask->tiles, mtp, mtc, (const W *)mtt, a->trp, a->tci, \
-               (const W *)a->tiles, bt->trp, bt->tci, (const W *)bt->tiles, fitems.p, n_fitems, next_row.p, out.p,  \
+        for (int ranged = 0; ranged < 2; ranged++) {
+            const uint32_t ni = ranged ? n_ritems : n_fitems;
+            const uint4 *its = fitems.p + (ranged ? n_fitems : 0);
+            if (!ni) continue;
+            CK(cudaMemsetAsync(next_row.p, 0, 4, s));
+            switch (a->dim * 4 + (sym ? 2 : 0) + ranged) {
+#define TCB_CASE(DD, SY, RG, W)                                                                                      \
+    case DD * 4 + SY * 2 + RG:                                                                                       \
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tc_filter<DD, SY, RG>, TCB_THREADS, 0));         \
+        LAUNCH((k_tc_filter<DD, SY, RG>),                                                                            \
+               (unsigned)std::min<uint64_t>((uint64_t)num_sms() * std::max(per_sm, 1), ni), TCB_THREADS, 0, s,       \
+               mask->row0, mask->trp, mask->tci, (const W *)mask->tiles, mtp, mtc, (const W *)mtt, a->trp, a->tci,   \
+               (const W *)a->tiles, bt->trp, bt->tci, (const W *)bt->tiles, its, ni, next_row.p, out.p,             \
                work_out ? work.p : nullptr, ksh);                                                                     \
         break;
-            TCB_CASE(4, 0, uint8_t)
-            TCB_CASE(4, 1, uint8_t)
-            TCB_CASE(8, 0, uint8_t)
-            TCB_CASE(8, 1, uint8_t)
+                TCB_CASE(4, 0, 0, uint8_t)
+                TCB_CASE(4, 1, 0, uint8_t)
+                TCB_CASE(4, 1, 1, uint8_t)
+                TCB_CASE(8, 0, 0, uint8_t)
+                TCB_CASE(8, 1, 0, uint8_t)
+                TCB_CASE(8, 1, 1, uint8_t)
 #undef TCB_CASE
+            }
         }
     }
     if (n_items) switch (a->dim) {
@@ -760,7 +820,7 @@ __global__ void k_tc_row_work(uint32_t ntr, const uint32_t *__restrict__ trp, co
 }
 
 // SYM triangle counting: pair (I, J) costs its shorter row and is counted by the
-// owner of the longer row X when X can be staged, else by the owner of I
+// owner of the longer row X
 __global__ void k_tc_row_work_sym(uint32_t ntr, const uint32_t *__restrict__ trp, const uint32_t *__restrict__ tci,
                                   unsigned long long *__restrict__ work) {
     const uint32_t lane = lane_id(), warps = (gridDim.x * blockDim.x) >> 5;
@@ -768,9 +828,8 @@ __global__ void k_tc_row_work_sym(uint32_t ntr, const uint32_t *__restrict__ trp
         const uint32_t t0 = trp[I], t1 = trp[I + 1], li = t1 - t0;
         for (uint32_t t = t0 + lane; t < t1; t += 32) {
             const uint32_t J = tci[t], lj = trp[J + 1] - trp[J];
-            const uint32_t X = lj > li ? J : I, lx = lj > li ? lj : li;
-            const uint32_t owner = (lx > 0 && lx <= TCB_CAP) ? X : I;
-            atomicAdd(work + owner, (unsigned long long)(li < lj ? li : lj) + 1ull);
+            const uint32_t X = lj > li ? J : I;  // every non-empty row can be staged
+            atomicAdd(work + X, (unsigned long long)(li < lj ? li : lj) + 1ull);
         }
     }
 }

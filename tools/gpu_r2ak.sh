@@ -1,0 +1,6 @@
+set -x
+O=gpurun_out
+timeout -s KILL 600 python -m pytest tests/test_gpu_dist_native.py tests/test_gpu_parity.py -q -x -p no:cacheprovider -k "tc or triangle or masked_spgemm or bmm or algorithms" 2>&1 | tail -1
+timeout -s KILL 300 python tools/tc_ab.py 20 4,8
+timeout -s KILL 600 python tools/tc_ab.py 26 4
+timeout -s KILL 900 python -m pytest tests/test_gpu_configs.py -q -x -p no:cacheprovider -k "triangle" 2>&1 | tail -1
