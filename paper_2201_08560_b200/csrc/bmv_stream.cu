@@ -406,6 +406,20 @@ __device__ __forceinline__ void push_entries(uint32_t n_entries, const uint2 *__
     }
 }
 
+// The three pull variants of the fused level kernel, each compiled out of line:
+// inlined into one kernel body under the 64-register cap of a 1024-thread CTA
+// they spilled (20 B per thread); as separate callees each gets the whole
+// register budget.
+template <int D, bool LIST, bool LAZY>
+__device__ __noinline__ void bfs_pull(uint32_t p0, uint32_t p1, uint32_t n_loads, uint64_t T,
+                                      const uint32_t *__restrict__ list, const uint4 *__restrict__ desc,
+                                      const uint32_t *__restrict__ trp, const uint8_t *__restrict__ tiles,
+                                      const uint32_t *__restrict__ tci2, const void *__restrict__ x, uint32_t S,
+                                      void *__restrict__ y) {
+    XHot<D> gx(x, S);
+    bbb_stream<D, LIST, XHot<D>, LAZY>(p0, p1, n_loads, T, list, desc, trp, tiles, tci2, gx, y);
+}
+
 // One BFS level in one launch: the direction chosen by the device-side plan
 // (BfsCtl::mode) selects the push body, the full flat-stream pull, or the
 // stream over the listed active loads.
@@ -429,13 +443,12 @@ __global__ void __launch_bounds__(NT, 1)
     if (n_pos == 0) return;
     stage_hot(const_cast<uint8_t *>(hot_bytes()), hx, hx_bytes16);
     __syncthreads();
-    XHot<D> gx(frontier, S);
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5, w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t per = (n_pos + warps - 1) / warps;
     const uint32_t p0 = std::min(n_pos, w * per), p1 = std::min(n_pos, p0 + per);
-    if (listed) bbb_stream<D, true>(p0, p1, n_loads, T, alist, desc, trp, tiles, tci2, gx, next);
-    else if (ctl->sparse) bbb_stream<D, false, XHot<D>, true>(p0, p1, n_loads, T, nullptr, desc, trp, tiles, tci2, gx, next);
-    else bbb_stream<D, false>(p0, p1, n_loads, T, nullptr, desc, trp, tiles, tci2, gx, next);
+    if (listed) bfs_pull<D, true, false>(p0, p1, n_loads, T, alist, desc, trp, tiles, tci2, frontier, S, next);
+    else if (ctl->sparse) bfs_pull<D, false, true>(p0, p1, n_loads, T, nullptr, desc, trp, tiles, tci2, frontier, S, next);
+    else bfs_pull<D, false, false>(p0, p1, n_loads, T, nullptr, desc, trp, tiles, tci2, frontier, S, next);
 }
 
 // Push-only level (BFS without a transpose): every level top-down over a.
