@@ -93,13 +93,72 @@ bool page_locked(const void *p) {
 // T-th chunk of the whole list, so several arrays stream without a join
 // between them.  kind COPY: memcpy; kind PACK4: d = 4 bit tiles, four row
 // bytes -> 16 bits (only the low nibbles may be set, formats.py:289).
-enum { COPY = 0, PACK4 = 1 };
+enum { COPY = 0, PACK4 = 1, PACKB = 2 };
 struct Job {
     void *dst;
     const void *src;
     size_t bytes;  // source bytes
     int kind;
+    int bits = 0;  // PACKB: bits per u32 value (the column range of tile_col_ind)
 };
+
+// PACKB: n u32 values (n a multiple of 32, or the tail) packed at `bits` bits
+// each: group g of 32 values -> words [g*bits, (g+1)*bits).  Returns the OR of
+// the values' bits above `bits` (non-zero: a value does not fit -- the caller
+// re-sends plainly so the device check reports it).
+template <int BITS>
+static uint32_t pack_bits_t(const uint32_t *in, size_t n, uint32_t *out) {
+    constexpr uint32_t LIM = BITS == 32 ? 0u : ~0u << BITS;
+    uint32_t over = 0;
+    size_t g = 0;
+    for (; g + 32 <= n; g += 32) {  // whole groups: every shift is a constant
+        const uint32_t *v = in + g;
+        uint32_t *o = out + (g / 32) * BITS;
+        uint64_t acc = 0;
+        int fill = 0, w = 0;
+        for (int k = 0; k < 32; k++) {
+            over |= v[k] & LIM;
+            acc |= (uint64_t)v[k] << fill;
+            fill += BITS;
+            if (fill >= 32) {
+                o[w++] = (uint32_t)acc;
+                acc >>= 32;
+                fill -= 32;
+            }
+        }
+    }
+    if (g < n) {  // the tail group
+        uint32_t *o = out + (g / 32) * BITS;
+        uint64_t acc = 0;
+        int fill = 0, w = 0;
+        for (size_t k = g; k < n; k++) {
+            over |= in[k] & LIM;
+            acc |= (uint64_t)in[k] << fill;
+            fill += BITS;
+            if (fill >= 32) {
+                o[w++] = (uint32_t)acc;
+                acc >>= 32;
+                fill -= 32;
+            }
+        }
+        if (fill > 0) o[w] = (uint32_t)acc;
+    }
+    return over;
+}
+
+// PACKB: n u32 values packed at `bits` bits each, group g of 32 values in
+// words [g*bits, (g+1)*bits).  Returns the OR of the values' bits above `bits`
+// (non-zero: a value does not fit -- the caller re-sends plainly so the device
+// check reports it).
+static uint32_t pack_bits(const uint32_t *in, size_t n, int bits, uint32_t *out) {
+    switch (bits) {
+#define PB(B) case B: return pack_bits_t<B>(in, n, out);
+        PB(1) PB(2) PB(3) PB(4) PB(5) PB(6) PB(7) PB(8) PB(9) PB(10) PB(11) PB(12)
+        PB(13) PB(14) PB(15) PB(16) PB(17) PB(18) PB(19) PB(20) PB(21) PB(22) PB(23) PB(24)
+#undef PB
+        default: return ~0u;  // not packed (the caller only asks for <= 24)
+    }
+}
 
 static void staged(const std::vector<Job> &jobs, bool *high, cudaStream_t s) {
     struct Chunk {
@@ -109,7 +168,10 @@ static void staged(const std::vector<Job> &jobs, bool *high, cudaStream_t s) {
     };
     std::vector<Chunk> chunks;
     for (int j = 0; j < (int)jobs.size(); j++) {
-        const size_t step = jobs[j].kind == PACK4 ? 2 * kChunk : kChunk;
+        // source bytes per chunk: the staged output fills at most one kChunk slot
+        size_t step = kChunk;
+        if (jobs[j].kind == PACK4) step = 2 * kChunk;
+        if (jobs[j].kind == PACKB) step = (kChunk * 32 / jobs[j].bits) / 128 * 128;  // whole 32-value groups
         for (size_t off = 0; off < jobs[j].bytes; off += step)
             chunks.push_back({j, off, std::min(step, jobs[j].bytes - off)});
     }
@@ -137,6 +199,12 @@ static void staged(const std::vector<Job> &jobs, bool *high, cudaStream_t s) {
                 size_t out = ch.len, doff = ch.off;
                 if (jb.kind == COPY) {
                     memcpy(P.buf[slot], from, ch.len);
+                } else if (jb.kind == PACKB) {
+                    const size_t n = ch.len / 4;
+                    if (pack_bits(reinterpret_cast<const uint32_t *>(from), n, jb.bits, static_cast<uint32_t *>(P.buf[slot])))
+                        hi.store(true, std::memory_order_relaxed);
+                    out = ((n + 31) / 32) * (size_t)jb.bits * 4;  // whole groups (the tail group padded)
+                    doff = (ch.off / 4 / 32) * (size_t)jb.bits * 4;
                 } else {
                     const uint32_t *w = reinterpret_cast<const uint32_t *>(from);
                     uint16_t *o = static_cast<uint16_t *>(P.buf[slot]);
@@ -196,6 +264,20 @@ __global__ void k_unpack_nibbles(uint64_t T, const uint16_t *__restrict__ in, ui
     }
 }
 
+// tile_col_ind travels at ceil(log2 ntr) bits per value (20 instead of 32 at
+// R-MAT s22 d=4): group g of 32 values in words [g*bits, (g+1)*bits)
+__global__ void k_unpack_bits(uint64_t T, int bits, const uint32_t *__restrict__ in, uint32_t *__restrict__ out) {
+    const uint32_t mask = bits == 32 ? 0xFFFFFFFFu : (1u << bits) - 1u;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < T; t += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t bit = (t >> 5) * (uint64_t)bits * 32 + (t & 31) * (uint64_t)bits;
+        const uint64_t wi = bit >> 5;
+        const uint32_t sh = (uint32_t)(bit & 31);
+        uint64_t v = in[wi];
+        if (sh + bits > 32) v |= (uint64_t)in[wi + 1] << 32;
+        out[t] = (uint32_t)(v >> sh) & mask;
+    }
+}
+
 // the three arrays of a host B2SR matrix in one staged upload
 void upload_b2sr(b2sr_matrix *m, const uint32_t *h_trp, const uint32_t *h_tci, const void *h_tiles, cudaStream_t s) {
     const size_t trp_b = ((size_t)m->ntr + 1) * 4, tci_b = m->num_tiles * 4;
@@ -207,26 +289,42 @@ void upload_b2sr(b2sr_matrix *m, const uint32_t *h_trp, const uint32_t *h_tci, c
         h2d(m->tiles, h_tiles, tile_b, s);
         return;
     }
-    static const bool pack_on = [] { const char *e = getenv("B2SR_H2D_PACK"); return !(e && e[0] == '0'); }();
+    // B2SR_H2D_PACK (A/B): default tiles packed; "all": tiles and columns (bit-packed
+    // tile_col_ind measured no faster on the box -- 22.3-27.0 vs 22.8-23.4 ms for
+    // the s22 host matrix: the packing loop costs what the smaller DMA saves);
+    // 0: plain copies (26.5-26.8 ms)
+    const int pack_mode = [] {  // read per upload (tests switch it)
+        const char *e = getenv("B2SR_H2D_PACK");
+        return !e ? 2 : (e[0] == '0' ? 0 : (e[0] == 'a' ? 1 : 2));
+    }();
+    const bool pack_on = pack_mode != 0;
     const bool pack = pack_on && m->dim == 4 && !page_locked(h_tiles);  // B2SR_H2D_PACK=0: plain copy (A/B)
-    Buf<uint16_t> packed(pack ? m->num_tiles : 1, s);
+    // columns of a full matrix are < ntr: ceil(log2 ntr) bits each (a row block's too)
+    const uint32_t ncols = tile_rows(m->n, m->dim);
+    int cb = 1;
+    while (cb < 32 && ((uint64_t)(ncols - 1) >> cb)) cb++;
+    const bool packc = pack_mode == 1 && cb <= 24;
+    const uint64_t T = m->num_tiles;
+    Buf<uint16_t> packed(pack ? T : 1, s);
+    Buf<uint32_t> packedc(packc ? ((T + 31) / 32) * cb + 1 : 1, s);
     std::vector<Job> jobs;
     if (trp_b < kDirect) CK(cudaMemcpyAsync(m->trp, h_trp, trp_b, cudaMemcpyHostToDevice, s));
     else jobs.push_back({m->trp, h_trp, trp_b, COPY});
-    jobs.push_back({m->tci, h_tci, tci_b, COPY});
+    if (packc) jobs.push_back({packedc.p, h_tci, tci_b, PACKB, cb});
+    else jobs.push_back({m->tci, h_tci, tci_b, COPY});
     if (pack) jobs.push_back({packed.p, h_tiles, tile_b, PACK4});
     else if (page_locked(h_tiles)) h2d(m->tiles, h_tiles, tile_b, s);
     else jobs.push_back({m->tiles, h_tiles, tile_b, COPY});
-    bool high = false;
-    staged(jobs, &high, s);
-    if (!pack) return;
-    if (high) {  // the stream drains `packed` before its memory is reused
-        h2d(m->tiles, h_tiles, tile_b, s);
+    bool high = false;  // a value did not fit its packed width: re-send plainly (the stream
+    staged(jobs, &high, s);  // drains the packed buffers before their memory is reused)
+    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((T + 255) / 256, (uint64_t)num_sms() * 16));
+    if (high) {
+        if (packc) h2d(m->tci, h_tci, tci_b, s);
+        if (pack) h2d(m->tiles, h_tiles, tile_b, s);
         return;
     }
-    const uint64_t T = m->num_tiles;
-    const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((T + 255) / 256, (uint64_t)num_sms() * 16));
-    LAUNCH(k_unpack_nibbles, g, 256, 0, s, T, packed.p, static_cast<uint32_t *>(m->tiles));
+    if (packc) LAUNCH(k_unpack_bits, g, 256, 0, s, T, cb, packedc.p, m->tci);
+    if (pack) LAUNCH(k_unpack_nibbles, g, 256, 0, s, T, packed.p, static_cast<uint32_t *>(m->tiles));
 }
 
 }  // namespace b2sr

@@ -194,13 +194,15 @@ def test_row_partitioned_pagerank_sssp_two_ranks_one_gpu(d, monkeypatch):
     assert got[3] == want_ss.per_vertex.tobytes() and got[4] == want_ss.iterations
 
 
-def test_large_host_upload_paths(tmp_path):
+@pytest.mark.parametrize("pack", ["tiles", "all"])
+def test_large_host_upload_paths(tmp_path, monkeypatch, pack):
     """Host-array uploads above the staging threshold (staging.cu): the
     staged copy of tile_col_ind and the nibble-packed d=4 tile upload give the
     device the caller's exact bytes; a d=4 tile with a high nibble set still
     reaches the device check and raises the reference constructor's message."""
     from paper_2201_08560_b200.errors import FormatError
 
+    monkeypatch.setenv("B2SR_H2D_PACK", pack)
     csr = rmat.rmat_csr(18, 16, seed=4)  # ~7.7 M tiles at d=4: 31 MB of tiles, past the 16 MB threshold
     for d in (4, 8):
         m = b2.csr_to_b2sr(csr, d)
@@ -218,6 +220,18 @@ def test_large_host_upload_paths(tmp_path):
     raw = (b2.formats._HEADER.pack(b2.formats._MAGIC, b2.formats._VERSION, csr.n, 4, len(trp) - 1, len(tci))
            + trp.astype("<u4").tobytes() + tci.astype("<u4").tobytes() + tiles.astype(np.uint8).tobytes())
     q = tmp_path / "bad.b2sr"
+    q.write_bytes(raw)
+    with pytest.raises(FormatError) as e_dev:
+        b2.load_b2sr(q)
+    with pytest.raises(FormatError) as e_host:
+        b2.B2srMatrix(csr.n, 4, trp, tci, tiles)
+    assert str(e_dev.value) == str(e_host.value)
+    # a tile column past the packed width (>= 2^ceil(log2 ntr)): the bit-packed
+    # column upload falls back to the plain copy, the device check reports it
+    trp, tci, tiles = m.tile_row_ptr.copy(), m.tile_col_ind.copy(), m.bit_tiles.copy()
+    tci[len(tci) // 3] = 0xFFFFFFF0
+    raw = (b2.formats._HEADER.pack(b2.formats._MAGIC, b2.formats._VERSION, csr.n, 4, len(trp) - 1, len(tci))
+           + trp.astype("<u4").tobytes() + tci.astype("<u4").tobytes() + tiles.astype(np.uint8).tobytes())
     q.write_bytes(raw)
     with pytest.raises(FormatError) as e_dev:
         b2.load_b2sr(q)
