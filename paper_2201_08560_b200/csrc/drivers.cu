@@ -1160,7 +1160,15 @@ struct BfsSnapshots {
     }
     const volatile BfsSnap *slot(uint32_t level) const { return host + level % N; }
 };
-constexpr uint32_t LOOKAHEAD = 1;  // levels enqueued beyond the one whose end is being checked
+// levels enqueued beyond the one whose end is being checked (B2SR_BFS_LOOKAHEAD, A/B)
+static uint32_t bfs_lookahead() {
+    static const uint32_t v = [] {
+        const char *e = getenv("B2SR_BFS_LOOKAHEAD");
+        const int k = e ? atoi(e) : 1;
+        return (uint32_t)std::max(1, std::min(k, 6));  // < the 8 snapshot slots
+    }();
+    return v;
+}
 
 static BfsSnapshots &bfs_snapshots() {
     // per host thread (re-entrant C ABI) and per device (the events belong to one)
@@ -1228,6 +1236,7 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
         // the host checks level L-LOOKAHEAD's outcome while levels up to L are
         // already enqueued (levels past the end are gated no-ops): no poll
         // ever drains the queue
+        const uint32_t LOOKAHEAD = bfs_lookahead();
         if (trace || L > LOOKAHEAD) {
             const uint32_t Lc = trace ? L : L - LOOKAHEAD;
             const volatile BfsSnap *sn = snaps.slot(Lc);
@@ -1292,6 +1301,7 @@ static void bfs_push_only(const b2sr_matrix *a, uint32_t src, double *d_levels, 
         LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L, a->trp,
                nullptr, nullptr, ctl.p, (uint4 *)frontier, 1, 0.0, (unsigned long long)a->num_tiles, 1, snaps.dev, L, active_frac);
         std::swap(frontier, next);
+        const uint32_t LOOKAHEAD = bfs_lookahead();
         if (trace || L > LOOKAHEAD) {
             const uint32_t Lc = trace ? L : L - LOOKAHEAD;
             const volatile BfsSnap *sn = snaps.slot(Lc);
@@ -1484,6 +1494,7 @@ static void dist_bfs_run(b2sr_dist_bfs *p, uint32_t src, double *d_levels, int64
                p->trp_a, p->trp_at, (const uint4 *)p->live_at, ctl.p, (uint4 *)contrib.p, 1, alpha,
                (unsigned long long)p->tiles_at, 1, snaps.dev, L, active_frac);
         std::swap(frontier, next);
+        const uint32_t LOOKAHEAD = bfs_lookahead();
         if (trace || L > LOOKAHEAD) {
             const uint32_t Lc = trace ? L : L - LOOKAHEAD;
             const volatile BfsSnap *sn = snaps.slot(Lc);
