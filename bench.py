@@ -769,7 +769,7 @@ def run_strong(args, rank, world, local_rank, tdist=None, headline=True):
         tc = {"scale": scale, "nnz": nnz, "triangles": int(tri), "ms": round(tms, 3),
               "edges_per_s": round((nnz // 2) / (tms / 1e3), 1), "edges_per_s_per_gpu": round((nnz // 2) / (tms / 1e3) / world, 1),
               "mask_row_cuts": cuts, "lower_tiles": int(lower.num_tiles),
-              "parallelism": f"mask tile rows x{world} (equal estimated work), L replicated, NCCL int64 all-reduce"}
+              "parallelism": f"mask tile rows x{world} (equal estimated work), L and L^T replicated, each pair counted by the owner of its longer row, NCCL int64 all-reduce"}
         del lower
     del csr
     torch.cuda.empty_cache()
