@@ -230,15 +230,14 @@ __global__ void __launch_bounds__(ConvMerge<D>::NW * 32) k_conv_merge(
 #pragma unroll
         for (uint32_t l = 0; l < S; l++) {
             for (uint32_t i = lane; i < E; i += 32) {
-                uint32_t r = 0;
-#pragma unroll
-                for (int q = 1; q < D; q++) r += off[q] <= i;
-                const uint32_t j = r >> l;                   // level-l run of element i
+                const uint32_t v = X[i];
+                // the value carries its bit-row r, and the level-l run holding
+                // element i is the one of runs [j << l, (j + 1) << l), j = r >> l
+                const uint32_t j = (v & (D - 1)) >> l;       // level-l run of element i
                 const uint32_t a = off[j << l];              // its start
                 const uint32_t pj = j ^ 1u;                  // partner run
                 const uint32_t pa = off[pj << l], pb = off[min((pj + 1) << l, (uint32_t)D)];
                 const uint32_t ms = off[(j & ~1u) << l];     // merged run start
-                const uint32_t v = X[i];
                 uint32_t lo = pa, hi = pb;
                 while (lo < hi) { const uint32_t m = (lo + hi) >> 1; if (X[m] < v) lo = m + 1; else hi = m; }
                 Y[ms + (i - a) + (lo - pa)] = v;
