@@ -4,7 +4,7 @@
 //
 // Per pass: (1) per-CTA digit histograms, digit-major; (2) exclusive scan;
 // (3) scatter with an in-CTA stable rank: each warp walks its 512 keys in 16
-// rounds of 32, ranks equal digits with __match_any_sync, keeps warp-private
+// rounds of 32, ranks equal digits with ballots (multi-split), keeps warp-private
 // digit counters in shared memory, then warps are offset by a per-digit
 // prefix.  Order = (CTA, warp, round, lane) = input order, so it is stable.
 #include "b2sr_internal.cuh"
@@ -59,7 +59,16 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__
         key[j] = ok ? kin[i] : (K)0;
         if constexpr (VALS) val[j] = ok ? vin[i] : 0u;
         uint32_t dg = ok ? ((uint32_t)(key[j] >> sh) & dm) : 256u;  // 256 = no item
-        uint32_t peers = __match_any_sync(0xffffffffu, dg);
+        // lanes with the same digit: nine ballots (8 digit bits + the no-item
+        // flag) instead of __match_any_sync (MATCH.ANY is a slow, multi-pass
+        // instruction; this is the classic multi-split ranking)
+        uint32_t peers = 0xffffffffu;
+#pragma unroll
+        for (int b = 0; b < 9; b++) {
+            const bool bit = (dg >> b) & 1u;
+            const uint32_t bb = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? bb : ~bb;
+        }
         uint32_t leader = __ffs(peers) - 1;
         uint32_t before = dg < 256 ? wc[w][dg] : 0u;
         rank[j] = before + __popc(peers & lt);
