@@ -22,8 +22,9 @@ extern "C" const char *b2sr_last_error(void);
 namespace b2sr {
 
 struct CsrPlan {
-    uint32_t *rp = nullptr;  // n + 1
-    uint32_t *ci = nullptr;  // nnz
+    uint32_t *rp = nullptr;     // n + 1
+    uint32_t *ci = nullptr;     // nnz
+    uint32_t *order = nullptr;  // rows, longest first: the hub rows' serial folds start at once
     uint64_t nnz = 0;
 };
 
@@ -32,6 +33,7 @@ void free_csrplan(void *p) {
     if (!c) return;
     dfree(c->rp, nullptr);
     dfree(c->ci, nullptr);
+    dfree(c->order, nullptr);
     delete c;
 }
 
@@ -39,6 +41,14 @@ void free_csrplan(void *p) {
 bool bff_csr_enabled(const b2sr_matrix *m) {
     const char *e = getenv("B2SR_BFF_CSR");  // read per call: tests switch it
     return !(e && e[0] == '0') && m->dim >= 16 && m->row0 == 0 && m->ntr == tile_rows(m->n, m->dim) && m->num_tiles;
+}
+
+__global__ void k_csr_len_keys(uint32_t n, const uint32_t *__restrict__ rp, uint32_t *__restrict__ key,
+                               uint32_t *__restrict__ row) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        key[i] = 0xFFFFFFFFu - (rp[i + 1] - rp[i]);  // ascending key = descending length
+        row[i] = i;
+    }
 }
 
 static CsrPlan *csr_plan(b2sr_matrix *m, cudaStream_t s) {
@@ -51,9 +61,18 @@ static CsrPlan *csr_plan(b2sr_matrix *m, cudaStream_t s) {
             if (b2sr_to_csr_rowptr(m, rp.p, &nnz, s) != B2SR_OK) B2SR_THROW(B2SR_ECUDA, "%s", b2sr_last_error());
             Buf<uint32_t> ci(std::max<uint64_t>(nnz, 1), s);
             if (b2sr_to_csr_fill(m, rp.p, ci.p, s) != B2SR_OK) B2SR_THROW(B2SR_ECUDA, "%s", b2sr_last_error());
+            const uint32_t n = m->n;
+            Buf<uint32_t> key(n, s), row(n, s), kalt, valt;
+            const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms() * 16));
+            LAUNCH(k_csr_len_keys, g, 256, 0, s, n, rp.p, key.p, row.p);
+            uint32_t *ko = nullptr, *vo = nullptr;
+            radix_sort_pairs_u32(key.p, row.p, n, 32, s, &ko, &vo, &kalt, &valt);
+            Buf<uint32_t> order(n, s);
+            CK(cudaMemcpyAsync(order.p, vo, (size_t)n * 4, cudaMemcpyDeviceToDevice, s));
             c->nnz = nnz;
             c->rp = rp.release();
             c->ci = ci.release();
+            c->order = order.release();
         } catch (...) {
             free_csrplan(c);
             throw;
@@ -87,13 +106,18 @@ __device__ __forceinline__ double csr_pick(double a, double b) {
 #define CSR_G 4  // s16 d=32: 4 -> 0.159 ms, 8 -> 0.187 ms (63 registers)
 #endif
 template <int D, int RING>
-__global__ void __launch_bounds__(256) k_bff_csr(uint32_t n, const uint32_t *__restrict__ rp,
+__global__ void __launch_bounds__(256) k_bff_csr(uint32_t n, const uint32_t *__restrict__ order,
+                                                 const uint32_t *__restrict__ rp,
                                                  const uint32_t *__restrict__ ci, const double *__restrict__ x,
                                                  double inc, double ident, const void *__restrict__ keep,
                                                  double *__restrict__ y) {
     const uint32_t lane = lane_id(), warps = (gridDim.x * blockDim.x) >> 5;
     constexpr int G = CSR_G;  // 32-term chunks in flight: a hub row's gathers overlap its fold
-    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < n; i += warps) {
+    __shared__ double2 csr_sbuf[8][16];  // per warp: one chunk of terms (ARITHMETIC)
+    double *sb = reinterpret_cast<double *>(csr_sbuf[threadIdx.x >> 5]);
+    const double2 *sbuf2 = csr_sbuf[threadIdx.x >> 5];
+    for (uint32_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < n; w += warps) {
+        const uint32_t i = __ldg(order + w);  // longest rows first
         const uint32_t a = __ldg(rp + i), b = __ldg(rp + i + 1);
         double acc = ident;
         double cur[G], nxt[G];
@@ -114,12 +138,25 @@ __global__ void __launch_bounds__(256) k_bff_csr(uint32_t n, const uint32_t *__r
                 const uint32_t cnt = min(32u, b - cb);
                 double v = cur[g];
                 if constexpr (RING == B2SR_RING_ARITHMETIC) {
-                    // the serial chain of the reference: the shuffles are independent
-                    // of acc, so unrolled they issue ahead of the dependent adds
+                    // the serial chain of the reference: the 32 terms go through
+                    // shared memory and are read back as 16 broadcast 16-byte
+                    // loads before the chain, so only the dependent adds are
+                    // serial (a shuffle per term put its latency on the chain:
+                    // ~30 instead of 8 cycles per term on a hub row)
+                    __syncwarp();
+                    sb[lane] = v;
+                    __syncwarp();
+                    if (cnt == 32) {
+                        double2 t[16];
 #pragma unroll
-                    for (uint32_t j = 0; j < 32; j++) {
-                        const double t = __shfl_sync(0xffffffffu, v, j);
-                        if (j < cnt) acc = __dadd_rn(acc, t);
+                        for (int q = 0; q < 16; q++) t[q] = sbuf2[q];
+#pragma unroll
+                        for (int q = 0; q < 16; q++) {
+                            acc = __dadd_rn(acc, t[q].x);
+                            acc = __dadd_rn(acc, t[q].y);
+                        }
+                    } else {
+                        for (uint32_t q = 0; q < cnt; q++) acc = __dadd_rn(acc, sb[q]);
                     }
                 } else {
                     if constexpr (RING == B2SR_RING_MINPLUS) v = __dadd_rn(v, inc);
@@ -151,11 +188,11 @@ static void bff_csr_ring(const CsrPlan *c, uint32_t n, const double *x, int ring
                          const void *keep, double *y, cudaStream_t s) {
     const unsigned g = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)n + 7) / 8, (uint64_t)num_sms() * 8));
     if (ring == B2SR_RING_ARITHMETIC)
-        LAUNCH((k_bff_csr<D, B2SR_RING_ARITHMETIC>), g, 256, 0, s, n, c->rp, c->ci, x, inc, ident, keep, y);
+        LAUNCH((k_bff_csr<D, B2SR_RING_ARITHMETIC>), g, 256, 0, s, n, c->order, c->rp, c->ci, x, inc, ident, keep, y);
     else if (ring == B2SR_RING_MINPLUS)
-        LAUNCH((k_bff_csr<D, B2SR_RING_MINPLUS>), g, 256, 0, s, n, c->rp, c->ci, x, inc, ident, keep, y);
+        LAUNCH((k_bff_csr<D, B2SR_RING_MINPLUS>), g, 256, 0, s, n, c->order, c->rp, c->ci, x, inc, ident, keep, y);
     else
-        LAUNCH((k_bff_csr<D, B2SR_RING_MAXTIMES>), g, 256, 0, s, n, c->rp, c->ci, x, inc, ident, keep, y);
+        LAUNCH((k_bff_csr<D, B2SR_RING_MAXTIMES>), g, 256, 0, s, n, c->order, c->rp, c->ci, x, inc, ident, keep, y);
 }
 
 void launch_bff_csr(b2sr_matrix *m, const double *x, int ring, double inc, double ident, const void *keep, double *y,
