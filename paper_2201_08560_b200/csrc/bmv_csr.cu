@@ -39,8 +39,9 @@ void free_csrplan(void *p) {
 
 // B2SR_BFF_CSR=0: wide tiles keep the tile walk (A/B)
 bool bff_csr_enabled(const b2sr_matrix *m) {
-    const char *e = getenv("B2SR_BFF_CSR");  // read per call: tests switch it
-    return !(e && e[0] == '0') && m->dim >= 16 && m->row0 == 0 && m->ntr == tile_rows(m->n, m->dim) && m->num_tiles;
+    const char *e = getenv("B2SR_BFF_CSR");  // read per call: tests switch it; "all": d = 4, 8 too (A/B)
+    const bool wide = m->dim >= 16 || (e && e[0] == 'a');
+    return !(e && e[0] == '0') && wide && m->row0 == 0 && m->ntr == tile_rows(m->n, m->dim) && m->num_tiles;
 }
 
 __global__ void k_csr_len_keys(uint32_t n, const uint32_t *__restrict__ rp, uint32_t *__restrict__ key,
@@ -198,8 +199,12 @@ static void bff_csr_ring(const CsrPlan *c, uint32_t n, const double *x, int ring
 void launch_bff_csr(b2sr_matrix *m, const double *x, int ring, double inc, double ident, const void *keep, double *y,
                     cudaStream_t s) {
     const CsrPlan *c = csr_plan(m, s);
-    if (m->dim == 16) bff_csr_ring<16>(c, m->n, x, ring, inc, ident, keep, y, s);
-    else bff_csr_ring<32>(c, m->n, x, ring, inc, ident, keep, y, s);
+    switch (m->dim) {
+        case 4: bff_csr_ring<4>(c, m->n, x, ring, inc, ident, keep, y, s); break;
+        case 8: bff_csr_ring<8>(c, m->n, x, ring, inc, ident, keep, y, s); break;
+        case 16: bff_csr_ring<16>(c, m->n, x, ring, inc, ident, keep, y, s); break;
+        default: bff_csr_ring<32>(c, m->n, x, ring, inc, ident, keep, y, s); break;
+    }
 }
 
 }  // namespace b2sr
