@@ -831,28 +831,12 @@ __global__ void __launch_bounds__(256) k_cc_min(const WorkItem *__restrict__ ite
                     wd[u][1] = ok ? ld_stream32(tiles + (size_t)tu * 8 + 4) : 0u;
                 }
             }
-            // every tile's FIRST set bit is gathered unconditionally (R-MAT: ~1
-            // bit per tile), so the U label loads are in flight together; the
-            // further bits of a tile are the rare tail
-            uint32_t fv[U], fp[U];
 #pragma unroll
             for (int u = 0; u < U; u++) {
-                const uint32_t w0 = wd[u][0], w1 = D == 8 ? wd[u][D / 4 - 1] : 0u;
-                const int p = w0 ? __ffs(w0) - 1 : (w1 ? 32 + __ffs(w1) - 1 : -1);
-                fp[u] = (uint32_t)p;
-                fv[u] = p >= 0 ? __ldg(lab + (size_t)k[u] * D + (p & 7)) : 0xFFFFFFFFu;
-            }
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                if (fp[u] == 0xFFFFFFFFu) continue;
                 const uint32_t *xs = lab + (size_t)k[u] * D;
 #pragma unroll
                 for (int r = 0; r < D; r++) {
                     uint32_t b = (wd[u][r / 4] >> (8 * (r % 4))) & 0xFFu;
-                    if ((uint32_t)r == fp[u] >> 3) {  // the first bit: its label is already loaded
-                        mn[r] = min(mn[r], fv[u]);
-                        b &= b - 1;
-                    }
                     while (b) {
                         mn[r] = min(mn[r], __ldg(xs + __ffs(b) - 1));
                         b &= b - 1;
