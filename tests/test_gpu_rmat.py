@@ -194,7 +194,7 @@ def test_row_partitioned_pagerank_sssp_two_ranks_one_gpu(d, monkeypatch):
     assert got[3] == want_ss.per_vertex.tobytes() and got[4] == want_ss.iterations
 
 
-@pytest.mark.parametrize("pack", ["tiles", "all"])
+@pytest.mark.parametrize("pack", ["tiles", "all", "split"])
 def test_large_host_upload_paths(tmp_path, monkeypatch, pack):
     """Host-array uploads above the staging threshold (staging.cu): the
     staged copy of tile_col_ind and the nibble-packed d=4 tile upload give the
@@ -237,4 +237,41 @@ def test_large_host_upload_paths(tmp_path, monkeypatch, pack):
         b2.load_b2sr(q)
     with pytest.raises(FormatError) as e_host:
         b2.B2srMatrix(csr.n, 4, trp, tci, tiles)
+    assert str(e_dev.value) == str(e_host.value)
+
+
+@pytest.mark.parametrize("logn", [20, 25])
+def test_host_upload_split_columns(tmp_path, logn):
+    """The default host upload splits tile_col_ind into a u16 stream plus the
+    column bits above 16 (staging.cu SPLIT): a nibble per column when the
+    columns need <= 20 bits (2^20 vertices at d=4: 18 bits), a byte up to 24
+    (2^25 vertices: 23 bits).  The device gets the caller's exact bytes, and a
+    column past the packed width falls back to the plain copy and raises the
+    reference constructor's message."""
+    from paper_2201_08560_b200.errors import FormatError
+
+    n = 1 << logn
+    rng = np.random.default_rng(logn)
+    key = np.unique(rng.integers(0, n, 4_500_000, dtype=np.int64) * n + rng.integers(0, n, 4_500_000, dtype=np.int64))
+    rows, cols = (key // n).astype(np.uint32), (key % n).astype(np.uint32)
+    row_ptr = np.zeros(n + 1, dtype=np.uint32)
+    np.cumsum(np.bincount(rows, minlength=n), out=row_ptr[1:])
+    csr = b2.CsrMatrix(n, row_ptr, cols)
+    m = b2.csr_to_b2sr(csr, 4)
+    assert m.num_tiles * 8 > (16 << 20)  # past the staging threshold
+    trp, tci, tiles = m.tile_row_ptr.copy(), m.tile_col_ind.copy(), m.bit_tiles.copy()
+    h = b2.B2srMatrix(n, 4, trp, tci, tiles)
+    assert h == m
+    hb = b2.formats.B2srMatrix._wrap(b2.formats._new_handle("b2sr_transpose", h.handle().ptr, 0))
+    assert hb == b2.b2sr_transpose(m)
+    bad = tci.copy()
+    bad[len(bad) // 2] = np.uint32(n)  # >= ntr, and past 2^ceil(log2 ntr)
+    raw = (b2.formats._HEADER.pack(b2.formats._MAGIC, b2.formats._VERSION, n, 4, len(trp) - 1, len(bad))
+           + trp.astype("<u4").tobytes() + bad.astype("<u4").tobytes() + tiles.astype(np.uint8).tobytes())
+    q = tmp_path / "bad.b2sr"
+    q.write_bytes(raw)
+    with pytest.raises(FormatError) as e_dev:
+        b2.load_b2sr(q)  # read straight into the staged upload, checked on the device
+    with pytest.raises(FormatError) as e_host:
+        b2.B2srMatrix(n, 4, trp, bad, tiles)
     assert str(e_dev.value) == str(e_host.value)
