@@ -76,7 +76,8 @@ __global__ void __launch_bounds__(256) k_conv(const ConvItem *__restrict__ items
                                               const uint32_t *__restrict__ col_ind, const uint64_t *__restrict__ iofs,
                                               uint32_t *__restrict__ cnt, uint32_t *__restrict__ tci,
                                               typename WordT<D>::T *__restrict__ tiles,
-                                              const uint32_t *__restrict__ order, const uint8_t *__restrict__ only) {
+                                              const uint32_t *__restrict__ order, const uint8_t *__restrict__ only,
+                                              uint64_t *__restrict__ toff) {
     constexpr uint32_t GPW = 32 / D;  // groups (items) per warp
     const uint32_t lane = lane_id(), r = lane % D;
     const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
@@ -87,9 +88,9 @@ __global__ void __launch_bounds__(256) k_conv(const ConvItem *__restrict__ items
         if (valid && only && !only[item]) valid = false;  // the warp merge did this item
         ConvItem it = valid ? items[item] : ConvItem{0, 0, 0, 0};
         uint64_t row = (uint64_t)it.row * D + r;
-        uint32_t p = 0, end = 0;
+        uint32_t p = 0, end = 0, rs = 0;
         if (valid && row < n) {
-            p = row_ptr[row];
+            p = rs = row_ptr[row];
             end = row_ptr[row + 1];
             if (it.klo > 0) {  // split range: first entry with c >= klo*D
                 uint32_t key = it.klo * (uint32_t)D, a = p, b = end;
@@ -105,7 +106,16 @@ __global__ void __launch_bounds__(256) k_conv(const ConvItem *__restrict__ items
             c = col_ind[p];
             if (c / D < it.khi) cur = c / D;
         }
-        uint64_t t = (PACK && valid) ? iofs[item] : 0;
+        uint64_t t = 0;
+        if (PACK && toff) {  // fused: the item's tiles go to its first CSR entry's slot of the staging arrays
+            uint32_t skip = p - rs;
+#pragma unroll
+            for (int o = D / 2; o; o >>= 1) skip += __shfl_xor_sync(0xffffffffu, skip, o, D);
+            t = (uint64_t)__shfl_sync(0xffffffffu, rs, 0, D) + skip;
+        } else if (PACK && valid) {
+            t = iofs[item];
+        }
+        const uint64_t t0 = t;
         uint32_t count = 0;
         while (__any_sync(0xffffffffu, cur != INF32)) {
             uint32_t K = group_min<D>(cur);
@@ -129,8 +139,9 @@ __global__ void __launch_bounds__(256) k_conv(const ConvItem *__restrict__ items
                 ++count;
             }
         }
-        if constexpr (!PACK) {
-            if (valid && r == 0) cnt[item] = count;
+        if (valid && r == 0 && (!PACK || toff)) {
+            cnt[item] = count;
+            if (PACK) toff[item] = t0;
         }
     }
 }
@@ -164,7 +175,8 @@ template <int D, bool PACK>
 __global__ void __launch_bounds__(ConvMerge<D>::NW * 32) k_conv_merge(
     const ConvItem *__restrict__ items, uint32_t n_items, uint32_t n, const uint32_t *__restrict__ row_ptr,
     const uint32_t *__restrict__ col_ind, const uint64_t *__restrict__ iofs, uint32_t *__restrict__ cnt,
-    uint32_t *__restrict__ tci, uint32_t *__restrict__ tiles32, uint8_t *__restrict__ big) {
+    uint32_t *__restrict__ tci, uint32_t *__restrict__ tiles32, uint8_t *__restrict__ big,
+    uint64_t *__restrict__ toff) {
     using CMt = ConvMerge<D>;
     constexpr uint32_t S = CMt::S, NW = CMt::NW, TW = CMt::TW;
     __shared__ uint32_t buf[NW][2][CM_CAP];
@@ -178,11 +190,11 @@ __global__ void __launch_bounds__(ConvMerge<D>::NW * 32) k_conv_merge(
     for (uint32_t item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < n_items; item += warps) {
         const ConvItem it = items[item];
         // run r = bit-row r of tile row it.row, restricted to tile columns [klo, khi)
-        uint32_t p0 = 0, p1 = 0;
+        uint32_t p0 = 0, p1 = 0, rs = 0;
         if (lane < (uint32_t)D) {
             const uint64_t row = (uint64_t)it.row * D + lane;
             if (row < n) {
-                p0 = row_ptr[row];
+                p0 = rs = row_ptr[row];
                 p1 = row_ptr[row + 1];
                 if (it.klo > 0) {
                     uint32_t a = p0, b = p1;
@@ -207,9 +219,15 @@ __global__ void __launch_bounds__(ConvMerge<D>::NW * 32) k_conv_merge(
         }
         const uint32_t E = __shfl_sync(0xffffffffu, incl, D - 1);
         if (E > CM_CAP) {  // the lock-step merge takes it
-            if (!PACK && lane == 0) big[item] = 1;
+            if ((!PACK || toff) && lane == 0) big[item] = 1;
             continue;
         }
+        // fused mode: this item's tiles go to the slot of its first CSR entry
+        // (an item has at most as many tiles as entries, so the items' slot
+        // ranges of the staging arrays are disjoint)
+        const uint64_t tslot = toff ? (uint64_t)__shfl_sync(0xffffffffu, rs, 0) +
+                                          __reduce_add_sync(0xffffffffu, p0 - rs)
+                                    : 0;
         __syncwarp();  // the previous item's readers of off/st are done
         if (lane < (uint32_t)D) {
             off[lane + 1] = incl;
@@ -219,11 +237,21 @@ __global__ void __launch_bounds__(ConvMerge<D>::NW * 32) k_conv_merge(
         __syncwarp();
         // stage: element i of run r (CSR index st[r] + i - off[r]) -> c << S | r
         uint32_t *X = buf[wid][0], *Y = buf[wid][1];
-        for (uint32_t i = lane; i < E; i += 32) {
-            uint32_t r = 0;
+        for (uint32_t i0 = 0; i0 < E; i0 += 128) {  // four loads in flight per lane
+            uint32_t v[4];
 #pragma unroll
-            for (int q = 1; q < D; q++) r += off[q] <= i;
-            X[i] = (__ldg(col_ind + st[r] + (i - off[r])) << S) | r;
+            for (int j = 0; j < 4; j++) {
+                const uint32_t i = i0 + j * 32 + lane;
+                uint32_t r = 0;
+#pragma unroll
+                for (int q = 1; q < D; q++) r += off[q] <= i;
+                v[j] = i < E ? (__ldg(col_ind + st[r] + (i - off[r])) << S) | r : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const uint32_t i = i0 + j * 32 + lane;
+                if (i < E) X[i] = v[j];
+            }
         }
         __syncwarp();
         // S pairwise merge levels: level l merges runs of 2^l bit-rows in pairs
@@ -250,7 +278,7 @@ __global__ void __launch_bounds__(ConvMerge<D>::NW * 32) k_conv_merge(
             uint32_t *T = CMt::TBUF ? tbuf[wid] : Y;
             for (uint32_t q = lane; q < E * TW; q += 32) T[q] = 0;
             __syncwarp();
-            const uint64_t tb = iofs[item];
+            const uint64_t tb = toff ? tslot : iofs[item];
             uint32_t run = 0;
             for (uint32_t base = 0; base < E; base += 32) {
                 const uint32_t i = base + lane;
@@ -270,6 +298,10 @@ __global__ void __launch_bounds__(ConvMerge<D>::NW * 32) k_conv_merge(
             __syncwarp();
             uint32_t *dst = tiles32 + tb * TW;
             for (uint32_t q = lane; q < run * TW; q += 32) dst[q] = T[q];
+            if (toff && lane == 0) {
+                cnt[item] = run;
+                toff[item] = tb;
+            }
         } else {
             uint32_t run = 0;
             for (uint32_t base = 0; base < E; base += 32) {
@@ -290,7 +322,7 @@ __global__ void k_conv_trp(uint32_t ntr, const uint64_t *pofs, const uint64_t *i
 template <int D>
 static void conv_launch(bool pack, const ConvItem *items, uint32_t n_items, uint32_t n, const uint32_t *row_ptr,
                         const uint32_t *col_ind, const uint64_t *iofs, uint32_t *cnt, uint32_t *tci, void *tiles,
-                        cudaStream_t s, const uint32_t *order, const uint8_t *only) {
+                        cudaStream_t s, const uint32_t *order, const uint8_t *only, uint64_t *toff) {
     constexpr uint32_t GPW = 32 / D;
     uint64_t warps = (n_items + GPW - 1) / GPW;
     uint64_t blocks = (warps + 7) / 8;
@@ -298,21 +330,21 @@ static void conv_launch(bool pack, const ConvItem *items, uint32_t n_items, uint
     unsigned g = (unsigned)(blocks < cap ? blocks : cap);
     if (pack)
         LAUNCH((k_conv<D, true>), g, 256, 0, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
-               (typename WordT<D>::T *)tiles, order, only);
+               (typename WordT<D>::T *)tiles, order, only, toff);
     else
         LAUNCH((k_conv<D, false>), g, 256, 0, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
-               (typename WordT<D>::T *)tiles, order, only);
+               (typename WordT<D>::T *)tiles, order, only, nullptr);
 }
 
 static void conv_dispatch(uint32_t d, bool pack, const ConvItem *items, uint32_t n_items, uint32_t n,
                           const uint32_t *row_ptr, const uint32_t *col_ind, const uint64_t *iofs, uint32_t *cnt,
                           uint32_t *tci, void *tiles, cudaStream_t s, const uint32_t *order = nullptr,
-                          const uint8_t *only = nullptr) {
+                          const uint8_t *only = nullptr, uint64_t *toff = nullptr) {
     switch (d) {
-        case 4: conv_launch<4>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order, only); break;
-        case 8: conv_launch<8>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order, only); break;
-        case 16: conv_launch<16>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order, only); break;
-        default: conv_launch<32>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order, only); break;
+        case 4: conv_launch<4>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order, only, toff); break;
+        case 8: conv_launch<8>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order, only, toff); break;
+        case 16: conv_launch<16>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order, only, toff); break;
+        default: conv_launch<32>(pack, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci, tiles, s, order, only, toff); break;
     }
 }
 
@@ -405,7 +437,7 @@ __global__ void __launch_bounds__(256) k_conv_count_hash(const ConvItem *__restr
 template <int D>
 static void merge_launch(bool pack, const ConvItem *items, uint32_t n_items, uint32_t n, const uint32_t *row_ptr,
                          const uint32_t *col_ind, const uint64_t *iofs, uint32_t *cnt, uint32_t *tci, void *tiles,
-                         uint8_t *big, cudaStream_t s) {
+                         uint8_t *big, cudaStream_t s, uint64_t *toff = nullptr) {
     constexpr uint32_t NW = ConvMerge<D>::NW;
     int per_sm = 1;
     if (pack) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_conv_merge<D, true>, NW * 32, 0));
@@ -414,10 +446,10 @@ static void merge_launch(bool pack, const ConvItem *items, uint32_t n_items, uin
                                                     (uint64_t)num_sms() * std::max(per_sm, 1));
     if (pack)
         LAUNCH((k_conv_merge<D, true>), g, NW * 32, 0, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
-               (uint32_t *)tiles, big);
+               (uint32_t *)tiles, big, toff);
     else
         LAUNCH((k_conv_merge<D, false>), g, NW * 32, 0, s, items, n_items, n, row_ptr, col_ind, iofs, cnt, tci,
-               (uint32_t *)tiles, big);
+               (uint32_t *)tiles, big, nullptr);
 }
 
 // warp merge for d = 4, 8 (B2SR_CONV_MERGE=0: lock-step merge only, A/B)
@@ -454,6 +486,53 @@ static bool conv_sorted() {
     return e && e[0] == '1';
 }
 
+// fused conversion, last step: each item's tiles move from the slot of its
+// first CSR entry in the staging arrays to their place in the matrix (a warp
+// per item, coalesced 4-byte copies; tiles are TW u32 words)
+template <int TW>
+__global__ void __launch_bounds__(256) k_conv_compact(uint32_t n_items, const uint64_t *__restrict__ toff,
+                                                      const uint64_t *__restrict__ iofs,
+                                                      const uint32_t *__restrict__ stci,
+                                                      const uint32_t *__restrict__ stiles, uint32_t *__restrict__ tci,
+                                                      uint32_t *__restrict__ tiles) {
+    const uint32_t lane = lane_id(), warps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; item < n_items; item += warps) {
+        const uint64_t src = toff[item], dst = iofs[item];
+        const uint32_t c = (uint32_t)(iofs[item + 1] - dst);
+        // all loads of a 128-tile step in flight before the stores (a plain
+        // strided loop waited one DRAM round trip per 32 tiles: 0.67 ms at s22)
+        for (uint32_t base = 0; base < c; base += 128) {
+            uint32_t a[4], b[4 * TW];
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const uint32_t q = base + j * 32 + lane;
+                if (q < c) a[j] = stci[src + q];
+            }
+#pragma unroll
+            for (int j = 0; j < 4 * TW; j++) {
+                const uint32_t q = base * TW + j * 32 + lane;
+                if (q < c * TW) b[j] = stiles[src * TW + q];
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const uint32_t q = base + j * 32 + lane;
+                if (q < c) tci[dst + q] = a[j];
+            }
+#pragma unroll
+            for (int j = 0; j < 4 * TW; j++) {
+                const uint32_t q = base * TW + j * 32 + lane;
+                if (q < c * TW) tiles[dst * TW + q] = b[j];
+            }
+        }
+    }
+}
+
+// B2SR_CONV_FUSED=0 (A/B): count pass, then pack straight into the matrix
+static bool conv_fused_enabled() {
+    const char *e = getenv("B2SR_CONV_FUSED");
+    return !(e && e[0] == '0');
+}
+
 b2sr_matrix *csr_to_b2sr_device(uint32_t n, uint32_t d, const uint32_t *row_ptr, const uint32_t *col_ind,
                                 cudaStream_t s) {
     uint32_t ntr = tile_rows(n, d);
@@ -483,6 +562,37 @@ b2sr_matrix *csr_to_b2sr_device(uint32_t n, uint32_t d, const uint32_t *row_ptr,
     Buf<uint32_t> cnt(n_items, s);
     Buf<uint64_t> iofs((size_t)n_items + 1, s);
     Buf<uint8_t> big;
+    if (merge && conv_fused_enabled() && !order) {
+        // one merge pass: pack every item into staging arrays at the slot of its
+        // first CSR entry (tiles <= entries), counting its tiles; scan; move
+        // the items' tiles into the matrix.  Replaces the count pass.
+        const uint64_t nnz = read_scalar(row_ptr + n, s);
+        const uint32_t TW = d == 4 ? 1 : 2;
+        Buf<uint32_t> stci(std::max<uint64_t>(nnz, 1), s), stiles(std::max<uint64_t>(nnz, 1) * TW, s);
+        Buf<uint64_t> toff(std::max<uint32_t>(n_items, 1), s);
+        big = Buf<uint8_t>(std::max<uint32_t>(n_items, 1), s);
+        CK(cudaMemsetAsync(big.p, 0, n_items, s));
+        if (d == 4) merge_launch<4>(true, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, stci.p, stiles.p, big.p, s, toff.p);
+        else merge_launch<8>(true, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, stci.p, stiles.p, big.p, s, toff.p);
+        conv_dispatch(d, true, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, stci.p, stiles.p, s, nullptr, big.p,
+                      toff.p);
+        exclusive_scan_u32_to_u64(cnt.p, iofs.p, n_items, s);
+        uint64_t T = read_scalar(iofs.p + n_items, s);
+        if (T > 0xFFFFFFFFull) B2SR_THROW(B2SR_EFORMAT, "tile count exceeds 32-bit index range");
+        b2sr_matrix *m = new_matrix(n, d, ntr, T, s);
+        try {
+            LAUNCH(k_conv_trp, (ntr + 256) / 256, 256, 0, s, ntr, pofs.p, iofs.p, m->trp);
+            if (T) {
+                const unsigned g = (unsigned)std::min<uint64_t>(((uint64_t)n_items + 7) / 8, (uint64_t)num_sms() * 8);
+                if (d == 4) LAUNCH(k_conv_compact<1>, g, 256, 0, s, n_items, toff.p, iofs.p, stci.p, stiles.p, m->tci, (uint32_t *)m->tiles);
+                else LAUNCH(k_conv_compact<2>, g, 256, 0, s, n_items, toff.p, iofs.p, stci.p, stiles.p, m->tci, (uint32_t *)m->tiles);
+            }
+        } catch (...) {
+            free_matrix(m);
+            throw;
+        }
+        return m;
+    }
     if (merge) {
         big = Buf<uint8_t>(std::max<uint32_t>(n_items, 1), s);
         CK(cudaMemsetAsync(big.p, 0, n_items, s));
