@@ -240,6 +240,8 @@ void exclusive_scan_u64(const uint64_t *in, uint64_t *out, size_t n, cudaStream_
 size_t radix_sort_pairs_u32(uint32_t *keys, uint32_t *vals, size_t n, int bits, cudaStream_t s,
                             uint32_t **keys_out, uint32_t **vals_out, Buf<uint32_t> *kalt,
                             Buf<uint32_t> *valt);
+void radix_sort_unpack4(uint64_t *keys, size_t n, int bits, uint32_t ntr, uint32_t *trp, uint32_t *tci,
+                        uint32_t *tiles, cudaStream_t s);
 void radix_sort_keys_u64(uint64_t *keys, size_t n, int bits, cudaStream_t s, uint64_t **keys_out,
                          Buf<uint64_t> *kalt);
 

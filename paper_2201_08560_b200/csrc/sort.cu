@@ -14,7 +14,7 @@ namespace b2sr {
 constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_ROUNDS = 8;   // 16: 122 registers, 2 CTAs per SM
-constexpr int RS_TILE = RS_THREADS * RS_ROUNDS;  // 4096 keys per CTA
+constexpr int RS_TILE = RS_THREADS * RS_ROUNDS;  // 2048 keys per CTA
 
 template <typename K>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K *__restrict__ keys, size_t n, int sh, uint32_t dm,
@@ -32,11 +32,32 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K *__restrict__ ke
     counts[(size_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
 }
 
-template <typename K, bool VALS>
+// The d = 4 transpose's last pass writes the transposed matrix itself instead
+// of the sorted keys (key = column | row << cb | 16-bit tile << 2 cb): the row
+// as the new tile column, the bit-transposed tile, and tile_row_ptr -- a
+// column's first element inside its CTA digit run fills (previous column,
+// column] (empty columns included); an element that opens a CTA digit run
+// does not know its predecessor and takes atomicMin on its own column; the
+// columns left unset are closed by a suffix minimum afterwards.
+struct Unpack4 {
+    uint32_t *trp, *tci, *tiles;
+    int cb;
+};
+
+__device__ __forceinline__ uint32_t tr4x4(uint32_t x) {  // 4x4 bit transpose, rows -> bytes
+    uint32_t t = (x ^ (x >> 3)) & 0x0A0Au;
+    x ^= t ^ (t << 3);
+    t = (x ^ (x >> 6)) & 0x00CCu;
+    x ^= t ^ (t << 6);
+    return (x & 0xFu) | ((x & 0xF0u) << 4) | ((x & 0xF00u) << 8) | ((x & 0xF000u) << 12);
+}
+
+template <typename K, bool VALS, bool UNPACK = false>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
                                                            K *__restrict__ kout, uint32_t *__restrict__ vout,
                                                            size_t n, int sh, uint32_t dm,
-                                                           const uint64_t *__restrict__ offs, uint32_t nblocks) {
+                                                           const uint64_t *__restrict__ offs, uint32_t nblocks,
+                                                           Unpack4 up = {}) {
     __shared__ uint32_t wc[RS_WARPS][256];
     __shared__ uint32_t dbase[256];            // CTA-local start of each digit run
     __shared__ K skey[RS_TILE];                // keys re-ordered by digit inside the CTA
@@ -116,10 +137,88 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__
         K k = skey[lp];
         uint32_t dg = (uint32_t)(k >> sh) & dm;
         size_t pos = goff[dg] + (lp - dbase[dg]);
-        kout[pos] = k;
-        if constexpr (VALS) vout[pos] = sval[lp];
+        if constexpr (UNPACK) {
+            const uint64_t cm = (1ull << up.cb) - 1;
+            const uint32_t col = (uint32_t)(k & cm);
+            up.tci[pos] = (uint32_t)((k >> up.cb) & cm);  // the source row is the transposed column
+            up.tiles[pos] = tr4x4((uint32_t)(k >> (2 * up.cb)) & 0xFFFFu);
+            if (lp == dbase[dg]) {
+                atomicMin(up.trp + col, (uint32_t)pos);
+            } else {
+                const uint32_t pc = (uint32_t)(skey[lp - 1] & cm);
+                for (uint32_t q = pc + 1; q <= col; q++) up.trp[q] = (uint32_t)pos;
+            }
+        } else {
+            kout[pos] = k;
+            if constexpr (VALS) vout[pos] = sval[lp];
+        }
     }
 }
+
+// tile_row_ptr[q] = min over c >= q of the marks (unset = ~0; the last entry
+// is set to `last` here): block minima, an exclusive suffix minimum over the
+// blocks (one CTA), then a block-local suffix minimum
+constexpr int SM_TILE = 1024;
+__global__ void __launch_bounds__(SM_TILE) k_sufmin_blocks(uint32_t m, uint32_t *__restrict__ a, uint32_t last,
+                                                           uint32_t *__restrict__ bmin) {
+    const uint32_t i = blockIdx.x * SM_TILE + threadIdx.x;
+    uint32_t v = 0xFFFFFFFFu;
+    if (i + 1 == m) a[i] = v = last;
+    else if (i < m) v = a[i];
+    v = __reduce_min_sync(0xffffffffu, v);
+    __shared__ uint32_t w[SM_TILE / 32];
+    if (lane_id() == 0) w[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = __reduce_min_sync(0xffffffffu, w[threadIdx.x]);
+        if (threadIdx.x == 0) bmin[blockIdx.x] = v;
+    }
+}
+
+// block-wide inclusive suffix minimum of one value per thread
+__device__ __forceinline__ uint32_t block_sufmin(uint32_t v, uint32_t *w) {
+    const uint32_t lane = lane_id(), wi = threadIdx.x >> 5;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_down_sync(0xffffffffu, v, o);
+        if (lane + o < 32) v = min(v, y);
+    }
+    if (lane == 0) w[wi] = v;
+    __syncthreads();
+    uint32_t rest = 0xFFFFFFFFu;
+    for (uint32_t ww = wi + 1; ww < SM_TILE / 32; ww++) rest = min(rest, w[ww]);
+    __syncthreads();
+    return min(v, rest);
+}
+
+__global__ void __launch_bounds__(SM_TILE) k_sufmin_scan(uint32_t nb, uint32_t *__restrict__ bmin) {
+    __shared__ uint32_t w[SM_TILE / 32];
+    uint32_t carry = 0xFFFFFFFFu;  // minimum of the blocks after this chunk
+    for (int64_t c0 = ((int64_t)(nb - 1) / SM_TILE) * SM_TILE; c0 >= 0; c0 -= SM_TILE) {
+        const uint32_t i = (uint32_t)c0 + threadIdx.x;
+        const uint32_t v = i < nb ? bmin[i] : 0xFFFFFFFFu;
+        const uint32_t inc = min(block_sufmin(v, w), carry);
+        // exclusive: the minimum strictly after block i
+        const uint32_t nxt = __shfl_down_sync(0xffffffffu, inc, 1);
+        __shared__ uint32_t first[SM_TILE / 32];
+        if (lane_id() == 0) first[threadIdx.x >> 5] = inc;
+        __syncthreads();
+        uint32_t ex = lane_id() < 31 ? nxt : ((threadIdx.x >> 5) + 1 < SM_TILE / 32 ? first[(threadIdx.x >> 5) + 1] : carry);
+        const uint32_t c_new = first[0];
+        __syncthreads();
+        if (i < nb) bmin[i] = ex;
+        carry = c_new;
+    }
+}
+
+__global__ void __launch_bounds__(SM_TILE) k_sufmin_apply(uint32_t m, uint32_t *__restrict__ a,
+                                                          const uint32_t *__restrict__ after) {
+    __shared__ uint32_t w[SM_TILE / 32];
+    const uint32_t i = blockIdx.x * SM_TILE + threadIdx.x;
+    const uint32_t v = i < m ? a[i] : 0xFFFFFFFFu;
+    const uint32_t r = min(block_sufmin(v, w), after[blockIdx.x]);
+    if (i < m) a[i] = r;
+}
+
 template <typename K, bool VALS>
 static void rs_passes(K *ka, uint32_t *va, K *kb, uint32_t *vb, size_t n, int bits, cudaStream_t s, K **kres,
                       uint32_t **vres) {
@@ -134,7 +233,8 @@ static void rs_passes(K *ka, uint32_t *va, K *kb, uint32_t *vb, size_t n, int bi
         const uint32_t dm = bits - sh >= 8 ? 0xFFu : (1u << (bits - sh)) - 1u;
         LAUNCH(k_rs_hist<K>, nblocks, RS_THREADS, 0, s, kin, n, sh, dm, counts.p, nblocks);
         exclusive_scan_u32_to_u64(counts.p, offs.p, (size_t)nblocks * 256, s);
-        LAUNCH((k_rs_scatter<K, VALS>), nblocks, RS_THREADS, 0, s, kin, vin, kout, vout, n, sh, dm, offs.p, nblocks);
+        LAUNCH((k_rs_scatter<K, VALS>), nblocks, RS_THREADS, 0, s, kin, vin, kout, vout, n, sh, dm, offs.p, nblocks,
+               Unpack4{});
         std::swap(kin, kout);
         std::swap(vin, vout);
     }
@@ -153,6 +253,36 @@ size_t radix_sort_pairs_u32(uint32_t *keys, uint32_t *vals, size_t n, int bits, 
     }
     rs_passes<uint32_t, true>(keys, vals, kalt->p, valt->p, n, bits, s, keys_out, vals_out);
     return n;
+}
+
+// The d = 4 transpose: LSD passes over the column bits, the last one writing
+// the transposed matrix (Unpack4 above).  trp has ntr + 1 entries.
+void radix_sort_unpack4(uint64_t *keys, size_t n, int bits, uint32_t ntr, uint32_t *trp, uint32_t *tci,
+                        uint32_t *tiles, cudaStream_t s) {
+    Buf<uint64_t> kalt(n, s);
+    const uint32_t nblocks = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
+    Buf<uint32_t> counts((size_t)nblocks * 256, s);
+    Buf<uint64_t> offs((size_t)nblocks * 256 + 1, s);
+    CK(cudaMemsetAsync(trp, 0xFF, ((size_t)ntr + 1) * 4, s));
+    uint64_t *kin = keys, *kout = kalt.p;
+    for (int sh = 0; sh < bits; sh += 8) {
+        const uint32_t dm = bits - sh >= 8 ? 0xFFu : (1u << (bits - sh)) - 1u;
+        LAUNCH(k_rs_hist<uint64_t>, nblocks, RS_THREADS, 0, s, kin, n, sh, dm, counts.p, nblocks);
+        exclusive_scan_u32_to_u64(counts.p, offs.p, (size_t)nblocks * 256, s);
+        if (sh + 8 >= bits) {
+            LAUNCH((k_rs_scatter<uint64_t, false, true>), nblocks, RS_THREADS, 0, s, kin, nullptr, kout, nullptr, n, sh,
+                   dm, offs.p, nblocks, Unpack4{trp, tci, tiles, bits});
+        } else {
+            LAUNCH((k_rs_scatter<uint64_t, false>), nblocks, RS_THREADS, 0, s, kin, nullptr, kout, nullptr, n, sh, dm,
+                   offs.p, nblocks, Unpack4{});
+            std::swap(kin, kout);
+        }
+    }
+    const uint32_t m = ntr + 1, nb = (m + SM_TILE - 1) / SM_TILE;
+    Buf<uint32_t> bmin(nb, s);
+    LAUNCH(k_sufmin_blocks, nb, SM_TILE, 0, s, m, trp, (uint32_t)n, bmin.p);
+    LAUNCH(k_sufmin_scan, 1, SM_TILE, 0, s, nb, bmin.p);
+    LAUNCH(k_sufmin_apply, nb, SM_TILE, 0, s, m, trp, bmin.p);
 }
 
 void radix_sort_keys_u64(uint64_t *keys, size_t n, int bits, cudaStream_t s, uint64_t **keys_out,

@@ -124,6 +124,101 @@ __global__ void k_pack4(uint64_t T, const uint32_t *__restrict__ rowid, const ui
     }
 }
 
+// k_pack4 without the row-id array: a CTA packs PK_TILES consecutive tiles and
+// recovers their rows from tile_row_ptr in shared memory.  Q(x) = #{r in
+// [1, ntr] : trp[r] <= x} is the row of tile x; the rows that start inside the
+// CTA's range are r in (Q(t0), Q(t0 + PK_TILES - 1)], each adds one at its
+// start position, and an inclusive scan over the positions gives every tile's
+// row (empty rows add at the same position: no special case).  Saves the row-id
+// pass (a 4-byte write and read per tile).
+constexpr int PK_THREADS = 256, PK_PER = 8, PK_TILES = PK_THREADS * PK_PER;
+
+__global__ void k_pack4_bounds(uint64_t T, uint32_t ntr, const uint32_t *__restrict__ trp, uint32_t nb,
+                               uint32_t *__restrict__ q) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nb) return;
+    const uint64_t t0 = (uint64_t)b * PK_TILES, te = min(T - 1, t0 + PK_TILES - 1);
+    for (int k = 0; k < 2; k++) {
+        const uint64_t x = k ? te : t0;
+        uint32_t lo = 1, hi = ntr + 1;  // first r in [1, ntr] with trp[r] > x
+        while (lo < hi) {
+            const uint32_t m = (lo + hi) >> 1;
+            if (trp[m] <= x) lo = m + 1; else hi = m;
+        }
+        q[2 * b + k] = lo - 1;
+    }
+}
+
+__global__ void __launch_bounds__(PK_THREADS) k_pack4_rows(uint64_t T, const uint32_t *__restrict__ trp,
+                                                           const uint32_t *__restrict__ q,
+                                                           const uint32_t *__restrict__ tci,
+                                                           const uint32_t *__restrict__ tiles, int cb,
+                                                           uint64_t *__restrict__ keys) {
+    __shared__ uint32_t cnt[PK_TILES];
+    __shared__ uint32_t wsum[PK_THREADS / 32];
+    const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5;
+    const uint64_t t0 = (uint64_t)blockIdx.x * PK_TILES;
+    for (int j = 0; j < PK_PER; j++) cnt[j * PK_THREADS + tid] = 0;
+    // this CTA's tiles: loads issued before the row recovery
+    uint32_t c[PK_PER], v[PK_PER];
+    const uint64_t tb = t0 + tid * PK_PER;
+    if (tb + PK_PER <= T) {  // 32-byte aligned: two 16-byte loads per array
+        const uint4 c0 = reinterpret_cast<const uint4 *>(tci + tb)[0], c1 = reinterpret_cast<const uint4 *>(tci + tb)[1];
+        const uint4 v0 = reinterpret_cast<const uint4 *>(tiles + tb)[0], v1 = reinterpret_cast<const uint4 *>(tiles + tb)[1];
+        c[0] = c0.x; c[1] = c0.y; c[2] = c0.z; c[3] = c0.w; c[4] = c1.x; c[5] = c1.y; c[6] = c1.z; c[7] = c1.w;
+        v[0] = v0.x; v[1] = v0.y; v[2] = v0.z; v[3] = v0.w; v[4] = v1.x; v[5] = v1.y; v[6] = v1.z; v[7] = v1.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < PK_PER; j++) {
+            const uint64_t t = tb + j;
+            c[j] = t < T ? tci[t] : 0u;
+            v[j] = t < T ? tiles[t] : 0u;
+        }
+    }
+    __syncthreads();
+    const uint32_t qa = q[2 * blockIdx.x], qb = q[2 * blockIdx.x + 1];
+    for (uint32_t r = qa + 1 + tid; r <= qb; r += PK_THREADS) atomicAdd(&cnt[trp[r] - t0], 1u);
+    __syncthreads();
+    // inclusive scan over the positions: thread tid owns positions [tid*8, tid*8+8)
+    uint32_t loc[PK_PER], run = 0;
+#pragma unroll
+    for (int j = 0; j < PK_PER; j++) {
+        run += cnt[tid * PK_PER + j];
+        loc[j] = run;
+    }
+    uint32_t inc = run;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= (uint32_t)o) inc += y;
+    }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    uint32_t off = inc - run;
+    for (uint32_t ww = 0; ww < w; ww++) off += wsum[ww];
+    uint64_t k[PK_PER];
+#pragma unroll
+    for (int j = 0; j < PK_PER; j++) {
+        const uint32_t row = qa + off + loc[j];
+        const uint32_t x = v[j];
+        const uint32_t nib = (x & 0xFu) | ((x >> 4) & 0xF0u) | ((x >> 8) & 0xF00u) | ((x >> 12) & 0xF000u);
+        k[j] = (uint64_t)c[j] | ((uint64_t)row << cb) | ((uint64_t)nib << (2 * cb));
+    }
+    if (tb + PK_PER <= T) {
+        ulonglong2 *o = reinterpret_cast<ulonglong2 *>(keys + tb);
+#pragma unroll
+        for (int j = 0; j < PK_PER / 2; j++) o[j] = make_ulonglong2(k[2 * j], k[2 * j + 1]);
+    } else {
+#pragma unroll
+        for (int j = 0; j < PK_PER; j++)
+            if (tb + j < T) keys[tb + j] = k[j];
+    }
+}
+
+static bool pack_rows_enabled() {  // B2SR_TR_PACK=rowid: the row-id array + k_pack4 (A/B)
+    const char *e = getenv("B2SR_TR_PACK");
+    return !(e && !strcmp(e, "rowid"));
+}
+
 // tile_row_ptr of the transpose from the column-sorted keys: position p starts
 // every column in (column of p-1, column of p]; the last position closes the
 // columns up to ntr (replaces a column histogram of T global atomics + scan)
@@ -512,14 +607,24 @@ b2sr_matrix *transpose_device(const b2sr_matrix *m, cudaStream_t s) {
             CK(cudaMemsetAsync(o->trp, 0, ((size_t)ntr + 1) * 4, s));
         } else if (m->dim == 4 && 2 * cb + 16 <= 64) {
             Buf<uint64_t> keys(T, s), kalt;
-            {
+            if (pack_rows_enabled()) {
+                const uint32_t nb = (uint32_t)((T + PK_TILES - 1) / PK_TILES);
+                Buf<uint32_t> q(2 * (size_t)nb, s);
+                LAUNCH(k_pack4_bounds, (nb + 255) / 256, 256, 0, s, T, ntr, m->trp, nb, q.p);
+                LAUNCH(k_pack4_rows, nb, PK_THREADS, 0, s, T, m->trp, q.p, m->tci, (const uint32_t *)m->tiles, cb, keys.p);
+            } else {
                 Buf<uint32_t> rowid(T, s);
                 LAUNCH(k_row_ids, grid_for((uint64_t)ntr * 32), 256, 0, s, ntr, m->trp, rowid.p);
                 LAUNCH(k_pack4, grid_for(T), 256, 0, s, T, rowid.p, m->tci, (const uint32_t *)m->tiles, cb, keys.p);
             }
-            uint64_t *ks = nullptr;
-            radix_sort_keys_u64(keys.p, T, cb, s, &ks, &kalt);
-            LAUNCH(k_unpack4, grid_for(T), 256, 0, s, T, ks, cb, ntr, o->trp, o->tci, (uint32_t *)o->tiles);
+            const char *ue = getenv("B2SR_TR_UNPACK");  // 0: sorted keys + k_unpack4 (A/B)
+            if (ue && ue[0] == '0') {
+                uint64_t *ks = nullptr;
+                radix_sort_keys_u64(keys.p, T, cb, s, &ks, &kalt);
+                LAUNCH(k_unpack4, grid_for(T), 256, 0, s, T, ks, cb, ntr, o->trp, o->tci, (uint32_t *)o->tiles);
+            } else {  // the last sort pass writes the transpose (sort.cu, Unpack4)
+                radix_sort_unpack4(keys.p, T, cb, ntr, o->trp, o->tci, (uint32_t *)o->tiles, s);
+            }
         } else {
             Buf<uint32_t> keys(T, s), vals(T, s), rowid(T, s), kalt, valt;
             CK(cudaMemcpyAsync(keys.p, m->tci, T * 4, cudaMemcpyDeviceToDevice, s));
