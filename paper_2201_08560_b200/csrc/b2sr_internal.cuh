@@ -240,8 +240,11 @@ void exclusive_scan_u64(const uint64_t *in, uint64_t *out, size_t n, cudaStream_
 size_t radix_sort_pairs_u32(uint32_t *keys, uint32_t *vals, size_t n, int bits, cudaStream_t s,
                             uint32_t **keys_out, uint32_t **vals_out, Buf<uint32_t> *kalt,
                             Buf<uint32_t> *valt);
+// keys per CTA tile of the radix passes (sort.cu); counts0, when given, holds
+// the first pass's per-tile digit counts (digit-major, RADIX_TILE keys per tile)
+constexpr int RADIX_TILE = 2048;
 void radix_sort_unpack4(uint64_t *keys, size_t n, int bits, uint32_t ntr, uint32_t *trp, uint32_t *tci,
-                        uint32_t *tiles, cudaStream_t s);
+                        uint32_t *tiles, cudaStream_t s, const uint32_t *counts0 = nullptr);
 void radix_sort_keys_u64(uint64_t *keys, size_t n, int bits, cudaStream_t s, uint64_t **keys_out,
                          Buf<uint64_t> *kalt);
 

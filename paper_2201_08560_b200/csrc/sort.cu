@@ -15,6 +15,7 @@ constexpr int RS_THREADS = 256;
 constexpr int RS_WARPS = RS_THREADS / 32;
 constexpr int RS_ROUNDS = 8;   // 16: 122 registers, 2 CTAs per SM
 constexpr int RS_TILE = RS_THREADS * RS_ROUNDS;  // 2048 keys per CTA
+static_assert(RS_TILE == RADIX_TILE, "k_pack4_rows counts the first digit over the same tiles");
 
 template <typename K>
 __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const K *__restrict__ keys, size_t n, int sh, uint32_t dm,
@@ -258,7 +259,7 @@ size_t radix_sort_pairs_u32(uint32_t *keys, uint32_t *vals, size_t n, int bits, 
 // The d = 4 transpose: LSD passes over the column bits, the last one writing
 // the transposed matrix (Unpack4 above).  trp has ntr + 1 entries.
 void radix_sort_unpack4(uint64_t *keys, size_t n, int bits, uint32_t ntr, uint32_t *trp, uint32_t *tci,
-                        uint32_t *tiles, cudaStream_t s) {
+                        uint32_t *tiles, cudaStream_t s, const uint32_t *counts0) {
     Buf<uint64_t> kalt(n, s);
     const uint32_t nblocks = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
     Buf<uint32_t> counts((size_t)nblocks * 256, s);
@@ -267,8 +268,12 @@ void radix_sort_unpack4(uint64_t *keys, size_t n, int bits, uint32_t ntr, uint32
     uint64_t *kin = keys, *kout = kalt.p;
     for (int sh = 0; sh < bits; sh += 8) {
         const uint32_t dm = bits - sh >= 8 ? 0xFFu : (1u << (bits - sh)) - 1u;
-        LAUNCH(k_rs_hist<uint64_t>, nblocks, RS_THREADS, 0, s, kin, n, sh, dm, counts.p, nblocks);
-        exclusive_scan_u32_to_u64(counts.p, offs.p, (size_t)nblocks * 256, s);
+        if (sh == 0 && counts0) {
+            exclusive_scan_u32_to_u64(counts0, offs.p, (size_t)nblocks * 256, s);
+        } else {
+            LAUNCH(k_rs_hist<uint64_t>, nblocks, RS_THREADS, 0, s, kin, n, sh, dm, counts.p, nblocks);
+            exclusive_scan_u32_to_u64(counts.p, offs.p, (size_t)nblocks * 256, s);
+        }
         if (sh + 8 >= bits) {
             LAUNCH((k_rs_scatter<uint64_t, false, true>), nblocks, RS_THREADS, 0, s, kin, nullptr, kout, nullptr, n, sh,
                    dm, offs.p, nblocks, Unpack4{trp, tci, tiles, bits});

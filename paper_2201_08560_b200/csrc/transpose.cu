@@ -132,6 +132,7 @@ __global__ void k_pack4(uint64_t T, const uint32_t *__restrict__ rowid, const ui
 // row (empty rows add at the same position: no special case).  Saves the row-id
 // pass (a 4-byte write and read per tile).
 constexpr int PK_THREADS = 256, PK_PER = 8, PK_TILES = PK_THREADS * PK_PER;
+static_assert(PK_TILES == RADIX_TILE, "the first digit's counts are per radix tile");
 
 __global__ void k_pack4_bounds(uint64_t T, uint32_t ntr, const uint32_t *__restrict__ trp, uint32_t nb,
                                uint32_t *__restrict__ q) {
@@ -153,12 +154,15 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack4_rows(uint64_t T, const uin
                                                            const uint32_t *__restrict__ q,
                                                            const uint32_t *__restrict__ tci,
                                                            const uint32_t *__restrict__ tiles, int cb,
-                                                           uint64_t *__restrict__ keys) {
+                                                           uint64_t *__restrict__ keys, uint32_t *__restrict__ counts0,
+                                                           uint32_t dm0) {
     __shared__ uint32_t cnt[PK_TILES];
+    __shared__ uint32_t hist[256];  // the first radix pass's digit counts of this tile
     __shared__ uint32_t wsum[PK_THREADS / 32];
     const uint32_t tid = threadIdx.x, lane = lane_id(), w = tid >> 5;
     const uint64_t t0 = (uint64_t)blockIdx.x * PK_TILES;
     for (int j = 0; j < PK_PER; j++) cnt[j * PK_THREADS + tid] = 0;
+    hist[tid] = 0;
     // this CTA's tiles: loads issued before the row recovery
     uint32_t c[PK_PER], v[PK_PER];
     const uint64_t tb = t0 + tid * PK_PER;
@@ -195,6 +199,9 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack4_rows(uint64_t T, const uin
     __syncthreads();
     uint32_t off = inc - run;
     for (uint32_t ww = 0; ww < w; ww++) off += wsum[ww];
+#pragma unroll
+    for (int j = 0; j < PK_PER; j++)
+        if (tb + j < T) atomicAdd(&hist[c[j] & dm0], 1u);
     uint64_t k[PK_PER];
 #pragma unroll
     for (int j = 0; j < PK_PER; j++) {
@@ -212,6 +219,8 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack4_rows(uint64_t T, const uin
         for (int j = 0; j < PK_PER; j++)
             if (tb + j < T) keys[tb + j] = k[j];
     }
+    __syncthreads();
+    counts0[(size_t)tid * gridDim.x + blockIdx.x] = hist[tid];
 }
 
 static bool pack_rows_enabled() {  // B2SR_TR_PACK=rowid: the row-id array + k_pack4 (A/B)
@@ -607,11 +616,14 @@ b2sr_matrix *transpose_device(const b2sr_matrix *m, cudaStream_t s) {
             CK(cudaMemsetAsync(o->trp, 0, ((size_t)ntr + 1) * 4, s));
         } else if (m->dim == 4 && 2 * cb + 16 <= 64) {
             Buf<uint64_t> keys(T, s), kalt;
+            Buf<uint32_t> counts0;
             if (pack_rows_enabled()) {
                 const uint32_t nb = (uint32_t)((T + PK_TILES - 1) / PK_TILES);
                 Buf<uint32_t> q(2 * (size_t)nb, s);
+                counts0 = Buf<uint32_t>((size_t)nb * 256, s);
                 LAUNCH(k_pack4_bounds, (nb + 255) / 256, 256, 0, s, T, ntr, m->trp, nb, q.p);
-                LAUNCH(k_pack4_rows, nb, PK_THREADS, 0, s, T, m->trp, q.p, m->tci, (const uint32_t *)m->tiles, cb, keys.p);
+                LAUNCH(k_pack4_rows, nb, PK_THREADS, 0, s, T, m->trp, q.p, m->tci, (const uint32_t *)m->tiles, cb, keys.p,
+                       counts0.p, cb >= 8 ? 0xFFu : (1u << cb) - 1u);
             } else {
                 Buf<uint32_t> rowid(T, s);
                 LAUNCH(k_row_ids, grid_for((uint64_t)ntr * 32), 256, 0, s, ntr, m->trp, rowid.p);
@@ -623,7 +635,8 @@ b2sr_matrix *transpose_device(const b2sr_matrix *m, cudaStream_t s) {
                 radix_sort_keys_u64(keys.p, T, cb, s, &ks, &kalt);
                 LAUNCH(k_unpack4, grid_for(T), 256, 0, s, T, ks, cb, ntr, o->trp, o->tci, (uint32_t *)o->tiles);
             } else {  // the last sort pass writes the transpose (sort.cu, Unpack4)
-                radix_sort_unpack4(keys.p, T, cb, ntr, o->trp, o->tci, (uint32_t *)o->tiles, s);
+                radix_sort_unpack4(keys.p, T, cb, ntr, o->trp, o->tci, (uint32_t *)o->tiles, s,
+                                   counts0.p ? counts0.p : nullptr);
             }
         } else {
             Buf<uint32_t> keys(T, s), vals(T, s), rowid(T, s), kalt, valt;

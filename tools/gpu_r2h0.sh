@@ -1,0 +1,6 @@
+set -x
+O=gpurun_out
+timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py -q -x -p no:cacheprovider -k 'transpose or rmat or random or roundtrip' 2>&1 | tail -3
+for r in 1 2; do for v in rowid rows; do B2SR_TR_PACK=$v timeout -s KILL 300 python tools/conv_ab.py 22 4; done; done
+timeout -s KILL 300 python tools/conv_ab.py 24 4
+timeout -s KILL 300 python tools/conv_ab.py 20 4,8
