@@ -53,16 +53,28 @@ __device__ __forceinline__ uint32_t tr4x4(uint32_t x) {  // 4x4 bit transpose, r
     return (x & 0xFu) | ((x & 0xF0u) << 4) | ((x & 0xF00u) << 8) | ((x & 0xF000u) << 12);
 }
 
-template <typename K, bool VALS, bool UNPACK = false>
-__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__ kin, const uint32_t *__restrict__ vin,
-                                                           K *__restrict__ kout, uint32_t *__restrict__ vout,
+__device__ __forceinline__ uint64_t tr8x8(uint64_t x) {  // 8x8 bit transpose, rows in bytes
+    uint64_t t = (x ^ (x >> 7)) & 0x00AA00AA00AA00AAull;
+    x ^= t ^ (t << 7);
+    t = (x ^ (x >> 14)) & 0x0000CCCC0000CCCCull;
+    x ^= t ^ (t << 14);
+    t = (x ^ (x >> 28)) & 0x00000000F0F0F0F0ull;
+    x ^= t ^ (t << 28);
+    return x;
+}
+
+// V = uint64_t carries the d = 8 tile through the passes (UNPACK: the last
+// pass writes the transpose from key (column | row) and value (tile))
+template <typename K, bool VALS, bool UNPACK = false, typename V = uint32_t>
+__global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__ kin, const V *__restrict__ vin,
+                                                           K *__restrict__ kout, V *__restrict__ vout,
                                                            size_t n, int sh, uint32_t dm,
                                                            const uint64_t *__restrict__ offs, uint32_t nblocks,
                                                            Unpack4 up = {}) {
     __shared__ uint32_t wc[RS_WARPS][256];
     __shared__ uint32_t dbase[256];            // CTA-local start of each digit run
     __shared__ K skey[RS_TILE];                // keys re-ordered by digit inside the CTA
-    __shared__ uint32_t sval[VALS ? RS_TILE : 1];
+    __shared__ V sval[VALS ? RS_TILE : 1];
     __shared__ uint64_t goff[256];             // this CTA's global start of each digit run
     const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
     for (int b = threadIdx.x; b < RS_WARPS * 256; b += RS_THREADS) (&wc[0][0])[b] = 0;
@@ -71,7 +83,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__
     __syncthreads();
     size_t base = (size_t)blockIdx.x * RS_TILE + (size_t)w * (32 * RS_ROUNDS);
     K key[RS_ROUNDS];
-    uint32_t val[RS_ROUNDS];
+    V val[RS_ROUNDS];
     uint32_t rank[RS_ROUNDS];
     const uint32_t lt = (1u << lane) - 1u;
 #pragma unroll
@@ -79,7 +91,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__
         size_t i = base + (size_t)j * 32 + lane;
         bool ok = i < n;
         key[j] = ok ? kin[i] : (K)0;
-        if constexpr (VALS) val[j] = ok ? vin[i] : 0u;
+        if constexpr (VALS) val[j] = ok ? vin[i] : (V)0;
         uint32_t dg = ok ? ((uint32_t)(key[j] >> sh) & dm) : 256u;  // 256 = no item
         // lanes with the same digit: nine ballots (8 digit bits + the no-item
         // flag) instead of __match_any_sync (MATCH.ANY is a slow, multi-pass
@@ -142,7 +154,8 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const K *__restrict__
             const uint64_t cm = (1ull << up.cb) - 1;
             const uint32_t col = (uint32_t)(k & cm);
             up.tci[pos] = (uint32_t)((k >> up.cb) & cm);  // the source row is the transposed column
-            up.tiles[pos] = tr4x4((uint32_t)(k >> (2 * up.cb)) & 0xFFFFu);
+            if constexpr (sizeof(V) == 8) reinterpret_cast<uint64_t *>(up.tiles)[pos] = tr8x8((uint64_t)sval[lp]);
+            else up.tiles[pos] = tr4x4((uint32_t)(k >> (2 * up.cb)) & 0xFFFFu);
             if (lp == dbase[dg]) {
                 atomicMin(up.trp + col, (uint32_t)pos);
             } else {
@@ -275,12 +288,47 @@ void radix_sort_unpack4(uint64_t *keys, size_t n, int bits, uint32_t ntr, uint32
             exclusive_scan_u32_to_u64(counts.p, offs.p, (size_t)nblocks * 256, s);
         }
         if (sh + 8 >= bits) {
-            LAUNCH((k_rs_scatter<uint64_t, false, true>), nblocks, RS_THREADS, 0, s, kin, nullptr, kout, nullptr, n, sh,
+            LAUNCH((k_rs_scatter<uint64_t, false, true, uint32_t>), nblocks, RS_THREADS, 0, s, kin, (const uint32_t *)nullptr, kout, (uint32_t *)nullptr, n, sh,
                    dm, offs.p, nblocks, Unpack4{trp, tci, tiles, bits});
         } else {
-            LAUNCH((k_rs_scatter<uint64_t, false>), nblocks, RS_THREADS, 0, s, kin, nullptr, kout, nullptr, n, sh, dm,
+            LAUNCH((k_rs_scatter<uint64_t, false, false, uint32_t>), nblocks, RS_THREADS, 0, s, kin, (const uint32_t *)nullptr, kout, (uint32_t *)nullptr, n, sh, dm,
                    offs.p, nblocks, Unpack4{});
             std::swap(kin, kout);
+        }
+    }
+    const uint32_t m = ntr + 1, nb = (m + SM_TILE - 1) / SM_TILE;
+    Buf<uint32_t> bmin(nb, s);
+    LAUNCH(k_sufmin_blocks, nb, SM_TILE, 0, s, m, trp, (uint32_t)n, bmin.p);
+    LAUNCH(k_sufmin_scan, 1, SM_TILE, 0, s, nb, bmin.p);
+    LAUNCH(k_sufmin_apply, nb, SM_TILE, 0, s, m, trp, bmin.p);
+}
+
+// The d = 8 transpose: (column | row) keys with the 8-byte tile as the value,
+// the last pass writing the transpose (no random tile / row-id gathers).
+void radix_sort_unpack8(uint64_t *keys, uint64_t *vals, size_t n, int bits, uint32_t ntr, uint32_t *trp, uint32_t *tci,
+                        uint64_t *tiles, cudaStream_t s, const uint32_t *counts0) {
+    Buf<uint64_t> kalt(n, s), valt(n, s);
+    const uint32_t nblocks = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
+    Buf<uint32_t> counts((size_t)nblocks * 256, s);
+    Buf<uint64_t> offs((size_t)nblocks * 256 + 1, s);
+    CK(cudaMemsetAsync(trp, 0xFF, ((size_t)ntr + 1) * 4, s));
+    uint64_t *kin = keys, *kout = kalt.p, *vin = vals, *vout = valt.p;
+    for (int sh = 0; sh < bits; sh += 8) {
+        const uint32_t dm = bits - sh >= 8 ? 0xFFu : (1u << (bits - sh)) - 1u;
+        if (sh == 0 && counts0) {
+            exclusive_scan_u32_to_u64(counts0, offs.p, (size_t)nblocks * 256, s);
+        } else {
+            LAUNCH(k_rs_hist<uint64_t>, nblocks, RS_THREADS, 0, s, kin, n, sh, dm, counts.p, nblocks);
+            exclusive_scan_u32_to_u64(counts.p, offs.p, (size_t)nblocks * 256, s);
+        }
+        if (sh + 8 >= bits) {
+            LAUNCH((k_rs_scatter<uint64_t, true, true, uint64_t>), nblocks, RS_THREADS, 0, s, kin, vin, kout, vout, n, sh,
+                   dm, offs.p, nblocks, Unpack4{trp, tci, reinterpret_cast<uint32_t *>(tiles), bits});
+        } else {
+            LAUNCH((k_rs_scatter<uint64_t, true, false, uint64_t>), nblocks, RS_THREADS, 0, s, kin, vin, kout, vout, n,
+                   sh, dm, offs.p, nblocks, Unpack4{});
+            std::swap(kin, kout);
+            std::swap(vin, vout);
         }
     }
     const uint32_t m = ntr + 1, nb = (m + SM_TILE - 1) / SM_TILE;

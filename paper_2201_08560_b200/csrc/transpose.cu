@@ -6,6 +6,8 @@
 // thread per tile, 16-byte loads/stores of whole tiles).  The reference
 // unpacks every tile into a (T, d, d) uint64 temporary (~16*d^2 bytes per
 // tile); here the working set is 16 bytes of indices per tile.
+#include <type_traits>
+
 #include "b2sr_internal.cuh"
 
 namespace b2sr {
@@ -150,12 +152,17 @@ __global__ void k_pack4_bounds(uint64_t T, uint32_t ntr, const uint32_t *__restr
     }
 }
 
-__global__ void __launch_bounds__(PK_THREADS) k_pack4_rows(uint64_t T, const uint32_t *__restrict__ trp,
-                                                           const uint32_t *__restrict__ q,
-                                                           const uint32_t *__restrict__ tci,
-                                                           const uint32_t *__restrict__ tiles, int cb,
-                                                           uint64_t *__restrict__ keys, uint32_t *__restrict__ counts0,
-                                                           uint32_t dm0) {
+// D = 4: key = column | row << cb | 16-bit tile << 2 cb; D = 8: key = column |
+// row << cb and the 8-byte tile goes to vals
+template <int D>
+__global__ void __launch_bounds__(PK_THREADS) k_pack_rows(uint64_t T, const uint32_t *__restrict__ trp,
+                                                          const uint32_t *__restrict__ q,
+                                                          const uint32_t *__restrict__ tci,
+                                                          const void *__restrict__ tiles_, int cb,
+                                                          uint64_t *__restrict__ keys, uint64_t *__restrict__ vals,
+                                                          uint32_t *__restrict__ counts0, uint32_t dm0) {
+    using TW = typename std::conditional<D == 4, uint32_t, uint64_t>::type;  // one tile
+    const TW *__restrict__ tiles = static_cast<const TW *>(tiles_);
     __shared__ uint32_t cnt[PK_TILES];
     __shared__ uint32_t hist[256];  // the first radix pass's digit counts of this tile
     __shared__ uint32_t wsum[PK_THREADS / 32];
@@ -164,19 +171,29 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack4_rows(uint64_t T, const uin
     for (int j = 0; j < PK_PER; j++) cnt[j * PK_THREADS + tid] = 0;
     hist[tid] = 0;
     // this CTA's tiles: loads issued before the row recovery
-    uint32_t c[PK_PER], v[PK_PER];
+    uint32_t c[PK_PER];
+    TW v[PK_PER];
     const uint64_t tb = t0 + tid * PK_PER;
-    if (tb + PK_PER <= T) {  // 32-byte aligned: two 16-byte loads per array
+    if (tb + PK_PER <= T) {  // 32-byte aligned: 16-byte loads
         const uint4 c0 = reinterpret_cast<const uint4 *>(tci + tb)[0], c1 = reinterpret_cast<const uint4 *>(tci + tb)[1];
-        const uint4 v0 = reinterpret_cast<const uint4 *>(tiles + tb)[0], v1 = reinterpret_cast<const uint4 *>(tiles + tb)[1];
         c[0] = c0.x; c[1] = c0.y; c[2] = c0.z; c[3] = c0.w; c[4] = c1.x; c[5] = c1.y; c[6] = c1.z; c[7] = c1.w;
-        v[0] = v0.x; v[1] = v0.y; v[2] = v0.z; v[3] = v0.w; v[4] = v1.x; v[5] = v1.y; v[6] = v1.z; v[7] = v1.w;
+        if constexpr (D == 4) {
+            const uint4 v0 = reinterpret_cast<const uint4 *>(tiles + tb)[0], v1 = reinterpret_cast<const uint4 *>(tiles + tb)[1];
+            v[0] = v0.x; v[1] = v0.y; v[2] = v0.z; v[3] = v0.w; v[4] = v1.x; v[5] = v1.y; v[6] = v1.z; v[7] = v1.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < PK_PER / 2; j++) {
+                const ulonglong2 x = reinterpret_cast<const ulonglong2 *>(tiles + tb)[j];
+                v[2 * j] = x.x;
+                v[2 * j + 1] = x.y;
+            }
+        }
     } else {
 #pragma unroll
         for (int j = 0; j < PK_PER; j++) {
             const uint64_t t = tb + j;
             c[j] = t < T ? tci[t] : 0u;
-            v[j] = t < T ? tiles[t] : 0u;
+            v[j] = t < T ? tiles[t] : (TW)0;
         }
     }
     __syncthreads();
@@ -206,21 +223,37 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack4_rows(uint64_t T, const uin
 #pragma unroll
     for (int j = 0; j < PK_PER; j++) {
         const uint32_t row = qa + off + loc[j];
-        const uint32_t x = v[j];
-        const uint32_t nib = (x & 0xFu) | ((x >> 4) & 0xF0u) | ((x >> 8) & 0xF00u) | ((x >> 12) & 0xF000u);
-        k[j] = (uint64_t)c[j] | ((uint64_t)row << cb) | ((uint64_t)nib << (2 * cb));
+        k[j] = (uint64_t)c[j] | ((uint64_t)row << cb);
+        if constexpr (D == 4) {
+            const uint32_t x = v[j];
+            const uint32_t nib = (x & 0xFu) | ((x >> 4) & 0xF0u) | ((x >> 8) & 0xF00u) | ((x >> 12) & 0xF000u);
+            k[j] |= (uint64_t)nib << (2 * cb);
+        }
     }
     if (tb + PK_PER <= T) {
         ulonglong2 *o = reinterpret_cast<ulonglong2 *>(keys + tb);
 #pragma unroll
         for (int j = 0; j < PK_PER / 2; j++) o[j] = make_ulonglong2(k[2 * j], k[2 * j + 1]);
+        if constexpr (D == 8) {
+            ulonglong2 *ov = reinterpret_cast<ulonglong2 *>(vals + tb);
+#pragma unroll
+            for (int j = 0; j < PK_PER / 2; j++) ov[j] = make_ulonglong2(v[2 * j], v[2 * j + 1]);
+        }
     } else {
 #pragma unroll
         for (int j = 0; j < PK_PER; j++)
-            if (tb + j < T) keys[tb + j] = k[j];
+            if (tb + j < T) {
+                keys[tb + j] = k[j];
+                if constexpr (D == 8) vals[tb + j] = v[j];
+            }
     }
     __syncthreads();
     counts0[(size_t)tid * gridDim.x + blockIdx.x] = hist[tid];
+}
+
+static bool tr8_sort_enabled() {  // B2SR_TR8=gather: (column, tile id) sort + random gathers (A/B)
+    const char *e = getenv("B2SR_TR8");
+    return !(e && !strcmp(e, "gather"));
 }
 
 static bool pack_rows_enabled() {  // B2SR_TR_PACK=rowid: the row-id array + k_pack4 (A/B)
@@ -622,7 +655,7 @@ b2sr_matrix *transpose_device(const b2sr_matrix *m, cudaStream_t s) {
                 Buf<uint32_t> q(2 * (size_t)nb, s);
                 counts0 = Buf<uint32_t>((size_t)nb * 256, s);
                 LAUNCH(k_pack4_bounds, (nb + 255) / 256, 256, 0, s, T, ntr, m->trp, nb, q.p);
-                LAUNCH(k_pack4_rows, nb, PK_THREADS, 0, s, T, m->trp, q.p, m->tci, (const uint32_t *)m->tiles, cb, keys.p,
+                LAUNCH(k_pack_rows<4>, nb, PK_THREADS, 0, s, T, m->trp, q.p, m->tci, m->tiles, cb, keys.p, nullptr,
                        counts0.p, cb >= 8 ? 0xFFu : (1u << cb) - 1u);
             } else {
                 Buf<uint32_t> rowid(T, s);
@@ -638,6 +671,16 @@ b2sr_matrix *transpose_device(const b2sr_matrix *m, cudaStream_t s) {
                 radix_sort_unpack4(keys.p, T, cb, ntr, o->trp, o->tci, (uint32_t *)o->tiles, s,
                                    counts0.p ? counts0.p : nullptr);
             }
+        } else if (m->dim == 8 && 2 * cb <= 64 && tr8_sort_enabled()) {
+            // (column | row) keys carrying the 8-byte tile: the last pass writes
+            // the transpose, no random gathers of tiles and row ids
+            const uint32_t nb = (uint32_t)((T + PK_TILES - 1) / PK_TILES);
+            Buf<uint64_t> keys(T, s), vals(T, s);
+            Buf<uint32_t> q(2 * (size_t)nb, s), counts0((size_t)nb * 256, s);
+            LAUNCH(k_pack4_bounds, (nb + 255) / 256, 256, 0, s, T, ntr, m->trp, nb, q.p);
+            LAUNCH(k_pack_rows<8>, nb, PK_THREADS, 0, s, T, m->trp, q.p, m->tci, m->tiles, cb, keys.p, vals.p, counts0.p,
+                   cb >= 8 ? 0xFFu : (1u << cb) - 1u);
+            radix_sort_unpack8(keys.p, vals.p, T, cb, ntr, o->trp, o->tci, static_cast<uint64_t *>(o->tiles), s, counts0.p);
         } else {
             Buf<uint32_t> keys(T, s), vals(T, s), rowid(T, s), kalt, valt;
             CK(cudaMemcpyAsync(keys.p, m->tci, T * 4, cudaMemcpyDeviceToDevice, s));
