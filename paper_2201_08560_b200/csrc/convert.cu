@@ -562,20 +562,26 @@ b2sr_matrix *csr_to_b2sr_device(uint32_t n, uint32_t d, const uint32_t *row_ptr,
     Buf<uint32_t> cnt(n_items, s);
     Buf<uint64_t> iofs((size_t)n_items + 1, s);
     Buf<uint8_t> big;
-    if (merge && conv_fused_enabled() && !order) {
+    // d = 16 too (lock-step merge only): its count pass is a whole second
+    // merge, the staging costs 36 bytes per CSR entry (bounded below); at
+    // d = 32 (132 bytes per entry) moving the staged tiles costs what it saves
+    const uint64_t nnz = (merge || d == 16) && conv_fused_enabled() && !order ? read_scalar(row_ptr + n, s) : 0;
+    const uint32_t TWc = d == 4 ? 1 : d == 8 ? 2 : 8;  // u32 words per tile
+    if ((merge || (d == 16 && nnz * (4 + 4 * TWc) <= (24ull << 30))) && conv_fused_enabled() && !order) {
         // one merge pass: pack every item into staging arrays at the slot of its
         // first CSR entry (tiles <= entries), counting its tiles; scan; move
         // the items' tiles into the matrix.  Replaces the count pass.
-        const uint64_t nnz = read_scalar(row_ptr + n, s);
-        const uint32_t TW = d == 4 ? 1 : 2;
+        const uint32_t TW = TWc;
         Buf<uint32_t> stci(std::max<uint64_t>(nnz, 1), s), stiles(std::max<uint64_t>(nnz, 1) * TW, s);
         Buf<uint64_t> toff(std::max<uint32_t>(n_items, 1), s);
-        big = Buf<uint8_t>(std::max<uint32_t>(n_items, 1), s);
-        CK(cudaMemsetAsync(big.p, 0, n_items, s));
-        if (d == 4) merge_launch<4>(true, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, stci.p, stiles.p, big.p, s, toff.p);
-        else merge_launch<8>(true, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, stci.p, stiles.p, big.p, s, toff.p);
-        conv_dispatch(d, true, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, stci.p, stiles.p, s, nullptr, big.p,
-                      toff.p);
+        if (merge) {
+            big = Buf<uint8_t>(std::max<uint32_t>(n_items, 1), s);
+            CK(cudaMemsetAsync(big.p, 0, n_items, s));
+            if (d == 4) merge_launch<4>(true, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, stci.p, stiles.p, big.p, s, toff.p);
+            else merge_launch<8>(true, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, stci.p, stiles.p, big.p, s, toff.p);
+        }
+        conv_dispatch(d, true, items.p, n_items, n, row_ptr, col_ind, nullptr, cnt.p, stci.p, stiles.p, s, nullptr,
+                      merge ? big.p : nullptr, toff.p);
         exclusive_scan_u32_to_u64(cnt.p, iofs.p, n_items, s);
         uint64_t T = read_scalar(iofs.p + n_items, s);
         if (T > 0xFFFFFFFFull) B2SR_THROW(B2SR_EFORMAT, "tile count exceeds 32-bit index range");
@@ -585,7 +591,8 @@ b2sr_matrix *csr_to_b2sr_device(uint32_t n, uint32_t d, const uint32_t *row_ptr,
             if (T) {
                 const unsigned g = (unsigned)std::min<uint64_t>(((uint64_t)n_items + 7) / 8, (uint64_t)num_sms() * 8);
                 if (d == 4) LAUNCH(k_conv_compact<1>, g, 256, 0, s, n_items, toff.p, iofs.p, stci.p, stiles.p, m->tci, (uint32_t *)m->tiles);
-                else LAUNCH(k_conv_compact<2>, g, 256, 0, s, n_items, toff.p, iofs.p, stci.p, stiles.p, m->tci, (uint32_t *)m->tiles);
+                else if (d == 8) LAUNCH(k_conv_compact<2>, g, 256, 0, s, n_items, toff.p, iofs.p, stci.p, stiles.p, m->tci, (uint32_t *)m->tiles);
+                else LAUNCH(k_conv_compact<8>, g, 256, 0, s, n_items, toff.p, iofs.p, stci.p, stiles.p, m->tci, (uint32_t *)m->tiles);
             }
         } catch (...) {
             free_matrix(m);
