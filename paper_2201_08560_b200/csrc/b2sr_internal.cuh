@@ -245,6 +245,8 @@ size_t radix_sort_pairs_u32(uint32_t *keys, uint32_t *vals, size_t n, int bits, 
 constexpr int RADIX_TILE = 2048;
 void radix_sort_unpack4(uint64_t *keys, size_t n, int bits, uint32_t ntr, uint32_t *trp, uint32_t *tci,
                         uint32_t *tiles, cudaStream_t s, const uint32_t *counts0 = nullptr);
+void radix_sort_ids(uint64_t *keys, uint32_t *vals, size_t n, int bits, cudaStream_t s, const uint32_t *counts0,
+                    Buf<uint64_t> *kalt, Buf<uint32_t> *valt, uint64_t **kres, uint32_t **vres);
 void radix_sort_unpack8(uint64_t *keys, uint64_t *vals, size_t n, int bits, uint32_t ntr, uint32_t *trp, uint32_t *tci,
                         uint64_t *tiles, cudaStream_t s, const uint32_t *counts0 = nullptr);
 void radix_sort_keys_u64(uint64_t *keys, size_t n, int bits, cudaStream_t s, uint64_t **keys_out,

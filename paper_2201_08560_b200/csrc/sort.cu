@@ -338,6 +338,34 @@ void radix_sort_unpack8(uint64_t *keys, uint64_t *vals, size_t n, int bits, uint
     LAUNCH(k_sufmin_apply, nb, SM_TILE, 0, s, m, trp, bmin.p);
 }
 
+// (u64 key, u32 value) passes over the low `bits` of the key; counts0, when
+// given, holds the first pass's per-tile digit counts
+void radix_sort_ids(uint64_t *keys, uint32_t *vals, size_t n, int bits, cudaStream_t s, const uint32_t *counts0,
+                    Buf<uint64_t> *kalt, Buf<uint32_t> *valt, uint64_t **kres, uint32_t **vres) {
+    *kalt = Buf<uint64_t>(n, s);
+    *valt = Buf<uint32_t>(n, s);
+    const uint32_t nblocks = (uint32_t)((n + RS_TILE - 1) / RS_TILE);
+    Buf<uint32_t> counts((size_t)nblocks * 256, s);
+    Buf<uint64_t> offs((size_t)nblocks * 256 + 1, s);
+    uint64_t *kin = keys, *kout = kalt->p;
+    uint32_t *vin = vals, *vout = valt->p;
+    for (int sh = 0; sh < bits; sh += 8) {
+        const uint32_t dm = bits - sh >= 8 ? 0xFFu : (1u << (bits - sh)) - 1u;
+        if (sh == 0 && counts0) {
+            exclusive_scan_u32_to_u64(counts0, offs.p, (size_t)nblocks * 256, s);
+        } else {
+            LAUNCH(k_rs_hist<uint64_t>, nblocks, RS_THREADS, 0, s, kin, n, sh, dm, counts.p, nblocks);
+            exclusive_scan_u32_to_u64(counts.p, offs.p, (size_t)nblocks * 256, s);
+        }
+        LAUNCH((k_rs_scatter<uint64_t, true, false, uint32_t>), nblocks, RS_THREADS, 0, s, kin, vin, kout, vout, n, sh,
+               dm, offs.p, nblocks, Unpack4{});
+        std::swap(kin, kout);
+        std::swap(vin, vout);
+    }
+    *kres = kin;
+    *vres = vin;
+}
+
 void radix_sort_keys_u64(uint64_t *keys, size_t n, int bits, cudaStream_t s, uint64_t **keys_out,
                          Buf<uint64_t> *kalt) {
     *kalt = Buf<uint64_t>(n, s);

@@ -161,8 +161,11 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack_rows(uint64_t T, const uint
                                                           const void *__restrict__ tiles_, int cb,
                                                           uint64_t *__restrict__ keys, uint64_t *__restrict__ vals,
                                                           uint32_t *__restrict__ counts0, uint32_t dm0) {
-    using TW = typename std::conditional<D == 4, uint32_t, uint64_t>::type;  // one tile
+    // D >= 16: no tile payload -- vals (u32) take the tile id, the tile is
+    // gathered after the sort (one 32 / 128-byte read per tile)
+    using TW = typename std::conditional<D == 4, uint32_t, uint64_t>::type;  // one tile (D = 4, 8)
     const TW *__restrict__ tiles = static_cast<const TW *>(tiles_);
+    constexpr bool IDS = D >= 16;
     __shared__ uint32_t cnt[PK_TILES];
     __shared__ uint32_t hist[256];  // the first radix pass's digit counts of this tile
     __shared__ uint32_t wsum[PK_THREADS / 32];
@@ -177,7 +180,10 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack_rows(uint64_t T, const uint
     if (tb + PK_PER <= T) {  // 32-byte aligned: 16-byte loads
         const uint4 c0 = reinterpret_cast<const uint4 *>(tci + tb)[0], c1 = reinterpret_cast<const uint4 *>(tci + tb)[1];
         c[0] = c0.x; c[1] = c0.y; c[2] = c0.z; c[3] = c0.w; c[4] = c1.x; c[5] = c1.y; c[6] = c1.z; c[7] = c1.w;
-        if constexpr (D == 4) {
+        if constexpr (IDS) {
+#pragma unroll
+            for (int j = 0; j < PK_PER; j++) v[j] = 0;
+        } else if constexpr (D == 4) {
             const uint4 v0 = reinterpret_cast<const uint4 *>(tiles + tb)[0], v1 = reinterpret_cast<const uint4 *>(tiles + tb)[1];
             v[0] = v0.x; v[1] = v0.y; v[2] = v0.z; v[3] = v0.w; v[4] = v1.x; v[5] = v1.y; v[6] = v1.z; v[7] = v1.w;
         } else {
@@ -193,7 +199,7 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack_rows(uint64_t T, const uint
         for (int j = 0; j < PK_PER; j++) {
             const uint64_t t = tb + j;
             c[j] = t < T ? tci[t] : 0u;
-            v[j] = t < T ? tiles[t] : (TW)0;
+            v[j] = (t < T && !IDS) ? tiles[t] : (TW)0;
         }
     }
     __syncthreads();
@@ -238,6 +244,11 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack_rows(uint64_t T, const uint
             ulonglong2 *ov = reinterpret_cast<ulonglong2 *>(vals + tb);
 #pragma unroll
             for (int j = 0; j < PK_PER / 2; j++) ov[j] = make_ulonglong2(v[2 * j], v[2 * j + 1]);
+        } else if constexpr (IDS) {
+            uint4 *ov = reinterpret_cast<uint4 *>(reinterpret_cast<uint32_t *>(vals) + tb);
+            const uint32_t t32 = (uint32_t)tb;
+            ov[0] = make_uint4(t32, t32 + 1, t32 + 2, t32 + 3);
+            ov[1] = make_uint4(t32 + 4, t32 + 5, t32 + 6, t32 + 7);
         }
     } else {
 #pragma unroll
@@ -245,6 +256,7 @@ __global__ void __launch_bounds__(PK_THREADS) k_pack_rows(uint64_t T, const uint
             if (tb + j < T) {
                 keys[tb + j] = k[j];
                 if constexpr (D == 8) vals[tb + j] = v[j];
+                if constexpr (IDS) reinterpret_cast<uint32_t *>(vals)[tb + j] = (uint32_t)(tb + j);
             }
     }
     __syncthreads();
@@ -272,6 +284,28 @@ __device__ __forceinline__ void trp_bounds(uint64_t p, uint64_t T, K key, K prev
     for (uint32_t q = c0; q <= c; q++) trp_out[q] = (uint32_t)p;
     if (p + 1 == T)
         for (uint32_t q = c + 1; q <= ntr; q++) trp_out[q] = (uint32_t)T;
+}
+
+// d >= 16 after a (column | row, tile id) sort: the row comes with the key,
+// only the tile is gathered
+template <int D>
+__global__ void __launch_bounds__(256) k_transpose_gather_ids(uint64_t T, const uint64_t *__restrict__ keys,
+                                                              const uint32_t *__restrict__ ids, int cb, uint32_t ntr,
+                                                              const void *__restrict__ tiles,
+                                                              uint32_t *__restrict__ trp_out,
+                                                              uint32_t *__restrict__ tci_out,
+                                                              void *__restrict__ tiles_out) {
+    const uint64_t mask = (1ull << cb) - 1;
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < T; p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[p];
+        const uint32_t t = ids[p];
+        uint32_t a[D];
+        load_tile<D>(tiles, t, a);
+        trp_bounds<uint64_t>(p, T, k, p ? keys[p - 1] : 0ull, mask, ntr, trp_out);
+        tci_out[p] = (uint32_t)((k >> cb) & mask);
+        bit_transpose<D>(a);
+        store_tile<D>(tiles_out, p, a);
+    }
 }
 
 __global__ void k_trp_sorted(uint64_t T, const uint32_t *__restrict__ cols, uint32_t ntr, uint32_t *__restrict__ trp_out) {
@@ -681,6 +715,23 @@ b2sr_matrix *transpose_device(const b2sr_matrix *m, cudaStream_t s) {
             LAUNCH(k_pack_rows<8>, nb, PK_THREADS, 0, s, T, m->trp, q.p, m->tci, m->tiles, cb, keys.p, vals.p, counts0.p,
                    cb >= 8 ? 0xFFu : (1u << cb) - 1u);
             radix_sort_unpack8(keys.p, vals.p, T, cb, ntr, o->trp, o->tci, static_cast<uint64_t *>(o->tiles), s, counts0.p);
+        } else if (m->dim >= 16 && tr8_sort_enabled()) {
+            // (column | row, tile id): the row travels with the key, only the
+            // 32 / 128-byte tile is gathered afterwards (no row-id array)
+            const uint32_t nb = (uint32_t)((T + PK_TILES - 1) / PK_TILES);
+            Buf<uint64_t> keys(T, s), kalt;
+            Buf<uint32_t> ids(T, s), valt, q(2 * (size_t)nb, s), counts0((size_t)nb * 256, s);
+            LAUNCH(k_pack4_bounds, (nb + 255) / 256, 256, 0, s, T, ntr, m->trp, nb, q.p);
+            LAUNCH(k_pack_rows<16>, nb, PK_THREADS, 0, s, T, m->trp, q.p, m->tci, m->tiles, cb, keys.p,
+                   reinterpret_cast<uint64_t *>(ids.p), counts0.p, cb >= 8 ? 0xFFu : (1u << cb) - 1u);
+            uint64_t *ks = nullptr;
+            uint32_t *vs = nullptr;
+            radix_sort_ids(keys.p, ids.p, T, cb, s, counts0.p, &kalt, &valt, &ks, &vs);
+            const unsigned g = grid_for(T);
+            if (m->dim == 16)
+                LAUNCH(k_transpose_gather_ids<16>, g, 256, 0, s, T, ks, vs, cb, ntr, m->tiles, o->trp, o->tci, o->tiles);
+            else
+                LAUNCH(k_transpose_gather_ids<32>, g, 256, 0, s, T, ks, vs, cb, ntr, m->tiles, o->trp, o->tci, o->tiles);
         } else {
             Buf<uint32_t> keys(T, s), vals(T, s), rowid(T, s), kalt, valt;
             CK(cudaMemcpyAsync(keys.p, m->tci, T * 4, cudaMemcpyDeviceToDevice, s));
