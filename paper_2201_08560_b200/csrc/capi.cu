@@ -127,6 +127,10 @@ void free_matrix(b2sr_matrix *m) {
     free_bff(m->bff);
     free_xperm(m->xperm);
     free_csrplan(m->csrplan);
+    // let the frees complete now: an allocation on another stream reuses
+    // completed frees opportunistically, while pending ones made the pool map
+    // fresh memory (s22 d = 32 conversions after a free: 77-101 vs 14 ms)
+    cudaStreamSynchronize(nullptr);
     if (cur != m->device) cudaSetDevice(cur);
     delete m;
 }
