@@ -58,6 +58,31 @@ void clear_error();
 
 // ---------------------------------------------------------------- launches
 extern std::atomic<uint64_t> g_launches;
+// Programmatic dependent launch: the kernel may be scheduled while its
+// predecessor in the stream drains (it must start with pdl_prologue(), which
+// waits for the predecessor's completion and memory before anything is read).
+// Used between the back-to-back kernels of the device-controlled BFS levels.
+__device__ __forceinline__ void pdl_prologue() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+#define LAUNCH_PDL(pdl, kernel, grid, block, smem, strm_, ...)                                   \
+    do {                                                                                          \
+        if ((grid) > 0) {                                                                         \
+            cudaLaunchConfig_t cfg_{};                                                            \
+            cfg_.gridDim = dim3(grid);                                                            \
+            cfg_.blockDim = dim3(block);                                                          \
+            cfg_.dynamicSmemBytes = (smem);                                                       \
+            cfg_.stream = (strm_);                                                                \
+            cudaLaunchAttribute at_[1];                                                           \
+            at_[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                       \
+            at_[0].val.programmaticStreamSerializationAllowed = 1;                                \
+            cfg_.attrs = at_;                                                                     \
+            cfg_.numAttrs = (pdl) ? 1 : 0;                                                        \
+            CK(cudaLaunchKernelEx(&cfg_, kernel, __VA_ARGS__));                                   \
+            ::b2sr::g_launches.fetch_add(1, std::memory_order_relaxed);                           \
+        }                                                                                         \
+    } while (0)
+
 #define LAUNCH(kernel, grid, block, smem, stream, ...)                     \
     do {                                                                   \
         if ((grid) > 0) {                                                  \

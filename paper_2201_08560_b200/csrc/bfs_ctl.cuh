@@ -48,10 +48,11 @@ struct BfsSnap {
 // pfrontier = frontier, pnext = next (one GPU).
 void launch_bfs_level(b2sr_matrix *at, const b2sr_matrix *a, BfsCtl *ctl, const uint2 *push_list,
                       const uint32_t *active_list, const void *hx, size_t hb, const void *frontier, void *next,
-                      const void *visited, cudaStream_t s, const void *pfrontier = nullptr, void *pnext = nullptr);
+                      const void *visited, cudaStream_t s, const void *pfrontier = nullptr, void *pnext = nullptr,
+                      bool pdl = false);
 // Top-down level of the push-only BFS (no transpose; d = 4, 8): the listed
 // chunks of a, bits of visited vertices dropped before the scatter.
 void launch_bfs_push_level(const b2sr_matrix *a, const BfsCtl *ctl, const uint2 *push_list, const void *frontier,
-                           const void *visited, void *next, cudaStream_t s);
+                           const void *visited, void *next, cudaStream_t s, bool pdl = false);
 
 }  // namespace b2sr

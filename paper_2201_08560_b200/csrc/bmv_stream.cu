@@ -432,6 +432,7 @@ __global__ void __launch_bounds__(NT, 1)
                 const void *__restrict__ hx, uint32_t hx_bytes16, uint32_t S, const void *__restrict__ frontier,
                 void *__restrict__ next, const void *__restrict__ visited, const void *__restrict__ pfrontier,
                 void *__restrict__ pnext) {
+    pdl_prologue();
     const int mode = ctl->mode;
     if (mode == BFS_NONE) return;
     if (mode == BFS_PUSH) {
@@ -457,24 +458,25 @@ __global__ void __launch_bounds__(256) k_bfs_push_level(const BfsCtl *__restrict
                                                         const uint32_t *__restrict__ trp, const uint32_t *__restrict__ tci,
                                                         const uint8_t *__restrict__ tiles, const void *__restrict__ frontier,
                                                         const void *__restrict__ visited, void *__restrict__ next) {
+    pdl_prologue();
     if (ctl->mode != BFS_PUSH) return;
     push_entries<D>(ctl->list_n, plist, trp, tci, tiles, frontier, next, visited);
 }
 
 void launch_bfs_push_level(const b2sr_matrix *a, const BfsCtl *ctl, const uint2 *push_list, const void *frontier,
-                           const void *visited, void *next, cudaStream_t s) {
+                           const void *visited, void *next, cudaStream_t s, bool pdl) {
     const unsigned g = (unsigned)num_sms() * 8;
     if (a->dim == 4)
-        LAUNCH(k_bfs_push_level<4>, g, 256, 0, s, ctl, push_list, a->trp, a->tci, (const uint8_t *)a->tiles, frontier,
-               visited, next);
+        LAUNCH_PDL(pdl, k_bfs_push_level<4>, g, 256, 0, s, ctl, push_list, a->trp, a->tci, (const uint8_t *)a->tiles,
+                   frontier, visited, next);
     else
-        LAUNCH(k_bfs_push_level<8>, g, 256, 0, s, ctl, push_list, a->trp, a->tci, (const uint8_t *)a->tiles, frontier,
-               visited, next);
+        LAUNCH_PDL(pdl, k_bfs_push_level<8>, g, 256, 0, s, ctl, push_list, a->trp, a->tci, (const uint8_t *)a->tiles,
+                   frontier, visited, next);
 }
 
 void launch_bfs_level(b2sr_matrix *at, const b2sr_matrix *a, BfsCtl *ctl, const uint2 *push_list,
                       const uint32_t *active_list, const void *hx, size_t hb, const void *frontier, void *next,
-                      const void *visited, cudaStream_t s, const void *pfrontier, void *pnext) {
+                      const void *visited, cudaStream_t s, const void *pfrontier, void *pnext, bool pdl) {
     if (!pfrontier) pfrontier = frontier;
     if (!pnext) pnext = next;
     StreamPlan *sp = stream_plan(at, LT, s);
@@ -484,12 +486,12 @@ void launch_bfs_level(b2sr_matrix *at, const b2sr_matrix *a, BfsCtl *ctl, const 
     const uint8_t *atl = a ? (const uint8_t *)a->tiles : nullptr;
     if (at->dim == 4) {
         hot_smem_attr(k_bfs_level<4, 1024>, hb);
-        LAUNCH((k_bfs_level<4, 1024>), g, 1024, hb, s, ctl, push_list, atrp, atci, atl, sp->n_loads, active_list,
+        LAUNCH_PDL(pdl, (k_bfs_level<4, 1024>), g, 1024, hb, s, ctl, push_list, atrp, atci, atl, sp->n_loads, active_list,
                at->num_tiles, sp->desc, at->trp, (const uint8_t *)at->tiles, hv.tci2, hx, (uint32_t)hb, hv.S,
                frontier, next, visited, pfrontier, pnext);
     } else {
         hot_smem_attr(k_bfs_level<8, 768>, hb);
-        LAUNCH((k_bfs_level<8, 768>), g, 768, hb, s, ctl, push_list, atrp, atci, atl, sp->n_loads, active_list,
+        LAUNCH_PDL(pdl, (k_bfs_level<8, 768>), g, 768, hb, s, ctl, push_list, atrp, atci, atl, sp->n_loads, active_list,
                at->num_tiles, sp->desc, at->trp, (const uint8_t *)at->tiles, hv.tci2, hx, (uint32_t)hb, hv.S,
                frontier, next, visited, pfrontier, pnext);
     }

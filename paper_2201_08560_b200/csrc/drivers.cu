@@ -937,6 +937,7 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
                                 unsigned long long tiles_at, int has_a, BfsSnap *__restrict__ snap,
                                 uint32_t level_no, double active_frac) {
     using W = typename WordT<D>::T;
+    pdl_prologue();
     if (ctl->mode == BFS_NONE && mask) return;  // BFS already over
     constexpr int WPC = 16 / sizeof(W);
     unsigned long long ft = 0, rt = 0, fv = 0;
@@ -1062,6 +1063,7 @@ __global__ void k_bfs_prep(BfsCtl *__restrict__ c, uint32_t ntr, const uint32_t 
                            uint32_t *__restrict__ alist, const void *__restrict__ pfrontier) {
     // row blocks: pfrontier / visited are shifted to the block's first row
     // (a and at blocks share the row range); frontier stays global (hot fill)
+    pdl_prologue();
     const int mode = c->mode;
     if (mode == BFS_NONE) return;
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
@@ -1225,13 +1227,17 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     const unsigned gp = (unsigned)num_sms() * 8;
     int done = 0;
     long long sweeps = 0;
+    // programmatic dependent launch between the level's kernels (B2SR_BFS_PDL=0: plain launches, A/B)
+    const char *pde = getenv("B2SR_BFS_PDL");
+    const bool pdl = !(pde && pde[0] == '0');
     for (uint32_t L = 1;; L++) {
-        LAUNCH(k_bfs_prep<D>, gp, 256, 0, s, ctl.p, ntr, ta, list.p, hv.S, hv.cols, frontier, hx.p, n_loads, desc,
-               visited.p, at->live, alist.p, frontier);
-        launch_bfs_level(at, a, ctl.p, list.p, alist.p, hx.p, hb, frontier, next, push_vis ? visited.p : nullptr, s);
-        LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L, ta,
-               at->trp, (const uint4 *)at->live, ctl.p, (uint4 *)frontier, 1, alpha,
-               (unsigned long long)at->num_tiles, a ? 1 : 0, snaps.dev, L, active_frac);
+        LAUNCH_PDL(pdl, k_bfs_prep<D>, gp, 256, 0, s, ctl.p, ntr, ta, list.p, hv.S, hv.cols, frontier, hx.p, n_loads,
+                   desc, (const void *)visited.p, (const void *)at->live, alist.p, (const void *)frontier);
+        launch_bfs_level(at, a, ctl.p, list.p, alist.p, hx.p, hb, frontier, next, push_vis ? visited.p : nullptr, s,
+                         nullptr, nullptr, pdl);
+        LAUNCH_PDL(pdl, k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L,
+                   ta, (const uint32_t *)at->trp, (const uint4 *)at->live, ctl.p, (uint4 *)frontier, 1, alpha,
+                   (unsigned long long)at->num_tiles, a ? 1 : 0, snaps.dev, L, active_frac);
         std::swap(frontier, next);
         // the host checks level L-LOOKAHEAD's outcome while levels up to L are
         // already enqueued (levels past the end are gated no-ops): no poll
@@ -1294,12 +1300,16 @@ static void bfs_push_only(const b2sr_matrix *a, uint32_t src, double *d_levels, 
     const unsigned gp = (unsigned)num_sms() * 8;
     int done = 0;
     long long sweeps = 0;
+    const char *pde = getenv("B2SR_BFS_PDL");  // programmatic dependent launch between the level's kernels
+    const bool pdl = !(pde && pde[0] == '0');
     for (uint32_t L = 1;; L++) {
-        LAUNCH(k_bfs_prep<D>, gp, 256, 0, s, ctl.p, ntr, a->trp, list.p, 0u, nullptr, frontier, nullptr, 0u, nullptr,
-               visited.p, nullptr, nullptr, frontier);
-        launch_bfs_push_level(a, ctl.p, list.p, frontier, push_vis ? visited.p : nullptr, next, s);
-        LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L, a->trp,
-               nullptr, nullptr, ctl.p, (uint4 *)frontier, 1, 0.0, (unsigned long long)a->num_tiles, 1, snaps.dev, L, active_frac);
+        LAUNCH_PDL(pdl, k_bfs_prep<D>, gp, 256, 0, s, ctl.p, ntr, (const uint32_t *)a->trp, list.p, 0u,
+                   (const uint32_t *)nullptr, (const void *)frontier, (uint8_t *)nullptr, 0u, (const uint4 *)nullptr,
+                   (const void *)visited.p, (const void *)nullptr, (uint32_t *)nullptr, (const void *)frontier);
+        launch_bfs_push_level(a, ctl.p, list.p, frontier, push_vis ? visited.p : nullptr, next, s, pdl);
+        LAUNCH_PDL(pdl, k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)next, (uint4 *)visited.p, d_levels, (double)L,
+                   (const uint32_t *)a->trp, (const uint32_t *)nullptr, (const uint4 *)nullptr, ctl.p, (uint4 *)frontier,
+                   1, 0.0, (unsigned long long)a->num_tiles, 1, snaps.dev, L, active_frac);
         std::swap(frontier, next);
         const uint32_t LOOKAHEAD = bfs_lookahead();
         if (trace || L > LOOKAHEAD) {
