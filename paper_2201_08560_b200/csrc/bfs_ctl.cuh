@@ -32,11 +32,21 @@ struct BfsCtl {
 };
 
 // One level's outcome as the host sees it (mapped host memory ring).
+// One 8-byte word (a single store from the device, a single load on the host:
+// no system-scope fence between fields): level | done << 32 | sweeps << 33.
 struct BfsSnap {
-    uint32_t level;  // written last: the slot is valid for this level
-    int done;
-    long long sweeps;
+    unsigned long long w;
 };
+__host__ __device__ inline unsigned long long bfs_snap_pack(uint32_t level, int done, long long sweeps) {
+    return (unsigned long long)level | ((unsigned long long)(done ? 1 : 0) << 32) |
+           ((unsigned long long)(sweeps & 0x7FFFFFFFll) << 33);
+}
+inline void bfs_snap_read(const volatile BfsSnap *s, uint32_t *level, int *done, long long *sweeps) {
+    const unsigned long long w = s->w;
+    *level = (uint32_t)w;
+    *done = (int)((w >> 32) & 1u);
+    *sweeps = (long long)(w >> 33);
+}
 
 // One fused level (bmv_stream.cu): push levels scatter the OR of the frontier
 // bit-rows of every listed chunk of a into next (visited != null: bits of

@@ -1044,10 +1044,7 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
         }
         if (snap) {  // the level's outcome, straight into mapped host memory
             volatile BfsSnap *hs = snap + level_no % 8;
-            hs->done = done;
-            hs->sweeps = sweeps;
-            __threadfence_system();  // done/sweeps land before the level that publishes them
-            hs->level = level_no;    // no fence after: the kernel's completion flushes it
+            hs->w = bfs_snap_pack(level_no, done, sweeps);  // one store: no fence between fields
         }
     }
 }
@@ -1158,7 +1155,7 @@ struct BfsSnapshots {
         reset();
     }
     void reset() {
-        for (uint32_t i = 0; i < N; i++) host[i].level = 0xFFFFFFFFu;
+        for (uint32_t i = 0; i < N; i++) host[i].w = 0xFFFFFFFFull;  // level ~0: no level yet
     }
     const volatile BfsSnap *slot(uint32_t level) const { return host + level % N; }
 };
@@ -1246,16 +1243,19 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
         if (trace || L > LOOKAHEAD) {
             const uint32_t Lc = trace ? L : L - LOOKAHEAD;
             const volatile BfsSnap *sn = snaps.slot(Lc);
-            while (sn->level != Lc) {
+            uint32_t lv_seen = 0;
+            for (;;) {
+                bfs_snap_read(sn, &lv_seen, &done, &sweeps);
+                if (lv_seen == Lc) break;
                 const cudaError_t q = cudaStreamQuery(s);
-                if (q != cudaErrorNotReady && sn->level != Lc) {
+                bfs_snap_read(sn, &lv_seen, &done, &sweeps);
+                if (lv_seen == Lc) break;
+                if (q != cudaErrorNotReady) {
                     CK(q);  // a failed kernel surfaces here
                     B2SR_THROW(B2SR_ECUDA, "BFS level %u finished without its outcome", Lc);
                 }
                 std::this_thread::yield();
             }
-            done = sn->done;
-            sweeps = sn->sweeps;
             if (trace) fprintf(stderr, "[b2sr bfs] after level %u: done=%d sweeps=%lld\n", Lc, done, sweeps);
             if (done) break;
         }
@@ -1315,16 +1315,19 @@ static void bfs_push_only(const b2sr_matrix *a, uint32_t src, double *d_levels, 
         if (trace || L > LOOKAHEAD) {
             const uint32_t Lc = trace ? L : L - LOOKAHEAD;
             const volatile BfsSnap *sn = snaps.slot(Lc);
-            while (sn->level != Lc) {
+            uint32_t lv_seen = 0;
+            for (;;) {
+                bfs_snap_read(sn, &lv_seen, &done, &sweeps);
+                if (lv_seen == Lc) break;
                 const cudaError_t q = cudaStreamQuery(s);
-                if (q != cudaErrorNotReady && sn->level != Lc) {
+                bfs_snap_read(sn, &lv_seen, &done, &sweeps);
+                if (lv_seen == Lc) break;
+                if (q != cudaErrorNotReady) {
                     CK(q);
                     B2SR_THROW(B2SR_ECUDA, "BFS level %u finished without its outcome", Lc);
                 }
                 std::this_thread::yield();
             }
-            done = sn->done;
-            sweeps = sn->sweeps;
             if (trace) fprintf(stderr, "[b2sr bfs push] after level %u: done=%d sweeps=%lld\n", Lc, done, sweeps);
             if (done) break;
         }
@@ -1508,16 +1511,19 @@ static void dist_bfs_run(b2sr_dist_bfs *p, uint32_t src, double *d_levels, int64
         if (trace || L > LOOKAHEAD) {
             const uint32_t Lc = trace ? L : L - LOOKAHEAD;
             const volatile BfsSnap *sn = snaps.slot(Lc);
-            while (sn->level != Lc) {
+            uint32_t lv_seen = 0;
+            for (;;) {
+                bfs_snap_read(sn, &lv_seen, &done, &sweeps);
+                if (lv_seen == Lc) break;
                 const cudaError_t q = cudaStreamQuery(s);
-                if (q != cudaErrorNotReady && sn->level != Lc) {
+                bfs_snap_read(sn, &lv_seen, &done, &sweeps);
+                if (lv_seen == Lc) break;
+                if (q != cudaErrorNotReady) {
                     CK(q);
                     B2SR_THROW(B2SR_ECUDA, "BFS level %u finished without its outcome", Lc);
                 }
                 std::this_thread::yield();
             }
-            done = sn->done;
-            sweeps = sn->sweeps;
             if (trace) fprintf(stderr, "[b2sr dist bfs r%d] after level %u: done=%d sweeps=%lld\n", R, Lc, done, sweeps);
             if (done) break;
         }
