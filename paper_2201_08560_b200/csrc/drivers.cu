@@ -1009,12 +1009,15 @@ __global__ void k_bfs_update_dc(uint32_t ntr, uint4 *__restrict__ next, uint4 *_
         if (b) atomicAdd(&cnt->removed_tiles, b);
         if (c) atomicAdd(&cnt->frontier_vertices, c);
         if (o) atomicOr(&cnt->any, 1);
-        __threadfence();  // the block's counters land before it is counted done
-        last = atomicAdd(&ctl->blocks_done, 1u) == gridDim.x - 1;
+        // acq_rel: this block's counters are ordered before its "done" (release)
+        // and the last block sees every block's counters (acquire) -- in place
+        // of a full fence on each side
+        unsigned int prev;
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&ctl->blocks_done) : "memory");
+        last = prev == gridDim.x - 1;
     }
     __syncthreads();
     if (last && threadIdx.x == 0) {  // the last block plans the next level
-        __threadfence();
         // one batch of independent L2 reads (a chain of volatile accesses costs
         // a round trip each), then plain stores: later kernels see them
         const int done0 = __ldcg(&ctl->done), any_all = __ldcg(&ctl->cnt.any);
