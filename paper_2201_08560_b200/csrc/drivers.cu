@@ -1172,6 +1172,16 @@ static uint32_t bfs_lookahead() {
     return v;
 }
 
+// CTAs per SM of the per-level prep kernel (B2SR_BFS_PREP_CTAS, A/B)
+static unsigned bfs_prep_ctas() {
+    static const unsigned v = [] {
+        const char *e = getenv("B2SR_BFS_PREP_CTAS");
+        const int k = e ? atoi(e) : 8;
+        return (unsigned)std::max(1, std::min(k, 16));
+    }();
+    return v;
+}
+
 static BfsSnapshots &bfs_snapshots() {
     // per host thread (re-entrant C ABI) and per device (the events belong to one)
     static thread_local BfsSnapshots *snaps[16] = {};
@@ -1224,7 +1234,7 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
            (const uint4 *)at->live, ctl.p, nullptr, 0, alpha, (unsigned long long)at->num_tiles, a ? 1 : 0,
            snaps.dev, 0u, active_frac);
     void *frontier = fb.p, *next = fa.p;
-    const unsigned gp = (unsigned)num_sms() * 8;
+    const unsigned gp = (unsigned)num_sms() * bfs_prep_ctas();
     int done = 0;
     long long sweeps = 0;
     // programmatic dependent launch between the level's kernels (B2SR_BFS_PDL=0: plain launches, A/B)
@@ -1300,7 +1310,7 @@ static void bfs_push_only(const b2sr_matrix *a, uint32_t src, double *d_levels, 
     LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)fb.p, (uint4 *)visited.p, d_levels, 0.0, a->trp, nullptr,
            nullptr, ctl.p, nullptr, 0, 0.0, (unsigned long long)a->num_tiles, 1, snaps.dev, 0u, active_frac);
     void *frontier = fb.p, *next = fa.p;
-    const unsigned gp = (unsigned)num_sms() * 8;
+    const unsigned gp = (unsigned)num_sms() * bfs_prep_ctas();
     int done = 0;
     long long sweeps = 0;
     const char *pde = getenv("B2SR_BFS_PDL");  // programmatic dependent launch between the level's kernels
@@ -1490,7 +1500,7 @@ static void dist_bfs_run(b2sr_dist_bfs *p, uint32_t src, double *d_levels, int64
     const uint32_t own16 = (uint32_t)(p->len[R] / 16);
     const unsigned gm = grid_for(own16);
     void *frontier = fb.p, *next = fa.p;
-    const unsigned gp = (unsigned)num_sms() * 8;
+    const unsigned gp = (unsigned)num_sms() * bfs_prep_ctas();
     const uint8_t *vis_blk = visited.p + off;
     int done = 0;
     long long sweeps = 0;
