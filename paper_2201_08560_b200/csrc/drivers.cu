@@ -924,6 +924,36 @@ __global__ void k_bfs_ctl_init(BfsCtl *c, unsigned long long unvisited) {
     c->cnt = BfsCounters{};
 }
 
+// One kernel for a root's setup (instead of a fill, four memsets, the seed
+// and the control init): levels = +inf except the source (0), visited = next
+// = 0, frontier = {src}, control block reset.
+__global__ void k_bfs_init(uint32_t n, double *__restrict__ levels, uint32_t nw, uint32_t *__restrict__ visited,
+                           uint32_t *__restrict__ next, uint32_t *__restrict__ frontier, uint32_t src, uint32_t d,
+                           BfsCtl *__restrict__ c, unsigned long long unvisited) {
+    const uint32_t wb = d == 32 ? 4 : (d == 16 ? 2 : 1);  // bytes per tile-row word
+    const size_t byte = (size_t)(src / d) * wb;
+    const size_t sw = byte >> 2;
+    const uint32_t sm = (1u << (src % d)) << (8 * (byte & 3));
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) levels[i] = i == src ? 0.0 : HUGE_VAL;
+    for (size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x; j < nw; j += stride) {
+        visited[j] = 0;
+        next[j] = 0;
+        frontier[j] = j == sw ? sm : 0u;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        c->mode = BFS_NONE;
+        c->done = 0;
+        c->list_n = 0;
+        c->active_n = 0;
+        c->unvisited = unvisited;
+        c->sweeps = 0;
+        c->blocks_done = 0;
+        c->sparse = 0;
+        c->cnt = BfsCounters{};
+    }
+}
+
 // Level update of the device-controlled BFS.  Per 16-byte chunk of the raw
 // sweep output: keep unvisited live vertices (stored back: the next frontier),
 // visited |= it (one vector RMW), levels of the new vertices, counters for the
@@ -1218,13 +1248,8 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     // levels are the sparse ones (92.9 vs 97.6 GTEPS at s22), so off
     const char *pve = getenv("B2SR_PUSH_VISITED");
     const bool push_vis = pve && pve[0] == '1';
-    LAUNCH(k_fill_f64, grid_for(n), 256, 0, s, d_levels, (size_t)n, HUGE_VAL);
-    CK(cudaMemsetAsync(visited.p, 0, n16 * 16, s));
-    CK(cudaMemsetAsync(fb.p, 0, n16 * 16, s));
-    CK(cudaMemsetAsync(fa.p, 0, n16 * 16, s));
-    LAUNCH(k_bfs_seed, 1, 1, 0, s, src, (uint32_t)D, d_levels, fa.p, fb.p);
-    CK(cudaMemsetAsync(fa.p, 0, n16 * 16, s));
-    LAUNCH(k_bfs_ctl_init, 1, 1, 0, s, ctl.p, (unsigned long long)at->live_tiles);
+    LAUNCH(k_bfs_init, grid_for(n), 256, 0, s, n, d_levels, n16 * 4, (uint32_t *)visited.p, (uint32_t *)fa.p,
+           (uint32_t *)fb.p, src, (uint32_t)D, ctl.p, (unsigned long long)at->live_tiles);
     const unsigned gu = grid_for(n16);  // one thread per 16-byte chunk: the last-block plan waits on every block
     const uint32_t *ta = a ? a->trp : nullptr;
     BfsSnapshots &snaps = bfs_snapshots();
@@ -1297,13 +1322,9 @@ static void bfs_push_only(const b2sr_matrix *a, uint32_t src, double *d_levels, 
     const double active_frac = 0.0;  // every level is a push here
     const char *pve = getenv("B2SR_PUSH_VISITED");  // A/B (default on: every level is a push here)
     const bool push_vis = !(pve && pve[0] == '0');
-    LAUNCH(k_fill_f64, grid_for(n), 256, 0, s, d_levels, (size_t)n, HUGE_VAL);
-    CK(cudaMemsetAsync(visited.p, 0, n16 * 16, s));
-    CK(cudaMemsetAsync(fb.p, 0, n16 * 16, s));
-    CK(cudaMemsetAsync(fa.p, 0, n16 * 16, s));
-    LAUNCH(k_bfs_seed, 1, 1, 0, s, src, (uint32_t)D, d_levels, fa.p, fb.p);
-    CK(cudaMemsetAsync(fa.p, 0, n16 * 16, s));
-    LAUNCH(k_bfs_ctl_init, 1, 1, 0, s, ctl.p, 1ull);  // alpha = 0 below: every level is a push
+    // alpha = 0 below: every level is a push
+    LAUNCH(k_bfs_init, grid_for(n), 256, 0, s, n, d_levels, n16 * 4, (uint32_t *)visited.p, (uint32_t *)fa.p,
+           (uint32_t *)fb.p, src, (uint32_t)D, ctl.p, 1ull);
     const unsigned gu = grid_for(n16);  // one thread per 16-byte chunk: the last-block plan waits on every block
     BfsSnapshots &snaps = bfs_snapshots();
     snaps.reset();
