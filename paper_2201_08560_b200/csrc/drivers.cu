@@ -1222,24 +1222,64 @@ static BfsSnapshots &bfs_snapshots() {
     return *snaps[dev];
 }
 
+// Per-thread, per-device scratch of the single-GPU BFS drivers, kept between
+// calls (every call ends with a stream sync, so the next may reuse it): the
+// seven stream-ordered allocations and frees of a root cost ~15 us of host
+// time between roots.  Grown on demand; lives as long as the thread.
+struct BfsScratch {
+    uint8_t *p = nullptr;
+    size_t bytes = 0;
+    bool busy = false;  // set while a call uses it: a call that threw may have left work queued
+};
+static BfsScratch &bfs_scratch_slot() {
+    static thread_local BfsScratch w[16];
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    return w[dev & 15];
+}
+static uint8_t *bfs_scratch(size_t bytes, cudaStream_t s) {
+    BfsScratch &x = bfs_scratch_slot();
+    if (x.busy) CK(cudaDeviceSynchronize());  // the previous call did not finish normally
+    x.busy = true;
+    if (x.bytes < bytes) {
+        if (x.p) dfree(x.p, s);
+        x.p = static_cast<uint8_t *>(dalloc(bytes, s));
+        x.bytes = bytes;
+    }
+    return x.p;
+}
+// carve consecutive 256-byte aligned pieces out of a scratch block
+struct Carve {
+    size_t off = 0;
+    size_t take(size_t b) {
+        const size_t o = off;
+        off += (b + 255) & ~size_t(255);
+        return o;
+    }
+};
+
 template <int D>
 static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, double *d_levels, int64_t *iterations,
                        cudaStream_t s) {
     const uint32_t n = at->n, ntr = at->ntr;
     const size_t vb = padded_vec_bytes(ntr, D);
     const uint32_t n16 = (uint32_t)((vb + 15) / 16);
-    Buf<uint8_t> visited(n16 * 16, s), fa(n16 * 16, s), fb(n16 * 16, s);
-    Buf<BfsCtl> ctl(1, s);
     size_t list_cap = a ? (size_t)ntr + a->num_tiles / PUSH_CH + 1 : 1;
-    Buf<uint2> list(list_cap, s);
     ensure_live(at, s);
     HotView hv = hot_view(at, s);
     const size_t hb = hot_fill_bytes(hv, D);
-    Buf<uint8_t> hx(hb, s);
-    CK(cudaMemsetAsync(hx.p, 0, hb, s));
     uint32_t n_loads = 0;
     const uint4 *desc = stream_desc(at, s, &n_loads);
-    Buf<uint32_t> alist(std::max<uint32_t>(n_loads, 1), s);
+    Carve cv;
+    const size_t o_vis = cv.take(n16 * 16), o_fa = cv.take(n16 * 16), o_fb = cv.take(n16 * 16),
+                 o_ctl = cv.take(sizeof(BfsCtl)), o_list = cv.take(list_cap * sizeof(uint2)), o_hx = cv.take(hb),
+                 o_al = cv.take((size_t)std::max<uint32_t>(n_loads, 1) * 4);
+    uint8_t *ws = bfs_scratch(cv.off, s);
+    struct { uint8_t *p; } visited{ws + o_vis}, fa{ws + o_fa}, fb{ws + o_fb}, hx{ws + o_hx};
+    struct { BfsCtl *p; } ctl{reinterpret_cast<BfsCtl *>(ws + o_ctl)};
+    struct { uint2 *p; } list{reinterpret_cast<uint2 *>(ws + o_list)};
+    struct { uint32_t *p; } alist{reinterpret_cast<uint32_t *>(ws + o_al)};
+    CK(cudaMemsetAsync(hx.p, 0, hb, s));
     const double alpha = bfs_alpha();
     const char *afe = getenv("B2SR_BFS_ACTIVE");  // pull only the loads of unvisited rows below this tile fraction
     const double active_frac = afe ? atof(afe) : 0.5;
@@ -1300,6 +1340,7 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
         if (L > n + 2 + LOOKAHEAD) B2SR_THROW(B2SR_ENOCONV, "BFS failed to drain its frontier");
     }
     CK(cudaStreamSynchronize(s));  // the enqueued no-op levels are done
+    bfs_scratch_slot().busy = false;
     *iterations = sweeps;
 }
 

@@ -1,0 +1,4 @@
+set -x
+timeout -s KILL 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_rmat.py tests/test_gpu_dist_native.py tests/test_acceptance_ports.py tests/test_gpu_configs.py -q -x -p no:cacheprovider -k 'bfs or algorithms or rmat or worked or hot or push or sssp or errors or concurrent' 2>&1 | tail -3
+for r in 1 2 3; do timeout -s KILL 300 python tools/bfs_time.py 22 64; done
+timeout -s KILL 300 python tools/bfs_time.py 20 64
