@@ -1294,17 +1294,17 @@ static void bfs_devctl(const b2sr_matrix *a, b2sr_matrix *at, uint32_t src, doub
     const uint32_t *ta = a ? a->trp : nullptr;
     BfsSnapshots &snaps = bfs_snapshots();
     snaps.reset();
+    // programmatic dependent launch between the level's kernels (B2SR_BFS_PDL=0: plain launches, A/B)
+    const char *pde = getenv("B2SR_BFS_PDL");
+    const bool pdl = !(pde && pde[0] == '0');
     // level 0 = {src}: visited, levels, counters, the push list of level 1 and its plan
-    LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)fb.p, (uint4 *)visited.p, d_levels, 0.0, ta, at->trp,
-           (const uint4 *)at->live, ctl.p, nullptr, 0, alpha, (unsigned long long)at->num_tiles, a ? 1 : 0,
-           snaps.dev, 0u, active_frac);
+    LAUNCH_PDL(pdl, k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)fb.p, (uint4 *)visited.p, d_levels, 0.0, ta,
+               (const uint32_t *)at->trp, (const uint4 *)at->live, ctl.p, (uint4 *)nullptr, 0, alpha,
+               (unsigned long long)at->num_tiles, a ? 1 : 0, snaps.dev, 0u, active_frac);
     void *frontier = fb.p, *next = fa.p;
     const unsigned gp = (unsigned)num_sms() * bfs_prep_ctas();
     int done = 0;
     long long sweeps = 0;
-    // programmatic dependent launch between the level's kernels (B2SR_BFS_PDL=0: plain launches, A/B)
-    const char *pde = getenv("B2SR_BFS_PDL");
-    const bool pdl = !(pde && pde[0] == '0');
     for (uint32_t L = 1;; L++) {
         LAUNCH_PDL(pdl, k_bfs_prep<D>, gp, 256, 0, s, ctl.p, ntr, ta, list.p, hv.S, hv.cols, frontier, hx.p, n_loads,
                    desc, (const void *)visited.p, (const void *)at->live, alist.p, (const void *)frontier);
@@ -1369,14 +1369,15 @@ static void bfs_push_only(const b2sr_matrix *a, uint32_t src, double *d_levels, 
     const unsigned gu = grid_for(n16);  // one thread per 16-byte chunk: the last-block plan waits on every block
     BfsSnapshots &snaps = bfs_snapshots();
     snaps.reset();
-    LAUNCH(k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)fb.p, (uint4 *)visited.p, d_levels, 0.0, a->trp, nullptr,
-           nullptr, ctl.p, nullptr, 0, 0.0, (unsigned long long)a->num_tiles, 1, snaps.dev, 0u, active_frac);
+    const char *pde = getenv("B2SR_BFS_PDL");  // programmatic dependent launch between the level's kernels
+    const bool pdl = !(pde && pde[0] == '0');
+    LAUNCH_PDL(pdl, k_bfs_update_dc<D>, gu, 256, 0, s, ntr, (uint4 *)fb.p, (uint4 *)visited.p, d_levels, 0.0,
+               (const uint32_t *)a->trp, (const uint32_t *)nullptr, (const uint4 *)nullptr, ctl.p, (uint4 *)nullptr, 0,
+               0.0, (unsigned long long)a->num_tiles, 1, snaps.dev, 0u, active_frac);
     void *frontier = fb.p, *next = fa.p;
     const unsigned gp = (unsigned)num_sms() * bfs_prep_ctas();
     int done = 0;
     long long sweeps = 0;
-    const char *pde = getenv("B2SR_BFS_PDL");  // programmatic dependent launch between the level's kernels
-    const bool pdl = !(pde && pde[0] == '0');
     for (uint32_t L = 1;; L++) {
         LAUNCH_PDL(pdl, k_bfs_prep<D>, gp, 256, 0, s, ctl.p, ntr, (const uint32_t *)a->trp, list.p, 0u,
                    (const uint32_t *)nullptr, (const void *)frontier, (uint8_t *)nullptr, 0u, (const uint4 *)nullptr,
